@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Learner throughput of the PPO locomotion-shape update (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one learner iteration of R:runtime/ppo_runner.py:95-104 on a
+synthetic cfg2 rollout (T=24 x N=4096 envs, obs = critic_obs = 235, act 12,
+actor/critic 512-256-128, PpoConfig defaults: 5 epochs x 4 minibatches):
+GAE + ppo_update.
+
+  value  device-resident: the segment is already in HBM; K x (GAE kernel +
+         the update plan replayed as one CUDA graph), CUDA events, max over
+         ranks.  Minibatch indices: device permutation ("performance mode").
+  e2e    through the public drop-in API (algos.gae + algos.ppo_update) from
+         pinned HOST buffers: every step H2D of the segment, the update, and
+         the D2H of UpdateStats.
+Multi-GPU (torchrun): one process per GPU, NCCL all-reduce of the gradient
+buffer every minibatch step; every rank owns its own 4096-env segment (weak
+scaling), so value = (N x 98,304 transitions) / max-over-ranks step time.
+
+``--impl reference`` times the reference's CPU learner (the numpy oracle port
+of R:algos/estimators.py + R:algos/ppo.py, kind "port") on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "learner transitions/sec at 1/2/4/8 B200 vs host-CPU ref; PPO update ms/iter"
+UNIT = "transitions/s"
+CFG = "cfg2"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clocks / throttle reasons
+    during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------- CPU reference arm
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_limits
+
+        n = os.cpu_count() or 1
+        return threadpool_limits(limits=n), n
+    except Exception:
+        return None, 1
+
+
+def cpu_reference_sample(seed: int = 0, epochs_sampled: int = 1):
+    """Time the reference CPU learner on a bounded cfg2 sample: GAE + the first
+    `epochs_sampled` of 5 epochs (4 minibatch steps each), extrapolated to the
+    full update.  Returns (transitions/s, update_ms, seconds spent)."""
+    from oracle import port as O
+    from paper_2605_30313_b200.workload import CONFIGS, make_rollout
+
+    T, N, od, cd, ad, hid = CONFIGS[CFG]
+    w = make_rollout(CFG, seed)
+    actor = O.net_init((od, *hid, ad), 0)
+    critic = O.net_init((cd, *hid, 1), 1)
+    flat = lambda a: a.reshape(-1, a.shape[-1])
+    mean, _ = O.mlp_forward(actor, flat(w.obs))
+    blogp = O.gauss_logp(mean, actor.log_std, flat(w.actions)).reshape(T, N).astype(np.float64)
+    vals = O.value_forward(critic, flat(w.critic_obs))[0].reshape(T, N).astype(np.float64)
+    cfg = O.PpoCfg(epochs=epochs_sampled)
+    oa, oc = O.Opt.for_net(actor, cfg.lr), O.Opt.for_net(critic, cfg.lr)
+    t0 = time.perf_counter()
+    adv, ret = O.gae(w.rewards, vals, w.terminated, w.truncated, w.bootstrap_value, 0.99, 0.95,
+                     w.truncation_values)
+    t1 = time.perf_counter()
+    seg = dict(obs=w.obs, critic_obs=w.critic_obs, actions=w.actions, behavior_log_prob=blogp,
+               rewards=w.rewards, terminated=w.terminated, truncated=w.truncated, values=vals,
+               bootstrap_value=w.bootstrap_value, advantages=adv, returns=ret)
+    O.ppo_update(seg, actor, critic, oa, oc, cfg, O.philox_stream(1, "update"))
+    t2 = time.perf_counter()
+    update_s = (t1 - t0) + (t2 - t1) * (5.0 / epochs_sampled)
+    return T * N / update_s, update_s * 1e3, t2 - t0
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    lim, cores = _cpu_threads()
+    for _ in range(max(args.warmup, 0)):
+        cpu_reference_sample()
+    vals, ms = [], []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, m, _ = cpu_reference_sample()
+        vals.append(v)
+        ms.append(m)
+    wall = time.perf_counter() - t0
+    value = float(np.median(vals))
+    sample = ("cfg2 GAE + 1 of 5 PPO epochs (4 minibatch steps of 24,576 rows), "
+              "extrapolated x5 to the full update; numpy/OpenBLAS oracle port")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.median(ms)), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": "PPO update, cfg2 locomotion shape (4096 envs x 24, obs 235, "
+                                   "act 12, 512-256-128, 5x4 minibatches)",
+                       "global_batch": 98304, "parallelism": "host CPU"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_30313_b200 import _dev, _dist
+    from paper_2605_30313_b200 import algos as A
+    from paper_2605_30313_b200 import tensornet as TN
+    from paper_2605_30313_b200.algos import ppo as P
+    from paper_2605_30313_b200.algos._staging import staging_for
+    from paper_2605_30313_b200.workload import CONFIGS, make_rollout
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        _dist.set_segment_mode("local")
+    T, N, od, cd, ad, hid = CONFIGS[CFG]
+    cfg = A.PpoConfig()
+
+    # networks (reference init, seeds 0 / 1) and a pinned host rollout per rank
+    actor = TN.init_params(TN.Arch(od, hid, ad), 0)
+    critic = TN.init_params(TN.Arch(cd, hid, 1), 1)
+    params = A.AcParams(actor, critic)
+    opt = A.AcOpt.for_params(params, cfg.lr)
+    w = make_rollout(CFG, seed=rank, alloc=_dev.pinned_empty)
+    # behaviour log-prob and values at init, computed by our own kernels
+    mean, _ = TN.forward(actor, w.obs.reshape(-1, od))
+    blogp = TN.gaussian_log_prob(mean, actor.log_std, w.actions.reshape(-1, ad))
+    vals, _ = TN.value_forward(critic, w.critic_obs.reshape(-1, cd))
+    w.behavior_log_prob = _dev.pinned_empty((T, N), np.float64)
+    w.behavior_log_prob[...] = blogp.cpu().numpy().reshape(T, N)
+    w.values = _dev.pinned_empty((T, N), np.float64)
+    w.values[...] = vals.cpu().numpy().reshape(T, N)
+    seg = A.RolloutSegment(obs=w.obs, critic_obs=w.critic_obs, actions=w.actions,
+                           behavior_log_prob=w.behavior_log_prob, rewards=w.rewards,
+                           terminated=w.terminated, truncated=w.truncated, values=w.values,
+                           bootstrap_value=w.bootstrap_value, truncation_values=w.truncation_values)
+
+    ds = staging_for(T, N, od, cd, ad, cfg.epochs)
+    ds.load(seg, with_advantages=False)
+    rng = A.DeviceRng(seed=1000 + rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident learner steps (value)
+    for _ in range(args.warmup):
+        P.ppo_update_resident(ds, params, opt, cfg, rng)
+    torch.cuda.synchronize()
+    smi = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with smi:
+        e0.record()
+        for _ in range(args.steps):
+            P.ppo_update_resident(ds, params, opt, cfg, rng)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    transitions = world * T * N
+    value = transitions / (ms / 1e3)
+
+    # ---- parity mode: the reference's own host Philox permutations
+    from paper_2605_30313_b200.algos.ppo import fill_permutations  # noqa: F401
+
+    prng = np.random.Generator(np.random.Philox(key=1234 + rank))
+    P.ppo_update_resident(ds, params, opt, cfg, prng)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    n_par = 3
+    for _ in range(n_par):
+        P.ppo_update_resident(ds, params, opt, cfg, prng)
+    torch.cuda.synchronize()
+    par_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_par)
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
+    for _ in range(2):
+        seg.advantages, seg.returns = A.gae(seg.rewards, seg.values, seg.terminated,
+                                            seg.truncated, seg.bootstrap_value, cfg.gamma,
+                                            cfg.lam, truncation_values=seg.truncation_values)
+        A.ppo_update(seg, params, opt, cfg, rng)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        seg.advantages, seg.returns = A.gae(seg.rewards, seg.values, seg.terminated,
+                                            seg.truncated, seg.bootstrap_value, cfg.gamma,
+                                            cfg.lam, truncation_values=seg.truncation_values)
+        st = A.ppo_update(seg, params, opt, cfg, rng)  # returns host UpdateStats (D2H)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps)
+    h2d = ds.h2d_bytes(seg, with_advantages=False) + T * N * (4 + 4 + 1 + 1 + 4) + N * 4
+    d2h = 8 * 9 + 8 * 3  # ul_ppo_result + stats
+
+    # ---- roofline of the dominant kernel class (the MLP GEMMs)
+    counts = P.plan_stats(params, cfg, ds)
+    prof = P.profile_update(params, opt, cfg, ds)
+    hbm, bf16, bf16_sus, src = _peaks()
+    gemm_tflops = counts["gemm_flops_per_update"] / (prof["gemm"] / 1e3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("sgemm_kernel_bytes_per_update")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "PPO update (GAE + 5 epochs x 4 minibatches), cfg2 locomotion "
+                               "shape: 4096 envs x 24 steps per GPU, obs 235 / act 12, "
+                               "actor+critic 512-256-128",
+                   "global_batch": transitions, "minibatch_rows": transitions // 4,
+                   "parallelism": f"dp{world}", "indices": "device permutation (performance "
+                   "mode)", "inputs_larger_than_l2": True,
+                   "segment_bytes_per_gpu": ds.h2d_bytes(seg), "gemm_precision": "fp32 SIMT"},
+        "update_ms": ms,
+        "parity_mode": {"value": transitions / (par_ms / 1e3), "unit": UNIT, "update_ms": par_ms,
+                        "indices": "host numpy Philox permutation per epoch (reference stream)"},
+        "e2e": {"value": transitions / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": e2e_ms, "api": "algos.gae + algos.ppo_update, pinned host segment"},
+        "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_sus,
+                     "unit": "TFLOP/s", "frac": gemm_tflops / bf16_sus, "traffic": traffic,
+                     "kernel": "sgemm_kernel (all MLP GEMMs of one update)",
+                     "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
+                     "algorithmic_flops_per_update": counts["gemm_flops_per_update"],
+                     "phase_ms_per_update": prof},
+        "clocks": smi.summary(),
+        "gpu_launches": int((counts["kernels_per_update"] + 1) * args.steps),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        lim, cores = _cpu_threads()
+        v, m, spent = cpu_reference_sample()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                "update_ms": m,
+                                "sample": "cfg2 GAE + 1 of 5 PPO epochs on the numpy oracle port, "
+                                          "extrapolated x5", "seconds": spent}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,277 @@
+/* libunilite_b200 -- C ABI of the B200-native UniLab learner hot path.
+ *
+ * The reference (arxiv/paper_2605_30313, package `unilite`) has no FFI: its
+ * boundary is the Python function/class API re-exported by
+ * R:tensornet/__init__.py, R:algos/__init__.py, R:replaypath/__init__.py and
+ * R:runtime/__init__.py (R: = /root/reference/pkg/src/unilite/).  Every entry
+ * point below replaces one of those Python functions (cited per function);
+ * the Python package `paper_2605_30313_b200` binds them with ctypes and keeps
+ * the reference names/signatures.
+ *
+ * Conventions
+ *   - all tensor pointers are DEVICE pointers unless named `host_*`;
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous
+ *     on that stream unless documented otherwise;
+ *   - float32 storage, row-major, explicit leading dimensions (`ld*`, in
+ *     elements); [T, N] arrays are t-major (element (t, n) at t*N + n);
+ *   - flags are uint8 (0/1); indices are int64;
+ *   - return value is a status code; on error ul_last_error() holds a message
+ *     (thread local).  No C++ exception crosses this boundary.
+ */
+#ifndef UNILITE_B200_H
+#define UNILITE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UL_ABI_VERSION 1
+
+/* status codes -> Python exception in the shim */
+#define UL_OK 0
+#define UL_ERR_VALUE 1      /* ValueError            */
+#define UL_ERR_INDEX 2      /* IndexError            */
+#define UL_ERR_DIVERGENCE 3 /* DivergenceError       */
+#define UL_ERR_SLOT 4       /* SlotStateError        */
+#define UL_ERR_CUDA 5       /* RuntimeError (CUDA)   */
+
+const char* ul_last_error(void);
+int ul_version(void);
+int ul_device_count(int* count);
+int ul_stream_sync(void* stream);
+int ul_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* strided 2-D async copy (row pitch change, e.g. 235 -> 236 floats) */
+int ul_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
+                      int64_t width_bytes, int64_t rows, void* stream);
+int ul_host_alloc_pinned(void** ptr, int64_t bytes);
+int ul_host_free_pinned(void* ptr);
+int ul_event_create(void** ev);
+int ul_event_destroy(void* ev);
+int ul_event_record(void* ev, void* stream);
+int ul_stream_wait_event(void* stream, void* ev);
+int ul_event_query(void* ev, int* done);
+int ul_event_sync(void* ev);
+
+/* ------------------------------------------------------------------ K1/K2 */
+/* GAE reverse scan.  Replaces R:algos/estimators.py:29-63 (+ _next_values
+ * :15-26).  truncation_values may be NULL (reference default None).
+ * f64 arithmetic, f32 outputs adv/ret [T, N]. */
+int ul_gae_f32(const float* rewards, const float* values, const uint8_t* terminated,
+               const uint8_t* truncated, const float* truncation_values, const float* bootstrap,
+               int64_t T, int64_t N, double gamma, double lam, float* adv, float* ret,
+               void* stream);
+
+/* V-trace reverse scan.  Replaces R:algos/estimators.py:66-122.  truncated and
+ * truncation_values may be NULL.  Outputs vs, pg_adv [T, N]. */
+int ul_vtrace_f32(const float* behavior_logp, const float* target_logp, const float* rewards,
+                  const float* values, const uint8_t* terminated, const uint8_t* truncated,
+                  const float* truncation_values, const float* bootstrap, int64_t T, int64_t N,
+                  double gamma, double rho_bar, double c_bar, float* vs, float* pg_adv,
+                  void* stream);
+
+/* --------------------------------------------------------------- K12/K13 */
+#define UL_MAX_SEG 4
+#define UL_PREP_BLOCKS 296
+/* Device-resident optimizer control record (allocate ul_opt_ctl_bytes() of
+ * device memory, initialise on the host with ul_opt_ctl_init, upload). */
+typedef struct ul_opt_ctl {
+  double lr[UL_MAX_SEG];        /* per-segment learning rate            */
+  double beta1, beta2, eps;     /* Adam hyper-parameters                */
+  double max_norm;              /* joint clip threshold, <= 0 disables  */
+  int64_t t[UL_MAX_SEG];        /* Adam step counters (device-updated)  */
+  double norm;                  /* pre-clip joint norm of the last call */
+  double factor;                /* clip factor applied by the last call */
+  double sumsq[UL_MAX_SEG];
+  int32_t seg_bad[UL_MAX_SEG];  /* non-finite gradients seen           */
+  int32_t seg_update[UL_MAX_SEG];
+  int32_t loss_bad;             /* set by loss heads, cleared per step  */
+  int32_t diverged;             /* sticky DivergenceError latch         */
+  int32_t steps;                /* prepare calls so far                 */
+  int32_t fail_step;            /* first failing step, -1 if none       */
+  uint32_t ticket;              /* internal last-block counter          */
+  int32_t pad0;
+  double part[UL_PREP_BLOCKS][UL_MAX_SEG]; /* internal partials */
+  int32_t part_bad[UL_PREP_BLOCKS][UL_MAX_SEG];
+} ul_opt_ctl;
+
+int64_t ul_opt_ctl_bytes(void);
+int ul_opt_ctl_init(ul_opt_ctl* host_ctl, int nseg, const double* lr, double beta1,
+                    double beta2, double eps, double max_norm);
+
+/* Joint global-norm clip of nseg gradient segments, in place.  Replaces
+ * R:tensornet/adam.py:30-40; the pre-clip norm lands in ctl->norm. */
+int ul_clip_global_norm(float* const* grads, const int64_t* sizes, int nseg, ul_opt_ctl* ctl,
+                        void* stream);
+
+/* Adam (+ optional joint clip via ctl->max_norm, + finiteness latch).
+ * Replaces R:tensornet/adam.py:43-80 (run over several segments it is the
+ * PPO step's clip_global_norm([actor, critic]) + two adam_step calls,
+ * R:algos/ppo.py:181-185). */
+int ul_adam_step(float* const* params, float* const* grads, float* const* m, float* const* v,
+                 const int64_t* sizes, int nseg, ul_opt_ctl* ctl, int write_clipped_grads,
+                 void* stream);
+
+/* Polyak target update target <- (1-tau) target + tau online over a flat
+ * parameter vector.  Replaces R:algos/sac.py:100-108. */
+int ul_polyak(float* target, const float* online, int64_t n, double tau, void* stream);
+
+/* ------------------------------------------------------------- K7/K8 MLP */
+#define UL_MAX_LAYERS 8
+/* A dense ELU MLP (R:tensornet/mlp.py:16-76): dims = (in, h1, ..., out),
+ * parameters in ONE flat float32 buffer in ModelParams.flat order
+ * (W0 (out x in, row-major), b0, W1, b1, ..., log_std). */
+typedef struct ul_net_desc {
+  int32_t n_layers;
+  int32_t dims[UL_MAX_LAYERS + 1];
+} ul_net_desc;
+
+/* number of floats of the flat parameter vector (incl. log_std) */
+int64_t ul_net_param_count(const ul_net_desc* net);
+/* activation cache floats for a batch of M rows (hidden layers only) */
+int64_t ul_mlp_act_floats(const ul_net_desc* net, int64_t M);
+/* backward workspace floats for a batch of M rows */
+int64_t ul_mlp_bwd_work_floats(const ul_net_desc* net, int64_t M);
+
+/* Forward: out[M, out] (ld_out) = MLP(x[M, in] (ldx)); hidden activations are
+ * cached in `acts` (ul_mlp_act_floats).  Replaces R:tensornet/mlp.py:153-172. */
+int ul_mlp_forward(const ul_net_desc* net, const float* params, const float* x, int64_t ldx,
+                   int64_t M, float* acts, float* out, int64_t ld_out, void* stream);
+
+/* Backward from the upstream gradient dout[M, out] (ld_dout): writes the flat
+ * gradient vector `grads` (log_std slot zeroed) and, if dx != NULL, the input
+ * gradient dx[M, in] (lddx).  Replaces R:tensornet/mlp.py:175-198. */
+int ul_mlp_backward(const ul_net_desc* net, const float* params, const float* x, int64_t ldx,
+                    int64_t M, const float* acts, const float* dout, int64_t ld_dout,
+                    float* grads, float* dx, int64_t lddx, float* work, void* stream);
+
+/* Plain fp32 GEMM C = op(A) op(B) (+bias/ELU epilogues), exposed for tests.
+ * layout bit0: A is K-major ([M,K] row-major) else M-major ([K,M]);
+ * layout bit1: B is K-major ([N,K] row-major) else N-major ([K,N]).
+ * epi: 0 store, 1 +bias, 2 ELU(+bias), 3 *(min(aux,0)+1). */
+int ul_gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A,
+                int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                const float* bias, const float* aux, int64_t ldaux, void* stream);
+
+/* ------------------------------------------------- K4 / K5 / K6 data path */
+/* Gather rows of up to 12 arrays sharing one index vector (PPO minibatch
+ * copies of R:algos/ppo.py:161-176; replay sample copy of
+ * R:replaypath/storage.py:106-110).  Strides / row widths in BYTES.  Rows
+ * outside [lo, hi) are skipped and set *err (device int, may be NULL);
+ * modulo > 0 maps absolute replay indices to ring slots. */
+int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
+                   const int64_t* src_stride, const int64_t* dst_stride, const int64_t* row_bytes,
+                   const int64_t* idx, int64_t n, int64_t modulo, int64_t lo, int64_t hi, int* err,
+                   void* stream);
+
+/* Replay ring insert (R:replaypath/storage.py:76-104): n rows of `width`
+ * floats at absolute index `head`; rows may be pinned-host or device memory.
+ * n >= cap keeps only the last cap rows (each at its own absolute slot). */
+int ul_ring_insert(float* ring, int64_t cap, int64_t width, int64_t head, const float* rows,
+                   int64_t n, void* stream);
+
+/* Device permutation of [0, n) (performance mode only; NOT the numpy Philox
+ * shuffle of R:algos/ppo.py:162). */
+int ul_device_permutation(int64_t n, uint64_t key, int64_t* out, void* stream);
+
+/* ------------------------------------------------------------ K3 normaliser */
+/* state = float64 [1 + 2D]: count, mean[D], var[D]
+ * (R:tensornet/normalizer.py:14-25).  work = ul_norm_work_bytes(D) bytes of
+ * zero-initialised device memory. */
+int64_t ul_norm_work_bytes(int64_t D);
+/* Normalizer.update (R:tensornet/normalizer.py:27-45) */
+int ul_norm_update(const float* x, int64_t B, int64_t D, int64_t ldx, double* state, void* work,
+                   int frozen, void* stream);
+/* Normalizer.apply (R:tensornet/normalizer.py:47-49) */
+int ul_norm_apply(const float* x, int64_t B, int64_t D, int64_t ldx, const double* state,
+                  float* out, int64_t ldo, void* stream);
+
+/* Diagonal Gaussian log-prob summed over A action dims
+ * (R:tensornet/distributions.py:11-18); out[n] float32. */
+int ul_gaussian_logp(const float* mean, int64_t ld_mean, const float* log_std,
+                     const float* action, int64_t ld_act, int64_t n, int A, float* out,
+                     void* stream);
+
+/* --------------------------------------------------- PPO / APPO update plan */
+#define UL_MAX_ACT 64
+typedef struct ul_ppo_stats {
+  double policy_sum, value_sum, entropy_sum, kl_epoch_sum, kl_last;
+  int64_t steps;
+} ul_ppo_stats;
+
+typedef struct ul_ppo_plan_desc {
+  ul_net_desc actor, critic;
+  int64_t rows;                     /* T*N transitions per segment            */
+  int64_t ld_obs, ld_cobs, ld_act;  /* row strides of the bound device arrays */
+  int32_t epochs, minibatches;
+  double clip_param, entropy_coef, value_loss_coef;
+  int32_t use_clipped_value_loss;
+  double max_grad_norm;
+  int32_t world_size, rank;         /* data-parallel minibatch sharding       */
+  int32_t raw_advantages;           /* 1: advantages already normalised       */
+  int32_t local_shards;             /* 0: every rank holds the whole segment and
+                                       takes rows [rank*mb/G, (rank+1)*mb/G) of
+                                       each permuted minibatch; 1: each rank owns
+                                       its own segment rows (weak scaling) and a
+                                       global minibatch is the union of the
+                                       ranks' local minibatches              */
+} ul_ppo_plan_desc;
+
+typedef struct ul_ppo_bindings {
+  const float* obs;   /* [rows, ld_obs]  */
+  const float* cobs;  /* [rows, ld_cobs] */
+  const float* act;   /* [rows, ld_act]  */
+  const float* blogp; /* [rows] behaviour log-prob          */
+  const float* adv;   /* [rows] advantages (pg_adv for APPO) */
+  const float* ret;   /* [rows] returns (vs for APPO)       */
+  const float* oldv;  /* [rows] old values                  */
+  float* actor_params;
+  float* critic_params;
+  float* actor_m;
+  float* actor_v;
+  float* critic_m;
+  float* critic_v;
+  const int64_t* perm; /* [epochs, rows] minibatch permutations */
+  float* reduce_buf;   /* optional caller-owned all-reduce buffer of
+                          ul_ppo_plan_reduce_buffer() floats, NULL = internal */
+} ul_ppo_bindings;
+
+typedef struct ul_ppo_result {
+  double policy_loss, value_loss, entropy, kl, grad_norm;
+  int64_t t_actor, t_critic;
+  int32_t diverged, fail_step;
+} ul_ppo_result;
+
+/* The epoch x minibatch loop of R:algos/ppo.py:136-199 as a native plan:
+ * per step gather -> actor/critic forward -> loss head -> backward ->
+ * [all-reduce of the plan's gradient buffer] -> loss check, joint clip,
+ * Adam(actor), Adam(critic).  Whole updates replay as one CUDA graph. */
+int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan);
+int ul_ppo_plan_destroy(void* plan);
+int ul_ppo_plan_bind(void* plan, const ul_ppo_bindings* b);
+/* upload lr / step counters, reset stats, advantage statistics */
+int ul_ppo_plan_begin(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
+                      int64_t t_critic, void* stream);
+int ul_ppo_plan_step_grads(void* plan, int epoch, int k, void* stream);
+int ul_ppo_plan_step_apply(void* plan, int epoch, int k, void* stream);
+/* contiguous [actor grads | critic grads | 3 loss partials] buffer that a
+ * data-parallel caller all-reduces (sum) between step_grads and step_apply */
+int ul_ppo_plan_reduce_buffer(void* plan, float** ptr, int64_t* n);
+/* begin + every step (graph-captured when use_graph) */
+int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
+                    int64_t t_critic, int use_graph, void* stream);
+/* D2H of the statistics + stream sync; UL_ERR_DIVERGENCE if a step diverged */
+int ul_ppo_plan_finish(void* plan, ul_ppo_result* out, void* stream);
+/* kernels per update (graph kernel nodes) and algorithmic GEMM FLOPs per update */
+int ul_ppo_plan_counts(void* plan, int64_t* kernels_per_update, double* gemm_flops_per_update);
+/* One un-graphed update with CUDA events around every kernel class:
+ * ms[0] GEMMs, ms[1] gather, ms[2] heads/finalize, ms[3] optimizer, ms[4] all.
+ * Synchronises the stream. */
+int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
+                        int64_t t_critic, double* ms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNILITE_B200_H */

@@ -1,0 +1,65 @@
+"""Data-parallel plumbing: one process per GPU, torch.distributed (NCCL on
+B200 / NVLink, gloo in the CPU tests) for the gradient all-reduce.
+
+The learner shards every minibatch across ranks (rank r takes rows
+[r*mb/G, (r+1)*mb/G) of the reference permutation slice);
+gradients are summed once per optimizer step and every rank applies the same
+clip + Adam, so parameters stay bit-identical across ranks.
+"""
+
+from __future__ import annotations
+
+import torch
+
+
+# "replicated": every rank holds the full segment and takes a 1/G slice of each
+# reference-permuted minibatch (parity with the single-process reference).
+# "local": every rank owns its own segment rows (its own collector's envs);
+# a global minibatch is the union of the ranks' local minibatches (weak scaling).
+_MODE = {"segment": "replicated"}
+
+
+def set_segment_mode(mode: str) -> None:
+    if mode not in ("replicated", "local"):
+        raise ValueError("segment mode must be 'replicated' or 'local'")
+    _MODE["segment"] = mode
+
+
+def segment_mode() -> str:
+    return _MODE["segment"]
+
+
+def world_info() -> tuple[int, int]:
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(), dist.get_rank()
+    return 1, 0
+
+
+def shard_rows(start: int, mb: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) of a minibatch slice perm[start:start+mb] owned by `rank`."""
+    if mb % world:
+        raise ValueError("world_size must divide the minibatch")
+    per = mb // world
+    return start + rank * per, start + (rank + 1) * per
+
+
+_BUFS: dict = {}
+
+
+def reduce_buffer(n: int, device=None) -> torch.Tensor:
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    key = (n, str(dev))
+    t = _BUFS.get(key)
+    if t is None:
+        t = torch.zeros(n, dtype=torch.float32, device=dev)
+        _BUFS[key] = t
+    return t
+
+
+def all_reduce_sum(t: torch.Tensor) -> None:
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)

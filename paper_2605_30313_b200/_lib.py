@@ -1,0 +1,179 @@
+"""ctypes binding of libunilite_b200.so (the C ABI in include/unilite_b200.h).
+
+This is the whole Python<->native boundary.  There is no CPU fallback: if the
+library is missing or no CUDA device is present, every entry point raises.
+Status codes map to the reference's exception types.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import DivergenceError, SlotStateError
+
+LIB_PATH = Path(__file__).resolve().with_name("libunilite_b200.so")
+
+UL_MAX_SEG = 4
+UL_MAX_LAYERS = 8
+UL_PREP_BLOCKS = 296
+UL_MAX_ACT = 64
+
+vp = C.c_void_p
+i64 = C.c_int64
+i32 = C.c_int32
+f64 = C.c_double
+
+
+class NetDesc(C.Structure):
+    _fields_ = [("n_layers", i32), ("dims", i32 * (UL_MAX_LAYERS + 1))]
+
+    @classmethod
+    def of(cls, dims) -> "NetDesc":
+        d = cls()
+        d.n_layers = len(dims) - 1
+        for i, x in enumerate(dims):
+            d.dims[i] = int(x)
+        return d
+
+
+class OptCtl(C.Structure):
+    _fields_ = [
+        ("lr", f64 * UL_MAX_SEG), ("beta1", f64), ("beta2", f64), ("eps", f64),
+        ("max_norm", f64), ("t", i64 * UL_MAX_SEG), ("norm", f64), ("factor", f64),
+        ("sumsq", f64 * UL_MAX_SEG), ("seg_bad", i32 * UL_MAX_SEG),
+        ("seg_update", i32 * UL_MAX_SEG), ("loss_bad", i32), ("diverged", i32),
+        ("steps", i32), ("fail_step", i32), ("ticket", C.c_uint32), ("pad0", i32),
+        ("part", (f64 * UL_MAX_SEG) * UL_PREP_BLOCKS),
+        ("part_bad", (i32 * UL_MAX_SEG) * UL_PREP_BLOCKS),
+    ]
+
+
+class PpoPlanDesc(C.Structure):
+    _fields_ = [
+        ("actor", NetDesc), ("critic", NetDesc), ("rows", i64), ("ld_obs", i64),
+        ("ld_cobs", i64), ("ld_act", i64), ("epochs", i32), ("minibatches", i32),
+        ("clip_param", f64), ("entropy_coef", f64), ("value_loss_coef", f64),
+        ("use_clipped_value_loss", i32), ("max_grad_norm", f64), ("world_size", i32),
+        ("rank", i32), ("raw_advantages", i32), ("local_shards", i32),
+    ]
+
+
+class PpoBindings(C.Structure):
+    _fields_ = [(n, vp) for n in ("obs", "cobs", "act", "blogp", "adv", "ret", "oldv",
+                                  "actor_params", "critic_params", "actor_m", "actor_v",
+                                  "critic_m", "critic_v", "perm", "reduce_buf")]
+
+
+class PpoResult(C.Structure):
+    _fields_ = [("policy_loss", f64), ("value_loss", f64), ("entropy", f64), ("kl", f64),
+                ("grad_norm", f64), ("t_actor", i64), ("t_critic", i64), ("diverged", i32),
+                ("fail_step", i32)]
+
+
+# name -> (restype, argtypes)
+_PROTOS = {
+    "ul_last_error": (C.c_char_p, []),
+    "ul_version": (C.c_int, []),
+    "ul_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "ul_stream_sync": (C.c_int, [vp]),
+    "ul_memcpy_async": (C.c_int, [vp, vp, i64, vp]),
+    "ul_memcpy2d_async": (C.c_int, [vp, i64, vp, i64, i64, i64, vp]),
+    "ul_host_alloc_pinned": (C.c_int, [C.POINTER(vp), i64]),
+    "ul_host_free_pinned": (C.c_int, [vp]),
+    "ul_event_create": (C.c_int, [C.POINTER(vp)]),
+    "ul_event_destroy": (C.c_int, [vp]),
+    "ul_event_record": (C.c_int, [vp, vp]),
+    "ul_stream_wait_event": (C.c_int, [vp, vp]),
+    "ul_event_query": (C.c_int, [vp, C.POINTER(C.c_int)]),
+    "ul_event_sync": (C.c_int, [vp]),
+    "ul_gae_f32": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, i64, f64, f64, vp, vp, vp]),
+    "ul_vtrace_f32": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, f64, f64, f64, vp, vp,
+                                vp]),
+    "ul_opt_ctl_bytes": (i64, []),
+    "ul_opt_ctl_init": (C.c_int, [C.POINTER(OptCtl), C.c_int, C.POINTER(f64), f64, f64, f64,
+                                  f64]),
+    "ul_clip_global_norm": (C.c_int, [C.POINTER(vp), C.POINTER(i64), C.c_int, vp, vp]),
+    "ul_adam_step": (C.c_int, [C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                               C.POINTER(i64), C.c_int, vp, C.c_int, vp]),
+    "ul_polyak": (C.c_int, [vp, vp, i64, f64, vp]),
+    "ul_net_param_count": (i64, [C.POINTER(NetDesc)]),
+    "ul_mlp_act_floats": (i64, [C.POINTER(NetDesc), i64]),
+    "ul_mlp_bwd_work_floats": (i64, [C.POINTER(NetDesc), i64]),
+    "ul_mlp_forward": (C.c_int, [C.POINTER(NetDesc), vp, vp, i64, i64, vp, vp, i64, vp]),
+    "ul_mlp_backward": (C.c_int, [C.POINTER(NetDesc), vp, vp, i64, i64, vp, vp, i64, vp, vp,
+                                  i64, vp, vp]),
+    "ul_gemm_f32": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
+                              vp, i64, vp]),
+    "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
+                                 C.POINTER(i64), C.POINTER(i64), vp, i64, i64, i64, i64, vp, vp]),
+    "ul_ring_insert": (C.c_int, [vp, i64, i64, i64, vp, i64, vp]),
+    "ul_device_permutation": (C.c_int, [i64, C.c_uint64, vp, vp]),
+    "ul_norm_work_bytes": (i64, [i64]),
+    "ul_norm_update": (C.c_int, [vp, i64, i64, i64, vp, vp, C.c_int, vp]),
+    "ul_norm_apply": (C.c_int, [vp, i64, i64, i64, vp, vp, i64, vp]),
+    "ul_gaussian_logp": (C.c_int, [vp, i64, vp, vp, i64, i64, C.c_int, vp, vp]),
+    "ul_ppo_plan_create": (C.c_int, [C.POINTER(PpoPlanDesc), C.POINTER(vp)]),
+    "ul_ppo_plan_destroy": (C.c_int, [vp]),
+    "ul_ppo_plan_bind": (C.c_int, [vp, C.POINTER(PpoBindings)]),
+    "ul_ppo_plan_begin": (C.c_int, [vp, f64, f64, i64, i64, vp]),
+    "ul_ppo_plan_step_grads": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "ul_ppo_plan_step_apply": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+    "ul_ppo_plan_reduce_buffer": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),
+    "ul_ppo_plan_run": (C.c_int, [vp, f64, f64, i64, i64, C.c_int, vp]),
+    "ul_ppo_plan_finish": (C.c_int, [vp, C.POINTER(PpoResult), vp]),
+    "ul_ppo_plan_counts": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64)]),
+    "ul_ppo_plan_profile": (C.c_int, [vp, f64, f64, i64, i64, C.POINTER(f64), vp]),
+}
+
+_lib = None
+
+
+def exported_names():
+    return list(_PROTOS)
+
+
+def lib():
+    """Load the library once; raises (no fallback) when it is missing."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH.name} is not built (run __graft_entry__.build()); "
+                "paper_2605_30313_b200 has no CPU fallback")
+        h = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _PROTOS.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = h
+    return _lib
+
+
+_EXC = {1: ValueError, 2: IndexError, 3: DivergenceError, 4: SlotStateError, 5: RuntimeError}
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = lib().ul_last_error().decode(errors="replace")
+    exc = _EXC.get(status, RuntimeError)
+    raise exc(f"{what}: {msg}" if what and status == 5 else msg)
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)
+
+
+def ptr_array(ptrs):
+    arr = (vp * len(ptrs))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+def i64_array(vals):
+    arr = (i64 * len(vals))()
+    for i, v in enumerate(vals):
+        arr[i] = int(v)
+    return arr

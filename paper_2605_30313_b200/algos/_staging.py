@@ -1,0 +1,108 @@
+"""HBM layout of a rollout segment and the H2D staging into it.
+
+Layout (rows = T*N transitions, t-major like the reference's reshape(-1)):
+  obs   [rows, ld_o] f32   ld_o = round_up(obs_dim, 4)  (16 B rows)
+  cobs  [rows, ld_c] f32
+  act   [rows, ld_a] f32
+  blogp, rewards, values, tv, adv, ret   [rows] f32
+  term, trunc                           [rows] u8
+  boot  [N] f32
+  perm  [epochs, rows] i64   minibatch permutations
+Buffers are cached per shape so a bound update plan (and its CUDA graph)
+stays valid across updates: each update overwrites the same HBM.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .. import _dev
+
+
+def _is_dev(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+class DeviceSegment:
+    def __init__(self, T: int, N: int, obs_dim: int, cobs_dim: int, act_dim: int, epochs: int):
+        dev = _dev.require_cuda()
+        self.T, self.N, self.rows = T, N, T * N
+        self.dims = (obs_dim, cobs_dim, act_dim)
+        self.ld = tuple(_dev.feature_ld(d) for d in self.dims)
+        f32 = dict(dtype=torch.float32, device=dev)
+        rows = self.rows
+        self.obs = torch.zeros((rows, self.ld[0]), **f32)
+        self.cobs = torch.zeros((rows, self.ld[1]), **f32)
+        self.act = torch.zeros((rows, self.ld[2]), **f32)
+        self.blogp = torch.zeros(rows, **f32)
+        self.rewards = torch.zeros(rows, **f32)
+        self.values = torch.zeros(rows, **f32)
+        self.tv = torch.zeros(rows, **f32)
+        self.adv = torch.zeros(rows, **f32)
+        self.ret = torch.zeros(rows, **f32)
+        self.term = torch.zeros(rows, dtype=torch.uint8, device=dev)
+        self.trunc = torch.zeros(rows, dtype=torch.uint8, device=dev)
+        self.boot = torch.zeros(N, **f32)
+        self.perm = torch.zeros((max(epochs, 1), rows), dtype=torch.int64, device=dev)
+        self.has_tv = False
+
+    # ------------------------------------------------------------- loading
+    def _put_rows(self, dst: torch.Tensor, src, width: int) -> None:
+        if _is_dev(src):
+            src = src.reshape(self.rows, width)
+            dst[:, :width].copy_(src)  # device -> device staging copy
+            return
+        a = np.asarray(src)
+        if a.dtype != np.float32:
+            a = a.astype(np.float32)
+        _dev.h2d_rows(dst, a.reshape(self.rows, width))
+
+    def _put_vec(self, dst: torch.Tensor, src, dtype=np.float32) -> None:
+        if _is_dev(src):
+            dst.copy_(src.reshape(-1).to(dst.dtype))
+            return
+        a = np.asarray(src)
+        if a.dtype != dtype:
+            a = a.astype(dtype)
+        _dev.h2d(dst, a.reshape(-1))
+
+    def load(self, seg, with_advantages: bool = True) -> None:
+        """Stage every field the learner reads (async on the current stream;
+        pinned host arrays copy without a host sync)."""
+        od, cd, ad = self.dims
+        self._put_rows(self.obs, seg.obs, od)
+        self._put_rows(self.cobs, seg.critic_obs, cd)
+        self._put_rows(self.act, seg.actions, ad)
+        self._put_vec(self.blogp, seg.behavior_log_prob)
+        self._put_vec(self.rewards, seg.rewards)
+        self._put_vec(self.values, seg.values)
+        self._put_vec(self.term, seg.terminated, np.uint8)
+        self._put_vec(self.trunc, seg.truncated, np.uint8)
+        self._put_vec(self.boot, seg.bootstrap_value)
+        self.has_tv = seg.truncation_values is not None
+        if self.has_tv:
+            self._put_vec(self.tv, seg.truncation_values)
+        if with_advantages:
+            self._put_vec(self.adv, seg.advantages)
+            self._put_vec(self.ret, seg.returns)
+
+    def h2d_bytes(self, seg, with_advantages: bool = True) -> int:
+        od, cd, ad = self.dims
+        n = self.rows * 4 * (od + cd + ad + 3 + (2 if with_advantages else 0))
+        n += self.rows * 2 + self.N * 4
+        if seg.truncation_values is not None:
+            n += self.rows * 4
+        return n
+
+
+_CACHE: dict = {}
+
+
+def staging_for(T, N, obs_dim, cobs_dim, act_dim, epochs, slot: str = "ppo") -> DeviceSegment:
+    key = (slot, T, N, obs_dim, cobs_dim, act_dim, max(epochs, 1), torch.cuda.current_device())
+    ds = _CACHE.get(key)
+    if ds is None:
+        ds = DeviceSegment(T, N, obs_dim, cobs_dim, act_dim, epochs)
+        _CACHE[key] = ds
+    return ds

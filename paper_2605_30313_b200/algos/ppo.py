@@ -1,0 +1,330 @@
+"""Clipped-surrogate PPO on the device (mirror of R:algos/ppo.py).
+
+``ppo_update`` keeps the reference signature.  It stages the segment into HBM,
+draws the per-epoch minibatch permutations exactly as the reference does
+(``rng.permutation(n)`` per epoch, R:algos/ppo.py:162) when ``rng`` is a numpy
+Generator ("parity mode"), or on the device when ``rng`` is a
+:class:`DeviceRng` ("performance mode"), and replays the native update plan
+(ul_ppo_plan_*) -- a single CUDA graph per update on one GPU.  Under
+torch.distributed with world_size > 1 each rank takes its 1/G slice of every
+minibatch and the plan's gradient buffer is all-reduced (NCCL) between the
+backward and the optimizer step.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .. import _dev, _dist, _lib
+from ..errors import DivergenceError
+from ..tensornet.adam import OptState
+from ..tensornet.mlp import Grads, ModelParams
+from ._staging import staging_for
+from .configs import PpoConfig
+from .segment import UpdateStats
+
+
+@dataclass
+class AcParams:
+    """R:algos/ppo.py:38-46."""
+
+    actor: ModelParams
+    critic: ModelParams
+
+    def copy(self) -> "AcParams":
+        return AcParams(self.actor.copy(), self.critic.copy())
+
+
+@dataclass
+class AcOpt:
+    """R:algos/ppo.py:49-67."""
+
+    actor: OptState
+    critic: OptState
+
+    @classmethod
+    def for_params(cls, params: AcParams, lr: float) -> "AcOpt":
+        return cls(OptState.for_params(params.actor, lr), OptState.for_params(params.critic, lr))
+
+    @property
+    def lr(self) -> float:
+        return self.actor.lr
+
+    def set_lr(self, lr: float) -> None:
+        self.actor.lr = lr
+        self.critic.lr = lr
+
+
+class DeviceRng:
+    """Performance-mode minibatch index source: a keyed device permutation per
+    epoch (ul_device_permutation).  Statistically a uniform shuffle, NOT the
+    numpy Philox stream -- results then match the reference in distribution,
+    not bit-for-bit."""
+
+    def __init__(self, seed: int = 0):
+        self.seed = int(seed)
+        self.counter = 0
+
+    def next_key(self) -> int:
+        self.counter += 1
+        x = (self.seed * 0x9E3779B97F4A7C15 + self.counter * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+        x ^= x >> 31
+        return x
+
+
+# ------------------------------------------------------------------- plans
+class _Plan:
+    def __init__(self, desc: _lib.PpoPlanDesc):
+        h = C.c_void_p()
+        _lib.call("ul_ppo_plan_create", C.byref(desc), C.byref(h))
+        self.h = h
+        self.desc = desc
+        self._bind_key = None
+        n = C.c_int64()
+        p = C.c_void_p()
+        _lib.call("ul_ppo_plan_reduce_buffer", self.h, C.byref(p), C.byref(n))
+        self.red_len = n.value
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.lib().ul_ppo_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    def bind(self, ds, adv, ret, oldv, params: AcParams, opt: AcOpt, red=None):
+        b = _lib.PpoBindings()
+        vals = dict(obs=ds.obs, cobs=ds.cobs, act=ds.act, blogp=ds.blogp, adv=adv, ret=ret,
+                    oldv=oldv, actor_params=params.actor.buf, critic_params=params.critic.buf,
+                    actor_m=opt.actor.m.buf, actor_v=opt.actor.v.buf, critic_m=opt.critic.m.buf,
+                    critic_v=opt.critic.v.buf, perm=ds.perm, reduce_buf=red)
+        for k, v in vals.items():
+            setattr(b, k, _dev.ptr(v) if v is not None else None)
+        _lib.call("ul_ppo_plan_bind", self.h, C.byref(b))
+
+
+_PLANS: dict = {}
+
+
+def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
+              raw_adv: bool = False) -> _Plan:
+    key = (params.actor.arch, params.critic.arch, ds.rows, ds.ld, cfg.epochs, cfg.minibatches,
+           cfg.clip_param, cfg.entropy_coef, cfg.value_loss_coef, cfg.use_clipped_value_loss,
+           cfg.max_grad_norm, world, rank, raw_adv, _dist.segment_mode(),
+           torch.cuda.current_device())
+    plan = _PLANS.get(key)
+    if plan is None:
+        d = _lib.PpoPlanDesc()
+        d.actor = params.actor.arch.desc()
+        d.critic = params.critic.arch.desc()
+        d.rows = ds.rows
+        d.ld_obs, d.ld_cobs, d.ld_act = ds.ld
+        d.epochs, d.minibatches = cfg.epochs, cfg.minibatches
+        d.clip_param, d.entropy_coef = cfg.clip_param, cfg.entropy_coef
+        d.value_loss_coef = cfg.value_loss_coef
+        d.use_clipped_value_loss = int(cfg.use_clipped_value_loss)
+        d.max_grad_norm = cfg.max_grad_norm
+        d.world_size, d.rank, d.raw_advantages = world, rank, int(raw_adv)
+        d.local_shards = int(_dist.segment_mode() == "local" and world > 1)
+        plan = _Plan(d)
+        _PLANS[key] = plan
+    return plan
+
+
+_PINNED_PERM: dict = {}
+
+
+def fill_permutations(ds, rng, epochs: int) -> None:
+    """Per-epoch permutations into ds.perm: host Philox (parity) or device."""
+    n = ds.rows
+    if rng is None or isinstance(rng, DeviceRng):
+        rng = rng if rng is not None else DeviceRng(0)
+        for e in range(epochs):
+            _lib.call("ul_device_permutation", n, rng.next_key(), _dev.ptr(ds.perm[e]),
+                      _dev.stream())
+        return
+    key = (n, epochs)
+    host = _PINNED_PERM.get(key)
+    if host is None:
+        host = _dev.pinned_empty((epochs, n), np.int64)
+        _PINNED_PERM[key] = host
+    # the pinned buffer may still be read by a previous async copy
+    _lib.call("ul_stream_sync", _dev.stream())
+    for e in range(epochs):
+        host[e] = rng.permutation(n)
+    _dev.h2d(ds.perm[:epochs], host)
+
+
+def _world():
+    return _dist.world_info()
+
+
+def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib.PpoResult:
+    s = _dev.stream()
+    cfgd = plan.desc
+    if world == 1:
+        _lib.call("ul_ppo_plan_run", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
+                  opt.critic.t, 1, s)
+    else:
+        _lib.call("ul_ppo_plan_begin", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
+                  opt.critic.t, s)
+        for e in range(cfgd.epochs):
+            for k in range(cfgd.minibatches):
+                _lib.call("ul_ppo_plan_step_grads", plan.h, e, k, s)
+                _dist.all_reduce_sum(red)
+                _lib.call("ul_ppo_plan_step_apply", plan.h, e, k, s)
+    res = _lib.PpoResult()
+    st = _lib.lib().ul_ppo_plan_finish(plan.h, C.byref(res), s)
+    opt.actor.t = int(res.t_actor)
+    opt.critic.t = int(res.t_critic)
+    if st != 0:
+        _lib.check(st, "ul_ppo_plan_finish")
+    return res
+
+
+def _epochs_on_device(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False) -> UpdateStats:
+    world, rank = _world()
+    fill_permutations(ds, rng, cfg.epochs)
+    plan = _plan_for(params, cfg, ds, world, rank, raw_adv)
+    red = None
+    if world > 1:
+        red = _dist.reduce_buffer(plan.red_len)
+    plan.bind(ds, adv, ret, oldv, params, opt, red)
+    res = run_plan(plan, params, opt, world, red)
+    return UpdateStats(policy_loss=res.policy_loss, value_loss=res.value_loss,
+                       entropy=res.entropy, kl=res.kl, lr=opt.lr, grad_norm=res.grad_norm)
+
+
+def _check_dims(segment, params: AcParams):
+    od, cd = params.actor.arch.input_dim, params.critic.arch.input_dim
+    ad = params.actor.arch.output_dim
+    if tuple(segment.obs.shape[2:]) != (od,) or tuple(segment.critic_obs.shape[2:]) != (cd,) \
+            or tuple(segment.actions.shape[2:]) != (ad,):
+        raise ValueError("segment feature widths do not match the networks")
+    return od, cd, ad
+
+
+def ppo_update(segment, params: AcParams, opt: AcOpt, cfg: PpoConfig, rng) -> UpdateStats:
+    """Epochs x minibatches of clipped-surrogate updates on one segment
+    (R:algos/ppo.py:202-229).  The segment must carry advantages/returns."""
+    if segment.advantages is None or segment.returns is None:
+        raise ValueError("segment advantages/returns not computed")
+    od, cd, ad = _check_dims(segment, params)
+    T, N = segment.horizon, segment.n_envs
+    if (T * N) % cfg.minibatches != 0:
+        raise ValueError(f"minibatches {cfg.minibatches} must divide batch size {T * N}")
+    ds = staging_for(T, N, od, cd, ad, cfg.epochs)
+    ds.load(segment)
+    return _epochs_on_device(ds, ds.adv, ds.ret, ds.values, params, opt, cfg, rng)
+
+
+def normalize_advantages(advantages):
+    """(A - mean)/(std + 1e-8) (R:algos/ppo.py:132-133).  Host helper for the
+    API surface; the update plan folds this into its loss head on device."""
+    a = _dev.to_numpy(advantages).astype(np.float64)
+    return (a - a.mean()) / (a.std() + 1e-8)
+
+
+def ppo_loss_and_grads(params: AcParams, obs, critic_obs, actions, behavior_logp, advantages,
+                       returns, old_values, cfg: PpoConfig):
+    """Loss terms + exact actor/critic gradients of one minibatch, no optimizer
+    step (R:algos/ppo.py:70-129).  Runs the plan's grad phase over all rows."""
+    from .segment import RolloutSegment
+
+    obs = np.asarray(_dev.to_numpy(obs))
+    n = obs.shape[0]
+
+    def one(x):  # (n, ...) -> (1, n, ...): a one-step "segment"
+        a = np.asarray(_dev.to_numpy(x))
+        return a.reshape(1, n, *a.shape[1:])
+
+    seg = RolloutSegment(obs=one(obs), critic_obs=one(critic_obs), actions=one(actions),
+                         behavior_log_prob=one(behavior_logp), rewards=np.zeros((1, n)),
+                         terminated=np.zeros((1, n), bool), truncated=np.zeros((1, n), bool),
+                         values=one(old_values), bootstrap_value=np.zeros(n),
+                         advantages=one(advantages), returns=one(returns))
+    od, cd, ad = _check_dims(seg, params)
+    cfg1 = PpoConfig(**{**cfg.__dict__, "epochs": 1, "minibatches": 1})
+    ds = staging_for(1, n, od, cd, ad, 1, slot="loss")
+    ds.load(seg)
+    _dev.h2d(ds.perm[0], np.arange(n, dtype=np.int64))
+    plan = _plan_for(params, cfg1, ds, 1, 0, raw_adv=True)
+    scratch = AcOpt.for_params(params, 0.0)
+    plan.bind(ds, ds.adv, ds.ret, ds.values, params, scratch)
+    s = _dev.stream()
+    _lib.call("ul_ppo_plan_begin", plan.h, 0.0, 0.0, 0, 0, s)
+    _lib.call("ul_ppo_plan_step_grads", plan.h, 0, 0, s)
+    p = C.c_void_p()
+    m = C.c_int64()
+    _lib.call("ul_ppo_plan_reduce_buffer", plan.h, C.byref(p), C.byref(m))
+    host = np.empty(m.value, np.float32)
+    _lib.call("ul_memcpy_async", host.ctypes.data, p.value, host.nbytes, s)
+    _lib.call("ul_stream_sync", s)
+    pa, pc = params.actor.buf.numel(), params.critic.buf.numel()
+    ga = Grads(torch.empty_like(params.actor.buf), params.actor.arch)
+    gc = Grads(torch.empty_like(params.critic.buf), params.critic.arch)
+    _dev.h2d(ga.buf, host[:pa])
+    _dev.h2d(gc.buf, host[pa:pa + pc])
+    pol_sum, val_sum, kl_sum = (float(x) for x in host[pa + pc:pa + pc + 3])
+    log_std = _dev.to_numpy(params.actor.log_std).astype(np.float64)
+    entropy = float(np.sum(log_std + 0.5 * (np.log(2 * np.pi) + 1.0)))
+    policy_loss, value_loss = -pol_sum / n, val_sum / n
+    total = policy_loss + cfg.value_loss_coef * value_loss - cfg.entropy_coef * entropy
+    terms = dict(policy_loss=policy_loss, value_loss=value_loss, entropy=entropy, total=total,
+                 kl=kl_sum / n)
+    return terms, ga, gc
+
+
+def adaptive_lr_step(lr: float, measured_kl: float, cfg: PpoConfig, update_index: int) -> float:
+    """Dead-band adaptive LR (R:algos/ppo.py:232-250); host scalar logic."""
+    if cfg.schedule != "adaptive":
+        return lr
+    if update_index % cfg.adaptive_lr_update_interval != 0:
+        return lr
+    if measured_kl > cfg.desired_kl / cfg.adaptive_kl_beta:
+        lr = lr / cfg.adaptive_lr_decay
+    elif measured_kl < cfg.desired_kl * cfg.adaptive_kl_beta:
+        lr = lr * cfg.adaptive_lr_growth
+    return float(np.clip(lr, 1e-6, 1e-2))
+
+
+def gae_into(ds, gamma: float, lam: float) -> None:
+    """GAE (K1) over a staged DeviceSegment, writing ds.adv / ds.ret in place."""
+    _lib.call("ul_gae_f32", _dev.ptr(ds.rewards), _dev.ptr(ds.values), _dev.ptr(ds.term),
+              _dev.ptr(ds.trunc), _dev.ptr(ds.tv) if ds.has_tv else None, _dev.ptr(ds.boot),
+              ds.T, ds.N, float(gamma), float(lam), _dev.ptr(ds.adv), _dev.ptr(ds.ret),
+              _dev.stream())
+
+
+def ppo_update_resident(ds, params: AcParams, opt: AcOpt, cfg: PpoConfig, rng) -> UpdateStats:
+    """gae + ppo_update on a segment that is already resident in HBM (the
+    learner half of R:runtime/ppo_runner.py:95-102 without the H2D)."""
+    gae_into(ds, cfg.gamma, cfg.lam)
+    return _epochs_on_device(ds, ds.adv, ds.ret, ds.values, params, opt, cfg, rng)
+
+
+def plan_stats(params: AcParams, cfg: PpoConfig, ds) -> dict:
+    """Kernels per update and algorithmic GEMM FLOPs of the bound plan."""
+    world, rank = _world()
+    plan = _plan_for(params, cfg, ds, world, rank)
+    k = C.c_int64()
+    f = C.c_double()
+    _lib.call("ul_ppo_plan_counts", plan.h, C.byref(k), C.byref(f))
+    return {"kernels_per_update": int(k.value), "gemm_flops_per_update": float(f.value)}
+
+
+def profile_update(params: AcParams, opt: AcOpt, cfg: PpoConfig, ds) -> dict:
+    """One un-graphed update with CUDA events per kernel class (ms)."""
+    world, rank = _world()
+    plan = _plan_for(params, cfg, ds, world, rank)
+    ms = (C.c_double * 5)()
+    _lib.call("ul_ppo_plan_profile", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
+              opt.critic.t, ms, _dev.stream())
+    res = _lib.PpoResult()
+    _lib.lib().ul_ppo_plan_finish(plan.h, C.byref(res), _dev.stream())
+    opt.actor.t, opt.critic.t = int(res.t_actor), int(res.t_critic)
+    return dict(gemm=ms[0], gather=ms[1], heads=ms[2], optimizer=ms[3], total=ms[4])

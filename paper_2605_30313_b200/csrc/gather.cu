@@ -1,0 +1,192 @@
+// K4 minibatch gather, K5 replay ring insert, K6 replay sample gather,
+// plus the device minibatch permutation used in performance mode.
+//
+// Replaces the fancy-index copies of R:algos/ppo.py:161-176 (obs[idx], ...),
+// ReplayStorage.insert R:replaypath/storage.py:76-104 and the sampled-row
+// copy of _read_rows_locked :106-110 / DeviceReplayCache :245-249.
+//
+// One launch gathers several arrays that share an index vector ("descs"):
+// the work of each desc is flattened to (row, 16/8/4-byte unit) items so a
+// warp always streams contiguous bytes of a row, whatever the row width
+// (obs 940 B, actions 48 B, scalars 4 B).  Algorithmic bytes: 2 x rows x
+// row_bytes + 8 B/index.
+#include "internal.cuh"
+
+namespace ul {
+namespace {
+
+constexpr int kMaxDesc = 12;
+
+struct GatherTable {
+  const char* src[kMaxDesc];
+  char* dst[kMaxDesc];
+  int64_t src_stride[kMaxDesc];  // bytes
+  int64_t dst_stride[kMaxDesc];  // bytes
+  int64_t units[kMaxDesc];       // units per row
+  int unit[kMaxDesc];            // unit bytes (16, 8 or 4)
+  int ndesc;
+};
+
+template <int U>
+struct Vec;
+template <>
+struct Vec<16> { using T = uint4; };
+template <>
+struct Vec<8> { using T = uint2; };
+template <>
+struct Vec<4> { using T = uint32_t; };
+
+template <int U>
+__device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __restrict__ dst,
+                                          int64_t sst, int64_t dstr, int64_t upr,
+                                          const int64_t* __restrict__ idx, int64_t n,
+                                          int64_t modulo, int64_t lo, int64_t hi, int* err) {
+  using T = typename Vec<U>::T;
+  const int64_t total = n * upr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += stride) {
+    const int64_t r = w / upr, u = w - r * upr;
+    int64_t s = idx ? idx[r] : r;
+    if (s < lo || s >= hi) {
+      if (err) atomicOr(err, 1);
+      continue;
+    }
+    if (modulo > 0) s %= modulo;
+    const T v = __ldg(reinterpret_cast<const T*>(src + s * sst) + u);
+    reinterpret_cast<T*>(dst + r * dstr)[u] = v;
+  }
+}
+
+__global__ void gather_kernel(GatherTable t, const int64_t* __restrict__ idx, int64_t n,
+                              int64_t modulo, int64_t lo, int64_t hi, int* err) {
+  const int d = blockIdx.y;
+  if (d >= t.ndesc) return;
+  switch (t.unit[d]) {
+    case 16:
+      copy_rows<16>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
+                    modulo, lo, hi, err);
+      break;
+    case 8:
+      copy_rows<8>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
+                   modulo, lo, hi, err);
+      break;
+    default:
+      copy_rows<4>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
+                   modulo, lo, hi, err);
+  }
+}
+
+int unit_for(uintptr_t a, uintptr_t b, int64_t s1, int64_t s2, int64_t rb) {
+  for (int u = 16; u >= 4; u >>= 1)
+    if (a % u == 0 && b % u == 0 && s1 % u == 0 && s2 % u == 0 && rb % u == 0) return u;
+  return 0;
+}
+
+// ------------------------------------------------- device permutation (perf mode)
+// Keyed Feistel bijection on [0, 2^(2h)) + cycle walking into [0, n).  Not the
+// numpy Philox shuffle (that stream is sequential); used only when the caller
+// opts into device-generated minibatch indices.
+__device__ __forceinline__ uint32_t mix32(uint32_t x, uint32_t k) {
+  x ^= k;
+  x *= 0x9E3779B1u;
+  x ^= x >> 15;
+  x *= 0x85EBCA77u;
+  x ^= x >> 13;
+  return x;
+}
+
+__global__ void feistel_perm_kernel(int64_t n, int half_bits, uint64_t seed, int64_t* out) {
+  const uint32_t mask = (1u << half_bits) - 1u;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t x = (uint64_t)i;
+    do {
+      uint32_t L = (uint32_t)(x >> half_bits) & mask, R = (uint32_t)x & mask;
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const uint32_t F = mix32(R + (uint32_t)r * 0x632BE5ABu, (r & 1) ? k1 : k0) & mask;
+        const uint32_t nl = R;
+        R = L ^ F;
+        L = nl;
+      }
+      x = ((uint64_t)L << half_bits) | R;
+    } while (x >= (uint64_t)n);
+    out[i] = (int64_t)x;
+  }
+}
+
+}  // namespace
+}  // namespace ul
+
+// Gather rows of up to 12 arrays by one index vector.  desc arrays have ndesc
+// entries: src/dst device pointers, strides and row widths in BYTES.  Rows are
+// src + (idx[i] [% modulo]) * src_stride.  Indices outside [lo, hi) are
+// skipped and raise *err (device flag).  idx == NULL gathers rows 0..n-1.
+extern "C" int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
+                              const int64_t* src_stride, const int64_t* dst_stride,
+                              const int64_t* row_bytes, const int64_t* idx, int64_t n,
+                              int64_t modulo, int64_t lo, int64_t hi, int* err, void* stream) {
+  UL_CHECK_ARG(ndesc >= 1 && ndesc <= ul::kMaxDesc, "gather: ndesc %d outside [1,%d]", ndesc,
+               ul::kMaxDesc);
+  UL_CHECK_ARG(n >= 0, "gather: negative row count");
+  if (n == 0) return UL_OK;
+  ul::GatherTable t{};
+  t.ndesc = ndesc;
+  int64_t max_units = 1;
+  for (int d = 0; d < ndesc; ++d) {
+    const int u = ul::unit_for((uintptr_t)src[d], (uintptr_t)dst[d], src_stride[d], dst_stride[d],
+                               row_bytes[d]);
+    UL_CHECK_ARG(u > 0, "gather: desc %d not 4-byte aligned", d);
+    t.src[d] = (const char*)src[d];
+    t.dst[d] = (char*)dst[d];
+    t.src_stride[d] = src_stride[d];
+    t.dst_stride[d] = dst_stride[d];
+    t.unit[d] = u;
+    t.units[d] = row_bytes[d] / u;
+    max_units = t.units[d] > max_units ? t.units[d] : max_units;
+  }
+  int64_t blocks = ul::ceil_div(n * max_units, 256);
+  blocks = blocks > 4 * ul::kNumSMs ? 4 * ul::kNumSMs : blocks;
+  ul::gather_kernel<<<dim3((unsigned)blocks, ndesc), 256, 0, ul::as_stream(stream)>>>(
+      t, idx, n, modulo, lo, hi, err);
+  return ul::check_launch("gather_kernel");
+}
+
+// Replay ring insert (R:replaypath/storage.py:76-104): write n rows of `width`
+// floats at absolute index head.. into ring[cap, width]; rows may live in
+// pinned host memory (H2D) or device memory (D2D).  n >= cap keeps only the
+// last cap rows, each at its own absolute slot.  1-2 async copies.
+extern "C" int ul_ring_insert(float* ring, int64_t cap, int64_t width, int64_t head,
+                              const float* rows, int64_t n, void* stream) {
+  UL_CHECK_ARG(cap >= 1 && width >= 1 && head >= 0 && n >= 0, "ring insert: bad shape");
+  if (n == 0) return UL_OK;
+  cudaStream_t s = ul::as_stream(stream);
+  int64_t first = head, count = n;
+  const float* src = rows;
+  if (n >= cap) {
+    first = head + n - cap;
+    count = cap;
+    src = rows + (n - cap) * width;
+  }
+  const int64_t start = first % cap;
+  const int64_t part1 = count < cap - start ? count : cap - start;
+  const size_t rb = sizeof(float) * (size_t)width;
+  UL_CUDA(cudaMemcpyAsync(ring + start * width, src, rb * part1, cudaMemcpyDefault, s));
+  if (count > part1)
+    UL_CUDA(cudaMemcpyAsync(ring, src + part1 * width, rb * (count - part1), cudaMemcpyDefault,
+                            s));
+  return UL_OK;
+}
+
+// Device minibatch permutation of [0, n) from a 64-bit key (performance mode).
+extern "C" int ul_device_permutation(int64_t n, uint64_t key, int64_t* out, void* stream) {
+  UL_CHECK_ARG(n >= 0 && n < (int64_t(1) << 62), "permutation: bad n");
+  if (n == 0) return UL_OK;
+  int bits = 1;
+  while ((int64_t(1) << (2 * bits)) < n) ++bits;
+  int64_t blocks = ul::ceil_div(n, 256);
+  blocks = blocks > 8 * ul::kNumSMs ? 8 * ul::kNumSMs : blocks;
+  ul::feistel_perm_kernel<<<(unsigned)blocks, 256, 0, ul::as_stream(stream)>>>(n, bits, key, out);
+  return ul::check_launch("feistel_perm_kernel");
+}

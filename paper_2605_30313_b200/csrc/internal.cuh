@@ -1,0 +1,76 @@
+// Cross-translation-unit declarations inside libunilite_b200 (not part of the ABI).
+#pragma once
+#include "common.cuh"
+
+namespace ul {
+
+// ---------------------------------------------------------------- optimizer
+struct SegTable {
+  float* g[UL_MAX_SEG];
+  float* p[UL_MAX_SEG];
+  float* m[UL_MAX_SEG];
+  float* v[UL_MAX_SEG];
+  int64_t n[UL_MAX_SEG];
+  int nseg;
+};
+int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s);
+int launch_apply(const SegTable& st, ul_opt_ctl* ctl, int write_grads, int do_adam,
+                 cudaStream_t s);
+
+// --------------------------------------------------------------------- GEMM
+// C[M,N] = sum_k A(m,k) B(k,n), fp32.
+//   A(m,k) = A[m*lda + k] if a_kmajor else A[k*lda + m]
+//   B(k,n) = B[n*ldb + k] if b_kmajor else B[k*ldb + n]
+enum Epilogue : int {
+  kEpiStore = 0,     // C = acc
+  kEpiBias = 1,      // C = acc + bias[n]
+  kEpiBiasElu = 2,   // C = elu(acc + bias[n])
+  kEpiEluGrad = 3,   // C = acc * (min(aux[m,n],0)+1)
+};
+
+struct GemmDesc {
+  int64_t M, N, K;
+  const float* A;
+  int64_t lda;
+  const float* B;
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+  const float* bias;
+  const float* aux;
+  int64_t ldaux;
+  bool a_kmajor, b_kmajor;
+  int epi;
+  // split-K over K: when splits > 1, C must be a workspace of splits*M*N
+  // floats (partial tiles, ld = N) and a reduction pass follows.
+  int splits;
+  // optional: per-row sums of A over K (db of a dW GEMM), written per split
+  // into rowsum[z*M + m]
+  float* rowsum;
+};
+int gemm_f32(const GemmDesc& d, cudaStream_t s);
+// number of K splits gemm_f32 actually launches for a requested split count
+int gemm_num_splits(int64_t K, int splits);
+// out[j] (+)= sum_z ws[z*len + j], j < len
+int reduce_splits(const float* ws, int splits, int64_t len, float* out, int64_t ld_rows,
+                  int64_t row_len, cudaStream_t s);
+
+// ------------------------------------------------------------------ MLP
+struct NetView {
+  int n_layers;
+  int dims[UL_MAX_LAYERS + 1];
+  int64_t w_off[UL_MAX_LAYERS], b_off[UL_MAX_LAYERS], logstd_off, total;
+};
+int make_view(const ul_net_desc* d, NetView* v);
+int64_t act_floats(const NetView& v, int64_t M);
+int64_t bwd_work_floats(const NetView& v, int64_t M);
+int mlp_forward(const NetView& v, const float* params, const float* x, int64_t ldx, int64_t M,
+                float* acts, float* out, int64_t ld_out, cudaStream_t s);
+// dx_cols: compute dX only for input columns [dx_col0, dx_col0 + dx_ncols) (SAC dQ/da);
+// want_dw = false skips dW/db (pure input-gradient pass).
+int mlp_backward(const NetView& v, const float* params, const float* x, int64_t ldx, int64_t M,
+                 const float* acts, const float* dout, int64_t ld_dout, float* grads,
+                 float* dx, int64_t lddx, int dx_col0, int dx_ncols, bool want_dw,
+                 bool zero_logstd, float* work, cudaStream_t s);
+
+}  // namespace ul

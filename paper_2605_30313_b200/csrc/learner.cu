@@ -1,0 +1,473 @@
+// Native PPO/APPO update plan: the epoch x minibatch loop of R:algos/ppo.py:136-199.
+//
+// A plan owns every per-step device buffer (minibatch staging, activation
+// caches, gradient/all-reduce buffer, loss partials, optimizer control) so a
+// whole update is a fixed sequence of launches on fixed pointers; it is
+// captured once into a CUDA graph and replayed per update (one launch, no
+// host round trip until the statistics are read back).  Per step:
+//   gather (K4) -> actor fwd, critic fwd (K7) -> PPO head (K9) ->
+//   actor bwd, critic bwd (K8) -> [caller all-reduce] -> loss finalize ->
+//   joint clip + Adam(actor) + Adam(critic) (K13).
+#include <stdlib.h>
+
+#include <new>
+
+#include "learner.cuh"
+
+namespace ul {
+namespace {
+
+
+struct PpoPlan {
+  ul_ppo_plan_desc d{};
+  NetView va{}, vc{};
+  int A = 0;
+  int64_t rows = 0, mb = 0, mb_local = 0;
+  int64_t ld_mo = 0, ld_mc = 0, ld_ma = 0;  // minibatch staging row strides
+  int64_t Pa = 0, Pc = 0;
+  // device arena
+  char* arena = nullptr;
+  float *mb_obs = nullptr, *mb_cobs = nullptr, *mb_act = nullptr, *mb_scal = nullptr;
+  float *acts_a = nullptr, *acts_c = nullptr, *out_a = nullptr, *out_c = nullptr;
+  float *dmean = nullptr, *dv = nullptr, *work = nullptr, *red = nullptr, *red_own = nullptr;
+  double *head_part = nullptr, *adv_stats = nullptr, *adv_part = nullptr;
+  unsigned int* tickets = nullptr;  // [0] head, [1] adv stats
+  ul_opt_ctl* ctl_d = nullptr;
+  ul_ppo_stats* st_d = nullptr;
+  // pinned mirrors
+  ul_opt_ctl* ctl_h = nullptr;
+  ul_ppo_stats* st_h = nullptr;
+  ul_ppo_bindings b{};
+  bool bound = false;
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_kernels = 0;
+  // optional per-phase CUDA-event profiling (ul_ppo_plan_profile)
+  struct Prof {
+    static constexpr int kMax = 4096;
+    cudaEvent_t ev[kMax];
+    int cat[kMax];
+    int n = 0;
+    bool on = false;
+  };
+  Prof* prof = nullptr;
+};
+
+// record a phase boundary: the interval ending here belongs to class `cat`
+inline void mark(PpoPlan* p, int cat, cudaStream_t s) {
+  if (!p->prof || !p->prof->on || p->prof->n >= PpoPlan::Prof::kMax) return;
+  auto* pr = p->prof;
+  cudaEventRecord(pr->ev[pr->n], s);
+  pr->cat[pr->n] = cat;
+  pr->n++;
+}
+
+size_t ctl_header_bytes() { return offsetof(ul_opt_ctl, part); }
+
+int alloc_plan(PpoPlan* p) {
+  const int64_t ml = p->mb_local;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_obs = carve(sizeof(float) * ml * p->ld_mo);
+  const size_t o_cobs = carve(sizeof(float) * ml * p->ld_mc);
+  const size_t o_act = carve(sizeof(float) * ml * p->ld_ma);
+  const size_t o_scal = carve(sizeof(float) * ml * 4);
+  const size_t o_acta = carve(sizeof(float) * act_floats(p->va, ml));
+  const size_t o_actc = carve(sizeof(float) * act_floats(p->vc, ml));
+  const size_t o_outa = carve(sizeof(float) * ml * p->A);
+  const size_t o_outc = carve(sizeof(float) * ml);
+  const size_t o_dmean = carve(sizeof(float) * ml * p->A);
+  const size_t o_dv = carve(sizeof(float) * ml);
+  const int64_t wa = bwd_work_floats(p->va, ml), wc = bwd_work_floats(p->vc, ml);
+  const size_t o_work = carve(sizeof(float) * (wa > wc ? wa : wc));
+  const size_t o_red = carve(sizeof(float) * (p->Pa + p->Pc + 4));
+  const size_t o_hp = carve(sizeof(double) * ppo_head_partial_doubles(ml, p->A));
+  const size_t o_as = carve(sizeof(double) * 4);
+  const size_t o_ap = carve(sizeof(double) * 2 * kAdvStatBlocks);
+  const size_t o_tk = carve(sizeof(unsigned int) * 8);
+  const size_t o_ctl = carve(sizeof(ul_opt_ctl));
+  const size_t o_st = carve(sizeof(ul_ppo_stats));
+  UL_CUDA(cudaMalloc(&p->arena, off));
+  UL_CUDA(cudaMemset(p->arena, 0, off));
+  char* a = p->arena;
+  p->mb_obs = (float*)(a + o_obs);
+  p->mb_cobs = (float*)(a + o_cobs);
+  p->mb_act = (float*)(a + o_act);
+  p->mb_scal = (float*)(a + o_scal);
+  p->acts_a = (float*)(a + o_acta);
+  p->acts_c = (float*)(a + o_actc);
+  p->out_a = (float*)(a + o_outa);
+  p->out_c = (float*)(a + o_outc);
+  p->dmean = (float*)(a + o_dmean);
+  p->dv = (float*)(a + o_dv);
+  p->work = (float*)(a + o_work);
+  p->red_own = (float*)(a + o_red);
+  p->red = p->red_own;
+  p->head_part = (double*)(a + o_hp);
+  p->adv_stats = (double*)(a + o_as);
+  p->adv_part = (double*)(a + o_ap);
+  p->tickets = (unsigned int*)(a + o_tk);
+  p->ctl_d = (ul_opt_ctl*)(a + o_ctl);
+  p->st_d = (ul_ppo_stats*)(a + o_st);
+  UL_CUDA(cudaHostAlloc(&p->ctl_h, sizeof(ul_opt_ctl), cudaHostAllocPortable));
+  UL_CUDA(cudaHostAlloc(&p->st_h, sizeof(ul_ppo_stats), cudaHostAllocPortable));
+  UL_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+  return UL_OK;
+}
+
+void free_plan(PpoPlan* p) {
+  if (p->prof) {
+    for (int i = 0; i < PpoPlan::Prof::kMax; ++i) cudaEventDestroy(p->prof->ev[i]);
+    delete p->prof;
+  }
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  if (p->arena) cudaFree(p->arena);
+  if (p->ctl_h) cudaFreeHost(p->ctl_h);
+  if (p->st_h) cudaFreeHost(p->st_h);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
+}
+
+// device part of begin: stats reset + advantage statistics (graph-capturable)
+int begin_device(PpoPlan* p, cudaStream_t s) {
+  UL_CUDA(cudaMemsetAsync(p->st_d, 0, sizeof(ul_ppo_stats), s));
+  // critic log_std never receives a gradient (R:algos/ppo.py:119); keep its slot zero
+  UL_CUDA(cudaMemsetAsync(p->red + p->Pa + p->vc.logstd_off, 0, sizeof(float), s));
+  if (p->d.raw_advantages) return UL_OK;
+  return launch_adv_stats(p->b.adv, p->rows, p->adv_part, p->tickets + 1, p->adv_stats, s);
+}
+
+int upload_ctl(PpoPlan* p, double lr_a, double lr_c, int64_t t_a, int64_t t_c, cudaStream_t s) {
+  const double lr[2] = {lr_a, lr_c};
+  UL_TRY(ul_opt_ctl_init(p->ctl_h, 2, lr, 0.9, 0.999, 1e-8, p->d.max_grad_norm));
+  p->ctl_h->t[0] = t_a;
+  p->ctl_h->t[1] = t_c;
+  UL_CUDA(cudaMemcpyAsync(p->ctl_d, p->ctl_h, ctl_header_bytes(), cudaMemcpyHostToDevice, s));
+  return UL_OK;
+}
+
+int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
+  const ul_ppo_bindings& b = p->b;
+  const int64_t ml = p->mb_local;
+  const int64_t* idx = p->d.local_shards
+                           ? b.perm + (int64_t)e * p->rows + (int64_t)k * ml
+                           : b.perm + (int64_t)e * p->rows + (int64_t)k * p->mb + p->d.rank * ml;
+  // K4: one gather launch for the 7 per-row arrays
+  const void* src[7] = {b.obs, b.cobs, b.act, b.blogp, b.adv, b.ret, b.oldv};
+  void* dst[7] = {p->mb_obs, p->mb_cobs, p->mb_act, p->mb_scal, p->mb_scal + ml,
+                  p->mb_scal + 2 * ml, p->mb_scal + 3 * ml};
+  const int64_t sst[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->d.ld_act, 4, 4, 4, 4};
+  const int64_t dstr[7] = {4 * p->ld_mo, 4 * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
+  const int64_t rb[7] = {4 * p->ld_mo, 4 * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
+  UL_TRY(ul_gather_rows(7, src, dst, sst, dstr, rb, idx, ml, 0, 0, p->rows, nullptr, s));
+  mark(p, 1, s);
+  // K7 forwards
+  UL_TRY(mlp_forward(p->va, b.actor_params, p->mb_obs, p->ld_mo, ml, p->acts_a, p->out_a, p->A, s));
+  UL_TRY(mlp_forward(p->vc, b.critic_params, p->mb_cobs, p->ld_mc, ml, p->acts_c, p->out_c, 1, s));
+  mark(p, 0, s);
+  // K9 head
+  PpoHeadArgs h{};
+  h.n_local = ml;
+  h.n_global = (double)p->mb;
+  h.A = p->A;
+  h.mean = p->out_a;
+  h.ld_mean = p->A;
+  h.log_std = b.actor_params + p->va.logstd_off;
+  h.act = p->mb_act;
+  h.ld_act = p->ld_ma;
+  h.blogp = p->mb_scal;
+  h.adv = p->mb_scal + ml;
+  h.ret = p->mb_scal + 2 * ml;
+  h.oldv = p->mb_scal + 3 * ml;
+  h.v = p->out_c;
+  h.ld_v = 1;
+  h.adv_stats = p->d.raw_advantages ? nullptr : p->adv_stats;
+  h.clip = p->d.clip_param;
+  h.vcoef = p->d.value_loss_coef;
+  h.clipped_v = p->d.use_clipped_value_loss;
+  h.dmean = p->dmean;
+  h.ld_dmean = p->A;
+  h.dv = p->dv;
+  h.part = p->head_part;
+  h.ticket = p->tickets;
+  h.dlogstd_out = p->red + p->va.logstd_off;
+  h.loss_out = p->red + p->Pa + p->Pc;
+  h.ent_coef_add = p->d.rank == 0 ? -p->d.entropy_coef : 0.0;
+  UL_TRY(launch_ppo_head(h, s));
+  mark(p, 2, s);
+  // K8 backwards into the contiguous all-reduce buffer
+  UL_TRY(mlp_backward(p->va, b.actor_params, p->mb_obs, p->ld_mo, ml, p->acts_a, p->dmean, p->A,
+                      p->red, nullptr, 0, 0, 0, true, false, p->work, s));
+  UL_TRY(mlp_backward(p->vc, b.critic_params, p->mb_cobs, p->ld_mc, ml, p->acts_c, p->dv, 1,
+                      p->red + p->Pa, nullptr, 0, 0, 0, true, true, p->work, s));
+  mark(p, 0, s);
+  return UL_OK;
+}
+
+int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
+  (void)e;
+  const ul_ppo_bindings& b = p->b;
+  UL_TRY(launch_ppo_loss_finalize(p->red + p->Pa + p->Pc, b.actor_params + p->va.logstd_off, p->A,
+                                  (double)p->mb, p->d.value_loss_coef, p->d.entropy_coef,
+                                  k == p->d.minibatches - 1, p->ctl_d, p->st_d, s));
+  mark(p, 2, s);
+  SegTable st{};
+  st.nseg = 2;
+  st.g[0] = p->red;
+  st.g[1] = p->red + p->Pa;
+  st.p[0] = b.actor_params;
+  st.p[1] = b.critic_params;
+  st.m[0] = b.actor_m;
+  st.m[1] = b.critic_m;
+  st.v[0] = b.actor_v;
+  st.v[1] = b.critic_v;
+  st.n[0] = p->Pa;
+  st.n[1] = p->Pc;
+  UL_TRY(launch_prepare(st, p->ctl_d, s));
+  UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s));
+  mark(p, 3, s);
+  return UL_OK;
+}
+
+int all_steps(PpoPlan* p, cudaStream_t s) {
+  UL_TRY(begin_device(p, s));
+  for (int e = 0; e < p->d.epochs; ++e)
+    for (int k = 0; k < p->d.minibatches; ++k) {
+      UL_TRY(step_grads(p, e, k, s));
+      UL_TRY(step_apply(p, e, k, s));
+    }
+  return UL_OK;
+}
+
+}  // namespace
+}  // namespace ul
+
+using ul::PpoPlan;
+
+extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
+  UL_CHECK_ARG(desc && plan, "ppo plan: null argument");
+  PpoPlan* p = new (std::nothrow) PpoPlan();
+  UL_CHECK_ARG(p != nullptr, "ppo plan: out of host memory");
+  p->d = *desc;
+  int st = ul::make_view(&desc->actor, &p->va);
+  if (st == UL_OK) st = ul::make_view(&desc->critic, &p->vc);
+  if (st != UL_OK) {
+    delete p;
+    return st;
+  }
+  p->A = p->va.dims[p->va.n_layers];
+  p->rows = desc->rows;
+  const int ws = desc->world_size < 1 ? 1 : desc->world_size;
+  auto fail = [&](const char* msg) {
+    ul::set_error("%s", msg);
+    delete p;
+    return UL_ERR_VALUE;
+  };
+  if (p->vc.dims[p->vc.n_layers] != 1) return fail("ppo plan: critic output must be 1");
+  if (p->A > UL_MAX_ACT) return fail("ppo plan: action dim above UL_MAX_ACT");
+  if (desc->minibatches < 1 || desc->epochs < 0) return fail("ppo plan: bad epochs/minibatches");
+  if (desc->rows % desc->minibatches != 0) {
+    ul::set_error("minibatches %d must divide batch size %lld", desc->minibatches,
+                  (long long)desc->rows);
+    delete p;
+    return UL_ERR_VALUE;
+  }
+  if (desc->rank < 0 || desc->rank >= ws) return fail("ppo plan: bad rank");
+  if (desc->local_shards) {
+    p->mb_local = desc->rows / desc->minibatches;
+    p->mb = p->mb_local * ws;
+  } else {
+    p->mb = desc->rows / desc->minibatches;
+    if (p->mb % ws != 0) return fail("ppo plan: world_size must divide the minibatch");
+    p->mb_local = p->mb / ws;
+  }
+  if (desc->ld_obs < p->va.dims[0] || desc->ld_cobs < p->vc.dims[0] || desc->ld_act < p->A)
+    return fail("ppo plan: leading dimension below feature width");
+  p->ld_mo = desc->ld_obs;
+  p->ld_mc = desc->ld_cobs;
+  p->ld_ma = desc->ld_act;
+  p->Pa = p->va.total;
+  p->Pc = p->vc.total;
+  st = ul::alloc_plan(p);
+  if (st != UL_OK) {
+    ul::free_plan(p);
+    delete p;
+    return st;
+  }
+  *plan = p;
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_destroy(void* plan) {
+  PpoPlan* p = (PpoPlan*)plan;
+  if (!p) return UL_OK;
+  ul::free_plan(p);
+  delete p;
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_bind(void* plan, const ul_ppo_bindings* b) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && b, "ppo plan: null argument");
+  const bool same = p->bound && memcmp(&p->b, b, sizeof(*b)) == 0;
+  if (!same && p->graph) {
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+  }
+  p->b = *b;
+  p->bound = true;
+  p->red = b->reduce_buf ? b->reduce_buf : p->red_own;
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_begin(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
+                                 int64_t t_critic, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "ppo plan: not bound");
+  cudaStream_t s = ul::as_stream(stream);
+  UL_TRY(ul::upload_ctl(p, lr_actor, lr_critic, t_actor, t_critic, s));
+  return ul::begin_device(p, s);
+}
+
+extern "C" int ul_ppo_plan_step_grads(void* plan, int epoch, int k, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "ppo plan: not bound");
+  UL_CHECK_ARG(epoch >= 0 && epoch < p->d.epochs && k >= 0 && k < p->d.minibatches,
+               "ppo plan: step out of range");
+  return ul::step_grads(p, epoch, k, ul::as_stream(stream));
+}
+
+extern "C" int ul_ppo_plan_step_apply(void* plan, int epoch, int k, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "ppo plan: not bound");
+  return ul::step_apply(p, epoch, k, ul::as_stream(stream));
+}
+
+extern "C" int ul_ppo_plan_reduce_buffer(void* plan, float** ptr, int64_t* n) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && ptr && n, "ppo plan: null argument");
+  *ptr = p->red;
+  *n = p->Pa + p->Pc + 3;
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
+                               int64_t t_critic, int use_graph, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "ppo plan: not bound");
+  cudaStream_t s = ul::as_stream(stream);
+  UL_TRY(ul::upload_ctl(p, lr_actor, lr_critic, t_actor, t_critic, s));
+  if (!use_graph) return ul::all_steps(p, s);
+  // run on the plan's capture stream, ordered after / before the caller's stream
+  UL_CUDA(cudaEventRecord(p->ev_in, s));
+  UL_CUDA(cudaStreamWaitEvent(p->cap_stream, p->ev_in, 0));
+  if (!p->graph) {
+    cudaGraph_t g;
+    UL_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int st = ul::all_steps(p, p->cap_stream);
+    cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &g);
+    if (st != UL_OK) return st;
+    UL_CUDA(ce);
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    cudaGraphNode_t* nodes = (cudaGraphNode_t*)malloc(sizeof(cudaGraphNode_t) * (nn ? nn : 1));
+    cudaGraphGetNodes(g, nodes, &nn);
+    p->graph_kernels = 0;
+    for (size_t i = 0; i < nn; ++i) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nodes[i], &t);
+      if (t == cudaGraphNodeTypeKernel) p->graph_kernels++;
+    }
+    free(nodes);
+    ce = cudaGraphInstantiate(&p->graph, g, 0);
+    cudaGraphDestroy(g);
+    UL_CUDA(ce);
+  }
+  UL_CUDA(cudaGraphLaunch(p->graph, p->cap_stream));
+  UL_CUDA(cudaEventRecord(p->ev_out, p->cap_stream));
+  UL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_finish(void* plan, ul_ppo_result* out, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && out, "ppo plan: null argument");
+  cudaStream_t s = ul::as_stream(stream);
+  UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl_d, ul::ctl_header_bytes(), cudaMemcpyDeviceToHost, s));
+  UL_CUDA(cudaMemcpyAsync(p->st_h, p->st_d, sizeof(ul_ppo_stats), cudaMemcpyDeviceToHost, s));
+  UL_CUDA(cudaStreamSynchronize(s));
+  const double nb = (double)p->d.epochs * p->d.minibatches;
+  const ul_ppo_stats& st = *p->st_h;
+  out->policy_loss = nb > 0 ? st.policy_sum / nb : 0.0;
+  out->value_loss = nb > 0 ? st.value_sum / nb : 0.0;
+  out->entropy = nb > 0 ? st.entropy_sum / nb : 0.0;
+  out->kl = p->d.epochs > 0 ? st.kl_epoch_sum / p->d.epochs : 0.0;
+  out->grad_norm = p->ctl_h->steps > 0 ? p->ctl_h->norm : 0.0;
+  out->t_actor = p->ctl_h->t[0];
+  out->t_critic = p->ctl_h->t[1];
+  out->diverged = p->ctl_h->diverged;
+  out->fail_step = p->ctl_h->fail_step;
+  if (out->diverged) {
+    ul::set_error("non-finite PPO loss or gradients at step %d", out->fail_step);
+    return UL_ERR_DIVERGENCE;
+  }
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_counts(void* plan, int64_t* kernels_per_update,
+                                  double* gemm_flops_per_update) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && kernels_per_update && gemm_flops_per_update, "ppo plan: null argument");
+  *kernels_per_update = p->graph_kernels;
+  // algorithmic FLOPs: forward + dW of every layer, dX of every layer but the first
+  double f = 0.0;
+  for (const ul::NetView* v : {&p->va, &p->vc}) {
+    double macs = 0.0, first = (double)v->dims[0] * v->dims[1];
+    for (int i = 0; i < v->n_layers; ++i) macs += (double)v->dims[i] * v->dims[i + 1];
+    f += 2.0 * (double)p->mb_local * (macs + macs + (macs - first));
+  }
+  *gemm_flops_per_update = f * p->d.epochs * p->d.minibatches;
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
+                                   int64_t t_critic, double* ms, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound && ms, "ppo plan: not bound");
+  cudaStream_t s = ul::as_stream(stream);
+  if (!p->prof) {
+    p->prof = new PpoPlan::Prof();
+    for (int i = 0; i < PpoPlan::Prof::kMax; ++i) UL_CUDA(cudaEventCreate(&p->prof->ev[i]));
+  }
+  p->prof->n = 0;
+  p->prof->on = true;
+  UL_TRY(ul::upload_ctl(p, lr_actor, lr_critic, t_actor, t_critic, s));
+  UL_TRY(ul::begin_device(p, s));
+  ul::mark(p, 4, s);
+  int st = UL_OK;
+  for (int e = 0; e < p->d.epochs && st == UL_OK; ++e)
+    for (int k = 0; k < p->d.minibatches && st == UL_OK; ++k) {
+      st = ul::step_grads(p, e, k, s);
+      if (st == UL_OK) st = ul::step_apply(p, e, k, s);
+    }
+  p->prof->on = false;
+  UL_TRY(st);
+  UL_CUDA(cudaStreamSynchronize(s));
+  for (int c = 0; c < 5; ++c) ms[c] = 0.0;
+  for (int i = 1; i < p->prof->n; ++i) {
+    float t = 0.f;
+    UL_CUDA(cudaEventElapsedTime(&t, p->prof->ev[i - 1], p->prof->ev[i]));
+    const int c = p->prof->cat[i];
+    if (c >= 0 && c < 4) ms[c] += t;
+    ms[4] += t;
+  }
+  return UL_OK;
+}

@@ -1,0 +1,233 @@
+// K13 Adam + joint global-norm clip + finiteness, K12 Polyak.
+//
+// Replaces R:tensornet/adam.py:30-40 (clip_global_norm), :43-80 (adam_step) and
+// R:algos/sac.py:100-108 (soft_update).  All state (lr, t, norm, divergence) is
+// device resident in a ul_opt_ctl record so the whole PPO step sequence can be
+// captured in one CUDA graph with no host round trip:
+//   prepare : one persistent pass over every gradient segment -> per-block
+//             (sum g^2, #non-finite) partials; the last block reduces them in a
+//             fixed order (deterministic), computes the joint norm and clip
+//             factor, decides per segment whether Adam runs (reference order:
+//             loss check, then segment 0 finiteness, then segment 1, ...),
+//             increments the per-segment step counters and latches `diverged`.
+//   apply   : elementwise clip-scale + Adam update.  The f32 operation order of
+//             the reference (m*=b1; m+=(1-b1)g; v*=b2; v+=(1-b2)g*g;
+//             p -= lr*(m/bc1)/(sqrt(v/bc2)+eps)) is reproduced with
+//             round-to-nearest intrinsics (no FMA contraction), so given equal
+//             gradients the update is bit-identical to numpy.
+// HBM bytes: prepare 4 B/param, apply 28 B/param (+4 if clipped grads are
+// written back for the clip_global_norm API).
+#include "internal.cuh"
+
+namespace ul {
+namespace {
+
+constexpr int kPrepThreads = 256;
+
+__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl) {
+  __shared__ double scratch[32];
+  const int nb = gridDim.x;
+  for (int s = 0; s < st.nseg; ++s) {
+    const float* g = st.g[s];
+    const int64_t n = st.n[s];
+    double acc = 0.0;
+    int bad = 0;
+    const int64_t stride = (int64_t)nb * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float x = g[i];
+      acc += (double)x * (double)x;
+      bad |= !isfinite(x);
+    }
+    const double tot = block_sum(acc, scratch);
+    const int any_bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+      ctl->part[blockIdx.x][s] = tot;
+      ctl->part_bad[blockIdx.x][s] = any_bad;
+    }
+  }
+  if (!last_block_ticket(&ctl->ticket, nb)) return;
+  if (threadIdx.x != 0) return;
+  double joint = 0.0;
+  int earlier_bad = ctl->loss_bad;
+  const int was_diverged = ctl->diverged;
+  for (int s = 0; s < st.nseg; ++s) {
+    double sum = 0.0;
+    int bad = 0;
+    for (int b = 0; b < nb; ++b) {
+      sum += ctl->part[b][s];
+      bad |= ctl->part_bad[b][s];
+    }
+    ctl->sumsq[s] = sum;
+    ctl->seg_bad[s] = bad;
+    joint += sum;
+    earlier_bad |= bad;
+    const int upd = !was_diverged && !earlier_bad;
+    ctl->seg_update[s] = upd;
+    if (upd) ctl->t[s] += 1;
+  }
+  const double norm = sqrt(joint);
+  ctl->norm = norm;
+  // reference: factor applied only when max_norm > 0 and total > max_norm (NaN -> no clip)
+  ctl->factor = (ctl->max_norm > 0.0 && norm > ctl->max_norm) ? ctl->max_norm / (norm + 1e-12) : 1.0;
+  if (earlier_bad && !was_diverged) {
+    ctl->diverged = 1;
+    ctl->fail_step = ctl->steps;
+  }
+  ctl->loss_bad = 0;
+  ctl->steps += 1;
+}
+
+struct AdamScalars {
+  float b1, one_m_b1, b2, one_m_b2, bc1, bc2, lr, eps;
+};
+
+__global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
+                             int do_adam) {
+  const int s = blockIdx.y;
+  if (s >= st.nseg) return;
+  const int upd = ctl->seg_update[s];
+  // clip_global_norm scales even when a later Adam raises; Adam itself only on upd
+  const float f = (float)ctl->factor;
+  const bool scale = ctl->factor != 1.0;
+  float* __restrict__ g = st.g[s];
+  const int64_t n = st.n[s];
+  AdamScalars k;
+  if (do_adam) {
+    const double t = (double)ctl->t[s];
+    k.b1 = (float)ctl->beta1;
+    k.one_m_b1 = (float)(1.0 - ctl->beta1);
+    k.b2 = (float)ctl->beta2;
+    k.one_m_b2 = (float)(1.0 - ctl->beta2);
+    k.bc1 = (float)(1.0 - pow(ctl->beta1, t));
+    k.bc2 = (float)(1.0 - pow(ctl->beta2, t));
+    k.lr = (float)ctl->lr[s];
+    k.eps = (float)ctl->eps;
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float gi = g[i];
+    if (scale) gi = __fmul_rn(gi, f);
+    if (write_grads && scale) g[i] = gi;
+    if (!do_adam || !upd) continue;
+    float m = st.m[s][i], v = st.v[s][i], p = st.p[s][i];
+    m = __fadd_rn(__fmul_rn(m, k.b1), __fmul_rn(k.one_m_b1, gi));
+    v = __fadd_rn(__fmul_rn(v, k.b2), __fmul_rn(__fmul_rn(k.one_m_b2, gi), gi));
+    const float mh = __fdiv_rn(m, k.bc1);
+    const float vh = __fdiv_rn(v, k.bc2);
+    const float step = __fdiv_rn(__fmul_rn(k.lr, mh), __fadd_rn(__fsqrt_rn(vh), k.eps));
+    st.m[s][i] = m;
+    st.v[s][i] = v;
+    st.p[s][i] = __fsub_rn(p, step);
+  }
+}
+
+__global__ void polyak_kernel(float* __restrict__ tgt, const float* __restrict__ src, int64_t n,
+                              float keep, float tau) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    // reference order: t *= (1-tau); t += tau*o   (two f32 roundings each)
+    tgt[i] = __fadd_rn(__fmul_rn(tgt[i], keep), __fmul_rn(tau, src[i]));
+  }
+}
+
+int fill_table(SegTable& st, int nseg, float* const* params, float* const* grads,
+               float* const* m, float* const* v, const int64_t* sizes, bool need_state) {
+  UL_CHECK_ARG(nseg >= 1 && nseg <= UL_MAX_SEG, "adam: nseg %d outside [1, %d]", nseg,
+               UL_MAX_SEG);
+  st.nseg = nseg;
+  for (int s = 0; s < nseg; ++s) {
+    UL_CHECK_ARG(sizes[s] >= 0, "adam: negative segment size");
+    UL_CHECK_ARG(grads[s] != nullptr || sizes[s] == 0, "adam: null grad segment");
+    st.g[s] = grads[s];
+    st.n[s] = sizes[s];
+    st.p[s] = need_state ? params[s] : nullptr;
+    st.m[s] = need_state ? m[s] : nullptr;
+    st.v[s] = need_state ? v[s] : nullptr;
+    if (need_state)
+      UL_CHECK_ARG(sizes[s] == 0 || (params[s] && m[s] && v[s]), "adam: null state segment");
+  }
+  for (int s = nseg; s < UL_MAX_SEG; ++s) {
+    st.g[s] = st.p[s] = st.m[s] = st.v[s] = nullptr;
+    st.n[s] = 0;
+  }
+  return UL_OK;
+}
+
+int64_t max_n(const SegTable& st) {
+  int64_t mx = 1;
+  for (int s = 0; s < st.nseg; ++s) mx = st.n[s] > mx ? st.n[s] : mx;
+  return mx;
+}
+
+}  // namespace
+
+int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s) {
+  int64_t nmax = max_n(st);
+  int blocks = (int)ceil_div(nmax, kPrepThreads * 4);
+  blocks = blocks < 1 ? 1 : (blocks > UL_PREP_BLOCKS ? UL_PREP_BLOCKS : blocks);
+  prepare_kernel<<<blocks, kPrepThreads, 0, s>>>(st, ctl);
+  return check_launch("prepare_kernel");
+}
+
+int launch_apply(const SegTable& st, ul_opt_ctl* ctl, int write_grads, int do_adam,
+                 cudaStream_t s) {
+  int64_t nmax = max_n(st);
+  int bx = (int)ceil_div(nmax, 256 * 4);
+  bx = bx < 1 ? 1 : (bx > 4 * kNumSMs ? 4 * kNumSMs : bx);
+  apply_kernel<<<dim3(bx, st.nseg), 256, 0, s>>>(st, ctl, write_grads, do_adam);
+  return check_launch("apply_kernel");
+}
+
+}  // namespace ul
+
+extern "C" int ul_opt_ctl_init(ul_opt_ctl* host_ctl, int nseg, const double* lr, double beta1,
+                               double beta2, double eps, double max_norm) {
+  UL_CHECK_ARG(host_ctl != nullptr, "opt ctl: null");
+  UL_CHECK_ARG(nseg >= 1 && nseg <= UL_MAX_SEG, "opt ctl: bad nseg");
+  memset(host_ctl, 0, sizeof(ul_opt_ctl));
+  for (int s = 0; s < nseg; ++s) host_ctl->lr[s] = lr[s];
+  host_ctl->beta1 = beta1;
+  host_ctl->beta2 = beta2;
+  host_ctl->eps = eps;
+  host_ctl->max_norm = max_norm;
+  host_ctl->factor = 1.0;
+  host_ctl->fail_step = -1;
+  return UL_OK;
+}
+
+extern "C" int64_t ul_opt_ctl_bytes(void) { return (int64_t)sizeof(ul_opt_ctl); }
+
+// Joint norm over `nseg` gradient segments; optional clip-scale of the grads in
+// place (clip_global_norm semantics).  No Adam.  ctl->norm receives the pre-clip
+// norm; ctl->max_norm is the clip threshold.
+extern "C" int ul_clip_global_norm(float* const* grads, const int64_t* sizes, int nseg,
+                                   ul_opt_ctl* ctl, void* stream) {
+  ul::SegTable st;
+  UL_TRY(ul::fill_table(st, nseg, nullptr, grads, nullptr, nullptr, sizes, false));
+  cudaStream_t s = ul::as_stream(stream);
+  UL_TRY(ul::launch_prepare(st, ctl, s));
+  return ul::launch_apply(st, ctl, /*write_grads=*/1, /*do_adam=*/0, s);
+}
+
+// One Adam step over `nseg` (param, grad, m, v) segments sharing one clip
+// group: prepare (norm / finiteness / step counters) then apply.
+extern "C" int ul_adam_step(float* const* params, float* const* grads, float* const* m,
+                            float* const* v, const int64_t* sizes, int nseg, ul_opt_ctl* ctl,
+                            int write_clipped_grads, void* stream) {
+  ul::SegTable st;
+  UL_TRY(ul::fill_table(st, nseg, params, grads, m, v, sizes, true));
+  cudaStream_t s = ul::as_stream(stream);
+  UL_TRY(ul::launch_prepare(st, ctl, s));
+  return ul::launch_apply(st, ctl, write_clipped_grads, /*do_adam=*/1, s);
+}
+
+extern "C" int ul_polyak(float* target, const float* online, int64_t n, double tau,
+                         void* stream) {
+  UL_CHECK_ARG(n >= 0, "polyak: negative size");
+  if (n == 0) return UL_OK;
+  int blocks = (int)ul::ceil_div(n, 256 * 4);
+  blocks = blocks > 4 * ul::kNumSMs ? 4 * ul::kNumSMs : blocks;
+  ul::polyak_kernel<<<blocks, 256, 0, ul::as_stream(stream)>>>(target, online, n,
+                                                               (float)(1.0 - tau), (float)tau);
+  return ul::check_launch("polyak_kernel");
+}

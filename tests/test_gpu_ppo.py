@@ -1,0 +1,181 @@
+"""GPU parity of the PPO / APPO learner (plan = K4 + K7 + K9 + K8 + K13)."""
+
+import numpy as np
+import pytest
+
+from oracle import port as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2605_30313_b200 import algos as A  # noqa: E402
+from paper_2605_30313_b200 import tensornet as TN  # noqa: E402
+
+
+def rel_err(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+
+
+def _seg_kwargs(g, p):
+    keys = ["obs", "critic_obs", "actions", "behavior_log_prob", "rewards", "terminated",
+            "truncated", "values", "bootstrap_value", "truncation_values"]
+    return {k: g[p + k] for k in keys}
+
+
+def _ac(actor_dims, critic_dims, fa, fc):
+    a = TN.ModelParams.from_numpy(TN.Arch(actor_dims[0], actor_dims[1:-1], actor_dims[-1]), fa)
+    c = TN.ModelParams.from_numpy(TN.Arch(critic_dims[0], critic_dims[1:-1], critic_dims[-1]), fc)
+    return A.AcParams(a, c)
+
+
+def test_ppo_loss_and_grads_match_reference(golden):
+    g = golden("ppo")
+    seg = _seg_kwargs(g, "s_")
+    params = _ac((10, 32, 16, 4), (12, 32, 16, 1), g["s_actor"], g["s_critic"])
+    idx = g["s_idx"]
+    adv = g["s_adv"].reshape(-1)
+    advn = (adv - adv.mean()) / (adv.std() + 1e-8)
+    flat = lambda a: a.reshape(-1, *a.shape[2:])
+    terms, ga, gc = A.ppo_loss_and_grads(
+        params, flat(seg["obs"])[idx], flat(seg["critic_obs"])[idx], flat(seg["actions"])[idx],
+        seg["behavior_log_prob"].reshape(-1)[idx], advn[idx], g["s_ret"].reshape(-1)[idx],
+        seg["values"].reshape(-1)[idx], A.PpoConfig())
+    got = [terms[k] for k in ("policy_loss", "value_loss", "entropy", "total", "kl")]
+    assert rel_err(got, g["s_terms"]) < 1e-5
+    assert rel_err(ga.flat(), g["s_ga"]) < 1e-5
+    assert rel_err(gc.flat(), g["s_gc"]) < 1e-5
+
+
+def test_ppo_update_matches_reference(golden):
+    """Full update on the reference's own permutation stream: parameters and
+    stats within the fp32 full-update tolerance of SURVEY.md §8(c)."""
+    from oracle.port import philox_stream
+
+    g = golden("ppo")
+    seg = A.RolloutSegment(**_seg_kwargs(g, "u_"))
+    seg.advantages, seg.returns = A.gae(seg.rewards, seg.values, seg.terminated, seg.truncated,
+                                        seg.bootstrap_value, 0.99, 0.95,
+                                        truncation_values=seg.truncation_values)
+    params = _ac((6, 16, 16, 3), (7, 16, 16, 1), g["u_actor0"], g["u_critic0"])
+    cfg = A.PpoConfig(epochs=2, minibatches=4)
+    opt = A.AcOpt.for_params(params, cfg.lr)
+    st = A.ppo_update(seg, params, opt, cfg, philox_stream(1, "update"))
+    d_ref = g["u_actor1"] - g["u_actor0"]
+    d_gpu = params.actor.flat() - g["u_actor0"]
+    assert np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref) < 0.02
+    np.testing.assert_allclose(params.actor.flat(), g["u_actor1"], atol=2e-5)
+    np.testing.assert_allclose(params.critic.flat(), g["u_critic1"], atol=2e-5)
+    got = [st.policy_loss, st.value_loss, st.entropy, st.kl, st.lr, st.grad_norm]
+    assert rel_err(got, g["u_stats"]) < 1e-4
+    assert opt.actor.t == 8 and opt.critic.t == 8
+
+
+def test_ppo_update_divergence():
+    rng = np.random.default_rng(8)
+    t, b = 4, 3
+    params = A.AcParams(TN.init_params(TN.Arch(3, (4,), 2), 7), TN.init_params(TN.Arch(4, (4,), 1), 8))
+    seg = A.RolloutSegment(obs=rng.normal(size=(t, b, 3)).astype(np.float32),
+                           critic_obs=rng.normal(size=(t, b, 4)).astype(np.float32),
+                           actions=rng.normal(size=(t, b, 2)).astype(np.float32),
+                           behavior_log_prob=rng.normal(size=(t, b)), rewards=rng.normal(size=(t, b)),
+                           terminated=np.zeros((t, b), bool), truncated=np.zeros((t, b), bool),
+                           values=rng.normal(size=(t, b)), bootstrap_value=rng.normal(size=b))
+    opt = A.AcOpt.for_params(params, 1e-3)
+    with pytest.raises(ValueError, match="advantages"):
+        A.ppo_update(seg, params, opt, A.PpoConfig(), np.random.default_rng(0))
+    seg.advantages = np.full((t, b), np.nan)
+    seg.returns = np.zeros((t, b))
+    before = params.actor.flat().copy()
+    with pytest.raises(TN.DivergenceError):
+        A.ppo_update(seg, params, opt, A.PpoConfig(minibatches=2), np.random.default_rng(0))
+    np.testing.assert_array_equal(params.actor.flat(), before)
+    seg.advantages = np.zeros((t, b))
+    with pytest.raises(ValueError, match="divide"):
+        A.ppo_update(seg, params, opt, A.PpoConfig(minibatches=5), np.random.default_rng(0))
+
+
+def _synthetic(T, N, od, cd, ad, hid, seed=0):
+    """BASELINE.md synthetic recipe (values / blogp from the oracle nets)."""
+    rng = np.random.default_rng(seed)
+    actor = O.net_init((od, *hid, ad), 0)
+    critic = O.net_init((cd, *hid, 1), 1)
+    obs = rng.normal(size=(T, N, od)).astype(np.float32)
+    cobs = rng.normal(size=(T, N, cd)).astype(np.float32)
+    act = rng.normal(size=(T, N, ad)).astype(np.float32)
+    rew = 0.1 * rng.normal(size=(T, N))
+    term = rng.random((T, N)) < 0.01
+    trunc = (rng.random((T, N)) < 0.005) & ~term
+    boot = rng.normal(size=N)
+    tv = rng.normal(size=(T, N)) * trunc
+    mean, _ = O.mlp_forward(actor, obs.reshape(-1, od))
+    blogp = O.gauss_logp(mean, actor.log_std, act.reshape(-1, ad)).reshape(T, N).astype(np.float64)
+    vals = O.value_forward(critic, cobs.reshape(-1, cd))[0].reshape(T, N).astype(np.float64)
+    seg = dict(obs=obs, critic_obs=cobs, actions=act, behavior_log_prob=blogp, rewards=rew,
+               terminated=term, truncated=trunc, values=vals, bootstrap_value=boot,
+               truncation_values=tv)
+    return seg, actor, critic
+
+
+def test_ppo_single_step_cfg2_shape_vs_oracle_f64():
+    """cfg2 shapes (obs 235, 512-256-128, mb 24576): one minibatch's grads vs
+    the f64 oracle within 1e-5 x max(1, |ref|)."""
+    T, N = 24, 1024  # 24,576 rows = one cfg2 minibatch
+    seg, actor, critic = _synthetic(T, N, 235, 235, 12, (512, 256, 128), seed=3)
+    adv, ret = O.gae(seg["rewards"], seg["values"], seg["terminated"], seg["truncated"],
+                     seg["bootstrap_value"], 0.99, 0.95, seg["truncation_values"])
+    advn = O.normalize_adv(adv.reshape(-1))
+    to64 = lambda n: O.Net(n.dims, [[w.astype(np.float64), b.astype(np.float64)] for w, b in n.layers],
+                           n.log_std.astype(np.float64))
+    f = lambda a: a.reshape(-1, *a.shape[2:])
+    args = (f(seg["obs"]).astype(np.float64), f(seg["critic_obs"]).astype(np.float64),
+            f(seg["actions"]).astype(np.float64), seg["behavior_log_prob"].reshape(-1), advn,
+            ret.reshape(-1), seg["values"].reshape(-1))
+    terms, ga, gc = O.ppo_loss_grads(to64(actor), to64(critic), *args, O.PpoCfg())
+    params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(235, (512, 256, 128), 12), actor.flat()),
+                        TN.ModelParams.from_numpy(TN.Arch(235, (512, 256, 128), 1), critic.flat()))
+    gterms, gga, ggc = A.ppo_loss_and_grads(params, f(seg["obs"]), f(seg["critic_obs"]),
+                                            f(seg["actions"]), seg["behavior_log_prob"].reshape(-1),
+                                            advn, ret.reshape(-1), seg["values"].reshape(-1),
+                                            A.PpoConfig())
+    for k in ("policy_loss", "value_loss", "entropy", "kl"):
+        assert abs(gterms[k] - terms[k]) <= 1e-5 * max(1.0, abs(terms[k])), k
+    assert rel_err(gga.flat(), ga.flat()) < 1e-5
+    assert rel_err(ggc.flat(), gc.flat()) < 1e-5
+
+
+def test_ppo_full_update_cfg1_vs_oracle():
+    """cfg1 (1024 x 24, obs 48, 256-128-128, 5x4) full update: norm-based
+    parameter-delta parity against the f32 oracle with the SAME permutations."""
+    from oracle.port import philox_stream
+
+    T, N = 24, 1024
+    segd, actor, critic = _synthetic(T, N, 48, 48, 12, (256, 128, 128), seed=5)
+    adv, ret = O.gae(segd["rewards"], segd["values"], segd["terminated"], segd["truncated"],
+                     segd["bootstrap_value"], 0.99, 0.95, segd["truncation_values"])
+    cfg = O.PpoCfg()
+    a_ref, c_ref = actor.clone(), critic.clone()
+    oa, oc = O.Opt.for_net(a_ref, cfg.lr), O.Opt.for_net(c_ref, cfg.lr)
+    ref_seg = dict(segd, advantages=adv, returns=ret)
+    ost = O.ppo_update(ref_seg, a_ref, c_ref, oa, oc, cfg, philox_stream(1, "update"))
+
+    params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(48, (256, 128, 128), 12), actor.flat()),
+                        TN.ModelParams.from_numpy(TN.Arch(48, (256, 128, 128), 1), critic.flat()))
+    seg = A.RolloutSegment(**segd)
+    seg.advantages, seg.returns = A.gae(seg.rewards, seg.values, seg.terminated, seg.truncated,
+                                        seg.bootstrap_value, 0.99, 0.95,
+                                        truncation_values=seg.truncation_values)
+    opt = A.AcOpt.for_params(params, 1e-3)
+    st = A.ppo_update(seg, params, opt, A.PpoConfig(), philox_stream(1, "update"))
+    for ref_net, got, init in ((a_ref, params.actor, actor), (c_ref, params.critic, critic)):
+        d_ref = ref_net.flat() - init.flat()
+        d_gpu = got.flat() - init.flat()
+        rel = np.linalg.norm(d_gpu - d_ref) / np.linalg.norm(d_ref)
+        cos = float(d_gpu @ d_ref / (np.linalg.norm(d_gpu) * np.linalg.norm(d_ref)))
+        assert rel <= 0.10 and cos >= 0.995, (rel, cos)
+    assert abs(st.policy_loss - ost["policy_loss"]) < 1e-3
+    assert abs(st.value_loss - ost["value_loss"]) <= 1e-3 * max(1, abs(ost["value_loss"]))
+    assert abs(st.entropy - ost["entropy"]) < 1e-4
