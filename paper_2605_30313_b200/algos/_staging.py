@@ -41,6 +41,8 @@ class DeviceSegment:
         self.tv = torch.zeros(rows, **f32)
         self.adv = torch.zeros(rows, **f32)
         self.ret = torch.zeros(rows, **f32)
+        self.vnow = torch.zeros(rows, **f32)   # APPO: values under the current critic
+        self.tlogp = torch.zeros(rows, **f32)  # APPO: target log-prob
         self.term = torch.zeros(rows, dtype=torch.uint8, device=dev)
         self.trunc = torch.zeros(rows, dtype=torch.uint8, device=dev)
         self.boot = torch.zeros(N, **f32)

@@ -24,6 +24,7 @@ struct GatherTable {
   int64_t dst_stride[kMaxDesc];  // bytes
   int64_t units[kMaxDesc];       // units per row
   int unit[kMaxDesc];            // unit bytes (16, 8 or 4)
+  int64_t ones[kMaxDesc];        // byte offset of a float set to 1.0 in each row, -1 none
   int ndesc;
 };
 
@@ -40,7 +41,8 @@ template <int U>
 __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __restrict__ dst,
                                           int64_t sst, int64_t dstr, int64_t upr,
                                           const int64_t* __restrict__ idx, int64_t n,
-                                          int64_t modulo, int64_t lo, int64_t hi, int* err) {
+                                          int64_t modulo, int64_t lo, int64_t hi, int* err,
+                                          int64_t ones) {
   using T = typename Vec<U>::T;
   const int64_t total = n * upr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -52,7 +54,11 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
       continue;
     }
     if (modulo > 0) s %= modulo;
-    const T v = __ldg(reinterpret_cast<const T*>(src + s * sst) + u);
+    T v = __ldg(reinterpret_cast<const T*>(src + s * sst) + u);
+    if (ones >= 0 && ones / U == u) {
+      float* f = reinterpret_cast<float*>(&v);
+      f[(ones % U) / 4] = 1.f;
+    }
     reinterpret_cast<T*>(dst + r * dstr)[u] = v;
   }
 }
@@ -64,15 +70,15 @@ __global__ void gather_kernel(GatherTable t, const int64_t* __restrict__ idx, in
   switch (t.unit[d]) {
     case 16:
       copy_rows<16>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                    modulo, lo, hi, err);
+                    modulo, lo, hi, err, t.ones[d]);
       break;
     case 8:
       copy_rows<8>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                   modulo, lo, hi, err);
+                   modulo, lo, hi, err, t.ones[d]);
       break;
     default:
       copy_rows<4>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                   modulo, lo, hi, err);
+                   modulo, lo, hi, err, t.ones[d]);
   }
 }
 
@@ -125,7 +131,8 @@ __global__ void feistel_perm_kernel(int64_t n, int half_bits, uint64_t seed, int
 // skipped and raise *err (device flag).  idx == NULL gathers rows 0..n-1.
 extern "C" int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
                               const int64_t* src_stride, const int64_t* dst_stride,
-                              const int64_t* row_bytes, const int64_t* idx, int64_t n,
+                              const int64_t* row_bytes, const int64_t* ones_byte,
+                              const int64_t* idx, int64_t n,
                               int64_t modulo, int64_t lo, int64_t hi, int* err, void* stream) {
   UL_CHECK_ARG(ndesc >= 1 && ndesc <= ul::kMaxDesc, "gather: ndesc %d outside [1,%d]", ndesc,
                ul::kMaxDesc);
@@ -144,6 +151,8 @@ extern "C" int ul_gather_rows(int ndesc, const void* const* src, void* const* ds
     t.dst_stride[d] = dst_stride[d];
     t.unit[d] = u;
     t.units[d] = row_bytes[d] / u;
+    t.ones[d] = ones_byte ? ones_byte[d] : -1;
+    UL_CHECK_ARG(t.ones[d] < row_bytes[d], "gather: ones column outside the row");
     max_units = t.units[d] > max_units ? t.units[d] : max_units;
   }
   int64_t blocks = ul::ceil_div(n * max_units, 256);

@@ -31,6 +31,7 @@ struct KArgs {
   int64_t ldaux;
   int64_t k_per_split;
   float* rowsum;
+  int ones_col;
 };
 
 template <bool KMAJOR>
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(kThreads) sgemm_kernel(KArgs p) {
     const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
     if (m >= p.M) continue;
     if (do_rowsum && tx == 0) p.rowsum[(int64_t)blockIdx.z * p.M + m] = rs[i];
+    if (!SPLIT && p.ones_col >= 0 && blockIdx.y == 0 && tx == 0) C[m * p.ldc + p.ones_col] = 1.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
@@ -180,7 +182,8 @@ int gemm_num_splits(int64_t K, int splits) {
 
 int gemm_f32(const GemmDesc& d, cudaStream_t s) {
   if (d.M == 0 || d.N == 0) return UL_OK;
-  KArgs a{d.M, d.N, d.K, d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.bias, d.aux, d.ldaux, 0, d.rowsum};
+  KArgs a{d.M, d.N, d.K, d.A, d.lda, d.B, d.ldb, d.C, d.ldc, d.bias, d.aux, d.ldaux, 0, d.rowsum,
+          d.ones_col};
   a.k_per_split = k_per_split(d.K, d.splits);
   const int zs = gemm_num_splits(d.K, d.splits);
   dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)zs);
@@ -227,189 +230,7 @@ int reduce_splits(const float* ws, int splits, int64_t len, float* out, int64_t 
   return check_launch("reduce_splits_kernel");
 }
 
-// ------------------------------------------------------------------- MLP
-int make_view(const ul_net_desc* d, NetView* v) {
-  UL_CHECK_ARG(d != nullptr, "net: null descriptor");
-  UL_CHECK_ARG(d->n_layers >= 1 && d->n_layers <= UL_MAX_LAYERS, "net: n_layers %d outside [1,%d]",
-               d->n_layers, UL_MAX_LAYERS);
-  v->n_layers = d->n_layers;
-  int64_t off = 0;
-  for (int i = 0; i <= d->n_layers; ++i) {
-    UL_CHECK_ARG(d->dims[i] > 0, "all layer dims must be positive");
-    v->dims[i] = d->dims[i];
-  }
-  for (int i = 0; i < d->n_layers; ++i) {
-    v->w_off[i] = off;
-    off += (int64_t)v->dims[i + 1] * v->dims[i];
-    v->b_off[i] = off;
-    off += v->dims[i + 1];
-  }
-  v->logstd_off = off;
-  v->total = off + v->dims[d->n_layers];
-  return UL_OK;
-}
-
-int64_t act_floats(const NetView& v, int64_t M) {
-  int64_t s = 0;
-  for (int i = 1; i < v.n_layers; ++i) s += (int64_t)v.dims[i] * M;
-  return s;
-}
-
-static int64_t max_hidden(const NetView& v) {
-  int64_t h = 1;
-  for (int i = 1; i <= v.n_layers; ++i) h = v.dims[i] > h ? v.dims[i] : h;
-  return h;
-}
-
-// dW split count: enough CTAs for ~2 waves, at least 512 batch rows per split
-static int dw_splits(int64_t out, int64_t in, int64_t M) {
-  const int64_t tiles = ceil_div(out, BM) * ceil_div(in, BN);
-  int64_t sp = ceil_div(2 * kNumSMs, tiles);
-  const int64_t cap = ceil_div(M, 512);
-  sp = sp < cap ? sp : cap;
-  sp = sp < 1 ? 1 : sp;
-  return (int)(sp > 64 ? 64 : sp);
-}
-
-int64_t bwd_work_floats(const NetView& v, int64_t M) {
-  int64_t ws = 0;
-  for (int i = 0; i < v.n_layers; ++i) {
-    const int64_t out = v.dims[i + 1], in = v.dims[i];
-    const int sp = dw_splits(out, in, M);
-    const int64_t need = (int64_t)sp * (out * in + out);
-    ws = need > ws ? need : ws;
-  }
-  return 2 * M * max_hidden(v) + ws;
-}
-
-static const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i) {
-  // hidden activation after layer i (i < n_layers-1)
-  int64_t off = 0;
-  for (int j = 1; j <= i; ++j) off += (int64_t)v.dims[j] * M;
-  return acts + off;
-}
-
-int mlp_forward(const NetView& v, const float* params, const float* x, int64_t ldx, int64_t M,
-                float* acts, float* out, int64_t ld_out, cudaStream_t s) {
-  const float* h = x;
-  int64_t ldh = ldx;
-  for (int i = 0; i < v.n_layers; ++i) {
-    const bool last = i == v.n_layers - 1;
-    float* dst = last ? out : const_cast<float*>(act_ptr(v, acts, M, i));
-    const int64_t lddst = last ? ld_out : v.dims[i + 1];
-    GemmDesc g{};
-    g.M = M; g.N = v.dims[i + 1]; g.K = v.dims[i];
-    g.A = h; g.lda = ldh; g.B = params + v.w_off[i]; g.ldb = v.dims[i];
-    g.C = dst; g.ldc = lddst; g.bias = params + v.b_off[i];
-    g.a_kmajor = true; g.b_kmajor = true;
-    g.epi = last ? kEpiBias : kEpiBiasElu;
-    g.splits = 1;
-    UL_TRY(gemm_f32(g, s));
-    h = dst;
-    ldh = lddst;
-  }
-  return UL_OK;
-}
-
-int mlp_backward(const NetView& v, const float* params, const float* x, int64_t ldx, int64_t M,
-                 const float* acts, const float* dout, int64_t ld_dout, float* grads, float* dx,
-                 int64_t lddx, int dx_col0, int dx_ncols, bool want_dw, bool zero_logstd,
-                 float* work, cudaStream_t s) {
-  const int64_t H = max_hidden(v);
-  float* dh_buf[2] = {work, work + M * H};
-  float* ws = work + 2 * M * H;
-  const float* dh = dout;
-  int64_t lddh = ld_dout;
-  int ping = 0;
-  if (want_dw && zero_logstd && grads) UL_CUDA(cudaMemsetAsync(grads + v.logstd_off, 0,
-                                                sizeof(float) * v.dims[v.n_layers], s));
-  for (int i = v.n_layers - 1; i >= 0; --i) {
-    const int64_t out = v.dims[i + 1], in = v.dims[i];
-    const float* inp = i == 0 ? x : act_ptr(v, acts, M, i - 1);
-    const int64_t ldin = i == 0 ? ldx : in;
-    if (want_dw) {
-      // dW[out, in] = dh^T inp ; db = colsum(dh) (row-sum of dh^T)
-      const int sp = gemm_num_splits(M, dw_splits(out, in, M));
-      GemmDesc g{};
-      g.M = out; g.N = in; g.K = M;
-      g.A = dh; g.lda = lddh; g.B = inp; g.ldb = ldin;
-      g.a_kmajor = false; g.b_kmajor = false; g.epi = kEpiStore;
-      g.splits = sp;
-      g.C = ws;
-      g.rowsum = ws + (int64_t)sp * out * in;
-      g.ldc = in;
-      UL_TRY(gemm_f32(g, s));
-      UL_TRY(reduce_splits(ws, sp, out * in, grads + v.w_off[i], in, in, s));
-      UL_TRY(reduce_splits(g.rowsum, sp, out, grads + v.b_off[i], out, out, s));
-    }
-    if (i == 0) {
-      if (dx == nullptr) break;
-      // dX[:, cols] = dh W[:, cols]
-      GemmDesc g{};
-      g.M = M; g.N = dx_ncols; g.K = out;
-      g.A = dh; g.lda = lddh; g.B = params + v.w_off[0] + dx_col0; g.ldb = in;
-      g.C = dx; g.ldc = lddx;
-      g.a_kmajor = true; g.b_kmajor = false; g.epi = kEpiStore; g.splits = 1;
-      UL_TRY(gemm_f32(g, s));
-      break;
-    }
-    // dh_prev = (dh W) * elu'(h_{i-1})
-    float* nxt = dh_buf[ping];
-    ping ^= 1;
-    GemmDesc g{};
-    g.M = M; g.N = in; g.K = out;
-    g.A = dh; g.lda = lddh; g.B = params + v.w_off[i]; g.ldb = in;
-    g.C = nxt; g.ldc = in;
-    g.aux = act_ptr(v, acts, M, i - 1); g.ldaux = in;
-    g.a_kmajor = true; g.b_kmajor = false; g.epi = kEpiEluGrad; g.splits = 1;
-    UL_TRY(gemm_f32(g, s));
-    dh = nxt;
-    lddh = in;
-  }
-  return UL_OK;
-}
-
 }  // namespace ul
-
-// -------------------------------------------------------------- C ABI
-extern "C" int64_t ul_net_param_count(const ul_net_desc* net) {
-  ul::NetView v;
-  if (ul::make_view(net, &v) != UL_OK) return -1;
-  return v.total;
-}
-
-extern "C" int64_t ul_mlp_act_floats(const ul_net_desc* net, int64_t M) {
-  ul::NetView v;
-  if (ul::make_view(net, &v) != UL_OK) return -1;
-  return ul::act_floats(v, M);
-}
-
-extern "C" int64_t ul_mlp_bwd_work_floats(const ul_net_desc* net, int64_t M) {
-  ul::NetView v;
-  if (ul::make_view(net, &v) != UL_OK) return -1;
-  return ul::bwd_work_floats(v, M);
-}
-
-extern "C" int ul_mlp_forward(const ul_net_desc* net, const float* params, const float* x,
-                              int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
-                              void* stream) {
-  ul::NetView v;
-  UL_TRY(ul::make_view(net, &v));
-  UL_CHECK_ARG(M >= 0, "forward: negative batch");
-  UL_CHECK_ARG(ldx >= v.dims[0], "forward: ldx %lld < input_dim %d", (long long)ldx, v.dims[0]);
-  return ul::mlp_forward(v, params, x, ldx, M, acts, out, ld_out, ul::as_stream(stream));
-}
-
-extern "C" int ul_mlp_backward(const ul_net_desc* net, const float* params, const float* x,
-                               int64_t ldx, int64_t M, const float* acts, const float* dout,
-                               int64_t ld_dout, float* grads, float* dx, int64_t lddx,
-                               float* work, void* stream) {
-  ul::NetView v;
-  UL_TRY(ul::make_view(net, &v));
-  UL_CHECK_ARG(M >= 0, "backward: negative batch");
-  return ul::mlp_backward(v, params, x, ldx, M, acts, dout, ld_dout, grads, dx, lddx, 0,
-                          v.dims[0], true, true, work, ul::as_stream(stream));
-}
 
 extern "C" int ul_gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A,
                            int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,

@@ -1,0 +1,386 @@
+// K7/K8 tensor-core path: tcgen05 (5th-gen tensor core) + TMEM + TMA GEMM for sm_100a.
+//
+// C[M,N] = A(M,K) B(K,N) with kind::tf32 MMAs reading the fp32 HBM buffers
+// directly (no conversion pass): TMA streams 128-byte-swizzled [rows x 32]
+// fp32 tiles into a STAGES-deep shared-memory ring, one elected thread issues
+// tcgen05.mma (UMMA M=128, N=BN, K=8) into a TMEM accumulator, and four
+// epilogue warps drain TMEM with tcgen05.ld and apply the fused MLP epilogue
+// (bias / ELU / ELU-gradient / split-K partial store).  Operands may be
+// K-major or MN-major (the MLP's dX and dW GEMMs read W and the activations
+// transposed; UMMA's MN-major smem descriptors absorb that, nothing is
+// transposed in HBM).
+//   warp 0      : TMA producer            (one elected lane)
+//   warp 1      : TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  : epilogue (TMEM lane quarter = warp % 4)
+#include <cuda.h>
+
+#include "internal.cuh"
+
+namespace ul {
+namespace tc {
+
+constexpr int BM = 128, BK = 32;  // BK fp32 = 128 B = one swizzle row
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm100 version bit.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcArgs {
+  int M, N, K;
+  int k_per_split;  // multiple of BK
+  float* C;
+  int64_t ldc;
+  const float* bias;
+  const float* aux;
+  int64_t ldaux;
+  int64_t split_stride;  // elements between split partial tiles
+  int ones_col;          // >= 0: also write C[m, ones_col] = 1 (dW bias trick)
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kABytes = BM * BK * 4;  // 16 KB
+  static constexpr int kBBytes = BN * BK * 4;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <bool A_MN, bool B_MN, int EPI, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   TcArgs p) {
+  using S = Smem<BN>;
+  constexpr int kStages = S::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* done = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb = blockIdx.z * p.k_per_split;
+  const int ke = min(p.K, kb + p.k_per_split);
+  const int ktiles = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % kStages;
+        mbar_wait(&empty[s], ((kt / kStages) & 1) ^ 1);
+        uint8_t* sa = smem + s * S::kStageBytes;
+        uint8_t* sb = sa + S::kABytes;
+        mbar_expect_tx(&full[s], S::kStageBytes);
+        const int k0 = kb + kt * BK;
+        if (A_MN) {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_2d(sa + c * 4096, &tmA, &full[s], m0 + 32 * c, k0);
+        } else {
+          tma_load_2d(sa, &tmA, &full[s], k0, m0);
+        }
+        if (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tma_load_2d(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0);
+        } else {
+          tma_load_2d(sb, &tmB, &full[s], k0, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    // instruction descriptor: f32 accum, tf32 A/B, majors, N>>3, M>>4
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                           ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % kStages;
+        mbar_wait(&full[s], (kt / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a_base = su32(smem + s * S::kStageBytes);
+        const uint32_t b_base = a_base + S::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t da = A_MN ? smem_desc(a_base + kk * 1024, 4096, 1024)
+                                   : smem_desc(a_base + kk * 32, 16, 1024);
+          const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 1024)
+                                   : smem_desc(b_base + kk * 32, 16, 1024);
+          mma_tf32(tmem, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+      }
+      mma_commit(done);  // accumulator complete
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int m = m0 + row;
+    if (ktiles > 0) mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    float* C = p.C + (int64_t)blockIdx.z * p.split_stride;
+    const bool vec = (p.ldc % 4 == 0);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      if (ktiles > 0) {
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      if (m >= p.M || n0 + c0 >= p.N) continue;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = n0 + c0 + i;
+        if (n < p.N) {
+          if (EPI == kEpiBias || EPI == kEpiBiasElu) v[i] += __ldg(p.bias + n);
+          if (EPI == kEpiBiasElu) v[i] = elu_f(v[i]);
+          if (EPI == kEpiEluGrad) v[i] *= elu_grad_from_act(__ldg(p.aux + (int64_t)m * p.ldaux + n));
+        }
+      }
+      float* dst = C + (int64_t)m * p.ldc + n0 + c0;
+      if (vec && n0 + c0 + 16 <= p.N) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (n0 + c0 + i < p.N) dst[i] = v[i];
+      }
+    }
+    if (p.ones_col >= 0 && blockIdx.y == 0 && m < p.M) C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(BN < 32 ? 32 : BN));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner (contiguous) extent, outer extent, row pitch
+// (elements), box {32, box_outer}, 128-byte swizzle, OOB -> zero.
+int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t ld,
+             int box_outer) {
+  EncodeFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return UL_ERR_CUDA;
+  }
+  if (((uintptr_t)base & 15) || ((ld * 4) & 15)) {
+    set_error("tensor map: base/pitch not 16-byte aligned");
+    return UL_ERR_VALUE;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return UL_ERR_CUDA;
+  }
+  return UL_OK;
+}
+
+template <bool A_MN, bool B_MN, int EPI, int BN>
+int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_stride, int ones_col,
+           cudaStream_t s) {
+  CUtensorMap ma, mb;
+  // A(m,k): K-major -> rows=M, inner=K ; MN-major -> rows=K, inner=M
+  if (A_MN) UL_TRY(make_map(&ma, d.A, d.M, d.K, d.lda, 32));
+  else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM));
+  if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32));
+  else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN));
+  TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, C, d.ldc, d.bias, d.aux, d.ldaux, split_stride,
+           ones_col};
+  auto kern = tc_gemm_kernel<A_MN, B_MN, EPI, BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Smem<BN>::kBytes));
+    attr_set = true;
+  }
+  dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)splits);
+  kern<<<grid, kThreads, Smem<BN>::kBytes, s>>>(ma, mb, a);
+  return check_launch("tc_gemm_kernel");
+}
+
+}  // namespace tc
+
+bool tc_eligible(const GemmDesc& d) {
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  return d.M >= 128 && d.N >= 32 && d.K >= 32 && d.M < (1ll << 31) && d.N < (1ll << 31) &&
+         d.K < (1ll << 31) && al(d.A) && al(d.B) && (d.lda % 4 == 0) && (d.ldb % 4 == 0) &&
+         !(d.a_kmajor == false && d.b_kmajor == true);
+}
+
+int tc_num_splits(int64_t K, int splits) {
+  splits = splits < 1 ? 1 : splits;
+  const int64_t kps = ceil_div(ceil_div(K, splits), tc::BK) * tc::BK;
+  return (int)ceil_div(K > 0 ? K : 1, kps);
+}
+
+// Same contract as gemm_f32 (split partials of ld N at C + z*M*N when
+// splits > 1); `ones_col` >= 0 additionally writes 1.0 into that column.
+int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
+  if (d.M == 0 || d.N == 0) return UL_OK;
+  if (ones_col < 0) ones_col = d.ones_col;
+  const int splits = d.splits < 1 ? 1 : d.splits;
+  const int kps = (int)(ceil_div(ceil_div(d.K, splits), tc::BK) * tc::BK);
+  const int zs = (int)ceil_div(d.K > 0 ? d.K : 1, kps);
+  const int64_t sstride = zs > 1 ? d.M * d.N : 0;
+  const int bn = d.N > 128 ? 256 : (d.N > 64 ? 128 : 64);
+  const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
+#define UL_TC_CASE(AMN, BMN, EPI)                                                             \
+  if (amn == AMN && bmn == BMN && d.epi == EPI) {                                             \
+    if (bn == 256) return tc::launch<AMN, BMN, EPI, 256>(d, zs, kps, d.C, sstride, ones_col, s); \
+    if (bn == 128) return tc::launch<AMN, BMN, EPI, 128>(d, zs, kps, d.C, sstride, ones_col, s); \
+    return tc::launch<AMN, BMN, EPI, 64>(d, zs, kps, d.C, sstride, ones_col, s);              \
+  }
+  UL_TC_CASE(false, false, kEpiBias)
+  UL_TC_CASE(false, false, kEpiBiasElu)
+  UL_TC_CASE(false, false, kEpiStore)
+  UL_TC_CASE(false, true, kEpiEluGrad)
+  UL_TC_CASE(false, true, kEpiStore)
+  UL_TC_CASE(true, true, kEpiStore)
+#undef UL_TC_CASE
+  set_error("gemm_tc: unsupported layout/epilogue combination");
+  return UL_ERR_VALUE;
+}
+
+}  // namespace ul
+
+// Test hook: one tcgen05 GEMM, same layout/epilogue codes as ul_gemm_f32.
+extern "C" int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A,
+                          int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                          const float* bias, const float* aux, int64_t ldaux, int splits,
+                          void* stream) {
+  ul::GemmDesc g{};
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
+  g.bias = bias; g.aux = aux; g.ldaux = ldaux;
+  g.a_kmajor = layout & 1; g.b_kmajor = (layout >> 1) & 1; g.epi = epi; g.splits = splits;
+  UL_CHECK_ARG(ul::tc_eligible(g), "gemm_tc: shape/alignment not eligible for tcgen05");
+  return ul::gemm_tc(g, -1, ul::as_stream(stream));
+}

@@ -47,6 +47,8 @@ struct GemmDesc {
   // optional: per-row sums of A over K (db of a dW GEMM), written per split
   // into rowsum[z*M + m]
   float* rowsum;
+  // >= 0: the epilogue also writes C[m, ones_col] = 1 (activation ones column)
+  int ones_col = -1;
 };
 int gemm_f32(const GemmDesc& d, cudaStream_t s);
 // number of K splits gemm_f32 actually launches for a requested split count
@@ -60,17 +62,25 @@ struct NetView {
   int n_layers;
   int dims[UL_MAX_LAYERS + 1];
   int64_t w_off[UL_MAX_LAYERS], b_off[UL_MAX_LAYERS], logstd_off, total;
+  int64_t wp_off[UL_MAX_LAYERS], wp_total;  // staged (16 B-row) weight layout
 };
 int make_view(const ul_net_desc* d, NetView* v);
+int64_t act_ld(int d);  // hidden activation row stride: round_up(d + 1, 4)
 int64_t act_floats(const NetView& v, int64_t M);
+const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i);
 int64_t bwd_work_floats(const NetView& v, int64_t M);
-int mlp_forward(const NetView& v, const float* params, const float* x, int64_t ldx, int64_t M,
-                float* acts, float* out, int64_t ld_out, cudaStream_t s);
+int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t s);
+// backend 0: fp32 SIMT; 1: tcgen05 tf32 (wp = staged weights, may be null -> SIMT)
+int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
+                const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
+                cudaStream_t s);
 // dx_cols: compute dX only for input columns [dx_col0, dx_col0 + dx_ncols) (SAC dQ/da);
-// want_dw = false skips dW/db (pure input-gradient pass).
-int mlp_backward(const NetView& v, const float* params, const float* x, int64_t ldx, int64_t M,
-                 const float* acts, const float* dout, int64_t ld_dout, float* grads,
-                 float* dx, int64_t lddx, int dx_col0, int dx_ncols, bool want_dw,
-                 bool zero_logstd, float* work, cudaStream_t s);
+// want_dw = false skips dW/db (pure input-gradient pass).  x_has_ones: column
+// dims[0] of x holds 1.0 (lets the tensor-core dW of layer 0 produce db).
+int mlp_backward(const NetView& v, const float* params, const float* wp, int backend,
+                 const float* x, int64_t ldx, bool x_has_ones, int64_t M, const float* acts,
+                 const float* dout, int64_t ld_dout, float* grads, float* dx, int64_t lddx,
+                 int dx_col0, int dx_ncols, bool want_dw, bool zero_logstd, float* work,
+                 cudaStream_t s);
 
 }  // namespace ul

@@ -30,6 +30,7 @@ struct PpoPlan {
   float *mb_obs = nullptr, *mb_cobs = nullptr, *mb_act = nullptr, *mb_scal = nullptr;
   float *acts_a = nullptr, *acts_c = nullptr, *out_a = nullptr, *out_c = nullptr;
   float *dmean = nullptr, *dv = nullptr, *work = nullptr, *red = nullptr, *red_own = nullptr;
+  float *wst_a = nullptr, *wst_c = nullptr;  // staged (16 B-row) weights, tensor-core path
   double *head_part = nullptr, *adv_stats = nullptr, *adv_part = nullptr;
   unsigned int* tickets = nullptr;  // [0] head, [1] adv stats
   ul_opt_ctl* ctl_d = nullptr;
@@ -92,6 +93,8 @@ int alloc_plan(PpoPlan* p) {
   const size_t o_tk = carve(sizeof(unsigned int) * 8);
   const size_t o_ctl = carve(sizeof(ul_opt_ctl));
   const size_t o_st = carve(sizeof(ul_ppo_stats));
+  const size_t o_wa = carve(sizeof(float) * p->va.wp_total);
+  const size_t o_wc = carve(sizeof(float) * p->vc.wp_total);
   UL_CUDA(cudaMalloc(&p->arena, off));
   UL_CUDA(cudaMemset(p->arena, 0, off));
   char* a = p->arena;
@@ -114,6 +117,8 @@ int alloc_plan(PpoPlan* p) {
   p->tickets = (unsigned int*)(a + o_tk);
   p->ctl_d = (ul_opt_ctl*)(a + o_ctl);
   p->st_d = (ul_ppo_stats*)(a + o_st);
+  p->wst_a = (float*)(a + o_wa);
+  p->wst_c = (float*)(a + o_wc);
   UL_CUDA(cudaHostAlloc(&p->ctl_h, sizeof(ul_opt_ctl), cudaHostAllocPortable));
   UL_CUDA(cudaHostAlloc(&p->st_h, sizeof(ul_ppo_stats), cudaHostAllocPortable));
   UL_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
@@ -160,18 +165,30 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   const int64_t* idx = p->d.local_shards
                            ? b.perm + (int64_t)e * p->rows + (int64_t)k * ml
                            : b.perm + (int64_t)e * p->rows + (int64_t)k * p->mb + p->d.rank * ml;
-  // K4: one gather launch for the 7 per-row arrays
+  const bool tc = p->d.gemm_backend == 1;
+  if (tc) {  // weights changed at the previous Adam step: restage 16 B-row copies
+    UL_TRY(stage_weights(p->va, b.actor_params, p->wst_a, s));
+    UL_TRY(stage_weights(p->vc, b.critic_params, p->wst_c, s));
+  }
+  // K4: one gather launch for the 7 per-row arrays; the obs / critic-obs
+  // pad column is set to 1.0 (the tensor-core dW's bias column)
   const void* src[7] = {b.obs, b.cobs, b.act, b.blogp, b.adv, b.ret, b.oldv};
   void* dst[7] = {p->mb_obs, p->mb_cobs, p->mb_act, p->mb_scal, p->mb_scal + ml,
                   p->mb_scal + 2 * ml, p->mb_scal + 3 * ml};
   const int64_t sst[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->d.ld_act, 4, 4, 4, 4};
   const int64_t dstr[7] = {4 * p->ld_mo, 4 * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
   const int64_t rb[7] = {4 * p->ld_mo, 4 * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
-  UL_TRY(ul_gather_rows(7, src, dst, sst, dstr, rb, idx, ml, 0, 0, p->rows, nullptr, s));
+  const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
+  const int64_t ones[7] = {p->ld_mo > od ? 4 * od : -1, p->ld_mc > cd ? 4 * cd : -1, -1, -1, -1,
+                           -1, -1};
+  UL_TRY(ul_gather_rows(7, src, dst, sst, dstr, rb, ones, idx, ml, 0, 0, p->rows, nullptr, s));
   mark(p, 1, s);
   // K7 forwards
-  UL_TRY(mlp_forward(p->va, b.actor_params, p->mb_obs, p->ld_mo, ml, p->acts_a, p->out_a, p->A, s));
-  UL_TRY(mlp_forward(p->vc, b.critic_params, p->mb_cobs, p->ld_mc, ml, p->acts_c, p->out_c, 1, s));
+  const int be = p->d.gemm_backend;
+  UL_TRY(mlp_forward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, ml, p->acts_a,
+                     p->out_a, p->A, s));
+  UL_TRY(mlp_forward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, ml, p->acts_c,
+                     p->out_c, 1, s));
   mark(p, 0, s);
   // K9 head
   PpoHeadArgs h{};
@@ -204,10 +221,12 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   UL_TRY(launch_ppo_head(h, s));
   mark(p, 2, s);
   // K8 backwards into the contiguous all-reduce buffer
-  UL_TRY(mlp_backward(p->va, b.actor_params, p->mb_obs, p->ld_mo, ml, p->acts_a, p->dmean, p->A,
-                      p->red, nullptr, 0, 0, 0, true, false, p->work, s));
-  UL_TRY(mlp_backward(p->vc, b.critic_params, p->mb_cobs, p->ld_mc, ml, p->acts_c, p->dv, 1,
-                      p->red + p->Pa, nullptr, 0, 0, 0, true, true, p->work, s));
+  UL_TRY(mlp_backward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, p->ld_mo > od, ml,
+                      p->acts_a, p->dmean, p->A, p->red, nullptr, 0, 0, 0, true, false, p->work,
+                      s));
+  UL_TRY(mlp_backward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, p->ld_mc > cd,
+                      ml, p->acts_c, p->dv, 1, p->red + p->Pa, nullptr, 0, 0, 0, true, true,
+                      p->work, s));
   mark(p, 0, s);
   return UL_OK;
 }
