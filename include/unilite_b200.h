@@ -129,22 +129,34 @@ typedef struct ul_net_desc {
 
 /* number of floats of the flat parameter vector (incl. log_std) */
 int64_t ul_net_param_count(const ul_net_desc* net);
-/* activation cache floats for a batch of M rows (hidden layers only) */
+/* activation cache floats for a batch of M rows (hidden layers only; layer
+ * i's rows have pitch round_up(d_i + 1, 4): 16 B rows + a ones column) */
 int64_t ul_mlp_act_floats(const ul_net_desc* net, int64_t M);
 /* backward workspace floats for a batch of M rows */
 int64_t ul_mlp_bwd_work_floats(const ul_net_desc* net, int64_t M);
+/* staged-weight floats (tensor-core path: W rows padded to 16 B) */
+int64_t ul_mlp_wstage_floats(const ul_net_desc* net);
+/* copy the flat W_i into the staged 16 B-row layout (call after every update) */
+int ul_stage_weights(const ul_net_desc* net, const float* params, float* wstage, void* stream);
+
+/* GEMM back ends for the MLP passes */
+#define UL_GEMM_FP32 0 /* SIMT fp32 FFMA: the exact-fp32 parity path            */
+#define UL_GEMM_TF32 1 /* tcgen05.mma kind::tf32 + TMEM + TMA (needs wstage)    */
 
 /* Forward: out[M, out] (ld_out) = MLP(x[M, in] (ldx)); hidden activations are
  * cached in `acts` (ul_mlp_act_floats).  Replaces R:tensornet/mlp.py:153-172. */
-int ul_mlp_forward(const ul_net_desc* net, const float* params, const float* x, int64_t ldx,
-                   int64_t M, float* acts, float* out, int64_t ld_out, void* stream);
+int ul_mlp_forward(const ul_net_desc* net, const float* params, const float* wstage, int backend,
+                   const float* x, int64_t ldx, int64_t M, float* acts, float* out,
+                   int64_t ld_out, void* stream);
 
 /* Backward from the upstream gradient dout[M, out] (ld_dout): writes the flat
  * gradient vector `grads` (log_std slot zeroed) and, if dx != NULL, the input
- * gradient dx[M, in] (lddx).  Replaces R:tensornet/mlp.py:175-198. */
-int ul_mlp_backward(const ul_net_desc* net, const float* params, const float* x, int64_t ldx,
-                    int64_t M, const float* acts, const float* dout, int64_t ld_dout,
-                    float* grads, float* dx, int64_t lddx, float* work, void* stream);
+ * gradient dx[M, in] (lddx).  x_has_ones: column `in` of x holds 1.0 (lets
+ * the tensor-core dW of layer 0 emit db).  Replaces R:tensornet/mlp.py:175-198. */
+int ul_mlp_backward(const ul_net_desc* net, const float* params, const float* wstage, int backend,
+                    const float* x, int64_t ldx, int x_has_ones, int64_t M, const float* acts,
+                    const float* dout, int64_t ld_dout, float* grads, float* dx, int64_t lddx,
+                    float* work, void* stream);
 
 /* Plain fp32 GEMM C = op(A) op(B) (+bias/ELU epilogues), exposed for tests.
  * layout bit0: A is K-major ([M,K] row-major) else M-major ([K,M]);
@@ -154,16 +166,25 @@ int ul_gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const floa
                 int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                 const float* bias, const float* aux, int64_t ldaux, void* stream);
 
+/* Same contract on the tcgen05 tensor-core kernel (kind::tf32, fp32 in/out):
+ * 16 B-aligned operands, row pitches multiple of 4, M >= 128, N, K >= 32;
+ * splits > 1 writes split-K partials at C + z*M*N (ld N). */
+int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A,
+               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, const float* bias,
+               const float* aux, int64_t ldaux, int splits, void* stream);
+
 /* ------------------------------------------------- K4 / K5 / K6 data path */
 /* Gather rows of up to 12 arrays sharing one index vector (PPO minibatch
  * copies of R:algos/ppo.py:161-176; replay sample copy of
  * R:replaypath/storage.py:106-110).  Strides / row widths in BYTES.  Rows
  * outside [lo, hi) are skipped and set *err (device int, may be NULL);
- * modulo > 0 maps absolute replay indices to ring slots. */
+ * modulo > 0 maps absolute replay indices to ring slots.  ones_byte (may be
+ * NULL): per desc, byte offset of a float overwritten with 1.0 in every
+ * gathered row (-1 = none; the MLP's bias column). */
 int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
                    const int64_t* src_stride, const int64_t* dst_stride, const int64_t* row_bytes,
-                   const int64_t* idx, int64_t n, int64_t modulo, int64_t lo, int64_t hi, int* err,
-                   void* stream);
+                   const int64_t* ones_byte, const int64_t* idx, int64_t n, int64_t modulo,
+                   int64_t lo, int64_t hi, int* err, void* stream);
 
 /* Replay ring insert (R:replaypath/storage.py:76-104): n rows of `width`
  * floats at absolute index `head`; rows may be pinned-host or device memory.
@@ -216,6 +237,7 @@ typedef struct ul_ppo_plan_desc {
                                        its own segment rows (weak scaling) and a
                                        global minibatch is the union of the
                                        ranks' local minibatches              */
+  int32_t gemm_backend;             /* UL_GEMM_FP32 or UL_GEMM_TF32           */
 } ul_ppo_plan_desc;
 
 typedef struct ul_ppo_bindings {

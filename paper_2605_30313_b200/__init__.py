@@ -3,3 +3,20 @@ learner API).  Compute runs in libunilite_b200.so (sm_100a); PyTorch is the
 host shell for HBM allocations, streams and torch.distributed."""
 
 __version__ = "0.1.0"
+
+
+def set_precision(gemm: str) -> None:
+    """Select the MLP GEMM back end: "tf32" (default; tcgen05 tensor cores,
+    fp32 storage, ~1e-3 relative GEMM error) or "fp32" (SIMT FFMA, exact fp32:
+    the reference-parity configuration, R:tensornet/mlp.py is float32)."""
+    from . import _lib
+
+    if gemm not in ("fp32", "tf32"):
+        raise ValueError("gemm precision must be 'fp32' or 'tf32'")
+    _lib._PRECISION["gemm"] = gemm
+
+
+def get_precision() -> str:
+    from . import _lib
+
+    return _lib._PRECISION["gemm"]

@@ -45,8 +45,9 @@ def round_up(x: int, m: int) -> int:
 
 
 def feature_ld(d: int) -> int:
-    """Device row stride for a feature width: 16-byte aligned rows."""
-    return round_up(max(int(d), 1), 4)
+    """Device row stride for a feature width: 16-byte aligned rows with at
+    least one spare column (the MLP's bias 'ones column')."""
+    return round_up(max(int(d), 1) + 1, 4)
 
 
 # ----------------------------------------------------------------- pinned host

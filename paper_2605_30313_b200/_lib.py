@@ -18,6 +18,16 @@ UL_MAX_SEG = 4
 UL_MAX_LAYERS = 8
 UL_PREP_BLOCKS = 296
 UL_MAX_ACT = 64
+UL_GEMM_FP32 = 0
+UL_GEMM_TF32 = 1
+
+# Process-wide GEMM back end of the MLP passes ("fp32": SIMT exact-fp32 parity
+# path; "tf32": tcgen05 tensor cores).  See paper_2605_30313_b200.set_precision.
+_PRECISION = {"gemm": "tf32"}
+
+
+def gemm_backend() -> int:
+    return UL_GEMM_TF32 if _PRECISION["gemm"] == "tf32" else UL_GEMM_FP32
 
 vp = C.c_void_p
 i64 = C.c_int64
@@ -55,7 +65,7 @@ class PpoPlanDesc(C.Structure):
         ("ld_cobs", i64), ("ld_act", i64), ("epochs", i32), ("minibatches", i32),
         ("clip_param", f64), ("entropy_coef", f64), ("value_loss_coef", f64),
         ("use_clipped_value_loss", i32), ("max_grad_norm", f64), ("world_size", i32),
-        ("rank", i32), ("raw_advantages", i32), ("local_shards", i32),
+        ("rank", i32), ("raw_advantages", i32), ("local_shards", i32), ("gemm_backend", i32),
     ]
 
 
@@ -100,13 +110,19 @@ _PROTOS = {
     "ul_net_param_count": (i64, [C.POINTER(NetDesc)]),
     "ul_mlp_act_floats": (i64, [C.POINTER(NetDesc), i64]),
     "ul_mlp_bwd_work_floats": (i64, [C.POINTER(NetDesc), i64]),
-    "ul_mlp_forward": (C.c_int, [C.POINTER(NetDesc), vp, vp, i64, i64, vp, vp, i64, vp]),
-    "ul_mlp_backward": (C.c_int, [C.POINTER(NetDesc), vp, vp, i64, i64, vp, vp, i64, vp, vp,
-                                  i64, vp, vp]),
+    "ul_mlp_wstage_floats": (i64, [C.POINTER(NetDesc)]),
+    "ul_stage_weights": (C.c_int, [C.POINTER(NetDesc), vp, vp, vp]),
+    "ul_mlp_forward": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp, i64, i64, vp, vp, i64,
+                                 vp]),
+    "ul_mlp_backward": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp, i64, C.c_int, i64, vp,
+                                  vp, i64, vp, vp, i64, vp, vp]),
     "ul_gemm_f32": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
                               vp, i64, vp]),
+    "ul_gemm_tc": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
+                             vp, i64, C.c_int, vp]),
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
-                                 C.POINTER(i64), C.POINTER(i64), vp, i64, i64, i64, i64, vp, vp]),
+                                 C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
+                                 vp]),
     "ul_ring_insert": (C.c_int, [vp, i64, i64, i64, vp, i64, vp]),
     "ul_device_permutation": (C.c_int, [i64, C.c_uint64, vp, vp]),
     "ul_norm_work_bytes": (i64, [i64]),

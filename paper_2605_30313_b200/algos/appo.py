@@ -11,6 +11,7 @@ from __future__ import annotations
 import torch
 
 from .. import _dev, _lib
+from ..tensornet.mlp import _staged
 from ._staging import staging_for
 from .configs import AppoConfig
 from .ppo import AcOpt, AcParams, _check_dims, _epochs_on_device
@@ -40,15 +41,17 @@ def recompute_targets(ds, params: AcParams) -> None:
     mean = _scratch("mean", chunk * ad, dev)
     s = _dev.stream()
     ls = params.actor.buf[params.actor.buf.numel() - ad:]
+    be_a, ws_a = _staged(params.actor)
+    be_c, ws_c = _staged(params.critic)
     for r0 in range(0, rows, chunk):
         m = min(chunk, rows - r0)
-        _lib.call("ul_mlp_forward", a_arch.desc(), _dev.ptr(params.actor.buf),
-                  _dev.ptr(ds.obs[r0]), ds.obs.stride(0), m, _dev.ptr(acts_a), _dev.ptr(mean),
-                  ad, s)
+        _lib.call("ul_mlp_forward", a_arch.desc(), _dev.ptr(params.actor.buf), _dev.ptr(ws_a),
+                  be_a, _dev.ptr(ds.obs[r0]), ds.obs.stride(0), m, _dev.ptr(acts_a),
+                  _dev.ptr(mean), ad, s)
         _lib.call("ul_gaussian_logp", _dev.ptr(mean), ad, _dev.ptr(ls), _dev.ptr(ds.act[r0]),
                   ds.act.stride(0), m, ad, _dev.ptr(ds.tlogp[r0:]), s)
-        _lib.call("ul_mlp_forward", c_arch.desc(), _dev.ptr(params.critic.buf),
-                  _dev.ptr(ds.cobs[r0]), ds.cobs.stride(0), m, _dev.ptr(acts_c),
+        _lib.call("ul_mlp_forward", c_arch.desc(), _dev.ptr(params.critic.buf), _dev.ptr(ws_c),
+                  be_c, _dev.ptr(ds.cobs[r0]), ds.cobs.stride(0), m, _dev.ptr(acts_c),
                   _dev.ptr(ds.vnow[r0:]), 1, s)
 
 

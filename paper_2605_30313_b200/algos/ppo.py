@@ -115,7 +115,7 @@ def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
     key = (params.actor.arch, params.critic.arch, ds.rows, ds.ld, cfg.epochs, cfg.minibatches,
            cfg.clip_param, cfg.entropy_coef, cfg.value_loss_coef, cfg.use_clipped_value_loss,
            cfg.max_grad_norm, world, rank, raw_adv, _dist.segment_mode(),
-           torch.cuda.current_device())
+           _lib.gemm_backend(), torch.cuda.current_device())
     plan = _PLANS.get(key)
     if plan is None:
         d = _lib.PpoPlanDesc()
@@ -130,6 +130,7 @@ def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
         d.max_grad_norm = cfg.max_grad_norm
         d.world_size, d.rank, d.raw_advantages = world, rank, int(raw_adv)
         d.local_shards = int(_dist.segment_mode() == "local" and world > 1)
+        d.gemm_backend = _lib.gemm_backend()
         plan = _Plan(d)
         _PLANS[key] = plan
     return plan

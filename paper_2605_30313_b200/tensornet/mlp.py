@@ -165,6 +165,8 @@ class ForwardCache:
     out: torch.Tensor
     rows: int
     pre_acts: list = field(default_factory=list)
+    wstage: torch.Tensor = None
+    backend: int = None
 
 
 def forward(params: ModelParams, x) -> tuple:
@@ -185,9 +187,23 @@ def forward(params: ModelParams, x) -> tuple:
     acts = torch.empty(max(_lib.lib().ul_mlp_act_floats(desc, rows), 1), dtype=torch.float32,
                        device=xd.device)
     out = torch.empty((rows, arch.output_dim), dtype=torch.float32, device=xd.device)
-    _lib.call("ul_mlp_forward", desc, _dev.ptr(params.buf), _dev.ptr(xd), xd.stride(0), rows,
-              _dev.ptr(acts), _dev.ptr(out), arch.output_dim, _dev.stream())
-    return out, ForwardCache(xd, acts, out, rows)
+    be, ws = _staged(params)
+    _lib.call("ul_mlp_forward", desc, _dev.ptr(params.buf), _dev.ptr(ws), be, _dev.ptr(xd),
+              xd.stride(0), rows, _dev.ptr(acts), _dev.ptr(out), arch.output_dim, _dev.stream())
+    return out, ForwardCache(xd, acts, out, rows, wstage=ws, backend=be)
+
+
+def _staged(params: ModelParams):
+    """(backend, staged weights) for one MLP pass: the tensor-core path reads
+    W through 16-byte-aligned padded rows restaged from the live parameters."""
+    be = _lib.gemm_backend()
+    if be != _lib.UL_GEMM_TF32:
+        return be, None
+    desc = params.arch.desc()
+    ws = torch.empty(max(_lib.lib().ul_mlp_wstage_floats(desc), 1), dtype=torch.float32,
+                     device=params.buf.device)
+    _lib.call("ul_stage_weights", desc, _dev.ptr(params.buf), _dev.ptr(ws), _dev.stream())
+    return be, ws
 
 
 def backward(params: ModelParams, cache: ForwardCache, dout) -> tuple:
@@ -204,9 +220,11 @@ def backward(params: ModelParams, cache: ForwardCache, dout) -> tuple:
     dx = torch.empty((rows, arch.input_dim), dtype=torch.float32, device=params.buf.device)
     work = torch.empty(max(_lib.lib().ul_mlp_bwd_work_floats(desc, rows), 1),
                        dtype=torch.float32, device=params.buf.device)
-    _lib.call("ul_mlp_backward", desc, _dev.ptr(params.buf), _dev.ptr(cache.x),
-              cache.x.stride(0), rows, _dev.ptr(cache.acts), _dev.ptr(dd), arch.output_dim,
-              _dev.ptr(grads.buf), _dev.ptr(dx), arch.input_dim, _dev.ptr(work), _dev.stream())
+    be, ws = (cache.backend, cache.wstage) if cache.backend is not None else _staged(params)
+    _lib.call("ul_mlp_backward", desc, _dev.ptr(params.buf), _dev.ptr(ws), be,
+              _dev.ptr(cache.x), cache.x.stride(0), 0, rows, _dev.ptr(cache.acts), _dev.ptr(dd),
+              arch.output_dim, _dev.ptr(grads.buf), _dev.ptr(dx), arch.input_dim,
+              _dev.ptr(work), _dev.stream())
     return dx, grads
 
 

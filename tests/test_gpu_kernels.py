@@ -15,6 +15,16 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 from paper_2605_30313_b200 import _dev, _lib  # noqa: E402
 from paper_2605_30313_b200 import algos as A  # noqa: E402
 from paper_2605_30313_b200 import tensornet as TN  # noqa: E402
+import paper_2605_30313_b200 as P  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def fp32_mode():
+    """The exact-fp32 parity configuration (SIMT GEMMs)."""
+    old = P.get_precision()
+    P.set_precision("fp32")
+    yield
+    P.set_precision(old)
 
 
 def rel_err(a, b):
@@ -164,7 +174,7 @@ def test_gather_rows_bit_exact():
     idd = torch.tensor(idx, device="cuda")
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("ul_gather_rows", 1, _lib.ptr_array([_dev.ptr(sd)]), _lib.ptr_array([_dev.ptr(dd)]),
-              _lib.i64_array([944]), _lib.i64_array([944]), _lib.i64_array([944]), _dev.ptr(idd),
+              _lib.i64_array([944]), _lib.i64_array([944]), _lib.i64_array([944]), None, _dev.ptr(idd),
               333, 0, 0, 1000, _dev.ptr(err), _dev.stream())
     np.testing.assert_array_equal(dd.cpu().numpy(), src[idx])
     assert int(err.item()) == 0

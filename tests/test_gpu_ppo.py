@@ -13,6 +13,16 @@ if not torch.cuda.is_available():  # pragma: no cover
 
 from paper_2605_30313_b200 import algos as A  # noqa: E402
 from paper_2605_30313_b200 import tensornet as TN  # noqa: E402
+import paper_2605_30313_b200 as P  # noqa: E402
+
+
+@pytest.fixture(autouse=True)
+def fp32_mode():
+    """The exact-fp32 parity configuration (SIMT GEMMs)."""
+    old = P.get_precision()
+    P.set_precision("fp32")
+    yield
+    P.set_precision(old)
 
 
 def rel_err(a, b):
