@@ -50,6 +50,7 @@ def _args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--precision", choices=("fp32", "tf32"), default=None)
     return ap.parse_args()
 
 
@@ -202,6 +203,12 @@ def run_ours(args):
     from paper_2605_30313_b200.algos._staging import staging_for
     from paper_2605_30313_b200.workload import CONFIGS, make_rollout
 
+    import paper_2605_30313_b200 as PKG
+
+    if args.precision:
+        PKG.set_precision(args.precision)
+    prec = PKG.get_precision()
+    prec_name = {"fp32": "fp32 SIMT FFMA", "tf32": "tcgen05 kind::tf32 (TMA + TMEM)"}[prec]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -311,14 +318,15 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "tf32 (f32 storage/accum)",
+        "data": "synthetic",
         "config": {"workload": "PPO update (GAE + 5 epochs x 4 minibatches), cfg2 locomotion "
                                "shape: 4096 envs x 24 steps per GPU, obs 235 / act 12, "
                                "actor+critic 512-256-128",
                    "global_batch": transitions, "minibatch_rows": transitions // 4,
                    "parallelism": f"dp{world}", "indices": "device permutation (performance "
                    "mode)", "inputs_larger_than_l2": True,
-                   "segment_bytes_per_gpu": ds.h2d_bytes(seg), "gemm_precision": "fp32 SIMT"},
+                   "segment_bytes_per_gpu": ds.h2d_bytes(seg), "gemm_precision": prec_name},
         "update_ms": ms,
         "parity_mode": {"value": transitions / (par_ms / 1e3), "unit": UNIT, "update_ms": par_ms,
                         "indices": "host numpy Philox permutation per epoch (reference stream)"},
@@ -327,7 +335,7 @@ def run_ours(args):
                 "ms_per_step": e2e_ms, "api": "algos.gae + algos.ppo_update, pinned host segment"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_sus,
                      "unit": "TFLOP/s", "frac": gemm_tflops / bf16_sus, "traffic": traffic,
-                     "kernel": "sgemm_kernel (all MLP GEMMs of one update)",
+                     "kernel": "MLP GEMMs of one update (tc_gemm_kernel + sgemm_kernel heads)",
                      "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
                      "algorithmic_flops_per_update": counts["gemm_flops_per_update"],
                      "phase_ms_per_update": prof},

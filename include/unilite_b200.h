@@ -293,6 +293,51 @@ int ul_ppo_plan_counts(void* plan, int64_t* kernels_per_update, double* gemm_flo
 int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
                         int64_t t_critic, double* ms, void* stream);
 
+/* ------------------------------------------ SAC / FastSAC / FlashSAC plan */
+/* Device-resident SAC scalars: log_alpha and its ScalarAdam state
+ * (R:algos/sac.py:35-53), plus the last update's loss terms. */
+typedef struct ul_sac_ctl {
+  double log_alpha, a_m, a_v, a_t, alpha_lr;
+  double critic_loss, actor_loss, alpha_loss, logp_sum;
+  int32_t diverged, pad0;
+} ul_sac_ctl;
+
+typedef struct ul_sac_plan_desc {
+  ul_net_desc actor;  /* obs -> act                                   */
+  ul_net_desc critic; /* obs+act -> 1 (q1, q2 and both targets)        */
+  int64_t batch;
+  int32_t obs_dim, act_dim;
+  double gamma, tau, target_entropy, max_grad_norm;
+  int32_t gemm_backend, pad0;
+} ul_sac_plan_desc;
+
+typedef struct ul_sac_bindings {
+  float *actor, *actor_m, *actor_v;
+  float *q1, *q1_m, *q1_v;
+  float *q2, *q2_m, *q2_v;
+  float *q1t, *q2t;
+} ul_sac_bindings;
+
+/* sac_update (R:algos/sac.py:139-178) as a native plan.  Batches come as
+ * codec rows (R:replaypath/storage.py:17-46) gathered from a device replay
+ * ring or a staged batch. */
+int ul_sac_plan_create(const ul_sac_plan_desc* desc, void** plan);
+int ul_sac_plan_destroy(void* plan);
+int ul_sac_plan_bind(void* plan, const ul_sac_bindings* b);
+/* rows[(idx[i] % modulo)] (pitch in floats); idx NULL = rows 0..B-1 */
+int ul_sac_plan_load_rows(void* plan, const float* rows, int64_t pitch, const int64_t* idx,
+                          int64_t modulo, int64_t lo, int64_t hi, int* err, void* stream);
+/* upload alpha state + per-network (lr, t): order actor, q1, q2 */
+int ul_sac_plan_begin(void* plan, const ul_sac_ctl* host_ctl, const double* lrs,
+                      const int64_t* ts, void* stream);
+/* noise: [2, B, A] float32 (eps for the target, eps for the actor step);
+ * either fill it from the host (parity mode) or on the device */
+int ul_sac_plan_noise_ptr(void* plan, float** eps);
+int ul_sac_plan_device_noise(void* plan, uint64_t key, uint64_t counter, void* stream);
+int ul_sac_plan_update(void* plan, int do_actor, void* stream);
+/* D2H of the control records (+ sync): ts = step counters (actor, q1, q2) */
+int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

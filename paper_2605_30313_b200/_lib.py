@@ -75,6 +75,23 @@ class PpoBindings(C.Structure):
                                   "critic_m", "critic_v", "perm", "reduce_buf")]
 
 
+class SacCtl(C.Structure):
+    _fields_ = [(n, f64) for n in ("log_alpha", "a_m", "a_v", "a_t", "alpha_lr", "critic_loss",
+                                   "actor_loss", "alpha_loss", "logp_sum")] + \
+               [("diverged", i32), ("pad0", i32)]
+
+
+class SacPlanDesc(C.Structure):
+    _fields_ = [("actor", NetDesc), ("critic", NetDesc), ("batch", i64), ("obs_dim", i32),
+                ("act_dim", i32), ("gamma", f64), ("tau", f64), ("target_entropy", f64),
+                ("max_grad_norm", f64), ("gemm_backend", i32), ("pad0", i32)]
+
+
+class SacBindings(C.Structure):
+    _fields_ = [(n, vp) for n in ("actor", "actor_m", "actor_v", "q1", "q1_m", "q1_v", "q2",
+                                  "q2_m", "q2_v", "q1t", "q2t")]
+
+
 class PpoResult(C.Structure):
     _fields_ = [("policy_loss", f64), ("value_loss", f64), ("entropy", f64), ("kl", f64),
                 ("grad_norm", f64), ("t_actor", i64), ("t_critic", i64), ("diverged", i32),
@@ -138,6 +155,15 @@ _PROTOS = {
     "ul_ppo_plan_reduce_buffer": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),
     "ul_ppo_plan_run": (C.c_int, [vp, f64, f64, i64, i64, C.c_int, vp]),
     "ul_ppo_plan_finish": (C.c_int, [vp, C.POINTER(PpoResult), vp]),
+    "ul_sac_plan_create": (C.c_int, [C.POINTER(SacPlanDesc), C.POINTER(vp)]),
+    "ul_sac_plan_destroy": (C.c_int, [vp]),
+    "ul_sac_plan_bind": (C.c_int, [vp, C.POINTER(SacBindings)]),
+    "ul_sac_plan_load_rows": (C.c_int, [vp, vp, i64, vp, i64, i64, i64, vp, vp]),
+    "ul_sac_plan_begin": (C.c_int, [vp, C.POINTER(SacCtl), C.POINTER(f64), C.POINTER(i64), vp]),
+    "ul_sac_plan_noise_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "ul_sac_plan_device_noise": (C.c_int, [vp, C.c_uint64, C.c_uint64, vp]),
+    "ul_sac_plan_update": (C.c_int, [vp, C.c_int, vp]),
+    "ul_sac_plan_finish": (C.c_int, [vp, C.POINTER(SacCtl), C.POINTER(i64), vp]),
     "ul_ppo_plan_counts": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64)]),
     "ul_ppo_plan_profile": (C.c_int, [vp, f64, f64, i64, i64, C.POINTER(f64), vp]),
 }

@@ -1,0 +1,276 @@
+"""Soft actor-critic on the device (mirror of R:algos/sac.py).
+
+``sac_update`` keeps the reference signature and order (target -> q1 Adam ->
+q2 Adam -> [actor + alpha every policy_frequency] -> Polyak) and runs the
+native SAC plan (ul_sac_plan_*, csrc/sac.cu).  Noise: a numpy Generator is
+consumed exactly like the reference (eps for the target, then eps for the
+actor step, each ``standard_normal((B, A))``: "parity mode"); a
+:class:`~paper_2605_30313_b200.algos.ppo.DeviceRng` draws both on the device
+(Philox4x32-10, "performance mode").  The batch may be a reference-style dict
+(host arrays, RowCodec field names) or a :class:`DeviceRows` handle pointing at
+device replay rows (the DeviceReplayCache fast path: no decode, no H2D).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .. import _dev, _lib
+from ..errors import DivergenceError
+from ..tensornet.adam import OptState
+from ..tensornet.mlp import ModelParams
+from .configs import SacConfig
+from .ppo import DeviceRng
+from .segment import UpdateStats
+
+
+@dataclass
+class ScalarAdam:
+    """R:algos/sac.py:35-53 (host copy of the device alpha optimizer)."""
+
+    lr: float
+    m: float = 0.0
+    v: float = 0.0
+    t: int = 0
+    betas: tuple = (0.9, 0.999)
+    eps: float = 1e-8
+
+    def step(self, x: float, g: float) -> float:
+        if not np.isfinite(g):
+            raise DivergenceError("non-finite gradient in ScalarAdam")
+        self.t += 1
+        b1, b2 = self.betas
+        self.m = b1 * self.m + (1 - b1) * g
+        self.v = b2 * self.v + (1 - b2) * g * g
+        m_hat = self.m / (1 - b1 ** self.t)
+        v_hat = self.v / (1 - b2 ** self.t)
+        return x - self.lr * m_hat / (np.sqrt(v_hat) + self.eps)
+
+
+@dataclass
+class SacParams:
+    """R:algos/sac.py:56-69."""
+
+    actor: ModelParams
+    q1: ModelParams
+    q2: ModelParams
+    q1_targ: ModelParams
+    q2_targ: ModelParams
+    log_alpha: float
+
+    def copy(self) -> "SacParams":
+        return SacParams(self.actor.copy(), self.q1.copy(), self.q2.copy(), self.q1_targ.copy(),
+                         self.q2_targ.copy(), self.log_alpha)
+
+
+@dataclass
+class SacState:
+    """R:algos/sac.py:72-97."""
+
+    params: SacParams
+    actor_opt: OptState
+    q1_opt: OptState
+    q2_opt: OptState
+    alpha_opt: ScalarAdam
+    action_dim: int
+    update_count: int = 0
+
+    @classmethod
+    def create(cls, actor: ModelParams, q1: ModelParams, q2: ModelParams,
+               cfg: SacConfig) -> "SacState":
+        params = SacParams(actor=actor, q1=q1, q2=q2, q1_targ=q1.copy(), q2_targ=q2.copy(),
+                           log_alpha=float(np.log(cfg.alpha_init)))
+        return cls(params=params, actor_opt=OptState.for_params(actor, cfg.actor_lr),
+                   q1_opt=OptState.for_params(q1, cfg.critic_lr),
+                   q2_opt=OptState.for_params(q2, cfg.critic_lr),
+                   alpha_opt=ScalarAdam(lr=cfg.alpha_lr), action_dim=actor.arch.output_dim)
+
+
+def soft_update(target: ModelParams, online: ModelParams, tau: float) -> None:
+    """target <- (1 - tau) target + tau online, in place (R:algos/sac.py:100-108)."""
+    _lib.call("ul_polyak", _dev.ptr(target.buf), _dev.ptr(online.buf), target.buf.numel(),
+              float(tau), _dev.stream())
+
+
+class DeviceRows:
+    """A replay batch still in codec-row form on the device: rows of
+    ``ring[idx[i] % modulo]`` (pitch in floats).  Produced by
+    :class:`~paper_2605_30313_b200.replaypath.DeviceReplayCache`."""
+
+    def __init__(self, ring: torch.Tensor, pitch: int, idx: torch.Tensor | None, n: int,
+                 modulo: int = 0, lo: int = 0, hi: int = 2**62):
+        self.ring, self.pitch, self.idx, self.n = ring, pitch, idx, n
+        self.modulo, self.lo, self.hi = modulo, lo, hi
+
+
+# ------------------------------------------------------------------- plan
+class _SacPlan:
+    def __init__(self, state: SacState, batch: int, cfg: SacConfig):
+        d = _lib.SacPlanDesc()
+        p = state.params
+        d.actor = p.actor.arch.desc()
+        d.critic = p.q1.arch.desc()
+        d.batch = batch
+        d.obs_dim = p.actor.arch.input_dim
+        d.act_dim = p.actor.arch.output_dim
+        d.gamma, d.tau = cfg.gamma, cfg.tau
+        d.target_entropy = -cfg.target_entropy_ratio * state.action_dim
+        d.max_grad_norm = cfg.max_grad_norm
+        d.gemm_backend = _lib.gemm_backend()
+        h = C.c_void_p()
+        _lib.call("ul_sac_plan_create", C.byref(d), C.byref(h))
+        self.h, self.desc, self.batch = h, d, batch
+        eps = C.c_void_p()
+        _lib.call("ul_sac_plan_noise_ptr", h, C.byref(eps))
+        self.eps_ptr = eps.value
+        self._bound = None
+        self.stage = None
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.lib().ul_sac_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    def bind(self, state: SacState):
+        p = state.params
+        key = (p.actor.buf.data_ptr(), p.q1.buf.data_ptr(), p.q2.buf.data_ptr(),
+               p.q1_targ.buf.data_ptr(), p.q2_targ.buf.data_ptr(),
+               state.actor_opt.m.buf.data_ptr(), state.q1_opt.m.buf.data_ptr(),
+               state.q2_opt.m.buf.data_ptr())
+        if key == self._bound:
+            return
+        b = _lib.SacBindings()
+        vals = dict(actor=p.actor.buf, actor_m=state.actor_opt.m.buf,
+                    actor_v=state.actor_opt.v.buf, q1=p.q1.buf, q1_m=state.q1_opt.m.buf,
+                    q1_v=state.q1_opt.v.buf, q2=p.q2.buf, q2_m=state.q2_opt.m.buf,
+                    q2_v=state.q2_opt.v.buf, q1t=p.q1_targ.buf, q2t=p.q2_targ.buf)
+        for k, v in vals.items():
+            setattr(b, k, _dev.ptr(v))
+        _lib.call("ul_sac_plan_bind", self.h, C.byref(b))
+        self._bound = key
+
+
+_PLANS: dict = {}
+
+
+def _plan_for(state: SacState, batch: int, cfg: SacConfig) -> _SacPlan:
+    p = state.params
+    key = (p.actor.arch, p.q1.arch, batch, cfg.gamma, cfg.tau, cfg.target_entropy_ratio,
+           cfg.max_grad_norm, _lib.gemm_backend(), torch.cuda.current_device())
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = _SacPlan(state, batch, cfg)
+        _PLANS[key] = plan
+    plan.bind(state)
+    return plan
+
+
+_PINNED: dict = {}
+
+
+def _pinned(key, shape, dtype=np.float32) -> np.ndarray:
+    """Reusable page-locked staging (callers sync before reuse: sac_update
+    reads its statistics back at the end of every call)."""
+    buf = _PINNED.get(key)
+    if buf is None or buf.shape != tuple(shape):
+        buf = _dev.pinned_empty(shape, dtype)
+        _PINNED[key] = buf
+    return buf
+
+
+def _encode_rows(batch: dict, obs_dim: int, act_dim: int) -> np.ndarray:
+    """RowCodec.encode (R:replaypath/storage.py:25-35) into a pinned staging row block."""
+    n = len(batch["obs"])
+    width = 2 * obs_dim + act_dim + 3
+    rows = _pinned(("rows", n, width), (n, width))
+    d, a = obs_dim, act_dim
+    rows[:, :d] = _dev.to_numpy(batch["obs"])
+    rows[:, d:d + a] = _dev.to_numpy(batch["action"])
+    rows[:, d + a] = _dev.to_numpy(batch["reward"])
+    rows[:, d + a + 1:2 * d + a + 1] = _dev.to_numpy(batch["next_obs"])
+    rows[:, 2 * d + a + 1] = np.asarray(_dev.to_numpy(batch["terminated"]), np.float32)
+    rows[:, 2 * d + a + 2] = np.asarray(_dev.to_numpy(batch["n_used"]), np.float32)
+    return rows
+
+
+def _load_batch(plan: _SacPlan, batch, obs_dim: int, act_dim: int) -> None:
+    s = _dev.stream()
+    if isinstance(batch, DeviceRows):
+        _lib.call("ul_sac_plan_load_rows", plan.h, _dev.ptr(batch.ring), batch.pitch,
+                  _dev.ptr(batch.idx) if batch.idx is not None else None, batch.modulo,
+                  batch.lo, batch.hi, None, s)
+        return
+    rows_dev = getattr(batch, "rows", None)
+    if isinstance(rows_dev, torch.Tensor) and rows_dev.is_cuda:
+        # DeviceBatch from DeviceReplayCache / RowCodec.decode: rows already in HBM
+        _lib.call("ul_sac_plan_load_rows", plan.h, _dev.ptr(rows_dev), rows_dev.stride(0), None,
+                  0, 0, 2**62, None, s)
+        return
+    rows = _encode_rows(batch, obs_dim, act_dim)
+    if plan.stage is None or tuple(plan.stage.shape) != rows.shape:
+        plan.stage = torch.empty(rows.shape, dtype=torch.float32, device="cuda")
+    dev = plan.stage
+    _dev.h2d(dev, rows)
+    _lib.call("ul_sac_plan_load_rows", plan.h, _dev.ptr(dev), rows.shape[1], None, 0, 0,
+              2**62, None, s)
+
+
+def _fill_noise(plan: _SacPlan, rng, B: int, A: int, do_actor: bool) -> None:
+    s = _dev.stream()
+    if rng is None or isinstance(rng, DeviceRng):
+        rng = rng if rng is not None else DeviceRng(0)
+        _lib.call("ul_sac_plan_device_noise", plan.h, rng.next_key(), rng.counter, s)
+        return
+    eps = _pinned(("eps", B, A), (2, B, A))
+    eps[0] = rng.standard_normal((B, A))       # critic_target (R:algos/sac.py:117)
+    if do_actor:
+        eps[1] = rng.standard_normal((B, A))   # actor step (R:algos/sac.py:237)
+    _lib.call("ul_memcpy_async", plan.eps_ptr, eps.ctypes.data, eps.nbytes, s)
+
+
+def sac_update(batch, state: SacState, cfg: SacConfig, rng) -> UpdateStats:
+    """One critic update (+ periodic actor/alpha update) on a replay batch
+    (R:algos/sac.py:139-178)."""
+    n = batch.n if isinstance(batch, DeviceRows) else len(batch["obs"])
+    if n < 2:
+        raise ValueError("sac_update needs a batch of at least 2 rows")
+    p = state.params
+    od, ad = p.actor.arch.input_dim, p.actor.arch.output_dim
+    plan = _plan_for(state, n, cfg)
+    _load_batch(plan, batch, od, ad)
+    do_actor = (state.update_count + 1) % cfg.policy_frequency == 0
+    _fill_noise(plan, rng, n, ad, do_actor)
+    ctl = _lib.SacCtl()
+    ctl.log_alpha = p.log_alpha
+    ctl.a_m, ctl.a_v, ctl.a_t = state.alpha_opt.m, state.alpha_opt.v, float(state.alpha_opt.t)
+    ctl.alpha_lr = state.alpha_opt.lr
+    lrs = (C.c_double * 3)(state.actor_opt.lr, state.q1_opt.lr, state.q2_opt.lr)
+    ts = (C.c_int64 * 3)(state.actor_opt.t, state.q1_opt.t, state.q2_opt.t)
+    s = _dev.stream()
+    _lib.call("ul_sac_plan_begin", plan.h, C.byref(ctl), lrs, ts, s)
+    alpha_before = float(np.exp(p.log_alpha))
+    _lib.call("ul_sac_plan_update", plan.h, int(do_actor), s)
+    out = _lib.SacCtl()
+    st = _lib.lib().ul_sac_plan_finish(plan.h, C.byref(out), ts, s)
+    state.actor_opt.t, state.q1_opt.t, state.q2_opt.t = int(ts[0]), int(ts[1]), int(ts[2])
+    state.update_count += 1
+    if do_actor:
+        p.log_alpha = float(out.log_alpha)
+        state.alpha_opt.m, state.alpha_opt.v = float(out.a_m), float(out.a_v)
+        state.alpha_opt.t = int(round(out.a_t))
+    if st != 0:
+        _lib.check(st, "ul_sac_plan_finish")
+    stats = UpdateStats(lr=cfg.critic_lr)
+    stats.extra["critic_loss"] = float(out.critic_loss)
+    stats.extra["alpha"] = alpha_before
+    if do_actor:
+        stats.extra["actor_loss"] = float(out.actor_loss)
+        stats.extra["alpha_loss"] = float(out.alpha_loss)
+        stats.extra["alpha"] = float(np.exp(p.log_alpha))
+    return stats

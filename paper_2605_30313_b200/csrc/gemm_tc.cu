@@ -36,16 +36,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// Bounded wait: a pipeline bug traps (error surfaces at the next sync) instead
+// of hanging the GPU until the host-side timeout.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(su32(bar)),
-      "r"(parity)
-      : "memory");
+  uint32_t done = 0;
+  for (uint32_t spin = 0; spin < (1u << 26); ++spin) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+  }
+  __trap();
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -57,14 +64,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// UMMA shared-memory matrix descriptor, SWIZZLE_128B, sm100 version bit.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory matrix descriptor, sm100 version bit.  Layout type 2 =
+// SWIZZLE_128B (16-byte atoms; K-major tiles), 1 = SWIZZLE_128B_BASE32B
+// (32-byte atoms; the only legal layout for MN-major tf32 operands).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -199,10 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b_base = a_base + S::kABytes;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t da = A_MN ? smem_desc(a_base + kk * 1024, 4096, 1024)
-                                   : smem_desc(a_base + kk * 32, 16, 1024);
-          const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 1024)
-                                   : smem_desc(b_base + kk * 32, 16, 1024);
+          // K-major: 8-row x 128 B swizzle atoms (SBO 1024), K step = +32 B.
+          // MN-major: 128 B of M/N per row, 4-row x 128 B atoms with 32 B
+          // swizzle granules (SBO 512), 32-element M/N chunks 4 KB apart
+          // (LBO), K step = 8 rows = +1024 B.
+          const uint64_t da = A_MN ? smem_desc(a_base + kk * 1024, 4096, 512, 1)
+                                   : smem_desc(a_base + kk * 32, 16, 1024, 2);
+          const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 512, 1)
+                                   : smem_desc(b_base + kk * 32, 16, 1024, 2);
           mma_tf32(tmem, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
@@ -280,7 +294,7 @@ EncodeFn encode_fn() {
 // 2-D fp32 tensor map: inner (contiguous) extent, outer extent, row pitch
 // (elements), box {32, box_outer}, 128-byte swizzle, OOB -> zero.
 int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t ld,
-             int box_outer) {
+             int box_outer, bool mn_major) {
   EncodeFn fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -295,7 +309,8 @@ int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, 
   cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1u, 1u};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -309,10 +324,10 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
            cudaStream_t s) {
   CUtensorMap ma, mb;
   // A(m,k): K-major -> rows=M, inner=K ; MN-major -> rows=K, inner=M
-  if (A_MN) UL_TRY(make_map(&ma, d.A, d.M, d.K, d.lda, 32));
-  else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM));
-  if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32));
-  else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN));
+  if (A_MN) UL_TRY(make_map(&ma, d.A, d.M, d.K, d.lda, 32, true));
+  else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM, false));
+  if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32, true));
+  else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN, false));
   TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, C, d.ldc, d.bias, d.aux, d.ldaux, split_stride,
            ones_col};
   auto kern = tc_gemm_kernel<A_MN, B_MN, EPI, BN>;

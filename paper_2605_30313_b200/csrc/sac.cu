@@ -1,0 +1,587 @@
+// K10 SAC soft target, K11 SAC critic / actor / alpha heads, and the native
+// SAC update plan (FastSAC = reference algo "sac", FlashSAC = "flashsac").
+//
+// Replaces R:algos/sac.py:35-53 (ScalarAdam), :100-108 (soft_update),
+// :111-125 (critic_target), :128-136 (critic_loss_and_grads), :139-178
+// (sac_update), :181-221 (actor_loss_and_grads), :224-229
+// (alpha_loss_and_grad), :232-249 (_actor_and_alpha_step) and
+// R:tensornet/distributions.py:66-84 (squashed sample / log-prob).
+// One update, in the reference order:
+//   target:  actor fwd(next_obs) -> squash(eps1) -> q1t/q2t fwd -> y (f64)
+//   critics: q1, q2 fwd -> MSE head -> q1, q2 bwd -> Adam(q1), Adam(q2)
+//   [actor every policy_frequency updates]: actor fwd(obs) -> squash(eps2)
+//            -> q1, q2 fwd (UPDATED critics) -> argmin pick -> q1/q2 dX only
+//            over the action columns -> actor head -> actor bwd -> Adam(actor)
+//            -> alpha ScalarAdam (f64, device)
+//   Polyak q1t <- q1, q2t <- q2 (incl. log_std)
+// The replay batch arrives as codec rows (obs | action | r | next_obs | term |
+// n_used, R:replaypath/storage.py:17-46) gathered straight from the device
+// replay ring (K6) into the critic / actor / target input matrices.
+#include <new>
+
+#include "learner.cuh"
+
+namespace ul {
+namespace {
+
+constexpr double kLog2Pi = 1.8378770664093453;
+constexpr float kSquashEps = 1e-6f;
+
+// ---------------------------------------------------------------- kernels
+// a = tanh(mean + std*eps) (f32 like the reference), logp = Gaussian(u) -
+// sum log1p(-a^2 + 1e-6); a is written into dst[:, col0:col0+A] (a critic
+// input matrix) and, optionally, a_out (for the actor gradient).
+__global__ void squash_kernel(const float* __restrict__ mean, int64_t ldm,
+                              const float* __restrict__ log_std, const float* __restrict__ eps,
+                              int64_t lde, int64_t n, int A, float* __restrict__ dst, int64_t ldd,
+                              int col0, float* __restrict__ a_out, float* __restrict__ logp) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double lp = 0.0;
+    for (int j = 0; j < A; ++j) {
+      const float ls = log_std[j];
+      const float sd = expf(ls);
+      const float m = mean[i * ldm + j];
+      const float u = __fadd_rn(m, __fmul_rn(sd, eps[i * lde + j]));
+      const float a = tanhf(u);
+      const double z = ((double)u - (double)m) / (double)sd;
+      lp += -(double)ls - 0.5 * kLog2Pi - 0.5 * z * z;
+      lp -= log1p(-(double)a * (double)a + 1e-6);
+      dst[i * ldd + col0 + j] = a;
+      if (a_out) a_out[i * A + j] = a;
+    }
+    logp[i] = (float)lp;
+  }
+}
+
+// y = r + gamma^n_used (1 - term) (min(q1t, q2t) - alpha logp)  (float64)
+__global__ void sac_target_kernel(const float* __restrict__ r, const float* __restrict__ term,
+                                  const float* __restrict__ nused, const float* __restrict__ q1t,
+                                  const float* __restrict__ q2t, const float* __restrict__ logp,
+                                  const ul_sac_ctl* __restrict__ ctl, double gamma, int64_t n,
+                                  double* __restrict__ y) {
+  const double alpha = exp(ctl->log_alpha);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double keep = term[i] > 0.5f ? 0.0 : 1.0;
+    const double soft = fmin((double)q1t[i], (double)q2t[i]) - alpha * (double)logp[i];
+    y[i] = (double)r[i] + pow(gamma, (double)(int64_t)nused[i]) * keep * soft;
+  }
+}
+
+// twin-critic MSE head: dq_k = 2 (q_k - y)/B ; loss_k = mean (q_k - y)^2
+__global__ void __launch_bounds__(256) critic_head_kernel(const float* __restrict__ q1,
+                                                          const float* __restrict__ q2,
+                                                          const double* __restrict__ y, int64_t n,
+                                                          double inv_n, float* __restrict__ dq1,
+                                                          float* __restrict__ dq2, double* part,
+                                                          unsigned int* ticket, ul_sac_ctl* ctl) {
+  __shared__ double scratch[32];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double l1 = 0.0, l2 = 0.0;
+  if (i < n) {
+    const double e1 = (double)q1[i] - y[i], e2 = (double)q2[i] - y[i];
+    l1 = e1 * e1;
+    l2 = e2 * e2;
+    dq1[i] = (float)(2.0 * e1 * inv_n);
+    dq2[i] = (float)(2.0 * e2 * inv_n);
+  }
+  double r1 = block_sum(l1, scratch);
+  double r2 = block_sum(l2, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r1;
+    part[2 * blockIdx.x + 1] = r2;
+  }
+  if (!last_block_ticket(ticket, gridDim.x)) return;
+  if (threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      s1 += part[2 * b];
+      s2 += part[2 * b + 1];
+    }
+    ctl->critic_loss = s1 * inv_n + s2 * inv_n;
+  }
+}
+
+// actor-step pick head: pick = (q1 <= q2), loss = mean(alpha logp - min q)
+__global__ void __launch_bounds__(256) pick_head_kernel(const float* __restrict__ q1,
+                                                        const float* __restrict__ q2,
+                                                        const float* __restrict__ logp, int64_t n,
+                                                        float* __restrict__ d1,
+                                                        float* __restrict__ d2, double* part,
+                                                        unsigned int* ticket, ul_sac_ctl* ctl) {
+  __shared__ double scratch[32];
+  const double alpha = exp(ctl->log_alpha);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double l = 0.0, lp = 0.0;
+  if (i < n) {
+    const float a = q1[i], b = q2[i];
+    const bool pick = a <= b;
+    d1[i] = pick ? 1.f : 0.f;
+    d2[i] = pick ? 0.f : 1.f;
+    l = alpha * (double)logp[i] - (double)fminf(a, b);
+    lp = (double)logp[i];
+  }
+  double r1 = block_sum(l, scratch);
+  double r2 = block_sum(lp, scratch);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = r1;
+    part[2 * blockIdx.x + 1] = r2;
+  }
+  if (!last_block_ticket(ticket, gridDim.x)) return;
+  if (threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      s1 += part[2 * b];
+      s2 += part[2 * b + 1];
+    }
+    ctl->actor_loss = s1 / (double)n;
+    ctl->logp_sum = s2;
+  }
+}
+
+// actor gradient head (R:algos/sac.py:207-217): dmean, dlog_std
+__global__ void __launch_bounds__(256) actor_head_kernel(
+    const float* __restrict__ a, const float* __restrict__ eps, int64_t lde,
+    const float* __restrict__ din1, const float* __restrict__ din2, int64_t ldin,
+    const float* __restrict__ log_std, int64_t n, int A, const ul_sac_ctl* __restrict__ ctl,
+    float* __restrict__ dmean, double* part, unsigned int* ticket, float* __restrict__ dls_out) {
+  __shared__ double scratch[32];
+  const double alpha = exp(ctl->log_alpha);
+  const double inv_n = 1.0 / (double)n;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double* pp = part + (int64_t)blockIdx.x * A;
+  for (int j = 0; j < A; ++j) {
+    double t = 0.0;
+    if (i < n) {
+      const double av = (double)a[i * A + j];
+      const double oma = 1.0 - av * av;
+      const double dlogp_du = 2.0 * av * oma / (oma + 1e-6);
+      const double dq = (double)din1[i * ldin + j] + (double)din2[i * ldin + j];
+      const double du_dls = exp((double)log_std[j]) * (double)eps[i * lde + j];
+      dmean[i * A + j] = (float)((alpha * dlogp_du - dq * oma) * inv_n);
+      t = (alpha * (-1.0 + dlogp_du * du_dls) - dq * oma * du_dls) * inv_n;
+    }
+    const double r = block_sum(t, scratch);
+    if (threadIdx.x == 0) pp[j] = r;
+  }
+  if (!last_block_ticket(ticket, gridDim.x)) return;
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += part[(int64_t)b * A + j];
+    dls_out[j] = (float)s;
+  }
+}
+
+// ScalarAdam on log_alpha (R:algos/sac.py:35-53, :224-229, :245-249)
+__global__ void alpha_step_kernel(ul_sac_ctl* ctl, int64_t n, double target_entropy) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double excess = ctl->logp_sum / (double)n + target_entropy;
+  const double la = ctl->log_alpha;
+  ctl->alpha_loss = -la * excess;
+  const double g = -excess;
+  if (!isfinite(g)) {
+    ctl->diverged = 1;
+    return;
+  }
+  ctl->a_t += 1.0;
+  const double b1 = 0.9, b2 = 0.999;
+  ctl->a_m = b1 * ctl->a_m + (1.0 - b1) * g;
+  ctl->a_v = b2 * ctl->a_v + (1.0 - b2) * g * g;
+  const double mh = ctl->a_m / (1.0 - pow(b1, ctl->a_t));
+  const double vh = ctl->a_v / (1.0 - pow(b2, ctl->a_t));
+  ctl->log_alpha = la - ctl->alpha_lr * mh / (sqrt(vh) + 1e-8);
+}
+
+// device standard normals (performance mode): Philox4x32-10 + Box-Muller
+__device__ __forceinline__ void philox(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t h0 = (uint32_t)(p0 >> 32), l0 = (uint32_t)p0;
+    const uint32_t h1 = (uint32_t)(p1 >> 32), l1 = (uint32_t)p1;
+    c[0] = h1 ^ c[1] ^ k0;
+    c[1] = l1;
+    c[2] = h0 ^ c[3] ^ k1;
+    c[3] = l0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__global__ void normal_kernel(float* out, int64_t n, uint64_t key, uint64_t counter) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q * 4 < n; q += stride) {
+    uint32_t c[4] = {(uint32_t)q, (uint32_t)(q >> 32), (uint32_t)counter,
+                     (uint32_t)(counter >> 32)};
+    philox(c, (uint32_t)key, (uint32_t)(key >> 32));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float u1 = ((float)c[2 * h] + 1.0f) * 2.3283064e-10f;  // (0, 1]
+      const float u2 = (float)c[2 * h + 1] * 2.3283064e-10f;
+      const float rr = sqrtf(-2.f * logf(u1));
+      float s, co;
+      sincospif(2.f * u2, &s, &co);
+      const int64_t o = q * 4 + 2 * h;
+      if (o < n) out[o] = rr * co;
+      if (o + 1 < n) out[o + 1] = rr * s;
+    }
+  }
+}
+
+int grid_for(int64_t n) {
+  int64_t b = ceil_div(n > 0 ? n : 1, 256);
+  return (int)(b > 8 * kNumSMs ? 8 * kNumSMs : b);
+}
+
+// ------------------------------------------------------------------- plan
+struct SacPlan {
+  ul_sac_plan_desc d{};
+  NetView va{}, vq{};
+  int D = 0, A = 0;
+  int64_t B = 0, ldq = 0, ldo = 0, Pa = 0, Pq = 0;
+  char* arena = nullptr;
+  float *qin = nullptr, *qn = nullptr, *qa = nullptr, *obs = nullptr, *rew = nullptr,
+        *term = nullptr, *nused = nullptr;
+  float *acts_a = nullptr, *acts_q1 = nullptr, *acts_q2 = nullptr;
+  float *mean = nullptr, *a_pi = nullptr, *logp = nullptr, *q1o = nullptr, *q2o = nullptr,
+        *q1t = nullptr, *q2t = nullptr, *dq1 = nullptr, *dq2 = nullptr, *din1 = nullptr,
+        *din2 = nullptr, *dmean = nullptr;
+  double* y = nullptr;
+  float *g_a = nullptr, *g_q1 = nullptr, *g_q2 = nullptr, *work = nullptr;
+  float *ws_a = nullptr, *ws_q1 = nullptr, *ws_q2 = nullptr, *ws_q1t = nullptr, *ws_q2t = nullptr;
+  float *eps = nullptr;  // [2, B, A] device noise
+  double* part = nullptr;
+  unsigned int* tickets = nullptr;
+  ul_opt_ctl *oc_a = nullptr, *oc_q1 = nullptr, *oc_q2 = nullptr;
+  ul_opt_ctl* oc_h = nullptr;  // pinned staging
+  ul_sac_ctl* ctl = nullptr;
+  ul_sac_ctl* ctl_h = nullptr;
+  ul_sac_bindings b{};
+  bool bound = false;
+};
+
+int alloc_sac(SacPlan* p) {
+  size_t off = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const int64_t B = p->B;
+  const int64_t wa = bwd_work_floats(p->va, B), wq = bwd_work_floats(p->vq, B);
+  size_t o[40];
+  int k = 0;
+  o[k++] = carve(4 * B * p->ldq);                 // 0 qin
+  o[k++] = carve(4 * B * p->ldq);                 // 1 qn
+  o[k++] = carve(4 * B * p->ldq);                 // 2 qa
+  o[k++] = carve(4 * B * p->ldo);                 // 3 obs
+  o[k++] = carve(4 * B);                          // 4 rew
+  o[k++] = carve(4 * B);                          // 5 term
+  o[k++] = carve(4 * B);                          // 6 nused
+  o[k++] = carve(4 * act_floats(p->va, B));       // 7
+  o[k++] = carve(4 * act_floats(p->vq, B));       // 8
+  o[k++] = carve(4 * act_floats(p->vq, B));       // 9
+  o[k++] = carve(4 * B * p->A);                   // 10 mean
+  o[k++] = carve(4 * B * p->A);                   // 11 a_pi
+  o[k++] = carve(4 * B);                          // 12 logp
+  o[k++] = carve(4 * B);                          // 13 q1o
+  o[k++] = carve(4 * B);                          // 14 q2o
+  o[k++] = carve(4 * B);                          // 15 q1t
+  o[k++] = carve(4 * B);                          // 16 q2t
+  o[k++] = carve(4 * B);                          // 17 dq1
+  o[k++] = carve(4 * B);                          // 18 dq2
+  o[k++] = carve(4 * B * p->A);                   // 19 din1
+  o[k++] = carve(4 * B * p->A);                   // 20 din2
+  o[k++] = carve(4 * B * p->A);                   // 21 dmean
+  o[k++] = carve(8 * B);                          // 22 y
+  o[k++] = carve(4 * (p->Pa + 8));                // 23 g_a
+  o[k++] = carve(4 * (p->Pq + 8));                // 24 g_q1
+  o[k++] = carve(4 * (p->Pq + 8));                // 25 g_q2
+  o[k++] = carve(4 * (wa > wq ? wa : wq));        // 26 work
+  o[k++] = carve(4 * p->va.wp_total);             // 27
+  o[k++] = carve(4 * p->vq.wp_total);             // 28
+  o[k++] = carve(4 * p->vq.wp_total);             // 29
+  o[k++] = carve(4 * p->vq.wp_total);             // 30
+  o[k++] = carve(4 * p->vq.wp_total);             // 31
+  o[k++] = carve(4 * 2 * B * p->A);               // 32 eps
+  o[k++] = carve(8 * (ceil_div(B, 256) * (UL_MAX_ACT + 2) + 64));  // 33 part
+  o[k++] = carve(4 * 16);                         // 34 tickets
+  o[k++] = carve(sizeof(ul_opt_ctl));             // 35
+  o[k++] = carve(sizeof(ul_opt_ctl));             // 36
+  o[k++] = carve(sizeof(ul_opt_ctl));             // 37
+  o[k++] = carve(sizeof(ul_sac_ctl));             // 38
+  UL_CUDA(cudaMalloc(&p->arena, off));
+  UL_CUDA(cudaMemset(p->arena, 0, off));
+  char* a = p->arena;
+  float** fp[] = {&p->qin, &p->qn, &p->qa, &p->obs, &p->rew, &p->term, &p->nused, &p->acts_a,
+                  &p->acts_q1, &p->acts_q2, &p->mean, &p->a_pi, &p->logp, &p->q1o, &p->q2o,
+                  &p->q1t, &p->q2t, &p->dq1, &p->dq2, &p->din1, &p->din2, &p->dmean};
+  for (int i = 0; i < 22; ++i) *fp[i] = (float*)(a + o[i]);
+  p->y = (double*)(a + o[22]);
+  p->g_a = (float*)(a + o[23]);
+  p->g_q1 = (float*)(a + o[24]);
+  p->g_q2 = (float*)(a + o[25]);
+  p->work = (float*)(a + o[26]);
+  p->ws_a = (float*)(a + o[27]);
+  p->ws_q1 = (float*)(a + o[28]);
+  p->ws_q2 = (float*)(a + o[29]);
+  p->ws_q1t = (float*)(a + o[30]);
+  p->ws_q2t = (float*)(a + o[31]);
+  p->eps = (float*)(a + o[32]);
+  p->part = (double*)(a + o[33]);
+  p->tickets = (unsigned int*)(a + o[34]);
+  p->oc_a = (ul_opt_ctl*)(a + o[35]);
+  p->oc_q1 = (ul_opt_ctl*)(a + o[36]);
+  p->oc_q2 = (ul_opt_ctl*)(a + o[37]);
+  p->ctl = (ul_sac_ctl*)(a + o[38]);
+  UL_CUDA(cudaHostAlloc(&p->oc_h, sizeof(ul_opt_ctl), cudaHostAllocPortable));
+  UL_CUDA(cudaHostAlloc(&p->ctl_h, sizeof(ul_sac_ctl), cudaHostAllocPortable));
+  return UL_OK;
+}
+
+void free_sac(SacPlan* p) {
+  if (p->arena) cudaFree(p->arena);
+  if (p->oc_h) cudaFreeHost(p->oc_h);
+  if (p->ctl_h) cudaFreeHost(p->ctl_h);
+}
+
+size_t ctl_hdr() { return offsetof(ul_opt_ctl, part); }
+
+int adam_one(SacPlan* p, float* params, float* grads, float* m, float* v, int64_t n,
+             ul_opt_ctl* oc, cudaStream_t s) {
+  SegTable st{};
+  st.nseg = 1;
+  st.g[0] = grads;
+  st.p[0] = params;
+  st.m[0] = m;
+  st.v[0] = v;
+  st.n[0] = n;
+  UL_TRY(launch_prepare(st, oc, s));
+  return launch_apply(st, oc, 0, 1, s);
+}
+
+}  // namespace
+}  // namespace ul
+
+using ul::SacPlan;
+
+extern "C" int ul_sac_plan_create(const ul_sac_plan_desc* desc, void** plan) {
+  UL_CHECK_ARG(desc && plan, "sac plan: null argument");
+  SacPlan* p = new (std::nothrow) SacPlan();
+  UL_CHECK_ARG(p, "sac plan: out of host memory");
+  p->d = *desc;
+  int st = ul::make_view(&desc->actor, &p->va);
+  if (st == UL_OK) st = ul::make_view(&desc->critic, &p->vq);
+  if (st != UL_OK) {
+    delete p;
+    return st;
+  }
+  p->D = desc->obs_dim;
+  p->A = desc->act_dim;
+  p->B = desc->batch;
+  auto fail = [&](const char* m) {
+    ul::set_error("%s", m);
+    delete p;
+    return UL_ERR_VALUE;
+  };
+  if (p->B < 2) return fail("sac_update needs a batch of at least 2 rows");
+  if (p->va.dims[0] != p->D || p->va.dims[p->va.n_layers] != p->A)
+    return fail("sac plan: actor dims do not match obs/act");
+  if (p->vq.dims[0] != p->D + p->A || p->vq.dims[p->vq.n_layers] != 1)
+    return fail("sac plan: critic must map obs+act -> 1");
+  if (p->A > UL_MAX_ACT) return fail("sac plan: action dim above UL_MAX_ACT");
+  p->ldq = ul::act_ld(p->D + p->A);
+  p->ldo = ul::act_ld(p->D);
+  p->Pa = p->va.total;
+  p->Pq = p->vq.total;
+  st = ul::alloc_sac(p);
+  if (st != UL_OK) {
+    ul::free_sac(p);
+    delete p;
+    return st;
+  }
+  *plan = p;
+  return UL_OK;
+}
+
+extern "C" int ul_sac_plan_destroy(void* plan) {
+  SacPlan* p = (SacPlan*)plan;
+  if (!p) return UL_OK;
+  ul::free_sac(p);
+  delete p;
+  return UL_OK;
+}
+
+extern "C" int ul_sac_plan_bind(void* plan, const ul_sac_bindings* b) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && b, "sac plan: null argument");
+  p->b = *b;
+  p->bound = true;
+  return UL_OK;
+}
+
+// Load a batch of codec rows (obs | act | r | next_obs | term | n_used):
+// rows[idx[i] % modulo] for device ring rows (idx may be NULL for rows 0..B-1).
+extern "C" int ul_sac_plan_load_rows(void* plan, const float* rows, int64_t pitch,
+                                     const int64_t* idx, int64_t modulo, int64_t lo, int64_t hi,
+                                     int* err, void* stream) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p, "sac plan: null");
+  const int64_t D = p->D, A = p->A;
+  const int64_t width = 2 * D + A + 3;
+  UL_CHECK_ARG(pitch >= width, "sac plan: row pitch below codec width");
+  const char* r = (const char*)rows;
+  const void* src[7] = {r, r, r, r + 4 * (D + A + 1), r + 4 * (D + A), r + 4 * (2 * D + A + 1),
+                        r + 4 * (2 * D + A + 2)};
+  void* dst[7] = {p->qin, p->obs, p->qa, p->qn, p->rew, p->term, p->nused};
+  const int64_t ps = 4 * pitch;
+  const int64_t sst[7] = {ps, ps, ps, ps, ps, ps, ps};
+  const int64_t dstr[7] = {4 * p->ldq, 4 * p->ldo, 4 * p->ldq, 4 * p->ldq, 4, 4, 4};
+  // critic input [obs | act] and actor input obs each carry one extra column
+  // overwritten with 1.0: the bias column of the tensor-core dW
+  const int64_t rb[7] = {4 * (D + A + 1), 4 * (D + 1), 4 * D, 4 * D, 4, 4, 4};
+  const int64_t ones[7] = {4 * (D + A), 4 * D, -1, -1, -1, -1, -1};
+  return ul_gather_rows(7, src, dst, sst, dstr, rb, ones, idx, p->B, modulo, lo, hi, err, stream);
+}
+
+// Upload the optimizer / alpha control state (host values -> device).
+extern "C" int ul_sac_plan_begin(void* plan, const ul_sac_ctl* host_ctl, const double* lrs,
+                                 const int64_t* ts, void* stream) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && p->bound && host_ctl && lrs && ts, "sac plan: not bound");
+  cudaStream_t s = ul::as_stream(stream);
+  *p->ctl_h = *host_ctl;
+  UL_CUDA(cudaMemcpyAsync(p->ctl, p->ctl_h, sizeof(ul_sac_ctl), cudaMemcpyHostToDevice, s));
+  ul_opt_ctl* dst[3] = {p->oc_a, p->oc_q1, p->oc_q2};
+  for (int k = 0; k < 3; ++k) {
+    const double lr = lrs[k];
+    UL_TRY(ul_opt_ctl_init(p->oc_h, 1, &lr, 0.9, 0.999, 1e-8, p->d.max_grad_norm));
+    p->oc_h->t[0] = ts[k];
+    UL_CUDA(cudaMemcpyAsync(dst[k], p->oc_h, ul::ctl_hdr(), cudaMemcpyHostToDevice, s));
+    UL_CUDA(cudaStreamSynchronize(s));  // pinned staging reused for the next record
+  }
+  return UL_OK;
+}
+
+// Fill the two noise blocks [2, B, A] on device (performance mode).
+extern "C" int ul_sac_plan_device_noise(void* plan, uint64_t key, uint64_t counter,
+                                        void* stream) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p, "sac plan: null");
+  const int64_t n = 2 * p->B * p->A;
+  ul::normal_kernel<<<ul::grid_for(ul::ceil_div(n, 4)), 256, 0, ul::as_stream(stream)>>>(
+      p->eps, n, key, counter);
+  return ul::check_launch("normal_kernel");
+}
+
+extern "C" int ul_sac_plan_noise_ptr(void* plan, float** eps) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && eps, "sac plan: null");
+  *eps = p->eps;
+  return UL_OK;
+}
+
+// One sac_update (R:algos/sac.py:139-178).  do_actor: update_count %
+// policy_frequency == 0 after the increment.
+extern "C" int ul_sac_plan_update(void* plan, int do_actor, void* stream) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "sac plan: not bound");
+  cudaStream_t s = ul::as_stream(stream);
+  const ul_sac_bindings& b = p->b;
+  const int be = p->d.gemm_backend;
+  const int64_t B = p->B, D = p->D, A = p->A;
+  const float* ls = b.actor + p->va.logstd_off;
+  if (be == 1) {
+    UL_TRY(ul::stage_weights(p->va, b.actor, p->ws_a, s));
+    UL_TRY(ul::stage_weights(p->vq, b.q1, p->ws_q1, s));
+    UL_TRY(ul::stage_weights(p->vq, b.q2, p->ws_q2, s));
+    UL_TRY(ul::stage_weights(p->vq, b.q1t, p->ws_q1t, s));
+    UL_TRY(ul::stage_weights(p->vq, b.q2t, p->ws_q2t, s));
+  }
+  // ---- K10 target
+  UL_TRY(ul::mlp_forward(p->va, b.actor, p->ws_a, be, p->qn, p->ldq, B, p->acts_a, p->mean, A, s));
+  ul::squash_kernel<<<ul::grid_for(B), 256, 0, s>>>(p->mean, A, ls, p->eps, A, B, (int)A, p->qn,
+                                                   p->ldq, (int)D, nullptr, p->logp);
+  UL_TRY(ul::check_launch("squash_kernel"));
+  UL_TRY(ul::mlp_forward(p->vq, b.q1t, p->ws_q1t, be, p->qn, p->ldq, B, p->acts_q1, p->q1t, 1, s));
+  UL_TRY(ul::mlp_forward(p->vq, b.q2t, p->ws_q2t, be, p->qn, p->ldq, B, p->acts_q2, p->q2t, 1, s));
+  ul::sac_target_kernel<<<ul::grid_for(B), 256, 0, s>>>(p->rew, p->term, p->nused, p->q1t,
+                                                       p->q2t, p->logp, p->ctl, p->d.gamma, B,
+                                                       p->y);
+  UL_TRY(ul::check_launch("sac_target_kernel"));
+  // ---- K11 critics (ones column of qin at D+A feeds the tensor-core db)
+  UL_TRY(ul::mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, B, p->acts_q1, p->q1o, 1, s));
+  UL_TRY(ul::mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  const unsigned nb = (unsigned)ul::ceil_div(B, 256);
+  ul::critic_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->y, B, 1.0 / (double)B, p->dq1,
+                                            p->dq2, p->part, p->tickets, p->ctl);
+  UL_TRY(ul::check_launch("critic_head_kernel"));
+  UL_TRY(ul::mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, true, B, p->acts_q1,
+                          p->dq1, 1, p->g_q1, nullptr, 0, 0, 0, true, true, p->work, s));
+  UL_TRY(ul::adam_one(p, b.q1, p->g_q1, b.q1_m, b.q1_v, p->Pq, p->oc_q1, s));
+  UL_TRY(ul::mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, true, B, p->acts_q2,
+                          p->dq2, 1, p->g_q2, nullptr, 0, 0, 0, true, true, p->work, s));
+  UL_TRY(ul::adam_one(p, b.q2, p->g_q2, b.q2_m, b.q2_v, p->Pq, p->oc_q2, s));
+  if (do_actor) {
+    // ---- actor + alpha (critics already updated, R:algos/sac.py:232-249)
+    if (be == 1) {
+      UL_TRY(ul::stage_weights(p->vq, b.q1, p->ws_q1, s));
+      UL_TRY(ul::stage_weights(p->vq, b.q2, p->ws_q2, s));
+    }
+    const float* eps2 = p->eps + B * A;
+    UL_TRY(ul::mlp_forward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, B, p->acts_a, p->mean, A, s));
+    ul::squash_kernel<<<ul::grid_for(B), 256, 0, s>>>(p->mean, A, ls, eps2, A, B, (int)A, p->qa,
+                                                     p->ldq, (int)D, p->a_pi, p->logp);
+    UL_TRY(ul::check_launch("squash_kernel"));
+    UL_TRY(ul::mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, B, p->acts_q1, p->q1o, 1, s));
+    UL_TRY(ul::mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+    ul::pick_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->logp, B, p->dq1, p->dq2, p->part,
+                                            p->tickets + 1, p->ctl);
+    UL_TRY(ul::check_launch("pick_head_kernel"));
+    // dQ/da through each critic's input gradient, action columns only
+    UL_TRY(ul::mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, false, B, p->acts_q1,
+                            p->dq1, 1, nullptr, p->din1, A, (int)D, (int)A, false, false, p->work,
+                            s));
+    UL_TRY(ul::mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, false, B, p->acts_q2,
+                            p->dq2, 1, nullptr, p->din2, A, (int)D, (int)A, false, false, p->work,
+                            s));
+    ul::actor_head_kernel<<<nb, 256, 0, s>>>(p->a_pi, eps2, A, p->din1, p->din2, A, ls, B, (int)A,
+                                             p->ctl, p->dmean, p->part, p->tickets + 2,
+                                             p->g_a + p->va.logstd_off);
+    UL_TRY(ul::check_launch("actor_head_kernel"));
+    UL_TRY(ul::mlp_backward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, true, B, p->acts_a,
+                            p->dmean, A, p->g_a, nullptr, 0, 0, 0, true, false, p->work, s));
+    UL_TRY(ul::adam_one(p, b.actor, p->g_a, b.actor_m, b.actor_v, p->Pa, p->oc_a, s));
+    ul::alpha_step_kernel<<<1, 32, 0, s>>>(p->ctl, B, p->d.target_entropy);
+    UL_TRY(ul::check_launch("alpha_step_kernel"));
+  }
+  // ---- K12 Polyak (R:algos/sac.py:176-177)
+  UL_TRY(ul_polyak(b.q1t, b.q1, p->Pq, p->d.tau, stream));
+  UL_TRY(ul_polyak(b.q2t, b.q2, p->Pq, p->d.tau, stream));
+  return UL_OK;
+}
+
+// Read back the control records; UL_ERR_DIVERGENCE if an Adam step or the
+// critic / actor loss saw non-finite values.
+extern "C" int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, void* stream) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && out && ts, "sac plan: null");
+  cudaStream_t s = ul::as_stream(stream);
+  UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl, sizeof(ul_sac_ctl), cudaMemcpyDeviceToHost, s));
+  ul_opt_ctl* srcs[3] = {p->oc_a, p->oc_q1, p->oc_q2};
+  int bad = 0;
+  for (int k = 0; k < 3; ++k) {
+    UL_CUDA(cudaMemcpyAsync(p->oc_h, srcs[k], ul::ctl_hdr(), cudaMemcpyDeviceToHost, s));
+    UL_CUDA(cudaStreamSynchronize(s));
+    ts[k] = p->oc_h->t[0];
+    bad |= p->oc_h->diverged;
+  }
+  *out = *p->ctl_h;
+  if (bad || out->diverged || !isfinite(out->critic_loss)) {
+    ul::set_error("non-finite SAC loss or gradients");
+    return UL_ERR_DIVERGENCE;
+  }
+  return UL_OK;
+}

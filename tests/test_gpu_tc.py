@@ -129,7 +129,7 @@ def test_ppo_update_tf32_cfg2_vs_oracle():
     seconds) on the tensor-core path vs the f32 oracle with the same
     permutation stream: parameter deltas within the bf16/tf32 tolerance."""
     from oracle.port import philox_stream
-    from tests.test_gpu_ppo import _synthetic
+    from helpers import _synthetic
 
     T, N = 24, 1024
     segd, actor, critic = _synthetic(T, N, 235, 235, 12, (512, 256, 128), seed=9)
