@@ -1,0 +1,215 @@
+"""Cross-role synchronisation for a device learner (mirror of R:runtime/sync.py).
+
+``WeightSlot.publish`` is the learner -> collector weight handoff
+(R:runtime/sync.py:25-63): the flat HBM parameter
+vector is copied D2H into a pooled page-locked buffer and exposed to the
+(host, numpy) collector as a frozen reference-compatible record (``layers``,
+``log_std``, ``arch``, ``version``), so the reference's own SegmentCollector
+/ SAC collector can run inference on it unchanged.  Buffers are recycled only
+after every reader has dropped the snapshot (weakref), so a reader never sees
+a torn or overwritten version.
+"""
+
+from __future__ import annotations
+
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from .. import _dev, _lib
+from ..errors import PipelineStall
+from ..trace import Tracer, now_ns
+
+DEADLOCK_TIMEOUT_S = 10.0
+
+
+class HostParams:
+    """Read-only host snapshot of a device ModelParams (numpy views into a
+    pinned buffer); duck-compatible with the reference ModelParams."""
+
+    def __init__(self, buf: np.ndarray, arch, version: int):
+        self._buf = buf
+        self.arch = arch
+        self.version = version
+        layers, off = [], 0
+        for out_dim, in_dim in arch.layer_dims:
+            w = buf[off:off + out_dim * in_dim].reshape(out_dim, in_dim)
+            off += out_dim * in_dim
+            b = buf[off:off + out_dim]
+            off += out_dim
+            layers.append((w, b))
+        self.layers = layers
+        self.log_std = buf[off:off + arch.output_dim]
+
+    def flat(self) -> np.ndarray:
+        return self._buf.copy()
+
+    def copy(self) -> "HostParams":
+        return HostParams(self._buf.copy(), self.arch, self.version)
+
+
+@dataclass
+class HostAcParams:
+    actor: HostParams
+    critic: HostParams
+
+    def copy(self) -> "HostAcParams":
+        return HostAcParams(self.actor.copy(), self.critic.copy())
+
+
+class _PinnedPool:
+    def __init__(self):
+        self._free: dict[int, list] = {}
+        self._lock = threading.Lock()
+
+    def take(self, n: int) -> np.ndarray:
+        with self._lock:
+            lst = self._free.get(n)
+            if lst:
+                return lst.pop()
+        return _dev.pinned_empty((n,), np.float32)
+
+    def give(self, arr: np.ndarray) -> None:
+        with self._lock:
+            self._free.setdefault(arr.size, []).append(arr)
+
+
+def _snapshot(params, pool: _PinnedPool, version: int, stream: int) -> HostParams:
+    n = params.buf.numel()
+    buf = pool.take(n)
+    _lib.call("ul_memcpy_async", buf.ctypes.data, _dev.ptr(params.buf), n * 4, stream)
+    _lib.call("ul_stream_sync", stream)
+    view = buf[:]
+    view.setflags(write=False)
+    snap = HostParams(view, params.arch, version)
+    weakref.finalize(snap, pool.give, buf)
+    for w, b in snap.layers:
+        w.setflags(write=False)
+        b.setflags(write=False)
+    snap.log_std.setflags(write=False)
+    return snap
+
+
+class WeightSlot:
+    """Single-writer weight handoff with strictly increasing versions."""
+
+    def __init__(self, tracer: Tracer | None = None):
+        self._tracer = tracer if tracer is not None else Tracer(enabled=False)
+        self._lock = threading.Lock()
+        self._pair = None
+        self._pool = _PinnedPool()
+        self.publish_timestamp = 0
+
+    @property
+    def version(self) -> int:
+        pair = self._pair
+        return 0 if pair is None else pair[0]
+
+    def publish(self, params, track: str = "learner") -> int:
+        """D2H snapshot + atomic swap; returns the new version."""
+        with self._tracer.span(track, "learner/weight_sync_write") as args:
+            with self._lock:
+                version = self.version + 1
+                s = _dev.stream()
+                if hasattr(params, "actor") and hasattr(params, "critic") \
+                        and not hasattr(params, "q1"):
+                    snap = HostAcParams(_snapshot(params.actor, self._pool, version, s),
+                                        _snapshot(params.critic, self._pool, version, s))
+                else:
+                    snap = _snapshot(params, self._pool, version, s)
+                self._pair = (version, snap)
+                self.publish_timestamp = now_ns()
+            args["version"] = version
+        return version
+
+    def fetch(self, track: str = "collector"):
+        with self._tracer.span(track, "collector/weight_read") as args:
+            pair = self._pair
+            if pair is None:
+                raise RuntimeError("fetch_weights before first publish")
+            args["version"] = pair[0]
+        return pair
+
+
+def publish_weights(slot: WeightSlot, params) -> int:
+    return slot.publish(params)
+
+
+def fetch_weights(slot: WeightSlot):
+    return slot.fetch()
+
+
+class RolloutRing:
+    """Bounded SPSC FIFO of rollout segments (R:runtime/sync.py:74-137)."""
+
+    def __init__(self, capacity: int):
+        if capacity < 1:
+            raise ValueError("ring capacity must be >= 1")
+        self.capacity = capacity
+        self._items: list = []
+        self._cond = threading.Condition()
+
+    def __len__(self) -> int:
+        with self._cond:
+            return len(self._items)
+
+    def _block(self, pred, stop, what: str, tracer, track, name) -> bool:
+        t0 = now_ns()
+        waited = False
+        while not pred():
+            waited = True
+            if stop is not None and stop.is_set():
+                return False
+            if not self._cond.wait(timeout=0.05) and (now_ns() - t0) / 1e9 > DEADLOCK_TIMEOUT_S:
+                raise PipelineStall(f"{what} for {DEADLOCK_TIMEOUT_S}s")
+        if waited and tracer is not None:
+            tracer.record(track, name, t0, now_ns())
+        return True
+
+    def put(self, segment, stop=None, tracer: Tracer | None = None) -> bool:
+        with self._cond:
+            ok = self._block(lambda: len(self._items) < self.capacity, stop,
+                             f"collector blocked on full ring (capacity {self.capacity})",
+                             tracer, "collector", "collector/stall")
+            if not ok:
+                return False
+            self._items.append(segment)
+            self._cond.notify_all()
+        return True
+
+    def get(self, stop=None, tracer: Tracer | None = None):
+        with self._cond:
+            ok = self._block(lambda: len(self._items) > 0, stop,
+                             "learner blocked on empty ring", tracer, "learner", "learner/gap")
+            if not ok:
+                return None
+            item = self._items.pop(0)
+            self._cond.notify_all()
+        return item
+
+
+@dataclass
+class RoleError:
+    exc: BaseException
+    role: str
+
+
+class ErrorBox:
+    """First background-role exception, re-raised in the learner (R:runtime/sync.py:140-162)."""
+
+    def __init__(self):
+        self._error = None
+        self._lock = threading.Lock()
+
+    def set(self, role: str, exc: BaseException) -> None:
+        with self._lock:
+            if self._error is None:
+                self._error = RoleError(exc=exc, role=role)
+
+    def raise_if_set(self) -> None:
+        with self._lock:
+            err = self._error
+        if err is not None:
+            raise RuntimeError(f"{err.role} role failed: {err.exc!r}") from err.exc
