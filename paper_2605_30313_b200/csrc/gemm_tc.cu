@@ -20,7 +20,6 @@ namespace ul {
 namespace tc {
 
 constexpr int BM = 128, BK = 32;  // BK fp32 = 128 B = one swizzle row
-constexpr int kThreads = 192;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -112,6 +111,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
 struct TcArgs {
   int M, N, K;
   int k_per_split;  // multiple of BK
+  int mt, nt, zt;   // tile counts (M, N, K-split)
   float* C;
   int64_t ldc;
   const float* bias;
@@ -127,42 +127,52 @@ struct Smem {
   static constexpr int kABytes = BM * BK * 4;  // 16 KB
   static constexpr int kBBytes = BN * BK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
+                                2 * BN * 4 /*bias, double-buffered by accumulator*/;
 };
 
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each half the columns
+constexpr int kPThreads = (2 + kEpiWarps) * 32;
+
+// Persistent: grid = min(#tiles, #SMs); tile t = blockIdx.x + i * gridDim.x
+// walks (m, n, split) tiles.  The smem ring runs continuously across tiles and
+// the TMEM accumulator is double-buffered, so tile i's epilogue overlaps tile
+// i+1's TMA + MMA main loop.
 template <bool A_MN, bool B_MN, int EPI, int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    TcArgs p) {
   using S = Smem<BN>;
   constexpr int kStages = S::kStages;
+  constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + kStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int kb = blockIdx.z * p.k_per_split;
-  const int ke = min(p.K, kb + p.k_per_split);
-  const int ktiles = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  const int ntiles = p.mt * p.nt * p.zt;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
-                 "r"(BN < 32 ? 32 : BN));
+                 "r"(kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -170,27 +180,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  auto tile_coords = [&](int t, int& m0, int& n0, int& z) {
+    z = t / (p.mt * p.nt);
+    const int r = t - z * p.mt * p.nt;
+    n0 = (r / p.mt) * BN;  // M-fastest: neighbouring CTAs share the B (weight) tile
+    m0 = (r % p.mt) * BM;
+  };
+  auto k_tiles = [&](int z) {
+    const int kb = z * p.k_per_split;
+    const int ke = min(p.K, kb + p.k_per_split);
+    return ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % kStages;
-        mbar_wait(&empty[s], ((kt / kStages) & 1) ^ 1);
-        uint8_t* sa = smem + s * S::kStageBytes;
-        uint8_t* sb = sa + S::kABytes;
-        mbar_expect_tx(&full[s], S::kStageBytes);
-        const int k0 = kb + kt * BK;
-        if (A_MN) {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, n0, z;
+        tile_coords(t, m0, n0, z);
+        const int kt_n = k_tiles(z);
+        for (int kt = 0; kt < kt_n; ++kt, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          uint8_t* sa = smem + s * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          mbar_expect_tx(&full[s], S::kStageBytes);
+          const int k0 = z * p.k_per_split + kt * BK;
+          if (A_MN) {
 #pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_2d(sa + c * 4096, &tmA, &full[s], m0 + 32 * c, k0);
-        } else {
-          tma_load_2d(sa, &tmA, &full[s], k0, m0);
-        }
-        if (B_MN) {
+            for (int c = 0; c < BM / 32; ++c)
+              tma_load_2d(sa + c * 4096, &tmA, &full[s], m0 + 32 * c, k0);
+          } else {
+            tma_load_2d(sa, &tmA, &full[s], k0, m0);
+          }
+          if (B_MN) {
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) tma_load_2d(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0);
-        } else {
-          tma_load_2d(sb, &tmB, &full[s], k0, n0);
+            for (int c = 0; c < BN / 32; ++c)
+              tma_load_2d(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0);
+          } else {
+            tma_load_2d(sb, &tmB, &full[s], k0, n0);
+          }
         }
       }
     }
@@ -201,74 +231,126 @@ __global__ void __launch_bounds__(kThreads, 1)
                            ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
-      for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % kStages;
-        mbar_wait(&full[s], (kt / kStages) & 1);
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        int m0, n0, z;
+        tile_coords(t, m0, n0, z);
+        const int kt_n = k_tiles(z);
+        const int b = local & 1;
+        mbar_wait(&acc_empty[b], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a_base = su32(smem + s * S::kStageBytes);
-        const uint32_t b_base = a_base + S::kABytes;
+        const uint32_t acc = tmem + (uint32_t)(b * BN);
+        for (int kt = 0; kt < kt_n; ++kt, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a_base = su32(smem + s * S::kStageBytes);
+          const uint32_t b_base = a_base + S::kABytes;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          // K-major: 8-row x 128 B swizzle atoms (SBO 1024), K step = +32 B.
-          // MN-major: 128 B of M/N per row, 4-row x 128 B atoms with 32 B
-          // swizzle granules (SBO 512), 32-element M/N chunks 4 KB apart
-          // (LBO), K step = 8 rows = +1024 B.
-          const uint64_t da = A_MN ? smem_desc(a_base + kk * 1024, 4096, 512, 1)
-                                   : smem_desc(a_base + kk * 32, 16, 1024, 2);
-          const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 512, 1)
-                                   : smem_desc(b_base + kk * 32, 16, 1024, 2);
-          mma_tf32(tmem, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // K-major: 8-row x 128 B swizzle atoms (SBO 1024), K step = +32 B.
+            // MN-major: 128 B of M/N per row, 4-row x 128 B atoms with 32 B
+            // swizzle granules (SBO 512), 32-element M/N chunks 4 KB apart
+            // (LBO), K step = 8 rows = +1024 B.
+            const uint64_t da = A_MN ? smem_desc(a_base + kk * 1024, 4096, 512, 1)
+                                     : smem_desc(a_base + kk * 32, 16, 1024, 2);
+            const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 512, 1)
+                                     : smem_desc(b_base + kk * 32, 16, 1024, 2);
+            mma_tf32(acc, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        mma_commit(&acc_full[b]);  // accumulator b complete
       }
-      mma_commit(done);  // accumulator complete
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;
+    const int ew = warp - 2;
+    const int quarter = warp & 3;         // TMEM lane quarter this warp may access
+    const int half = ew >> 2;             // column half
     const int row = quarter * 32 + lane;
-    const int m = m0 + row;
-    if (ktiles > 0) mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    float* C = p.C + (int64_t)blockIdx.z * p.split_stride;
-    const bool vec = (p.ldc % 4 == 0);
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      if (ktiles > 0) {
-        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0, v);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    constexpr int kHalf = BN / 2;
+    float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+    int local = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      int m0, n0, z;
+      tile_coords(t, m0, n0, z);
+      const int b = local & 1;
+      const bool have = k_tiles(z) > 0;
+      if (EPI == kEpiBias || EPI == kEpiBiasElu) {
+        // stage this tile's bias slice (each epilogue warp loads its own half)
+        for (int c = lane; c < kHalf; c += 32) {
+          const int n = n0 + half * kHalf + c;
+          sbias[b * BN + half * kHalf + c] = n < p.N ? __ldg(p.bias + n) : 0.f;
+        }
+        __syncwarp();
       }
-      if (m >= p.M || n0 + c0 >= p.N) continue;
+      if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + row;
+      float* C = p.C + (int64_t)z * p.split_stride;
+      const bool full_rows = (n0 + BN <= p.N) && (p.ldc % 4 == 0);
+#pragma unroll 1
+      for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 16) {
+        float v[16];
+        if (have) {
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN + c0), v);
+        } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int n = n0 + c0 + i;
-        if (n < p.N) {
-          if (EPI == kEpiBias || EPI == kEpiBiasElu) v[i] += __ldg(p.bias + n);
-          if (EPI == kEpiBiasElu) v[i] = elu_f(v[i]);
-          if (EPI == kEpiEluGrad) v[i] *= elu_grad_from_act(__ldg(p.aux + (int64_t)m * p.ldaux + n));
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (m >= p.M || n0 + c0 >= p.N) continue;
+        if (EPI == kEpiBias || EPI == kEpiBiasElu) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += sbias[b * BN + c0 + i];
+        }
+        if (EPI == kEpiBiasElu) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = elu_f(v[i]);
+        }
+        float* dst = C + (int64_t)m * p.ldc + n0 + c0;
+        if (EPI == kEpiEluGrad) {
+          const float* ax = p.aux + (int64_t)m * p.ldaux + n0 + c0;
+          if (full_rows && (p.ldaux % 4 == 0)) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const float4 h4 = __ldg(reinterpret_cast<const float4*>(ax + i));
+              v[i] *= elu_grad_from_act(h4.x);
+              v[i + 1] *= elu_grad_from_act(h4.y);
+              v[i + 2] *= elu_grad_from_act(h4.z);
+              v[i + 3] *= elu_grad_from_act(h4.w);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (n0 + c0 + i < p.N) v[i] *= elu_grad_from_act(__ldg(ax + i));
+          }
+        }
+        if (full_rows) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (n0 + c0 + i < p.N) dst[i] = v[i];
         }
       }
-      float* dst = C + (int64_t)m * p.ldc + n0 + c0;
-      if (vec && n0 + c0 + 16 <= p.N) {
-#pragma unroll
-        for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (n0 + c0 + i < p.N) dst[i] = v[i];
+      if (p.ones_col >= 0 && n0 == 0 && half == 0 && m < p.M)
+        C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
+      // release accumulator buffer b to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[b]))
+                     : "memory");
       }
     }
-    if (p.ones_col >= 0 && blockIdx.y == 0 && m < p.M) C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(BN < 32 ? 32 : BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
   }
 }
 
@@ -328,8 +410,9 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
   else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM, false));
   if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32, true));
   else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN, false));
-  TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, C, d.ldc, d.bias, d.aux, d.ldaux, split_stride,
-           ones_col};
+  const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
+  TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, C, d.ldc, d.bias, d.aux, d.ldaux,
+           split_stride, ones_col};
   auto kern = tc_gemm_kernel<A_MN, B_MN, EPI, BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -337,8 +420,9 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
                                  Smem<BN>::kBytes));
     attr_set = true;
   }
-  dim3 grid((unsigned)ceil_div(d.M, BM), (unsigned)ceil_div(d.N, BN), (unsigned)splits);
-  kern<<<grid, kThreads, Smem<BN>::kBytes, s>>>(ma, mb, a);
+  const int ntiles = mt * nt * splits;
+  const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;  // persistent: one CTA per SM
+  kern<<<grid, kPThreads, Smem<BN>::kBytes, s>>>(ma, mb, a);
   return check_launch("tc_gemm_kernel");
 }
 

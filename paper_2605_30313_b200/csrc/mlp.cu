@@ -18,6 +18,13 @@ namespace ul {
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
 bool tc_eligible(const GemmDesc& d);
 int tc_num_splits(int64_t K, int splits);
+bool skinny_ok(int N);
+int64_t skinny_part_floats(int64_t M, int K, int N);
+int skinny_fwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float* W,
+               const float* b, float* out, int64_t ldo, cudaStream_t s);
+int skinny_bwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float* W,
+               const float* dout, int64_t ldd, float* dh, int64_t lddh, bool elu_grad,
+               float* gw, float* gb, float* part, cudaStream_t s);
 
 namespace {
 
@@ -113,7 +120,11 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
     const int64_t out = v.dims[i + 1], in = v.dims[i];
     const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
                        ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
-    const int64_t need = (int64_t)sp * (out * (in + 1) + out);
+    int64_t need = (int64_t)sp * (out * (in + 1) + out);
+    if (skinny_ok((int)out)) {
+      const int64_t sk = skinny_part_floats(M, (int)in, (int)out);
+      need = sk > need ? sk : need;
+    }
     ws = need > ws ? need : ws;
   }
   return 2 * M * max_hidden_ld(v) + ws;
@@ -166,6 +177,11 @@ int mlp_forward(const NetView& v, const float* params, const float* wp, int back
     g.epi = last ? kEpiBias : kEpiBiasElu;
     g.splits = 1;
     g.C = dst; g.ldc = lddst;
+    if (last && skinny_ok(v.dims[i + 1])) {  // 12-/1-wide head layer
+      UL_TRY(skinny_fwd(h, ldh, M, v.dims[i], v.dims[i + 1], params + v.w_off[i],
+                        params + v.b_off[i], dst, lddst, s));
+      break;
+    }
     const bool tc_here = tc && !last;
     if (tc_here) {
       g.B = wp + v.wp_off[i];
@@ -200,6 +216,17 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
     const float* inp = i == 0 ? x : act_ptr(v, acts, M, i - 1);
     const int64_t ldin = i == 0 ? ldx : act_ld(v.dims[i]);
     const bool has_ones = i == 0 ? (x_has_ones && ldx >= in + 1) : true;
+    if (i == v.n_layers - 1 && skinny_ok((int)out) && i > 0) {
+      // fused last-layer backward: dW, db and dh_prev in one pass over h
+      float* nxt = dh_buf[ping];
+      ping ^= 1;
+      UL_TRY(skinny_bwd(inp, ldin, M, (int)in, (int)out, params + v.w_off[i], dh, lddh, nxt,
+                        act_ld((int)in), true, want_dw ? grads + v.w_off[i] : nullptr,
+                        want_dw ? grads + v.b_off[i] : nullptr, ws, s));
+      dh = nxt;
+      lddh = act_ld((int)in);
+      continue;
+    }
     if (want_dw) {
       GemmDesc g{};
       g.M = out; g.K = M;
