@@ -108,6 +108,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ELU on the tensor-core path: exp via ex2.approx (abs. error ~1e-7 near 0,
+// far inside the tf32 GEMM error; the fp32 parity path keeps expm1f)
+__device__ __forceinline__ float elu_fast(float z) {
+  const float e = __expf(fmaxf(z, -60.f)) - 1.f;
+  return z > 0.f ? z : e;
+}
+
 struct TcArgs {
   int M, N, K;
   int k_per_split;  // multiple of BK
@@ -131,7 +138,7 @@ struct Smem {
                                 2 * BN * 4 /*bias, double-buffered by accumulator*/;
 };
 
-constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each half the columns
+constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
 constexpr int kPThreads = (2 + kEpiWarps) * 32;
 
 // Persistent: grid = min(#tiles, #SMs); tile t = blockIdx.x + i * gridDim.x
@@ -265,11 +272,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // 16 warps: TMEM lane quarter = warp % 4 (hardware rule), column slice =
+    // (warp - 2) / 4 of four BN/4-wide slices.  Two 16-column TMEM loads are
+    // kept in flight per iteration.
     const int ew = warp - 2;
-    const int quarter = warp & 3;         // TMEM lane quarter this warp may access
-    const int half = ew >> 2;             // column half
+    const int quarter = warp & 3;
+    const int slice = ew >> 2;
     const int row = quarter * 32 + lane;
-    constexpr int kHalf = BN / 2;
+    constexpr int kSlice = BN / 4;
     float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
     int local = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
@@ -278,10 +288,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int b = local & 1;
       const bool have = k_tiles(z) > 0;
       if (EPI == kEpiBias || EPI == kEpiBiasElu) {
-        // stage this tile's bias slice (each epilogue warp loads its own half)
-        for (int c = lane; c < kHalf; c += 32) {
-          const int n = n0 + half * kHalf + c;
-          sbias[b * BN + half * kHalf + c] = n < p.N ? __ldg(p.bias + n) : 0.f;
+        for (int c = lane; c < kSlice; c += 32) {
+          const int n = n0 + slice * kSlice + c;
+          sbias[b * BN + slice * kSlice + c] = n < p.N ? __ldg(p.bias + n) : 0.f;
         }
         __syncwarp();
       }
@@ -290,23 +299,31 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int m = m0 + row;
       float* C = p.C + (int64_t)z * p.split_stride;
       const bool full_rows = (n0 + BN <= p.N) && (p.ldc % 4 == 0);
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
-      for (int c0 = half * kHalf; c0 < (half + 1) * kHalf; c0 += 16) {
+      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 16) {
         float v[16];
         if (have) {
-          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN + c0), v);
+          tmem_ld16(taddr + (uint32_t)c0, v);
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = 0.f;
         }
         if (m >= p.M || n0 + c0 >= p.N) continue;
         if (EPI == kEpiBias || EPI == kEpiBiasElu) {
+          const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + c0);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] += sbias[b * BN + c0 + i];
+          for (int i = 0; i < 4; ++i) {
+            const float4 q = bv[i];
+            v[4 * i] += q.x;
+            v[4 * i + 1] += q.y;
+            v[4 * i + 2] += q.z;
+            v[4 * i + 3] += q.w;
+          }
         }
         if (EPI == kEpiBiasElu) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = elu_f(v[i]);
+          for (int i = 0; i < 16; ++i) v[i] = elu_fast(v[i]);
         }
         float* dst = C + (int64_t)m * p.ldc + n0 + c0;
         if (EPI == kEpiEluGrad) {
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             if (n0 + c0 + i < p.N) dst[i] = v[i];
         }
       }
-      if (p.ones_col >= 0 && n0 == 0 && half == 0 && m < p.M)
+      if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M)
         C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
       // release accumulator buffer b to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

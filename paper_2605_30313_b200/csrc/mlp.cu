@@ -30,17 +30,28 @@ namespace {
 
 int64_t rup(int64_t x, int64_t m) { return ceil_div(x, m) * m; }
 
-__global__ void reduce_dw_kernel(const float* __restrict__ ws, int splits, int64_t out, int64_t in,
-                                 float* __restrict__ gw, float* __restrict__ gb) {
-  // ws: splits x [out, in+1]; column `in` is the bias gradient
+__global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict__ ws, int splits,
+                                                        int64_t out, int64_t in,
+                                                        float* __restrict__ gw,
+                                                        float* __restrict__ gb) {
+  // ws: splits x [out, in+1]; column `in` is the bias gradient.  32 outputs per
+  // CTA, splits spread over 8 warps, fixed-order combine (deterministic).
+  __shared__ float sm[8][33];
   const int64_t len = out * (in + 1);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += stride) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += ws[(int64_t)z * len + j];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (j < len)
+    for (int z = w; z < splits; z += 8) s += ws[(int64_t)z * len + j];
+  sm[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && j < len) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][lane];
     const int64_t r = j / (in + 1), c = j - r * (in + 1);
-    if (c < in) gw[r * in + c] = s;
-    else gb[r] = s;
+    if (c < in) gw[r * in + c] = t;
+    else gb[r] = t;
   }
 }
 
@@ -241,8 +252,7 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
         const int sp = tc_num_splits(M, gt.splits);
         gt.splits = sp;
         UL_TRY(gemm_tc(gt, -1, s));
-        int64_t blocks = ceil_div(out * (in + 1), 256);
-        blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
+        const int64_t blocks = ceil_div(out * (in + 1), 32);
         reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(ws, sp, out, in, grads + v.w_off[i],
                                                           grads + v.b_off[i]);
         UL_TRY(check_launch("reduce_dw_kernel"));

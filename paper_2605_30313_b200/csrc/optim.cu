@@ -46,17 +46,31 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_o
     }
   }
   if (!last_block_ticket(&ctl->ticket, nb)) return;
+  // last CTA: fixed-order, block-parallel fold of the per-CTA partials
+  __shared__ double red[UL_MAX_SEG];
+  __shared__ int red_bad[UL_MAX_SEG];
+  for (int s = 0; s < st.nseg; ++s) {
+    double a = 0.0;
+    int bad = 0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      a += ctl->part[b][s];
+      bad |= ctl->part_bad[b][s];
+    }
+    const double tot = block_sum(a, scratch);
+    const int any_bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+      red[s] = tot;
+      red_bad[s] = any_bad;
+    }
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double joint = 0.0;
   int earlier_bad = ctl->loss_bad;
   const int was_diverged = ctl->diverged;
   for (int s = 0; s < st.nseg; ++s) {
-    double sum = 0.0;
-    int bad = 0;
-    for (int b = 0; b < nb; ++b) {
-      sum += ctl->part[b][s];
-      bad |= ctl->part_bad[b][s];
-    }
+    const double sum = red[s];
+    const int bad = red_bad[s];
     ctl->sumsq[s] = sum;
     ctl->seg_bad[s] = bad;
     joint += sum;

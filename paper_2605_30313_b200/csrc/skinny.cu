@@ -122,13 +122,24 @@ __global__ void __launch_bounds__(kThr) skinny_bwd_kernel(
   }
 }
 
-__global__ void reduce_parts_kernel(const float* __restrict__ part, int nblk, int64_t len,
-                                    float* __restrict__ out) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += stride) {
-    float s = 0.f;
-    for (int z = 0; z < nblk; ++z) s += part[(int64_t)z * len + j];
-    out[j] = s;
+// out[j] = sum_z part[z*len + j]: 32 outputs per CTA (coalesced lanes), the
+// partial index split across 8 warps, fixed-order smem combine (deterministic)
+__global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part,
+                                                           int nblk, int64_t len,
+                                                           float* __restrict__ out) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (j < len)
+    for (int z = w; z < nblk; z += 8) s += part[(int64_t)z * len + j];
+  sm[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && j < len) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][lane];
+    out[j] = t;
   }
 }
 
@@ -160,12 +171,12 @@ int skinny_bwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float
                                           pw, pb);
   UL_TRY(check_launch("skinny_bwd_kernel"));
   if (gw) {
-    reduce_parts_kernel<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, s>>>(pw, nblk,
+    reduce_parts_kernel<<<(unsigned)ceil_div((int64_t)N * K, 32), 256, 0, s>>>(pw, nblk,
                                                                                (int64_t)N * K, gw);
     UL_TRY(check_launch("reduce_parts_kernel"));
   }
   if (gb) {
-    reduce_parts_kernel<<<1, 256, 0, s>>>(pb, nblk, N, gb);
+    reduce_parts_kernel<<<(unsigned)ceil_div(N, 32), 256, 0, s>>>(pb, nblk, N, gb);
     UL_TRY(check_launch("reduce_parts_kernel"));
   }
   return UL_OK;
