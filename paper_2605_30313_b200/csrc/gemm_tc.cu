@@ -128,18 +128,20 @@ struct TcArgs {
   int ones_col;          // >= 0: also write C[m, ones_col] = 1 (dW bias trick)
 };
 
+constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
+constexpr int kPThreads = (2 + kEpiWarps) * 32;
+
+// [stage ring][16 x 4 KB epilogue staging][barriers][bias x 2]
 template <int BN>
 struct Smem {
-  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 6 : 8);
+  static constexpr int kStages = BN >= 256 ? 3 : 4;
   static constexpr int kABytes = BM * BK * 4;  // 16 KB
   static constexpr int kBBytes = BN * BK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
-                                2 * BN * 4 /*bias, double-buffered by accumulator*/;
+  static constexpr int kStagingBytes = kEpiWarps * 4096;
+  static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + 1024 /*align*/ +
+                                512 /*barriers*/ + 2 * BN * 4 /*bias, per accumulator*/;
 };
-
-constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
-constexpr int kPThreads = (2 + kEpiWarps) * 32;
 
 // Persistent: grid = min(#tiles, #SMs); tile t = blockIdx.x + i * gridDim.x
 // walks (m, n, split) tiles.  The smem ring runs continuously across tiles and
@@ -148,6 +150,7 @@ constexpr int kPThreads = (2 + kEpiWarps) * 32;
 template <bool A_MN, bool B_MN, int EPI, int BN>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                    TcArgs p) {
   using S = Smem<BN>;
   constexpr int kStages = S::kStages;
@@ -155,11 +158,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
+  uint64_t* full =
+      reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes + S::kStagingBytes);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* aux_bar = acc_empty + 2;  // [kEpiWarps]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.mt * p.nt * p.zt;
@@ -173,6 +178,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiWarps);
     }
+    for (int w = 0; w < kEpiWarps; ++w) mbar_init(&aux_bar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -273,14 +279,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     // 16 warps: TMEM lane quarter = warp % 4 (hardware rule), column slice =
-    // (warp - 2) / 4 of four BN/4-wide slices.  Two 16-column TMEM loads are
-    // kept in flight per iteration.
+    // (warp - 2) / 4 of four BN/4-wide slices.  Per 32-column group each warp
+    // owns a 32 x 32 fp32 staging tile (4 KB, 128 B swizzle): the ELU-gradient
+    // operand arrives there by TMA, results leave by TMA store (full 128 B
+    // lines instead of thread-per-row scattered stores).
     const int ew = warp - 2;
     const int quarter = warp & 3;
     const int slice = ew >> 2;
     const int row = quarter * 32 + lane;
     constexpr int kSlice = BN / 4;
     float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+    uint8_t* stg = smem + kStages * S::kStageBytes + ew * 4096;
+    uint64_t* abar = aux_bar + ew;
+    uint32_t aphase = 0;
     int local = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
       int m0, n0, z;
@@ -297,23 +308,31 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + row;
-      float* C = p.C + (int64_t)z * p.split_stride;
-      const bool full_rows = (n0 + BN <= p.N) && (p.ldc % 4 == 0);
+      const int crow = z * p.M + m0 + quarter * 32;  // row of this warp's 32-row box in C
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
-      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 16) {
-        float v[16];
+      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 32) {
+        // staging tile free again (previous TMA store has read it)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        if (EPI == kEpiEluGrad) {
+          if (lane == 0) {
+            mbar_expect_tx(abar, 4096);
+            tma_load_2d(stg, &tmX, abar, n0 + c0, m0 + quarter * 32);
+          }
+        }
+        float v[32];
         if (have) {
-          tmem_ld16(taddr + (uint32_t)c0, v);
+          tmem_ld16(taddr + (uint32_t)c0, *reinterpret_cast<float(*)[16]>(v));
+          tmem_ld16(taddr + (uint32_t)(c0 + 16), *reinterpret_cast<float(*)[16]>(v + 16));
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
-        if (m >= p.M || n0 + c0 >= p.N) continue;
         if (EPI == kEpiBias || EPI == kEpiBiasElu) {
           const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + c0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < 8; ++i) {
             const float4 q = bv[i];
             v[4 * i] += q.x;
             v[4 * i + 1] += q.y;
@@ -323,38 +342,37 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         if (EPI == kEpiBiasElu) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = elu_fast(v[i]);
+          for (int i = 0; i < 32; ++i) v[i] = elu_fast(v[i]);
         }
-        float* dst = C + (int64_t)m * p.ldc + n0 + c0;
+        float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
         if (EPI == kEpiEluGrad) {
-          const float* ax = p.aux + (int64_t)m * p.ldaux + n0 + c0;
-          if (full_rows && (p.ldaux % 4 == 0)) {
+          mbar_wait(abar, aphase);
+          aphase ^= 1;
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              const float4 h4 = __ldg(reinterpret_cast<const float4*>(ax + i));
-              v[i] *= elu_grad_from_act(h4.x);
-              v[i + 1] *= elu_grad_from_act(h4.y);
-              v[i + 2] *= elu_grad_from_act(h4.z);
-              v[i + 3] *= elu_grad_from_act(h4.w);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (n0 + c0 + i < p.N) v[i] *= elu_grad_from_act(__ldg(ax + i));
+          for (int q = 0; q < 8; ++q) {
+            const float4 h4 = srow[q ^ (lane & 7)];
+            v[4 * q] *= elu_grad_from_act(h4.x);
+            v[4 * q + 1] *= elu_grad_from_act(h4.y);
+            v[4 * q + 2] *= elu_grad_from_act(h4.z);
+            v[4 * q + 3] *= elu_grad_from_act(h4.w);
           }
         }
-        if (full_rows) {
 #pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n0 + c0 + i < p.N) dst[i] = v[i];
+        for (int q = 0; q < 8; ++q)
+          srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  &tmC),
+              "r"(su32(stg)), "r"(n0 + c0), "r"(crow)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
       if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M)
-        C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
+        p.C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
       // release accumulator buffer b to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -363,6 +381,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                      : "memory");
       }
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -421,12 +440,16 @@ int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, 
 template <bool A_MN, bool B_MN, int EPI, int BN>
 int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_stride, int ones_col,
            cudaStream_t s) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mx;
   // A(m,k): K-major -> rows=M, inner=K ; MN-major -> rows=K, inner=M
   if (A_MN) UL_TRY(make_map(&ma, d.A, d.M, d.K, d.lda, 32, true));
   else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM, false));
   if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32, true));
   else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN, false));
+  // C (and split-K partials stacked as [splits*M, ldc]) stored by 32x32 TMA boxes
+  UL_TRY(make_map(&mc, C, d.N, (int64_t)splits * d.M, d.ldc, 32, false));
+  if (EPI == kEpiEluGrad) UL_TRY(make_map(&mx, d.aux, d.N, d.M, d.ldaux, 32, false));
+  else mx = mc;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
   TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, C, d.ldc, d.bias, d.aux, d.ldaux,
            split_stride, ones_col};
@@ -439,7 +462,7 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
   }
   const int ntiles = mt * nt * splits;
   const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;  // persistent: one CTA per SM
-  kern<<<grid, kPThreads, Smem<BN>::kBytes, s>>>(ma, mb, a);
+  kern<<<grid, kPThreads, Smem<BN>::kBytes, s>>>(ma, mb, mc, mx, a);
   return check_launch("tc_gemm_kernel");
 }
 
@@ -447,8 +470,10 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
 
 bool tc_eligible(const GemmDesc& d) {
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  return d.M >= 128 && d.N >= 32 && d.K >= 32 && d.M < (1ll << 31) && d.N < (1ll << 31) &&
-         d.K < (1ll << 31) && al(d.A) && al(d.B) && (d.lda % 4 == 0) && (d.ldb % 4 == 0) &&
+  return d.M >= 128 && d.N >= 64 && d.K >= 32 && d.M < (1ll << 31) && d.N < (1ll << 31) &&
+         d.K < (1ll << 31) && al(d.A) && al(d.B) && al(d.C) && (d.lda % 4 == 0) &&
+         (d.ldb % 4 == 0) && (d.ldc % 4 == 0) &&
+         (d.epi != kEpiEluGrad || (al(d.aux) && d.ldaux % 4 == 0)) &&
          !(d.a_kmajor == false && d.b_kmajor == true);
 }
 
@@ -466,14 +491,14 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   const int splits = d.splits < 1 ? 1 : d.splits;
   const int kps = (int)(ceil_div(ceil_div(d.K, splits), tc::BK) * tc::BK);
   const int zs = (int)ceil_div(d.K > 0 ? d.K : 1, kps);
-  const int64_t sstride = zs > 1 ? d.M * d.N : 0;
-  const int bn = d.N > 128 ? 256 : (d.N > 64 ? 128 : 64);
+  // split-K partials: [zs][M][ldc] (ldc >= N, multiple of 4 for the TMA store)
+  const int64_t sstride = zs > 1 ? d.M * d.ldc : 0;
+  const int bn = d.N > 128 ? 256 : 128;
   const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
 #define UL_TC_CASE(AMN, BMN, EPI)                                                             \
   if (amn == AMN && bmn == BMN && d.epi == EPI) {                                             \
     if (bn == 256) return tc::launch<AMN, BMN, EPI, 256>(d, zs, kps, d.C, sstride, ones_col, s); \
-    if (bn == 128) return tc::launch<AMN, BMN, EPI, 128>(d, zs, kps, d.C, sstride, ones_col, s); \
-    return tc::launch<AMN, BMN, EPI, 64>(d, zs, kps, d.C, sstride, ones_col, s);              \
+    return tc::launch<AMN, BMN, EPI, 128>(d, zs, kps, d.C, sstride, ones_col, s);             \
   }
   UL_TC_CASE(false, false, kEpiBias)
   UL_TC_CASE(false, false, kEpiBiasElu)

@@ -31,13 +31,14 @@ namespace {
 int64_t rup(int64_t x, int64_t m) { return ceil_div(x, m) * m; }
 
 __global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict__ ws, int splits,
-                                                        int64_t out, int64_t in,
+                                                        int64_t out, int64_t in, int64_t ldp,
                                                         float* __restrict__ gw,
                                                         float* __restrict__ gb) {
-  // ws: splits x [out, in+1]; column `in` is the bias gradient.  32 outputs per
-  // CTA, splits spread over 8 warps, fixed-order combine (deterministic).
+  // ws: splits x [out, ldp]; column `in` is the bias gradient, columns > in
+  // are TMA-row padding.  32 outputs per CTA, splits spread over 8 warps,
+  // fixed-order combine (deterministic).
   __shared__ float sm[8][33];
-  const int64_t len = out * (in + 1);
+  const int64_t len = out * ldp;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   float s = 0.f;
@@ -49,9 +50,9 @@ __global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict_
     float t = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) t += sm[k][lane];
-    const int64_t r = j / (in + 1), c = j - r * (in + 1);
+    const int64_t r = j / ldp, c = j - r * ldp;
     if (c < in) gw[r * in + c] = t;
-    else gb[r] = t;
+    else if (c == in) gb[r] = t;
   }
 }
 
@@ -131,7 +132,7 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
     const int64_t out = v.dims[i + 1], in = v.dims[i];
     const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
                        ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
-    int64_t need = (int64_t)sp * (out * (in + 1) + out);
+    int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out);
     if (skinny_ok((int)out)) {
       const int64_t sk = skinny_part_floats(M, (int)in, (int)out);
       need = sk > need ? sk : need;
@@ -247,13 +248,14 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
       GemmDesc gt = g;
       gt.N = in + 1;  // [dW | db] through the ones column
       gt.splits = dw_splits(out, in, M, true);
-      gt.ldc = in + 1;
+      gt.ldc = rup(in + 1, 4);  // 16 B partial rows (TMA store)
       if (tc && has_ones && out >= 64 && tc_eligible(gt)) {
         const int sp = tc_num_splits(M, gt.splits);
         gt.splits = sp;
         UL_TRY(gemm_tc(gt, -1, s));
-        const int64_t blocks = ceil_div(out * (in + 1), 32);
-        reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(ws, sp, out, in, grads + v.w_off[i],
+        const int64_t blocks = ceil_div(out * gt.ldc, 32);
+        reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(ws, sp, out, in, gt.ldc,
+                                                          grads + v.w_off[i],
                                                           grads + v.b_off[i]);
         UL_TRY(check_launch("reduce_dw_kernel"));
       } else {

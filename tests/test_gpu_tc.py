@@ -94,10 +94,11 @@ def test_tc_dw_layout_split_k(out, inp, rows, splits):
     A_, B_ = _dev_mat(dh), _dev_mat(x)
     kps = -(-(-(-rows // splits)) // 32) * 32  # split length, rounded to the 32-row K tile
     zs = -(-rows // kps)
-    C = torch.zeros((zs, out, inp), dtype=torch.float32, device="cuda")
+    ldc = (inp + 3) // 4 * 4  # split partials: [zs][out][ldc], 16 B rows
+    C = torch.zeros((zs, out, ldc), dtype=torch.float32, device="cuda")
     _lib.call("ul_gemm_tc", 0, 0, out, inp, rows, _dev.ptr(A_), A_.stride(0), _dev.ptr(B_),
-              B_.stride(0), _dev.ptr(C), inp, None, None, 0, splits, _dev.stream())
-    got = C.sum(0).cpu().numpy()
+              B_.stride(0), _dev.ptr(C), ldc, None, None, 0, splits, _dev.stream())
+    got = C.sum(0)[:, :inp].cpu().numpy()
     assert _rel(got, ref) < 2e-3
 
 
