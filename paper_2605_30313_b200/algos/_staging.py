@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .. import _dev
+from .. import _dev, _lib
 
 
 def _is_dev(x) -> bool:
@@ -48,9 +48,13 @@ class DeviceSegment:
         self.boot = torch.zeros(N, **f32)
         self.perm = torch.zeros((max(epochs, 1), rows), dtype=torch.int64, device=dev)
         self.has_tv = False
+        self._raw: dict = {}  # width -> contiguous H2D landing buffer
 
     # ------------------------------------------------------------- loading
     def _put_rows(self, dst: torch.Tensor, src, width: int) -> None:
+        """Host [rows, width] -> HBM [rows, ld]: one contiguous H2D at full PCIe
+        rate into a raw landing buffer, then the K4 row kernel re-pitches it in
+        HBM (a pitched 2-D H2D of 940 B rows crawls at a fraction of link speed)."""
         if _is_dev(src):
             src = src.reshape(self.rows, width)
             dst[:, :width].copy_(src)  # device -> device staging copy
@@ -58,7 +62,17 @@ class DeviceSegment:
         a = np.asarray(src)
         if a.dtype != np.float32:
             a = a.astype(np.float32)
-        _dev.h2d_rows(dst, a.reshape(self.rows, width))
+        a = np.ascontiguousarray(a.reshape(self.rows, width))
+        raw = self._raw.get(width)
+        if raw is None:
+            raw = torch.empty(self.rows * width, dtype=torch.float32, device=dst.device)
+            self._raw[width] = raw
+        _dev.h2d(raw, a)
+        rb = width * 4
+        _lib.call("ul_gather_rows", 1, _lib.ptr_array([_dev.ptr(raw)]),
+                  _lib.ptr_array([_dev.ptr(dst)]), _lib.i64_array([rb]),
+                  _lib.i64_array([dst.stride(0) * 4]), _lib.i64_array([rb]), None, None, self.rows,
+                  0, 0, self.rows, None, _dev.stream())
 
     def _put_vec(self, dst: torch.Tensor, src, dtype=np.float32) -> None:
         if _is_dev(src):

@@ -42,8 +42,19 @@ __global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict_
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   float s = 0.f;
-  if (j < len)
-    for (int z = w; z < splits; z += 8) s += ws[(int64_t)z * len + j];
+  if (j < len) {
+    // four independent accumulators keep 4 loads in flight per warp
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int z = w;
+    for (; z + 24 < splits; z += 32) {
+      s0 += ws[(int64_t)z * len + j];
+      s1 += ws[(int64_t)(z + 8) * len + j];
+      s2 += ws[(int64_t)(z + 16) * len + j];
+      s3 += ws[(int64_t)(z + 24) * len + j];
+    }
+    for (; z < splits; z += 8) s0 += ws[(int64_t)z * len + j];
+    s = (s0 + s1) + (s2 + s3);
+  }
   sm[w][lane] = s;
   __syncthreads();
   if (w == 0 && j < len) {
@@ -52,7 +63,36 @@ __global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict_
     for (int k = 0; k < 8; ++k) t += sm[k][lane];
     const int64_t r = j / ldp, c = j - r * ldp;
     if (c < in) gw[r * in + c] = t;
-    else if (c == in) gb[r] = t;
+    else if (c == in && gb) gb[r] = t;
+  }
+}
+
+// db partials: column sums of dh [M, N] over row chunks; lanes = columns
+// (coalesced 128 B rows), 8 warps stride the rows; part[chunk][N]
+__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ x, int64_t ld,
+                                                     int64_t M, int64_t N, int64_t rows_per,
+                                                     float* __restrict__ part) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per;
+  const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
+  float s0 = 0.f, s1 = 0.f;
+  if (c < N) {
+    int64_t r = r0 + w;
+    for (; r + 8 < r1; r += 16) {
+      s0 += x[r * ld + c];
+      s1 += x[(r + 8) * ld + c];
+    }
+    for (; r < r1; r += 8) s0 += x[r * ld + c];
+  }
+  sm[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && c < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][lane];
+    part[(int64_t)blockIdx.y * N + c] = t;
   }
 }
 
@@ -132,7 +172,7 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
     const int64_t out = v.dims[i + 1], in = v.dims[i];
     const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
                        ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
-    int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out);
+    int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 64 * out;
     if (skinny_ok((int)out)) {
       const int64_t sk = skinny_part_floats(M, (int)in, (int)out);
       need = sk > need ? sk : need;
@@ -245,19 +285,33 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
       g.A = dh; g.lda = lddh; g.B = inp; g.ldb = ldin;
       g.a_kmajor = false; g.b_kmajor = false; g.epi = kEpiStore;
       g.C = ws;
+      // [dW | db] through the ones column when that column rides in a tile the
+      // GEMM computes anyway; otherwise dW alone + a column-sum pass for db
+      auto bn_of = [](int64_t n) { return n > 128 ? 256 : 128; };
+      const bool ones_free = has_ones && bn_of(in + 1) == bn_of(in) &&
+                             ceil_div(in + 1, bn_of(in + 1)) == ceil_div(in, bn_of(in));
       GemmDesc gt = g;
-      gt.N = in + 1;  // [dW | db] through the ones column
+      gt.N = ones_free ? in + 1 : in;
       gt.splits = dw_splits(out, in, M, true);
-      gt.ldc = rup(in + 1, 4);  // 16 B partial rows (TMA store)
-      if (tc && has_ones && out >= 64 && tc_eligible(gt)) {
+      gt.ldc = rup(gt.N, 4);  // 16 B partial rows (TMA store)
+      if (tc && out >= 64 && tc_eligible(gt)) {
         const int sp = tc_num_splits(M, gt.splits);
         gt.splits = sp;
         UL_TRY(gemm_tc(gt, -1, s));
         const int64_t blocks = ceil_div(out * gt.ldc, 32);
-        reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(ws, sp, out, in, gt.ldc,
-                                                          grads + v.w_off[i],
-                                                          grads + v.b_off[i]);
+        reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+            ws, sp, out, in, gt.ldc, grads + v.w_off[i],
+            ones_free ? grads + v.b_off[i] : nullptr);
         UL_TRY(check_launch("reduce_dw_kernel"));
+        if (!ones_free) {
+          const int64_t chunks = ceil_div(M, 2048) < 64 ? ceil_div(M, 2048) : 64;
+          const int64_t rows_per = ceil_div(M, chunks);
+          float* part = ws + (int64_t)sp * out * gt.ldc;
+          colsum_kernel<<<dim3((unsigned)ceil_div(out, 32), (unsigned)chunks), 256, 0, s>>>(
+              dh, lddh, M, out, rows_per, part);
+          UL_TRY(check_launch("colsum_kernel"));
+          UL_TRY(reduce_splits(part, (int)chunks, out, grads + v.b_off[i], out, out, s));
+        }
       } else {
         const int sp = gemm_num_splits(M, dw_splits(out, in, M, false));
         g.N = in;

@@ -131,8 +131,18 @@ __global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restri
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
   float s = 0.f;
-  if (j < len)
-    for (int z = w; z < nblk; z += 8) s += part[(int64_t)z * len + j];
+  if (j < len) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int z = w;
+    for (; z + 24 < nblk; z += 32) {
+      s0 += part[(int64_t)z * len + j];
+      s1 += part[(int64_t)(z + 8) * len + j];
+      s2 += part[(int64_t)(z + 16) * len + j];
+      s3 += part[(int64_t)(z + 24) * len + j];
+    }
+    for (; z < nblk; z += 8) s0 += part[(int64_t)z * len + j];
+    s = (s0 + s1) + (s2 + s3);
+  }
   sm[w][lane] = s;
   __syncthreads();
   if (w == 0 && j < len) {

@@ -170,3 +170,67 @@ def test_ppo_full_update_cfg1_vs_oracle():
     assert abs(st.policy_loss - ost["policy_loss"]) < 1e-3
     assert abs(st.value_loss - ost["value_loss"]) <= 1e-3 * max(1, abs(ost["value_loss"]))
     assert abs(st.entropy - ost["entropy"]) < 1e-4
+
+
+def test_appo_update_matches_reference(golden):
+    """appo_update on the reference's goldens (behaviour policy perturbed by
+    1e-2, V-trace rho/c clips 1, reference Philox permutations)."""
+    from oracle.port import philox_stream
+
+    g = golden("ppo")
+    seg = A.RolloutSegment(**_seg_kwargs(g, "a_"), behavior_version=3)
+    params = _ac((6, 16, 16, 3), (7, 16, 16, 1), g["a_actor0"], g["a_critic0"])
+    cfg = A.AppoConfig(epochs=2, minibatches=2)
+    opt = A.AcOpt.for_params(params, cfg.lr)
+    st = A.appo_update(seg, params, opt, cfg, philox_stream(1, "update"), learner_version=5)
+    np.testing.assert_allclose(params.actor.flat(), g["a_actor1"], atol=2e-5)
+    np.testing.assert_allclose(params.critic.flat(), g["a_critic1"], atol=2e-5)
+    got = [st.policy_loss, st.value_loss, st.entropy, st.kl, st.lr, st.grad_norm, st.staleness]
+    assert rel_err(got, g["a_stats"]) < 1e-4
+
+
+def test_learners_and_weight_slot():
+    """PpoLearner / AppoLearner (runtime learner halves) + WeightSlot host snapshots."""
+    import threading
+
+    from paper_2605_30313_b200 import runtime as RT
+
+    rng = np.random.default_rng(3)
+    t, b, od, ad = 8, 32, 6, 2
+    params = RT.build_ac_params(od, od, ad, (16, 16), seed=1)
+
+    def segment(seq, version):
+        return A.RolloutSegment(
+            obs=rng.normal(size=(t, b, od)).astype(np.float32),
+            critic_obs=rng.normal(size=(t, b, od)).astype(np.float32),
+            actions=rng.normal(size=(t, b, ad)).astype(np.float32),
+            behavior_log_prob=rng.normal(size=(t, b)) - 3.0, rewards=rng.normal(size=(t, b)),
+            terminated=rng.random((t, b)) < 0.05, truncated=np.zeros((t, b), bool),
+            values=rng.normal(size=(t, b)), bootstrap_value=rng.normal(size=b),
+            truncation_values=np.zeros((t, b)), behavior_version=version, seq=seq)
+
+    learner = RT.PpoLearner(params, A.PpoConfig(epochs=1, minibatches=2), A.DeviceRng(0))
+    learner.slot.publish(params)
+    v0, snap0 = learner.slot.fetch()
+    st = learner.learn(segment(0, v0), 0)
+    assert np.isfinite(st.policy_loss)
+    v1, snap1 = learner.slot.fetch()
+    assert v1 == v0 + 1
+    np.testing.assert_array_equal(snap1.actor.flat(), params.actor.flat())
+    assert not np.array_equal(snap0.actor.flat(), snap1.actor.flat())
+    with pytest.raises(ValueError):
+        snap1.actor.layers[0][0][0, 0] = 1.0  # published snapshots are frozen
+
+    appo = RT.AppoLearner(params, A.AppoConfig(epochs=1, minibatches=2), A.DeviceRng(1))
+    appo.slot.publish(params)
+    ring = RT.RolloutRing(2)
+
+    def produce():
+        for s in range(4):
+            ring.put(segment(s, appo.slot.version))
+
+    th = threading.Thread(target=produce)
+    th.start()
+    stats = appo.drain(ring, 4)
+    th.join()
+    assert len(stats) == 4 and max(appo.staleness) <= 2 + 1
