@@ -44,22 +44,40 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
                                           int64_t modulo, int64_t lo, int64_t hi, int* err,
                                           int64_t ones) {
   using T = typename Vec<U>::T;
+  constexpr int kIlp = 4;  // units in flight per thread: all loads issued before any store
   const int64_t total = n * upr;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += stride) {
-    const int64_t r = w / upr, u = w - r * upr;
-    int64_t s = idx ? idx[r] : r;
-    if (s < lo || s >= hi) {
-      if (err) atomicOr(err, 1);
-      continue;
+  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < total;
+       w0 += stride * kIlp) {
+    T v[kIlp];
+    int64_t drow[kIlp], du[kIlp];
+    bool ok[kIlp];
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const int64_t w = w0 + k * stride;
+      ok[k] = false;
+      if (w >= total) continue;
+      const int64_t r = w / upr, u = w - r * upr;
+      int64_t s = idx ? __ldg(idx + r) : r;
+      drow[k] = r;
+      du[k] = u;
+      if (s < lo || s >= hi) {
+        if (err) atomicOr(err, 1);
+        continue;
+      }
+      if (modulo > 0) s %= modulo;
+      v[k] = __ldg(reinterpret_cast<const T*>(src + s * sst) + u);
+      ok[k] = true;
     }
-    if (modulo > 0) s %= modulo;
-    T v = __ldg(reinterpret_cast<const T*>(src + s * sst) + u);
-    if (ones >= 0 && ones / U == u) {
-      float* f = reinterpret_cast<float*>(&v);
-      f[(ones % U) / 4] = 1.f;
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      if (!ok[k]) continue;
+      if (ones >= 0 && ones / U == du[k]) {
+        float* f = reinterpret_cast<float*>(&v[k]);
+        f[(ones % U) / 4] = 1.f;
+      }
+      reinterpret_cast<T*>(dst + drow[k] * dstr)[du[k]] = v[k];
     }
-    reinterpret_cast<T*>(dst + r * dstr)[u] = v;
   }
 }
 

@@ -152,15 +152,35 @@ __global__ void __launch_bounds__(kThreads) sgemm_kernel(KArgs p) {
   }
 }
 
-__global__ void reduce_splits_kernel(const float* __restrict__ ws, int splits, int64_t len,
-                                     float* __restrict__ out, int64_t ld_rows, int64_t row_len) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += stride) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += ws[(int64_t)z * len + j];
+// out[j] = sum_z ws[z*len + j]: 32 outputs per CTA (coalesced lanes), splits
+// spread over 8 warps with 4 loads in flight each, fixed-order combine.
+__global__ void __launch_bounds__(256) reduce_splits_kernel(const float* __restrict__ ws,
+                                                            int splits, int64_t len,
+                                                            float* __restrict__ out,
+                                                            int64_t ld_rows, int64_t row_len) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (j < len) {
+    int z = w;
+    for (; z + 24 < splits; z += 32) {
+      s0 += ws[(int64_t)z * len + j];
+      s1 += ws[(int64_t)(z + 8) * len + j];
+      s2 += ws[(int64_t)(z + 16) * len + j];
+      s3 += ws[(int64_t)(z + 24) * len + j];
+    }
+    for (; z < splits; z += 8) s0 += ws[(int64_t)z * len + j];
+  }
+  sm[w][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (w == 0 && j < len) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][lane];
     // out may be strided by rows (ld_rows) when row_len < ld_rows
     const int64_t r = j / row_len, c = j - r * row_len;
-    out[r * ld_rows + c] = s;
+    out[r * ld_rows + c] = t;
   }
 }
 
@@ -224,8 +244,7 @@ int gemm_f32(const GemmDesc& d, cudaStream_t s) {
 int reduce_splits(const float* ws, int splits, int64_t len, float* out, int64_t ld_rows,
                   int64_t row_len, cudaStream_t s) {
   if (len == 0) return UL_OK;
-  int blocks = (int)ceil_div(len, 256);
-  blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
+  const unsigned blocks = (unsigned)ceil_div(len, 32);
   reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, splits, len, out, ld_rows, row_len);
   return check_launch("reduce_splits_kernel");
 }

@@ -77,16 +77,18 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ x
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
-  float s0 = 0.f, s1 = 0.f;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   if (c < N) {
     int64_t r = r0 + w;
-    for (; r + 8 < r1; r += 16) {
+    for (; r + 24 < r1; r += 32) {
       s0 += x[r * ld + c];
       s1 += x[(r + 8) * ld + c];
+      s2 += x[(r + 16) * ld + c];
+      s3 += x[(r + 24) * ld + c];
     }
     for (; r < r1; r += 8) s0 += x[r * ld + c];
   }
-  sm[w][lane] = s0 + s1;
+  sm[w][lane] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (w == 0 && c < N) {
     float t = 0.f;
@@ -172,7 +174,7 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
     const int64_t out = v.dims[i + 1], in = v.dims[i];
     const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
                        ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
-    int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 64 * out;
+    int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 256 * out;
     if (skinny_ok((int)out)) {
       const int64_t sk = skinny_part_floats(M, (int)in, (int)out);
       need = sk > need ? sk : need;
@@ -304,7 +306,8 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
             ones_free ? grads + v.b_off[i] : nullptr);
         UL_TRY(check_launch("reduce_dw_kernel"));
         if (!ones_free) {
-          const int64_t chunks = ceil_div(M, 2048) < 64 ? ceil_div(M, 2048) : 64;
+          // 256-row chunks (8 warps x 32 rows, 4 loads in flight each), <= 256 chunks
+          const int64_t chunks = ceil_div(M, 256) < 256 ? ceil_div(M, 256) : 256;
           const int64_t rows_per = ceil_div(M, chunks);
           float* part = ws + (int64_t)sp * out * gt.ldc;
           colsum_kernel<<<dim3((unsigned)ceil_div(out, 32), (unsigned)chunks), 256, 0, s>>>(

@@ -29,11 +29,30 @@ __global__ void __launch_bounds__(256) moments_kernel(const float* __restrict__ 
   double a1 = 0.0, a2 = 0.0;
   if (d < D) {
     const double c = (double)x[d];
-    for (int64_t r = r0 + w; r < r1; r += kRowWarps) {
+    // 4 rows in flight per warp (independent loads), then fold
+    double b1 = 0.0, b2 = 0.0, e1 = 0.0, e2 = 0.0, f1 = 0.0, f2 = 0.0;
+    int64_t r = r0 + w;
+    for (; r + 3 * kRowWarps < r1; r += 4 * kRowWarps) {
+      const double v0 = (double)__ldg(x + r * ldx + d) - c;
+      const double v1 = (double)__ldg(x + (r + kRowWarps) * ldx + d) - c;
+      const double v2 = (double)__ldg(x + (r + 2 * kRowWarps) * ldx + d) - c;
+      const double v3 = (double)__ldg(x + (r + 3 * kRowWarps) * ldx + d) - c;
+      a1 += v0;
+      a2 += v0 * v0;
+      b1 += v1;
+      b2 += v1 * v1;
+      e1 += v2;
+      e2 += v2 * v2;
+      f1 += v3;
+      f2 += v3 * v3;
+    }
+    for (; r < r1; r += kRowWarps) {
       const double v = (double)x[r * ldx + d] - c;
       a1 += v;
       a2 += v * v;
     }
+    a1 = (a1 + b1) + (e1 + f1);
+    a2 = (a2 + b2) + (e2 + f2);
   }
   s1[w][lane] = a1;
   s2[w][lane] = a2;

@@ -95,6 +95,17 @@ struct AdamScalars {
   float b1, one_m_b1, b2, one_m_b2, bc1, bc2, lr, eps;
 };
 
+// numpy's f32 operation order, round-to-nearest, no FMA contraction
+__device__ __forceinline__ void adam_elem(float gi, float& m, float& v, float& p,
+                                          const AdamScalars& k) {
+  m = __fadd_rn(__fmul_rn(m, k.b1), __fmul_rn(k.one_m_b1, gi));
+  v = __fadd_rn(__fmul_rn(v, k.b2), __fmul_rn(__fmul_rn(k.one_m_b2, gi), gi));
+  const float mh = __fdiv_rn(m, k.bc1);
+  const float vh = __fdiv_rn(v, k.bc2);
+  const float step = __fdiv_rn(__fmul_rn(k.lr, mh), __fadd_rn(__fsqrt_rn(vh), k.eps));
+  p = __fsub_rn(p, step);
+}
+
 __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
                              int do_adam) {
   const int s = blockIdx.y;
@@ -118,30 +129,74 @@ __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, in
     k.eps = (float)ctl->eps;
   }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!do_adam || !upd) {  // clip-only (clip_global_norm) or a skipped segment
+    if (write_grads && scale)
+      for (int64_t i = t0; i < n; i += stride) g[i] = __fmul_rn(g[i], f);
+    return;
+  }
+  float *pm = st.m[s], *pv = st.v[s], *pp = st.p[s];
+  const bool vec = (((uintptr_t)g | (uintptr_t)pm | (uintptr_t)pv | (uintptr_t)pp) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t i = t0; i < n4; i += stride) {  // 16 B per array per thread
+    float4 g4 = reinterpret_cast<const float4*>(g)[i];
+    float4 m4 = reinterpret_cast<float4*>(pm)[i], v4 = reinterpret_cast<float4*>(pv)[i];
+    float4 p4 = reinterpret_cast<float4*>(pp)[i];
+    float* ga = reinterpret_cast<float*>(&g4);
+    float* ma = reinterpret_cast<float*>(&m4);
+    float* va = reinterpret_cast<float*>(&v4);
+    float* pa = reinterpret_cast<float*>(&p4);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (scale) ga[e] = __fmul_rn(ga[e], f);
+      adam_elem(ga[e], ma[e], va[e], pa[e], k);
+    }
+    if (write_grads && scale) reinterpret_cast<float4*>(g)[i] = g4;
+    reinterpret_cast<float4*>(pm)[i] = m4;
+    reinterpret_cast<float4*>(pv)[i] = v4;
+    reinterpret_cast<float4*>(pp)[i] = p4;
+  }
+  for (int64_t i = 4 * n4 + t0; i < n; i += stride) {
     float gi = g[i];
     if (scale) gi = __fmul_rn(gi, f);
     if (write_grads && scale) g[i] = gi;
-    if (!do_adam || !upd) continue;
-    float m = st.m[s][i], v = st.v[s][i], p = st.p[s][i];
-    m = __fadd_rn(__fmul_rn(m, k.b1), __fmul_rn(k.one_m_b1, gi));
-    v = __fadd_rn(__fmul_rn(v, k.b2), __fmul_rn(__fmul_rn(k.one_m_b2, gi), gi));
-    const float mh = __fdiv_rn(m, k.bc1);
-    const float vh = __fdiv_rn(v, k.bc2);
-    const float step = __fdiv_rn(__fmul_rn(k.lr, mh), __fadd_rn(__fsqrt_rn(vh), k.eps));
-    st.m[s][i] = m;
-    st.v[s][i] = v;
-    st.p[s][i] = __fsub_rn(p, step);
+    float m = pm[i], v = pv[i], p = pp[i];
+    adam_elem(gi, m, v, p, k);
+    pm[i] = m;
+    pv[i] = v;
+    pp[i] = p;
   }
 }
 
 __global__ void polyak_kernel(float* __restrict__ tgt, const float* __restrict__ src, int64_t n,
                               float keep, float tau) {
+  // reference order: t *= (1-tau); t += tau*o   (two f32 roundings each)
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    // reference order: t *= (1-tau); t += tau*o   (two f32 roundings each)
-    tgt[i] = __fadd_rn(__fmul_rn(tgt[i], keep), __fmul_rn(tau, src[i]));
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool vec = (((uintptr_t)tgt | (uintptr_t)src) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  float4* t4 = reinterpret_cast<float4*>(tgt);
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  for (int64_t i = t0; i < n4; i += 2 * stride) {  // two 16 B loads in flight per array
+    const int64_t j = i + stride;
+    const float4 a = t4[i], b = __ldg(s4 + i);
+    float4 c, d;
+    if (j < n4) {
+      c = t4[j];
+      d = __ldg(s4 + j);
+    }
+    t4[i] = make_float4(__fadd_rn(__fmul_rn(a.x, keep), __fmul_rn(tau, b.x)),
+                        __fadd_rn(__fmul_rn(a.y, keep), __fmul_rn(tau, b.y)),
+                        __fadd_rn(__fmul_rn(a.z, keep), __fmul_rn(tau, b.z)),
+                        __fadd_rn(__fmul_rn(a.w, keep), __fmul_rn(tau, b.w)));
+    if (j < n4)
+      t4[j] = make_float4(__fadd_rn(__fmul_rn(c.x, keep), __fmul_rn(tau, d.x)),
+                          __fadd_rn(__fmul_rn(c.y, keep), __fmul_rn(tau, d.y)),
+                          __fadd_rn(__fmul_rn(c.z, keep), __fmul_rn(tau, d.z)),
+                          __fadd_rn(__fmul_rn(c.w, keep), __fmul_rn(tau, d.w)));
   }
+  for (int64_t i = 4 * n4 + t0; i < n; i += stride)
+    tgt[i] = __fadd_rn(__fmul_rn(tgt[i], keep), __fmul_rn(tau, src[i]));
 }
 
 int fill_table(SegTable& st, int nseg, float* const* params, float* const* grads,
