@@ -13,6 +13,7 @@
 //   warp 1      : TMEM allocator + MMA issuer (one elected lane)
 //   warps 2..5  : epilogue (TMEM lane quarter = warp % 4)
 #include <cuda.h>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -126,6 +127,7 @@ struct TcArgs {
   int64_t ldaux;
   int64_t split_stride;  // elements between split partial tiles
   int ones_col;          // >= 0: also write C[m, ones_col] = 1 (dW bias trick)
+  int dbg;               // diagnostics (UL_TC_DBG): 1 no C store, 2 A from tile 0, 4 no MMA
 };
 
 constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
@@ -147,7 +149,35 @@ struct Smem {
 // walks (m, n, split) tiles.  The smem ring runs continuously across tiles and
 // the TMEM accumulator is double-buffered, so tile i's epilogue overlaps tile
 // i+1's TMA + MMA main loop.
-template <bool A_MN, bool B_MN, int EPI, int BN>
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+
+// CS = cluster size along M.  The CS CTAs of a cluster work on CS consecutive
+// M-tiles of the same (N-tile, K-split) and share its B tile: CTA r fetches
+// 1/CS of B and TMA-multicasts it into every CTA of the cluster, so B leaves
+// L2 once per cluster instead of once per M-tile.  A stage is refilled only
+// after every CTA's MMAs consumed it (empty barriers count CS multicast
+// commits).
+template <bool A_MN, bool B_MN, int EPI, int BN, int CS>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
@@ -167,12 +197,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ntiles = p.mt * p.nt * p.zt;
+
+  uint32_t crank = 0;
+  if (CS > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int mgroups = (p.mt + CS - 1) / CS;
+  const int ngroups = mgroups * p.nt * p.zt;
+  const int cl = blockIdx.x / CS, ncl = gridDim.x / CS;
+  constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1u);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);  // one multicast MMA commit from every CTA of the cluster
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -190,14 +226,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CS > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // group t -> (M-tile group, N-tile, split); this CTA takes M-tile
+  // group*CS + rank, so the cluster shares one B tile per group
   auto tile_coords = [&](int t, int& m0, int& n0, int& z) {
-    z = t / (p.mt * p.nt);
-    const int r = t - z * p.mt * p.nt;
-    n0 = (r / p.mt) * BN;  // M-fastest: neighbouring CTAs share the B (weight) tile
-    m0 = (r % p.mt) * BM;
+    z = t / (mgroups * p.nt);
+    const int r = t - z * mgroups * p.nt;
+    n0 = (r / mgroups) * BN;
+    m0 = ((r % mgroups) * CS + (int)crank) * BM;
   };
   auto k_tiles = [&](int z) {
     const int kb = z * p.k_per_split;
@@ -209,7 +248,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cl; t < ngroups; t += ncl) {
         int m0, n0, z;
         tile_coords(t, m0, n0, z);
         const int kt_n = k_tiles(z);
@@ -223,16 +262,29 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (A_MN) {
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c)
-              tma_load_2d(sa + c * 4096, &tmA, &full[s], m0 + 32 * c, k0);
+              tma_load_2d(sa + c * 4096, &tmA, &full[s], ((p.dbg & 2) ? 0 : m0) + 32 * c, k0);
           } else {
-            tma_load_2d(sa, &tmA, &full[s], k0, m0);
+            tma_load_2d(sa, &tmA, &full[s], k0, (p.dbg & 2) ? 0 : m0);
           }
-          if (B_MN) {
+          if (CS == 1) {
+            if (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 32; ++c)
-              tma_load_2d(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0);
+              for (int c = 0; c < BN / 32; ++c)
+                tma_load_2d(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0);
+            } else {
+              tma_load_2d(sb, &tmB, &full[s], k0, n0);
+            }
           } else {
-            tma_load_2d(sb, &tmB, &full[s], k0, n0);
+            // this CTA's 1/CS share of B, multicast into every CTA of the cluster
+            if (B_MN) {
+#pragma unroll
+              for (int c = (int)crank; c < BN / 32; c += CS)
+                tma_load_2d_mc(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, kMask);
+            } else {
+              constexpr int kRowsPer = BN / CS;
+              tma_load_2d_mc(sb + crank * kRowsPer * 128, &tmB, &full[s], k0,
+                             n0 + (int)crank * kRowsPer, kMask);
+            }
           }
         }
       }
@@ -245,7 +297,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                            ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
       int it = 0, local = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      for (int t = cl; t < ngroups; t += ncl, ++local) {
         int m0, n0, z;
         tile_coords(t, m0, n0, z);
         const int kt_n = k_tiles(z);
@@ -269,9 +321,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                      : smem_desc(a_base + kk * 32, 16, 1024, 2);
             const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 512, 1)
                                      : smem_desc(b_base + kk * 32, 16, 1024, 2);
-            mma_tf32(acc, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+            if (!(p.dbg & 4)) mma_tf32(acc, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
           }
-          mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+          // frees the stage (in every CTA of the cluster) once these MMAs read it
+          if (CS == 1) mma_commit(&empty[s]);
+          else mma_commit_mc(&empty[s], kMask);
         }
         mma_commit(&acc_full[b]);  // accumulator b complete
       }
@@ -293,7 +347,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t* abar = aux_bar + ew;
     uint32_t aphase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+    for (int t = cl; t < ngroups; t += ncl, ++local) {
       int m0, n0, z;
       tile_coords(t, m0, n0, z);
       const int b = local & 1;
@@ -362,7 +416,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
+        if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M && !(p.dbg & 1)) {
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                   &tmC),
@@ -385,6 +439,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  // no CTA may leave while a peer can still multicast into its smem or
+  // arrive on its barriers
+  if (CS > 1) cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
   }
@@ -437,7 +494,7 @@ int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, 
   return UL_OK;
 }
 
-template <bool A_MN, bool B_MN, int EPI, int BN>
+template <bool A_MN, bool B_MN, int EPI, int BN, int CS>
 int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_stride, int ones_col,
            cudaStream_t s) {
   CUtensorMap ma, mb, mc, mx;
@@ -445,24 +502,53 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
   if (A_MN) UL_TRY(make_map(&ma, d.A, d.M, d.K, d.lda, 32, true));
   else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM, false));
   if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32, true));
-  else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN, false));
+  else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN / CS, false));  // one CTA's share
   // C (and split-K partials stacked as [splits*M, ldc]) stored by 32x32 TMA boxes
   UL_TRY(make_map(&mc, C, d.N, (int64_t)splits * d.M, d.ldc, 32, false));
   if (EPI == kEpiEluGrad) UL_TRY(make_map(&mx, d.aux, d.N, d.M, d.ldaux, 32, false));
   else mx = mc;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
   TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, C, d.ldc, d.bias, d.aux, d.ldaux,
-           split_stride, ones_col};
-  auto kern = tc_gemm_kernel<A_MN, B_MN, EPI, BN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+           split_stride, ones_col, 0};
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("UL_TC_DBG");
+    dbg = e ? atoi(e) : 0;
+  }
+  a.dbg = dbg;
+  auto kern = tc_gemm_kernel<A_MN, B_MN, EPI, BN, CS>;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = Smem<BN>::kBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // persistent: as many clusters as can be co-resident (one CTA per SM; GPC
+  // sizes may leave SMs idle for CS > 1, so ask the occupancy API rather than
+  // queue a second wave behind the first)
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
     UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Smem<BN>::kBytes));
-    attr_set = true;
+    int n = kNumSMs / CS;
+    if (CS > 1) {
+      cfg.gridDim = dim3((unsigned)(n * CS));
+      int q = 0;
+      if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0 && q < n) n = q;
+      cudaGetLastError();
+    }
+    max_clusters = n;
   }
-  const int ntiles = mt * nt * splits;
-  const int grid = ntiles < kNumSMs ? ntiles : kNumSMs;  // persistent: one CTA per SM
-  kern<<<grid, kPThreads, Smem<BN>::kBytes, s>>>(ma, mb, mc, mx, a);
+  // a cluster of CS CTAs works on CS M-tiles that share one B tile (multicast)
+  const int ngroups = (int)ceil_div(mt, CS) * nt * splits;
+  const int grid = (ngroups < max_clusters ? ngroups : max_clusters) * CS;
+  cfg.gridDim = dim3((unsigned)grid);
+  UL_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, a));
   return check_launch("tc_gemm_kernel");
 }
 
@@ -493,12 +579,33 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   const int zs = (int)ceil_div(d.K > 0 ? d.K : 1, kps);
   // split-K partials: [zs][M][ldc] (ldc >= N, multiple of 4 for the TMA store)
   const int64_t sstride = zs > 1 ? d.M * d.ldc : 0;
-  const int bn = d.N > 128 ? 256 : 128;
+  static int bn_cap = -1;
+  if (bn_cap < 0) {
+    const char* e = getenv("UL_TC_BN");
+    bn_cap = e ? atoi(e) : 256;
+  }
+  const int bn = (d.N > 128 && bn_cap >= 256) ? 256 : 128;
   const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
-#define UL_TC_CASE(AMN, BMN, EPI)                                                             \
-  if (amn == AMN && bmn == BMN && d.epi == EPI) {                                             \
-    if (bn == 256) return tc::launch<AMN, BMN, EPI, 256>(d, zs, kps, d.C, sstride, ones_col, s); \
-    return tc::launch<AMN, BMN, EPI, 128>(d, zs, kps, d.C, sstride, ones_col, s);             \
+  // cluster size along M: B tiles are multicast to CS M-tiles.  UL_TC_CLUSTER
+  // (1, 2 or 4) caps it for experiments.
+  static int cs_cap = -1;
+  if (cs_cap < 0) {
+    const char* e = getenv("UL_TC_CLUSTER");
+    cs_cap = e ? atoi(e) : 4;
+    cs_cap = cs_cap >= 4 ? 4 : (cs_cap >= 2 ? 2 : 1);
+  }
+  const int64_t mt = ceil_div(d.M, tc::BM);
+  const int cs = (mt >= 4 && cs_cap >= 4) ? 4 : ((mt >= 2 && cs_cap >= 2) ? 2 : 1);
+#define UL_TC_BN(AMN, BMN, EPI, BN)                                                    \
+  if (cs == 4) return tc::launch<AMN, BMN, EPI, BN, 4>(d, zs, kps, d.C, sstride, ones_col, s); \
+  if (cs == 2) return tc::launch<AMN, BMN, EPI, BN, 2>(d, zs, kps, d.C, sstride, ones_col, s); \
+  return tc::launch<AMN, BMN, EPI, BN, 1>(d, zs, kps, d.C, sstride, ones_col, s);
+#define UL_TC_CASE(AMN, BMN, EPI)                 \
+  if (amn == AMN && bmn == BMN && d.epi == EPI) { \
+    if (bn == 256) {                              \
+      UL_TC_BN(AMN, BMN, EPI, 256)                \
+    }                                             \
+    UL_TC_BN(AMN, BMN, EPI, 128)                  \
   }
   UL_TC_CASE(false, false, kEpiBias)
   UL_TC_CASE(false, false, kEpiBiasElu)
@@ -507,6 +614,7 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   UL_TC_CASE(false, true, kEpiStore)
   UL_TC_CASE(true, true, kEpiStore)
 #undef UL_TC_CASE
+#undef UL_TC_BN
   set_error("gemm_tc: unsupported layout/epilogue combination");
   return UL_ERR_VALUE;
 }
