@@ -50,7 +50,7 @@ def _args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--precision", choices=("fp32", "tf32"), default=None)
+    ap.add_argument("--precision", choices=("fp32", "tf32", "bf16"), default=None)
     return ap.parse_args()
 
 
@@ -208,7 +208,8 @@ def run_ours(args):
     if args.precision:
         PKG.set_precision(args.precision)
     prec = PKG.get_precision()
-    prec_name = {"fp32": "fp32 SIMT FFMA", "tf32": "tcgen05 kind::tf32 (TMA + TMEM)"}[prec]
+    prec_name = {"fp32": "fp32 SIMT FFMA", "tf32": "tcgen05 kind::tf32 (TMA + TMEM)",
+                 "bf16": "tcgen05 kind::f16 bf16 operands, fp32 accumulation (TMA + TMEM)"}[prec]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -318,7 +319,8 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "tf32 (f32 storage/accum)",
+        "vs_baseline": None, "dtype": {"fp32": "f32", "tf32": "tf32 (f32 storage/accum)",
+                  "bf16": "bf16 GEMM operands/activations, f32 accum/params/optimizer"}[prec],
         "data": "synthetic",
         "config": {"workload": "PPO update (GAE + 5 epochs x 4 minibatches), cfg2 locomotion "
                                "shape: 4096 envs x 24 steps per GPU, obs 235 / act 12, "

@@ -134,7 +134,8 @@ int64_t ul_net_param_count(const ul_net_desc* net);
 int64_t ul_mlp_act_floats(const ul_net_desc* net, int64_t M);
 /* backward workspace floats for a batch of M rows */
 int64_t ul_mlp_bwd_work_floats(const ul_net_desc* net, int64_t M);
-/* staged-weight floats (tensor-core path: W rows padded to 16 B) */
+/* staged-weight floats (tensor-core path: W rows padded to 16 B; the bf16
+ * staging of UL_GEMM_BF16 fits in the same buffer) */
 int64_t ul_mlp_wstage_floats(const ul_net_desc* net);
 /* copy the flat W_i into the staged 16 B-row layout (call after every update) */
 int ul_stage_weights(const ul_net_desc* net, const float* params, float* wstage, void* stream);
@@ -142,6 +143,15 @@ int ul_stage_weights(const ul_net_desc* net, const float* params, float* wstage,
 /* GEMM back ends for the MLP passes */
 #define UL_GEMM_FP32 0 /* SIMT fp32 FFMA: the exact-fp32 parity path            */
 #define UL_GEMM_TF32 1 /* tcgen05.mma kind::tf32 + TMEM + TMA (needs wstage)    */
+#define UL_GEMM_BF16 2 /* tcgen05.mma kind::f16 (bf16 operands, fp32 accumulate):
+                        * x, hidden activations and hidden gradients stored bf16
+                        * (rows of round_up(d + 1, 8)); params, grads, outputs
+                        * and the upstream gradient stay fp32 (1e-2 tolerance) */
+/* activation row pitch (elements) of a hidden layer of width d for a back end */
+int64_t ul_mlp_act_ld(int d, int backend);
+/* stage W for a back end (UL_GEMM_BF16 writes bf16 rows of round_up(in, 8)) */
+int ul_stage_weights_ex(const ul_net_desc* net, const float* params, void* wstage, int backend,
+                        void* stream);
 
 /* Forward: out[M, out] (ld_out) = MLP(x[M, in] (ldx)); hidden activations are
  * cached in `acts` (ul_mlp_act_floats).  Replaces R:tensornet/mlp.py:153-172. */
@@ -166,12 +176,14 @@ int ul_gemm_f32(int layout, int epi, int64_t M, int64_t N, int64_t K, const floa
                 int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                 const float* bias, const float* aux, int64_t ldaux, void* stream);
 
-/* Same contract on the tcgen05 tensor-core kernel (kind::tf32, fp32 in/out):
- * 16 B-aligned operands, row pitches multiple of 4, M >= 128, N, K >= 32;
- * splits > 1 writes split-K partials at C + z*M*N (ld N). */
-int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A,
-               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, const float* bias,
-               const float* aux, int64_t ldaux, int splits, void* stream);
+/* Same contract on the tcgen05 tensor-core kernel.  dtype 0: fp32 operands
+ * (kind::tf32, fp32 out; M >= 128, N >= 64, K >= 32); dtype 1: bf16 operands
+ * (kind::f16; epilogues 2 and 3 read/write bf16, 0 and 1 write fp32; any
+ * shape).  16 B-aligned operands and row pitches; splits > 1 writes split-K
+ * partials [splits][M][ldc] at C. */
+int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+               const void* B, int64_t ldb, void* C, int64_t ldc, const float* bias,
+               const void* aux, int64_t ldaux, int splits, int dtype, void* stream);
 
 /* ------------------------------------------------- K4 / K5 / K6 data path */
 /* Gather rows of up to 12 arrays sharing one index vector (PPO minibatch
@@ -237,7 +249,7 @@ typedef struct ul_ppo_plan_desc {
                                        its own segment rows (weak scaling) and a
                                        global minibatch is the union of the
                                        ranks' local minibatches              */
-  int32_t gemm_backend;             /* UL_GEMM_FP32 or UL_GEMM_TF32           */
+  int32_t gemm_backend;             /* UL_GEMM_FP32 / _TF32 / _BF16           */
 } ul_ppo_plan_desc;
 
 typedef struct ul_ppo_bindings {

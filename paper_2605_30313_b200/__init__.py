@@ -7,12 +7,16 @@ __version__ = "0.1.0"
 
 def set_precision(gemm: str) -> None:
     """Select the MLP GEMM back end: "tf32" (default; tcgen05 tensor cores,
-    fp32 storage, ~1e-3 relative GEMM error) or "fp32" (SIMT FFMA, exact fp32:
-    the reference-parity configuration, R:tensornet/mlp.py is float32)."""
+    fp32 storage, ~1e-3 relative GEMM error), "bf16" (tcgen05 kind::f16 with
+    bf16 activations inside the fused PPO/APPO update plans, fp32 parameters,
+    gradients and optimizer; the north-star 1e-2 tolerance of bf16 GEMM paths)
+    or "fp32" (SIMT FFMA, exact fp32: the reference-parity configuration,
+    R:tensornet/mlp.py is float32).  Paths that need input gradients (SAC's
+    actor step, the module-level MLP backward) run "bf16" as "tf32"."""
     from . import _lib
 
-    if gemm not in ("fp32", "tf32"):
-        raise ValueError("gemm precision must be 'fp32' or 'tf32'")
+    if gemm not in ("fp32", "tf32", "bf16"):
+        raise ValueError("gemm precision must be 'fp32', 'tf32' or 'bf16'")
     _lib._PRECISION["gemm"] = gemm
 
 

@@ -20,14 +20,20 @@ UL_PREP_BLOCKS = 296
 UL_MAX_ACT = 64
 UL_GEMM_FP32 = 0
 UL_GEMM_TF32 = 1
+UL_GEMM_BF16 = 2
 
 # Process-wide GEMM back end of the MLP passes ("fp32": SIMT exact-fp32 parity
 # path; "tf32": tcgen05 tensor cores).  See paper_2605_30313_b200.set_precision.
 _PRECISION = {"gemm": "tf32"}
 
 
-def gemm_backend() -> int:
-    return UL_GEMM_TF32 if _PRECISION["gemm"] == "tf32" else UL_GEMM_FP32
+def gemm_backend(input_grads: bool = False) -> int:
+    """C back end code of the selected precision; `input_grads` callers (which
+    need dX through the network) get tf32 in place of bf16."""
+    g = _PRECISION["gemm"]
+    if g == "bf16":
+        return UL_GEMM_TF32 if input_grads else UL_GEMM_BF16
+    return UL_GEMM_TF32 if g == "tf32" else UL_GEMM_FP32
 
 vp = C.c_void_p
 i64 = C.c_int64
@@ -129,6 +135,8 @@ _PROTOS = {
     "ul_mlp_bwd_work_floats": (i64, [C.POINTER(NetDesc), i64]),
     "ul_mlp_wstage_floats": (i64, [C.POINTER(NetDesc)]),
     "ul_stage_weights": (C.c_int, [C.POINTER(NetDesc), vp, vp, vp]),
+    "ul_stage_weights_ex": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp]),
+    "ul_mlp_act_ld": (i64, [C.c_int, C.c_int]),
     "ul_mlp_forward": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp, i64, i64, vp, vp, i64,
                                  vp]),
     "ul_mlp_backward": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp, i64, C.c_int, i64, vp,
@@ -136,7 +144,7 @@ _PROTOS = {
     "ul_gemm_f32": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
                               vp, i64, vp]),
     "ul_gemm_tc": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
-                             vp, i64, C.c_int, vp]),
+                             vp, i64, C.c_int, C.c_int, vp]),
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                  C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
                                  vp]),

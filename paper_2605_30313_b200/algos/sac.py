@@ -120,7 +120,7 @@ class _SacPlan:
         d.gamma, d.tau = cfg.gamma, cfg.tau
         d.target_entropy = -cfg.target_entropy_ratio * state.action_dim
         d.max_grad_norm = cfg.max_grad_norm
-        d.gemm_backend = _lib.gemm_backend()
+        d.gemm_backend = _lib.gemm_backend(input_grads=True)
         h = C.c_void_p()
         _lib.call("ul_sac_plan_create", C.byref(d), C.byref(h))
         self.h, self.desc, self.batch = h, d, batch
@@ -162,7 +162,7 @@ _PLANS: dict = {}
 def _plan_for(state: SacState, batch: int, cfg: SacConfig) -> _SacPlan:
     p = state.params
     key = (p.actor.arch, p.q1.arch, batch, cfg.gamma, cfg.tau, cfg.target_entropy_ratio,
-           cfg.max_grad_norm, _lib.gemm_backend(), torch.cuda.current_device())
+           cfg.max_grad_norm, _lib.gemm_backend(input_grads=True), torch.cuda.current_device())
     plan = _PLANS.get(key)
     if plan is None:
         plan = _SacPlan(state, batch, cfg)

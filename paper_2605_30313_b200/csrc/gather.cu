@@ -10,6 +10,8 @@
 // warp always streams contiguous bytes of a row, whatever the row width
 // (obs 940 B, actions 48 B, scalars 4 B).  Algorithmic bytes: 2 x rows x
 // row_bytes + 8 B/index.
+#include <cuda_bf16.h>
+
 #include "internal.cuh"
 
 namespace ul {
@@ -25,6 +27,7 @@ struct GatherTable {
   int64_t units[kMaxDesc];       // units per row
   int unit[kMaxDesc];            // unit bytes (16, 8 or 4)
   int64_t ones[kMaxDesc];        // byte offset of a float set to 1.0 in each row, -1 none
+  int cvt[kMaxDesc];             // 1: fp32 source rows -> bf16 destination rows
   int ndesc;
 };
 
@@ -81,10 +84,61 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
   }
 }
 
+// fp32 -> bf16 rows (the bf16 MLP path's minibatch input): 16-byte source
+// units become 8-byte destination units
+__device__ __forceinline__ void copy_rows_bf16(const char* __restrict__ src,
+                                               char* __restrict__ dst, int64_t sst, int64_t dstr,
+                                               int64_t upr, const int64_t* __restrict__ idx,
+                                               int64_t n, int64_t modulo, int64_t lo, int64_t hi,
+                                               int* err, int64_t ones) {
+  constexpr int kIlp = 4;
+  const int64_t total = n * upr;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < total;
+       w0 += stride * kIlp) {
+    float4 v[kIlp];
+    int64_t drow[kIlp], du[kIlp];
+    bool ok[kIlp];
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      const int64_t w = w0 + k * stride;
+      ok[k] = false;
+      if (w >= total) continue;
+      const int64_t r = w / upr, u = w - r * upr;
+      int64_t s = idx ? __ldg(idx + r) : r;
+      drow[k] = r;
+      du[k] = u;
+      if (s < lo || s >= hi) {
+        if (err) atomicOr(err, 1);
+        continue;
+      }
+      if (modulo > 0) s %= modulo;
+      v[k] = __ldg(reinterpret_cast<const float4*>(src + s * sst) + u);
+      ok[k] = true;
+    }
+#pragma unroll
+    for (int k = 0; k < kIlp; ++k) {
+      if (!ok[k]) continue;
+      float f[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+      if (ones >= 0 && ones / 16 == du[k]) f[(ones % 16) / 4] = 1.f;
+      __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&a);
+      o.y = *reinterpret_cast<uint32_t*>(&b);
+      reinterpret_cast<uint2*>(dst + drow[k] * dstr)[du[k]] = o;
+    }
+  }
+}
+
 __global__ void gather_kernel(GatherTable t, const int64_t* __restrict__ idx, int64_t n,
                               int64_t modulo, int64_t lo, int64_t hi, int* err) {
   const int d = blockIdx.y;
   if (d >= t.ndesc) return;
+  if (t.cvt[d]) {
+    copy_rows_bf16(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
+                   modulo, lo, hi, err, t.ones[d]);
+    return;
+  }
   switch (t.unit[d]) {
     case 16:
       copy_rows<16>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
@@ -143,6 +197,53 @@ __global__ void feistel_perm_kernel(int64_t n, int half_bits, uint64_t seed, int
 }  // namespace
 }  // namespace ul
 
+namespace ul {
+// Gather rows of up to 12 arrays by one index vector (see ul_gather_rows);
+// cvt (may be null): per desc, 1 = fp32 source rows written as bf16 (row_bytes
+// counts source bytes, a multiple of 16; destination rows are half as wide).
+int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64_t* src_stride,
+                const int64_t* dst_stride, const int64_t* row_bytes, const int64_t* ones_byte,
+                const int* cvt, const int64_t* idx, int64_t n, int64_t modulo, int64_t lo,
+                int64_t hi, int* err, cudaStream_t stream) {
+  UL_CHECK_ARG(ndesc >= 1 && ndesc <= kMaxDesc, "gather: ndesc %d outside [1,%d]", ndesc,
+               kMaxDesc);
+  UL_CHECK_ARG(n >= 0, "gather: negative row count");
+  if (n == 0) return UL_OK;
+  GatherTable t{};
+  t.ndesc = ndesc;
+  int64_t max_units = 1;
+  for (int d = 0; d < ndesc; ++d) {
+    const int c = cvt ? cvt[d] : 0;
+    int u;
+    if (c) {
+      UL_CHECK_ARG(((uintptr_t)src[d] & 15) == 0 && ((uintptr_t)dst[d] & 7) == 0 &&
+                       src_stride[d] % 16 == 0 && dst_stride[d] % 8 == 0 && row_bytes[d] % 16 == 0,
+                   "gather: bf16 conversion needs 16-byte source rows (desc %d)", d);
+      u = 16;
+    } else {
+      u = unit_for((uintptr_t)src[d], (uintptr_t)dst[d], src_stride[d], dst_stride[d],
+                   row_bytes[d]);
+    }
+    UL_CHECK_ARG(u > 0, "gather: desc %d not 4-byte aligned", d);
+    t.src[d] = (const char*)src[d];
+    t.dst[d] = (char*)dst[d];
+    t.src_stride[d] = src_stride[d];
+    t.dst_stride[d] = dst_stride[d];
+    t.unit[d] = u;
+    t.units[d] = row_bytes[d] / u;
+    t.cvt[d] = c;
+    t.ones[d] = ones_byte ? ones_byte[d] : -1;
+    UL_CHECK_ARG(t.ones[d] < row_bytes[d], "gather: ones column outside the row");
+    max_units = t.units[d] > max_units ? t.units[d] : max_units;
+  }
+  int64_t blocks = ceil_div(n * max_units, 256);
+  blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
+  gather_kernel<<<dim3((unsigned)blocks, ndesc), 256, 0, stream>>>(t, idx, n, modulo, lo, hi,
+                                                                    err);
+  return check_launch("gather_kernel");
+}
+}  // namespace ul
+
 // Gather rows of up to 12 arrays by one index vector.  desc arrays have ndesc
 // entries: src/dst device pointers, strides and row widths in BYTES.  Rows are
 // src + (idx[i] [% modulo]) * src_stride.  Indices outside [lo, hi) are
@@ -152,32 +253,8 @@ extern "C" int ul_gather_rows(int ndesc, const void* const* src, void* const* ds
                               const int64_t* row_bytes, const int64_t* ones_byte,
                               const int64_t* idx, int64_t n,
                               int64_t modulo, int64_t lo, int64_t hi, int* err, void* stream) {
-  UL_CHECK_ARG(ndesc >= 1 && ndesc <= ul::kMaxDesc, "gather: ndesc %d outside [1,%d]", ndesc,
-               ul::kMaxDesc);
-  UL_CHECK_ARG(n >= 0, "gather: negative row count");
-  if (n == 0) return UL_OK;
-  ul::GatherTable t{};
-  t.ndesc = ndesc;
-  int64_t max_units = 1;
-  for (int d = 0; d < ndesc; ++d) {
-    const int u = ul::unit_for((uintptr_t)src[d], (uintptr_t)dst[d], src_stride[d], dst_stride[d],
-                               row_bytes[d]);
-    UL_CHECK_ARG(u > 0, "gather: desc %d not 4-byte aligned", d);
-    t.src[d] = (const char*)src[d];
-    t.dst[d] = (char*)dst[d];
-    t.src_stride[d] = src_stride[d];
-    t.dst_stride[d] = dst_stride[d];
-    t.unit[d] = u;
-    t.units[d] = row_bytes[d] / u;
-    t.ones[d] = ones_byte ? ones_byte[d] : -1;
-    UL_CHECK_ARG(t.ones[d] < row_bytes[d], "gather: ones column outside the row");
-    max_units = t.units[d] > max_units ? t.units[d] : max_units;
-  }
-  int64_t blocks = ul::ceil_div(n * max_units, 256);
-  blocks = blocks > 4 * ul::kNumSMs ? 4 * ul::kNumSMs : blocks;
-  ul::gather_kernel<<<dim3((unsigned)blocks, ndesc), 256, 0, ul::as_stream(stream)>>>(
-      t, idx, n, modulo, lo, hi, err);
-  return ul::check_launch("gather_kernel");
+  return ul::gather_rows(ndesc, src, dst, src_stride, dst_stride, row_bytes, ones_byte, nullptr,
+                         idx, n, modulo, lo, hi, err, ul::as_stream(stream));
 }
 
 // Replay ring insert (R:replaypath/storage.py:76-104): write n rows of `width`

@@ -1,18 +1,25 @@
 // K7/K8 tensor-core path: tcgen05 (5th-gen tensor core) + TMEM + TMA GEMM for sm_100a.
 //
-// C[M,N] = A(M,K) B(K,N) with kind::tf32 MMAs reading the fp32 HBM buffers
-// directly (no conversion pass): TMA streams 128-byte-swizzled [rows x 32]
-// fp32 tiles into a STAGES-deep shared-memory ring, one elected thread issues
-// tcgen05.mma (UMMA M=128, N=BN, K=8) into a TMEM accumulator, and four
-// epilogue warps drain TMEM with tcgen05.ld and apply the fused MLP epilogue
-// (bias / ELU / ELU-gradient / split-K partial store).  Operands may be
-// K-major or MN-major (the MLP's dX and dW GEMMs read W and the activations
-// transposed; UMMA's MN-major smem descriptors absorb that, nothing is
-// transposed in HBM).
-//   warp 0      : TMA producer            (one elected lane)
-//   warp 1      : TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  : epilogue (TMEM lane quarter = warp % 4)
+// C[M,N] = A(M,K) B(K,N) with fp32 accumulation in TMEM, two operand types:
+//   * fp32 storage read as kind::tf32 (UMMA K = 8), no conversion pass;
+//   * bf16 storage read as kind::f16 / bf16 (UMMA K = 16): the MLP's bf16
+//     activation path, half the operand bytes of tf32 per FLOP.
+// TMA streams 128-byte-swizzled [rows x 128 B] tiles into a STAGES-deep
+// shared-memory ring, one elected thread issues tcgen05.mma (UMMA M=128,
+// N=BN) into a double-buffered TMEM accumulator, and 16 epilogue warps drain
+// TMEM with tcgen05.ld and apply the fused MLP epilogue (bias / ELU /
+// ELU-gradient / split-K partial store), leaving through TMA stores.
+// Operands may be K-major or MN-major (the MLP's dX and dW GEMMs read W and
+// the activations transposed; UMMA's MN-major smem descriptors absorb that,
+// nothing is transposed in HBM).
+//   warp 0       : TMA producer               (one elected lane)
+//   warp 1       : TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..17  : epilogue (TMEM lane quarter = warp % 4, BN/4 column slice)
+// Output type: bf16 for the hidden-layer epilogues of the bf16 path (the next
+// GEMM's operand), fp32 otherwise (split-K dW partials, output layers).
 #include <cuda.h>
+#include <cuda_bf16.h>
+
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -20,7 +27,24 @@
 namespace ul {
 namespace tc {
 
-constexpr int BM = 128, BK = 32;  // BK fp32 = 128 B = one swizzle row
+constexpr int BM = 128;
+
+// operand traits: one 128-byte swizzle row holds BK elements of K
+template <typename T>
+struct Op;
+template <>
+struct Op<float> {
+  static constexpr int kBytes = 4, BK = 32, kChunk = 32;  // kChunk: MN elements per 128 B
+  static constexpr uint32_t kFmt = 2;                      // TF32
+  // MN-major: 32-byte swizzle atoms (the only legal MN-major tf32 layout)
+  static constexpr uint32_t kMnLayout = 1, kMnSbo = 512, kMnKStep = 1024;
+};
+template <>
+struct Op<__nv_bfloat16> {
+  static constexpr int kBytes = 2, BK = 64, kChunk = 64;
+  static constexpr uint32_t kFmt = 1;  // BF16 under kind::f16
+  static constexpr uint32_t kMnLayout = 2, kMnSbo = 1024, kMnKStep = 2048;
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -40,6 +64,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 // of hanging the GPU until the host-side timeout.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
+#pragma unroll 1
   for (uint32_t spin = 0; spin < (1u << 26); ++spin) {
     asm volatile(
         "{\n"
@@ -64,9 +89,26 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
 // UMMA shared-memory matrix descriptor, sm100 version bit.  Layout type 2 =
-// SWIZZLE_128B (16-byte atoms; K-major tiles), 1 = SWIZZLE_128B_BASE32B
-// (32-byte atoms; the only legal layout for MN-major tf32 operands).
+// SWIZZLE_128B (16-byte atoms), 1 = SWIZZLE_128B_BASE32B (32-byte atoms).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
                                               uint32_t layout) {
   uint64_t d = 0;
@@ -78,21 +120,45 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
-                                         uint32_t acc) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+template <typename T>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                    uint32_t acc) {
+  if constexpr (sizeof(T) == 4) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  }
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    su32(bar))
                : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
@@ -110,79 +176,70 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
 }
 
 // ELU on the tensor-core path: exp via ex2.approx (abs. error ~1e-7 near 0,
-// far inside the tf32 GEMM error; the fp32 parity path keeps expm1f)
+// far inside the tf32/bf16 GEMM error; the fp32 parity path keeps expm1f)
 __device__ __forceinline__ float elu_fast(float z) {
   const float e = __expf(fmaxf(z, -60.f)) - 1.f;
   return z > 0.f ? z : e;
 }
 
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+
 struct TcArgs {
   int M, N, K;
   int k_per_split;  // multiple of BK
   int mt, nt, zt;   // tile counts (M, N, K-split)
-  float* C;
+  void* C;          // output element type: see OutT
   int64_t ldc;
   const float* bias;
-  const float* aux;
-  int64_t ldaux;
-  int64_t split_stride;  // elements between split partial tiles
-  int ones_col;          // >= 0: also write C[m, ones_col] = 1 (dW bias trick)
-  int dbg;               // diagnostics (UL_TC_DBG): 1 no C store, 2 A from tile 0, 4 no MMA
+  int ones_col;          // >= 0: also write C[m, ones_col] = 1 (activation ones column)
 };
 
 constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
 constexpr int kPThreads = (2 + kEpiWarps) * 32;
 
+// bf16 operands -> bf16 hidden activations / gradients; everything else fp32
+template <typename TI, int EPI>
+using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu || EPI == kEpiEluGrad),
+                                       __nv_bfloat16, float>::type;
+
 // [stage ring][16 x 4 KB epilogue staging][barriers][bias x 2]
 template <int BN>
 struct Smem {
   static constexpr int kStages = BN >= 256 ? 3 : 4;
-  static constexpr int kABytes = BM * BK * 4;  // 16 KB
-  static constexpr int kBBytes = BN * BK * 4;
+  static constexpr int kABytes = BM * 128;
+  static constexpr int kBBytes = BN * 128;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStagingBytes = kEpiWarps * 4096;
   static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + 1024 /*align*/ +
                                 512 /*barriers*/ + 2 * BN * 4 /*bias, per accumulator*/;
 };
 
-// Persistent: grid = min(#tiles, #SMs); tile t = blockIdx.x + i * gridDim.x
-// walks (m, n, split) tiles.  The smem ring runs continuously across tiles and
-// the TMEM accumulator is double-buffered, so tile i's epilogue overlaps tile
-// i+1's TMA + MMA main loop.
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                               int c0, int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(su32(dst)),
-      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(su32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
-                   "memory");
-}
-
+// Persistent: the grid is sized to the co-resident CTAs; tile groups are
+// walked with a cluster-strided loop.  The smem ring runs continuously across
+// tiles and the TMEM accumulator is double-buffered, so tile i's epilogue
+// overlaps tile i+1's TMA + MMA main loop.
+//
 // CS = cluster size along M.  The CS CTAs of a cluster work on CS consecutive
 // M-tiles of the same (N-tile, K-split) and share its B tile: CTA r fetches
-// 1/CS of B and TMA-multicasts it into every CTA of the cluster, so B leaves
-// L2 once per cluster instead of once per M-tile.  A stage is refilled only
-// after every CTA's MMAs consumed it (empty barriers count CS multicast
-// commits).
-template <bool A_MN, bool B_MN, int EPI, int BN, int CS>
+// 1/CS of B and TMA-multicasts it into every CTA of the cluster.  A stage is
+// refilled only after every CTA's MMAs consumed it (empty barriers count CS
+// multicast commits).
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, int CS>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                    TcArgs p) {
   using S = Smem<BN>;
+  using O = Op<TI>;
+  using TO = OutT<TI, EPI>;
+  constexpr bool kOutBf16 = sizeof(TO) == 2;
+  constexpr int BK = O::BK;
+  constexpr uint32_t kChunkBytes = (uint32_t)BK * 128;  // one MN-major TMA box
   constexpr int kStages = S::kStages;
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
   extern __shared__ uint8_t smem_raw[];
@@ -193,7 +250,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
-  uint64_t* aux_bar = acc_empty + 2;  // [kEpiWarps]
+  uint64_t* aux_bar = acc_empty + 2;     // [kEpiWarps]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -208,7 +265,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CS);  // one multicast MMA commit from every CTA of the cluster
+      mbar_init(&empty[s], CS);  // one (multicast) MMA commit from every CTA of the cluster
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -217,6 +274,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&aux_bar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -261,16 +322,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const int k0 = z * p.k_per_split + kt * BK;
           if (A_MN) {
 #pragma unroll
-            for (int c = 0; c < BM / 32; ++c)
-              tma_load_2d(sa + c * 4096, &tmA, &full[s], ((p.dbg & 2) ? 0 : m0) + 32 * c, k0);
+            for (int c = 0; c < BM / O::kChunk; ++c)
+              tma_load_2d(sa + c * kChunkBytes, &tmA, &full[s], m0 + O::kChunk * c, k0);
           } else {
-            tma_load_2d(sa, &tmA, &full[s], k0, (p.dbg & 2) ? 0 : m0);
+            tma_load_2d(sa, &tmA, &full[s], k0, m0);
           }
           if (CS == 1) {
             if (B_MN) {
 #pragma unroll
-              for (int c = 0; c < BN / 32; ++c)
-                tma_load_2d(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0);
+              for (int c = 0; c < BN / O::kChunk; ++c)
+                tma_load_2d(sb + c * kChunkBytes, &tmB, &full[s], n0 + O::kChunk * c, k0);
             } else {
               tma_load_2d(sb, &tmB, &full[s], k0, n0);
             }
@@ -278,8 +339,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // this CTA's 1/CS share of B, multicast into every CTA of the cluster
             if (B_MN) {
 #pragma unroll
-              for (int c = (int)crank; c < BN / 32; c += CS)
-                tma_load_2d_mc(sb + c * 4096, &tmB, &full[s], n0 + 32 * c, k0, kMask);
+              for (int c = (int)crank; c < BN / O::kChunk; c += CS)
+                tma_load_2d_mc(sb + c * kChunkBytes, &tmB, &full[s], n0 + O::kChunk * c, k0,
+                               kMask);
             } else {
               constexpr int kRowsPer = BN / CS;
               tma_load_2d_mc(sb + crank * kRowsPer * 128, &tmB, &full[s], k0,
@@ -291,10 +353,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    // instruction descriptor: f32 accum, tf32 A/B, majors, N>>3, M>>4
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                           ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+    // instruction descriptor: f32 accum, A/B format, majors, N>>3, M>>4
+    const uint32_t idesc = (1u << 4) | (O::kFmt << 7) | (O::kFmt << 10) |
+                           ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
       int it = 0, local = 0;
       for (int t = cl; t < ngroups; t += ncl, ++local) {
@@ -312,16 +374,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t a_base = su32(smem + s * S::kStageBytes);
           const uint32_t b_base = a_base + S::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            // K-major: 8-row x 128 B swizzle atoms (SBO 1024), K step = +32 B.
-            // MN-major: 128 B of M/N per row, 4-row x 128 B atoms with 32 B
-            // swizzle granules (SBO 512), 32-element M/N chunks 4 KB apart
-            // (LBO), K step = 8 rows = +1024 B.
-            const uint64_t da = A_MN ? smem_desc(a_base + kk * 1024, 4096, 512, 1)
+          for (int kk = 0; kk < 4; ++kk) {
+            // K-major: 8-row x 128 B swizzle atoms (SBO 1024), one UMMA K step
+            // = 32 B along the row.  MN-major: 128 B of M/N per smem row,
+            // chunks of kChunk M/N elements kChunkBytes apart (LBO), one UMMA
+            // K step = 8 (tf32) / 16 (bf16) rows.
+            const uint64_t da = A_MN ? smem_desc(a_base + kk * O::kMnKStep, kChunkBytes,
+                                                 O::kMnSbo, O::kMnLayout)
                                      : smem_desc(a_base + kk * 32, 16, 1024, 2);
-            const uint64_t db = B_MN ? smem_desc(b_base + kk * 1024, 4096, 512, 1)
+            const uint64_t db = B_MN ? smem_desc(b_base + kk * O::kMnKStep, kChunkBytes,
+                                                 O::kMnSbo, O::kMnLayout)
                                      : smem_desc(b_base + kk * 32, 16, 1024, 2);
-            if (!(p.dbg & 4)) mma_tf32(acc, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+            mma<TI>(acc, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
           }
           // frees the stage (in every CTA of the cluster) once these MMAs read it
           if (CS == 1) mma_commit(&empty[s]);
@@ -334,14 +398,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ------------------------------------------------------------ epilogue
     // 16 warps: TMEM lane quarter = warp % 4 (hardware rule), column slice =
     // (warp - 2) / 4 of four BN/4-wide slices.  Per 32-column group each warp
-    // owns a 32 x 32 fp32 staging tile (4 KB, 128 B swizzle): the ELU-gradient
-    // operand arrives there by TMA, results leave by TMA store (full 128 B
-    // lines instead of thread-per-row scattered stores).
+    // owns a 32 x 32 staging tile (fp32: 4 KB, 128 B swizzle; bf16: 2 KB,
+    // 64 B swizzle): the ELU-gradient operand arrives there by TMA, results
+    // leave by TMA store (full lines instead of thread-per-row scattered
+    // stores).
     const int ew = warp - 2;
     const int quarter = warp & 3;
     const int slice = ew >> 2;
     const int row = quarter * 32 + lane;
     constexpr int kSlice = BN / 4;
+    constexpr uint32_t kBoxBytes = 32 * 32 * sizeof(TO);
     float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
     uint8_t* stg = smem + kStages * S::kStageBytes + ew * 4096;
     uint64_t* abar = aux_bar + ew;
@@ -362,7 +428,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + row;
-      const int crow = z * p.M + m0 + quarter * 32;  // row of this warp's 32-row box in C
+      const int crow = m0 + quarter * 32;  // row of this warp's 32-row box in C (split z)
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
       for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 32) {
@@ -371,8 +437,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
         __syncwarp();
         if (EPI == kEpiEluGrad) {
           if (lane == 0) {
-            mbar_expect_tx(abar, 4096);
-            tma_load_2d(stg, &tmX, abar, n0 + c0, m0 + quarter * 32);
+            mbar_expect_tx(abar, kBoxBytes);
+            tma_load_3d(stg, &tmX, abar, n0 + c0, m0 + quarter * 32, 0);
           }
         }
         float v[32];
@@ -398,35 +464,66 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = elu_fast(v[i]);
         }
-        float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
-        if (EPI == kEpiEluGrad) {
-          mbar_wait(abar, aphase);
-          aphase ^= 1;
+        if constexpr (!kOutBf16) {
+          // 32 rows x 128 B, 128 B swizzle: 16 B granule q of row r at q ^ (r & 7)
+          float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
+          if (EPI == kEpiEluGrad) {
+            mbar_wait(abar, aphase);
+            aphase ^= 1;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 h4 = srow[q ^ (lane & 7)];
-            v[4 * q] *= elu_grad_from_act(h4.x);
-            v[4 * q + 1] *= elu_grad_from_act(h4.y);
-            v[4 * q + 2] *= elu_grad_from_act(h4.z);
-            v[4 * q + 3] *= elu_grad_from_act(h4.w);
+            for (int q = 0; q < 8; ++q) {
+              const float4 h4 = srow[q ^ (lane & 7)];
+              v[4 * q] *= elu_grad_from_act(h4.x);
+              v[4 * q + 1] *= elu_grad_from_act(h4.y);
+              v[4 * q + 2] *= elu_grad_from_act(h4.z);
+              v[4 * q + 3] *= elu_grad_from_act(h4.w);
+            }
           }
-        }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          srow[q ^ (lane & 7)] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int q = 0; q < 8; ++q)
+            srow[q ^ (lane & 7)] =
+                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+          // 32 rows x 64 B, 64 B swizzle: 16 B granule q of row r at q ^ ((r >> 1) & 3)
+          uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
+          const int sw = (lane >> 1) & 3;
+          if (EPI == kEpiEluGrad) {
+            mbar_wait(abar, aphase);
+            aphase ^= 1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 h = srow[q ^ sw];
+              const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                v[8 * q + 2 * e] *= elu_grad_from_act(bf_lo(hw[e]));
+                v[8 * q + 2 * e + 1] *= elu_grad_from_act(bf_hi(hw[e]));
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            srow[q ^ sw] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]),
+                                      pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                      pack_bf16(v[8 * q + 4], v[8 * q + 5]),
+                                      pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M && !(p.dbg & 1)) {
+        if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
+          // 3-D map [splits][M][N]: a box never spills into the next split's rows
           asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+              "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                   &tmC),
-              "r"(su32(stg)), "r"(n0 + c0), "r"(crow)
+              "r"(su32(stg)), "r"(n0 + c0), "r"(crow), "r"(z)
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
-      if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M)
-        p.C[(int64_t)m * p.ldc + p.ones_col] = 1.f;
+      if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M) {
+        TO* cp = reinterpret_cast<TO*>(p.C);
+        cp[(int64_t)m * p.ldc + p.ones_col] = (TO)1.f;
+      }
       // release accumulator buffer b to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -466,27 +563,31 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 2-D fp32 tensor map: inner (contiguous) extent, outer extent, row pitch
-// (elements), box {32, box_outer}, 128-byte swizzle, OOB -> zero.
-int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t ld,
-             int box_outer, bool mn_major) {
+// 2-D (planes == 0) or 3-D tensor map over a row-major [planes][outer][inner]
+// array with row pitch `ld` elements and plane pitch outer * ld; box
+// {box_inner, box_outer(, 1)}; OOB -> zero.
+int make_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t inner, int64_t outer,
+             int64_t ld, int box_inner, int box_outer, CUtensorMapSwizzle sw,
+             int64_t planes = 0) {
   EncodeFn fn = encode_fn();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return UL_ERR_CUDA;
   }
-  if (((uintptr_t)base & 15) || ((ld * 4) & 15)) {
+  if (((uintptr_t)base & 15) || ((ld * elem_bytes) & 15)) {
     set_error("tensor map: base/pitch not 16-byte aligned");
     return UL_ERR_VALUE;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-  cuuint32_t box[2] = {32u, (cuuint32_t)box_outer};
-  cuuint32_t es[2] = {1u, 1u};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * elem_bytes), (cuuint64_t)(outer * ld * elem_bytes)};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1u};
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  CUresult r = fn(map,
+                  elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  planes > 0 ? 3 : 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
     return UL_ERR_CUDA;
@@ -494,29 +595,30 @@ int make_map(CUtensorMap* map, const float* base, int64_t inner, int64_t outer, 
   return UL_OK;
 }
 
-template <bool A_MN, bool B_MN, int EPI, int BN, int CS>
-int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_stride, int ones_col,
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, int CS>
+int launch(const GemmDesc& d, int splits, int kps, int ones_col,
            cudaStream_t s) {
+  using O = Op<TI>;
+  using TO = OutT<TI, EPI>;
+  constexpr int eb = O::kBytes, ob = (int)sizeof(TO);
+  const CUtensorMapSwizzle mn_sw =
+      eb == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const CUtensorMapSwizzle out_sw = ob == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   CUtensorMap ma, mb, mc, mx;
   // A(m,k): K-major -> rows=M, inner=K ; MN-major -> rows=K, inner=M
-  if (A_MN) UL_TRY(make_map(&ma, d.A, d.M, d.K, d.lda, 32, true));
-  else UL_TRY(make_map(&ma, d.A, d.K, d.M, d.lda, BM, false));
-  if (B_MN) UL_TRY(make_map(&mb, d.B, d.N, d.K, d.ldb, 32, true));
-  else UL_TRY(make_map(&mb, d.B, d.K, d.N, d.ldb, BN / CS, false));  // one CTA's share
+  if (A_MN) UL_TRY(make_map(&ma, d.A, eb, d.M, d.K, d.lda, O::kChunk, O::BK, mn_sw));
+  else UL_TRY(make_map(&ma, d.A, eb, d.K, d.M, d.lda, O::BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
+  if (B_MN) UL_TRY(make_map(&mb, d.B, eb, d.N, d.K, d.ldb, O::kChunk, O::BK, mn_sw));
+  else  // one CTA's share of the B tile
+    UL_TRY(make_map(&mb, d.B, eb, d.K, d.N, d.ldb, O::BK, BN / CS, CU_TENSOR_MAP_SWIZZLE_128B));
   // C (and split-K partials stacked as [splits*M, ldc]) stored by 32x32 TMA boxes
-  UL_TRY(make_map(&mc, C, d.N, (int64_t)splits * d.M, d.ldc, 32, false));
-  if (EPI == kEpiEluGrad) UL_TRY(make_map(&mx, d.aux, d.N, d.M, d.ldaux, 32, false));
+  UL_TRY(make_map(&mc, d.C, ob, d.N, d.M, d.ldc, 32, 32, out_sw, splits));
+  if (EPI == kEpiEluGrad) UL_TRY(make_map(&mx, d.aux, ob, d.N, d.M, d.ldaux, 32, 32, out_sw, 1));
   else mx = mc;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
-  TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, C, d.ldc, d.bias, d.aux, d.ldaux,
-           split_stride, ones_col, 0};
-  static int dbg = -1;
-  if (dbg < 0) {
-    const char* e = getenv("UL_TC_DBG");
-    dbg = e ? atoi(e) : 0;
-  }
-  a.dbg = dbg;
-  auto kern = tc_gemm_kernel<A_MN, B_MN, EPI, BN, CS>;
+  TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, d.C, d.ldc, d.bias,
+           ones_col};
+  auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, CS>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
   cfg.dynamicSmemBytes = Smem<BN>::kBytes;
@@ -552,54 +654,22 @@ int launch(const GemmDesc& d, int splits, int kps, float* C, int64_t split_strid
   return check_launch("tc_gemm_kernel");
 }
 
-}  // namespace tc
-
-bool tc_eligible(const GemmDesc& d) {
-  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  return d.M >= 128 && d.N >= 64 && d.K >= 32 && d.M < (1ll << 31) && d.N < (1ll << 31) &&
-         d.K < (1ll << 31) && al(d.A) && al(d.B) && al(d.C) && (d.lda % 4 == 0) &&
-         (d.ldb % 4 == 0) && (d.ldc % 4 == 0) &&
-         (d.epi != kEpiEluGrad || (al(d.aux) && d.ldaux % 4 == 0)) &&
-         !(d.a_kmajor == false && d.b_kmajor == true);
-}
-
-int tc_num_splits(int64_t K, int splits) {
-  splits = splits < 1 ? 1 : splits;
-  const int64_t kps = ceil_div(ceil_div(K, splits), tc::BK) * tc::BK;
-  return (int)ceil_div(K > 0 ? K : 1, kps);
-}
-
-// Same contract as gemm_f32 (split partials of ld N at C + z*M*N when
-// splits > 1); `ones_col` >= 0 additionally writes 1.0 into that column.
-int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
-  if (d.M == 0 || d.N == 0) return UL_OK;
-  if (ones_col < 0) ones_col = d.ones_col;
-  const int splits = d.splits < 1 ? 1 : d.splits;
-  const int kps = (int)(ceil_div(ceil_div(d.K, splits), tc::BK) * tc::BK);
-  const int zs = (int)ceil_div(d.K > 0 ? d.K : 1, kps);
-  // split-K partials: [zs][M][ldc] (ldc >= N, multiple of 4 for the TMA store)
-  const int64_t sstride = zs > 1 ? d.M * d.ldc : 0;
-  static int bn_cap = -1;
-  if (bn_cap < 0) {
-    const char* e = getenv("UL_TC_BN");
-    bn_cap = e ? atoi(e) : 256;
-  }
-  const int bn = (d.N > 128 && bn_cap >= 256) ? 256 : 128;
+template <typename TI>
+int dispatch(const GemmDesc& d, int zs, int kps, int ones_col, cudaStream_t s) {
+  const int bn = d.N > 128 ? 256 : 128;
   const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
-  // cluster size along M: B tiles are multicast to CS M-tiles.  UL_TC_CLUSTER
-  // (1, 2 or 4) caps it for experiments.
+  // cluster size along M (B tile multicast to CS M-tiles).  UL_TC_CLUSTER=1
+  // disables it (experiments).
   static int cs_cap = -1;
   if (cs_cap < 0) {
     const char* e = getenv("UL_TC_CLUSTER");
-    cs_cap = e ? atoi(e) : 4;
-    cs_cap = cs_cap >= 4 ? 4 : (cs_cap >= 2 ? 2 : 1);
+    cs_cap = e ? atoi(e) : 2;
   }
-  const int64_t mt = ceil_div(d.M, tc::BM);
-  const int cs = (mt >= 4 && cs_cap >= 4) ? 4 : ((mt >= 2 && cs_cap >= 2) ? 2 : 1);
-#define UL_TC_BN(AMN, BMN, EPI, BN)                                                    \
-  if (cs == 4) return tc::launch<AMN, BMN, EPI, BN, 4>(d, zs, kps, d.C, sstride, ones_col, s); \
-  if (cs == 2) return tc::launch<AMN, BMN, EPI, BN, 2>(d, zs, kps, d.C, sstride, ones_col, s); \
-  return tc::launch<AMN, BMN, EPI, BN, 1>(d, zs, kps, d.C, sstride, ones_col, s);
+  const int64_t mt = ceil_div(d.M, BM);
+  const int cs = (mt >= 2 && cs_cap >= 2) ? 2 : 1;
+#define UL_TC_BN(AMN, BMN, EPI, BN)                                                     \
+  if (cs == 2) return launch<TI, AMN, BMN, EPI, BN, 2>(d, zs, kps, ones_col, s); \
+  return launch<TI, AMN, BMN, EPI, BN, 1>(d, zs, kps, ones_col, s);
 #define UL_TC_CASE(AMN, BMN, EPI)                 \
   if (amn == AMN && bmn == BMN && d.epi == EPI) { \
     if (bn == 256) {                              \
@@ -619,17 +689,61 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   return UL_ERR_VALUE;
 }
 
+}  // namespace tc
+
+int tc_bk(int dtype) { return dtype == kBf16 ? tc::Op<__nv_bfloat16>::BK : tc::Op<float>::BK; }
+
+bool tc_eligible(const GemmDesc& d) {
+  const int eb = d.dtype == kBf16 ? 2 : 4;
+  const int ob = (d.dtype == kBf16 && (d.epi == kEpiBiasElu || d.epi == kEpiEluGrad)) ? 2 : 4;
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  // bf16 runs every hidden GEMM on the tensor cores (TMA zero-fills partial
+  // tiles); tf32 keeps tiny shapes on the SIMT kernel
+  const bool big = d.dtype == kBf16 || (d.M >= 128 && d.N >= 64 && d.K >= 32);
+  return big && d.M >= 1 && d.N >= 1 && d.K >= 1 && d.M < (1ll << 31) && d.N < (1ll << 31) &&
+         d.K < (1ll << 31) && al(d.A) && al(d.B) && al(d.C) && (d.lda * eb % 16 == 0) &&
+         (d.ldb * eb % 16 == 0) && (d.ldc * ob % 16 == 0) &&
+         (d.epi != kEpiEluGrad || (al(d.aux) && d.ldaux * ob % 16 == 0)) &&
+         !(d.a_kmajor == false && d.b_kmajor == true);
+}
+
+int tc_num_splits(int64_t K, int splits, int dtype) {
+  const int bk = tc_bk(dtype);
+  splits = splits < 1 ? 1 : splits;
+  const int64_t kps = ceil_div(ceil_div(K, splits), bk) * bk;
+  return (int)ceil_div(K > 0 ? K : 1, kps);
+}
+
+// Same contract as gemm_f32 (split partials [zs][M][ldc] at C when splits >
+// 1); `ones_col` >= 0 additionally writes 1.0 into that column.
+int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
+  if (d.M == 0 || d.N == 0) return UL_OK;
+  if (ones_col < 0) ones_col = d.ones_col;
+  const int bk = tc_bk(d.dtype);
+  const int splits = d.splits < 1 ? 1 : d.splits;
+  const int kps = (int)(ceil_div(ceil_div(d.K, splits), bk) * bk);
+  const int zs = (int)ceil_div(d.K > 0 ? d.K : 1, kps);
+  if (d.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(d, zs, kps, ones_col, s);
+  return tc::dispatch<float>(d, zs, kps, ones_col, s);
+}
+
 }  // namespace ul
 
 // Test hook: one tcgen05 GEMM, same layout/epilogue codes as ul_gemm_f32.
-extern "C" int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const float* A,
-                          int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
-                          const float* bias, const float* aux, int64_t ldaux, int splits,
+// dtype 0: fp32 operands (kind::tf32), 1: bf16 operands (kind::f16); with
+// dtype 1 the ELU / ELU-gradient epilogues read and write bf16.
+extern "C" int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const void* A,
+                          int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                          const float* bias, const void* aux, int64_t ldaux, int splits, int dtype,
                           void* stream) {
   ul::GemmDesc g{};
-  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
-  g.bias = bias; g.aux = aux; g.ldaux = ldaux;
+  g.M = M; g.N = N; g.K = K;
+  g.A = (const float*)A; g.lda = lda; g.B = (const float*)B; g.ldb = ldb;
+  g.C = (float*)C; g.ldc = ldc;
+  g.bias = bias; g.aux = (const float*)aux; g.ldaux = ldaux;
   g.a_kmajor = layout & 1; g.b_kmajor = (layout >> 1) & 1; g.epi = epi; g.splits = splits;
+  g.dtype = dtype;
+  UL_CHECK_ARG(dtype == 0 || dtype == 1, "gemm_tc: dtype must be 0 (fp32/tf32) or 1 (bf16)");
   UL_CHECK_ARG(ul::tc_eligible(g), "gemm_tc: shape/alignment not eligible for tcgen05");
   return ul::gemm_tc(g, -1, ul::as_stream(stream));
 }

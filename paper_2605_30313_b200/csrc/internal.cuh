@@ -28,6 +28,12 @@ enum Epilogue : int {
   kEpiEluGrad = 3,   // C = acc * (min(aux[m,n],0)+1)
 };
 
+// operand storage of a GEMM / activation buffer
+enum DType : int {
+  kF32 = 0,   // fp32 (SIMT fp32 or tcgen05 kind::tf32)
+  kBf16 = 1,  // bf16 (tcgen05 kind::f16), fp32 accumulation
+};
+
 struct GemmDesc {
   int64_t M, N, K;
   const float* A;
@@ -49,6 +55,9 @@ struct GemmDesc {
   float* rowsum;
   // >= 0: the epilogue also writes C[m, ones_col] = 1 (activation ones column)
   int ones_col = -1;
+  // kBf16: A, B (and aux / C of the ELU epilogues) hold bf16 despite the
+  // float* fields; only the tensor-core path accepts it
+  int dtype = kF32;
 };
 int gemm_f32(const GemmDesc& d, cudaStream_t s);
 // number of K splits gemm_f32 actually launches for a requested split count
@@ -63,14 +72,28 @@ struct NetView {
   int dims[UL_MAX_LAYERS + 1];
   int64_t w_off[UL_MAX_LAYERS], b_off[UL_MAX_LAYERS], logstd_off, total;
   int64_t wp_off[UL_MAX_LAYERS], wp_total;  // staged (16 B-row) weight layout
+  int64_t wb_off[UL_MAX_LAYERS];            // bf16 staged layout (ld round_up(in, 8))
 };
 int make_view(const ul_net_desc* d, NetView* v);
-int64_t act_ld(int d);  // hidden activation row stride: round_up(d + 1, 4)
+// hidden activation row stride (elements): round_up(d + 1, 4) fp32 /
+// round_up(d + 1, 8) bf16 -- 16-byte rows plus the ones column
+int64_t act_ld(int d, int dtype = kF32);
 int64_t act_floats(const NetView& v, int64_t M);
-const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i);
+const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i, int dtype = kF32);
 int64_t bwd_work_floats(const NetView& v, int64_t M);
 int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t s);
-// backend 0: fp32 SIMT; 1: tcgen05 tf32 (wp = staged weights, may be null -> SIMT)
+// backend 0: fp32 SIMT; 1: tcgen05 tf32 (wp = staged weights, may be null -> SIMT);
+// 2: tcgen05 bf16 -- x, the hidden activations and the backward's hidden
+// gradients are bf16 (rows of act_ld(d, kBf16)), params / grads / outputs fp32
+inline int backend_dtype(int backend) { return backend == 2 ? kBf16 : kF32; }
+int stage_weights_dt(const NetView& v, const float* params, void* wp, int dtype, cudaStream_t s);
+
+// ------------------------------------------------------------------ gather
+// ul_gather_rows with an optional per-desc fp32 -> bf16 conversion (cvt)
+int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64_t* src_stride,
+                const int64_t* dst_stride, const int64_t* row_bytes, const int64_t* ones_byte,
+                const int* cvt, const int64_t* idx, int64_t n, int64_t modulo, int64_t lo,
+                int64_t hi, int* err, cudaStream_t stream);
 int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
                 const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
                 cudaStream_t s);

@@ -23,13 +23,15 @@ struct PpoPlan {
   NetView va{}, vc{};
   int A = 0;
   int64_t rows = 0, mb = 0, mb_local = 0;
-  int64_t ld_mo = 0, ld_mc = 0, ld_ma = 0;  // minibatch staging row strides
+  int64_t ld_mo = 0, ld_mc = 0, ld_ma = 0;  // minibatch staging row strides (elements)
+  int dt = kF32;                            // MLP activation / input storage
   int64_t Pa = 0, Pc = 0;
   // device arena
   char* arena = nullptr;
   float *mb_obs = nullptr, *mb_cobs = nullptr, *mb_act = nullptr, *mb_scal = nullptr;
   float *acts_a = nullptr, *acts_c = nullptr, *out_a = nullptr, *out_c = nullptr;
-  float *dmean = nullptr, *dv = nullptr, *work = nullptr, *red = nullptr, *red_own = nullptr;
+  float *dmean = nullptr, *dv = nullptr, *work = nullptr, *work_c = nullptr, *red = nullptr,
+        *red_own = nullptr;
   float *wst_a = nullptr, *wst_c = nullptr;  // staged (16 B-row) weights, tensor-core path
   double *head_part = nullptr, *adv_stats = nullptr, *adv_part = nullptr;
   unsigned int* tickets = nullptr;  // [0] head, [1] adv stats
@@ -41,7 +43,8 @@ struct PpoPlan {
   ul_ppo_bindings b{};
   bool bound = false;
   cudaStream_t cap_stream = nullptr;
-  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaStream_t side = nullptr;  // critic branch (fork/join inside each step)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
   // optional per-phase CUDA-event profiling (ul_ppo_plan_profile)
@@ -85,7 +88,8 @@ int alloc_plan(PpoPlan* p) {
   const size_t o_dmean = carve(sizeof(float) * ml * p->A);
   const size_t o_dv = carve(sizeof(float) * ml);
   const int64_t wa = bwd_work_floats(p->va, ml), wc = bwd_work_floats(p->vc, ml);
-  const size_t o_work = carve(sizeof(float) * (wa > wc ? wa : wc));
+  const size_t o_work = carve(sizeof(float) * wa);
+  const size_t o_workc = carve(sizeof(float) * wc);
   const size_t o_red = carve(sizeof(float) * (p->Pa + p->Pc + 4));
   const size_t o_hp = carve(sizeof(double) * ppo_head_partial_doubles(ml, p->A));
   const size_t o_as = carve(sizeof(double) * 4);
@@ -109,6 +113,7 @@ int alloc_plan(PpoPlan* p) {
   p->dmean = (float*)(a + o_dmean);
   p->dv = (float*)(a + o_dv);
   p->work = (float*)(a + o_work);
+  p->work_c = (float*)(a + o_workc);
   p->red_own = (float*)(a + o_red);
   p->red = p->red_own;
   p->head_part = (double*)(a + o_hp);
@@ -124,6 +129,9 @@ int alloc_plan(PpoPlan* p) {
   UL_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+  UL_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   return UL_OK;
 }
 
@@ -139,6 +147,25 @@ void free_plan(PpoPlan* p) {
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
+  if (p->side) cudaStreamDestroy(p->side);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
+}
+
+// The actor and critic branches of a step are independent until the PPO head
+// (forward) and again until the optimizer (backward): the critic runs on a
+// side stream forked from / joined back into `s` (captured as parallel graph
+// branches), so the many sub-wave kernels of the two networks overlap.
+int fork(PpoPlan* p, cudaStream_t s) {
+  UL_CUDA(cudaEventRecord(p->ev_fork, s));
+  UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+  return UL_OK;
+}
+
+int join(PpoPlan* p, cudaStream_t s) {
+  UL_CUDA(cudaEventRecord(p->ev_join, p->side));
+  UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+  return UL_OK;
 }
 
 // device part of begin: stats reset + advantage statistics (graph-capturable)
@@ -165,30 +192,35 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   const int64_t* idx = p->d.local_shards
                            ? b.perm + (int64_t)e * p->rows + (int64_t)k * ml
                            : b.perm + (int64_t)e * p->rows + (int64_t)k * p->mb + p->d.rank * ml;
-  const bool tc = p->d.gemm_backend == 1;
-  if (tc) {  // weights changed at the previous Adam step: restage 16 B-row copies
-    UL_TRY(stage_weights(p->va, b.actor_params, p->wst_a, s));
-    UL_TRY(stage_weights(p->vc, b.critic_params, p->wst_c, s));
-  }
+  const bool tc = p->d.gemm_backend >= 1;
+  const bool bf = p->dt == kBf16;
   // K4: one gather launch for the 7 per-row arrays; the obs / critic-obs
   // pad column is set to 1.0 (the tensor-core dW's bias column)
   const void* src[7] = {b.obs, b.cobs, b.act, b.blogp, b.adv, b.ret, b.oldv};
   void* dst[7] = {p->mb_obs, p->mb_cobs, p->mb_act, p->mb_scal, p->mb_scal + ml,
                   p->mb_scal + 2 * ml, p->mb_scal + 3 * ml};
+  // (bf16 path: the two network inputs are converted to bf16 rows on the way)
+  const int64_t xb = bf ? 2 : 4;
   const int64_t sst[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->d.ld_act, 4, 4, 4, 4};
-  const int64_t dstr[7] = {4 * p->ld_mo, 4 * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
-  const int64_t rb[7] = {4 * p->ld_mo, 4 * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
+  const int64_t dstr[7] = {xb * p->ld_mo, xb * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
+  const int64_t rb[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->ld_ma, 4, 4, 4, 4};
   const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
-  const int64_t ones[7] = {p->ld_mo > od ? 4 * od : -1, p->ld_mc > cd ? 4 * cd : -1, -1, -1, -1,
-                           -1, -1};
-  UL_TRY(ul_gather_rows(7, src, dst, sst, dstr, rb, ones, idx, ml, 0, 0, p->rows, nullptr, s));
+  const bool ones_o = p->d.ld_obs > od, ones_c = p->d.ld_cobs > cd;
+  const int64_t ones[7] = {ones_o ? 4 * od : -1, ones_c ? 4 * cd : -1, -1, -1, -1, -1, -1};
+  const int cvt[7] = {bf ? 1 : 0, bf ? 1 : 0, 0, 0, 0, 0, 0};
+  UL_TRY(gather_rows(7, src, dst, sst, dstr, rb, ones, cvt, idx, ml, 0, 0, p->rows, nullptr, s));
   mark(p, 1, s);
-  // K7 forwards
+  // K7 forwards, actor on s and critic on the side stream.  Weights changed at
+  // the previous Adam step: the tensor-core path restages 16 B-row copies.
   const int be = p->d.gemm_backend;
+  UL_TRY(fork(p, s));
+  if (tc) UL_TRY(stage_weights_dt(p->vc, b.critic_params, p->wst_c, p->dt, p->side));
+  UL_TRY(mlp_forward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, ml, p->acts_c,
+                     p->out_c, 1, p->side));
+  if (tc) UL_TRY(stage_weights_dt(p->va, b.actor_params, p->wst_a, p->dt, s));
   UL_TRY(mlp_forward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, ml, p->acts_a,
                      p->out_a, p->A, s));
-  UL_TRY(mlp_forward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, ml, p->acts_c,
-                     p->out_c, 1, s));
+  UL_TRY(join(p, s));
   mark(p, 0, s);
   // K9 head
   PpoHeadArgs h{};
@@ -220,13 +252,15 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   h.ent_coef_add = p->d.rank == 0 ? -p->d.entropy_coef : 0.0;
   UL_TRY(launch_ppo_head(h, s));
   mark(p, 2, s);
-  // K8 backwards into the contiguous all-reduce buffer
-  UL_TRY(mlp_backward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, p->ld_mo > od, ml,
+  // K8 backwards into the contiguous all-reduce buffer (critic on the side stream)
+  UL_TRY(fork(p, s));
+  UL_TRY(mlp_backward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, ones_c,
+                      ml, p->acts_c, p->dv, 1, p->red + p->Pa, nullptr, 0, 0, 0, true, true,
+                      p->work_c, p->side));
+  UL_TRY(mlp_backward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, ones_o, ml,
                       p->acts_a, p->dmean, p->A, p->red, nullptr, 0, 0, 0, true, false, p->work,
                       s));
-  UL_TRY(mlp_backward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, p->ld_mc > cd,
-                      ml, p->acts_c, p->dv, 1, p->red + p->Pa, nullptr, 0, 0, 0, true, true,
-                      p->work, s));
+  UL_TRY(join(p, s));
   mark(p, 0, s);
   return UL_OK;
 }
@@ -310,8 +344,14 @@ extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
   }
   if (desc->ld_obs < p->va.dims[0] || desc->ld_cobs < p->vc.dims[0] || desc->ld_act < p->A)
     return fail("ppo plan: leading dimension below feature width");
-  p->ld_mo = desc->ld_obs;
-  p->ld_mc = desc->ld_cobs;
+  if (desc->gemm_backend < 0 || desc->gemm_backend > 2)
+    return fail("ppo plan: gemm_backend must be UL_GEMM_FP32, _TF32 or _BF16");
+  p->dt = ul::backend_dtype(desc->gemm_backend);
+  if (p->dt == ul::kBf16 && ((desc->ld_obs * 4) % 16 || (desc->ld_cobs * 4) % 16))
+    return fail("ppo plan: the bf16 back end needs 16-byte obs / critic-obs rows");
+  // bf16 staging rows: round_up(ld, 8) elements (16-byte TMA rows)
+  p->ld_mo = p->dt == ul::kBf16 ? (desc->ld_obs + 7) / 8 * 8 : desc->ld_obs;
+  p->ld_mc = p->dt == ul::kBf16 ? (desc->ld_cobs + 7) / 8 * 8 : desc->ld_cobs;
   p->ld_ma = desc->ld_act;
   p->Pa = p->va.total;
   p->Pc = p->vc.total;

@@ -11,20 +11,22 @@
 // Back ends: 0 = fp32 SIMT (exact-fp32 parity path), 1 = tcgen05 kind::tf32.
 // Per GEMM the tensor-core path is used when the shape fills a 128-row UMMA
 // tile (the 12-/1-wide heads stay on the SIMT kernel).
+#include <cuda_bf16.h>
+
 #include "internal.cuh"
 
 namespace ul {
 
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
 bool tc_eligible(const GemmDesc& d);
-int tc_num_splits(int64_t K, int splits);
-bool skinny_ok(int N);
+int tc_num_splits(int64_t K, int splits, int dtype);
+bool skinny_ok(int N, int K);
 int64_t skinny_part_floats(int64_t M, int K, int N);
-int skinny_fwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float* W,
-               const float* b, float* out, int64_t ldo, cudaStream_t s);
-int skinny_bwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float* W,
-               const float* dout, int64_t ldd, float* dh, int64_t lddh, bool elu_grad,
-               float* gw, float* gb, float* part, cudaStream_t s);
+int skinny_fwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
+               const float* b, float* out, int64_t ldo, int dtype, cudaStream_t s);
+int skinny_bwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
+               const float* dout, int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw,
+               float* gb, float* gcs, float* part, int dtype, cudaStream_t s);
 
 namespace {
 
@@ -67,9 +69,14 @@ __global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict_
   }
 }
 
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+
 // db partials: column sums of dh [M, N] over row chunks; lanes = columns
-// (coalesced 128 B rows), 8 warps stride the rows; part[chunk][N]
-__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ x, int64_t ld,
+// (coalesced rows), 8 warps stride the rows, 8 loads in flight per thread;
+// part[chunk][N]
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, int64_t ld,
                                                      int64_t M, int64_t N, int64_t rows_per,
                                                      float* __restrict__ part) {
   __shared__ float sm[8][33];
@@ -77,24 +84,37 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ x
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c < N) {
     int64_t r = r0 + w;
-    for (; r + 24 < r1; r += 32) {
-      s0 += x[r * ld + c];
-      s1 += x[(r + 8) * ld + c];
-      s2 += x[(r + 16) * ld + c];
-      s3 += x[(r + 24) * ld + c];
+    for (; r + 56 < r1; r += 64) {
+      T v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = x[(r + 8 * i) * ld + c];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s[i] += to_f(v[i]);
     }
-    for (; r < r1; r += 8) s0 += x[r * ld + c];
+    for (; r < r1; r += 8) s[0] += to_f(x[r * ld + c]);
   }
-  sm[w][lane] = (s0 + s1) + (s2 + s3);
+  sm[w][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
   __syncthreads();
   if (w == 0 && c < N) {
     float t = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) t += sm[k][lane];
     part[(int64_t)blockIdx.y * N + c] = t;
+  }
+}
+
+// fp32 rows -> bf16 rows (the upstream gradient of a wide output layer on the
+// bf16 path)
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, int64_t ldx, int64_t M,
+                                   int64_t N, __nv_bfloat16* __restrict__ y, int64_t ldy) {
+  const int64_t total = M * N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t r = i / N, c = i - r * N;
+    y[r * ldy + c] = __float2bfloat16_rn(x[r * ldx + c]);
   }
 }
 
@@ -105,21 +125,22 @@ struct StageTable {
   int64_t total;  // padded elements
 };
 
+template <typename T>
 __global__ void stage_weights_kernel(const float* __restrict__ params, StageTable t,
-                                     float* __restrict__ wp) {
+                                     T* __restrict__ wp) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < t.total; j += stride) {
     int l = 0;
     while (l + 1 < t.n && j >= t.dst_off[l + 1]) ++l;
     const int64_t k = j - t.dst_off[l];
     const int64_t r = k / t.ld[l], c = k - r * t.ld[l];
-    wp[j] = c < t.cols[l] ? params[t.src_off[l] + r * t.cols[l] + c] : 0.f;
+    wp[j] = (T)(c < t.cols[l] ? params[t.src_off[l] + r * t.cols[l] + c] : 0.f);
   }
 }
 
 }  // namespace
 
-int64_t act_ld(int d) { return rup((int64_t)d + 1, 4); }
+int64_t act_ld(int d, int dtype) { return rup((int64_t)d + 1, dtype == kBf16 ? 8 : 4); }
 
 int make_view(const ul_net_desc* d, NetView* v) {
   UL_CHECK_ARG(d != nullptr, "net: null descriptor");
@@ -139,6 +160,11 @@ int make_view(const ul_net_desc* d, NetView* v) {
     v->wp_off[i] = woff;
     woff += (int64_t)v->dims[i + 1] * rup(v->dims[i], 4);
   }
+  int64_t boff = 0;
+  for (int i = 0; i < d->n_layers; ++i) {
+    v->wb_off[i] = boff;
+    boff += (int64_t)v->dims[i + 1] * rup(v->dims[i], 8);
+  }
   v->logstd_off = off;
   v->total = off + v->dims[d->n_layers];
   v->wp_total = woff;
@@ -157,7 +183,7 @@ static int64_t max_hidden_ld(const NetView& v) {
   return h;
 }
 
-// dW split count: enough CTAs for ~2 waves, >= 512 batch rows per split
+// dW split count: about one persistent wave of tiles, >= 512 batch rows per split
 static int dw_splits(int64_t out, int64_t in, int64_t M, bool tc) {
   const int64_t tiles = tc ? ceil_div(out, 128) * ceil_div(in + 1, 256)
                            : ceil_div(out, 128) * ceil_div(in, 128);
@@ -175,7 +201,7 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
     const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
                        ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
     int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 256 * out;
-    if (skinny_ok((int)out)) {
+    if (skinny_ok((int)out, (int)in)) {
       const int64_t sk = skinny_part_floats(M, (int)in, (int)out);
       need = sk > need ? sk : need;
     }
@@ -184,45 +210,82 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
   return 2 * M * max_hidden_ld(v) + ws;
 }
 
-const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i) {
+// hidden layer i's activation rows (byte offsets: bf16 rows are half as wide)
+const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i, int dtype) {
+  const int64_t eb = dtype == kBf16 ? 2 : 4;
   int64_t off = 0;
-  for (int j = 1; j <= i; ++j) off += act_ld(v.dims[j]) * M;
-  return acts + off;
+  for (int j = 1; j <= i; ++j) off += act_ld(v.dims[j], dtype) * M * eb;
+  return reinterpret_cast<const float*>(reinterpret_cast<const char*>(acts) + off);
+}
+
+int stage_weights_dt(const NetView& v, const float* params, void* wp, int dtype, cudaStream_t s) {
+  StageTable t{};
+  t.n = v.n_layers;
+  const int a = dtype == kBf16 ? 8 : 4;
+  for (int i = 0; i < v.n_layers; ++i) {
+    t.src_off[i] = v.w_off[i];
+    t.dst_off[i] = dtype == kBf16 ? v.wb_off[i] : v.wp_off[i];
+    t.rows[i] = v.dims[i + 1];
+    t.cols[i] = v.dims[i];
+    t.ld[i] = (int)rup(v.dims[i], a);
+  }
+  const int last = v.n_layers - 1;
+  t.total = t.dst_off[last] + (int64_t)t.rows[last] * t.ld[last];
+  int64_t blocks = ceil_div(t.total, 256);
+  blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
+  if (dtype == kBf16)
+    stage_weights_kernel<<<(unsigned)blocks, 256, 0, s>>>(params, t,
+                                                          reinterpret_cast<__nv_bfloat16*>(wp));
+  else
+    stage_weights_kernel<<<(unsigned)blocks, 256, 0, s>>>(params, t, reinterpret_cast<float*>(wp));
+  return check_launch("stage_weights_kernel");
 }
 
 int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t s) {
-  StageTable t{};
-  t.n = v.n_layers;
-  for (int i = 0; i < v.n_layers; ++i) {
-    t.src_off[i] = v.w_off[i];
-    t.dst_off[i] = v.wp_off[i];
-    t.rows[i] = v.dims[i + 1];
-    t.cols[i] = v.dims[i];
-    t.ld[i] = (int)rup(v.dims[i], 4);
+  return stage_weights_dt(v, params, wp, kF32, s);
+}
+
+// staged W_i for a dtype and its row pitch (elements)
+static const float* staged_w(const NetView& v, const float* wp, int i, int dtype, int64_t* ld) {
+  if (dtype == kBf16) {
+    *ld = rup(v.dims[i], 8);
+    return reinterpret_cast<const float*>(reinterpret_cast<const __nv_bfloat16*>(wp) +
+                                          v.wb_off[i]);
   }
-  t.total = v.wp_total;
-  int64_t blocks = ceil_div(t.total, 256);
-  blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
-  stage_weights_kernel<<<(unsigned)blocks, 256, 0, s>>>(params, t, wp);
-  return check_launch("stage_weights_kernel");
+  *ld = rup(v.dims[i], 4);
+  return wp + v.wp_off[i];
 }
 
 static int run_gemm(GemmDesc g, bool use_tc, int ones_col, cudaStream_t s) {
   g.ones_col = ones_col;
   if (use_tc && tc_eligible(g)) return gemm_tc(g, ones_col, s);
+  UL_CHECK_ARG(g.dtype == kF32, "bf16 MLP: GEMM %lldx%lldx%lld not tensor-core eligible "
+               "(alignment)", (long long)g.M, (long long)g.N, (long long)g.K);
   return gemm_f32(g, s);
+}
+
+static bool al16(const void* p, int64_t ld, int eb) {
+  return ((uintptr_t)p & 15) == 0 && (ld * eb) % 16 == 0;
 }
 
 int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
                 const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
                 cudaStream_t s) {
+  const int dt = backend_dtype(backend);
+  const int eb = dt == kBf16 ? 2 : 4;
+  const bool tc = backend >= 1 && wp != nullptr;
+  UL_CHECK_ARG(dt == kF32 || tc, "bf16 MLP needs staged weights");
   const float* h = x;
   int64_t ldh = ldx;
-  const bool tc = backend == 1 && wp != nullptr;
   for (int i = 0; i < v.n_layers; ++i) {
     const bool last = i == v.n_layers - 1;
-    float* dst = last ? out : const_cast<float*>(act_ptr(v, acts, M, i));
-    const int64_t lddst = last ? ld_out : act_ld(v.dims[i + 1]);
+    float* dst = last ? out : const_cast<float*>(act_ptr(v, acts, M, i, dt));
+    const int64_t lddst = last ? ld_out : act_ld(v.dims[i + 1], dt);
+    if (last && skinny_ok(v.dims[i + 1], v.dims[i]) && al16(h, ldh, eb)) {  // 12-/1-wide head
+      UL_TRY(skinny_fwd(h, ldh, M, v.dims[i], v.dims[i + 1], params + v.w_off[i],
+                        params + v.b_off[i], dst, lddst, dt, s));
+      break;
+    }
     GemmDesc g{};
     g.M = M; g.N = v.dims[i + 1]; g.K = v.dims[i];
     g.A = h; g.lda = ldh;
@@ -231,15 +294,12 @@ int mlp_forward(const NetView& v, const float* params, const float* wp, int back
     g.epi = last ? kEpiBias : kEpiBiasElu;
     g.splits = 1;
     g.C = dst; g.ldc = lddst;
-    if (last && skinny_ok(v.dims[i + 1])) {  // 12-/1-wide head layer
-      UL_TRY(skinny_fwd(h, ldh, M, v.dims[i], v.dims[i + 1], params + v.w_off[i],
-                        params + v.b_off[i], dst, lddst, s));
-      break;
-    }
-    const bool tc_here = tc && !last;
+    g.dtype = dt;
+    // tf32 keeps a wide output layer on the SIMT kernel; bf16 runs it on the
+    // tensor cores with an fp32 bias epilogue
+    const bool tc_here = tc && (!last || dt == kBf16);
     if (tc_here) {
-      g.B = wp + v.wp_off[i];
-      g.ldb = rup(v.dims[i], 4);
+      g.B = staged_w(v, wp, i, dt, &g.ldb);
     } else {
       g.B = params + v.w_off[i];
       g.ldb = v.dims[i];
@@ -256,30 +316,65 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
                  const float* dout, int64_t ld_dout, float* grads, float* dx, int64_t lddx,
                  int dx_col0, int dx_ncols, bool want_dw, bool zero_logstd, float* work,
                  cudaStream_t s) {
+  const int dt = backend_dtype(backend);
+  const int eb = dt == kBf16 ? 2 : 4;
+  const bool tc = backend >= 1 && wp != nullptr;
+  UL_CHECK_ARG(dt == kF32 || tc, "bf16 MLP needs staged weights");
+  UL_CHECK_ARG(dt == kF32 || dx == nullptr,
+               "bf16 MLP backward: input gradients (dx) need the fp32 / tf32 back end");
   const int64_t H = max_hidden_ld(v);
   float* dh_buf[2] = {work, work + M * H};
   float* ws = work + 2 * M * H;
-  const float* dh = dout;
+  const float* dh = dout;  // fp32 until the first hidden layer, then dt
   int64_t lddh = ld_dout;
+  bool dh_f32 = true;
   int ping = 0;
-  const bool tc = backend == 1 && wp != nullptr;
+  // column sums of the next hidden gradient, produced by the layer above
+  // (fused into skinny_bwd): layer index whose db is already written
+  int db_done = -1;
   if (want_dw && zero_logstd && grads)
     UL_CUDA(cudaMemsetAsync(grads + v.logstd_off, 0, sizeof(float) * v.dims[v.n_layers], s));
   for (int i = v.n_layers - 1; i >= 0; --i) {
     const int64_t out = v.dims[i + 1], in = v.dims[i];
-    const float* inp = i == 0 ? x : act_ptr(v, acts, M, i - 1);
-    const int64_t ldin = i == 0 ? ldx : act_ld(v.dims[i]);
+    const float* inp = i == 0 ? x : act_ptr(v, acts, M, i - 1, dt);
+    const int64_t ldin = i == 0 ? ldx : act_ld(v.dims[i], dt);
     const bool has_ones = i == 0 ? (x_has_ones && ldx >= in + 1) : true;
-    if (i == v.n_layers - 1 && skinny_ok((int)out) && i > 0) {
-      // fused last-layer backward: dW, db and dh_prev in one pass over h
+    auto bn_of = [](int64_t n) { return n > 128 ? 256 : 128; };
+    auto ones_free_of = [&](int64_t n_in, bool ones) {
+      return ones && bn_of(n_in + 1) == bn_of(n_in) &&
+             ceil_div(n_in + 1, bn_of(n_in + 1)) == ceil_div(n_in, bn_of(n_in));
+    };
+    if (i == v.n_layers - 1 && skinny_ok((int)out, (int)in) && i > 0 && al16(inp, ldin, eb)) {
+      // fused last-layer backward: dW, db, dh_prev and (when the layer below
+      // cannot get its db from the ones column) colsum(dh_prev) in one pass
       float* nxt = dh_buf[ping];
       ping ^= 1;
+      const int64_t in_below = v.dims[i - 1];
+      const bool below_ones = i - 1 == 0 ? x_has_ones && ldx >= in_below + 1 : true;
+      const bool need_cs = want_dw && tc && !ones_free_of(in_below, below_ones);
       UL_TRY(skinny_bwd(inp, ldin, M, (int)in, (int)out, params + v.w_off[i], dh, lddh, nxt,
-                        act_ld((int)in), true, want_dw ? grads + v.w_off[i] : nullptr,
-                        want_dw ? grads + v.b_off[i] : nullptr, ws, s));
+                        act_ld((int)in, dt), true, want_dw ? grads + v.w_off[i] : nullptr,
+                        want_dw ? grads + v.b_off[i] : nullptr,
+                        need_cs ? grads + v.b_off[i - 1] : nullptr, ws, dt, s));
+      if (need_cs) db_done = i - 1;
       dh = nxt;
-      lddh = act_ld((int)in);
+      lddh = act_ld((int)in, dt);
+      dh_f32 = dt == kF32;
       continue;
+    }
+    if (dh_f32 && dt == kBf16) {
+      // wide output layer on the bf16 path: its upstream gradient as bf16 rows
+      float* cv = dh_buf[ping];
+      ping ^= 1;
+      const int64_t ldcv = act_ld((int)out, dt);
+      int64_t blocks = ceil_div(M * out, 256);
+      blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
+      f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
+          dh, lddh, M, out, reinterpret_cast<__nv_bfloat16*>(cv), ldcv);
+      UL_TRY(check_launch("f32_to_bf16_kernel"));
+      dh = cv;
+      lddh = ldcv;
+      dh_f32 = false;
     }
     if (want_dw) {
       GemmDesc g{};
@@ -287,17 +382,17 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
       g.A = dh; g.lda = lddh; g.B = inp; g.ldb = ldin;
       g.a_kmajor = false; g.b_kmajor = false; g.epi = kEpiStore;
       g.C = ws;
+      g.dtype = dt;
       // [dW | db] through the ones column when that column rides in a tile the
       // GEMM computes anyway; otherwise dW alone + a column-sum pass for db
-      auto bn_of = [](int64_t n) { return n > 128 ? 256 : 128; };
-      const bool ones_free = has_ones && bn_of(in + 1) == bn_of(in) &&
-                             ceil_div(in + 1, bn_of(in + 1)) == ceil_div(in, bn_of(in));
+      // (unless the layer above already produced it)
+      const bool ones_free = ones_free_of(in, has_ones);
       GemmDesc gt = g;
       gt.N = ones_free ? in + 1 : in;
       gt.splits = dw_splits(out, in, M, true);
-      gt.ldc = rup(gt.N, 4);  // 16 B partial rows (TMA store)
-      if (tc && out >= 64 && tc_eligible(gt)) {
-        const int sp = tc_num_splits(M, gt.splits);
+      gt.ldc = rup(gt.N, 4);  // 16 B fp32 partial rows (TMA store)
+      if (tc && (out >= 64 || dt == kBf16) && tc_eligible(gt)) {
+        const int sp = tc_num_splits(M, gt.splits, dt);
         gt.splits = sp;
         UL_TRY(gemm_tc(gt, -1, s));
         const int64_t blocks = ceil_div(out * gt.ldc, 32);
@@ -305,17 +400,21 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
             ws, sp, out, in, gt.ldc, grads + v.w_off[i],
             ones_free ? grads + v.b_off[i] : nullptr);
         UL_TRY(check_launch("reduce_dw_kernel"));
-        if (!ones_free) {
-          // 256-row chunks (8 warps x 32 rows, 4 loads in flight each), <= 256 chunks
-          const int64_t chunks = ceil_div(M, 256) < 256 ? ceil_div(M, 256) : 256;
+        if (!ones_free && db_done != i) {
+          const int64_t chunks = ceil_div(M, 512) < 256 ? ceil_div(M, 512) : 256;
           const int64_t rows_per = ceil_div(M, chunks);
           float* part = ws + (int64_t)sp * out * gt.ldc;
-          colsum_kernel<<<dim3((unsigned)ceil_div(out, 32), (unsigned)chunks), 256, 0, s>>>(
-              dh, lddh, M, out, rows_per, part);
+          const dim3 grid((unsigned)ceil_div(out, 32), (unsigned)chunks);
+          if (dt == kBf16)
+            colsum_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(dh), lddh,
+                                               M, out, rows_per, part);
+          else
+            colsum_kernel<<<grid, 256, 0, s>>>(dh, lddh, M, out, rows_per, part);
           UL_TRY(check_launch("colsum_kernel"));
           UL_TRY(reduce_splits(part, (int)chunks, out, grads + v.b_off[i], out, out, s));
         }
       } else {
+        UL_CHECK_ARG(dt == kF32, "bf16 MLP: dW GEMM not tensor-core eligible");
         const int sp = gemm_num_splits(M, dw_splits(out, in, M, false));
         g.N = in;
         g.splits = sp;
@@ -342,20 +441,20 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
     GemmDesc g{};
     g.M = M; g.N = in; g.K = out;
     g.A = dh; g.lda = lddh;
-    g.C = nxt; g.ldc = act_ld((int)in);
-    g.aux = act_ptr(v, acts, M, i - 1); g.ldaux = act_ld((int)in);
+    g.C = nxt; g.ldc = act_ld((int)in, dt);
+    g.aux = act_ptr(v, acts, M, i - 1, dt); g.ldaux = act_ld((int)in, dt);
     g.a_kmajor = true; g.b_kmajor = false; g.epi = kEpiEluGrad; g.splits = 1;
-    const bool tc_here = tc && out >= 32;
+    g.dtype = dt;
+    const bool tc_here = tc && (out >= 32 || dt == kBf16);
     if (tc_here) {
-      g.B = wp + v.wp_off[i];
-      g.ldb = rup(in, 4);
+      g.B = staged_w(v, wp, i, dt, &g.ldb);
     } else {
       g.B = params + v.w_off[i];
       g.ldb = in;
     }
     UL_TRY(run_gemm(g, tc_here, -1, s));
     dh = nxt;
-    lddh = act_ld((int)in);
+    lddh = act_ld((int)in, dt);
   }
   return UL_OK;
 }
@@ -394,6 +493,18 @@ extern "C" int ul_stage_weights(const ul_net_desc* net, const float* params, flo
   return ul::stage_weights(v, params, wstage, ul::as_stream(stream));
 }
 
+extern "C" int64_t ul_mlp_act_ld(int d, int backend) {
+  return ul::act_ld(d, ul::backend_dtype(backend));
+}
+
+extern "C" int ul_stage_weights_ex(const ul_net_desc* net, const float* params, void* wstage,
+                                   int backend, void* stream) {
+  ul::NetView v;
+  UL_TRY(ul::make_view(net, &v));
+  return ul::stage_weights_dt(v, params, wstage, ul::backend_dtype(backend),
+                              ul::as_stream(stream));
+}
+
 extern "C" int ul_mlp_forward(const ul_net_desc* net, const float* params, const float* wstage,
                               int backend, const float* x, int64_t ldx, int64_t M, float* acts,
                               float* out, int64_t ld_out, void* stream) {
@@ -401,7 +512,7 @@ extern "C" int ul_mlp_forward(const ul_net_desc* net, const float* params, const
   UL_TRY(ul::make_view(net, &v));
   UL_CHECK_ARG(M >= 0, "forward: negative batch");
   UL_CHECK_ARG(ldx >= v.dims[0], "forward: ldx %lld < input_dim %d", (long long)ldx, v.dims[0]);
-  UL_CHECK_ARG(backend == 0 || backend == 1, "forward: backend must be 0 (fp32) or 1 (tf32)");
+  UL_CHECK_ARG(backend >= 0 && backend <= 2, "forward: backend must be 0 (fp32), 1 (tf32) or 2 (bf16)");
   return ul::mlp_forward(v, params, wstage, backend, x, ldx, M, acts, out, ld_out,
                          ul::as_stream(stream));
 }
@@ -413,7 +524,7 @@ extern "C" int ul_mlp_backward(const ul_net_desc* net, const float* params, cons
   ul::NetView v;
   UL_TRY(ul::make_view(net, &v));
   UL_CHECK_ARG(M >= 0, "backward: negative batch");
-  UL_CHECK_ARG(backend == 0 || backend == 1, "backward: backend must be 0 (fp32) or 1 (tf32)");
+  UL_CHECK_ARG(backend >= 0 && backend <= 2, "backward: backend must be 0 (fp32), 1 (tf32) or 2 (bf16)");
   return ul::mlp_backward(v, params, wstage, backend, x, ldx, x_has_ones != 0, M, acts, dout,
                           ld_dout, grads, dx, lddx, 0, v.dims[0], true, true, work,
                           ul::as_stream(stream));

@@ -1,52 +1,128 @@
 // Skinny output layers (N = action dim 12/23/29 or the critic's 1): the last
 // MLP layer of every network, R:tensornet/mlp.py:165 (forward) and :192-197
-// (backward).  A 128x128 GEMM tile wastes > 90 % of its work at N <= 32, so
-// these layers get row-blocked kernels instead:
-//   skinny_fwd : out[M,N] = h[M,K] W^T + b      (one pass over h)
-//   skinny_bwd : dh[M,K] = (dout W) * elu'(h)  AND  dW/db block partials,
-//                reading h and dout exactly once (the dW and dX GEMMs of the
-//                last layer fused), then a fixed-order partial reduction.
-// Rows are staged through shared memory in 64-column chunks with coalesced
-// loads; W (N x K, the reference's flat layout) is read through L1/L2.
+// (backward).  A 128-row UMMA tile wastes > 90 % of its work at N <= 32, so
+// these layers get row-tiled SIMT kernels that read h exactly once:
+//   skinny_fwd : out[M,N] = h[M,K] W^T + b
+//   skinny_bwd : dh[M,K] = (dout W) * elu'(h), block partials of dW = dout^T h,
+//                db = colsum(dout) and (optionally) colsum(dh) -- the bias
+//                gradient of the layer below, so its dW GEMM needs no extra
+//                pass over dh -- then one fixed-order partial reduction.
+// A 64-row tile of h (fp32 or bf16 rows) is staged into shared memory with
+// 16-byte cp.async copies, all issued before the first wait (one memory round
+// trip per tile); W (N x K, the reference's flat layout) sits in shared memory
+// for the whole block.  Four threads per row; smem rows are padded by 16 B so
+// the per-row 16-byte reads of a warp fall in distinct banks.
+#include <cuda_bf16.h>
+
 #include "internal.cuh"
 
 namespace ul {
 namespace {
 
-constexpr int kRows = 64, kCols = 64, kThr = 256, kMaxN = 32;
+constexpr int kRows = 64, kThr = 256, kMaxN = 32, kMaxW = 8192 /* N*K floats in smem */;
+constexpr int kKC = 256;  // K columns per staged chunk
 
-__global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const float* __restrict__ h, int64_t ldh,
+template <typename T>
+__device__ __forceinline__ float4 ld4(const T* p);
+template <>
+__device__ __forceinline__ float4 ld4<float>(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+template <>
+__device__ __forceinline__ float4 ld4<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+}
+
+template <typename T>
+__device__ __forceinline__ void st4(T* p, float4 v);
+template <>
+__device__ __forceinline__ void st4<float>(float* p, float4 v) {
+  *reinterpret_cast<float4*>(p) = v;
+}
+template <>
+__device__ __forceinline__ void st4<__nv_bfloat16>(__nv_bfloat16* p, float4 v) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(sdst);
+  const int n = valid ? 16 : 0;  // 0 source bytes -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// smem row pitch (elements) for a chunk of kc columns: 16-byte rows + 16 B pad
+template <typename T>
+__host__ __device__ constexpr int pitch_of(int kc) {
+  return ((kc * (int)sizeof(T) + 15) / 16 * 16 + 16) / (int)sizeof(T);
+}
+
+// stage rows [r0, r0+kRows) x columns [k0, k0+kc) of h into sh (pitch P)
+template <typename T>
+__device__ __forceinline__ void stage_tile(const T* __restrict__ h, int64_t ldh, int64_t M,
+                                           int64_t r0, int k0, int kc, T* sh, int P) {
+  constexpr int kE = 16 / (int)sizeof(T);  // elements per 16-byte copy
+  const int per_row = (kc + kE - 1) / kE;
+  for (int e = threadIdx.x; e < kRows * per_row; e += kThr) {
+    const int rr = e / per_row, u = e - rr * per_row;
+    const int64_t gr = r0 + rr;
+    const bool ok = gr < M;
+    cp_async16(sh + rr * P + u * kE, h + (ok ? gr : 0) * ldh + k0 + u * kE, ok);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+// out[r, j] = b[j] + sum_k h[r, k] W[j, k]; thread (row r = t/4, q = t%4)
+// accumulates outputs j = q, q+4, ...
+template <typename TH>
+__global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const TH* __restrict__ h, int64_t ldh,
                                                           int64_t M, int K, int N,
                                                           const float* __restrict__ W,
                                                           const float* __restrict__ b,
                                                           float* __restrict__ out, int64_t ldo) {
-  __shared__ float sh[kRows][kCols + 1];
-  __shared__ float sw[kMaxN][kCols + 1];
-  const int t = threadIdx.x;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int KC = K < kKC ? (K + 7) / 8 * 8 : kKC;
+  const int P = pitch_of<TH>(KC), PW = pitch_of<float>(KC);
+  TH* sh = reinterpret_cast<TH*>(smem);
+  float* sw = reinterpret_cast<float*>(smem + (size_t)kRows * P * sizeof(TH));
+  const int t = threadIdx.x, r = t >> 2, q = t & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kRows;
-  const int r = t >> 2, q = t & 3;  // row, output lane (outputs q, q+4, ...)
   float acc[kMaxN / 4];
 #pragma unroll
   for (int u = 0; u < kMaxN / 4; ++u) acc[u] = 0.f;
-  for (int k0 = 0; k0 < K; k0 += kCols) {
-    for (int e = t; e < kRows * kCols; e += kThr) {
-      const int rr = e / kCols, cc = e % kCols;
-      const int64_t gr = r0 + rr;
-      sh[rr][cc] = (gr < M && k0 + cc < K) ? h[gr * ldh + k0 + cc] : 0.f;
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    const int kc = K - k0 < KC ? K - k0 : KC;
+    for (int e = t; e < N * KC; e += kThr) {
+      const int j = e / KC, c = e - j * KC;
+      sw[j * PW + c] = c < kc ? __ldg(W + (int64_t)j * K + k0 + c) : 0.f;
     }
-    for (int e = t; e < N * kCols; e += kThr) {
-      const int j = e / kCols, cc = e % kCols;
-      sw[j][cc] = k0 + cc < K ? W[(int64_t)j * K + k0 + cc] : 0.f;
-    }
-    __syncthreads();
+    stage_tile<TH>(h, ldh, M, r0, k0, kc, sh, P);
+    // zero the tail of the last 16-byte group (cp.async copies whole groups)
+    const TH* hr = sh + r * P;
+    for (int c = 0; c < kc; c += 4) {
+      float4 hv = ld4<TH>(hr + c);
+      if (c + 4 > kc) {
+        if (c + 1 >= kc) hv.y = 0.f;
+        if (c + 2 >= kc) hv.z = 0.f;
+        if (c + 3 >= kc) hv.w = 0.f;
+      }
 #pragma unroll
-    for (int u = 0; u < kMaxN / 4; ++u) {
-      const int j = q + 4 * u;
-      if (j < N) {
-        float s = acc[u];
-#pragma unroll 8
-        for (int c = 0; c < kCols; ++c) s = fmaf(sh[r][c], sw[j][c], s);
-        acc[u] = s;
+      for (int u = 0; u < kMaxN / 4; ++u) {
+        const int j = q + 4 * u;
+        if (j < N) {
+          const float4 w = *reinterpret_cast<const float4*>(sw + j * PW + c);
+          acc[u] = fmaf(hv.x, w.x, fmaf(hv.y, w.y, fmaf(hv.z, w.z, fmaf(hv.w, w.w, acc[u]))));
+        }
       }
     }
     __syncthreads();
@@ -61,135 +137,246 @@ __global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const float* __restric
   }
 }
 
-// part_w: [gridDim.x, N, K], part_b: [gridDim.x, N]
+// Per block z: part[z] = [dW partial (N x K) | db partial (N) | colsum(dh) (K, if csum)]
+template <typename TH>
 __global__ void __launch_bounds__(kThr) skinny_bwd_kernel(
-    const float* __restrict__ h, int64_t ldh, int64_t M, int K, int N,
-    const float* __restrict__ W, const float* __restrict__ dout, int64_t ldd,
-    float* __restrict__ dh, int64_t lddh, int elu_grad, float* __restrict__ part_w,
-    float* __restrict__ part_b) {
-  __shared__ float sh[kRows][kCols + 1];
-  __shared__ float sd[kRows][kMaxN + 1];
-  const int t = threadIdx.x;
+    const TH* __restrict__ h, int64_t ldh, int64_t M, int K, int N, const float* __restrict__ W,
+    const float* __restrict__ dout, int64_t ldd, TH* __restrict__ dh, int64_t lddh, int elu_grad,
+    float* __restrict__ part, int64_t plen, int want_dw, int csum) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int KC = K < kKC ? (K + 7) / 8 * 8 : kKC;
+  const int P = pitch_of<TH>(KC), PW = pitch_of<float>(KC);
+  TH* sh = reinterpret_cast<TH*>(smem);
+  float* sw = reinterpret_cast<float*>(smem + (size_t)kRows * P * sizeof(TH));
+  float* sd = sw + (size_t)N * PW;         // [kRows][kMaxN + 1] upstream gradient
+  float* sdh = sd + kRows * (kMaxN + 1);   // [kRows][PW] dh tile (column sums)
+  const int t = threadIdx.x, r = t >> 2, q = t & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kRows;
+  float* pz = part + (int64_t)blockIdx.x * plen;
   for (int e = t; e < kRows * N; e += kThr) {
-    const int rr = e / N, j = e % N;
+    const int rr = e / N, j = e - rr * N;
     const int64_t gr = r0 + rr;
-    sd[rr][j] = gr < M ? dout[gr * ldd + j] : 0.f;
+    sd[rr * (kMaxN + 1) + j] = gr < M ? dout[gr * ldd + j] : 0.f;
   }
   __syncthreads();
-  if (part_b && t < N) {
+  if (want_dw && t < N) {
     float s = 0.f;
-    for (int rr = 0; rr < kRows; ++rr) s += sd[rr][t];
-    part_b[(int64_t)blockIdx.x * N + t] = s;
+    for (int rr = 0; rr < kRows; ++rr) s += sd[rr * (kMaxN + 1) + t];
+    pz[(int64_t)N * K + t] = s;
   }
-  const int c = t & (kCols - 1), rq = t >> 6;  // column, row quarter (4 groups of 16 rows)
-  for (int k0 = 0; k0 < K; k0 += kCols) {
-    for (int e = t; e < kRows * kCols; e += kThr) {
-      const int rr = e / kCols, cc = e % kCols;
-      const int64_t gr = r0 + rr;
-      sh[rr][cc] = (gr < M && k0 + cc < K) ? h[gr * ldh + k0 + cc] : 0.f;
+  float g[kMaxN];
+#pragma unroll
+  for (int j = 0; j < kMaxN; ++j) g[j] = j < N ? sd[r * (kMaxN + 1) + j] : 0.f;
+  const int64_t gr = r0 + r;
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    const int kc = K - k0 < KC ? K - k0 : KC;
+    for (int e = t; e < N * KC; e += kThr) {
+      const int j = e / KC, c = e - j * KC;
+      sw[j * PW + c] = c < kc ? __ldg(W + (int64_t)j * K + k0 + c) : 0.f;
     }
-    __syncthreads();
-    const int k = k0 + c;
-    if (k < K) {
-      // W column k for all N outputs
-      float wk[kMaxN];
+    stage_tile<TH>(h, ldh, M, r0, k0, kc, sh, P);
+    // dh for row r, 4-column groups c = 4q, 4q + 16, ...
+    if (dh) {
+      for (int c = 4 * q; c < kc; c += 16) {
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < kMaxN; ++j) wk[j] = j < N ? __ldg(W + (int64_t)j * K + k) : 0.f;
-      if (dh) {
-        for (int rr = rq * 16; rr < rq * 16 + 16; ++rr) {
-          const int64_t gr = r0 + rr;
-          if (gr >= M) break;
-          float s = 0.f;
-#pragma unroll
-          for (int j = 0; j < kMaxN; ++j)
-            if (j < N) s = fmaf(sd[rr][j], wk[j], s);
-          if (elu_grad) s *= elu_grad_from_act(sh[rr][c]);
-          dh[gr * lddh + k] = s;
+        for (int j = 0; j < kMaxN; ++j) {
+          if (j < N) {
+            const float4 w = *reinterpret_cast<const float4*>(sw + j * PW + c);
+            s.x = fmaf(g[j], w.x, s.x);
+            s.y = fmaf(g[j], w.y, s.y);
+            s.z = fmaf(g[j], w.z, s.z);
+            s.w = fmaf(g[j], w.w, s.w);
+          }
+        }
+        if (elu_grad) {
+          const float4 hv = ld4<TH>(sh + r * P + c);
+          s.x *= elu_grad_from_act(hv.x);
+          s.y *= elu_grad_from_act(hv.y);
+          s.z *= elu_grad_from_act(hv.z);
+          s.w *= elu_grad_from_act(hv.w);
+        }
+        if (gr >= M) s = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (csum) *reinterpret_cast<float4*>(sdh + r * PW + c) = s;
+        if (gr < M) {
+          if (c + 4 <= kc) {
+            st4<TH>(dh + gr * lddh + k0 + c, s);
+          } else {
+            const float sv[4] = {s.x, s.y, s.z, s.w};
+            for (int i = 0; c + i < kc; ++i) dh[gr * lddh + k0 + c + i] = (TH)sv[i];
+          }
         }
       }
-      if (part_w) {
-        // dW[j, k] partial over this block's rows; outputs j = rq, rq+4, ...
-        for (int j = rq; j < N; j += 4) {
-          float s = 0.f;
+    }
+    // dW partial: pair (4-column group c4, output j), sum over the tile's rows
+    if (want_dw) {
+      const int g4 = (kc + 3) / 4;
+      for (int pr = t; pr < g4 * N; pr += kThr) {
+        const int j = pr / g4, c = 4 * (pr - j * g4);
+        float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-          for (int rr = 0; rr < kRows; ++rr) s = fmaf(sd[rr][j], sh[rr][c], s);
-          part_w[((int64_t)blockIdx.x * N + j) * K + k] = s;
+        for (int rr = 0; rr < kRows; ++rr) {
+          const float d = sd[rr * (kMaxN + 1) + j];
+          const float4 hv = ld4<TH>(sh + rr * P + c);
+          s.x = fmaf(d, hv.x, s.x);
+          s.y = fmaf(d, hv.y, s.y);
+          s.z = fmaf(d, hv.z, s.z);
+          s.w = fmaf(d, hv.w, s.w);
         }
+        const float sv[4] = {s.x, s.y, s.z, s.w};
+        for (int i = 0; i < 4 && c + i < kc; ++i) pz[(int64_t)j * K + k0 + c + i] = sv[i];
+      }
+    }
+    if (csum) {
+      __syncthreads();
+      for (int c = t; c < kc; c += kThr) {
+        float s = 0.f;
+        for (int rr = 0; rr < kRows; ++rr) s += sdh[rr * PW + c];
+        pz[(int64_t)N * K + N + k0 + c] = s;
       }
     }
     __syncthreads();
   }
 }
 
-// out[j] = sum_z part[z*len + j]: 32 outputs per CTA (coalesced lanes), the
-// partial index split across 8 warps, fixed-order smem combine (deterministic)
-__global__ void __launch_bounds__(256) reduce_parts_kernel(const float* __restrict__ part,
-                                                           int nblk, int64_t len,
-                                                           float* __restrict__ out) {
-  __shared__ float sm[8][33];
+// out_d[j] = sum_z part[z * plen + j] for j in segment d (fixed order over z):
+// 128 columns per CTA (float4 lanes), 32 warps over z, smem combine.  Three
+// destination segments share one launch: [0, n0) -> o0, [n0, n0+n1) -> o1,
+// [n0+n1, n0+n1+n2) -> o2 (a null destination skips its segment).
+__global__ void __launch_bounds__(1024) reduce_parts_kernel(const float* __restrict__ part,
+                                                            int nblk, int64_t plen, int64_t n0,
+                                                            float* o0, int64_t n1, float* o1,
+                                                            int64_t n2, float* o2) {
+  __shared__ float4 sm[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-  float s = 0.f;
-  if (j < len) {
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  const int64_t total = n0 + n1 + n2;
+  const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+  if (j < total) {
+    const bool vec = (plen & 3) == 0 && j + 4 <= total;
     int z = w;
-    for (; z + 24 < nblk; z += 32) {
-      s0 += part[(int64_t)z * len + j];
-      s1 += part[(int64_t)(z + 8) * len + j];
-      s2 += part[(int64_t)(z + 16) * len + j];
-      s3 += part[(int64_t)(z + 24) * len + j];
+    for (; z < nblk; z += 64) {
+      const float* p0 = part + (int64_t)z * plen + j;
+      const float* p1 = z + 32 < nblk ? p0 + 32 * plen : nullptr;
+      float4 x, y = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (vec) {
+        x = *reinterpret_cast<const float4*>(p0);
+        if (p1) y = *reinterpret_cast<const float4*>(p1);
+      } else {
+        x = make_float4(p0[0], j + 1 < total ? p0[1] : 0.f, j + 2 < total ? p0[2] : 0.f,
+                        j + 3 < total ? p0[3] : 0.f);
+        if (p1)
+          y = make_float4(p1[0], j + 1 < total ? p1[1] : 0.f, j + 2 < total ? p1[2] : 0.f,
+                          j + 3 < total ? p1[3] : 0.f);
+      }
+      a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+      b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
     }
-    for (; z < nblk; z += 8) s0 += part[(int64_t)z * len + j];
-    s = (s0 + s1) + (s2 + s3);
   }
-  sm[w][lane] = s;
+  sm[w][lane] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
   __syncthreads();
-  if (w == 0 && j < len) {
-    float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += sm[k][lane];
-    out[j] = t;
+  if (w == 0 && j < total) {
+    float4 s = sm[0][lane];
+    for (int k = 1; k < 32; ++k) {
+      const float4 v = sm[k][lane];
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    const float sv[4] = {s.x, s.y, s.z, s.w};
+    for (int i = 0; i < 4 && j + i < total; ++i) {
+      const int64_t c = j + i;
+      if (c < n0) {
+        if (o0) o0[c] = sv[i];
+      } else if (c < n0 + n1) {
+        if (o1) o1[c - n0] = sv[i];
+      } else if (o2) {
+        o2[c - n0 - n1] = sv[i];
+      }
+    }
   }
+}
+
+template <typename TH>
+size_t fwd_smem(int K, int N) {
+  const int KC = K < kKC ? (K + 7) / 8 * 8 : kKC;
+  return (size_t)kRows * pitch_of<TH>(KC) * sizeof(TH) + (size_t)N * pitch_of<float>(KC) * 4;
+}
+template <typename TH>
+size_t bwd_smem(int K, int N) {
+  const int KC = K < kKC ? (K + 7) / 8 * 8 : kKC;
+  return fwd_smem<TH>(K, N) + (size_t)kRows * (kMaxN + 1) * 4 +
+         (size_t)kRows * pitch_of<float>(KC) * 4;
+}
+
+template <typename TH>
+int fwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* b,
+          float* out, int64_t ldo, cudaStream_t s) {
+  const size_t sm = fwd_smem<TH>(K, N);
+  static bool attr = false;
+  if (!attr) {
+    UL_CUDA(cudaFuncSetAttribute(skinny_fwd_kernel<TH>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  skinny_fwd_kernel<TH><<<(unsigned)ceil_div(M, kRows), kThr, sm, s>>>(
+      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, b, out, ldo);
+  return check_launch("skinny_fwd_kernel");
+}
+
+template <typename TH>
+int bwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* dout,
+          int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw, float* gb, float* gcs,
+          float* part, cudaStream_t s) {
+  const int nblk = (int)ceil_div(M, kRows);
+  const bool want_dw = gw || gb;
+  const bool csum = gcs != nullptr && dh != nullptr;
+  const int64_t plen = (int64_t)N * K + N + (csum ? K : 0);
+  const size_t sm = bwd_smem<TH>(K, N);
+  static bool attr = false;
+  if (!attr) {
+    UL_CUDA(cudaFuncSetAttribute(skinny_bwd_kernel<TH>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  skinny_bwd_kernel<TH><<<nblk, kThr, sm, s>>>(
+      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, dout, ldd, reinterpret_cast<TH*>(dh), lddh,
+      elu_grad ? 1 : 0, part, plen, want_dw ? 1 : 0, csum ? 1 : 0);
+  UL_TRY(check_launch("skinny_bwd_kernel"));
+  if (want_dw || csum) {
+    const int64_t total = plen;
+    reduce_parts_kernel<<<(unsigned)ceil_div(total, 128), 1024, 0, s>>>(
+        part, nblk, plen, want_dw ? (int64_t)N * K : (int64_t)N * K, gw, N, gb,
+        csum ? K : 0, gcs);
+    UL_TRY(check_launch("reduce_parts_kernel"));
+  }
+  return UL_OK;
 }
 
 }  // namespace
 
-bool skinny_ok(int N) { return N >= 1 && N <= kMaxN; }
+bool skinny_ok(int N, int K) { return N >= 1 && N <= kMaxN && (int64_t)N * K <= kMaxW * 4; }
 
 int64_t skinny_part_floats(int64_t M, int K, int N) {
-  return ceil_div(M, kRows) * (int64_t)N * (K + 1);
+  return ceil_div(M, kRows) * ((int64_t)N * K + N + K);
 }
 
-int skinny_fwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float* W,
-               const float* b, float* out, int64_t ldo, cudaStream_t s) {
+int skinny_fwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
+               const float* b, float* out, int64_t ldo, int dtype, cudaStream_t s) {
   if (M == 0) return UL_OK;
-  skinny_fwd_kernel<<<(unsigned)ceil_div(M, kRows), kThr, 0, s>>>(h, ldh, M, K, N, W, b, out, ldo);
-  return check_launch("skinny_fwd_kernel");
+  if (dtype == kBf16) return fwd_t<__nv_bfloat16>(h, ldh, M, K, N, W, b, out, ldo, s);
+  return fwd_t<float>(h, ldh, M, K, N, W, b, out, ldo, s);
 }
 
-// gw [N, K] and gb [N] receive the reduced gradients when non-null; `part`
-// holds skinny_part_floats(M, K, N) floats of scratch.
-int skinny_bwd(const float* h, int64_t ldh, int64_t M, int K, int N, const float* W,
-               const float* dout, int64_t ldd, float* dh, int64_t lddh, bool elu_grad,
-               float* gw, float* gb, float* part, cudaStream_t s) {
+// gw [N, K], gb [N] and gcs [K] (column sums of dh: the bias gradient of the
+// layer below) receive reduced results when non-null; `part` holds
+// skinny_part_floats(M, K, N) floats of scratch.
+int skinny_bwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
+               const float* dout, int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw,
+               float* gb, float* gcs, float* part, int dtype, cudaStream_t s) {
   if (M == 0) return UL_OK;
-  const int nblk = (int)ceil_div(M, kRows);
-  float* pw = gw ? part : nullptr;
-  float* pb = gb ? part + (int64_t)nblk * N * K : nullptr;
-  skinny_bwd_kernel<<<nblk, kThr, 0, s>>>(h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad ? 1 : 0,
-                                          pw, pb);
-  UL_TRY(check_launch("skinny_bwd_kernel"));
-  if (gw) {
-    reduce_parts_kernel<<<(unsigned)ceil_div((int64_t)N * K, 32), 256, 0, s>>>(pw, nblk,
-                                                                               (int64_t)N * K, gw);
-    UL_TRY(check_launch("reduce_parts_kernel"));
-  }
-  if (gb) {
-    reduce_parts_kernel<<<(unsigned)ceil_div(N, 32), 256, 0, s>>>(pb, nblk, N, gb);
-    UL_TRY(check_launch("reduce_parts_kernel"));
-  }
-  return UL_OK;
+  if (dtype == kBf16)
+    return bwd_t<__nv_bfloat16>(h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs,
+                                part, s);
+  return bwd_t<float>(h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs, part, s);
 }
 
 }  // namespace ul

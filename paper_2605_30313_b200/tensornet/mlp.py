@@ -196,7 +196,7 @@ def forward(params: ModelParams, x) -> tuple:
 def _staged(params: ModelParams):
     """(backend, staged weights) for one MLP pass: the tensor-core path reads
     W through 16-byte-aligned padded rows restaged from the live parameters."""
-    be = _lib.gemm_backend()
+    be = _lib.gemm_backend(input_grads=True)
     if be != _lib.UL_GEMM_TF32:
         return be, None
     desc = params.arch.desc()

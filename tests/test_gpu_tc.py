@@ -61,7 +61,7 @@ def test_tc_forward_layout(M, N, K, epi):
     C = torch.zeros((M, (N + 3) // 4 * 4), dtype=torch.float32, device="cuda")
     bd = torch.from_numpy(bias).cuda()
     _lib.call("ul_gemm_tc", 3, epi, M, N, K, _dev.ptr(A_), A_.stride(0), _dev.ptr(B_),
-              B_.stride(0), _dev.ptr(C), C.stride(0), _dev.ptr(bd), None, 0, 1, _dev.stream())
+              B_.stride(0), _dev.ptr(C), C.stride(0), _dev.ptr(bd), None, 0, 1, 0, _dev.stream())
     got = C[:, :N].cpu().numpy()
     assert _rel(got, ref) < 2e-3
 
@@ -78,7 +78,7 @@ def test_tc_dx_layout_elu_grad(M, N, K):
     A_, B_, H_ = _dev_mat(dh), _dev_mat(w), _dev_mat(h)
     C = torch.zeros((M, (N + 3) // 4 * 4), dtype=torch.float32, device="cuda")
     _lib.call("ul_gemm_tc", 1, 3, M, N, K, _dev.ptr(A_), A_.stride(0), _dev.ptr(B_), B_.stride(0),
-              _dev.ptr(C), C.stride(0), None, _dev.ptr(H_), H_.stride(0), 1, _dev.stream())
+              _dev.ptr(C), C.stride(0), None, _dev.ptr(H_), H_.stride(0), 1, 0, _dev.stream())
     assert _rel(C[:, :N].cpu().numpy(), ref) < 2e-3
 
 
@@ -97,7 +97,7 @@ def test_tc_dw_layout_split_k(out, inp, rows, splits):
     ldc = (inp + 3) // 4 * 4  # split partials: [zs][out][ldc], 16 B rows
     C = torch.zeros((zs, out, ldc), dtype=torch.float32, device="cuda")
     _lib.call("ul_gemm_tc", 0, 0, out, inp, rows, _dev.ptr(A_), A_.stride(0), _dev.ptr(B_),
-              B_.stride(0), _dev.ptr(C), ldc, None, None, 0, splits, _dev.stream())
+              B_.stride(0), _dev.ptr(C), ldc, None, None, 0, splits, 0, _dev.stream())
     got = C.sum(0)[:, :inp].cpu().numpy()
     assert _rel(got, ref) < 2e-3
 

@@ -45,8 +45,17 @@ def _time(fn, reps=20, warm=3):
     return best
 
 
+DT = int(os.environ.get("BENCH_DT", "0"))  # 0: fp32 / tf32, 1: bf16
+EL = torch.bfloat16 if DT else torch.float32
+EB = 2 if DT else 4
+
+
 def _ld(c):
     return (c + 3) // 4 * 4
+
+
+def _lda(c):  # operand / activation rows: 16 bytes
+    return (c + 7) // 8 * 8 if DT else (c + 3) // 4 * 4
 
 
 def main():
@@ -54,45 +63,46 @@ def main():
     dims = [235, 512, 256, 128]
     dev = "cuda"
     P = _dev.ptr
-    out = {"cluster_cap": os.environ.get("UL_TC_CLUSTER", "default")}
+    out = {"cluster_cap": os.environ.get("UL_TC_CLUSTER", "default"), "dtype": DT}
     for i in range(3):
         k, n = dims[i], dims[i + 1]
         kk = k + 1  # ones column
-        x = torch.randn(rows, _ld(kk), device=dev)
-        w = torch.randn(n, _ld(kk), device=dev) * 0.05
+        x = torch.randn(rows, _lda(kk), device=dev).to(EL)
+        w = (torch.randn(n, _lda(kk), device=dev) * 0.05).to(EL)
         b = torch.randn(n, device=dev)
-        h = torch.empty(rows, _ld(n), device=dev)
+        h = torch.empty(rows, _lda(n), device=dev, dtype=EL)
         t = _time(lambda: _lib.call("ul_gemm_tc", 3, 2, rows, n, kk, P(x), x.stride(0), P(w),
-                                    w.stride(0), P(h), h.stride(0), P(b), None, 0, 1, _dev.stream()))
+                                    w.stride(0), P(h), h.stride(0), P(b), None, 0, 1, DT, _dev.stream()))
         fl = 2.0 * rows * n * kk
-        by = 4.0 * rows * (kk + n)
+        by = EB * rows * (kk + n)
         out[f"fwd{i}"] = dict(MNK=[rows, n, kk], us=t * 1e6, tflops=fl / t / 1e12,
                               gbs=by / t / 1e9)
         # dW = dH^T X : M = n (out), N = kk (in + ones), K = rows
-        dh = torch.randn(rows, _ld(n), device=dev)
+        dh = torch.randn(rows, _lda(n), device=dev).to(EL)
         mt = -(-n // 128)
         nt = -(-kk // (256 if kk > 128 else 128))
         splits = max(1, -(-148 // (mt * nt)))
-        kps = -(-(-(-rows // splits)) // 32) * 32
+        bk = 64 if DT else 32
+        kps = -(-(-(-rows // splits)) // bk) * bk
         zs = -(-rows // kps)
         C = torch.empty(zs, n, _ld(kk), device=dev)
         t = _time(lambda: _lib.call("ul_gemm_tc", 0, 0, n, kk, rows, P(dh), dh.stride(0), P(x),
-                                    x.stride(0), P(C), _ld(kk), None, None, 0, splits,
+                                    x.stride(0), P(C), _ld(kk), None, None, 0, splits, DT,
                                     _dev.stream()))
         fl = 2.0 * rows * n * kk
-        by = 4.0 * rows * (kk + n) + 4.0 * zs * n * kk
+        by = EB * rows * (kk + n) + 4.0 * zs * n * kk
         out[f"dw{i}"] = dict(MNK=[n, kk, rows], splits=zs, us=t * 1e6, tflops=fl / t / 1e12,
                              gbs=by / t / 1e9)
         if i > 0:
             # dX = dH W (ELU-grad epilogue): M = rows, N = k, K = n
-            wt = torch.randn(n, _ld(k), device=dev) * 0.05
-            hp = torch.randn(rows, _ld(k), device=dev)
-            dx = torch.empty(rows, _ld(k), device=dev)
+            wt = (torch.randn(n, _lda(k), device=dev) * 0.05).to(EL)
+            hp = torch.randn(rows, _lda(k), device=dev).to(EL)
+            dx = torch.empty(rows, _lda(k), device=dev, dtype=EL)
             t = _time(lambda: _lib.call("ul_gemm_tc", 1, 3, rows, k, n, P(dh), dh.stride(0),
                                         P(wt), wt.stride(0), P(dx), dx.stride(0), None, P(hp),
-                                        hp.stride(0), 1, _dev.stream()))
+                                        hp.stride(0), 1, DT, _dev.stream()))
             fl = 2.0 * rows * n * k
-            by = 4.0 * rows * (n + 2 * k)
+            by = EB * rows * (n + 2 * k)
             out[f"dx{i}"] = dict(MNK=[rows, k, n], us=t * 1e6, tflops=fl / t / 1e12,
                                  gbs=by / t / 1e9)
     out["total_us"] = sum(v["us"] for v in out.values() if isinstance(v, dict))
