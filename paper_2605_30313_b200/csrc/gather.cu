@@ -28,6 +28,7 @@ struct GatherTable {
   int unit[kMaxDesc];            // unit bytes (16, 8 or 4)
   int64_t ones[kMaxDesc];        // byte offset of a float set to 1.0 in each row, -1 none
   int cvt[kMaxDesc];             // 1: fp32 source rows -> bf16 destination rows
+  int lpr_shift[kMaxDesc];       // log2(lanes per row)
   int ndesc;
 };
 
@@ -40,117 +41,107 @@ struct Vec<8> { using T = uint2; };
 template <>
 struct Vec<4> { using T = uint32_t; };
 
-template <int U>
+// One desc's rows.  A warp owns 32 / lpr rows at a time, lpr = a power of two
+// >= units per row (<= 32) lanes per row: lanes stream contiguous 16/8/4-byte
+// units of a row, no per-unit division, and R row groups are in flight per
+// warp (all loads issued before any store).  CVT: 16-byte fp32 source units
+// become 8-byte bf16 destination units.
+template <int U, bool CVT>
 __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __restrict__ dst,
-                                          int64_t sst, int64_t dstr, int64_t upr,
+                                          int64_t sst, int64_t dstr, int upr, int lpr_shift,
                                           const int64_t* __restrict__ idx, int64_t n,
                                           int64_t modulo, int64_t lo, int64_t hi, int* err,
                                           int64_t ones) {
   using T = typename Vec<U>::T;
-  constexpr int kIlp = 4;  // units in flight per thread: all loads issued before any store
-  const int64_t total = n * upr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < total;
-       w0 += stride * kIlp) {
-    T v[kIlp];
-    int64_t drow[kIlp], du[kIlp];
-    bool ok[kIlp];
+  constexpr int R = 4;
+  const int lane = threadIdx.x & 31;
+  const int lpr = 1 << lpr_shift, rpw = 32 >> lpr_shift;
+  const int sub = lane & (lpr - 1);
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t step = nw * rpw;  // rows between a warp's consecutive row groups
+  const int ones_u = ones >= 0 ? (int)(ones / U) : -1;
+  const int ones_e = ones >= 0 ? (int)((ones % U) / 4) : 0;
+  for (int64_t base = gw * rpw + (lane >> lpr_shift); base < n; base += step * R) {
+    const char* sp[R];
+    char* dp[R];
 #pragma unroll
-    for (int k = 0; k < kIlp; ++k) {
-      const int64_t w = w0 + k * stride;
-      ok[k] = false;
-      if (w >= total) continue;
-      const int64_t r = w / upr, u = w - r * upr;
+    for (int k = 0; k < R; ++k) {
+      const int64_t r = base + k * step;
+      sp[k] = nullptr;
+      dp[k] = dst + r * dstr;
+      if (r >= n) continue;
       int64_t s = idx ? __ldg(idx + r) : r;
-      drow[k] = r;
-      du[k] = u;
       if (s < lo || s >= hi) {
-        if (err) atomicOr(err, 1);
+        if (err && sub == 0) atomicOr(err, 1);
         continue;
       }
       if (modulo > 0) s %= modulo;
-      v[k] = __ldg(reinterpret_cast<const T*>(src + s * sst) + u);
-      ok[k] = true;
+      sp[k] = src + s * sst;
     }
+    // two units per lane per row in flight (rows up to 64 units = 1 KB of
+    // 16-byte units), then any remainder
+    for (int u0 = sub; u0 < upr; u0 += 2 * lpr) {
+      const int u1 = u0 + lpr;
+      T v[R][2];
 #pragma unroll
-    for (int k = 0; k < kIlp; ++k) {
-      if (!ok[k]) continue;
-      if (ones >= 0 && ones / U == du[k]) {
-        float* f = reinterpret_cast<float*>(&v[k]);
-        f[(ones % U) / 4] = 1.f;
+      for (int k = 0; k < R; ++k) {
+        if (sp[k]) {
+          v[k][0] = __ldg(reinterpret_cast<const T*>(sp[k]) + u0);
+          if (u1 < upr) v[k][1] = __ldg(reinterpret_cast<const T*>(sp[k]) + u1);
+        }
       }
-      reinterpret_cast<T*>(dst + drow[k] * dstr)[du[k]] = v[k];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        if (!sp[k]) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u = e ? u1 : u0;
+          if (u >= upr) continue;
+          if (CVT) {
+            float4 f4 = *reinterpret_cast<float4*>(&v[k][e]);
+            float f[4] = {f4.x, f4.y, f4.z, f4.w};
+            if (u == ones_u) f[ones_e] = 1.f;
+            __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]);
+            __nv_bfloat162 b = __floats2bfloat162_rn(f[2], f[3]);
+            uint2 o;
+            o.x = *reinterpret_cast<uint32_t*>(&a);
+            o.y = *reinterpret_cast<uint32_t*>(&b);
+            reinterpret_cast<uint2*>(dp[k])[u] = o;
+          } else {
+            if (u == ones_u) reinterpret_cast<float*>(&v[k][e])[ones_e] = 1.f;
+            reinterpret_cast<T*>(dp[k])[u] = v[k][e];
+          }
+        }
+      }
     }
   }
 }
 
-// fp32 -> bf16 rows (the bf16 MLP path's minibatch input): 16-byte source
-// units become 8-byte destination units
-__device__ __forceinline__ void copy_rows_bf16(const char* __restrict__ src,
-                                               char* __restrict__ dst, int64_t sst, int64_t dstr,
-                                               int64_t upr, const int64_t* __restrict__ idx,
-                                               int64_t n, int64_t modulo, int64_t lo, int64_t hi,
-                                               int* err, int64_t ones) {
-  constexpr int kIlp = 4;
-  const int64_t total = n * upr;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w0 < total;
-       w0 += stride * kIlp) {
-    float4 v[kIlp];
-    int64_t drow[kIlp], du[kIlp];
-    bool ok[kIlp];
-#pragma unroll
-    for (int k = 0; k < kIlp; ++k) {
-      const int64_t w = w0 + k * stride;
-      ok[k] = false;
-      if (w >= total) continue;
-      const int64_t r = w / upr, u = w - r * upr;
-      int64_t s = idx ? __ldg(idx + r) : r;
-      drow[k] = r;
-      du[k] = u;
-      if (s < lo || s >= hi) {
-        if (err) atomicOr(err, 1);
-        continue;
-      }
-      if (modulo > 0) s %= modulo;
-      v[k] = __ldg(reinterpret_cast<const float4*>(src + s * sst) + u);
-      ok[k] = true;
-    }
-#pragma unroll
-    for (int k = 0; k < kIlp; ++k) {
-      if (!ok[k]) continue;
-      float f[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-      if (ones >= 0 && ones / 16 == du[k]) f[(ones % 16) / 4] = 1.f;
-      __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]), b = __floats2bfloat162_rn(f[2], f[3]);
-      uint2 o;
-      o.x = *reinterpret_cast<uint32_t*>(&a);
-      o.y = *reinterpret_cast<uint32_t*>(&b);
-      reinterpret_cast<uint2*>(dst + drow[k] * dstr)[du[k]] = o;
-    }
-  }
-}
-
-__global__ void gather_kernel(GatherTable t, const int64_t* __restrict__ idx, int64_t n,
-                              int64_t modulo, int64_t lo, int64_t hi, int* err) {
+__global__ void __launch_bounds__(256) gather_kernel(GatherTable t,
+                                                     const int64_t* __restrict__ idx, int64_t n,
+                                                     int64_t modulo, int64_t lo, int64_t hi,
+                                                     int* err) {
   const int d = blockIdx.y;
   if (d >= t.ndesc) return;
+  const int upr = (int)t.units[d], sh = t.lpr_shift[d];
   if (t.cvt[d]) {
-    copy_rows_bf16(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                   modulo, lo, hi, err, t.ones[d]);
+    copy_rows<16, true>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
+                        modulo, lo, hi, err, t.ones[d]);
     return;
   }
   switch (t.unit[d]) {
     case 16:
-      copy_rows<16>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                    modulo, lo, hi, err, t.ones[d]);
+      copy_rows<16, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
+                           modulo, lo, hi, err, t.ones[d]);
       break;
     case 8:
-      copy_rows<8>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                   modulo, lo, hi, err, t.ones[d]);
+      copy_rows<8, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
+                          modulo, lo, hi, err, t.ones[d]);
       break;
     default:
-      copy_rows<4>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], t.units[d], idx, n,
-                   modulo, lo, hi, err, t.ones[d]);
+      copy_rows<4, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
+                          modulo, lo, hi, err, t.ones[d]);
   }
 }
 
@@ -234,10 +225,16 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
     t.cvt[d] = c;
     t.ones[d] = ones_byte ? ones_byte[d] : -1;
     UL_CHECK_ARG(t.ones[d] < row_bytes[d], "gather: ones column outside the row");
-    max_units = t.units[d] > max_units ? t.units[d] : max_units;
+    UL_CHECK_ARG(t.units[d] < (1 << 30), "gather: row too wide");
+    int sh = 0;
+    while (sh < 5 && (1 << sh) < t.units[d]) ++sh;
+    t.lpr_shift[d] = sh;
+    // warps needed for R = 4 row groups in flight each
+    const int64_t warps = ceil_div(n, (int64_t)(32 >> sh) * 4);
+    max_units = warps > max_units ? warps : max_units;
   }
-  int64_t blocks = ceil_div(n * max_units, 256);
-  blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
+  int64_t blocks = ceil_div(max_units, 8);  // max_units: most warps any desc wants
+  blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
   gather_kernel<<<dim3((unsigned)blocks, ndesc), 256, 0, stream>>>(t, idx, n, modulo, lo, hi,
                                                                     err);
   return check_launch("gather_kernel");

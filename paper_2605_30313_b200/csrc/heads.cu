@@ -19,21 +19,41 @@ namespace {
 
 constexpr double kLog2Pi = 1.8378770664093453;
 
-__global__ void __launch_bounds__(256) ppo_head_kernel(PpoHeadArgs a) {
-  __shared__ double scratch[32];
+constexpr int kHeadThr = 128, kHeadWarps = kHeadThr / 32;
+
+__global__ void __launch_bounds__(kHeadThr) ppo_head_kernel(PpoHeadArgs a) {
+  __shared__ double s_ls[UL_MAX_ACT], s_isd[UL_MAX_ACT];
+  __shared__ double red[kHeadWarps][3 + UL_MAX_ACT];
+  __shared__ double s_lsum;
+  const int A = a.A, nq = 3 + A;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // per-dimension constants once per block: log_std and 1/std
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    const double ls = (double)a.log_std[j];
+    s_ls[j] = ls;
+    s_isd[j] = exp(-ls);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int j = 0; j < A; ++j) t += s_ls[j];
+    s_lsum = t;
+  }
+  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int A = a.A;
   const bool act_row = i < a.n_local;
   double pol = 0.0, val = 0.0, kl = 0.0, dlogp = 0.0;
   const double adv_mean = a.adv_stats ? a.adv_stats[0] : 0.0;
   const double adv_den = a.adv_stats ? a.adv_stats[1] + 1e-8 : 1.0;
+  const float* act = a.act + i * a.ld_act;
+  const float* mean = a.mean + i * a.ld_mean;
   if (act_row) {
-    double logp = 0.0;
+    double zz = 0.0;
     for (int j = 0; j < A; ++j) {
-      const double ls = (double)a.log_std[j];
-      const double z = ((double)a.act[i * a.ld_act + j] - (double)a.mean[i * a.ld_mean + j]) / exp(ls);
-      logp += -ls - 0.5 * kLog2Pi - 0.5 * z * z;
+      const double z = ((double)act[j] - (double)mean[j]) * s_isd[j];
+      zz += z * z;
     }
+    const double logp = -s_lsum - A * (0.5 * kLog2Pi) - 0.5 * zz;
     const double b = (double)a.blogp[i];
     const double adv = ((double)a.adv[i] - adv_mean) / adv_den;
     const double ratio = exp(logp - b);
@@ -43,11 +63,6 @@ __global__ void __launch_bounds__(256) ppo_head_kernel(PpoHeadArgs a) {
     pol = fmin(s1, s2);
     dlogp = (s1 <= s2) ? -adv * ratio / a.n_global : 0.0;
     kl = b - logp;
-    for (int j = 0; j < A; ++j) {
-      const double sd = exp((double)a.log_std[j]);
-      const double z = ((double)a.act[i * a.ld_act + j] - (double)a.mean[i * a.ld_mean + j]) / sd;
-      a.dmean[i * a.ld_dmean + j] = (float)(dlogp * z / sd);
-    }
     // value head (R:algos/ppo.py:107-118)
     const double v = (double)a.v[i * a.ld_v];
     const double R = (double)a.ret[i];
@@ -64,30 +79,57 @@ __global__ void __launch_bounds__(256) ppo_head_kernel(PpoHeadArgs a) {
     }
     a.dv[i] = (float)(dv * a.vcoef);
   }
-  // block partials: [pol, val, kl, dls_0 .. dls_{A-1}]
-  double* part = a.part + (int64_t)blockIdx.x * (3 + A);
-  double r = block_sum(pol, scratch);
-  if (threadIdx.x == 0) part[0] = r;
-  r = block_sum(val, scratch);
-  if (threadIdx.x == 0) part[1] = r;
-  r = block_sum(kl, scratch);
-  if (threadIdx.x == 0) part[2] = r;
+  // row terms, warp-reduced: [pol, val, kl, dls_0 .. dls_{A-1}]
+  double r = warp_sum(pol);
+  if (lane == 0) red[w][0] = r;
+  r = warp_sum(val);
+  if (lane == 0) red[w][1] = r;
+  r = warp_sum(kl);
+  if (lane == 0) red[w][2] = r;
   for (int j = 0; j < A; ++j) {
     double t = 0.0;
-    if (act_row && dlogp != 0.0) {
-      const double sd = exp((double)a.log_std[j]);
-      const double z = ((double)a.act[i * a.ld_act + j] - (double)a.mean[i * a.ld_mean + j]) / sd;
+    if (act_row) {
+      const double z = ((double)act[j] - (double)mean[j]) * s_isd[j];
+      a.dmean[i * a.ld_dmean + j] = (float)(dlogp * z * s_isd[j]);
       t = dlogp * (z * z - 1.0);
     }
-    r = block_sum(t, scratch);
-    if (threadIdx.x == 0) part[3 + j] = r;
+    t = warp_sum(t);
+    if (lane == 0) red[w][3 + j] = t;
+  }
+  __syncthreads();
+  double* part = a.part + (int64_t)blockIdx.x * nq;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k < kHeadWarps; ++k) t += red[k][q];
+    part[q] = t;
   }
   if (!last_block_ticket(a.ticket, gridDim.x)) return;
-  for (int q = threadIdx.x; q < 3 + A; q += blockDim.x) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += a.part[(int64_t)b * (3 + A) + q];
-    if (q < 3) a.loss_out[q] = (float)s;
-    else a.dlogstd_out[q - 3] = (float)(s + a.ent_coef_add);
+  // last CTA: fixed-order fold of the per-CTA partials.  8 lanes per term
+  // (16 terms per pass), each summing blocks b = l, l + 8, ... with all loads
+  // in flight, then a 3-step shuffle tree within the 8 lanes.
+  const unsigned nb = gridDim.x;
+  for (int q0 = 0; q0 < nq; q0 += kHeadThr / 8) {
+    const int q = q0 + (int)(threadIdx.x >> 3), l = threadIdx.x & 7;
+    double t = 0.0;
+    if (q < nq) {
+      for (unsigned b0 = l; b0 < nb; b0 += 64) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const unsigned b = b0 + 8 * u;
+          v[u] = b < nb ? a.part[(int64_t)b * nq + q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t += v[u];
+      }
+    }
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    t += __shfl_xor_sync(0xffffffffu, t, 4);
+    if (q < nq && l == 0) {
+      if (q < 3) a.loss_out[q] = (float)t;
+      else a.dlogstd_out[q - 3] = (float)(t + a.ent_coef_add);
+    }
   }
 }
 
@@ -167,13 +209,13 @@ __global__ void gauss_logp_kernel(const float* __restrict__ mean, int64_t ldm,
 }  // namespace
 
 int launch_ppo_head(const PpoHeadArgs& a, cudaStream_t s) {
-  const unsigned blocks = (unsigned)ceil_div(a.n_local > 0 ? a.n_local : 1, 256);
-  ppo_head_kernel<<<blocks, 256, 0, s>>>(a);
+  const unsigned blocks = (unsigned)ceil_div(a.n_local > 0 ? a.n_local : 1, kHeadThr);
+  ppo_head_kernel<<<blocks, kHeadThr, 0, s>>>(a);
   return check_launch("ppo_head_kernel");
 }
 
 int ppo_head_partial_doubles(int64_t n_local, int A) {
-  return (int)(ceil_div(n_local > 0 ? n_local : 1, 256) * (3 + A));
+  return (int)(ceil_div(n_local > 0 ? n_local : 1, kHeadThr) * (3 + A));
 }
 
 int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ticket, double* out,

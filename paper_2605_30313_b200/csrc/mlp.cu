@@ -32,77 +32,128 @@ namespace {
 
 int64_t rup(int64_t x, int64_t m) { return ceil_div(x, m) * m; }
 
+// ws: splits x [out, ldp] fp32 partials (ldp % 4 == 0); column `in` is the
+// bias gradient, columns > in are TMA-row padding.  A warp owns 128 columns
+// (float4 lanes) and the splits z = w, w + 8, ... with every load issued
+// before the adds; the 8 warps combine in fixed order (deterministic).
 __global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict__ ws, int splits,
                                                         int64_t out, int64_t in, int64_t ldp,
                                                         float* __restrict__ gw,
                                                         float* __restrict__ gb) {
-  // ws: splits x [out, ldp]; column `in` is the bias gradient, columns > in
-  // are TMA-row padding.  32 outputs per CTA, splits spread over 8 warps,
-  // fixed-order combine (deterministic).
-  __shared__ float sm[8][33];
+  __shared__ float4 sm[8][32];
   const int64_t len = out * ldp;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-  float s = 0.f;
+  const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (j < len) {
-    // four independent accumulators keep 4 loads in flight per warp
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    int z = w;
-    for (; z + 24 < splits; z += 32) {
-      s0 += ws[(int64_t)z * len + j];
-      s1 += ws[(int64_t)(z + 8) * len + j];
-      s2 += ws[(int64_t)(z + 16) * len + j];
-      s3 += ws[(int64_t)(z + 24) * len + j];
+    for (int z0 = w; z0 < splits; z0 += 64) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int z = z0 + 8 * u;
+        v[u] = z < splits ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * len + j))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        s.x += v[u].x;
+        s.y += v[u].y;
+        s.z += v[u].z;
+        s.w += v[u].w;
+      }
     }
-    for (; z < splits; z += 8) s0 += ws[(int64_t)z * len + j];
-    s = (s0 + s1) + (s2 + s3);
   }
   sm[w][lane] = s;
   __syncthreads();
   if (w == 0 && j < len) {
-    float t = 0.f;
+    float4 t = sm[0][lane];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += sm[k][lane];
-    const int64_t r = j / ldp, c = j - r * ldp;
-    if (c < in) gw[r * in + c] = t;
-    else if (c == in && gb) gb[r] = t;
+    for (int k = 1; k < 8; ++k) {
+      const float4 q = sm[k][lane];
+      t.x += q.x;
+      t.y += q.y;
+      t.z += q.z;
+      t.w += q.w;
+    }
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+    const int64_t r = j / ldp, c0 = j - r * ldp;  // 4 | ldp: one row per float4
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t c = c0 + e;
+      if (c < in) gw[r * in + c] = tv[e];
+      else if (c == in && gb) gb[r] = tv[e];
+    }
   }
 }
 
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// db partials: column sums of dh [M, N] over row chunks; lanes = columns
-// (coalesced rows), 8 warps stride the rows, 8 loads in flight per thread;
-// part[chunk][N]
+// db partials: column sums of dh [M, N] over row chunks; a thread owns 8
+// consecutive columns (one 16 B bf16 / 2 x 16 B fp32 load per row), 8 warps
+// stride the rows with 4 rows in flight; part[chunk][N].  Needs ld % 8 == 0
+// and a 16 B-aligned base (the hidden-gradient buffers).
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float (&f)[8]);
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, int64_t ld,
                                                      int64_t M, int64_t N, int64_t rows_per,
                                                      float* __restrict__ part) {
-  __shared__ float sm[8][33];
+  __shared__ float sm[8][32 * 8 + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t c = ((int64_t)blockIdx.x * 32 + lane) * 8;  // first of 8 columns
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  if (c < N) {
+  if (c < N && c + 8 > ld) {
+    // row tail narrower than 8 columns of pitch: scalar loads
+    for (int64_t r = r0 + w; r < r1; r += 8)
+      for (int i = 0; i < 8 && c + i < N; ++i) s[i] += to_f(x[r * ld + c + i]);
+  } else if (c < N) {
     int64_t r = r0 + w;
-    for (; r + 56 < r1; r += 64) {
-      T v[8];
+    for (; r + 24 < r1; r += 32) {
+      float f[4][8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = x[(r + 8 * i) * ld + c];
+      for (int k = 0; k < 4; ++k) load8<T>(x + (r + 8 * k) * ld + c, f[k]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s[i] += to_f(v[i]);
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[i] += f[k][i];
     }
-    for (; r < r1; r += 8) s[0] += to_f(x[r * ld + c]);
+    for (; r < r1; r += 8) {
+      float f[8];
+      load8<T>(x + r * ld + c, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s[i] += f[i];
+    }
   }
-  sm[w][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sm[w][lane * 8 + i] = s[i];
   __syncthreads();
-  if (w == 0 && c < N) {
+  for (int q = threadIdx.x; q < 256; q += blockDim.x) {
+    const int64_t cc = (int64_t)blockIdx.x * 256 + q;
+    if (cc >= N) continue;
     float t = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += sm[k][lane];
-    part[(int64_t)blockIdx.y * N + c] = t;
+    for (int k = 0; k < 8; ++k) t += sm[k][q];
+    part[(int64_t)blockIdx.y * N + cc] = t;
   }
 }
 
@@ -395,16 +446,17 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
         const int sp = tc_num_splits(M, gt.splits, dt);
         gt.splits = sp;
         UL_TRY(gemm_tc(gt, -1, s));
-        const int64_t blocks = ceil_div(out * gt.ldc, 32);
+        const int64_t blocks = ceil_div(out * gt.ldc, 128);
         reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(
             ws, sp, out, in, gt.ldc, grads + v.w_off[i],
             ones_free ? grads + v.b_off[i] : nullptr);
         UL_TRY(check_launch("reduce_dw_kernel"));
         if (!ones_free && db_done != i) {
-          const int64_t chunks = ceil_div(M, 512) < 256 ? ceil_div(M, 512) : 256;
+          // 128-row chunks (8 warps x 4 rows in flight x 4), at most 256 of them
+          const int64_t chunks = ceil_div(M, 128) < 256 ? ceil_div(M, 128) : 256;
           const int64_t rows_per = ceil_div(M, chunks);
           float* part = ws + (int64_t)sp * out * gt.ldc;
-          const dim3 grid((unsigned)ceil_div(out, 32), (unsigned)chunks);
+          const dim3 grid((unsigned)ceil_div(out, 256), (unsigned)chunks);
           if (dt == kBf16)
             colsum_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(dh), lddh,
                                                M, out, rows_per, part);

@@ -33,10 +33,19 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_o
     double acc = 0.0;
     int bad = 0;
     const int64_t stride = (int64_t)nb * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-      const float x = g[i];
-      acc += (double)x * (double)x;
-      bad |= !isfinite(x);
+    // 8 loads in flight per thread (issued before the dependent adds)
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 8 * stride) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = i0 + u * stride;
+        x[u] = i < n ? __ldg(g + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc += (double)x[u] * (double)x[u];
+        bad |= !isfinite(x[u]);
+      }
     }
     const double tot = block_sum(acc, scratch);
     const int any_bad = __syncthreads_or(bad);
@@ -232,7 +241,7 @@ int64_t max_n(const SegTable& st) {
 
 int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s) {
   int64_t nmax = max_n(st);
-  int blocks = (int)ceil_div(nmax, kPrepThreads * 4);
+  int blocks = (int)ceil_div(nmax, kPrepThreads * 8);
   blocks = blocks < 1 ? 1 : (blocks > UL_PREP_BLOCKS ? UL_PREP_BLOCKS : blocks);
   prepare_kernel<<<blocks, kPrepThreads, 0, s>>>(st, ctl);
   return check_launch("prepare_kernel");

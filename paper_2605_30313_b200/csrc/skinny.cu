@@ -82,9 +82,32 @@ __device__ __forceinline__ void stage_tile(const T* __restrict__ h, int64_t ldh,
   __syncthreads();
 }
 
-// out[r, j] = b[j] + sum_k h[r, k] W[j, k]; thread (row r = t/4, q = t%4)
-// accumulates outputs j = q, q+4, ...
-template <typename TH>
+// W[:, k0:k0+kc] -> sw (pitch PW, zero beyond kc): all of a thread's loads are
+// issued before its smem stores (one memory round trip, not one per element)
+__device__ __forceinline__ void stage_w(const float* __restrict__ W, int K, int N, int NP, int k0,
+                                        int kc, int KC, float* sw, int PW) {
+  const int total = NP * KC;  // rows N..NP-1 are zero padding
+  for (int base = threadIdx.x; base < total; base += kThr * 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = base + u * kThr;
+      const int j = e / KC, c = e - j * KC;
+      v[u] = (e < total && c < kc && j < N) ? __ldg(W + (int64_t)j * K + k0 + c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = base + u * kThr;
+      const int j = e / KC, c = e - j * KC;
+      if (e < total) sw[j * PW + c] = v[u];
+    }
+  }
+}
+
+// out[r, j] = b[j] + sum_k h[r, k] W[j, k].  Thread (row r = t/4, q = t%4)
+// covers the 4-column groups c = 4q + 16i for all NP (>= N, padded) outputs;
+// the row's four partial sums meet through two lane shuffles.
+template <typename TH, int NP>
 __global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const TH* __restrict__ h, int64_t ldh,
                                                           int64_t M, int K, int N,
                                                           const float* __restrict__ W,
@@ -97,48 +120,45 @@ __global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const TH* __restrict__
   float* sw = reinterpret_cast<float*>(smem + (size_t)kRows * P * sizeof(TH));
   const int t = threadIdx.x, r = t >> 2, q = t & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kRows;
-  float acc[kMaxN / 4];
+  float acc[NP];
 #pragma unroll
-  for (int u = 0; u < kMaxN / 4; ++u) acc[u] = 0.f;
+  for (int j = 0; j < NP; ++j) acc[j] = 0.f;
   for (int k0 = 0; k0 < K; k0 += KC) {
     const int kc = K - k0 < KC ? K - k0 : KC;
-    for (int e = t; e < N * KC; e += kThr) {
-      const int j = e / KC, c = e - j * KC;
-      sw[j * PW + c] = c < kc ? __ldg(W + (int64_t)j * K + k0 + c) : 0.f;
-    }
+    stage_w(W, K, N, NP, k0, kc, KC, sw, PW);
     stage_tile<TH>(h, ldh, M, r0, k0, kc, sh, P);
-    // zero the tail of the last 16-byte group (cp.async copies whole groups)
     const TH* hr = sh + r * P;
-    for (int c = 0; c < kc; c += 4) {
+    for (int c = 4 * q; c < kc; c += 16) {
       float4 hv = ld4<TH>(hr + c);
+      // cp.async copies whole 16-byte groups: columns >= kc may hold padding
       if (c + 4 > kc) {
         if (c + 1 >= kc) hv.y = 0.f;
         if (c + 2 >= kc) hv.z = 0.f;
         if (c + 3 >= kc) hv.w = 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < kMaxN / 4; ++u) {
-        const int j = q + 4 * u;
-        if (j < N) {
-          const float4 w = *reinterpret_cast<const float4*>(sw + j * PW + c);
-          acc[u] = fmaf(hv.x, w.x, fmaf(hv.y, w.y, fmaf(hv.z, w.z, fmaf(hv.w, w.w, acc[u]))));
-        }
+      for (int j = 0; j < NP; ++j) {
+        const float4 w = *reinterpret_cast<const float4*>(sw + j * PW + c);
+        acc[j] = fmaf(hv.x, w.x, fmaf(hv.y, w.y, fmaf(hv.z, w.z, fmaf(hv.w, w.w, acc[j]))));
       }
     }
     __syncthreads();
   }
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+    acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 1);
+    acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 2);
+  }
   const int64_t gr = r0 + r;
   if (gr < M) {
 #pragma unroll
-    for (int u = 0; u < kMaxN / 4; ++u) {
-      const int j = q + 4 * u;
-      if (j < N) out[gr * ldo + j] = acc[u] + b[j];
-    }
+    for (int j = 0; j < NP; ++j)
+      if ((j & 3) == q && j < N) out[gr * ldo + j] = acc[j] + __ldg(b + j);
   }
 }
 
 // Per block z: part[z] = [dW partial (N x K) | db partial (N) | colsum(dh) (K, if csum)]
-template <typename TH>
+template <typename TH, int NP>
 __global__ void __launch_bounds__(kThr) skinny_bwd_kernel(
     const TH* __restrict__ h, int64_t ldh, int64_t M, int K, int N, const float* __restrict__ W,
     const float* __restrict__ dout, int64_t ldd, TH* __restrict__ dh, int64_t lddh, int elu_grad,
@@ -148,15 +168,26 @@ __global__ void __launch_bounds__(kThr) skinny_bwd_kernel(
   const int P = pitch_of<TH>(KC), PW = pitch_of<float>(KC);
   TH* sh = reinterpret_cast<TH*>(smem);
   float* sw = reinterpret_cast<float*>(smem + (size_t)kRows * P * sizeof(TH));
-  float* sd = sw + (size_t)N * PW;         // [kRows][kMaxN + 1] upstream gradient
+  float* sd = sw + (size_t)NP * PW;        // [kRows][kMaxN + 1] upstream gradient
   float* sdh = sd + kRows * (kMaxN + 1);   // [kRows][PW] dh tile (column sums)
   const int t = threadIdx.x, r = t >> 2, q = t & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kRows;
   float* pz = part + (int64_t)blockIdx.x * plen;
-  for (int e = t; e < kRows * N; e += kThr) {
-    const int rr = e / N, j = e - rr * N;
-    const int64_t gr = r0 + rr;
-    sd[rr * (kMaxN + 1) + j] = gr < M ? dout[gr * ldd + j] : 0.f;
+  for (int base = t; base < kRows * N; base += kThr * 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = base + u * kThr;
+      const int rr = e / N, j = e - rr * N;
+      const int64_t gr = r0 + rr;
+      v[u] = (e < kRows * N && gr < M) ? __ldg(dout + gr * ldd + j) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = base + u * kThr;
+      const int rr = e / N, j = e - rr * N;
+      if (e < kRows * N) sd[rr * (kMaxN + 1) + j] = v[u];
+    }
   }
   __syncthreads();
   if (want_dw && t < N) {
@@ -164,30 +195,25 @@ __global__ void __launch_bounds__(kThr) skinny_bwd_kernel(
     for (int rr = 0; rr < kRows; ++rr) s += sd[rr * (kMaxN + 1) + t];
     pz[(int64_t)N * K + t] = s;
   }
-  float g[kMaxN];
+  float g[NP];
 #pragma unroll
-  for (int j = 0; j < kMaxN; ++j) g[j] = j < N ? sd[r * (kMaxN + 1) + j] : 0.f;
+  for (int j = 0; j < NP; ++j) g[j] = j < N ? sd[r * (kMaxN + 1) + j] : 0.f;
   const int64_t gr = r0 + r;
   for (int k0 = 0; k0 < K; k0 += KC) {
     const int kc = K - k0 < KC ? K - k0 : KC;
-    for (int e = t; e < N * KC; e += kThr) {
-      const int j = e / KC, c = e - j * KC;
-      sw[j * PW + c] = c < kc ? __ldg(W + (int64_t)j * K + k0 + c) : 0.f;
-    }
+    stage_w(W, K, N, NP, k0, kc, KC, sw, PW);
     stage_tile<TH>(h, ldh, M, r0, k0, kc, sh, P);
     // dh for row r, 4-column groups c = 4q, 4q + 16, ...
     if (dh) {
       for (int c = 4 * q; c < kc; c += 16) {
         float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < kMaxN; ++j) {
-          if (j < N) {
-            const float4 w = *reinterpret_cast<const float4*>(sw + j * PW + c);
-            s.x = fmaf(g[j], w.x, s.x);
-            s.y = fmaf(g[j], w.y, s.y);
-            s.z = fmaf(g[j], w.z, s.z);
-            s.w = fmaf(g[j], w.w, s.w);
-          }
+        for (int j = 0; j < NP; ++j) {
+          const float4 w = *reinterpret_cast<const float4*>(sw + j * PW + c);
+          s.x = fmaf(g[j], w.x, s.x);
+          s.y = fmaf(g[j], w.y, s.y);
+          s.z = fmaf(g[j], w.z, s.z);
+          s.w = fmaf(g[j], w.w, s.w);
         }
         if (elu_grad) {
           const float4 hv = ld4<TH>(sh + r * P + c);
@@ -296,60 +322,90 @@ __global__ void __launch_bounds__(1024) reduce_parts_kernel(const float* __restr
 }
 
 template <typename TH>
-size_t fwd_smem(int K, int N) {
+size_t fwd_smem(int K, int NP) {
   const int KC = K < kKC ? (K + 7) / 8 * 8 : kKC;
-  return (size_t)kRows * pitch_of<TH>(KC) * sizeof(TH) + (size_t)N * pitch_of<float>(KC) * 4;
+  return (size_t)kRows * pitch_of<TH>(KC) * sizeof(TH) + (size_t)NP * pitch_of<float>(KC) * 4;
 }
 template <typename TH>
-size_t bwd_smem(int K, int N) {
+size_t bwd_smem(int K, int NP) {
   const int KC = K < kKC ? (K + 7) / 8 * 8 : kKC;
-  return fwd_smem<TH>(K, N) + (size_t)kRows * (kMaxN + 1) * 4 +
+  return fwd_smem<TH>(K, NP) + (size_t)kRows * (kMaxN + 1) * 4 +
          (size_t)kRows * pitch_of<float>(KC) * 4;
 }
+
+// padded output count: the kernels are instantiated for these
+inline int pad_n(int N) {
+  const int sizes[] = {1, 2, 4, 8, 12, 16, 24, 32};
+  for (int v : sizes)
+    if (N <= v) return v;
+  return 0;
+}
+
+template <typename TH, int NP>
+int fwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* b,
+           float* out, int64_t ldo, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    UL_CUDA(cudaFuncSetAttribute(skinny_fwd_kernel<TH, NP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  skinny_fwd_kernel<TH, NP><<<(unsigned)ceil_div(M, kRows), kThr, fwd_smem<TH>(K, NP), s>>>(
+      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, b, out, ldo);
+  return check_launch("skinny_fwd_kernel");
+}
+
+template <typename TH, int NP>
+int bwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* dout,
+           int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw, float* gb, float* gcs,
+           float* part, cudaStream_t s) {
+  const int nblk = (int)ceil_div(M, kRows);
+  const bool want_dw = gw || gb;
+  const bool csum = gcs != nullptr && dh != nullptr;
+  const int64_t plen = (int64_t)N * K + N + (csum ? K : 0);
+  static bool attr = false;
+  if (!attr) {
+    UL_CUDA(cudaFuncSetAttribute(skinny_bwd_kernel<TH, NP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  skinny_bwd_kernel<TH, NP><<<nblk, kThr, bwd_smem<TH>(K, NP), s>>>(
+      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, dout, ldd, reinterpret_cast<TH*>(dh), lddh,
+      elu_grad ? 1 : 0, part, plen, want_dw ? 1 : 0, csum ? 1 : 0);
+  UL_TRY(check_launch("skinny_bwd_kernel"));
+  if (want_dw || csum) {
+    reduce_parts_kernel<<<(unsigned)ceil_div(plen, 128), 1024, 0, s>>>(
+        part, nblk, plen, (int64_t)N * K, gw, N, gb, csum ? K : 0, gcs);
+    UL_TRY(check_launch("reduce_parts_kernel"));
+  }
+  return UL_OK;
+}
+
+#define UL_SKINNY_NP(FN, ...)                         \
+  switch (pad_n(N)) {                                 \
+    case 1: return FN<TH, 1>(__VA_ARGS__);            \
+    case 2: return FN<TH, 2>(__VA_ARGS__);            \
+    case 4: return FN<TH, 4>(__VA_ARGS__);            \
+    case 8: return FN<TH, 8>(__VA_ARGS__);            \
+    case 12: return FN<TH, 12>(__VA_ARGS__);          \
+    case 16: return FN<TH, 16>(__VA_ARGS__);          \
+    case 24: return FN<TH, 24>(__VA_ARGS__);          \
+    default: return FN<TH, 32>(__VA_ARGS__);          \
+  }
 
 template <typename TH>
 int fwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* b,
           float* out, int64_t ldo, cudaStream_t s) {
-  const size_t sm = fwd_smem<TH>(K, N);
-  static bool attr = false;
-  if (!attr) {
-    UL_CUDA(cudaFuncSetAttribute(skinny_fwd_kernel<TH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  skinny_fwd_kernel<TH><<<(unsigned)ceil_div(M, kRows), kThr, sm, s>>>(
-      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, b, out, ldo);
-  return check_launch("skinny_fwd_kernel");
+  UL_SKINNY_NP(fwd_np, h, ldh, M, K, N, W, b, out, ldo, s)
 }
 
 template <typename TH>
 int bwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* dout,
           int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw, float* gb, float* gcs,
           float* part, cudaStream_t s) {
-  const int nblk = (int)ceil_div(M, kRows);
-  const bool want_dw = gw || gb;
-  const bool csum = gcs != nullptr && dh != nullptr;
-  const int64_t plen = (int64_t)N * K + N + (csum ? K : 0);
-  const size_t sm = bwd_smem<TH>(K, N);
-  static bool attr = false;
-  if (!attr) {
-    UL_CUDA(cudaFuncSetAttribute(skinny_bwd_kernel<TH>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  skinny_bwd_kernel<TH><<<nblk, kThr, sm, s>>>(
-      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, dout, ldd, reinterpret_cast<TH*>(dh), lddh,
-      elu_grad ? 1 : 0, part, plen, want_dw ? 1 : 0, csum ? 1 : 0);
-  UL_TRY(check_launch("skinny_bwd_kernel"));
-  if (want_dw || csum) {
-    const int64_t total = plen;
-    reduce_parts_kernel<<<(unsigned)ceil_div(total, 128), 1024, 0, s>>>(
-        part, nblk, plen, want_dw ? (int64_t)N * K : (int64_t)N * K, gw, N, gb,
-        csum ? K : 0, gcs);
-    UL_TRY(check_launch("reduce_parts_kernel"));
-  }
-  return UL_OK;
+  UL_SKINNY_NP(bwd_np, h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs, part, s)
 }
+#undef UL_SKINNY_NP
 
 }  // namespace
 
