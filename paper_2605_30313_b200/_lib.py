@@ -145,6 +145,7 @@ _PROTOS = {
                               vp, i64, vp]),
     "ul_gemm_tc": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
                              vp, i64, C.c_int, C.c_int, vp]),
+    "ul_tc_trace": (C.c_int, [vp]),
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                  C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
                                  vp]),

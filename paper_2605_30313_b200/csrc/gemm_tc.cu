@@ -98,15 +98,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                               int c0, int c1, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(su32(dst)),
-      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-
 // UMMA shared-memory matrix descriptor, sm100 version bit.  Layout type 2 =
 // SWIZZLE_128B (16-byte atoms), 1 = SWIZZLE_128B_BASE32B (32-byte atoms).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
@@ -146,14 +137,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    su32(bar))
                : "memory");
-}
-
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;" ::"r"(su32(bar)),
-      "h"(mask)
-      : "memory");
 }
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -197,7 +180,19 @@ struct TcArgs {
   int64_t ldc;
   const float* bias;
   int ones_col;          // >= 0: also write C[m, ones_col] = 1 (activation ones column)
+  unsigned long long* trace;  // diagnostics (UL_TC_TRACE): CTA 0 event timestamps, or null
 };
+
+// trace slots: [0] entry, [1] setup done, [2..33] producer k-tile issue,
+// [34..65] MMA full-barrier pass, [66..81] epilogue acc ready, [82..97]
+// epilogue tile done, [98] exit
+__device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
+  if (tr && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[slot] = t;
+  }
+}
 
 constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
 constexpr int kPThreads = (2 + kEpiWarps) * 32;
@@ -207,41 +202,91 @@ template <typename TI, int EPI>
 using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu || EPI == kEpiEluGrad),
                                        __nv_bfloat16, float>::type;
 
-// [stage ring][16 x 4 KB epilogue staging][barriers][bias x 2]
-template <int BN>
+// [stage ring][16 epilogue staging boxes][barriers][bias x 2]; as many stages
+// as fit the 227 KB of dynamic shared memory (at most 6)
+template <int BN, bool PAIR, int OB /* output element bytes */>
 struct Smem {
-  static constexpr int kStages = BN >= 256 ? 3 : 4;
   static constexpr int kABytes = BM * 128;
-  static constexpr int kBBytes = BN * 128;
+  static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * 128;  // this CTA's share of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagingBytes = kEpiWarps * 4096;
-  static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + 1024 /*align*/ +
-                                512 /*barriers*/ + 2 * BN * 4 /*bias, per accumulator*/;
+  static constexpr int kStagingBytes = kEpiWarps * 32 * 32 * OB;
+  static constexpr int kFixed = 1024 /*align*/ + 512 /*barriers*/ + 2 * BN * 4 /*bias*/;
+  static constexpr int kBudget = 232448;
+  static constexpr int kStagesFit = (kBudget - kStagingBytes - kFixed) / kStageBytes;
+  static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
+  static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + kFixed;
 };
 
-// Persistent: the grid is sized to the co-resident CTAs; tile groups are
-// walked with a cluster-strided loop.  The smem ring runs continuously across
-// tiles and the TMEM accumulator is double-buffered, so tile i's epilogue
-// overlaps tile i+1's TMA + MMA main loop.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                         uint32_t idesc, uint32_t acc) {
+  if constexpr (sizeof(T) == 4) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  }
+}
+
+// commit the leader's MMAs to the same barrier offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// Persistent: the grid is sized to the co-resident CTAs (pairs); tiles are
+// walked with a strided loop.  The smem ring runs continuously across tiles
+// and the TMEM accumulator is double-buffered, so tile i's epilogue overlaps
+// tile i+1's TMA + MMA main loop.
 //
-// CS = cluster size along M.  The CS CTAs of a cluster work on CS consecutive
-// M-tiles of the same (N-tile, K-split) and share its B tile: CTA r fetches
-// 1/CS of B and TMA-multicasts it into every CTA of the cluster.  A stage is
-// refilled only after every CTA's MMAs consumed it (empty barriers count CS
-// multicast commits).
-template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, int CS>
+// PAIR (cta_group::2): the two CTAs of a cluster (one TPC) compute one
+// 256 x BN tile with M=256 UMMAs issued by the leader CTA.  Each CTA loads its
+// own 128 rows of A and HALF of the B tile (BN/2 rows of N), so a stage is
+// 32 KB instead of 48 KB per SM -- the L2->SM operand traffic (the bound of
+// these short-K GEMMs) drops by a third and one more stage fits in smem.  Both
+// CTAs' TMA loads complete on the leader's full barrier; the leader's commits
+// are multicast to both CTAs' empty / accumulator barriers; both epilogues
+// drain their own TMEM lanes and release the accumulator on the leader.
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
                    TcArgs p) {
-  using S = Smem<BN>;
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
+  using S = Smem<BN, PAIR, (int)sizeof(TO)>;
   constexpr bool kOutBf16 = sizeof(TO) == 2;
+  constexpr int CS = PAIR ? 2 : 1;
+  constexpr int BNL = BN / CS;  // B rows (N) this CTA loads
   constexpr int BK = O::BK;
   constexpr uint32_t kChunkBytes = (uint32_t)BK * 128;  // one MN-major TMA box
   constexpr int kStages = S::kStages;
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
+  constexpr uint32_t kBoxBytes = 32 * 32 * sizeof(TO);
+  static_assert(kStages >= 2, "shared memory too small for the pipeline");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -254,22 +299,23 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_at(p.trace, 0);
 
   uint32_t crank = 0;
-  if (CS > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const bool leader = crank == 0;
   const int mgroups = (p.mt + CS - 1) / CS;
   const int ngroups = mgroups * p.nt * p.zt;
   const int cl = blockIdx.x / CS, ncl = gridDim.x / CS;
-  constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1u);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CS);  // one (multicast) MMA commit from every CTA of the cluster
+      mbar_init(&full[s], 1);   // (leader) producer arrive + both CTAs' TMA bytes
+      mbar_init(&empty[s], 1);  // one (multicast) MMA commit
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], kEpiWarps);
+      mbar_init(&acc_empty[b], CS * kEpiWarps);  // both CTAs' epilogue warps (leader)
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&aux_bar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -280,19 +326,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(kCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(kCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_slot)),
+                   "r"(kCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (CS > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
+  if (PAIR) cluster_sync_all();  // peer barriers initialised before any cross-CTA signal
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) trace_at(p.trace, 1);
 
   // group t -> (M-tile group, N-tile, split); this CTA takes M-tile
-  // group*CS + rank, so the cluster shares one B tile per group
+  // group*CS + rank
   auto tile_coords = [&](int t, int& m0, int& n0, int& z) {
     z = t / (mgroups * p.nt);
     const int r = t - z * mgroups * p.nt;
@@ -313,39 +367,47 @@ __global__ void __launch_bounds__(kPThreads, 1)
         int m0, n0, z;
         tile_coords(t, m0, n0, z);
         const int kt_n = k_tiles(z);
+        const int nb0 = n0 + (int)crank * BNL;  // first B row (N) of this CTA's share
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           uint8_t* sa = smem + s * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
-          mbar_expect_tx(&full[s], S::kStageBytes);
           const int k0 = z * p.k_per_split + kt * BK;
-          if (A_MN) {
+          if (it < 32) trace_at(p.trace, 2 + it);
+          if (PAIR) {
+            // both CTAs' bytes complete on the leader's barrier (peer bit cleared)
+            const uint32_t fb = su32(&full[s]) & 0xFEFFFFFFu;
+            if (leader) mbar_expect_tx(&full[s], 2 * S::kStageBytes);
+            if (A_MN) {
 #pragma unroll
-            for (int c = 0; c < BM / O::kChunk; ++c)
-              tma_load_2d(sa + c * kChunkBytes, &tmA, &full[s], m0 + O::kChunk * c, k0);
+              for (int c = 0; c < BM / O::kChunk; ++c)
+                tma_load_2d_pair(sa + c * kChunkBytes, &tmA, fb, m0 + O::kChunk * c, k0);
+            } else {
+              tma_load_2d_pair(sa, &tmA, fb, k0, m0);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int c = 0; c < BNL / O::kChunk; ++c)
+                tma_load_2d_pair(sb + c * kChunkBytes, &tmB, fb, nb0 + O::kChunk * c, k0);
+            } else {
+              tma_load_2d_pair(sb, &tmB, fb, k0, nb0);
+            }
           } else {
-            tma_load_2d(sa, &tmA, &full[s], k0, m0);
-          }
-          if (CS == 1) {
+            mbar_expect_tx(&full[s], S::kStageBytes);
+            if (A_MN) {
+#pragma unroll
+              for (int c = 0; c < BM / O::kChunk; ++c)
+                tma_load_2d(sa + c * kChunkBytes, &tmA, &full[s], m0 + O::kChunk * c, k0);
+            } else {
+              tma_load_2d(sa, &tmA, &full[s], k0, m0);
+            }
             if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BN / O::kChunk; ++c)
                 tma_load_2d(sb + c * kChunkBytes, &tmB, &full[s], n0 + O::kChunk * c, k0);
             } else {
               tma_load_2d(sb, &tmB, &full[s], k0, n0);
-            }
-          } else {
-            // this CTA's 1/CS share of B, multicast into every CTA of the cluster
-            if (B_MN) {
-#pragma unroll
-              for (int c = (int)crank; c < BN / O::kChunk; c += CS)
-                tma_load_2d_mc(sb + c * kChunkBytes, &tmB, &full[s], n0 + O::kChunk * c, k0,
-                               kMask);
-            } else {
-              constexpr int kRowsPer = BN / CS;
-              tma_load_2d_mc(sb + crank * kRowsPer * 128, &tmB, &full[s], k0,
-                             n0 + (int)crank * kRowsPer, kMask);
             }
           }
         }
@@ -354,22 +416,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
     // instruction descriptor: f32 accum, A/B format, majors, N>>3, M>>4
+    // (M = 256 for a CTA pair)
     const uint32_t idesc = (1u << 4) | (O::kFmt << 7) | (O::kFmt << 10) |
                            ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-    if (lane == 0) {
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((CS * BM) >> 4) << 24);
+    if (lane == 0 && leader) {
       int it = 0, local = 0;
       for (int t = cl; t < ngroups; t += ncl, ++local) {
         int m0, n0, z;
         tile_coords(t, m0, n0, z);
         const int kt_n = k_tiles(z);
         const int b = local & 1;
-        mbar_wait(&acc_empty[b], ((local >> 1) & 1) ^ 1);  // epilogue drained this buffer
+        mbar_wait(&acc_empty[b], ((local >> 1) & 1) ^ 1);  // epilogues drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + (uint32_t)(b * BN);
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
+          if (it < 32) trace_at(p.trace, 34 + it);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = su32(smem + s * S::kStageBytes);
           const uint32_t b_base = a_base + S::kABytes;
@@ -385,13 +449,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const uint64_t db = B_MN ? smem_desc(b_base + kk * O::kMnKStep, kChunkBytes,
                                                  O::kMnSbo, O::kMnLayout)
                                      : smem_desc(b_base + kk * 32, 16, 1024, 2);
-            mma<TI>(acc, da, db, idesc, (kt > 0 || kk > 0) ? 1u : 0u);
+            const uint32_t accum = (kt > 0 || kk > 0) ? 1u : 0u;
+            if (PAIR) mma_pair<TI>(acc, da, db, idesc, accum);
+            else mma<TI>(acc, da, db, idesc, accum);
           }
-          // frees the stage (in every CTA of the cluster) once these MMAs read it
-          if (CS == 1) mma_commit(&empty[s]);
-          else mma_commit_mc(&empty[s], kMask);
+          // frees the stage (in both CTAs of a pair) once these MMAs read it
+          if (PAIR) mma_commit_pair(&empty[s]);
+          else mma_commit(&empty[s]);
         }
-        mma_commit(&acc_full[b]);  // accumulator b complete
+        if (PAIR) mma_commit_pair(&acc_full[b]);  // accumulator b complete (both CTAs)
+        else mma_commit(&acc_full[b]);
       }
     }
   } else {
@@ -407,9 +474,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int slice = ew >> 2;
     const int row = quarter * 32 + lane;
     constexpr int kSlice = BN / 4;
-    constexpr uint32_t kBoxBytes = 32 * 32 * sizeof(TO);
     float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
-    uint8_t* stg = smem + kStages * S::kStageBytes + ew * 4096;
+    uint8_t* stg = smem + kStages * S::kStageBytes + ew * kBoxBytes;
     uint64_t* abar = aux_bar + ew;
     uint32_t aphase = 0;
     int local = 0;
@@ -426,6 +492,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         __syncwarp();
       }
       if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
+      if (ew == 0 && lane == 0 && local < 16) trace_at(p.trace, 66 + local);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + row;
       const int crow = m0 + quarter * 32;  // row of this warp's 32-row box in C (split z)
@@ -524,23 +591,35 @@ __global__ void __launch_bounds__(kPThreads, 1)
         TO* cp = reinterpret_cast<TO*>(p.C);
         cp[(int64_t)m * p.ldc + p.ones_col] = (TO)1.f;
       }
-      // release accumulator buffer b to the MMA warp
+      if (ew == 0 && lane == 0 && local < 16) trace_at(p.trace, 82 + local);
+      // release accumulator buffer b to the (leader's) MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[b]))
-                     : "memory");
+        if (PAIR && !leader) {
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(&acc_empty[b])));
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                       : "memory");
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[b]))
+                       : "memory");
+        }
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  // no CTA may leave while a peer can still multicast into its smem or
-  // arrive on its barriers
-  if (CS > 1) cluster_sync_all();
+  // no CTA may leave (or free TMEM) while its pair can still write into its
+  // smem / TMEM or arrive on its barriers
+  if (PAIR) cluster_sync_all();
+  if (threadIdx.x == 0) trace_at(p.trace, 98);
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
   }
 }
 
@@ -595,9 +674,22 @@ int make_map(CUtensorMap* map, const void* base, int elem_bytes, int64_t inner, 
   return UL_OK;
 }
 
-template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, int CS>
-int launch(const GemmDesc& d, int splits, int kps, int ones_col,
-           cudaStream_t s) {
+// UL_TC_TRACE=1: every launch records CTA 0's event times (ul_tc_trace reads them)
+inline unsigned long long* trace_buffer() {
+  static int on = -1;
+  static unsigned long long* buf = nullptr;
+  if (on < 0) {
+    const char* e = getenv("UL_TC_TRACE");
+    on = e && atoi(e) != 0;
+    if (on && cudaMalloc(&buf, 128 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+    if (buf) cudaMemset(buf, 0, 128 * sizeof(unsigned long long));
+  }
+  return buf;
+}
+
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
+int launch(const GemmDesc& d, int splits, int kps, int ones_col, cudaStream_t s) {
+  constexpr int CS = PAIR ? 2 : 1;
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
   constexpr int eb = O::kBytes, ob = (int)sizeof(TO);
@@ -611,17 +703,18 @@ int launch(const GemmDesc& d, int splits, int kps, int ones_col,
   if (B_MN) UL_TRY(make_map(&mb, d.B, eb, d.N, d.K, d.ldb, O::kChunk, O::BK, mn_sw));
   else  // one CTA's share of the B tile
     UL_TRY(make_map(&mb, d.B, eb, d.K, d.N, d.ldb, O::BK, BN / CS, CU_TENSOR_MAP_SWIZZLE_128B));
+  using SM = Smem<BN, PAIR, ob>;
   // C (and split-K partials stacked as [splits*M, ldc]) stored by 32x32 TMA boxes
   UL_TRY(make_map(&mc, d.C, ob, d.N, d.M, d.ldc, 32, 32, out_sw, splits));
   if (EPI == kEpiEluGrad) UL_TRY(make_map(&mx, d.aux, ob, d.N, d.M, d.ldaux, 32, 32, out_sw, 1));
   else mx = mc;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
   TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, d.C, d.ldc, d.bias,
-           ones_col};
-  auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, CS>;
+           ones_col, trace_buffer()};
+  auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
-  cfg.dynamicSmemBytes = Smem<BN>::kBytes;
+  cfg.dynamicSmemBytes = SM::kBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -635,8 +728,7 @@ int launch(const GemmDesc& d, int splits, int kps, int ones_col,
   // queue a second wave behind the first)
   static int max_clusters = 0;
   if (max_clusters == 0) {
-    UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Smem<BN>::kBytes));
+    UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kBytes));
     int n = kNumSMs / CS;
     if (CS > 1) {
       cfg.gridDim = dim3((unsigned)(n * CS));
@@ -646,7 +738,7 @@ int launch(const GemmDesc& d, int splits, int kps, int ones_col,
     }
     max_clusters = n;
   }
-  // a cluster of CS CTAs works on CS M-tiles that share one B tile (multicast)
+  // a pair (cluster of 2) works on two M-tiles that share one B tile
   const int ngroups = (int)ceil_div(mt, CS) * nt * splits;
   const int grid = (ngroups < max_clusters ? ngroups : max_clusters) * CS;
   cfg.gridDim = dim3((unsigned)grid);
@@ -658,18 +750,18 @@ template <typename TI>
 int dispatch(const GemmDesc& d, int zs, int kps, int ones_col, cudaStream_t s) {
   const int bn = d.N > 128 ? 256 : 128;
   const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
-  // cluster size along M (B tile multicast to CS M-tiles).  UL_TC_CLUSTER=1
-  // disables it (experiments).
-  static int cs_cap = -1;
-  if (cs_cap < 0) {
-    const char* e = getenv("UL_TC_CLUSTER");
-    cs_cap = e ? atoi(e) : 2;
+  // CTA pairs (cta_group::2, M = 256 per UMMA) whenever there are two M
+  // tiles; UL_TC_PAIR=0 disables them (experiments).
+  static int pair_ok = -1;
+  if (pair_ok < 0) {
+    const char* e = getenv("UL_TC_PAIR");
+    pair_ok = e ? atoi(e) != 0 : 1;
   }
   const int64_t mt = ceil_div(d.M, BM);
-  const int cs = (mt >= 2 && cs_cap >= 2) ? 2 : 1;
-#define UL_TC_BN(AMN, BMN, EPI, BN)                                                     \
-  if (cs == 2) return launch<TI, AMN, BMN, EPI, BN, 2>(d, zs, kps, ones_col, s); \
-  return launch<TI, AMN, BMN, EPI, BN, 1>(d, zs, kps, ones_col, s);
+  const bool pair = pair_ok && mt >= 2;
+#define UL_TC_BN(AMN, BMN, EPI, BN)                                               \
+  if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(d, zs, kps, ones_col, s); \
+  return launch<TI, AMN, BMN, EPI, BN, false>(d, zs, kps, ones_col, s);
 #define UL_TC_CASE(AMN, BMN, EPI)                 \
   if (amn == AMN && bmn == BMN && d.epi == EPI) { \
     if (bn == 256) {                              \
@@ -728,6 +820,14 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
 }
 
 }  // namespace ul
+
+// Diagnostics: copy the last traced launch's CTA-0 timestamps (128 x u64, ns).
+extern "C" int ul_tc_trace(unsigned long long* host_out) {
+  unsigned long long* b = ul::tc::trace_buffer();
+  UL_CHECK_ARG(b != nullptr, "tc trace: set UL_TC_TRACE=1 before the first GEMM");
+  UL_CUDA(cudaMemcpy(host_out, b, 128 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return UL_OK;
+}
 
 // Test hook: one tcgen05 GEMM, same layout/epilogue codes as ul_gemm_f32.
 // dtype 0: fp32 operands (kind::tf32), 1: bf16 operands (kind::f16); with
