@@ -7,7 +7,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <utility>
 
 #include "../../include/unilite_b200.h"
 
@@ -29,6 +32,37 @@ constexpr int kNumSMs = 148;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch: kernels of the learner chain are launched
+// with programmatic stream serialization, so a dependent kernel is scheduled
+// while its predecessor drains and only its body waits (pdl_wait) for the
+// predecessor's completion.  UL_PDL=0 turns it off.
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_PDL");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
+}
+
+// Launch `kern` (which must call pdl_wait() before touching global memory
+// another kernel produces or consumes) with the PDL attribute.
+template <typename... KArgs, typename... Args>
+inline int launch_pdl(const char* what, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cuda_status(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), what);
+}
+
 }  // namespace ul
 
 #define UL_CHECK_ARG(cond, ...)            \
@@ -49,6 +83,13 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ----------------------------------------------------------------- device side
 namespace ul {
+
+// PDL: let the next kernel of the stream launch now / wait for the previous
+// kernel's completion and memory.  Both are no-ops without the attribute.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

@@ -122,6 +122,8 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t,
                                                      const int64_t* __restrict__ idx, int64_t n,
                                                      int64_t modulo, int64_t lo, int64_t hi,
                                                      int* err) {
+  pdl_trigger();
+  pdl_wait();
   const int d = blockIdx.y;
   if (d >= t.ndesc) return;
   const int upr = (int)t.units[d], sh = t.lpr_shift[d];
@@ -235,9 +237,8 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
   }
   int64_t blocks = ceil_div(max_units, 8);  // max_units: most warps any desc wants
   blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
-  gather_kernel<<<dim3((unsigned)blocks, ndesc), 256, 0, stream>>>(t, idx, n, modulo, lo, hi,
-                                                                    err);
-  return check_launch("gather_kernel");
+  return launch_pdl("gather_kernel", gather_kernel, dim3((unsigned)blocks, ndesc), dim3(256), 0,
+                    stream, t, idx, n, modulo, lo, hi, err);
 }
 }  // namespace ul
 

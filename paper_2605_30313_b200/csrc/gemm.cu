@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(256) reduce_splits_kernel(const float* __restr
   __shared__ float sm[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = (int64_t)blockIdx.x * 32 + lane;
+  pdl_trigger();
+  pdl_wait();
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   if (j < len) {
     int z = w;
@@ -245,8 +247,8 @@ int reduce_splits(const float* ws, int splits, int64_t len, float* out, int64_t 
                   int64_t row_len, cudaStream_t s) {
   if (len == 0) return UL_OK;
   const unsigned blocks = (unsigned)ceil_div(len, 32);
-  reduce_splits_kernel<<<blocks, 256, 0, s>>>(ws, splits, len, out, ld_rows, row_len);
-  return check_launch("reduce_splits_kernel");
+  return launch_pdl("reduce_splits_kernel", reduce_splits_kernel, dim3(blocks), dim3(256), 0, s,
+                    ws, splits, len, out, ld_rows, row_len);
 }
 
 }  // namespace ul

@@ -270,11 +270,17 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
 // CTAs' TMA loads complete on the leader's full barrier; the leader's commits
 // are multicast to both CTAs' empty / accumulator barriers; both epilogues
 // drain their own TMEM lanes and release the accumulator on the leader.
+// Up to two independent problems (the actor's and the critic's layer) share
+// one launch: tile groups [0, ng0) belong to problem 0, the rest to problem 1.
+struct TcMaps {
+  CUtensorMap a, b, c, x;
+};
+
 template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
 __global__ void __launch_bounds__(kPThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
-                   TcArgs p) {
+    tc_gemm_kernel(const __grid_constant__ TcMaps m0_, const __grid_constant__ TcMaps m1_,
+                   const __grid_constant__ TcArgs p0_, const __grid_constant__ TcArgs p1_,
+                   int ng0, int ngroups) {
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
   using S = Smem<BN, PAIR, (int)sizeof(TO)>;
@@ -299,13 +305,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) trace_at(p.trace, 0);
+  pdl_trigger();
+  if (threadIdx.x == 0) trace_at(p0_.trace, 0);
 
   uint32_t crank = 0;
   if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   const bool leader = crank == 0;
-  const int mgroups = (p.mt + CS - 1) / CS;
-  const int ngroups = mgroups * p.nt * p.zt;
   const int cl = blockIdx.x / CS, ncl = gridDim.x / CS;
 
   if (threadIdx.x == 0) {
@@ -322,8 +327,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&m0_.a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&m0_.b) : "memory");
+    if (ngroups > ng0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&m1_.a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&m1_.b) : "memory");
+    }
   }
   if (warp == 1) {
     if (PAIR) {
@@ -343,20 +352,28 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (PAIR) cluster_sync_all();  // peer barriers initialised before any cross-CTA signal
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) trace_at(p.trace, 1);
+  pdl_wait();  // setup above overlapped the previous kernel's tail
+  if (threadIdx.x == 0) trace_at(p0_.trace, 1);
 
-  // group t -> (M-tile group, N-tile, split); this CTA takes M-tile
+  // group t -> (problem, M-tile group, N-tile, split); this CTA takes M-tile
   // group*CS + rank
-  auto tile_coords = [&](int t, int& m0, int& n0, int& z) {
-    z = t / (mgroups * p.nt);
-    const int r = t - z * mgroups * p.nt;
-    n0 = (r / mgroups) * BN;
-    m0 = ((r % mgroups) * CS + (int)crank) * BM;
+  struct Tile {
+    int pr, m0, n0, z, kt_n;
   };
-  auto k_tiles = [&](int z) {
-    const int kb = z * p.k_per_split;
-    const int ke = min(p.K, kb + p.k_per_split);
-    return ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  auto tile_of = [&](int t) {
+    Tile T;
+    T.pr = t < ng0 ? 0 : 1;
+    const TcArgs& P = T.pr ? p1_ : p0_;
+    const int tl = T.pr ? t - ng0 : t;
+    const int mg = (P.mt + CS - 1) / CS;
+    T.z = tl / (mg * P.nt);
+    const int r = tl - T.z * mg * P.nt;
+    T.n0 = (r / mg) * BN;
+    T.m0 = ((r % mg) * CS + (int)crank) * BM;
+    const int kb = T.z * P.k_per_split;
+    const int ke = min(P.K, kb + P.k_per_split);
+    T.kt_n = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+    return T;
   };
 
   if (warp == 0) {
@@ -364,17 +381,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int t = cl; t < ngroups; t += ncl) {
-        int m0, n0, z;
-        tile_coords(t, m0, n0, z);
-        const int kt_n = k_tiles(z);
+        const Tile T = tile_of(t);
+        const int m0 = T.m0, n0 = T.n0, kt_n = T.kt_n;
+        const TcArgs& P = T.pr ? p1_ : p0_;
+        const CUtensorMap* tA = T.pr ? &m1_.a : &m0_.a;
+        const CUtensorMap* tB = T.pr ? &m1_.b : &m0_.b;
         const int nb0 = n0 + (int)crank * BNL;  // first B row (N) of this CTA's share
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
           uint8_t* sa = smem + s * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
-          const int k0 = z * p.k_per_split + kt * BK;
-          if (it < 32) trace_at(p.trace, 2 + it);
+          const int k0 = T.z * P.k_per_split + kt * BK;
+          if (it < 32) trace_at(p0_.trace, 2 + it);
           if (PAIR) {
             // both CTAs' bytes complete on the leader's barrier (peer bit cleared)
             const uint32_t fb = su32(&full[s]) & 0xFEFFFFFFu;
@@ -382,32 +401,32 @@ __global__ void __launch_bounds__(kPThreads, 1)
             if (A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / O::kChunk; ++c)
-                tma_load_2d_pair(sa + c * kChunkBytes, &tmA, fb, m0 + O::kChunk * c, k0);
+                tma_load_2d_pair(sa + c * kChunkBytes, tA, fb, m0 + O::kChunk * c, k0);
             } else {
-              tma_load_2d_pair(sa, &tmA, fb, k0, m0);
+              tma_load_2d_pair(sa, tA, fb, k0, m0);
             }
             if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BNL / O::kChunk; ++c)
-                tma_load_2d_pair(sb + c * kChunkBytes, &tmB, fb, nb0 + O::kChunk * c, k0);
+                tma_load_2d_pair(sb + c * kChunkBytes, tB, fb, nb0 + O::kChunk * c, k0);
             } else {
-              tma_load_2d_pair(sb, &tmB, fb, k0, nb0);
+              tma_load_2d_pair(sb, tB, fb, k0, nb0);
             }
           } else {
             mbar_expect_tx(&full[s], S::kStageBytes);
             if (A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / O::kChunk; ++c)
-                tma_load_2d(sa + c * kChunkBytes, &tmA, &full[s], m0 + O::kChunk * c, k0);
+                tma_load_2d(sa + c * kChunkBytes, tA, &full[s], m0 + O::kChunk * c, k0);
             } else {
-              tma_load_2d(sa, &tmA, &full[s], k0, m0);
+              tma_load_2d(sa, tA, &full[s], k0, m0);
             }
             if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BN / O::kChunk; ++c)
-                tma_load_2d(sb + c * kChunkBytes, &tmB, &full[s], n0 + O::kChunk * c, k0);
+                tma_load_2d(sb + c * kChunkBytes, tB, &full[s], n0 + O::kChunk * c, k0);
             } else {
-              tma_load_2d(sb, &tmB, &full[s], k0, n0);
+              tma_load_2d(sb, tB, &full[s], k0, n0);
             }
           }
         }
@@ -423,9 +442,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (lane == 0 && leader) {
       int it = 0, local = 0;
       for (int t = cl; t < ngroups; t += ncl, ++local) {
-        int m0, n0, z;
-        tile_coords(t, m0, n0, z);
-        const int kt_n = k_tiles(z);
+        const int kt_n = tile_of(t).kt_n;
         const int b = local & 1;
         mbar_wait(&acc_empty[b], ((local >> 1) & 1) ^ 1);  // epilogues drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -433,7 +450,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
-          if (it < 32) trace_at(p.trace, 34 + it);
+          if (it < 32) trace_at(p0_.trace, 34 + it);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = su32(smem + s * S::kStageBytes);
           const uint32_t b_base = a_base + S::kABytes;
@@ -480,10 +497,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint32_t aphase = 0;
     int local = 0;
     for (int t = cl; t < ngroups; t += ncl, ++local) {
-      int m0, n0, z;
-      tile_coords(t, m0, n0, z);
+      const Tile T = tile_of(t);
+      const int m0 = T.m0, n0 = T.n0, z = T.z;
+      const TcArgs& p = T.pr ? p1_ : p0_;
+      const CUtensorMap* tC = T.pr ? &m1_.c : &m0_.c;
+      const CUtensorMap* tX = T.pr ? &m1_.x : &m0_.x;
       const int b = local & 1;
-      const bool have = k_tiles(z) > 0;
+      const bool have = T.kt_n > 0;
       if (EPI == kEpiBias || EPI == kEpiBiasElu) {
         for (int c = lane; c < kSlice; c += 32) {
           const int n = n0 + slice * kSlice + c;
@@ -492,7 +512,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         __syncwarp();
       }
       if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
-      if (ew == 0 && lane == 0 && local < 16) trace_at(p.trace, 66 + local);
+      if (ew == 0 && lane == 0 && local < 16) trace_at(p0_.trace, 66 + local);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + row;
       const int crow = m0 + quarter * 32;  // row of this warp's 32-row box in C (split z)
@@ -505,7 +525,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (EPI == kEpiEluGrad) {
           if (lane == 0) {
             mbar_expect_tx(abar, kBoxBytes);
-            tma_load_3d(stg, &tmX, abar, n0 + c0, m0 + quarter * 32, 0);
+            tma_load_3d(stg, tX, abar, n0 + c0, m0 + quarter * 32, 0);
           }
         }
         float v[32];
@@ -581,7 +601,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           // 3-D map [splits][M][N]: a box never spills into the next split's rows
           asm volatile(
               "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                  &tmC),
+                  tC),
               "r"(su32(stg)), "r"(n0 + c0), "r"(crow), "r"(z)
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -591,7 +611,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         TO* cp = reinterpret_cast<TO*>(p.C);
         cp[(int64_t)m * p.ldc + p.ones_col] = (TO)1.f;
       }
-      if (ew == 0 && lane == 0 && local < 16) trace_at(p.trace, 82 + local);
+      if (ew == 0 && lane == 0 && local < 16) trace_at(p0_.trace, 82 + local);
       // release accumulator buffer b to the (leader's) MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -614,7 +634,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // no CTA may leave (or free TMEM) while its pair can still write into its
   // smem / TMEM or arrive on its barriers
   if (PAIR) cluster_sync_all();
-  if (threadIdx.x == 0) trace_at(p.trace, 98);
+  if (threadIdx.x == 0) trace_at(p0_.trace, 98);
   if (warp == 1) {
     if (PAIR)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
@@ -687,42 +707,67 @@ inline unsigned long long* trace_buffer() {
   return buf;
 }
 
+// one problem's tensor maps + kernel arguments (Prob: M/N/K split already fixed)
+struct Prob {
+  const GemmDesc* d;
+  int zs, kps, ones_col;
+};
+
 template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
-int launch(const GemmDesc& d, int splits, int kps, int ones_col, cudaStream_t s) {
-  constexpr int CS = PAIR ? 2 : 1;
+int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
+  constexpr int CS = PAIR ? 2 : 1;
   constexpr int eb = O::kBytes, ob = (int)sizeof(TO);
+  const GemmDesc& d = *q.d;
   const CUtensorMapSwizzle mn_sw =
       eb == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   const CUtensorMapSwizzle out_sw = ob == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  CUtensorMap ma, mb, mc, mx;
   // A(m,k): K-major -> rows=M, inner=K ; MN-major -> rows=K, inner=M
-  if (A_MN) UL_TRY(make_map(&ma, d.A, eb, d.M, d.K, d.lda, O::kChunk, O::BK, mn_sw));
-  else UL_TRY(make_map(&ma, d.A, eb, d.K, d.M, d.lda, O::BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
-  if (B_MN) UL_TRY(make_map(&mb, d.B, eb, d.N, d.K, d.ldb, O::kChunk, O::BK, mn_sw));
+  if (A_MN) UL_TRY(make_map(&m->a, d.A, eb, d.M, d.K, d.lda, O::kChunk, O::BK, mn_sw));
+  else UL_TRY(make_map(&m->a, d.A, eb, d.K, d.M, d.lda, O::BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
+  if (B_MN) UL_TRY(make_map(&m->b, d.B, eb, d.N, d.K, d.ldb, O::kChunk, O::BK, mn_sw));
   else  // one CTA's share of the B tile
-    UL_TRY(make_map(&mb, d.B, eb, d.K, d.N, d.ldb, O::BK, BN / CS, CU_TENSOR_MAP_SWIZZLE_128B));
-  using SM = Smem<BN, PAIR, ob>;
-  // C (and split-K partials stacked as [splits*M, ldc]) stored by 32x32 TMA boxes
-  UL_TRY(make_map(&mc, d.C, ob, d.N, d.M, d.ldc, 32, 32, out_sw, splits));
-  if (EPI == kEpiEluGrad) UL_TRY(make_map(&mx, d.aux, ob, d.N, d.M, d.ldaux, 32, 32, out_sw, 1));
-  else mx = mc;
+    UL_TRY(make_map(&m->b, d.B, eb, d.K, d.N, d.ldb, O::BK, BN / CS, CU_TENSOR_MAP_SWIZZLE_128B));
+  // C (and split-K partials [splits][M][ldc]) stored by 32x32 TMA boxes
+  UL_TRY(make_map(&m->c, d.C, ob, d.N, d.M, d.ldc, 32, 32, out_sw, q.zs));
+  if (EPI == kEpiEluGrad) UL_TRY(make_map(&m->x, d.aux, ob, d.N, d.M, d.ldaux, 32, 32, out_sw, 1));
+  else m->x = m->c;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
-  TcArgs a{(int)d.M, (int)d.N, (int)d.K, kps, mt, nt, splits, d.C, d.ldc, d.bias,
-           ones_col, trace_buffer()};
+  *a = TcArgs{(int)d.M, (int)d.N, (int)d.K, q.kps, mt, nt, q.zs, d.C, d.ldc, d.bias,
+              q.ones_col, trace_buffer()};
+  *ngroups = (int)ceil_div(mt, CS) * nt * q.zs;
+  return UL_OK;
+}
+
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
+int launch(const Prob* q, int np, cudaStream_t s) {
+  using TO = OutT<TI, EPI>;
+  using SM = Smem<BN, PAIR, (int)sizeof(TO)>;
+  constexpr int CS = PAIR ? 2 : 1;
+  TcMaps m[2];
+  TcArgs a[2];
+  int ng[2] = {0, 0};
+  for (int i = 0; i < np; ++i)
+    UL_TRY((make_problem<TI, A_MN, B_MN, EPI, BN, PAIR>(q[i], &m[i], &a[i], &ng[i])));
+  if (np == 1) {
+    m[1] = m[0];
+    a[1] = a[0];
+  }
   auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
   cfg.dynamicSmemBytes = SM::kBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   // persistent: as many clusters as can be co-resident (one CTA per SM; GPC
   // sizes may leave SMs idle for CS > 1, so ask the occupancy API rather than
   // queue a second wave behind the first)
@@ -732,23 +777,26 @@ int launch(const GemmDesc& d, int splits, int kps, int ones_col, cudaStream_t s)
     int n = kNumSMs / CS;
     if (CS > 1) {
       cfg.gridDim = dim3((unsigned)(n * CS));
-      int q = 0;
-      if (cudaOccupancyMaxActiveClusters(&q, kern, &cfg) == cudaSuccess && q > 0 && q < n) n = q;
+      int qn = 0;
+      if (cudaOccupancyMaxActiveClusters(&qn, kern, &cfg) == cudaSuccess && qn > 0 && qn < n)
+        n = qn;
       cudaGetLastError();
     }
     max_clusters = n;
   }
-  // a pair (cluster of 2) works on two M-tiles that share one B tile
-  const int ngroups = (int)ceil_div(mt, CS) * nt * splits;
-  const int grid = (ngroups < max_clusters ? ngroups : max_clusters) * CS;
+  const int total = ng[0] + ng[1];
+  const int grid = (total < max_clusters ? total : max_clusters) * CS;
   cfg.gridDim = dim3((unsigned)grid);
-  UL_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, a));
+  UL_CUDA(cudaLaunchKernelEx(&cfg, kern, m[0], m[1], a[0], a[1], ng[0], total));
   return check_launch("tc_gemm_kernel");
 }
 
+inline int bn_of(const GemmDesc& d) { return d.N > 128 ? 256 : 128; }
+
 template <typename TI>
-int dispatch(const GemmDesc& d, int zs, int kps, int ones_col, cudaStream_t s) {
-  const int bn = d.N > 128 ? 256 : 128;
+int dispatch(const Prob* q, int np, cudaStream_t s) {
+  const GemmDesc& d = *q[0].d;
+  const int bn = bn_of(d);
   const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
   // CTA pairs (cta_group::2, M = 256 per UMMA) whenever there are two M
   // tiles; UL_TC_PAIR=0 disables them (experiments).
@@ -757,11 +805,10 @@ int dispatch(const GemmDesc& d, int zs, int kps, int ones_col, cudaStream_t s) {
     const char* e = getenv("UL_TC_PAIR");
     pair_ok = e ? atoi(e) != 0 : 1;
   }
-  const int64_t mt = ceil_div(d.M, BM);
-  const bool pair = pair_ok && mt >= 2;
-#define UL_TC_BN(AMN, BMN, EPI, BN)                                               \
-  if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(d, zs, kps, ones_col, s); \
-  return launch<TI, AMN, BMN, EPI, BN, false>(d, zs, kps, ones_col, s);
+  const bool pair = pair_ok && ceil_div(d.M, BM) >= 2;
+#define UL_TC_BN(AMN, BMN, EPI, BN)                                        \
+  if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(q, np, s); \
+  return launch<TI, AMN, BMN, EPI, BN, false>(q, np, s);
 #define UL_TC_CASE(AMN, BMN, EPI)                 \
   if (amn == AMN && bmn == BMN && d.epi == EPI) { \
     if (bn == 256) {                              \
@@ -806,17 +853,47 @@ int tc_num_splits(int64_t K, int splits, int dtype) {
   return (int)ceil_div(K > 0 ? K : 1, kps);
 }
 
+static tc::Prob prob_of(const GemmDesc& d, int ones_col) {
+  const int bk = tc_bk(d.dtype);
+  const int splits = d.splits < 1 ? 1 : d.splits;
+  tc::Prob q;
+  q.d = &d;
+  q.kps = (int)(ceil_div(ceil_div(d.K, splits), bk) * bk);
+  q.zs = (int)ceil_div(d.K > 0 ? d.K : 1, q.kps);
+  q.ones_col = ones_col < 0 ? d.ones_col : ones_col;
+  return q;
+}
+
 // Same contract as gemm_f32 (split partials [zs][M][ldc] at C when splits >
 // 1); `ones_col` >= 0 additionally writes 1.0 into that column.
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   if (d.M == 0 || d.N == 0) return UL_OK;
-  if (ones_col < 0) ones_col = d.ones_col;
-  const int bk = tc_bk(d.dtype);
-  const int splits = d.splits < 1 ? 1 : d.splits;
-  const int kps = (int)(ceil_div(ceil_div(d.K, splits), bk) * bk);
-  const int zs = (int)ceil_div(d.K > 0 ? d.K : 1, kps);
-  if (d.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(d, zs, kps, ones_col, s);
-  return tc::dispatch<float>(d, zs, kps, ones_col, s);
+  const tc::Prob q = prob_of(d, ones_col);
+  if (d.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(&q, 1, s);
+  return tc::dispatch<float>(&q, 1, s);
+}
+
+// Two independent GEMMs (e.g. the actor's and the critic's layer) in one
+// persistent launch when they share dtype, layouts, epilogue, tile width and
+// CTA pairing; otherwise two launches.  Each desc's ones_col applies.
+int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
+  const bool e0 = d0.M == 0 || d0.N == 0, e1 = d1.M == 0 || d1.N == 0;
+  if (e0 || e1) {
+    if (!e0) UL_TRY(gemm_tc(d0, -1, s));
+    if (!e1) UL_TRY(gemm_tc(d1, -1, s));
+    return UL_OK;
+  }
+  const bool same = d0.dtype == d1.dtype && d0.a_kmajor == d1.a_kmajor &&
+                    d0.b_kmajor == d1.b_kmajor && d0.epi == d1.epi &&
+                    tc::bn_of(d0) == tc::bn_of(d1) &&
+                    (ceil_div(d0.M, tc::BM) >= 2) == (ceil_div(d1.M, tc::BM) >= 2);
+  if (!same) {
+    UL_TRY(gemm_tc(d0, -1, s));
+    return gemm_tc(d1, -1, s);
+  }
+  const tc::Prob q[2] = {prob_of(d0, -1), prob_of(d1, -1)};
+  if (d0.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(q, 2, s);
+  return tc::dispatch<float>(q, 2, s);
 }
 
 }  // namespace ul

@@ -27,6 +27,8 @@ __global__ void __launch_bounds__(kHeadThr) ppo_head_kernel(PpoHeadArgs a) {
   __shared__ double s_lsum;
   const int A = a.A, nq = 3 + A;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  pdl_trigger();
+  pdl_wait();
   // per-dimension constants once per block: log_std and 1/std
   for (int j = threadIdx.x; j < A; j += blockDim.x) {
     const double ls = (double)a.log_std[j];
@@ -173,6 +175,8 @@ __global__ void __launch_bounds__(256) adv_stats_kernel(const float* __restrict_
 __global__ void ppo_loss_finalize_kernel(const float* __restrict__ loss, const float* __restrict__ log_std,
                                          int A, double n, double vcoef, double ecoef,
                                          int last_in_epoch, ul_opt_ctl* ctl, ul_ppo_stats* st) {
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x != 0) return;
   const double pol = -(double)loss[0] / n;
   const double val = (double)loss[1] / n;
@@ -210,8 +214,7 @@ __global__ void gauss_logp_kernel(const float* __restrict__ mean, int64_t ldm,
 
 int launch_ppo_head(const PpoHeadArgs& a, cudaStream_t s) {
   const unsigned blocks = (unsigned)ceil_div(a.n_local > 0 ? a.n_local : 1, kHeadThr);
-  ppo_head_kernel<<<blocks, kHeadThr, 0, s>>>(a);
-  return check_launch("ppo_head_kernel");
+  return launch_pdl("ppo_head_kernel", ppo_head_kernel, dim3(blocks), dim3(kHeadThr), 0, s, a);
 }
 
 int ppo_head_partial_doubles(int64_t n_local, int A) {
@@ -229,9 +232,8 @@ int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ti
 int launch_ppo_loss_finalize(const float* loss, const float* log_std, int A, double n,
                              double vcoef, double ecoef, int last_in_epoch, ul_opt_ctl* ctl,
                              ul_ppo_stats* st, cudaStream_t s) {
-  ppo_loss_finalize_kernel<<<1, 32, 0, s>>>(loss, log_std, A, n, vcoef, ecoef, last_in_epoch, ctl,
-                                            st);
-  return check_launch("ppo_loss_finalize_kernel");
+  return launch_pdl("ppo_loss_finalize_kernel", ppo_loss_finalize_kernel, dim3(1), dim3(32), 0, s,
+                    loss, log_std, A, n, vcoef, ecoef, last_in_epoch, ctl, st);
 }
 
 }  // namespace ul

@@ -97,6 +97,33 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
 int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
                 const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
                 cudaStream_t s);
+// One network's operands for a (possibly paired) MLP pass: forward uses
+// x/acts/out, backward additionally dout..work.
+struct MlpNet {
+  const NetView* v;
+  const float* params;
+  const float* wp;  // staged weights (tensor-core back ends), else null
+  const float* x;
+  int64_t ldx;
+  bool x_has_ones;
+  float* acts;
+  float* out;
+  int64_t ld_out;
+  const float* dout;
+  int64_t ld_dout;
+  float* grads;
+  float* dx;
+  int64_t lddx;
+  int dx_col0, dx_ncols;
+  bool want_dw, zero_logstd;
+  float* work;
+};
+// n = 1 or 2 networks in lockstep (grouped tensor-core launches on s; network
+// 1's small kernels on `side` between fork/join events when side != null)
+int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
+                  cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
+int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
+                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 // dx_cols: compute dX only for input columns [dx_col0, dx_col0 + dx_ncols) (SAC dQ/da);
 // want_dw = false skips dW/db (pure input-gradient pass).  x_has_ones: column
 // dims[0] of x holds 1.0 (lets the tensor-core dW of layer 0 produce db).

@@ -152,22 +152,6 @@ void free_plan(PpoPlan* p) {
   if (p->ev_join) cudaEventDestroy(p->ev_join);
 }
 
-// The actor and critic branches of a step are independent until the PPO head
-// (forward) and again until the optimizer (backward): the critic runs on a
-// side stream forked from / joined back into `s` (captured as parallel graph
-// branches), so the many sub-wave kernels of the two networks overlap.
-int fork(PpoPlan* p, cudaStream_t s) {
-  UL_CUDA(cudaEventRecord(p->ev_fork, s));
-  UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
-  return UL_OK;
-}
-
-int join(PpoPlan* p, cudaStream_t s) {
-  UL_CUDA(cudaEventRecord(p->ev_join, p->side));
-  UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-  return UL_OK;
-}
-
 // device part of begin: stats reset + advantage statistics (graph-capturable)
 int begin_device(PpoPlan* p, cudaStream_t s) {
   UL_CUDA(cudaMemsetAsync(p->st_d, 0, sizeof(ul_ppo_stats), s));
@@ -210,17 +194,46 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   const int cvt[7] = {bf ? 1 : 0, bf ? 1 : 0, 0, 0, 0, 0, 0};
   UL_TRY(gather_rows(7, src, dst, sst, dstr, rb, ones, cvt, idx, ml, 0, 0, p->rows, nullptr, s));
   mark(p, 1, s);
-  // K7 forwards, actor on s and critic on the side stream.  Weights changed at
-  // the previous Adam step: the tensor-core path restages 16 B-row copies.
+  // K7 forwards of both networks in lockstep: one grouped tensor-core launch
+  // per layer, the critic's small kernels on the side stream.  Weights
+  // changed at the previous Adam step: the tensor-core path restages them.
   const int be = p->d.gemm_backend;
-  UL_TRY(fork(p, s));
-  if (tc) UL_TRY(stage_weights_dt(p->vc, b.critic_params, p->wst_c, p->dt, p->side));
-  UL_TRY(mlp_forward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, ml, p->acts_c,
-                     p->out_c, 1, p->side));
-  if (tc) UL_TRY(stage_weights_dt(p->va, b.actor_params, p->wst_a, p->dt, s));
-  UL_TRY(mlp_forward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, ml, p->acts_a,
-                     p->out_a, p->A, s));
-  UL_TRY(join(p, s));
+  if (tc) {
+    UL_TRY(stage_weights_dt(p->va, b.actor_params, p->wst_a, p->dt, s));
+    UL_TRY(stage_weights_dt(p->vc, b.critic_params, p->wst_c, p->dt, s));
+  }
+  MlpNet nets[2] = {};
+  nets[0].v = &p->va;
+  nets[0].params = b.actor_params;
+  nets[0].wp = tc ? p->wst_a : nullptr;
+  nets[0].x = p->mb_obs;
+  nets[0].ldx = p->ld_mo;
+  nets[0].x_has_ones = ones_o;
+  nets[0].acts = p->acts_a;
+  nets[0].out = p->out_a;
+  nets[0].ld_out = p->A;
+  nets[0].dout = p->dmean;
+  nets[0].ld_dout = p->A;
+  nets[0].grads = p->red;
+  nets[0].want_dw = true;
+  nets[0].zero_logstd = false;  // the head writes the actor's log_std gradient
+  nets[0].work = p->work;
+  nets[1].v = &p->vc;
+  nets[1].params = b.critic_params;
+  nets[1].wp = tc ? p->wst_c : nullptr;
+  nets[1].x = p->mb_cobs;
+  nets[1].ldx = p->ld_mc;
+  nets[1].x_has_ones = ones_c;
+  nets[1].acts = p->acts_c;
+  nets[1].out = p->out_c;
+  nets[1].ld_out = 1;
+  nets[1].dout = p->dv;
+  nets[1].ld_dout = 1;
+  nets[1].grads = p->red + p->Pa;
+  nets[1].want_dw = true;
+  nets[1].zero_logstd = true;  // critic log_std never receives a gradient
+  nets[1].work = p->work_c;
+  UL_TRY(mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join));
   mark(p, 0, s);
   // K9 head
   PpoHeadArgs h{};
@@ -252,15 +265,8 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   h.ent_coef_add = p->d.rank == 0 ? -p->d.entropy_coef : 0.0;
   UL_TRY(launch_ppo_head(h, s));
   mark(p, 2, s);
-  // K8 backwards into the contiguous all-reduce buffer (critic on the side stream)
-  UL_TRY(fork(p, s));
-  UL_TRY(mlp_backward(p->vc, b.critic_params, p->wst_c, be, p->mb_cobs, p->ld_mc, ones_c,
-                      ml, p->acts_c, p->dv, 1, p->red + p->Pa, nullptr, 0, 0, 0, true, true,
-                      p->work_c, p->side));
-  UL_TRY(mlp_backward(p->va, b.actor_params, p->wst_a, be, p->mb_obs, p->ld_mo, ones_o, ml,
-                      p->acts_a, p->dmean, p->A, p->red, nullptr, 0, 0, 0, true, false, p->work,
-                      s));
-  UL_TRY(join(p, s));
+  // K8 backwards of both networks into the contiguous all-reduce buffer
+  UL_TRY(mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join));
   mark(p, 0, s);
   return UL_OK;
 }

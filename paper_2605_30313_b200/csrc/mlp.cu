@@ -18,6 +18,7 @@
 namespace ul {
 
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
+int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s);
 bool tc_eligible(const GemmDesc& d);
 int tc_num_splits(int64_t K, int splits, int dtype);
 bool skinny_ok(int N, int K);
@@ -36,12 +37,29 @@ int64_t rup(int64_t x, int64_t m) { return ceil_div(x, m) * m; }
 // bias gradient, columns > in are TMA-row padding.  A warp owns 128 columns
 // (float4 lanes) and the splits z = w, w + 8, ... with every load issued
 // before the adds; the 8 warps combine in fixed order (deterministic).
-__global__ void __launch_bounds__(256) reduce_dw_kernel(const float* __restrict__ ws, int splits,
-                                                        int64_t out, int64_t in, int64_t ldp,
-                                                        float* __restrict__ gw,
-                                                        float* __restrict__ gb) {
+struct DwReduce {
+  const float* ws;
+  int splits;
+  int64_t out, in, ldp;
+  float* gw;
+  float* gb;
+};
+struct DwTable {
+  DwReduce r[2];  // blockIdx.y selects the network
+};
+
+__global__ void __launch_bounds__(256) reduce_dw_kernel(DwTable tab) {
   __shared__ float4 sm[8][32];
-  const int64_t len = out * ldp;
+  const DwReduce& q = tab.r[blockIdx.y];
+  const float* __restrict__ ws = q.ws;
+  const int splits = q.splits;
+  const int64_t in = q.in, ldp = q.ldp;
+  float* __restrict__ gw = q.gw;
+  float* __restrict__ gb = q.gb;
+  const int64_t len = q.out * ldp;
+  pdl_trigger();
+  pdl_wait();
+  if ((int64_t)blockIdx.x * 128 >= len) return;  // block-uniform
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -121,6 +139,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
   const int64_t c = ((int64_t)blockIdx.x * 32 + lane) * 8;  // first of 8 columns
   const int64_t r0 = (int64_t)blockIdx.y * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
+  pdl_trigger();
+  pdl_wait();
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   if (c < N && c + 8 > ld) {
     // row tail narrower than 8 columns of pitch: scalar loads
@@ -179,6 +199,8 @@ struct StageTable {
 template <typename T>
 __global__ void stage_weights_kernel(const float* __restrict__ params, StageTable t,
                                      T* __restrict__ wp) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < t.total; j += stride) {
     int l = 0;
@@ -285,11 +307,11 @@ int stage_weights_dt(const NetView& v, const float* params, void* wp, int dtype,
   int64_t blocks = ceil_div(t.total, 256);
   blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
   if (dtype == kBf16)
-    stage_weights_kernel<<<(unsigned)blocks, 256, 0, s>>>(params, t,
-                                                          reinterpret_cast<__nv_bfloat16*>(wp));
-  else
-    stage_weights_kernel<<<(unsigned)blocks, 256, 0, s>>>(params, t, reinterpret_cast<float*>(wp));
-  return check_launch("stage_weights_kernel");
+    return launch_pdl("stage_weights_kernel", stage_weights_kernel<__nv_bfloat16>,
+                      dim3((unsigned)blocks), dim3(256), 0, s, params, t,
+                      reinterpret_cast<__nv_bfloat16*>(wp));
+  return launch_pdl("stage_weights_kernel", stage_weights_kernel<float>, dim3((unsigned)blocks),
+                    dim3(256), 0, s, params, t, reinterpret_cast<float*>(wp));
 }
 
 int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t s) {
@@ -319,47 +341,356 @@ static bool al16(const void* p, int64_t ld, int eb) {
   return ((uintptr_t)p & 15) == 0 && (ld * eb) % 16 == 0;
 }
 
+// ---------------------------------------------------------------- drivers
+// One or two networks advance layer by layer in lockstep: their tensor-core
+// GEMMs of a layer share one grouped launch (gemm_tc_group), the per-network
+// small kernels (skinny heads, split-K reductions, column sums) of network 1
+// run on the side lane.
+namespace {
+
+struct Lanes {
+  cudaStream_t s, side;
+  cudaEvent_t fork, join;
+  cudaStream_t of(int k) const { return k == 1 && side ? side : s; }
+  int open() const {
+    if (!side) return UL_OK;
+    UL_CUDA(cudaEventRecord(fork, s));
+    UL_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    return UL_OK;
+  }
+  int close() const {
+    if (!side) return UL_OK;
+    UL_CUDA(cudaEventRecord(join, side));
+    UL_CUDA(cudaStreamWaitEvent(s, join, 0));
+    return UL_OK;
+  }
+};
+
+// run 1 or 2 independent GEMMs; tensor-core pairs share a launch
+int run_gemms(GemmDesc* g, const bool* has, const bool* use_tc, const int* ones, cudaStream_t s) {
+  bool tc_ok[2];
+  for (int k = 0; k < 2; ++k) {
+    g[k].ones_col = ones[k];
+    tc_ok[k] = has[k] && use_tc[k] && tc_eligible(g[k]);
+  }
+  if (tc_ok[0] && tc_ok[1]) return gemm_tc_group(g[0], g[1], s);
+  for (int k = 0; k < 2; ++k)
+    if (has[k]) UL_TRY(run_gemm(g[k], use_tc[k], ones[k], s));
+  return UL_OK;
+}
+
+bool ones_free_of(int64_t n_in, bool ones) {
+  auto bn_of = [](int64_t n) { return n > 128 ? 256 : 128; };
+  return ones && bn_of(n_in + 1) == bn_of(n_in) &&
+         ceil_div(n_in + 1, bn_of(n_in + 1)) == ceil_div(n_in, bn_of(n_in));
+}
+
+}  // namespace
+
+int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
+                  cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+  if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
+    UL_TRY(mlp_forward_n(nets, 1, backend, M, s, nullptr, nullptr, nullptr));
+    return mlp_forward_n(nets + 1, 1, backend, M, s, nullptr, nullptr, nullptr);
+  }
+  const Lanes L{s, n == 2 ? side : nullptr, fork, join};
+  const int dt = backend_dtype(backend);
+  const int eb = dt == kBf16 ? 2 : 4;
+  const bool tc = backend >= 1;
+  const float* h[2];
+  int64_t ldh[2];
+  for (int k = 0; k < n; ++k) {
+    UL_CHECK_ARG(dt == kF32 || nets[k].wp, "bf16 MLP needs staged weights");
+    h[k] = nets[k].x;
+    ldh[k] = nets[k].ldx;
+  }
+  const int nl = nets[0].v->n_layers;
+  for (int i = 0; i < nl; ++i) {
+    const bool last = i == nl - 1;
+    GemmDesc g[2] = {};
+    bool has[2] = {false, false}, use[2] = {false, false}, skinny[2] = {false, false};
+    int ones[2] = {-1, -1};
+    for (int k = 0; k < n; ++k) {
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      float* dst = last ? N.out : const_cast<float*>(act_ptr(v, N.acts, M, i, dt));
+      const int64_t lddst = last ? N.ld_out : act_ld(v.dims[i + 1], dt);
+      if (last && skinny_ok(v.dims[i + 1], v.dims[i]) && al16(h[k], ldh[k], eb)) {
+        skinny[k] = true;  // 12-/1-wide head, launched below
+        continue;
+      }
+      GemmDesc& G = g[k];
+      G.M = M; G.N = v.dims[i + 1]; G.K = v.dims[i];
+      G.A = h[k]; G.lda = ldh[k];
+      G.bias = N.params + v.b_off[i];
+      G.a_kmajor = true; G.b_kmajor = true;
+      G.epi = last ? kEpiBias : kEpiBiasElu;
+      G.splits = 1;
+      G.C = dst; G.ldc = lddst;
+      G.dtype = dt;
+      // tf32 keeps a wide output layer on the SIMT kernel; bf16 runs it on
+      // the tensor cores with an fp32 bias epilogue
+      use[k] = tc && N.wp && (!last || dt == kBf16);
+      if (use[k]) {
+        G.B = staged_w(v, N.wp, i, dt, &G.ldb);
+      } else {
+        G.B = N.params + v.w_off[i];
+        G.ldb = v.dims[i];
+      }
+      has[k] = true;
+      ones[k] = last ? -1 : v.dims[i + 1];
+      h[k] = dst;
+      ldh[k] = lddst;
+    }
+    UL_TRY(run_gemms(g, has, use, ones, s));
+    if (skinny[0] || skinny[1]) {
+      UL_TRY(L.open());
+      for (int k = 0; k < n; ++k) {
+        if (!skinny[k]) continue;
+        const MlpNet& N = nets[k];
+        const NetView& v = *N.v;
+        UL_TRY(skinny_fwd(h[k], ldh[k], M, v.dims[i], v.dims[i + 1], N.params + v.w_off[i],
+                          N.params + v.b_off[i], N.out, N.ld_out, dt, L.of(k)));
+      }
+      UL_TRY(L.close());
+    }
+  }
+  return UL_OK;
+}
+
+int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
+                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+  if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
+    UL_TRY(mlp_backward_n(nets, 1, backend, M, s, nullptr, nullptr, nullptr));
+    return mlp_backward_n(nets + 1, 1, backend, M, s, nullptr, nullptr, nullptr);
+  }
+  const Lanes L{s, n == 2 ? side : nullptr, fork, join};
+  const int dt = backend_dtype(backend);
+  const int eb = dt == kBf16 ? 2 : 4;
+  const bool tc = backend >= 1;
+  struct St {
+    float* dh_buf[2];
+    float* ws;
+    const float* dh;  // fp32 until the first hidden layer, then dt
+    int64_t lddh;
+    bool dh_f32;
+    int ping;
+    int db_done;  // layer whose db the layer above already produced (skinny column sums)
+  } st[2];
+  const int nl = nets[0].v->n_layers;
+  UL_TRY(L.open());
+  for (int k = 0; k < n; ++k) {
+    const MlpNet& N = nets[k];
+    const NetView& v = *N.v;
+    UL_CHECK_ARG(dt == kF32 || N.wp, "bf16 MLP needs staged weights");
+    UL_CHECK_ARG(dt == kF32 || N.dx == nullptr,
+                 "bf16 MLP backward: input gradients (dx) need the fp32 / tf32 back end");
+    const int64_t H = max_hidden_ld(v);
+    st[k].dh_buf[0] = N.work;
+    st[k].dh_buf[1] = N.work + M * H;
+    st[k].ws = N.work + 2 * M * H;
+    st[k].dh = N.dout;
+    st[k].lddh = N.ld_dout;
+    st[k].dh_f32 = true;
+    st[k].ping = 0;
+    st[k].db_done = -1;
+    if (N.want_dw && N.zero_logstd && N.grads)
+      UL_CUDA(cudaMemsetAsync(N.grads + v.logstd_off, 0, sizeof(float) * v.dims[nl], L.of(k)));
+  }
+  for (int i = nl - 1; i >= 0; --i) {
+    // ---- fused last-layer backward (skinny heads): dW, db, dh_prev and, when
+    // the layer below cannot get its db from the ones column, colsum(dh_prev)
+    bool skinny_done[2] = {false, false};
+    for (int k = 0; k < n; ++k) {
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      const int64_t out = v.dims[i + 1], in = v.dims[i];
+      const float* inp = i == 0 ? N.x : act_ptr(v, N.acts, M, i - 1, dt);
+      const int64_t ldin = i == 0 ? N.ldx : act_ld(v.dims[i], dt);
+      if (!(i == nl - 1 && skinny_ok((int)out, (int)in) && i > 0 && al16(inp, ldin, eb)))
+        continue;
+      St& S = st[k];
+      float* nxt = S.dh_buf[S.ping];
+      S.ping ^= 1;
+      const int64_t in_below = v.dims[i - 1];
+      const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
+      const bool need_cs = N.want_dw && tc && N.wp && !ones_free_of(in_below, below_ones);
+      UL_TRY(skinny_bwd(inp, ldin, M, (int)in, (int)out, N.params + v.w_off[i], S.dh, S.lddh,
+                        nxt, act_ld((int)in, dt), true, N.want_dw ? N.grads + v.w_off[i] : nullptr,
+                        N.want_dw ? N.grads + v.b_off[i] : nullptr,
+                        need_cs ? N.grads + v.b_off[i - 1] : nullptr, S.ws, dt, L.of(k)));
+      if (need_cs) S.db_done = i - 1;
+      S.dh = nxt;
+      S.lddh = act_ld((int)in, dt);
+      S.dh_f32 = dt == kF32;
+      skinny_done[k] = true;
+    }
+    if (skinny_done[0] || skinny_done[1]) {
+      bool any_rest = false;
+      for (int k = 0; k < n; ++k) any_rest |= !skinny_done[k];
+      if (!any_rest) continue;
+    }
+    // ---- upstream gradient of a wide output layer on the bf16 path -> bf16 rows
+    for (int k = 0; k < n; ++k) {
+      St& S = st[k];
+      if (skinny_done[k] || !(S.dh_f32 && dt == kBf16)) continue;
+      const int64_t out = nets[k].v->dims[i + 1];
+      float* cv = S.dh_buf[S.ping];
+      S.ping ^= 1;
+      const int64_t ldcv = act_ld((int)out, dt);
+      int64_t blocks = ceil_div(M * out, 256);
+      blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
+      f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, L.of(k)>>>(
+          S.dh, S.lddh, M, out, reinterpret_cast<__nv_bfloat16*>(cv), ldcv);
+      UL_TRY(check_launch("f32_to_bf16_kernel"));
+      S.dh = cv;
+      S.lddh = ldcv;
+      S.dh_f32 = false;
+    }
+    UL_TRY(L.close());
+    // ---- dW (+db via the ones column) for both networks: one grouped launch
+    GemmDesc gw[2] = {};
+    bool has_w[2] = {false, false}, tc_w[2] = {false, false}, free_w[2] = {false, false};
+    for (int k = 0; k < n; ++k) {
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      if (skinny_done[k] || !N.want_dw) continue;
+      const int64_t out = v.dims[i + 1], in = v.dims[i];
+      const float* inp = i == 0 ? N.x : act_ptr(v, N.acts, M, i - 1, dt);
+      const int64_t ldin = i == 0 ? N.ldx : act_ld(v.dims[i], dt);
+      const bool has_ones = i == 0 ? (N.x_has_ones && N.ldx >= in + 1) : true;
+      GemmDesc& G = gw[k];
+      G.M = out; G.K = M;
+      G.A = st[k].dh; G.lda = st[k].lddh; G.B = inp; G.ldb = ldin;
+      G.a_kmajor = false; G.b_kmajor = false; G.epi = kEpiStore;
+      G.C = st[k].ws;
+      G.dtype = dt;
+      free_w[k] = ones_free_of(in, has_ones);
+      G.N = free_w[k] ? in + 1 : in;
+      G.splits = dw_splits(out, in, M, true);
+      G.ldc = rup(G.N, 4);  // 16 B fp32 partial rows (TMA store)
+      tc_w[k] = tc && N.wp && (out >= 64 || dt == kBf16) && tc_eligible(G);
+      if (tc_w[k]) G.splits = tc_num_splits(M, G.splits, dt);
+      has_w[k] = true;
+    }
+    if (tc_w[0] && tc_w[1]) UL_TRY(gemm_tc_group(gw[0], gw[1], s));
+    else
+      for (int k = 0; k < n; ++k)
+        if (tc_w[k]) UL_TRY(gemm_tc(gw[k], -1, s));
+    if (tc_w[0] || tc_w[1]) {
+      DwTable tab{};
+      int64_t bx = 0;
+      int ny = 0;
+      for (int k = 0; k < n; ++k) {
+        if (!tc_w[k]) continue;
+        const NetView& v = *nets[k].v;
+        const int64_t out = v.dims[i + 1], in = v.dims[i];
+        tab.r[ny] = DwReduce{st[k].ws, gw[k].splits, out, in, gw[k].ldc, nets[k].grads + v.w_off[i],
+                             free_w[k] ? nets[k].grads + v.b_off[i] : nullptr};
+        const int64_t b = ceil_div(out * gw[k].ldc, 128);
+        bx = b > bx ? b : bx;
+        ++ny;
+      }
+      UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel, dim3((unsigned)bx, (unsigned)ny),
+                        dim3(256), 0, s, tab));
+    }
+    UL_TRY(L.open());
+    for (int k = 0; k < n; ++k) {
+      if (!has_w[k]) continue;
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      const int64_t out = v.dims[i + 1], in = v.dims[i];
+      St& S = st[k];
+      cudaStream_t sk = L.of(k);
+      if (tc_w[k]) {
+        if (!free_w[k] && S.db_done != i) {
+          // 128-row chunks (8 warps x 4 rows in flight x 4), at most 256 of them
+          const int64_t chunks = ceil_div(M, 128) < 256 ? ceil_div(M, 128) : 256;
+          const int64_t rows_per = ceil_div(M, chunks);
+          float* part = S.ws + (int64_t)gw[k].splits * out * gw[k].ldc;
+          const dim3 grid((unsigned)ceil_div(out, 256), (unsigned)chunks);
+          if (dt == kBf16)
+            UL_TRY(launch_pdl("colsum_kernel", colsum_kernel<__nv_bfloat16>, grid, dim3(256), 0,
+                              sk, reinterpret_cast<const __nv_bfloat16*>(S.dh), S.lddh, M,
+                              (int64_t)out, rows_per, part));
+          else
+            UL_TRY(launch_pdl("colsum_kernel", colsum_kernel<float>, grid, dim3(256), 0, sk,
+                              (const float*)S.dh, S.lddh, M, (int64_t)out, rows_per, part));
+          UL_TRY(reduce_splits(part, (int)chunks, out, N.grads + v.b_off[i], out, out, sk));
+        }
+      } else {
+        UL_CHECK_ARG(dt == kF32, "bf16 MLP: dW GEMM not tensor-core eligible");
+        GemmDesc G = gw[k];
+        const int sp = gemm_num_splits(M, dw_splits(out, in, M, false));
+        G.N = in;
+        G.splits = sp;
+        G.ldc = in;
+        G.rowsum = S.ws + (int64_t)sp * out * in;
+        UL_TRY(gemm_f32(G, sk));
+        UL_TRY(reduce_splits(S.ws, sp, out * in, N.grads + v.w_off[i], in, in, sk));
+        UL_TRY(reduce_splits(G.rowsum, sp, out, N.grads + v.b_off[i], out, out, sk));
+      }
+    }
+    if (i == 0) {
+      for (int k = 0; k < n; ++k) {
+        const MlpNet& N = nets[k];
+        if (N.dx == nullptr) continue;
+        const NetView& v = *N.v;
+        GemmDesc G{};
+        G.M = M; G.N = N.dx_ncols; G.K = v.dims[1];
+        G.A = st[k].dh; G.lda = st[k].lddh; G.B = N.params + v.w_off[0] + N.dx_col0;
+        G.ldb = v.dims[0];
+        G.C = N.dx; G.ldc = N.lddx;
+        G.a_kmajor = true; G.b_kmajor = false; G.epi = kEpiStore; G.splits = 1;
+        UL_TRY(gemm_f32(G, L.of(k)));
+      }
+      UL_TRY(L.close());
+      break;
+    }
+    UL_TRY(L.close());
+    // ---- dh_prev = (dh W) * elu'(h_{i-1}) for both networks: one grouped launch
+    GemmDesc gx[2] = {};
+    bool has_x[2] = {false, false}, tc_x[2] = {false, false};
+    const int no_ones[2] = {-1, -1};
+    for (int k = 0; k < n; ++k) {
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      if (skinny_done[k]) continue;
+      const int64_t out = v.dims[i + 1], in = v.dims[i];
+      St& S = st[k];
+      float* nxt = S.dh_buf[S.ping];
+      S.ping ^= 1;
+      GemmDesc& G = gx[k];
+      G.M = M; G.N = in; G.K = out;
+      G.A = S.dh; G.lda = S.lddh;
+      G.C = nxt; G.ldc = act_ld((int)in, dt);
+      G.aux = act_ptr(v, N.acts, M, i - 1, dt); G.ldaux = act_ld((int)in, dt);
+      G.a_kmajor = true; G.b_kmajor = false; G.epi = kEpiEluGrad; G.splits = 1;
+      G.dtype = dt;
+      tc_x[k] = tc && N.wp && (out >= 32 || dt == kBf16);
+      if (tc_x[k]) {
+        G.B = staged_w(v, N.wp, i, dt, &G.ldb);
+      } else {
+        G.B = N.params + v.w_off[i];
+        G.ldb = in;
+      }
+      has_x[k] = true;
+      S.dh = nxt;
+      S.lddh = act_ld((int)in, dt);
+    }
+    UL_TRY(run_gemms(gx, has_x, tc_x, no_ones, s));
+    UL_TRY(L.open());
+  }
+  return UL_OK;
+}
+
 int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
                 const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
                 cudaStream_t s) {
-  const int dt = backend_dtype(backend);
-  const int eb = dt == kBf16 ? 2 : 4;
-  const bool tc = backend >= 1 && wp != nullptr;
-  UL_CHECK_ARG(dt == kF32 || tc, "bf16 MLP needs staged weights");
-  const float* h = x;
-  int64_t ldh = ldx;
-  for (int i = 0; i < v.n_layers; ++i) {
-    const bool last = i == v.n_layers - 1;
-    float* dst = last ? out : const_cast<float*>(act_ptr(v, acts, M, i, dt));
-    const int64_t lddst = last ? ld_out : act_ld(v.dims[i + 1], dt);
-    if (last && skinny_ok(v.dims[i + 1], v.dims[i]) && al16(h, ldh, eb)) {  // 12-/1-wide head
-      UL_TRY(skinny_fwd(h, ldh, M, v.dims[i], v.dims[i + 1], params + v.w_off[i],
-                        params + v.b_off[i], dst, lddst, dt, s));
-      break;
-    }
-    GemmDesc g{};
-    g.M = M; g.N = v.dims[i + 1]; g.K = v.dims[i];
-    g.A = h; g.lda = ldh;
-    g.bias = params + v.b_off[i];
-    g.a_kmajor = true; g.b_kmajor = true;
-    g.epi = last ? kEpiBias : kEpiBiasElu;
-    g.splits = 1;
-    g.C = dst; g.ldc = lddst;
-    g.dtype = dt;
-    // tf32 keeps a wide output layer on the SIMT kernel; bf16 runs it on the
-    // tensor cores with an fp32 bias epilogue
-    const bool tc_here = tc && (!last || dt == kBf16);
-    if (tc_here) {
-      g.B = staged_w(v, wp, i, dt, &g.ldb);
-    } else {
-      g.B = params + v.w_off[i];
-      g.ldb = v.dims[i];
-    }
-    UL_TRY(run_gemm(g, tc_here, last ? -1 : v.dims[i + 1], s));
-    h = dst;
-    ldh = lddst;
-  }
-  return UL_OK;
+  MlpNet N{};
+  N.v = &v; N.params = params; N.wp = backend >= 1 ? wp : nullptr;
+  N.x = x; N.ldx = ldx; N.acts = acts; N.out = out; N.ld_out = ld_out;
+  return mlp_forward_n(&N, 1, backend, M, s, nullptr, nullptr, nullptr);
 }
 
 int mlp_backward(const NetView& v, const float* params, const float* wp, int backend,
@@ -367,148 +698,14 @@ int mlp_backward(const NetView& v, const float* params, const float* wp, int bac
                  const float* dout, int64_t ld_dout, float* grads, float* dx, int64_t lddx,
                  int dx_col0, int dx_ncols, bool want_dw, bool zero_logstd, float* work,
                  cudaStream_t s) {
-  const int dt = backend_dtype(backend);
-  const int eb = dt == kBf16 ? 2 : 4;
-  const bool tc = backend >= 1 && wp != nullptr;
-  UL_CHECK_ARG(dt == kF32 || tc, "bf16 MLP needs staged weights");
-  UL_CHECK_ARG(dt == kF32 || dx == nullptr,
-               "bf16 MLP backward: input gradients (dx) need the fp32 / tf32 back end");
-  const int64_t H = max_hidden_ld(v);
-  float* dh_buf[2] = {work, work + M * H};
-  float* ws = work + 2 * M * H;
-  const float* dh = dout;  // fp32 until the first hidden layer, then dt
-  int64_t lddh = ld_dout;
-  bool dh_f32 = true;
-  int ping = 0;
-  // column sums of the next hidden gradient, produced by the layer above
-  // (fused into skinny_bwd): layer index whose db is already written
-  int db_done = -1;
-  if (want_dw && zero_logstd && grads)
-    UL_CUDA(cudaMemsetAsync(grads + v.logstd_off, 0, sizeof(float) * v.dims[v.n_layers], s));
-  for (int i = v.n_layers - 1; i >= 0; --i) {
-    const int64_t out = v.dims[i + 1], in = v.dims[i];
-    const float* inp = i == 0 ? x : act_ptr(v, acts, M, i - 1, dt);
-    const int64_t ldin = i == 0 ? ldx : act_ld(v.dims[i], dt);
-    const bool has_ones = i == 0 ? (x_has_ones && ldx >= in + 1) : true;
-    auto bn_of = [](int64_t n) { return n > 128 ? 256 : 128; };
-    auto ones_free_of = [&](int64_t n_in, bool ones) {
-      return ones && bn_of(n_in + 1) == bn_of(n_in) &&
-             ceil_div(n_in + 1, bn_of(n_in + 1)) == ceil_div(n_in, bn_of(n_in));
-    };
-    if (i == v.n_layers - 1 && skinny_ok((int)out, (int)in) && i > 0 && al16(inp, ldin, eb)) {
-      // fused last-layer backward: dW, db, dh_prev and (when the layer below
-      // cannot get its db from the ones column) colsum(dh_prev) in one pass
-      float* nxt = dh_buf[ping];
-      ping ^= 1;
-      const int64_t in_below = v.dims[i - 1];
-      const bool below_ones = i - 1 == 0 ? x_has_ones && ldx >= in_below + 1 : true;
-      const bool need_cs = want_dw && tc && !ones_free_of(in_below, below_ones);
-      UL_TRY(skinny_bwd(inp, ldin, M, (int)in, (int)out, params + v.w_off[i], dh, lddh, nxt,
-                        act_ld((int)in, dt), true, want_dw ? grads + v.w_off[i] : nullptr,
-                        want_dw ? grads + v.b_off[i] : nullptr,
-                        need_cs ? grads + v.b_off[i - 1] : nullptr, ws, dt, s));
-      if (need_cs) db_done = i - 1;
-      dh = nxt;
-      lddh = act_ld((int)in, dt);
-      dh_f32 = dt == kF32;
-      continue;
-    }
-    if (dh_f32 && dt == kBf16) {
-      // wide output layer on the bf16 path: its upstream gradient as bf16 rows
-      float* cv = dh_buf[ping];
-      ping ^= 1;
-      const int64_t ldcv = act_ld((int)out, dt);
-      int64_t blocks = ceil_div(M * out, 256);
-      blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
-      f32_to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-          dh, lddh, M, out, reinterpret_cast<__nv_bfloat16*>(cv), ldcv);
-      UL_TRY(check_launch("f32_to_bf16_kernel"));
-      dh = cv;
-      lddh = ldcv;
-      dh_f32 = false;
-    }
-    if (want_dw) {
-      GemmDesc g{};
-      g.M = out; g.K = M;
-      g.A = dh; g.lda = lddh; g.B = inp; g.ldb = ldin;
-      g.a_kmajor = false; g.b_kmajor = false; g.epi = kEpiStore;
-      g.C = ws;
-      g.dtype = dt;
-      // [dW | db] through the ones column when that column rides in a tile the
-      // GEMM computes anyway; otherwise dW alone + a column-sum pass for db
-      // (unless the layer above already produced it)
-      const bool ones_free = ones_free_of(in, has_ones);
-      GemmDesc gt = g;
-      gt.N = ones_free ? in + 1 : in;
-      gt.splits = dw_splits(out, in, M, true);
-      gt.ldc = rup(gt.N, 4);  // 16 B fp32 partial rows (TMA store)
-      if (tc && (out >= 64 || dt == kBf16) && tc_eligible(gt)) {
-        const int sp = tc_num_splits(M, gt.splits, dt);
-        gt.splits = sp;
-        UL_TRY(gemm_tc(gt, -1, s));
-        const int64_t blocks = ceil_div(out * gt.ldc, 128);
-        reduce_dw_kernel<<<(unsigned)blocks, 256, 0, s>>>(
-            ws, sp, out, in, gt.ldc, grads + v.w_off[i],
-            ones_free ? grads + v.b_off[i] : nullptr);
-        UL_TRY(check_launch("reduce_dw_kernel"));
-        if (!ones_free && db_done != i) {
-          // 128-row chunks (8 warps x 4 rows in flight x 4), at most 256 of them
-          const int64_t chunks = ceil_div(M, 128) < 256 ? ceil_div(M, 128) : 256;
-          const int64_t rows_per = ceil_div(M, chunks);
-          float* part = ws + (int64_t)sp * out * gt.ldc;
-          const dim3 grid((unsigned)ceil_div(out, 256), (unsigned)chunks);
-          if (dt == kBf16)
-            colsum_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16*>(dh), lddh,
-                                               M, out, rows_per, part);
-          else
-            colsum_kernel<<<grid, 256, 0, s>>>(dh, lddh, M, out, rows_per, part);
-          UL_TRY(check_launch("colsum_kernel"));
-          UL_TRY(reduce_splits(part, (int)chunks, out, grads + v.b_off[i], out, out, s));
-        }
-      } else {
-        UL_CHECK_ARG(dt == kF32, "bf16 MLP: dW GEMM not tensor-core eligible");
-        const int sp = gemm_num_splits(M, dw_splits(out, in, M, false));
-        g.N = in;
-        g.splits = sp;
-        g.ldc = in;
-        g.rowsum = ws + (int64_t)sp * out * in;
-        UL_TRY(gemm_f32(g, s));
-        UL_TRY(reduce_splits(ws, sp, out * in, grads + v.w_off[i], in, in, s));
-        UL_TRY(reduce_splits(g.rowsum, sp, out, grads + v.b_off[i], out, out, s));
-      }
-    }
-    if (i == 0) {
-      if (dx == nullptr) break;
-      GemmDesc g{};
-      g.M = M; g.N = dx_ncols; g.K = out;
-      g.A = dh; g.lda = lddh; g.B = params + v.w_off[0] + dx_col0; g.ldb = in;
-      g.C = dx; g.ldc = lddx;
-      g.a_kmajor = true; g.b_kmajor = false; g.epi = kEpiStore; g.splits = 1;
-      UL_TRY(gemm_f32(g, s));
-      break;
-    }
-    // dh_prev = (dh W) * elu'(h_{i-1})
-    float* nxt = dh_buf[ping];
-    ping ^= 1;
-    GemmDesc g{};
-    g.M = M; g.N = in; g.K = out;
-    g.A = dh; g.lda = lddh;
-    g.C = nxt; g.ldc = act_ld((int)in, dt);
-    g.aux = act_ptr(v, acts, M, i - 1, dt); g.ldaux = act_ld((int)in, dt);
-    g.a_kmajor = true; g.b_kmajor = false; g.epi = kEpiEluGrad; g.splits = 1;
-    g.dtype = dt;
-    const bool tc_here = tc && (out >= 32 || dt == kBf16);
-    if (tc_here) {
-      g.B = staged_w(v, wp, i, dt, &g.ldb);
-    } else {
-      g.B = params + v.w_off[i];
-      g.ldb = in;
-    }
-    UL_TRY(run_gemm(g, tc_here, -1, s));
-    dh = nxt;
-    lddh = act_ld((int)in, dt);
-  }
-  return UL_OK;
+  MlpNet N{};
+  N.v = &v; N.params = params; N.wp = backend >= 1 ? wp : nullptr;
+  N.x = x; N.ldx = ldx; N.x_has_ones = x_has_ones;
+  N.acts = const_cast<float*>(acts);
+  N.dout = dout; N.ld_dout = ld_dout; N.grads = grads;
+  N.dx = dx; N.lddx = lddx; N.dx_col0 = dx_col0; N.dx_ncols = dx_ncols;
+  N.want_dw = want_dw; N.zero_logstd = zero_logstd; N.work = work;
+  return mlp_backward_n(&N, 1, backend, M, s, nullptr, nullptr, nullptr);
 }
 
 }  // namespace ul

@@ -27,6 +27,8 @@ constexpr int kPrepThreads = 256;
 __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl) {
   __shared__ double scratch[32];
   const int nb = gridDim.x;
+  pdl_trigger();
+  pdl_wait();
   for (int s = 0; s < st.nseg; ++s) {
     const float* g = st.g[s];
     const int64_t n = st.n[s];
@@ -117,6 +119,8 @@ __device__ __forceinline__ void adam_elem(float gi, float& m, float& v, float& p
 
 __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
                              int do_adam) {
+  pdl_trigger();
+  pdl_wait();
   const int s = blockIdx.y;
   if (s >= st.nseg) return;
   const int upd = ctl->seg_update[s];
@@ -243,8 +247,8 @@ int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s) {
   int64_t nmax = max_n(st);
   int blocks = (int)ceil_div(nmax, kPrepThreads * 8);
   blocks = blocks < 1 ? 1 : (blocks > UL_PREP_BLOCKS ? UL_PREP_BLOCKS : blocks);
-  prepare_kernel<<<blocks, kPrepThreads, 0, s>>>(st, ctl);
-  return check_launch("prepare_kernel");
+  return launch_pdl("prepare_kernel", prepare_kernel, dim3(blocks), dim3(kPrepThreads), 0, s, st,
+                    ctl);
 }
 
 int launch_apply(const SegTable& st, ul_opt_ctl* ctl, int write_grads, int do_adam,
@@ -252,8 +256,8 @@ int launch_apply(const SegTable& st, ul_opt_ctl* ctl, int write_grads, int do_ad
   int64_t nmax = max_n(st);
   int bx = (int)ceil_div(nmax, 256 * 4);
   bx = bx < 1 ? 1 : (bx > 4 * kNumSMs ? 4 * kNumSMs : bx);
-  apply_kernel<<<dim3(bx, st.nseg), 256, 0, s>>>(st, ctl, write_grads, do_adam);
-  return check_launch("apply_kernel");
+  return launch_pdl("apply_kernel", apply_kernel, dim3(bx, st.nseg), dim3(256), 0, s, st,
+                    (const ul_opt_ctl*)ctl, write_grads, do_adam);
 }
 
 }  // namespace ul

@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const TH* __restrict__
   float* sw = reinterpret_cast<float*>(smem + (size_t)kRows * P * sizeof(TH));
   const int t = threadIdx.x, r = t >> 2, q = t & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kRows;
+  pdl_trigger();
+  pdl_wait();
   float acc[NP];
 #pragma unroll
   for (int j = 0; j < NP; ++j) acc[j] = 0.f;
@@ -173,6 +175,8 @@ __global__ void __launch_bounds__(kThr) skinny_bwd_kernel(
   const int t = threadIdx.x, r = t >> 2, q = t & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kRows;
   float* pz = part + (int64_t)blockIdx.x * plen;
+  pdl_trigger();
+  pdl_wait();
   for (int base = t; base < kRows * N; base += kThr * 8) {
     float v[8];
 #pragma unroll
@@ -276,6 +280,8 @@ __global__ void __launch_bounds__(1024) reduce_parts_kernel(const float* __restr
   __shared__ float4 sm[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t total = n0 + n1 + n2;
+  pdl_trigger();
+  pdl_wait();
   const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
   if (j < total) {
@@ -350,9 +356,9 @@ int fwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, 
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  skinny_fwd_kernel<TH, NP><<<(unsigned)ceil_div(M, kRows), kThr, fwd_smem<TH>(K, NP), s>>>(
-      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, b, out, ldo);
-  return check_launch("skinny_fwd_kernel");
+  return launch_pdl("skinny_fwd_kernel", skinny_fwd_kernel<TH, NP>,
+                    dim3((unsigned)ceil_div(M, kRows)), dim3(kThr), fwd_smem<TH>(K, NP), s,
+                    reinterpret_cast<const TH*>(h), ldh, M, K, N, W, b, out, ldo);
 }
 
 template <typename TH, int NP>
@@ -369,14 +375,15 @@ int bwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, 
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  skinny_bwd_kernel<TH, NP><<<nblk, kThr, bwd_smem<TH>(K, NP), s>>>(
-      reinterpret_cast<const TH*>(h), ldh, M, K, N, W, dout, ldd, reinterpret_cast<TH*>(dh), lddh,
-      elu_grad ? 1 : 0, part, plen, want_dw ? 1 : 0, csum ? 1 : 0);
-  UL_TRY(check_launch("skinny_bwd_kernel"));
+  UL_TRY(launch_pdl("skinny_bwd_kernel", skinny_bwd_kernel<TH, NP>, dim3(nblk), dim3(kThr),
+                    bwd_smem<TH>(K, NP), s, reinterpret_cast<const TH*>(h), ldh, M, K, N, W, dout,
+                    ldd, reinterpret_cast<TH*>(dh), lddh, elu_grad ? 1 : 0, part, plen,
+                    want_dw ? 1 : 0, csum ? 1 : 0));
   if (want_dw || csum) {
-    reduce_parts_kernel<<<(unsigned)ceil_div(plen, 128), 1024, 0, s>>>(
-        part, nblk, plen, (int64_t)N * K, gw, N, gb, csum ? K : 0, gcs);
-    UL_TRY(check_launch("reduce_parts_kernel"));
+    UL_TRY(launch_pdl("reduce_parts_kernel", reduce_parts_kernel,
+                      dim3((unsigned)ceil_div(plen, 128)), dim3(1024), 0, s,
+                      (const float*)part, nblk, plen, (int64_t)N * K, gw, (int64_t)N, gb,
+                      (int64_t)(csum ? K : 0), gcs));
   }
   return UL_OK;
 }
