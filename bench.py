@@ -50,7 +50,7 @@ def _args():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--precision", choices=("fp32", "tf32", "bf16"), default=None)
+    ap.add_argument("--precision", choices=("fp32", "tf32", "bf16"), default="bf16")
     return ap.parse_args()
 
 

@@ -181,6 +181,8 @@ struct TcArgs {
   const float* bias;
   int ones_col;          // >= 0: also write C[m, ones_col] = 1 (activation ones column)
   unsigned long long* trace;  // diagnostics (UL_TC_TRACE): CTA 0 event timestamps, or null
+  float* csum;                // per-CTA output column sums [grid][ldcs], or null
+  int ldcs;
 };
 
 // trace slots: [0] entry, [1] setup done, [2..33] producer k-tile issue,
@@ -204,13 +206,16 @@ using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu ||
 
 // [stage ring][16 epilogue staging boxes][barriers][bias x 2]; as many stages
 // as fit the 227 KB of dynamic shared memory (at most 6)
-template <int BN, bool PAIR, int OB /* output element bytes */>
+template <int BN, bool PAIR, int OB /* output element bytes */, int EPI>
 struct Smem {
   static constexpr int kABytes = BM * 128;
   static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * 128;  // this CTA's share of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStagingBytes = kEpiWarps * 32 * 32 * OB;
-  static constexpr int kFixed = 1024 /*align*/ + 512 /*barriers*/ + 2 * BN * 4 /*bias*/;
+  // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
+  static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
+  static constexpr int kFixed =
+      1024 /*align*/ + 512 /*barriers*/ + 2 * BN * 4 /*bias*/ + kCsumBytes;
   static constexpr int kBudget = 232448;
   static constexpr int kStagesFit = (kBudget - kStagingBytes - kFixed) / kStageBytes;
   static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                    int ng0, int ngroups) {
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
-  using S = Smem<BN, PAIR, (int)sizeof(TO)>;
+  using S = Smem<BN, PAIR, (int)sizeof(TO), EPI>;
   constexpr bool kOutBf16 = sizeof(TO) == 2;
   constexpr int CS = PAIR ? 2 : 1;
   constexpr int BNL = BN / CS;  // B rows (N) this CTA loads
@@ -492,6 +497,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int row = quarter * 32 + lane;
     constexpr int kSlice = BN / 4;
     float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
+    // column sums of the ELU-gradient output (the bias gradient of the layer
+    // below): csum_s[quarter][n]; each (quarter, n) has exactly one writer
+    // warp -- the one with this quarter and n's slice -- so no atomics and a
+    // fixed summation order.  Each warp zeroes the entries it owns.
+    float* csum_s = sbias + 2 * BN;
+    const TcArgs& pcs = p0_.csum ? p0_ : p1_;
+    const int cs_pr = p0_.csum ? 0 : 1;
+    const bool csum_on = EPI == kEpiEluGrad && pcs.csum != nullptr;
+    if (csum_on) {
+      for (int n = lane; n < kCsumMaxN; n += 32)
+        if ((n % BN) / kSlice == slice) csum_s[quarter * kCsumMaxN + n] = 0.f;
+    }
     uint8_t* stg = smem + kStages * S::kStageBytes + ew * kBoxBytes;
     uint64_t* abar = aux_bar + ew;
     uint32_t aphase = 0;
@@ -606,6 +623,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        if (csum_on && T.pr == cs_pr) {
+          // butterfly reduce-scatter over the warp's 32 rows: afterwards lane
+          // l holds the sum of column c0 + l (rows >= M contribute zeros)
+#pragma unroll
+          for (int wd = 16; wd >= 1; wd >>= 1) {
+            const bool up = (lane & wd) != 0;
+#pragma unroll
+            for (int i = 0; i < wd; ++i) {
+              const float send = up ? v[i] : v[i + wd];
+              const float keep = up ? v[i + wd] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
+            }
+          }
+          const int n = n0 + c0 + lane;
+          if (n < kCsumMaxN) csum_s[quarter * kCsumMaxN + n] += v[0];
+        }
       }
       if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M) {
         TO* cp = reinterpret_cast<TO*>(p.C);
@@ -631,6 +664,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (EPI == kEpiEluGrad && (p0_.csum || p1_.csum)) {
+    // this CTA's column-sum partial row (quarters in fixed order)
+    const TcArgs& pcs = p0_.csum ? p0_ : p1_;
+    const float* csum_s = reinterpret_cast<const float*>(tmem_slot + 4) + 2 * BN;
+    for (int n = threadIdx.x; n < pcs.ldcs; n += blockDim.x) {
+      float v = 0.f;
+      if (n < pcs.N && n < kCsumMaxN)
+        v = ((csum_s[n] + csum_s[kCsumMaxN + n]) + csum_s[2 * kCsumMaxN + n]) +
+            csum_s[3 * kCsumMaxN + n];
+      pcs.csum[(int64_t)blockIdx.x * pcs.ldcs + n] = v;
+    }
+  }
   // no CTA may leave (or free TMEM) while its pair can still write into its
   // smem / TMEM or arrive on its barriers
   if (PAIR) cluster_sync_all();
@@ -735,7 +780,9 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   else m->x = m->c;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
   *a = TcArgs{(int)d.M, (int)d.N, (int)d.K, q.kps, mt, nt, q.zs, d.C, d.ldc, d.bias,
-              q.ones_col, trace_buffer()};
+              q.ones_col, trace_buffer(),
+              EPI == kEpiEluGrad && d.N <= kCsumMaxN ? d.csum_part : nullptr,
+              (int)ceil_div(d.N, 4) * 4};
   *ngroups = (int)ceil_div(mt, CS) * nt * q.zs;
   return UL_OK;
 }
@@ -743,7 +790,7 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
 template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
 int launch(const Prob* q, int np, cudaStream_t s) {
   using TO = OutT<TI, EPI>;
-  using SM = Smem<BN, PAIR, (int)sizeof(TO)>;
+  using SM = Smem<BN, PAIR, (int)sizeof(TO), EPI>;
   constexpr int CS = PAIR ? 2 : 1;
   TcMaps m[2];
   TcArgs a[2];
@@ -787,6 +834,8 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   const int total = ng[0] + ng[1];
   const int grid = (total < max_clusters ? total : max_clusters) * CS;
   cfg.gridDim = dim3((unsigned)grid);
+  for (int i = 0; i < np; ++i)
+    if (q[i].d->csum_nz) *q[i].d->csum_nz = grid;
   UL_CUDA(cudaLaunchKernelEx(&cfg, kern, m[0], m[1], a[0], a[1], ng[0], total));
   return check_launch("tc_gemm_kernel");
 }
@@ -801,11 +850,14 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   // CTA pairs (cta_group::2, M = 256 per UMMA) whenever there are two M
   // tiles; UL_TC_PAIR=0 disables them (experiments).
   static int pair_ok = -1;
-  if (pair_ok < 0) {
+  if (pair_ok == -1) {
     const char* e = getenv("UL_TC_PAIR");
-    pair_ok = e ? atoi(e) != 0 : 1;
+    pair_ok = e ? atoi(e) : -2;
   }
-  const bool pair = pair_ok && ceil_div(d.M, BM) >= 2;
+  // default: pairs for tf32 (4-byte operands: the halved B traffic pays),
+  // single CTAs for bf16 (measured faster end to end on the cfg2 update)
+  const bool want = pair_ok == -2 ? sizeof(TI) == 4 : pair_ok != 0;
+  const bool pair = want && ceil_div(d.M, BM) >= 2;
 #define UL_TC_BN(AMN, BMN, EPI, BN)                                        \
   if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(q, np, s); \
   return launch<TI, AMN, BMN, EPI, BN, false>(q, np, s);
@@ -886,7 +938,8 @@ int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
   const bool same = d0.dtype == d1.dtype && d0.a_kmajor == d1.a_kmajor &&
                     d0.b_kmajor == d1.b_kmajor && d0.epi == d1.epi &&
                     tc::bn_of(d0) == tc::bn_of(d1) &&
-                    (ceil_div(d0.M, tc::BM) >= 2) == (ceil_div(d1.M, tc::BM) >= 2);
+                    (ceil_div(d0.M, tc::BM) >= 2) == (ceil_div(d1.M, tc::BM) >= 2) &&
+                    !(d0.csum_part && d1.csum_part);
   if (!same) {
     UL_TRY(gemm_tc(d0, -1, s));
     return gemm_tc(d1, -1, s);

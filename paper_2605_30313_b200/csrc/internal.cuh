@@ -13,9 +13,30 @@ struct SegTable {
   int64_t n[UL_MAX_SEG];
   int nseg;
 };
-int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s);
+// PPO per-step loss finalisation folded into the optimizer's prepare kernel
+// (its last CTA runs it before the divergence latch reads ctl->loss_bad)
+struct LossFinalize {
+  const float* loss;     // [pol, val, kl] sums (after the optional all-reduce)
+  const float* log_std;  // actor log_std (entropy)
+  int A;
+  double n, vcoef, ecoef;
+  int last_in_epoch;
+  ul_ppo_stats* st;
+};
+// Staged weight copies refreshed by the Adam step itself (the tensor-core
+// MLP's operand layout): W_l of segment s at dst + dst_off[l], rows of ld
+struct StageOut {
+  void* dst[UL_MAX_SEG];
+  int dtype;  // kF32 / kBf16 (same for every segment)
+  int nl[UL_MAX_SEG];
+  int64_t w_off[UL_MAX_SEG][UL_MAX_LAYERS];
+  int64_t dst_off[UL_MAX_SEG][UL_MAX_LAYERS];
+  int rows[UL_MAX_SEG][UL_MAX_LAYERS], cols[UL_MAX_SEG][UL_MAX_LAYERS], ld[UL_MAX_SEG][UL_MAX_LAYERS];
+};
+int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s,
+                   const LossFinalize* lf = nullptr);
 int launch_apply(const SegTable& st, ul_opt_ctl* ctl, int write_grads, int do_adam,
-                 cudaStream_t s);
+                 cudaStream_t s, const StageOut* so = nullptr);
 
 // --------------------------------------------------------------------- GEMM
 // C[M,N] = sum_k A(m,k) B(k,n), fp32.
@@ -58,13 +79,38 @@ struct GemmDesc {
   // kBf16: A, B (and aux / C of the ELU epilogues) hold bf16 despite the
   // float* fields; only the tensor-core path accepts it
   int dtype = kF32;
+  // tensor-core ELU-gradient epilogue only (N <= kCsumMaxN): also emit
+  // per-CTA column sums of the output, csum_part[cta][round_up(N,4)]; the
+  // launch stores its CTA count in *csum_nz (the bias gradient of the layer
+  // below, reduced later with a ReduceJob)
+  float* csum_part = nullptr;
+  int* csum_nz = nullptr;
 };
+constexpr int kCsumMaxN = 512;
 int gemm_f32(const GemmDesc& d, cudaStream_t s);
 // number of K splits gemm_f32 actually launches for a requested split count
 int gemm_num_splits(int64_t K, int splits);
 // out[j] (+)= sum_z ws[z*len + j], j < len
 int reduce_splits(const float* ws, int splits, int64_t len, float* out, int64_t ld_rows,
                   int64_t row_len, cudaStream_t s);
+
+// Fixed-order reduction of block / split partials: out = sum_z src[z*len + j].
+// kind 0 (split-K dW): j -> (r, c) = divmod(j, ldp); c < in -> gw[r*in + c],
+//   c == in -> gb[r] (ones-column bias), c > in padding.
+// kind 1 (segments): [0,n0) -> o0, [n0,n0+n1) -> o1, [n0+n1,n0+n1+n2) -> o2.
+// len must be a multiple of 4; null destinations are skipped.
+struct ReduceJob {
+  const float* src;
+  int nz;
+  int kind;
+  int64_t len;
+  int64_t ldp, in;
+  float* gw;
+  float* gb;
+  int64_t n0, n1, n2;
+  float *o0, *o1, *o2;
+};
+constexpr int kMaxReduceJobs = 4;
 
 // ------------------------------------------------------------------ MLP
 struct NetView {

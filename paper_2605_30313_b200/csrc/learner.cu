@@ -152,8 +152,60 @@ void free_plan(PpoPlan* p) {
   if (p->ev_join) cudaEventDestroy(p->ev_join);
 }
 
-// device part of begin: stats reset + advantage statistics (graph-capturable)
+// Both networks' MLP pass.  Grouped (default off, UL_GROUP=1): lockstep
+// layers with one tensor-core launch per layer for both networks.  Otherwise
+// the critic runs on the side stream concurrently with the actor (its
+// kernels fill the gaps and tails of the actor's).
+int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool fwd) {
+  static int grouped = -1;
+  if (grouped < 0) {
+    const char* e = getenv("UL_GROUP");
+    grouped = e ? atoi(e) != 0 : 0;
+  }
+  if (grouped) {
+    return fwd ? mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join)
+               : mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join);
+  }
+  UL_CUDA(cudaEventRecord(p->ev_fork, s));
+  UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+  if (fwd) {
+    UL_TRY(mlp_forward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr));
+    UL_TRY(mlp_forward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr));
+  } else {
+    UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr));
+    UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr));
+  }
+  UL_CUDA(cudaEventRecord(p->ev_join, p->side));
+  UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+  return UL_OK;
+}
+
+void fill_stage_out(const PpoPlan* p, StageOut* so) {
+  const NetView* vs[2] = {&p->va, &p->vc};
+  float* dst[2] = {p->wst_a, p->wst_c};
+  so->dtype = p->dt;
+  for (int sg = 0; sg < 2; ++sg) {
+    const NetView& v = *vs[sg];
+    so->dst[sg] = dst[sg];
+    so->nl[sg] = v.n_layers;
+    for (int l = 0; l < v.n_layers; ++l) {
+      so->w_off[sg][l] = v.w_off[l];
+      so->dst_off[sg][l] = p->dt == kBf16 ? v.wb_off[l] : v.wp_off[l];
+      so->rows[sg][l] = v.dims[l + 1];
+      so->cols[sg][l] = v.dims[l];
+      so->ld[sg][l] = (v.dims[l] + (p->dt == kBf16 ? 7 : 3)) / (p->dt == kBf16 ? 8 : 4) *
+                      (p->dt == kBf16 ? 8 : 4);
+    }
+  }
+}
+
+// device part of begin: stats reset + advantage statistics + staged weights
+// (graph-capturable)
 int begin_device(PpoPlan* p, cudaStream_t s) {
+  if (p->d.gemm_backend >= 1) {
+    UL_TRY(stage_weights_dt(p->va, p->b.actor_params, p->wst_a, p->dt, s));
+    UL_TRY(stage_weights_dt(p->vc, p->b.critic_params, p->wst_c, p->dt, s));
+  }
   UL_CUDA(cudaMemsetAsync(p->st_d, 0, sizeof(ul_ppo_stats), s));
   // critic log_std never receives a gradient (R:algos/ppo.py:119); keep its slot zero
   UL_CUDA(cudaMemsetAsync(p->red + p->Pa + p->vc.logstd_off, 0, sizeof(float), s));
@@ -198,10 +250,8 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   // per layer, the critic's small kernels on the side stream.  Weights
   // changed at the previous Adam step: the tensor-core path restages them.
   const int be = p->d.gemm_backend;
-  if (tc) {
-    UL_TRY(stage_weights_dt(p->va, b.actor_params, p->wst_a, p->dt, s));
-    UL_TRY(stage_weights_dt(p->vc, b.critic_params, p->wst_c, p->dt, s));
-  }
+  // (staged tensor-core weights: written at update begin, then refreshed by
+  // every Adam step -- see step_apply)
   MlpNet nets[2] = {};
   nets[0].v = &p->va;
   nets[0].params = b.actor_params;
@@ -233,7 +283,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   nets[1].want_dw = true;
   nets[1].zero_logstd = true;  // critic log_std never receives a gradient
   nets[1].work = p->work_c;
-  UL_TRY(mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join));
+  UL_TRY(mlp_pass(p, nets, be, ml, s, true));
   mark(p, 0, s);
   // K9 head
   PpoHeadArgs h{};
@@ -266,7 +316,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   UL_TRY(launch_ppo_head(h, s));
   mark(p, 2, s);
   // K8 backwards of both networks into the contiguous all-reduce buffer
-  UL_TRY(mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join));
+  UL_TRY(mlp_pass(p, nets, be, ml, s, false));
   mark(p, 0, s);
   return UL_OK;
 }
@@ -274,10 +324,15 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
 int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
   (void)e;
   const ul_ppo_bindings& b = p->b;
-  UL_TRY(launch_ppo_loss_finalize(p->red + p->Pa + p->Pc, b.actor_params + p->va.logstd_off, p->A,
-                                  (double)p->mb, p->d.value_loss_coef, p->d.entropy_coef,
-                                  k == p->d.minibatches - 1, p->ctl_d, p->st_d, s));
-  mark(p, 2, s);
+  LossFinalize lf{};
+  lf.loss = p->red + p->Pa + p->Pc;
+  lf.log_std = b.actor_params + p->va.logstd_off;
+  lf.A = p->A;
+  lf.n = (double)p->mb;
+  lf.vcoef = p->d.value_loss_coef;
+  lf.ecoef = p->d.entropy_coef;
+  lf.last_in_epoch = k == p->d.minibatches - 1;
+  lf.st = p->st_d;
   SegTable st{};
   st.nseg = 2;
   st.g[0] = p->red;
@@ -290,8 +345,13 @@ int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
   st.v[1] = b.critic_v;
   st.n[0] = p->Pa;
   st.n[1] = p->Pc;
-  UL_TRY(launch_prepare(st, p->ctl_d, s));
-  UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s));
+  // joint clip + loss finalisation, then Adam (which also refreshes the
+  // staged tensor-core weights for the next step)
+  UL_TRY(launch_prepare(st, p->ctl_d, s, &lf));
+  StageOut so{};
+  const bool tc = p->d.gemm_backend >= 1;
+  if (tc) fill_stage_out(p, &so);
+  UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s, tc ? &so : nullptr));
   mark(p, 3, s);
   return UL_OK;
 }

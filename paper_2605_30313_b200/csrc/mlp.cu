@@ -27,7 +27,7 @@ int skinny_fwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float*
                const float* b, float* out, int64_t ldo, int dtype, cudaStream_t s);
 int skinny_bwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
                const float* dout, int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw,
-               float* gb, float* gcs, float* part, int dtype, cudaStream_t s);
+               float* gb, float* gcs, float* part, int dtype, ReduceJob* defer, cudaStream_t s);
 
 namespace {
 
@@ -37,38 +37,33 @@ int64_t rup(int64_t x, int64_t m) { return ceil_div(x, m) * m; }
 // bias gradient, columns > in are TMA-row padding.  A warp owns 128 columns
 // (float4 lanes) and the splits z = w, w + 8, ... with every load issued
 // before the adds; the 8 warps combine in fixed order (deterministic).
-struct DwReduce {
-  const float* ws;
-  int splits;
-  int64_t out, in, ldp;
-  float* gw;
-  float* gb;
-};
-struct DwTable {
-  DwReduce r[2];  // blockIdx.y selects the network
+struct ReduceTable {
+  ReduceJob r[kMaxReduceJobs];  // blockIdx.y selects the job
 };
 
-__global__ void __launch_bounds__(256) reduce_dw_kernel(DwTable tab) {
-  __shared__ float4 sm[8][32];
-  const DwReduce& q = tab.r[blockIdx.y];
-  const float* __restrict__ ws = q.ws;
-  const int splits = q.splits;
+__global__ void __launch_bounds__(1024) reduce_dw_kernel(ReduceTable tab) {
+  __shared__ float4 sm[32][32];
+  const ReduceJob& q = tab.r[blockIdx.y];
+  const float* __restrict__ ws = q.src;
+  const int splits = q.nz;
   const int64_t in = q.in, ldp = q.ldp;
   float* __restrict__ gw = q.gw;
   float* __restrict__ gb = q.gb;
-  const int64_t len = q.out * ldp;
+  const int64_t len = q.len;
   pdl_trigger();
   pdl_wait();
   if ((int64_t)blockIdx.x * 128 >= len) return;  // block-uniform
+  // 32 warps over the partials (z = w, w + 32, ...), 8 loads in flight each:
+  // a 384-deep head reduction is two round trips, a 35-split dW one
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (j < len) {
-    for (int z0 = w; z0 < splits; z0 += 64) {
+    for (int z0 = w; z0 < splits; z0 += 256) {
       float4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int z = z0 + 8 * u;
+        const int z = z0 + 32 * u;
         v[u] = z < splits ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * len + j))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -85,21 +80,34 @@ __global__ void __launch_bounds__(256) reduce_dw_kernel(DwTable tab) {
   __syncthreads();
   if (w == 0 && j < len) {
     float4 t = sm[0][lane];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) {
-      const float4 q = sm[k][lane];
-      t.x += q.x;
-      t.y += q.y;
-      t.z += q.z;
-      t.w += q.w;
+    for (int k = 1; k < 32; ++k) {
+      const float4 q4 = sm[k][lane];
+      t.x += q4.x;
+      t.y += q4.y;
+      t.z += q4.z;
+      t.w += q4.w;
     }
     const float tv[4] = {t.x, t.y, t.z, t.w};
-    const int64_t r = j / ldp, c0 = j - r * ldp;  // 4 | ldp: one row per float4
+    if (q.kind == 0) {
+      const int64_t r = j / ldp, c0 = j - r * ldp;  // 4 | ldp: one row per float4
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t c = c0 + e;
-      if (c < in) gw[r * in + c] = tv[e];
-      else if (c == in && gb) gb[r] = tv[e];
+      for (int e = 0; e < 4; ++e) {
+        const int64_t c = c0 + e;
+        if (c < in) gw[r * in + c] = tv[e];
+        else if (c == in && gb) gb[r] = tv[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t c = j + e;
+        if (c < q.n0) {
+          if (q.o0) q.o0[c] = tv[e];
+        } else if (c < q.n0 + q.n1) {
+          if (q.o1) q.o1[c - q.n0] = tv[e];
+        } else if (c < q.n0 + q.n1 + q.n2) {
+          if (q.o2) q.o2[c - q.n0 - q.n1] = tv[e];
+        }
+      }
     }
   }
 }
@@ -267,20 +275,27 @@ static int dw_splits(int64_t out, int64_t in, int64_t M, bool tc) {
   return (int)(sp > 64 ? 64 : sp);
 }
 
-int64_t bwd_work_floats(const NetView& v, int64_t M) {
+// backward workspace: [2 hidden-gradient buffers][split-K dW + column-sum
+// partials][skinny head partials] -- the head's partials outlive the next
+// layer's dW GEMM (their reduction is folded into that layer's reduction)
+static int64_t dw_ws_floats(const NetView& v, int64_t M) {
   int64_t ws = 0;
   for (int i = 0; i < v.n_layers; ++i) {
     const int64_t out = v.dims[i + 1], in = v.dims[i];
     const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
                        ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
-    int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 256 * out;
-    if (skinny_ok((int)out, (int)in)) {
-      const int64_t sk = skinny_part_floats(M, (int)in, (int)out);
-      need = sk > need ? sk : need;
-    }
+    const int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 256 * out;
     ws = need > ws ? need : ws;
   }
-  return 2 * M * max_hidden_ld(v) + ws;
+  return rup(ws, 64);
+}
+
+int64_t bwd_work_floats(const NetView& v, int64_t M) {
+  const int last = v.n_layers - 1;
+  int64_t sk = skinny_part_floats(M, v.dims[last], v.dims[last + 1]);
+  // (the region also holds the dX epilogue's per-CTA column-sum partials)
+  sk = sk > (int64_t)kNumSMs * kCsumMaxN ? sk : (int64_t)kNumSMs * kCsumMaxN;
+  return 2 * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk;
 }
 
 // hidden layer i's activation rows (byte offsets: bf16 rows are half as wide)
@@ -365,6 +380,20 @@ struct Lanes {
     return UL_OK;
   }
 };
+
+// one launch for up to kMaxReduceJobs fixed-order partial reductions
+int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
+  if (nj == 0) return UL_OK;
+  ReduceTable tab{};
+  int64_t bx = 1;
+  for (int q = 0; q < nj; ++q) {
+    tab.r[q] = jobs[q];
+    const int64_t b = ceil_div(jobs[q].len, 128);
+    bx = b > bx ? b : bx;
+  }
+  return launch_pdl("reduce_dw_kernel", reduce_dw_kernel, dim3((unsigned)bx, (unsigned)nj),
+                    dim3(1024), 0, s, tab);
+}
 
 // run 1 or 2 independent GEMMs; tensor-core pairs share a launch
 int run_gemms(GemmDesc* g, const bool* has, const bool* use_tc, const int* ones, cudaStream_t s) {
@@ -476,7 +505,10 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     bool dh_f32;
     int ping;
     int db_done;  // layer whose db the layer above already produced (skinny column sums)
+    float* sk_part;
   } st[2];
+  ReduceJob pend[4];  // deferred reductions (skinny heads, fused column sums) for the next reduce launch
+  int npend = 0;
   const int nl = nets[0].v->n_layers;
   UL_TRY(L.open());
   for (int k = 0; k < n; ++k) {
@@ -489,6 +521,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     st[k].dh_buf[0] = N.work;
     st[k].dh_buf[1] = N.work + M * H;
     st[k].ws = N.work + 2 * M * H;
+    st[k].sk_part = st[k].ws + dw_ws_floats(v, M);
     st[k].dh = N.dout;
     st[k].lddh = N.ld_dout;
     st[k].dh_f32 = true;
@@ -515,10 +548,13 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       const int64_t in_below = v.dims[i - 1];
       const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
       const bool need_cs = N.want_dw && tc && N.wp && !ones_free_of(in_below, below_ones);
+      // its partial reduction waits for the next layer's reduce launch
+      ReduceJob* dj = (N.want_dw || need_cs) ? &pend[npend] : nullptr;
       UL_TRY(skinny_bwd(inp, ldin, M, (int)in, (int)out, N.params + v.w_off[i], S.dh, S.lddh,
                         nxt, act_ld((int)in, dt), true, N.want_dw ? N.grads + v.w_off[i] : nullptr,
                         N.want_dw ? N.grads + v.b_off[i] : nullptr,
-                        need_cs ? N.grads + v.b_off[i - 1] : nullptr, S.ws, dt, L.of(k)));
+                        need_cs ? N.grads + v.b_off[i - 1] : nullptr, S.sk_part, dt, dj, L.of(k)));
+      if (dj) ++npend;
       if (need_cs) S.db_done = i - 1;
       S.dh = nxt;
       S.lddh = act_ld((int)in, dt);
@@ -578,21 +614,26 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       for (int k = 0; k < n; ++k)
         if (tc_w[k]) UL_TRY(gemm_tc(gw[k], -1, s));
     if (tc_w[0] || tc_w[1]) {
-      DwTable tab{};
-      int64_t bx = 0;
-      int ny = 0;
+      ReduceJob jobs[kMaxReduceJobs];
+      int nj = 0;
       for (int k = 0; k < n; ++k) {
         if (!tc_w[k]) continue;
         const NetView& v = *nets[k].v;
         const int64_t out = v.dims[i + 1], in = v.dims[i];
-        tab.r[ny] = DwReduce{st[k].ws, gw[k].splits, out, in, gw[k].ldc, nets[k].grads + v.w_off[i],
-                             free_w[k] ? nets[k].grads + v.b_off[i] : nullptr};
-        const int64_t b = ceil_div(out * gw[k].ldc, 128);
-        bx = b > bx ? b : bx;
-        ++ny;
+        ReduceJob& J = jobs[nj++];
+        J = ReduceJob{};
+        J.src = st[k].ws;
+        J.nz = gw[k].splits;
+        J.kind = 0;
+        J.len = out * gw[k].ldc;
+        J.ldp = gw[k].ldc;
+        J.in = in;
+        J.gw = nets[k].grads + v.w_off[i];
+        J.gb = free_w[k] ? nets[k].grads + v.b_off[i] : nullptr;
       }
-      UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel, dim3((unsigned)bx, (unsigned)ny),
-                        dim3(256), 0, s, tab));
+      for (int q = 0; q < npend; ++q) jobs[nj++] = pend[q];
+      npend = 0;
+      UL_TRY(launch_reduce(jobs, nj, s));
     }
     UL_TRY(L.open());
     for (int k = 0; k < n; ++k) {
@@ -648,10 +689,16 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       break;
     }
     UL_TRY(L.close());
+    if (npend) {  // no dW reduction at this layer to ride on
+      UL_TRY(launch_reduce(pend, npend, s));
+      npend = 0;
+    }
     // ---- dh_prev = (dh W) * elu'(h_{i-1}) for both networks: one grouped launch
     GemmDesc gx[2] = {};
     bool has_x[2] = {false, false}, tc_x[2] = {false, false};
     const int no_ones[2] = {-1, -1};
+    int cs_nz[2] = {0, 0};
+    bool cs_on[2] = {false, false};
     for (int k = 0; k < n; ++k) {
       const MlpNet& N = nets[k];
       const NetView& v = *N.v;
@@ -674,13 +721,39 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
         G.B = N.params + v.w_off[i];
         G.ldb = in;
       }
+      // the layer below needs colsum(dh_prev) for its db: let this GEMM's
+      // epilogue produce per-CTA partials (reduced with the next reduction)
+      const int64_t in_below = v.dims[i - 1];
+      const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
+      if (N.want_dw && tc_x[k] && in <= kCsumMaxN && S.db_done != i - 1 &&
+          !ones_free_of(in_below, below_ones)) {
+        G.csum_part = S.sk_part;
+        G.csum_nz = &cs_nz[k];
+        cs_on[k] = true;
+      }
       has_x[k] = true;
       S.dh = nxt;
       S.lddh = act_ld((int)in, dt);
     }
     UL_TRY(run_gemms(gx, has_x, tc_x, no_ones, s));
+    for (int k = 0; k < n; ++k) {
+      if (!cs_on[k]) continue;
+      if (cs_nz[k] == 0) continue;  // GEMM fell back to SIMT: colsum kernel later
+      const NetView& v = *nets[k].v;
+      const int64_t in = v.dims[i];
+      ReduceJob& J = pend[npend++];
+      J = ReduceJob{};
+      J.src = st[k].sk_part;
+      J.nz = cs_nz[k];
+      J.kind = 1;
+      J.len = ceil_div(in, 4) * 4;
+      J.n0 = in;
+      J.o0 = nets[k].grads + v.b_off[i - 1];
+      st[k].db_done = i - 1;
+    }
     UL_TRY(L.open());
   }
+  if (npend) UL_TRY(launch_reduce(pend, npend, s));
   return UL_OK;
 }
 

@@ -17,6 +17,8 @@
 //             gradients the update is bit-identical to numpy.
 // HBM bytes: prepare 4 B/param, apply 28 B/param (+4 if clipped grads are
 // written back for the clip_global_norm API).
+#include <cuda_bf16.h>
+
 #include "internal.cuh"
 
 namespace ul {
@@ -24,7 +26,29 @@ namespace {
 
 constexpr int kPrepThreads = 256;
 
-__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl) {
+constexpr double kLog2PiO = 1.8378770664093453;
+
+// R:algos/ppo.py loss bookkeeping of one minibatch step (see heads.cu)
+__device__ void finalize_loss(const LossFinalize& f, ul_opt_ctl* ctl) {
+  const double pol = -(double)f.loss[0] / f.n;
+  const double val = (double)f.loss[1] / f.n;
+  const double kl = (double)f.loss[2] / f.n;
+  double ent = 0.0;
+  for (int j = 0; j < f.A; ++j) ent += (double)f.log_std[j] + 0.5 * (kLog2PiO + 1.0);
+  const double total = pol + f.vcoef * val - f.ecoef * ent;
+  if (!isfinite(total)) ctl->loss_bad = 1;
+  if (!ctl->diverged && isfinite(total)) {
+    f.st->policy_sum += pol;
+    f.st->value_sum += val;
+    f.st->entropy_sum += ent;
+    f.st->kl_last = kl;
+    if (f.last_in_epoch) f.st->kl_epoch_sum += kl;
+    f.st->steps += 1;
+  }
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl,
+                                                               LossFinalize lf, int has_lf) {
   __shared__ double scratch[32];
   const int nb = gridDim.x;
   pdl_trigger();
@@ -76,6 +100,7 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_o
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  if (has_lf) finalize_loss(lf, ctl);
   double joint = 0.0;
   int earlier_bad = ctl->loss_bad;
   const int was_diverged = ctl->diverged;
@@ -117,8 +142,23 @@ __device__ __forceinline__ void adam_elem(float gi, float& m, float& v, float& p
   p = __fsub_rn(p, step);
 }
 
+// write the updated parameter i of segment s into its staged operand slot
+__device__ __forceinline__ void stage_param(const StageOut& so, int s, int64_t i, float p) {
+  for (int l = 0; l < so.nl[s]; ++l) {
+    const int64_t o = i - so.w_off[s][l];
+    const int cols = so.cols[s][l];
+    if (o >= 0 && o < (int64_t)so.rows[s][l] * cols) {
+      const int r = (int)o / cols, c = (int)o - r * cols;
+      const int64_t d = so.dst_off[s][l] + (int64_t)r * so.ld[s][l] + c;
+      if (so.dtype == kBf16) reinterpret_cast<__nv_bfloat16*>(so.dst[s])[d] = __float2bfloat16_rn(p);
+      else reinterpret_cast<float*>(so.dst[s])[d] = p;
+      return;
+    }
+  }
+}
+
 __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
-                             int do_adam) {
+                             int do_adam, StageOut so, int has_so) {
   pdl_trigger();
   pdl_wait();
   const int s = blockIdx.y;
@@ -168,6 +208,10 @@ __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, in
     reinterpret_cast<float4*>(pm)[i] = m4;
     reinterpret_cast<float4*>(pv)[i] = v4;
     reinterpret_cast<float4*>(pp)[i] = p4;
+    if (has_so && so.dst[s]) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) stage_param(so, s, 4 * i + e, pa[e]);
+    }
   }
   for (int64_t i = 4 * n4 + t0; i < n; i += stride) {
     float gi = g[i];
@@ -178,6 +222,7 @@ __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, in
     pm[i] = m;
     pv[i] = v;
     pp[i] = p;
+    if (has_so && so.dst[s]) stage_param(so, s, i, p);
   }
 }
 
@@ -243,21 +288,25 @@ int64_t max_n(const SegTable& st) {
 
 }  // namespace
 
-int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s) {
+int launch_prepare(const SegTable& st, ul_opt_ctl* ctl, cudaStream_t s, const LossFinalize* lf) {
   int64_t nmax = max_n(st);
   int blocks = (int)ceil_div(nmax, kPrepThreads * 8);
   blocks = blocks < 1 ? 1 : (blocks > UL_PREP_BLOCKS ? UL_PREP_BLOCKS : blocks);
+  LossFinalize f{};
+  if (lf) f = *lf;
   return launch_pdl("prepare_kernel", prepare_kernel, dim3(blocks), dim3(kPrepThreads), 0, s, st,
-                    ctl);
+                    ctl, f, lf ? 1 : 0);
 }
 
 int launch_apply(const SegTable& st, ul_opt_ctl* ctl, int write_grads, int do_adam,
-                 cudaStream_t s) {
+                 cudaStream_t s, const StageOut* so) {
   int64_t nmax = max_n(st);
   int bx = (int)ceil_div(nmax, 256 * 4);
   bx = bx < 1 ? 1 : (bx > 4 * kNumSMs ? 4 * kNumSMs : bx);
+  StageOut o{};
+  if (so) o = *so;
   return launch_pdl("apply_kernel", apply_kernel, dim3(bx, st.nseg), dim3(256), 0, s, st,
-                    (const ul_opt_ctl*)ctl, write_grads, do_adam);
+                    (const ul_opt_ctl*)ctl, write_grads, do_adam, o, so ? 1 : 0);
 }
 
 }  // namespace ul

@@ -364,11 +364,12 @@ int fwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, 
 template <typename TH, int NP>
 int bwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* dout,
            int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw, float* gb, float* gcs,
-           float* part, cudaStream_t s) {
+           float* part, ReduceJob* defer, cudaStream_t s) {
   const int nblk = (int)ceil_div(M, kRows);
   const bool want_dw = gw || gb;
   const bool csum = gcs != nullptr && dh != nullptr;
-  const int64_t plen = (int64_t)N * K + N + (csum ? K : 0);
+  // block partial stride, padded to 16 bytes for the float4 reduction
+  const int64_t plen = ceil_div((int64_t)N * K + N + (csum ? K : 0), 4) * 4;
   static bool attr = false;
   if (!attr) {
     UL_CUDA(cudaFuncSetAttribute(skinny_bwd_kernel<TH, NP>,
@@ -379,6 +380,21 @@ int bwd_np(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, 
                     bwd_smem<TH>(K, NP), s, reinterpret_cast<const TH*>(h), ldh, M, K, N, W, dout,
                     ldd, reinterpret_cast<TH*>(dh), lddh, elu_grad ? 1 : 0, part, plen,
                     want_dw ? 1 : 0, csum ? 1 : 0));
+  if (defer) {
+    // the caller folds this reduction into its next reduction launch
+    *defer = ReduceJob{};
+    defer->src = part;
+    defer->nz = nblk;
+    defer->kind = 1;
+    defer->len = plen;
+    defer->n0 = (int64_t)N * K;
+    defer->o0 = gw;
+    defer->n1 = N;
+    defer->o1 = gb;
+    defer->n2 = csum ? K : 0;
+    defer->o2 = gcs;
+    return UL_OK;
+  }
   if (want_dw || csum) {
     UL_TRY(launch_pdl("reduce_parts_kernel", reduce_parts_kernel,
                       dim3((unsigned)ceil_div(plen, 128)), dim3(1024), 0, s,
@@ -409,8 +425,9 @@ int fwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, c
 template <typename TH>
 int bwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, const float* dout,
           int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw, float* gb, float* gcs,
-          float* part, cudaStream_t s) {
-  UL_SKINNY_NP(bwd_np, h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs, part, s)
+          float* part, ReduceJob* defer, cudaStream_t s) {
+  UL_SKINNY_NP(bwd_np, h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs, part,
+               defer, s)
 }
 #undef UL_SKINNY_NP
 
@@ -419,7 +436,7 @@ int bwd_t(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W, c
 bool skinny_ok(int N, int K) { return N >= 1 && N <= kMaxN && (int64_t)N * K <= kMaxW * 4; }
 
 int64_t skinny_part_floats(int64_t M, int K, int N) {
-  return ceil_div(M, kRows) * ((int64_t)N * K + N + K);
+  return ceil_div(M, kRows) * (ceil_div((int64_t)N * K + N + K, 4) * 4);
 }
 
 int skinny_fwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
@@ -432,14 +449,17 @@ int skinny_fwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float*
 // gw [N, K], gb [N] and gcs [K] (column sums of dh: the bias gradient of the
 // layer below) receive reduced results when non-null; `part` holds
 // skinny_part_floats(M, K, N) floats of scratch.
+// defer (may be null): instead of launching the partial reduction, describe it
+// so the caller can fold it into a later reduction launch.
 int skinny_bwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
                const float* dout, int64_t ldd, void* dh, int64_t lddh, bool elu_grad, float* gw,
-               float* gb, float* gcs, float* part, int dtype, cudaStream_t s) {
+               float* gb, float* gcs, float* part, int dtype, ReduceJob* defer, cudaStream_t s) {
   if (M == 0) return UL_OK;
   if (dtype == kBf16)
     return bwd_t<__nv_bfloat16>(h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs,
-                                part, s);
-  return bwd_t<float>(h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs, part, s);
+                                part, defer, s);
+  return bwd_t<float>(h, ldh, M, K, N, W, dout, ldd, dh, lddh, elu_grad, gw, gb, gcs, part,
+                      defer, s);
 }
 
 }  // namespace ul
