@@ -48,6 +48,7 @@ class DeviceSegment:
         self.boot = torch.zeros(N, **f32)
         self.perm = torch.zeros((max(epochs, 1), rows), dtype=torch.int64, device=dev)
         self.has_tv = False
+        self.slot = "ppo"
         self._raw: dict = {}  # width -> contiguous H2D landing buffer
 
     # ------------------------------------------------------------- loading
@@ -120,5 +121,6 @@ def staging_for(T, N, obs_dim, cobs_dim, act_dim, epochs, slot: str = "ppo") -> 
     ds = _CACHE.get(key)
     if ds is None:
         ds = DeviceSegment(T, N, obs_dim, cobs_dim, act_dim, epochs)
+        ds.slot = slot
         _CACHE[key] = ds
     return ds

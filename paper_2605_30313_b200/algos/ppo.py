@@ -112,10 +112,11 @@ _PLANS: dict = {}
 
 def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
               raw_adv: bool = False) -> _Plan:
+    # one plan (and CUDA graph) per staging slot: the pipeline alternates two
     key = (params.actor.arch, params.critic.arch, ds.rows, ds.ld, cfg.epochs, cfg.minibatches,
            cfg.clip_param, cfg.entropy_coef, cfg.value_loss_coef, cfg.use_clipped_value_loss,
            cfg.max_grad_norm, world, rank, raw_adv, _dist.segment_mode(),
-           _lib.gemm_backend(), torch.cuda.current_device())
+           _lib.gemm_backend(), torch.cuda.current_device(), getattr(ds, "slot", "ppo"))
     plan = _PLANS.get(key)
     if plan is None:
         d = _lib.PpoPlanDesc()
@@ -164,7 +165,8 @@ def _world():
     return _dist.world_info()
 
 
-def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib.PpoResult:
+def launch_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> None:
+    """Enqueue one update (single GPU: one CUDA-graph launch, no host wait)."""
     s = _dev.stream()
     cfgd = plan.desc
     if world == 1:
@@ -178,8 +180,12 @@ def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib
                 _lib.call("ul_ppo_plan_step_grads", plan.h, e, k, s)
                 _dist.all_reduce_sum(red)
                 _lib.call("ul_ppo_plan_step_apply", plan.h, e, k, s)
+
+
+def finish_plan(plan: _Plan, opt: AcOpt) -> _lib.PpoResult:
+    """Read the update's statistics (the step's device->host result)."""
     res = _lib.PpoResult()
-    st = _lib.lib().ul_ppo_plan_finish(plan.h, C.byref(res), s)
+    st = _lib.lib().ul_ppo_plan_finish(plan.h, C.byref(res), _dev.stream())
     opt.actor.t = int(res.t_actor)
     opt.critic.t = int(res.t_critic)
     if st != 0:
@@ -187,7 +193,12 @@ def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib
     return res
 
 
-def _epochs_on_device(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False) -> UpdateStats:
+def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib.PpoResult:
+    launch_plan(plan, params, opt, world, red)
+    return finish_plan(plan, opt)
+
+
+def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False):
     world, rank = _world()
     fill_permutations(ds, rng, cfg.epochs)
     plan = _plan_for(params, cfg, ds, world, rank, raw_adv)
@@ -195,9 +206,18 @@ def _epochs_on_device(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False) 
     if world > 1:
         red = _dist.reduce_buffer(plan.red_len)
     plan.bind(ds, adv, ret, oldv, params, opt, red)
-    res = run_plan(plan, params, opt, world, red)
+    launch_plan(plan, params, opt, world, red)
+    return plan
+
+
+def _stats(res, opt) -> UpdateStats:
     return UpdateStats(policy_loss=res.policy_loss, value_loss=res.value_loss,
                        entropy=res.entropy, kl=res.kl, lr=opt.lr, grad_norm=res.grad_norm)
+
+
+def _epochs_on_device(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False) -> UpdateStats:
+    plan = _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv)
+    return _stats(finish_plan(plan, opt), opt)
 
 
 def _check_dims(segment, params: AcParams):
@@ -306,6 +326,71 @@ def ppo_update_resident(ds, params: AcParams, opt: AcOpt, cfg: PpoConfig, rng) -
     learner half of R:runtime/ppo_runner.py:95-102 without the H2D)."""
     gae_into(ds, cfg.gamma, cfg.lam)
     return _epochs_on_device(ds, ds.adv, ds.ret, ds.values, params, opt, cfg, rng)
+
+
+class PpoPipeline:
+    """The collector-to-learner transfer path of the north star: a
+    double-buffered pinned-host -> HBM staging ring.  Segment i+1 is copied
+    (and re-pitched) on a side stream into the idle slot while the update on
+    segment i runs; each slot owns its own bound update plan / CUDA graph.
+    GAE runs on the device (K1) inside the update, so only the raw rollout
+    fields cross PCIe.  Equivalent to ``gae`` + ``ppo_update`` per segment
+    (R:runtime/ppo_runner.py:95-102), pipelined.
+
+        pipe = PpoPipeline(params, opt, cfg, rng)
+        pipe.prefetch(seg0)
+        for it in range(iterations):
+            stats = pipe.update(next_segment=seg_next_or_None)
+    """
+
+    def __init__(self, params: AcParams, opt: AcOpt, cfg: PpoConfig, rng):
+        self.params, self.opt, self.cfg, self.rng = params, opt, cfg, rng
+        self.copy = torch.cuda.Stream()
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        self.slots: list = [None, None]
+        self.queue: list = []  # slots holding staged, not yet consumed segments
+        self.next_slot = 0
+
+    def prefetch(self, segment) -> None:
+        """Start the H2D of a segment into the idle slot (returns at once when
+        the host arrays are pinned)."""
+        if len(self.queue) >= 2:
+            raise RuntimeError("both staging slots hold segments not yet consumed")
+        od, cd, ad = _check_dims(segment, self.params)
+        T, N = segment.horizon, segment.n_envs
+        if (T * N) % self.cfg.minibatches != 0:
+            raise ValueError(f"minibatches {self.cfg.minibatches} must divide batch size {T * N}")
+        k = self.next_slot
+        self.next_slot ^= 1
+        ds = staging_for(T, N, od, cd, ad, self.cfg.epochs, slot=f"pipe{k}")
+        self.slots[k] = ds
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.free[k])  # the update that last read this slot
+            ds.load(segment, with_advantages=False)
+            self.ready[k].record(self.copy)
+        self.queue.append(k)
+
+    def update(self, next_segment=None) -> UpdateStats:
+        """Run the update on the oldest staged segment; stage `next_segment`
+        meanwhile.  Returns that update's statistics (host)."""
+        if not self.queue:
+            raise RuntimeError("no staged segment: call prefetch() first")
+        k = self.queue.pop(0)
+        ds = self.slots[k]
+        cur = torch.cuda.current_stream()
+        cur.wait_event(self.ready[k])
+        gae_into(ds, self.cfg.gamma, self.cfg.lam)
+        world, _ = _world()
+        if world > 1 and next_segment is not None:
+            self.prefetch(next_segment)  # host-driven DP steps: stage first
+            next_segment = None
+        plan = _launch_epochs(ds, ds.adv, ds.ret, ds.values, self.params, self.opt, self.cfg,
+                              self.rng)
+        self.free[k].record(cur)
+        if next_segment is not None:
+            self.prefetch(next_segment)  # overlaps the update just enqueued
+        return _stats(finish_plan(plan, self.opt), self.opt)
 
 
 def plan_stats(params: AcParams, cfg: PpoConfig, ds) -> dict:

@@ -234,3 +234,45 @@ def test_learners_and_weight_slot():
     stats = appo.drain(ring, 4)
     th.join()
     assert len(stats) == 4 and max(appo.staleness) <= 2 + 1
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_pipeline_matches_serial_updates(prec):
+    """PpoPipeline (double-buffered H2D ring, device GAE) == host gae +
+    ppo_update on the same segments and device permutation stream."""
+    old = P.get_precision()
+    P.set_precision(prec)
+    try:
+        T, N = 8, 512
+        segs = []
+        for sd in (3, 4, 5):
+            segd, actor, critic = _synthetic(T, N, 48, 52, 12, (128, 64), seed=sd)
+            segs.append(A.RolloutSegment(**segd))
+        cfg = A.PpoConfig(epochs=2, minibatches=2)
+        arch_a, arch_c = TN.Arch(48, (128, 64), 12), TN.Arch(52, (128, 64), 1)
+
+        def fresh():
+            p = A.AcParams(TN.ModelParams.from_numpy(arch_a, actor.flat()),
+                           TN.ModelParams.from_numpy(arch_c, critic.flat()))
+            return p, A.AcOpt.for_params(p, cfg.lr)
+
+        p1, o1 = fresh()
+        rng1 = A.DeviceRng(7)
+        serial = []
+        for sg in segs:
+            sg.advantages, sg.returns = A.gae(sg.rewards, sg.values, sg.terminated, sg.truncated,
+                                              sg.bootstrap_value, cfg.gamma, cfg.lam,
+                                              truncation_values=sg.truncation_values)
+            serial.append(A.ppo_update(sg, p1, o1, cfg, rng1))
+        p2, o2 = fresh()
+        pipe = A.PpoPipeline(p2, o2, cfg, A.DeviceRng(7))
+        pipe.prefetch(segs[0])
+        piped = []
+        for i in range(len(segs)):
+            piped.append(pipe.update(next_segment=segs[i + 1] if i + 1 < len(segs) else None))
+        for a, b in zip(serial, piped):
+            assert a.policy_loss == b.policy_loss and a.value_loss == b.value_loss
+        np.testing.assert_array_equal(p1.actor.flat(), p2.actor.flat())
+        np.testing.assert_array_equal(p1.critic.flat(), p2.critic.flat())
+    finally:
+        P.set_precision(old)
