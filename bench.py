@@ -330,7 +330,7 @@ def run_ours(args):
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("sgemm_kernel_bytes_per_update")
+        traffic = json.loads(tf.read_text()).get("tc_gemm_dram_bytes_per_update")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -355,7 +355,9 @@ def run_ours(args):
                 "serial_gae_ppo_update_ms": serial_ms},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_sus,
                      "unit": "TFLOP/s", "frac": gemm_tflops / bf16_sus, "traffic": traffic,
-                     "kernel": "MLP GEMMs of one update (tc_gemm_kernel + sgemm_kernel heads)",
+                     "kernel": "MLP phase of one update: tcgen05 GEMMs (tc_gemm_kernel) + "
+                               "skinny head kernels + split-K reductions; traffic = ncu DRAM "
+                               "bytes of the tc_gemm launches per update (profiles/)",
                      "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
                      "algorithmic_flops_per_update": counts["gemm_flops_per_update"],
                      "phase_ms_per_update": prof},

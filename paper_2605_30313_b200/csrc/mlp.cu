@@ -41,8 +41,9 @@ struct ReduceTable {
   ReduceJob r[kMaxReduceJobs];  // blockIdx.y selects the job
 };
 
-__global__ void __launch_bounds__(1024) reduce_dw_kernel(ReduceTable tab) {
-  __shared__ float4 sm[32][32];
+template <int W>  // warps per block: 8 for split-K depths (<= 64), 32 for deep partial sets
+__global__ void __launch_bounds__(W * 32) reduce_dw_kernel(ReduceTable tab) {
+  __shared__ float4 sm[W][32];
   const ReduceJob& q = tab.r[blockIdx.y];
   const float* __restrict__ ws = q.src;
   const int splits = q.nz;
@@ -53,17 +54,17 @@ __global__ void __launch_bounds__(1024) reduce_dw_kernel(ReduceTable tab) {
   pdl_trigger();
   pdl_wait();
   if ((int64_t)blockIdx.x * 128 >= len) return;  // block-uniform
-  // 32 warps over the partials (z = w, w + 32, ...), 8 loads in flight each:
-  // a 384-deep head reduction is two round trips, a 35-split dW one
+  // W warps over the partials (z = w, w + W, ...), 8 loads in flight each:
+  // one round trip for a 35-split dW (W = 8) or a 384-deep head set (W = 32)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t j = ((int64_t)blockIdx.x * 32 + lane) * 4;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (j < len) {
-    for (int z0 = w; z0 < splits; z0 += 256) {
+    for (int z0 = w; z0 < splits; z0 += 8 * W) {
       float4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int z = z0 + 32 * u;
+        const int z = z0 + W * u;
         v[u] = z < splits ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * len + j))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(1024) reduce_dw_kernel(ReduceTable tab) {
   __syncthreads();
   if (w == 0 && j < len) {
     float4 t = sm[0][lane];
-    for (int k = 1; k < 32; ++k) {
+    for (int k = 1; k < W; ++k) {
       const float4 q4 = sm[k][lane];
       t.x += q4.x;
       t.y += q4.y;
@@ -383,16 +384,27 @@ struct Lanes {
 
 // one launch for up to kMaxReduceJobs fixed-order partial reductions
 int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
-  if (nj == 0) return UL_OK;
-  ReduceTable tab{};
-  int64_t bx = 1;
-  for (int q = 0; q < nj; ++q) {
-    tab.r[q] = jobs[q];
-    const int64_t b = ceil_div(jobs[q].len, 128);
-    bx = b > bx ? b : bx;
+  // shallow (split-K) and deep (per-block / per-CTA partial) jobs take the
+  // 8- and 32-warp variants
+  for (int deep = 0; deep < 2; ++deep) {
+    ReduceTable tab{};
+    int64_t bx = 1;
+    int n = 0;
+    for (int q = 0; q < nj; ++q) {
+      if ((jobs[q].nz > 64) != (deep == 1)) continue;
+      tab.r[n++] = jobs[q];
+      const int64_t b = ceil_div(jobs[q].len, 128);
+      bx = b > bx ? b : bx;
+    }
+    if (n == 0) continue;
+    if (deep)
+      UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel<32>, dim3((unsigned)bx, (unsigned)n),
+                        dim3(1024), 0, s, tab));
+    else
+      UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel<8>, dim3((unsigned)bx, (unsigned)n),
+                        dim3(256), 0, s, tab));
   }
-  return launch_pdl("reduce_dw_kernel", reduce_dw_kernel, dim3((unsigned)bx, (unsigned)nj),
-                    dim3(1024), 0, s, tab);
+  return UL_OK;
 }
 
 // run 1 or 2 independent GEMMs; tensor-core pairs share a launch
