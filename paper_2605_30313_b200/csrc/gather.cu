@@ -29,6 +29,7 @@ struct GatherTable {
   int64_t ones[kMaxDesc];        // byte offset of a float set to 1.0 in each row, -1 none
   int cvt[kMaxDesc];             // 1: fp32 source rows -> bf16 destination rows
   int lpr_shift[kMaxDesc];       // log2(lanes per row)
+  int blk0[kMaxDesc + 1];        // desc d owns blocks [blk0[d], blk0[d+1]) of the 1-D grid
   int ndesc;
 };
 
@@ -41,6 +42,20 @@ struct Vec<8> { using T = uint2; };
 template <>
 struct Vec<4> { using T = uint32_t; };
 
+// float 1.0 into 4-byte lane e of a register vector (selects; a dynamic
+// index would push the vector to local memory)
+__device__ __forceinline__ void set_one(uint4& v, int e) {
+  v.x = e == 0 ? 0x3f800000u : v.x;
+  v.y = e == 1 ? 0x3f800000u : v.y;
+  v.z = e == 2 ? 0x3f800000u : v.z;
+  v.w = e == 3 ? 0x3f800000u : v.w;
+}
+__device__ __forceinline__ void set_one(uint2& v, int e) {
+  v.x = e == 0 ? 0x3f800000u : v.x;
+  v.y = e == 1 ? 0x3f800000u : v.y;
+}
+__device__ __forceinline__ void set_one(uint32_t& v, int) { v = 0x3f800000u; }
+
 // One desc's rows.  A warp owns 32 / lpr rows at a time, lpr = a power of two
 // >= units per row (<= 32) lanes per row: lanes stream contiguous 16/8/4-byte
 // units of a row, no per-unit division, and R row groups are in flight per
@@ -51,14 +66,14 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
                                           int64_t sst, int64_t dstr, int upr, int lpr_shift,
                                           const int64_t* __restrict__ idx, int64_t n,
                                           int64_t modulo, int64_t lo, int64_t hi, int* err,
-                                          int64_t ones) {
+                                          int64_t ones, int blk, int nblk) {
   using T = typename Vec<U>::T;
   constexpr int R = 4;
   const int lane = threadIdx.x & 31;
   const int lpr = 1 << lpr_shift, rpw = 32 >> lpr_shift;
   const int sub = lane & (lpr - 1);
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t gw = ((int64_t)blk * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)nblk * blockDim.x) >> 5;
   const int64_t step = nw * rpw;  // rows between a warp's consecutive row groups
   const int ones_u = ones >= 0 ? (int)(ones / U) : -1;
   const int ones_e = ones >= 0 ? (int)((ones % U) / 4) : 0;
@@ -101,7 +116,12 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
           if (CVT) {
             float4 f4 = *reinterpret_cast<float4*>(&v[k][e]);
             float f[4] = {f4.x, f4.y, f4.z, f4.w};
-            if (u == ones_u) f[ones_e] = 1.f;
+            if (u == ones_u) {  // (selects, no dynamically indexed local array)
+              f[0] = ones_e == 0 ? 1.f : f[0];
+              f[1] = ones_e == 1 ? 1.f : f[1];
+              f[2] = ones_e == 2 ? 1.f : f[2];
+              f[3] = ones_e == 3 ? 1.f : f[3];
+            }
             __nv_bfloat162 a = __floats2bfloat162_rn(f[0], f[1]);
             __nv_bfloat162 b = __floats2bfloat162_rn(f[2], f[3]);
             uint2 o;
@@ -109,7 +129,7 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
             o.y = *reinterpret_cast<uint32_t*>(&b);
             reinterpret_cast<uint2*>(dp[k])[u] = o;
           } else {
-            if (u == ones_u) reinterpret_cast<float*>(&v[k][e])[ones_e] = 1.f;
+            if (u == ones_u) set_one(v[k][e], ones_e);
             reinterpret_cast<T*>(dp[k])[u] = v[k][e];
           }
         }
@@ -124,26 +144,28 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t,
                                                      int* err) {
   pdl_trigger();
   pdl_wait();
-  const int d = blockIdx.y;
-  if (d >= t.ndesc) return;
+  // this block's desc: blocks are apportioned to descs by their row work
+  int d = 0;
+  while (d + 1 < t.ndesc && (int)blockIdx.x >= t.blk0[d + 1]) ++d;
+  const int blk = (int)blockIdx.x - t.blk0[d], nblk = t.blk0[d + 1] - t.blk0[d];
   const int upr = (int)t.units[d], sh = t.lpr_shift[d];
   if (t.cvt[d]) {
     copy_rows<16, true>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
-                        modulo, lo, hi, err, t.ones[d]);
+                        modulo, lo, hi, err, t.ones[d], blk, nblk);
     return;
   }
   switch (t.unit[d]) {
     case 16:
       copy_rows<16, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
-                           modulo, lo, hi, err, t.ones[d]);
+                           modulo, lo, hi, err, t.ones[d], blk, nblk);
       break;
     case 8:
       copy_rows<8, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
-                          modulo, lo, hi, err, t.ones[d]);
+                          modulo, lo, hi, err, t.ones[d], blk, nblk);
       break;
     default:
       copy_rows<4, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
-                          modulo, lo, hi, err, t.ones[d]);
+                          modulo, lo, hi, err, t.ones[d], blk, nblk);
   }
 }
 
@@ -204,7 +226,7 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
   if (n == 0) return UL_OK;
   GatherTable t{};
   t.ndesc = ndesc;
-  int64_t max_units = 1;
+  int nb_total = 0;
   for (int d = 0; d < ndesc; ++d) {
     const int c = cvt ? cvt[d] : 0;
     int u;
@@ -231,13 +253,15 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
     int sh = 0;
     while (sh < 5 && (1 << sh) < t.units[d]) ++sh;
     t.lpr_shift[d] = sh;
-    // warps needed for R = 4 row groups in flight each
+    // warps needed for R = 4 row groups in flight each -> 8-warp blocks
     const int64_t warps = ceil_div(n, (int64_t)(32 >> sh) * 4);
-    max_units = warps > max_units ? warps : max_units;
+    int64_t nb = ceil_div(warps, 8);
+    nb = nb > 4 * kNumSMs ? 4 * kNumSMs : nb;
+    t.blk0[d] = nb_total;
+    nb_total += (int)nb;
   }
-  int64_t blocks = ceil_div(max_units, 8);  // max_units: most warps any desc wants
-  blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
-  return launch_pdl("gather_kernel", gather_kernel, dim3((unsigned)blocks, ndesc), dim3(256), 0,
+  t.blk0[ndesc] = nb_total;
+  return launch_pdl("gather_kernel", gather_kernel, dim3((unsigned)nb_total), dim3(256), 0,
                     stream, t, idx, n, modulo, lo, hi, err);
 }
 }  // namespace ul

@@ -183,6 +183,8 @@ struct TcArgs {
   unsigned long long* trace;  // diagnostics (UL_TC_TRACE): CTA 0 event timestamps, or null
   float* csum;                // per-CTA output column sums [grid][ldcs], or null
   int ldcs;
+  int bres_kt;                // B-resident launches: K tiles of B held in smem
+  int tma_store;              // 1 (default): TMA bulk stores; 0: coalesced st.global (UL_TC_TMASTORE=0)
 };
 
 // trace slots: [0] entry, [1] setup done, [2..33] producer k-tile issue,
@@ -206,11 +208,13 @@ using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu ||
 
 // [stage ring][16 epilogue staging boxes][barriers][bias x 2]; as many stages
 // as fit the 227 KB of dynamic shared memory (at most 6)
-template <int BN, bool PAIR, int OB /* output element bytes */, int EPI>
+template <int BN, bool PAIR, int OB /* output element bytes */, int EPI, bool BRES = false>
 struct Smem {
   static constexpr int kABytes = BM * 128;
   static constexpr int kBBytes = (PAIR ? BN / 2 : BN) * 128;  // this CTA's share of B
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  // B-resident: the ring streams A only; B's K tiles sit in smem for the
+  // whole kernel (runtime-sized region after the ring)
+  static constexpr int kStageBytes = kABytes + (BRES ? 0 : kBBytes);
   static constexpr int kStagingBytes = kEpiWarps * 32 * 32 * OB;
   // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
   static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
@@ -218,8 +222,9 @@ struct Smem {
       1024 /*align*/ + 512 /*barriers*/ + 2 * BN * 4 /*bias*/ + kCsumBytes;
   static constexpr int kBudget = 232448;
   static constexpr int kStagesFit = (kBudget - kStagingBytes - kFixed) / kStageBytes;
-  static constexpr int kStages = kStagesFit > 6 ? 6 : kStagesFit;
-  static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + kFixed;
+  static constexpr int kStages = BRES ? 3 : (kStagesFit > 6 ? 6 : kStagesFit);
+  static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + kFixed;  // + B region
+  static constexpr int kBresMax = kBudget - kBytes;
 };
 
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
@@ -281,14 +286,19 @@ struct TcMaps {
   CUtensorMap a, b, c, x;
 };
 
-template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
+// BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
+// each CTA owns one N tile (CTA index mod nt) and walks M tiles; B's K tiles
+// are loaded once, so only A streams -- a third of the smem fill traffic of
+// the 48 KB/stage ring for the forward and dX GEMMs (K = 128..256).
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR, bool BRES>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_kernel(const __grid_constant__ TcMaps m0_, const __grid_constant__ TcMaps m1_,
                    const __grid_constant__ TcArgs p0_, const __grid_constant__ TcArgs p1_,
                    int ng0, int ngroups) {
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
-  using S = Smem<BN, PAIR, (int)sizeof(TO), EPI>;
+  using S = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
+  static_assert(!(BRES && PAIR), "B-resident launches are single-CTA");
   constexpr bool kOutBf16 = sizeof(TO) == 2;
   constexpr int CS = PAIR ? 2 : 1;
   constexpr int BNL = BN / CS;  // B rows (N) this CTA loads
@@ -301,13 +311,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full =
-      reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes + S::kStagingBytes);
+  const uint32_t bres_bytes = BRES ? (uint32_t)p0_.bres_kt * S::kBBytes : 0u;
+  uint8_t* sbres = smem + kStages * S::kStageBytes;  // B-resident K tiles
+  uint8_t* staging = sbres + bres_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + S::kStagingBytes);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;  // [2]
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint64_t* aux_bar = acc_empty + 2;     // [kEpiWarps]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_bar + kEpiWarps);
+  uint64_t* bres_bar = aux_bar + kEpiWarps;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 2);  // keeps sbias 16 B aligned
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
@@ -328,6 +341,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_init(&acc_empty[b], CS * kEpiWarps);  // both CTAs' epilogue warps (leader)
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&aux_bar[w], 1);
+    mbar_init(bres_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -371,10 +385,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const TcArgs& P = T.pr ? p1_ : p0_;
     const int tl = T.pr ? t - ng0 : t;
     const int mg = (P.mt + CS - 1) / CS;
-    T.z = tl / (mg * P.nt);
-    const int r = tl - T.z * mg * P.nt;
-    T.n0 = (r / mg) * BN;
-    T.m0 = ((r % mg) * CS + (int)crank) * BM;
+    if (BRES) {  // N fastest: the grid is a multiple of nt, so a CTA keeps one N tile
+      T.z = 0;
+      T.n0 = (tl % P.nt) * BN;
+      T.m0 = (tl / P.nt) * BM;
+    } else {
+      T.z = tl / (mg * P.nt);
+      const int r = tl - T.z * mg * P.nt;
+      T.n0 = (r / mg) * BN;
+      T.m0 = ((r % mg) * CS + (int)crank) * BM;
+    }
     const int kb = T.z * P.k_per_split;
     const int ke = min(P.K, kb + P.k_per_split);
     T.kt_n = ke > kb ? (ke - kb + BK - 1) / BK : 0;
@@ -385,6 +405,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int it = 0;
+      if (BRES && cl < ngroups) {
+        // this CTA's N tile of B, all K tiles, once
+        const Tile T0 = tile_of(cl);
+        mbar_expect_tx(bres_bar, bres_bytes);
+        for (int kt = 0; kt < T0.kt_n; ++kt) {
+          uint8_t* sb = sbres + kt * S::kBBytes;
+          if (B_MN) {
+#pragma unroll
+            for (int c = 0; c < BN / O::kChunk; ++c)
+              tma_load_2d(sb + c * kChunkBytes, &m0_.b, bres_bar, T0.n0 + O::kChunk * c,
+                          kt * BK);
+          } else {
+            tma_load_2d(sb, &m0_.b, bres_bar, kt * BK, T0.n0);
+          }
+        }
+      }
       for (int t = cl; t < ngroups; t += ncl) {
         const Tile T = tile_of(t);
         const int m0 = T.m0, n0 = T.n0, kt_n = T.kt_n;
@@ -417,6 +453,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             } else {
               tma_load_2d_pair(sb, tB, fb, k0, nb0);
             }
+          } else if (BRES) {
+            mbar_expect_tx(&full[s], S::kStageBytes);  // A only
+            tma_load_2d(sa, tA, &full[s], k0, m0);
           } else {
             mbar_expect_tx(&full[s], S::kStageBytes);
             if (A_MN) {
@@ -446,6 +485,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((CS * BM) >> 4) << 24);
     if (lane == 0 && leader) {
       int it = 0, local = 0;
+      if (BRES && cl < ngroups) mbar_wait(bres_bar, 0);
       for (int t = cl; t < ngroups; t += ncl, ++local) {
         const int kt_n = tile_of(t).kt_n;
         const int b = local & 1;
@@ -458,7 +498,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (it < 32) trace_at(p0_.trace, 34 + it);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = su32(smem + s * S::kStageBytes);
-          const uint32_t b_base = a_base + S::kABytes;
+          const uint32_t b_base =
+              BRES ? su32(sbres + kt * S::kBBytes) : a_base + S::kABytes;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             // K-major: 8-row x 128 B swizzle atoms (SBO 1024), one UMMA K step
@@ -509,7 +550,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int n = lane; n < kCsumMaxN; n += 32)
         if ((n % BN) / kSlice == slice) csum_s[quarter * kCsumMaxN + n] = 0.f;
     }
-    uint8_t* stg = smem + kStages * S::kStageBytes + ew * kBoxBytes;
+    uint8_t* stg = staging + ew * kBoxBytes;
     uint64_t* abar = aux_bar + ew;
     uint32_t aphase = 0;
     int local = 0;
@@ -612,16 +653,58 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                       pack_bf16(v[8 * q + 4], v[8 * q + 5]),
                                       pack_bf16(v[8 * q + 6], v[8 * q + 7]));
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
-          // 3-D map [splits][M][N]: a box never spills into the next split's rows
-          asm volatile(
-              "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-                  tC),
-              "r"(su32(stg)), "r"(n0 + c0), "r"(crow), "r"(z)
-              : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (p.tma_store) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
+            // 3-D map [splits][M][N]: a box never spills into the next split's rows
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                    tC),
+                "r"(su32(stg)), "r"(n0 + c0), "r"(crow), "r"(z)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else {
+          // coalesced 16-byte stores straight from the staging tile: the warp
+          // never waits on an async store engine shared with the operand loads
+          __syncwarp();
+          const int rows_ok = p.M - crow;  // rows of this warp's box inside M
+          TO* cb = reinterpret_cast<TO*>(p.C) + ((int64_t)z * p.M + crow) * p.ldc + n0 + c0;
+          if constexpr (!kOutBf16) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = i * 4 + (lane >> 3), g = lane & 7;
+              if (r < rows_ok) {
+                const float4 val = reinterpret_cast<const float4*>(stg + r * 128)[g ^ (r & 7)];
+                float* dst = reinterpret_cast<float*>(cb) + (int64_t)r * p.ldc + 4 * g;
+                const int col = n0 + c0 + 4 * g;
+                if (col + 4 <= p.N) {
+                  *reinterpret_cast<float4*>(dst) = val;
+                } else {
+                  const float e4[4] = {val.x, val.y, val.z, val.w};
+                  for (int e = 0; e < 4 && col + e < p.N; ++e) dst[e] = e4[e];
+                }
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = i * 8 + (lane >> 2), g = lane & 3;
+              if (r < rows_ok) {
+                const uint4 val = reinterpret_cast<const uint4*>(stg + r * 64)[g ^ ((r >> 1) & 3)];
+                __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(cb) + (int64_t)r * p.ldc + 8 * g;
+                const int col = n0 + c0 + 8 * g;
+                if (col + 8 <= p.N) {
+                  *reinterpret_cast<uint4*>(dst) = val;
+                } else {
+                  const __nv_bfloat16* e8 = reinterpret_cast<const __nv_bfloat16*>(&val);
+                  for (int e = 0; e < 8 && col + e < p.N; ++e) dst[e] = e8[e];
+                }
+              }
+            }
+          }
+          __syncwarp();  // staging reads done before the next chunk reuses it
         }
         if (csum_on && T.pr == cs_pr) {
           // butterfly reduce-scatter over the warp's 32 rows: afterwards lane
@@ -660,7 +743,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
       }
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // the staging smem must outlive the stores' reads; their global writes
+    // complete with the grid (kernel boundary / the dependent launch's
+    // griddepcontrol.wait), so the CTA need not wait for them
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -752,13 +838,22 @@ inline unsigned long long* trace_buffer() {
   return buf;
 }
 
+inline int tma_store_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_TC_TMASTORE");
+    on = e ? atoi(e) != 0 : 1;  // measured: TMA stores beat direct stores
+  }
+  return on;
+}
+
 // one problem's tensor maps + kernel arguments (Prob: M/N/K split already fixed)
 struct Prob {
   const GemmDesc* d;
   int zs, kps, ones_col;
 };
 
-template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR, bool BRES>
 int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
@@ -782,29 +877,29 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   *a = TcArgs{(int)d.M, (int)d.N, (int)d.K, q.kps, mt, nt, q.zs, d.C, d.ldc, d.bias,
               q.ones_col, trace_buffer(),
               EPI == kEpiEluGrad && d.N <= kCsumMaxN ? d.csum_part : nullptr,
-              (int)ceil_div(d.N, 4) * 4};
+              (int)ceil_div(d.N, 4) * 4, BRES ? (int)ceil_div(d.K, O::BK) : 0, tma_store_on()};
   *ngroups = (int)ceil_div(mt, CS) * nt * q.zs;
   return UL_OK;
 }
 
-template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR>
+template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR, bool BRES = false>
 int launch(const Prob* q, int np, cudaStream_t s) {
   using TO = OutT<TI, EPI>;
-  using SM = Smem<BN, PAIR, (int)sizeof(TO), EPI>;
+  using SM = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
   constexpr int CS = PAIR ? 2 : 1;
   TcMaps m[2];
   TcArgs a[2];
   int ng[2] = {0, 0};
   for (int i = 0; i < np; ++i)
-    UL_TRY((make_problem<TI, A_MN, B_MN, EPI, BN, PAIR>(q[i], &m[i], &a[i], &ng[i])));
+    UL_TRY((make_problem<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>(q[i], &m[i], &a[i], &ng[i])));
   if (np == 1) {
     m[1] = m[0];
     a[1] = a[0];
   }
-  auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR>;
+  auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
-  cfg.dynamicSmemBytes = SM::kBytes;
+  cfg.dynamicSmemBytes = SM::kBytes + (BRES ? (size_t)a[0].bres_kt * SM::kBBytes : 0);
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -820,7 +915,8 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   // queue a second wave behind the first)
   static int max_clusters = 0;
   if (max_clusters == 0) {
-    UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kBytes));
+    UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 BRES ? SM::kBudget : SM::kBytes));
     int n = kNumSMs / CS;
     if (CS > 1) {
       cfg.gridDim = dim3((unsigned)(n * CS));
@@ -832,7 +928,8 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     max_clusters = n;
   }
   const int total = ng[0] + ng[1];
-  const int grid = (total < max_clusters ? total : max_clusters) * CS;
+  int grid = (total < max_clusters ? total : max_clusters) * CS;
+  if (BRES) grid = grid / a[0].nt * a[0].nt;  // every CTA keeps one N tile
   cfg.gridDim = dim3((unsigned)grid);
   for (int i = 0; i < np; ++i)
     if (q[i].d->csum_nz) *q[i].d->csum_nz = grid;
@@ -858,8 +955,22 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   // single CTAs for bf16 (measured faster end to end on the cfg2 update)
   const bool want = pair_ok == -2 ? sizeof(TI) == 4 : pair_ok != 0;
   const bool pair = want && ceil_div(d.M, BM) >= 2;
-#define UL_TC_BN(AMN, BMN, EPI, BN)                                        \
-  if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(q, np, s); \
+  // B resident (A streamed alone) when one problem's whole N tile of B fits
+  // the smem left over by the 3-stage A ring, and there is no split-K
+  static int bres_ok = -1;
+  if (bres_ok < 0) {
+    const char* e = getenv("UL_TC_BRES");
+    bres_ok = e ? atoi(e) != 0 : 1;
+  }
+  const int64_t bk = sizeof(TI) == 2 ? 64 : 32;
+  const int64_t bres_bytes = ceil_div(d.K, bk) * (int64_t)bn * 128;
+  const bool bres_base = bres_ok && np == 1 && !amn && q[0].zs == 1 &&
+                         ceil_div(d.N, bn) <= kNumSMs && (sizeof(TI) == 2 || !pair);
+#define UL_TC_BN(AMN, BMN, EPI, BN)                                                          \
+  if (!AMN && bres_base &&                                                                  \
+      bres_bytes <= Smem<BN, false, (int)sizeof(OutT<TI, EPI>), EPI, true>::kBresMax)       \
+    return launch<TI, AMN, BMN, EPI, BN, false, true>(q, np, s);                            \
+  if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(q, np, s);                           \
   return launch<TI, AMN, BMN, EPI, BN, false>(q, np, s);
 #define UL_TC_CASE(AMN, BMN, EPI)                 \
   if (amn == AMN && bmn == BMN && d.epi == EPI) { \
