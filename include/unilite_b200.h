@@ -320,7 +320,9 @@ typedef struct ul_sac_plan_desc {
   int64_t batch;
   int32_t obs_dim, act_dim;
   double gamma, tau, target_entropy, max_grad_norm;
-  int32_t gemm_backend, pad0;
+  int32_t gemm_backend;
+  int32_t world_size; /* data-parallel ranks: `batch` is this rank's share, losses
+                       * and gradients are scaled by batch * world_size (0 = 1) */
 } ul_sac_plan_desc;
 
 typedef struct ul_sac_bindings {
@@ -328,6 +330,10 @@ typedef struct ul_sac_bindings {
   float *q1, *q1_m, *q1_v;
   float *q2, *q2_m, *q2_v;
   float *q1t, *q2t;
+  /* optional caller-owned all-reduce buffers (NULL = plan-owned):
+   * critic_red [2*Pq + 4] = [g_q1 | g_q2 | critic loss part], actor_red
+   * [Pa + 4] = [g_a | actor loss part | sum log pi] */
+  float *critic_red, *actor_red;
 } ul_sac_bindings;
 
 /* sac_update (R:algos/sac.py:139-178) as a native plan.  Batches come as
@@ -347,6 +353,17 @@ int ul_sac_plan_begin(void* plan, const ul_sac_ctl* host_ctl, const double* lrs,
 int ul_sac_plan_noise_ptr(void* plan, float** eps);
 int ul_sac_plan_device_noise(void* plan, uint64_t key, uint64_t counter, void* stream);
 int ul_sac_plan_update(void* plan, int do_actor, void* stream);
+/* The same update split at its two data-parallel exchange points (SURVEY
+ * 8(e)): critic_grads -> all-reduce(critic buffer) -> critic_apply ->
+ * [actor_grads -> all-reduce(actor buffer) -> actor_apply] -> polyak.
+ * ul_sac_plan_update == the sequence without exchanges. */
+int ul_sac_plan_reduce_buffers(void* plan, float** critic, int64_t* n_critic, float** actor,
+                               int64_t* n_actor);
+int ul_sac_plan_critic_grads(void* plan, void* stream);
+int ul_sac_plan_critic_apply(void* plan, void* stream);
+int ul_sac_plan_actor_grads(void* plan, void* stream);
+int ul_sac_plan_actor_apply(void* plan, void* stream);
+int ul_sac_plan_polyak(void* plan, void* stream);
 /* D2H of the control records (+ sync): ts = step counters (actor, q1, q2) */
 int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, void* stream);
 

@@ -9,7 +9,22 @@ clip + Adam, so parameters stay bit-identical across ranks.
 
 from __future__ import annotations
 
+import threading
+
 import torch
+
+# Test hook: emulate one rank of a data-parallel group inside a thread (the
+# all-reduce becomes a caller-provided function).  Lets a single-GPU test run
+# two ranks' learner code concurrently against the real kernels.
+_LOCAL = threading.local()
+
+
+def emulate_rank(world: int, rank: int, reducer) -> None:
+    _LOCAL.emu = (world, rank, reducer)
+
+
+def clear_emulation() -> None:
+    _LOCAL.emu = None
 
 
 # "replicated": every rank holds the full segment and takes a 1/G slice of each
@@ -32,6 +47,9 @@ def segment_mode() -> str:
 def world_info() -> tuple[int, int]:
     import torch.distributed as dist
 
+    emu = getattr(_LOCAL, "emu", None)
+    if emu is not None:
+        return emu[0], emu[1]
     if dist.is_available() and dist.is_initialized():
         return dist.get_world_size(), dist.get_rank()
     return 1, 0
@@ -50,7 +68,7 @@ _BUFS: dict = {}
 
 def reduce_buffer(n: int, device=None) -> torch.Tensor:
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-    key = (n, str(dev))
+    key = (n, str(dev), world_info()[1])
     t = _BUFS.get(key)
     if t is None:
         t = torch.zeros(n, dtype=torch.float32, device=dev)
@@ -61,5 +79,9 @@ def reduce_buffer(n: int, device=None) -> torch.Tensor:
 def all_reduce_sum(t: torch.Tensor) -> None:
     import torch.distributed as dist
 
+    emu = getattr(_LOCAL, "emu", None)
+    if emu is not None:
+        emu[2](t)
+        return
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)

@@ -90,12 +90,12 @@ class SacCtl(C.Structure):
 class SacPlanDesc(C.Structure):
     _fields_ = [("actor", NetDesc), ("critic", NetDesc), ("batch", i64), ("obs_dim", i32),
                 ("act_dim", i32), ("gamma", f64), ("tau", f64), ("target_entropy", f64),
-                ("max_grad_norm", f64), ("gemm_backend", i32), ("pad0", i32)]
+                ("max_grad_norm", f64), ("gemm_backend", i32), ("world_size", i32)]
 
 
 class SacBindings(C.Structure):
     _fields_ = [(n, vp) for n in ("actor", "actor_m", "actor_v", "q1", "q1_m", "q1_v", "q2",
-                                  "q2_m", "q2_v", "q1t", "q2t")]
+                                  "q2_m", "q2_v", "q1t", "q2t", "critic_red", "actor_red")]
 
 
 class PpoResult(C.Structure):
@@ -172,6 +172,13 @@ _PROTOS = {
     "ul_sac_plan_noise_ptr": (C.c_int, [vp, C.POINTER(vp)]),
     "ul_sac_plan_device_noise": (C.c_int, [vp, C.c_uint64, C.c_uint64, vp]),
     "ul_sac_plan_update": (C.c_int, [vp, C.c_int, vp]),
+    "ul_sac_plan_reduce_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64), C.POINTER(vp),
+                                             C.POINTER(i64)]),
+    "ul_sac_plan_critic_grads": (C.c_int, [vp, vp]),
+    "ul_sac_plan_critic_apply": (C.c_int, [vp, vp]),
+    "ul_sac_plan_actor_grads": (C.c_int, [vp, vp]),
+    "ul_sac_plan_actor_apply": (C.c_int, [vp, vp]),
+    "ul_sac_plan_polyak": (C.c_int, [vp, vp]),
     "ul_sac_plan_finish": (C.c_int, [vp, C.POINTER(SacCtl), C.POINTER(i64), vp]),
     "ul_ppo_plan_counts": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64)]),
     "ul_ppo_plan_profile": (C.c_int, [vp, f64, f64, i64, i64, C.POINTER(f64), vp]),

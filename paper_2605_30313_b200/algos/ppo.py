@@ -149,7 +149,7 @@ def fill_permutations(ds, rng, epochs: int) -> None:
             _lib.call("ul_device_permutation", n, rng.next_key(), _dev.ptr(ds.perm[e]),
                       _dev.stream())
         return
-    key = (n, epochs)
+    key = (n, epochs, _dist.world_info()[1])
     host = _PINNED_PERM.get(key)
     if host is None:
         host = _dev.pinned_empty((epochs, n), np.int64)
@@ -238,7 +238,8 @@ def ppo_update(segment, params: AcParams, opt: AcOpt, cfg: PpoConfig, rng) -> Up
     T, N = segment.horizon, segment.n_envs
     if (T * N) % cfg.minibatches != 0:
         raise ValueError(f"minibatches {cfg.minibatches} must divide batch size {T * N}")
-    ds = staging_for(T, N, od, cd, ad, cfg.epochs)
+    world, rank = _world()
+    ds = staging_for(T, N, od, cd, ad, cfg.epochs, slot="ppo" if world == 1 else f"ppo_r{rank}")
     ds.load(segment)
     return _epochs_on_device(ds, ds.adv, ds.ret, ds.values, params, opt, cfg, rng)
 

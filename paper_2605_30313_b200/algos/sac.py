@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from .. import _dev, _lib
+from .. import _dev, _dist, _lib
 from ..errors import DivergenceError
 from ..tensornet.adam import OptState
 from ..tensornet.mlp import ModelParams
@@ -109,7 +109,7 @@ class DeviceRows:
 
 # ------------------------------------------------------------------- plan
 class _SacPlan:
-    def __init__(self, state: SacState, batch: int, cfg: SacConfig):
+    def __init__(self, state: SacState, batch: int, cfg: SacConfig, world: int = 1):
         d = _lib.SacPlanDesc()
         p = state.params
         d.actor = p.actor.arch.desc()
@@ -121,9 +121,18 @@ class _SacPlan:
         d.target_entropy = -cfg.target_entropy_ratio * state.action_dim
         d.max_grad_norm = cfg.max_grad_norm
         d.gemm_backend = _lib.gemm_backend(input_grads=True)
+        d.world_size = world
         h = C.c_void_p()
         _lib.call("ul_sac_plan_create", C.byref(d), C.byref(h))
-        self.h, self.desc, self.batch = h, d, batch
+        self.h, self.desc, self.batch, self.world = h, d, batch, world
+        # data-parallel all-reduce buffers (torch-owned so torch.distributed
+        # can reduce them in place; bound into the plan)
+        self.red = None
+        if world > 1:
+            pq, pa = p.q1.arch.param_count, p.actor.arch.param_count
+            dev = p.actor.buf.device
+            self.red = (torch.zeros(2 * pq + 4, dtype=torch.float32, device=dev),
+                        torch.zeros(pa + 4, dtype=torch.float32, device=dev))
         eps = C.c_void_p()
         _lib.call("ul_sac_plan_noise_ptr", h, C.byref(eps))
         self.eps_ptr = eps.value
@@ -150,6 +159,8 @@ class _SacPlan:
                     actor_v=state.actor_opt.v.buf, q1=p.q1.buf, q1_m=state.q1_opt.m.buf,
                     q1_v=state.q1_opt.v.buf, q2=p.q2.buf, q2_m=state.q2_opt.m.buf,
                     q2_v=state.q2_opt.v.buf, q1t=p.q1_targ.buf, q2t=p.q2_targ.buf)
+        if self.red is not None:
+            vals["critic_red"], vals["actor_red"] = self.red
         for k, v in vals.items():
             setattr(b, k, _dev.ptr(v))
         _lib.call("ul_sac_plan_bind", self.h, C.byref(b))
@@ -159,13 +170,15 @@ class _SacPlan:
 _PLANS: dict = {}
 
 
-def _plan_for(state: SacState, batch: int, cfg: SacConfig) -> _SacPlan:
+def _plan_for(state: SacState, batch: int, cfg: SacConfig, world: int = 1,
+              rank: int = 0) -> _SacPlan:
     p = state.params
     key = (p.actor.arch, p.q1.arch, batch, cfg.gamma, cfg.tau, cfg.target_entropy_ratio,
-           cfg.max_grad_norm, _lib.gemm_backend(input_grads=True), torch.cuda.current_device())
+           cfg.max_grad_norm, _lib.gemm_backend(input_grads=True), torch.cuda.current_device(),
+           world, rank)
     plan = _PLANS.get(key)
     if plan is None:
-        plan = _SacPlan(state, batch, cfg)
+        plan = _SacPlan(state, batch, cfg, world)
         _PLANS[key] = plan
     plan.bind(state)
     return plan
@@ -188,7 +201,7 @@ def _encode_rows(batch: dict, obs_dim: int, act_dim: int) -> np.ndarray:
     """RowCodec.encode (R:replaypath/storage.py:25-35) into a pinned staging row block."""
     n = len(batch["obs"])
     width = 2 * obs_dim + act_dim + 3
-    rows = _pinned(("rows", n, width), (n, width))
+    rows = _pinned(("rows", n, width, _dist.world_info()[1]), (n, width))
     d, a = obs_dim, act_dim
     rows[:, :d] = _dev.to_numpy(batch["obs"])
     rows[:, d:d + a] = _dev.to_numpy(batch["action"])
@@ -221,17 +234,43 @@ def _load_batch(plan: _SacPlan, batch, obs_dim: int, act_dim: int) -> None:
               2**62, None, s)
 
 
-def _fill_noise(plan: _SacPlan, rng, B: int, A: int, do_actor: bool) -> None:
+def _fill_noise(plan: _SacPlan, rng, B: int, A: int, do_actor: bool, world: int = 1,
+                rank: int = 0) -> None:
+    """Noise for this rank's B rows.  Host Generator: the reference's global
+    [B*world, A] draws in the reference order, this rank's row slice; device
+    RNG: the rank folded into the stream key."""
     s = _dev.stream()
     if rng is None or isinstance(rng, DeviceRng):
         rng = rng if rng is not None else DeviceRng(0)
-        _lib.call("ul_sac_plan_device_noise", plan.h, rng.next_key(), rng.counter, s)
+        key = rng.next_key() ^ (0x9E3779B97F4A7C15 * rank & 0xFFFFFFFFFFFFFFFF)
+        _lib.call("ul_sac_plan_device_noise", plan.h, key, rng.counter, s)
         return
-    eps = _pinned(("eps", B, A), (2, B, A))
-    eps[0] = rng.standard_normal((B, A))       # critic_target (R:algos/sac.py:117)
+    eps = _pinned(("eps", B, A, rank), (2, B, A))
+    lo, hi = rank * B, (rank + 1) * B
+    eps[0] = rng.standard_normal((B * world, A))[lo:hi]      # critic_target (R:algos/sac.py:117)
     if do_actor:
-        eps[1] = rng.standard_normal((B, A))   # actor step (R:algos/sac.py:237)
+        eps[1] = rng.standard_normal((B * world, A))[lo:hi]  # actor step (R:algos/sac.py:237)
     _lib.call("ul_memcpy_async", plan.eps_ptr, eps.ctypes.data, eps.nbytes, s)
+
+
+def _shard_batch(batch, world: int, rank: int):
+    """This rank's contiguous 1/world slice of a global batch (SURVEY.md 8(e):
+    the host draws the global indices, each rank gathers its rows)."""
+    if world == 1:
+        return batch
+    if isinstance(batch, DeviceRows):
+        if batch.n % world:
+            raise ValueError("world_size must divide the SAC batch")
+        per = batch.n // world
+        idx = batch.idx[rank * per:(rank + 1) * per] if batch.idx is not None else None
+        if idx is None:
+            raise ValueError("data-parallel SAC needs an index vector for DeviceRows batches")
+        return DeviceRows(batch.ring, batch.pitch, idx, per, batch.modulo, batch.lo, batch.hi)
+    n = len(batch["obs"])
+    if n % world:
+        raise ValueError("world_size must divide the SAC batch")
+    per = n // world
+    return {k: v[rank * per:(rank + 1) * per] for k, v in batch.items()}
 
 
 def sac_update(batch, state: SacState, cfg: SacConfig, rng) -> UpdateStats:
@@ -240,12 +279,15 @@ def sac_update(batch, state: SacState, cfg: SacConfig, rng) -> UpdateStats:
     n = batch.n if isinstance(batch, DeviceRows) else len(batch["obs"])
     if n < 2:
         raise ValueError("sac_update needs a batch of at least 2 rows")
+    world, rank = _dist.world_info()
+    batch = _shard_batch(batch, world, rank)
+    n //= world
     p = state.params
     od, ad = p.actor.arch.input_dim, p.actor.arch.output_dim
-    plan = _plan_for(state, n, cfg)
+    plan = _plan_for(state, n, cfg, world, rank)
     _load_batch(plan, batch, od, ad)
     do_actor = (state.update_count + 1) % cfg.policy_frequency == 0
-    _fill_noise(plan, rng, n, ad, do_actor)
+    _fill_noise(plan, rng, n, ad, do_actor, world, rank)
     ctl = _lib.SacCtl()
     ctl.log_alpha = p.log_alpha
     ctl.a_m, ctl.a_v, ctl.a_t = state.alpha_opt.m, state.alpha_opt.v, float(state.alpha_opt.t)
@@ -255,7 +297,19 @@ def sac_update(batch, state: SacState, cfg: SacConfig, rng) -> UpdateStats:
     s = _dev.stream()
     _lib.call("ul_sac_plan_begin", plan.h, C.byref(ctl), lrs, ts, s)
     alpha_before = float(np.exp(p.log_alpha))
-    _lib.call("ul_sac_plan_update", plan.h, int(do_actor), s)
+    if world == 1:
+        _lib.call("ul_sac_plan_update", plan.h, int(do_actor), s)
+    else:
+        # the two exchange points of SURVEY.md 8(e): critic grads (+ loss), then
+        # actor grads (+ loss, sum log pi) on actor steps; Polyak stays local
+        _lib.call("ul_sac_plan_critic_grads", plan.h, s)
+        _dist.all_reduce_sum(plan.red[0])
+        _lib.call("ul_sac_plan_critic_apply", plan.h, s)
+        if do_actor:
+            _lib.call("ul_sac_plan_actor_grads", plan.h, s)
+            _dist.all_reduce_sum(plan.red[1])
+            _lib.call("ul_sac_plan_actor_apply", plan.h, s)
+        _lib.call("ul_sac_plan_polyak", plan.h, s)
     out = _lib.SacCtl()
     st = _lib.lib().ul_sac_plan_finish(plan.h, C.byref(out), ts, s)
     state.actor_opt.t, state.q1_opt.t, state.q2_opt.t = int(ts[0]), int(ts[1]), int(ts[2])

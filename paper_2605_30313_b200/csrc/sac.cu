@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(256) critic_head_kernel(const float* __restric
                                                           const double* __restrict__ y, int64_t n,
                                                           double inv_n, float* __restrict__ dq1,
                                                           float* __restrict__ dq2, double* part,
-                                                          unsigned int* ticket, ul_sac_ctl* ctl) {
+                                                          unsigned int* ticket, ul_sac_ctl* ctl,
+                                                          float* loss_slot) {
   __shared__ double scratch[32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double l1 = 0.0, l2 = 0.0;
@@ -100,6 +101,8 @@ __global__ void __launch_bounds__(256) critic_head_kernel(const float* __restric
       s2 += part[2 * b + 1];
     }
     ctl->critic_loss = s1 * inv_n + s2 * inv_n;
+    // data-parallel: this rank's share, all-reduced with the critic gradients
+    if (loss_slot) loss_slot[0] = (float)ctl->critic_loss;
   }
 }
 
@@ -107,9 +110,10 @@ __global__ void __launch_bounds__(256) critic_head_kernel(const float* __restric
 __global__ void __launch_bounds__(256) pick_head_kernel(const float* __restrict__ q1,
                                                         const float* __restrict__ q2,
                                                         const float* __restrict__ logp, int64_t n,
-                                                        float* __restrict__ d1,
+                                                        double n_global, float* __restrict__ d1,
                                                         float* __restrict__ d2, double* part,
-                                                        unsigned int* ticket, ul_sac_ctl* ctl) {
+                                                        unsigned int* ticket, ul_sac_ctl* ctl,
+                                                        float* slots) {
   __shared__ double scratch[32];
   const double alpha = exp(ctl->log_alpha);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -135,8 +139,23 @@ __global__ void __launch_bounds__(256) pick_head_kernel(const float* __restrict_
       s1 += part[2 * b];
       s2 += part[2 * b + 1];
     }
-    ctl->actor_loss = s1 / (double)n;
+    ctl->actor_loss = s1 / n_global;
     ctl->logp_sum = s2;
+    if (slots) {  // data-parallel shares, all-reduced with the actor gradients
+      slots[0] = (float)ctl->actor_loss;
+      slots[1] = (float)s2;
+    }
+  }
+}
+
+// data-parallel: take the all-reduced loss / log-prob sums back into ctl
+__global__ void sac_reduced_scalars_kernel(ul_sac_ctl* ctl, const float* cslot,
+                                           const float* aslots) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (cslot) ctl->critic_loss = (double)cslot[0];
+  if (aslots) {
+    ctl->actor_loss = (double)aslots[0];
+    ctl->logp_sum = (double)aslots[1];
   }
 }
 
@@ -144,11 +163,12 @@ __global__ void __launch_bounds__(256) pick_head_kernel(const float* __restrict_
 __global__ void __launch_bounds__(256) actor_head_kernel(
     const float* __restrict__ a, const float* __restrict__ eps, int64_t lde,
     const float* __restrict__ din1, const float* __restrict__ din2, int64_t ldin,
-    const float* __restrict__ log_std, int64_t n, int A, const ul_sac_ctl* __restrict__ ctl,
-    float* __restrict__ dmean, double* part, unsigned int* ticket, float* __restrict__ dls_out) {
+    const float* __restrict__ log_std, int64_t n, double n_global, int A,
+    const ul_sac_ctl* __restrict__ ctl, float* __restrict__ dmean, double* part,
+    unsigned int* ticket, float* __restrict__ dls_out) {
   __shared__ double scratch[32];
   const double alpha = exp(ctl->log_alpha);
-  const double inv_n = 1.0 / (double)n;
+  const double inv_n = 1.0 / n_global;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double* pp = part + (int64_t)blockIdx.x * A;
   for (int j = 0; j < A; ++j) {
@@ -174,9 +194,9 @@ __global__ void __launch_bounds__(256) actor_head_kernel(
 }
 
 // ScalarAdam on log_alpha (R:algos/sac.py:35-53, :224-229, :245-249)
-__global__ void alpha_step_kernel(ul_sac_ctl* ctl, int64_t n, double target_entropy) {
+__global__ void alpha_step_kernel(ul_sac_ctl* ctl, double n, double target_entropy) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const double excess = ctl->logp_sum / (double)n + target_entropy;
+  const double excess = ctl->logp_sum / n + target_entropy;
   const double la = ctl->log_alpha;
   ctl->alpha_loss = -la * excess;
   const double g = -excess;
@@ -250,6 +270,9 @@ struct SacPlan {
         *din2 = nullptr, *dmean = nullptr;
   double* y = nullptr;
   float *g_a = nullptr, *g_q1 = nullptr, *g_q2 = nullptr, *work = nullptr;
+  float *gq_own = nullptr, *ga_own = nullptr;  // plan-owned reduce buffers
+  int world = 1;
+  double n_global = 0.0;
   float *ws_a = nullptr, *ws_q1 = nullptr, *ws_q2 = nullptr, *ws_q1t = nullptr, *ws_q2t = nullptr;
   float *eps = nullptr;  // [2, B, A] device noise
   double* part = nullptr;
@@ -296,9 +319,9 @@ int alloc_sac(SacPlan* p) {
   o[k++] = carve(4 * B * p->A);                   // 20 din2
   o[k++] = carve(4 * B * p->A);                   // 21 dmean
   o[k++] = carve(8 * B);                          // 22 y
-  o[k++] = carve(4 * (p->Pa + 8));                // 23 g_a
-  o[k++] = carve(4 * (p->Pq + 8));                // 24 g_q1
-  o[k++] = carve(4 * (p->Pq + 8));                // 25 g_q2
+  o[k++] = carve(4 * (p->Pa + 8));                // 23 g_a | actor slots
+  o[k++] = carve(4 * (2 * p->Pq + 8));            // 24 g_q1 | g_q2 | critic slot
+  o[k++] = carve(4 * 8);                          // 25 (unused)
   o[k++] = carve(4 * (wa > wq ? wa : wq));        // 26 work
   o[k++] = carve(4 * p->va.wp_total);             // 27
   o[k++] = carve(4 * p->vq.wp_total);             // 28
@@ -320,9 +343,11 @@ int alloc_sac(SacPlan* p) {
                   &p->q1t, &p->q2t, &p->dq1, &p->dq2, &p->din1, &p->din2, &p->dmean};
   for (int i = 0; i < 22; ++i) *fp[i] = (float*)(a + o[i]);
   p->y = (double*)(a + o[22]);
-  p->g_a = (float*)(a + o[23]);
-  p->g_q1 = (float*)(a + o[24]);
-  p->g_q2 = (float*)(a + o[25]);
+  p->ga_own = (float*)(a + o[23]);
+  p->gq_own = (float*)(a + o[24]);
+  p->g_a = p->ga_own;
+  p->g_q1 = p->gq_own;
+  p->g_q2 = p->gq_own + p->Pq;
   p->work = (float*)(a + o[26]);
   p->ws_a = (float*)(a + o[27]);
   p->ws_q1 = (float*)(a + o[28]);
@@ -394,6 +419,8 @@ extern "C" int ul_sac_plan_create(const ul_sac_plan_desc* desc, void** plan) {
   if (p->A > UL_MAX_ACT) return fail("sac plan: action dim above UL_MAX_ACT");
   p->ldq = ul::act_ld(p->D + p->A);
   p->ldo = ul::act_ld(p->D);
+  p->world = desc->world_size > 1 ? desc->world_size : 1;
+  p->n_global = (double)p->B * p->world;
   p->Pa = p->va.total;
   p->Pq = p->vq.total;
   st = ul::alloc_sac(p);
@@ -419,6 +446,10 @@ extern "C" int ul_sac_plan_bind(void* plan, const ul_sac_bindings* b) {
   UL_CHECK_ARG(p && b, "sac plan: null argument");
   p->b = *b;
   p->bound = true;
+  float* gq = b->critic_red ? b->critic_red : p->gq_own;
+  p->g_q1 = gq;
+  p->g_q2 = gq + p->Pq;
+  p->g_a = b->actor_red ? b->actor_red : p->ga_own;
   return UL_OK;
 }
 
@@ -483,85 +514,155 @@ extern "C" int ul_sac_plan_noise_ptr(void* plan, float** eps) {
   return UL_OK;
 }
 
+namespace ul {
+namespace {
+
+// phase 1: staged weights, soft target, critic forwards + MSE head + critic
+// backwards into [g_q1 | g_q2 | loss share]
+int sac_critic_grads(SacPlan* p, cudaStream_t s) {
+  const ul_sac_bindings& b = p->b;
+  const int be = p->d.gemm_backend;
+  const int64_t B = p->B, D = p->D, A = p->A;
+  const float* ls = b.actor + p->va.logstd_off;
+  if (be == 1) {
+    UL_TRY(stage_weights(p->va, b.actor, p->ws_a, s));
+    UL_TRY(stage_weights(p->vq, b.q1, p->ws_q1, s));
+    UL_TRY(stage_weights(p->vq, b.q2, p->ws_q2, s));
+    UL_TRY(stage_weights(p->vq, b.q1t, p->ws_q1t, s));
+    UL_TRY(stage_weights(p->vq, b.q2t, p->ws_q2t, s));
+  }
+  // ---- K10 target
+  UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, p->qn, p->ldq, B, p->acts_a, p->mean, A, s));
+  squash_kernel<<<grid_for(B), 256, 0, s>>>(p->mean, A, ls, p->eps, A, B, (int)A, p->qn, p->ldq,
+                                           (int)D, nullptr, p->logp);
+  UL_TRY(check_launch("squash_kernel"));
+  UL_TRY(mlp_forward(p->vq, b.q1t, p->ws_q1t, be, p->qn, p->ldq, B, p->acts_q1, p->q1t, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q2t, p->ws_q2t, be, p->qn, p->ldq, B, p->acts_q2, p->q2t, 1, s));
+  sac_target_kernel<<<grid_for(B), 256, 0, s>>>(p->rew, p->term, p->nused, p->q1t, p->q2t,
+                                               p->logp, p->ctl, p->d.gamma, B, p->y);
+  UL_TRY(check_launch("sac_target_kernel"));
+  // ---- K11 critics (ones column of qin at D+A feeds the tensor-core db)
+  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, B, p->acts_q1, p->q1o, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  const unsigned nb = (unsigned)ceil_div(B, 256);
+  critic_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->y, B, 1.0 / p->n_global, p->dq1,
+                                        p->dq2, p->part, p->tickets, p->ctl,
+                                        p->world > 1 ? p->g_q1 + 2 * p->Pq : nullptr);
+  UL_TRY(check_launch("critic_head_kernel"));
+  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, true, B, p->acts_q1, p->dq1, 1,
+                      p->g_q1, nullptr, 0, 0, 0, true, true, p->work, s));
+  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, true, B, p->acts_q2, p->dq2, 1,
+                      p->g_q2, nullptr, 0, 0, 0, true, true, p->work, s));
+  return UL_OK;
+}
+
+// phase 2: (reduced loss back into ctl) Adam(q1), Adam(q2)
+int sac_critic_apply(SacPlan* p, cudaStream_t s) {
+  const ul_sac_bindings& b = p->b;
+  if (p->world > 1) {
+    sac_reduced_scalars_kernel<<<1, 32, 0, s>>>(p->ctl, p->g_q1 + 2 * p->Pq, nullptr);
+    UL_TRY(check_launch("sac_reduced_scalars_kernel"));
+  }
+  UL_TRY(adam_one(p, b.q1, p->g_q1, b.q1_m, b.q1_v, p->Pq, p->oc_q1, s));
+  return adam_one(p, b.q2, p->g_q2, b.q2_m, b.q2_v, p->Pq, p->oc_q2, s);
+}
+
+// phase 3 (actor steps): actor fwd -> squash(eps2) -> UPDATED critics fwd ->
+// argmin pick -> critic dX over the action columns -> actor head -> actor
+// backward into [g_a | loss share | sum log pi]
+int sac_actor_grads(SacPlan* p, cudaStream_t s) {
+  const ul_sac_bindings& b = p->b;
+  const int be = p->d.gemm_backend;
+  const int64_t B = p->B, D = p->D, A = p->A;
+  const float* ls = b.actor + p->va.logstd_off;
+  if (be == 1) {
+    UL_TRY(stage_weights(p->vq, b.q1, p->ws_q1, s));
+    UL_TRY(stage_weights(p->vq, b.q2, p->ws_q2, s));
+  }
+  const float* eps2 = p->eps + B * A;
+  UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, B, p->acts_a, p->mean, A, s));
+  squash_kernel<<<grid_for(B), 256, 0, s>>>(p->mean, A, ls, eps2, A, B, (int)A, p->qa, p->ldq,
+                                           (int)D, p->a_pi, p->logp);
+  UL_TRY(check_launch("squash_kernel"));
+  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, B, p->acts_q1, p->q1o, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  const unsigned nb = (unsigned)ceil_div(B, 256);
+  pick_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->logp, B, p->n_global, p->dq1, p->dq2,
+                                      p->part, p->tickets + 1, p->ctl,
+                                      p->world > 1 ? p->g_a + p->Pa : nullptr);
+  UL_TRY(check_launch("pick_head_kernel"));
+  // dQ/da through each critic's input gradient, action columns only
+  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, false, B, p->acts_q1, p->dq1, 1,
+                      nullptr, p->din1, A, (int)D, (int)A, false, false, p->work, s));
+  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, false, B, p->acts_q2, p->dq2, 1,
+                      nullptr, p->din2, A, (int)D, (int)A, false, false, p->work, s));
+  actor_head_kernel<<<nb, 256, 0, s>>>(p->a_pi, eps2, A, p->din1, p->din2, A, ls, B, p->n_global,
+                                       (int)A, p->ctl, p->dmean, p->part, p->tickets + 2,
+                                       p->g_a + p->va.logstd_off);
+  UL_TRY(check_launch("actor_head_kernel"));
+  return mlp_backward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, true, B, p->acts_a, p->dmean,
+                      A, p->g_a, nullptr, 0, 0, 0, true, false, p->work, s);
+}
+
+// phase 4: (reduced scalars back into ctl) Adam(actor), alpha ScalarAdam
+int sac_actor_apply(SacPlan* p, cudaStream_t s) {
+  const ul_sac_bindings& b = p->b;
+  if (p->world > 1) {
+    sac_reduced_scalars_kernel<<<1, 32, 0, s>>>(p->ctl, nullptr, p->g_a + p->Pa);
+    UL_TRY(check_launch("sac_reduced_scalars_kernel"));
+  }
+  UL_TRY(adam_one(p, b.actor, p->g_a, b.actor_m, b.actor_v, p->Pa, p->oc_a, s));
+  alpha_step_kernel<<<1, 32, 0, s>>>(p->ctl, p->n_global, p->d.target_entropy);
+  return check_launch("alpha_step_kernel");
+}
+
+// phase 5: Polyak q1t <- q1, q2t <- q2 (R:algos/sac.py:176-177)
+int sac_polyak(SacPlan* p, cudaStream_t s) {
+  UL_TRY(ul_polyak(p->b.q1t, p->b.q1, p->Pq, p->d.tau, s));
+  return ul_polyak(p->b.q2t, p->b.q2, p->Pq, p->d.tau, s);
+}
+
+}  // namespace
+}  // namespace ul
+
 // One sac_update (R:algos/sac.py:139-178).  do_actor: update_count %
 // policy_frequency == 0 after the increment.
 extern "C" int ul_sac_plan_update(void* plan, int do_actor, void* stream) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p && p->bound, "sac plan: not bound");
   cudaStream_t s = ul::as_stream(stream);
-  const ul_sac_bindings& b = p->b;
-  const int be = p->d.gemm_backend;
-  const int64_t B = p->B, D = p->D, A = p->A;
-  const float* ls = b.actor + p->va.logstd_off;
-  if (be == 1) {
-    UL_TRY(ul::stage_weights(p->va, b.actor, p->ws_a, s));
-    UL_TRY(ul::stage_weights(p->vq, b.q1, p->ws_q1, s));
-    UL_TRY(ul::stage_weights(p->vq, b.q2, p->ws_q2, s));
-    UL_TRY(ul::stage_weights(p->vq, b.q1t, p->ws_q1t, s));
-    UL_TRY(ul::stage_weights(p->vq, b.q2t, p->ws_q2t, s));
-  }
-  // ---- K10 target
-  UL_TRY(ul::mlp_forward(p->va, b.actor, p->ws_a, be, p->qn, p->ldq, B, p->acts_a, p->mean, A, s));
-  ul::squash_kernel<<<ul::grid_for(B), 256, 0, s>>>(p->mean, A, ls, p->eps, A, B, (int)A, p->qn,
-                                                   p->ldq, (int)D, nullptr, p->logp);
-  UL_TRY(ul::check_launch("squash_kernel"));
-  UL_TRY(ul::mlp_forward(p->vq, b.q1t, p->ws_q1t, be, p->qn, p->ldq, B, p->acts_q1, p->q1t, 1, s));
-  UL_TRY(ul::mlp_forward(p->vq, b.q2t, p->ws_q2t, be, p->qn, p->ldq, B, p->acts_q2, p->q2t, 1, s));
-  ul::sac_target_kernel<<<ul::grid_for(B), 256, 0, s>>>(p->rew, p->term, p->nused, p->q1t,
-                                                       p->q2t, p->logp, p->ctl, p->d.gamma, B,
-                                                       p->y);
-  UL_TRY(ul::check_launch("sac_target_kernel"));
-  // ---- K11 critics (ones column of qin at D+A feeds the tensor-core db)
-  UL_TRY(ul::mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, B, p->acts_q1, p->q1o, 1, s));
-  UL_TRY(ul::mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, B, p->acts_q2, p->q2o, 1, s));
-  const unsigned nb = (unsigned)ul::ceil_div(B, 256);
-  ul::critic_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->y, B, 1.0 / (double)B, p->dq1,
-                                            p->dq2, p->part, p->tickets, p->ctl);
-  UL_TRY(ul::check_launch("critic_head_kernel"));
-  UL_TRY(ul::mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, true, B, p->acts_q1,
-                          p->dq1, 1, p->g_q1, nullptr, 0, 0, 0, true, true, p->work, s));
-  UL_TRY(ul::adam_one(p, b.q1, p->g_q1, b.q1_m, b.q1_v, p->Pq, p->oc_q1, s));
-  UL_TRY(ul::mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, true, B, p->acts_q2,
-                          p->dq2, 1, p->g_q2, nullptr, 0, 0, 0, true, true, p->work, s));
-  UL_TRY(ul::adam_one(p, b.q2, p->g_q2, b.q2_m, b.q2_v, p->Pq, p->oc_q2, s));
+  UL_TRY(ul::sac_critic_grads(p, s));
+  UL_TRY(ul::sac_critic_apply(p, s));
   if (do_actor) {
-    // ---- actor + alpha (critics already updated, R:algos/sac.py:232-249)
-    if (be == 1) {
-      UL_TRY(ul::stage_weights(p->vq, b.q1, p->ws_q1, s));
-      UL_TRY(ul::stage_weights(p->vq, b.q2, p->ws_q2, s));
-    }
-    const float* eps2 = p->eps + B * A;
-    UL_TRY(ul::mlp_forward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, B, p->acts_a, p->mean, A, s));
-    ul::squash_kernel<<<ul::grid_for(B), 256, 0, s>>>(p->mean, A, ls, eps2, A, B, (int)A, p->qa,
-                                                     p->ldq, (int)D, p->a_pi, p->logp);
-    UL_TRY(ul::check_launch("squash_kernel"));
-    UL_TRY(ul::mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, B, p->acts_q1, p->q1o, 1, s));
-    UL_TRY(ul::mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, B, p->acts_q2, p->q2o, 1, s));
-    ul::pick_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->logp, B, p->dq1, p->dq2, p->part,
-                                            p->tickets + 1, p->ctl);
-    UL_TRY(ul::check_launch("pick_head_kernel"));
-    // dQ/da through each critic's input gradient, action columns only
-    UL_TRY(ul::mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, false, B, p->acts_q1,
-                            p->dq1, 1, nullptr, p->din1, A, (int)D, (int)A, false, false, p->work,
-                            s));
-    UL_TRY(ul::mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, false, B, p->acts_q2,
-                            p->dq2, 1, nullptr, p->din2, A, (int)D, (int)A, false, false, p->work,
-                            s));
-    ul::actor_head_kernel<<<nb, 256, 0, s>>>(p->a_pi, eps2, A, p->din1, p->din2, A, ls, B, (int)A,
-                                             p->ctl, p->dmean, p->part, p->tickets + 2,
-                                             p->g_a + p->va.logstd_off);
-    UL_TRY(ul::check_launch("actor_head_kernel"));
-    UL_TRY(ul::mlp_backward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, true, B, p->acts_a,
-                            p->dmean, A, p->g_a, nullptr, 0, 0, 0, true, false, p->work, s));
-    UL_TRY(ul::adam_one(p, b.actor, p->g_a, b.actor_m, b.actor_v, p->Pa, p->oc_a, s));
-    ul::alpha_step_kernel<<<1, 32, 0, s>>>(p->ctl, B, p->d.target_entropy);
-    UL_TRY(ul::check_launch("alpha_step_kernel"));
+    UL_TRY(ul::sac_actor_grads(p, s));
+    UL_TRY(ul::sac_actor_apply(p, s));
   }
-  // ---- K12 Polyak (R:algos/sac.py:176-177)
-  UL_TRY(ul_polyak(b.q1t, b.q1, p->Pq, p->d.tau, stream));
-  UL_TRY(ul_polyak(b.q2t, b.q2, p->Pq, p->d.tau, stream));
+  return ul::sac_polyak(p, s);
+}
+
+extern "C" int ul_sac_plan_reduce_buffers(void* plan, float** critic, int64_t* n_critic,
+                                          float** actor, int64_t* n_actor) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && critic && n_critic && actor && n_actor, "sac plan: null argument");
+  *critic = p->g_q1;
+  *n_critic = 2 * p->Pq + 4;
+  *actor = p->g_a;
+  *n_actor = p->Pa + 4;
   return UL_OK;
 }
+
+#define UL_SAC_PHASE(NAME, FN)                                  \
+  extern "C" int NAME(void* plan, void* stream) {               \
+    SacPlan* p = (SacPlan*)plan;                                \
+    UL_CHECK_ARG(p && p->bound, "sac plan: not bound");         \
+    return ul::FN(p, ul::as_stream(stream));                    \
+  }
+UL_SAC_PHASE(ul_sac_plan_critic_grads, sac_critic_grads)
+UL_SAC_PHASE(ul_sac_plan_critic_apply, sac_critic_apply)
+UL_SAC_PHASE(ul_sac_plan_actor_grads, sac_actor_grads)
+UL_SAC_PHASE(ul_sac_plan_actor_apply, sac_actor_apply)
+UL_SAC_PHASE(ul_sac_plan_polyak, sac_polyak)
+#undef UL_SAC_PHASE
 
 // Read back the control records; UL_ERR_DIVERGENCE if an Adam step or the
 // critic / actor loss saw non-finite values.

@@ -276,3 +276,86 @@ def test_pipeline_matches_serial_updates(prec):
         np.testing.assert_array_equal(p1.critic.flat(), p2.critic.flat())
     finally:
         P.set_precision(old)
+
+
+def test_ppo_data_parallel_two_ranks_match_single_process():
+    """SURVEY.md 8(e) for PPO: two ranks (threads on one GPU; the all-reduce a
+    barrier + sum) in replicated-segment mode each take half of every
+    reference-permuted minibatch; after the per-step gradient all-reduce the
+    replicated clip + Adam reproduce the single-process update."""
+    import threading
+
+    from oracle.port import philox_stream
+    from paper_2605_30313_b200 import _dist
+
+    old = P.get_precision()
+    P.set_precision("fp32")
+    try:
+        T, N = 8, 256
+        segd, actor, critic = _synthetic(T, N, 48, 52, 12, (128, 64), seed=11)
+        cfg = A.PpoConfig(epochs=2, minibatches=2)
+        arch_a, arch_c = TN.Arch(48, (128, 64), 12), TN.Arch(52, (128, 64), 1)
+
+        def fresh():
+            p = A.AcParams(TN.ModelParams.from_numpy(arch_a, actor.flat()),
+                           TN.ModelParams.from_numpy(arch_c, critic.flat()))
+            return p, A.AcOpt.for_params(p, cfg.lr)
+
+        def seg():
+            s = A.RolloutSegment(**segd)
+            s.advantages, s.returns = A.gae(s.rewards, s.values, s.terminated, s.truncated,
+                                            s.bootstrap_value, cfg.gamma, cfg.lam,
+                                            truncation_values=s.truncation_values)
+            return s
+
+        p_ref, o_ref = fresh()
+        want = A.ppo_update(seg(), p_ref, o_ref, cfg, philox_stream(1, "update"))
+
+        class Reducer:
+            def __init__(self):
+                self.bar = threading.Barrier(2)
+                self.slots = {}
+
+            def __call__(self, rank, t):
+                self.slots[rank] = t
+                torch.cuda.synchronize()
+                self.bar.wait()
+                if rank == 0:
+                    total = self.slots[0] + self.slots[1]
+                    self.slots[0].copy_(total)
+                    self.slots[1].copy_(total)
+                    torch.cuda.synchronize()
+                self.bar.wait()
+
+        red = Reducer()
+        got = [None, None]
+        errors = []
+        segs = [seg(), seg()]
+        states = [fresh(), fresh()]
+
+        def run(rank):
+            try:
+                _dist.emulate_rank(2, rank, lambda t: red(rank, t))
+                p, o = states[rank]
+                got[rank] = A.ppo_update(segs[rank], p, o, cfg, philox_stream(1, "update"))
+            except Exception as e:  # pragma: no cover
+                errors.append(e)
+                red.bar.abort()
+            finally:
+                _dist.clear_emulation()
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errors, errors
+        for p, _ in states:
+            np.testing.assert_allclose(p.actor.flat(), p_ref.actor.flat(), atol=3e-6)
+            np.testing.assert_allclose(p.critic.flat(), p_ref.critic.flat(), atol=3e-6)
+        np.testing.assert_array_equal(states[0][0].actor.flat(), states[1][0].actor.flat())
+        for g in got:
+            assert g.policy_loss == pytest.approx(want.policy_loss, abs=1e-5)
+            assert g.value_loss == pytest.approx(want.value_loss, rel=1e-5, abs=1e-6)
+    finally:
+        P.set_precision(old)

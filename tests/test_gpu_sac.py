@@ -74,3 +74,72 @@ def test_soft_update_known_answer():
     o.buf.fill_(1.0)
     A.soft_update(t, o, 0.125)
     assert float(t.buf[0].item()) == pytest.approx(0.125)
+
+
+def test_sac_data_parallel_two_ranks_match_single_process(golden):
+    """SURVEY.md 8(e) for SAC: two data-parallel ranks (emulated as threads on
+    one GPU, the all-reduce a barrier + sum) each update on half of the batch
+    with the global-batch loss scaling; after all-reducing the critic and
+    actor gradients (+ loss / log-pi sums) the replicated Adam / alpha /
+    Polyak steps reproduce the single-process trajectory on the whole batch."""
+    import threading
+
+    from oracle.port import philox_stream
+    from paper_2605_30313_b200 import _dist
+
+    g = golden("sac")
+    cfg = A.SacConfig(policy_frequency=2, batch_size=16)
+    ref = _state(g, cfg)
+    ranks = [_state(g, cfg), _state(g, cfg)]
+    rng_ref = philox_stream(1, "learner")
+    rngs = [philox_stream(1, "learner"), philox_stream(1, "learner")]
+
+    class Reducer:
+        def __init__(self):
+            self.bar = threading.Barrier(2)
+            self.slots = {}
+
+        def __call__(self, rank, t):
+            self.slots[rank] = t
+            self.bar.wait()
+            if rank == 0:
+                total = self.slots[0] + self.slots[1]
+                self.slots[0].copy_(total)
+                self.slots[1].copy_(total)
+            torch.cuda.synchronize()
+            self.bar.wait()
+
+    red = Reducer()
+    outs = [None, None]
+    errors = []
+
+    def run(rank, batch):
+        try:
+            _dist.emulate_rank(2, rank, lambda t: red(rank, t))
+            outs[rank] = A.sac_update(batch, ranks[rank], cfg, rngs[rank])
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+            red.bar.abort()
+        finally:
+            _dist.clear_emulation()
+
+    for s in range(4):
+        batch = {k: g[f"b{s}_{k}"] for k in ("obs", "action", "reward", "next_obs",
+                                             "terminated", "n_used")}
+        want = A.sac_update(batch, ref, cfg, rng_ref)
+        th = [threading.Thread(target=run, args=(r, batch)) for r in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errors, errors
+        for k in ("critic_loss", "actor_loss", "alpha_loss", "alpha"):
+            if k in want.extra:
+                for o in outs:
+                    assert o.extra[k] == pytest.approx(want.extra[k], rel=1e-5, abs=1e-6), k
+        for st in ranks:
+            for a, b in ((st.params.actor, ref.params.actor), (st.params.q1, ref.params.q1),
+                         (st.params.q2_targ, ref.params.q2_targ)):
+                np.testing.assert_allclose(a.flat(), b.flat(), atol=2e-6)
+            assert st.params.log_alpha == pytest.approx(ref.params.log_alpha, abs=1e-9)
+        np.testing.assert_array_equal(ranks[0].params.q1.flat(), ranks[1].params.q1.flat())
