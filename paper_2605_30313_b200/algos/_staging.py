@@ -104,6 +104,51 @@ class DeviceSegment:
             self._put_vec(self.adv, seg.advantages)
             self._put_vec(self.ret, seg.returns)
 
+    # ------------------------------------------------- per-step streaming
+    def _put_step_rows(self, dst: torch.Tensor, t: int, src, width: int) -> None:
+        """Step t's [N, width] host rows -> HBM rows [t*N, (t+1)*N) (t-major)."""
+        N = self.N
+        a = np.asarray(src)
+        if a.dtype != np.float32:
+            a = a.astype(np.float32)
+        a = np.ascontiguousarray(a.reshape(N, width))
+        raw = self._raw.get(width)
+        if raw is None:
+            raw = torch.empty(self.rows * width, dtype=torch.float32, device=dst.device)
+            self._raw[width] = raw
+        part = raw[t * N * width:(t + 1) * N * width]
+        _dev.h2d(part, a)
+        rb = width * 4
+        _lib.call("ul_gather_rows", 1, _lib.ptr_array([_dev.ptr(part)]),
+                  _lib.ptr_array([_dev.ptr(dst[t * N:(t + 1) * N])]), _lib.i64_array([rb]),
+                  _lib.i64_array([dst.stride(0) * 4]), _lib.i64_array([rb]), None, None, N,
+                  0, 0, N, None, _dev.stream())
+
+    def _put_step_vec(self, dst: torch.Tensor, t: int, src, dtype=np.float32) -> None:
+        a = np.asarray(src)
+        if a.dtype != dtype:
+            a = a.astype(dtype)
+        _dev.h2d(dst[t * self.N:(t + 1) * self.N], np.ascontiguousarray(a.reshape(-1)))
+
+    def load_step(self, t: int, obs, critic_obs, actions, behavior_log_prob, rewards,
+                  terminated, truncated, values, truncation_values=None) -> None:
+        """Stage one environment step (the [N, D] chunk SegmentCollector.collect
+        fills per step, R:runtime/collect.py:86-117) as soon as it exists."""
+        if not 0 <= t < self.T:
+            raise IndexError(f"step {t} outside [0, {self.T})")
+        od, cd, ad = self.dims
+        self._put_step_rows(self.obs, t, obs, od)
+        self._put_step_rows(self.cobs, t, critic_obs, cd)
+        self._put_step_rows(self.act, t, actions, ad)
+        self._put_step_vec(self.blogp, t, behavior_log_prob)
+        self._put_step_vec(self.rewards, t, rewards)
+        self._put_step_vec(self.term, t, terminated, np.uint8)
+        self._put_step_vec(self.trunc, t, truncated, np.uint8)
+        self._put_step_vec(self.values, t, values)
+        if truncation_values is not None:
+            self.has_tv = True
+            self._put_step_vec(self.tv, t, truncation_values)
+
     def h2d_bytes(self, seg, with_advantages: bool = True) -> int:
         od, cd, ad = self.dims
         n = self.rows * 4 * (od + cd + ad + 3 + (2 if with_advantages else 0))

@@ -372,6 +372,25 @@ class PpoPipeline:
             self.ready[k].record(self.copy)
         self.queue.append(k)
 
+    def stream_segment(self, T: int, N: int) -> "SegmentStream":
+        """Open the idle slot for per-step streaming:
+        each step's [N, D] chunk is copied as the collector produces it, so
+        the segment's PCIe time hides behind collection.  Close the stream
+        with ``finish(bootstrap_value)``; the segment then queues for update()."""
+        if len(self.queue) >= 2:
+            raise RuntimeError("both staging slots hold segments not yet consumed")
+        od, cd = self.params.actor.arch.input_dim, self.params.critic.arch.input_dim
+        ad = self.params.actor.arch.output_dim
+        if (T * N) % self.cfg.minibatches != 0:
+            raise ValueError(f"minibatches {self.cfg.minibatches} must divide batch size {T * N}")
+        k = self.next_slot
+        self.next_slot ^= 1
+        ds = staging_for(T, N, od, cd, ad, self.cfg.epochs, slot=f"pipe{k}")
+        self.slots[k] = ds
+        ds.has_tv = False
+        self.copy.wait_event(self.free[k])
+        return SegmentStream(self, k, ds)
+
     def update(self, next_segment=None) -> UpdateStats:
         """Run the update on the oldest staged segment; stage `next_segment`
         meanwhile.  Returns that update's statistics (host)."""
@@ -392,6 +411,33 @@ class PpoPipeline:
         if next_segment is not None:
             self.prefetch(next_segment)  # overlaps the update just enqueued
         return _stats(finish_plan(plan, self.opt), self.opt)
+
+
+class SegmentStream:
+    """Per-step writer into one PpoPipeline staging slot (copy stream)."""
+
+    def __init__(self, pipe: PpoPipeline, slot: int, ds):
+        self.pipe, self.slot, self.ds = pipe, slot, ds
+        self.steps = 0
+        self.closed = False
+
+    def push(self, t: int, obs, critic_obs, actions, behavior_log_prob, rewards, terminated,
+             truncated, values, truncation_values=None) -> None:
+        if self.closed:
+            raise RuntimeError("segment stream already finished")
+        with torch.cuda.stream(self.pipe.copy):
+            self.ds.load_step(t, obs, critic_obs, actions, behavior_log_prob, rewards,
+                              terminated, truncated, values, truncation_values)
+        self.steps += 1
+
+    def finish(self, bootstrap_value) -> None:
+        if self.steps != self.ds.T:
+            raise ValueError(f"segment stream got {self.steps} of {self.ds.T} steps")
+        with torch.cuda.stream(self.pipe.copy):
+            self.ds._put_vec(self.ds.boot, bootstrap_value)
+            self.pipe.ready[self.slot].record(self.pipe.copy)
+        self.pipe.queue.append(self.slot)
+        self.closed = True
 
 
 def plan_stats(params: AcParams, cfg: PpoConfig, ds) -> dict:

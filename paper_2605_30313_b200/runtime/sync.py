@@ -76,11 +76,13 @@ class _PinnedPool:
             self._free.setdefault(arr.size, []).append(arr)
 
 
-def _snapshot(params, pool: _PinnedPool, version: int, stream: int) -> HostParams:
+def _snapshot(params, pool: _PinnedPool, version: int, stream: int,
+              wait: bool = True) -> HostParams:
     n = params.buf.numel()
     buf = pool.take(n)
     _lib.call("ul_memcpy_async", buf.ctypes.data, _dev.ptr(params.buf), n * 4, stream)
-    _lib.call("ul_stream_sync", stream)
+    if wait:
+        _lib.call("ul_stream_sync", stream)
     view = buf[:]
     view.setflags(write=False)
     snap = HostParams(view, params.arch, version)
@@ -93,39 +95,85 @@ def _snapshot(params, pool: _PinnedPool, version: int, stream: int) -> HostParam
 
 
 class WeightSlot:
-    """Single-writer weight handoff with strictly increasing versions."""
+    """Single-writer weight handoff with strictly increasing versions.
 
-    def __init__(self, tracer: Tracer | None = None):
+    publish() never blocks the learner: the D2H snapshot runs on a copy
+    stream ordered after the learner's queued work, into a pooled page-locked
+    buffer (double buffering falls out of the pool: the previous version stays
+    readable while the next one lands), and a CUDA event marks it complete.
+    fetch() promotes the pending snapshot once its event has fired (waiting
+    only if a reader asks for a version still in flight)."""
+
+    def __init__(self, tracer: Tracer | None = None, blocking: bool = False):
         self._tracer = tracer if tracer is not None else Tracer(enabled=False)
         self._lock = threading.Lock()
         self._pair = None
+        self._pending = None  # (version, snapshot, event)
         self._pool = _PinnedPool()
+        self._copy = None
+        self._blocking = blocking
         self.publish_timestamp = 0
 
     @property
     def version(self) -> int:
+        pend = self._pending
+        if pend is not None:
+            return pend[0]
         pair = self._pair
         return 0 if pair is None else pair[0]
 
+    def _copy_stream(self):
+        import torch
+
+        if self._copy is None:
+            self._copy = torch.cuda.Stream()
+        return self._copy
+
     def publish(self, params, track: str = "learner") -> int:
-        """D2H snapshot + atomic swap; returns the new version."""
+        """Asynchronous D2H snapshot; returns the new version."""
+        import torch
+
         with self._tracer.span(track, "learner/weight_sync_write") as args:
             with self._lock:
                 version = self.version + 1
-                s = _dev.stream()
+                if self._blocking:
+                    s = _dev.stream()
+                    ev = None
+                else:
+                    cs = self._copy_stream()
+                    cs.wait_stream(torch.cuda.current_stream())
+                    s = cs.cuda_stream
+                    ev = torch.cuda.Event()
+                wait = self._blocking
                 if hasattr(params, "actor") and hasattr(params, "critic") \
                         and not hasattr(params, "q1"):
-                    snap = HostAcParams(_snapshot(params.actor, self._pool, version, s),
-                                        _snapshot(params.critic, self._pool, version, s))
+                    snap = HostAcParams(_snapshot(params.actor, self._pool, version, s, wait),
+                                        _snapshot(params.critic, self._pool, version, s, wait))
                 else:
-                    snap = _snapshot(params, self._pool, version, s)
-                self._pair = (version, snap)
+                    snap = _snapshot(params, self._pool, version, s, wait)
+                if ev is None:
+                    self._pair = (version, snap)
+                    self._pending = None
+                else:
+                    ev.record(self._copy)
+                    self._pending = (version, snap, ev)
                 self.publish_timestamp = now_ns()
             args["version"] = version
         return version
 
+    def _promote(self) -> None:
+        pend = self._pending
+        if pend is None:
+            return
+        pend[2].synchronize()
+        with self._lock:
+            if self._pending is pend:
+                self._pair = (pend[0], pend[1])
+                self._pending = None
+
     def fetch(self, track: str = "collector"):
         with self._tracer.span(track, "collector/weight_read") as args:
+            self._promote()
             pair = self._pair
             if pair is None:
                 raise RuntimeError("fetch_weights before first publish")

@@ -359,3 +359,36 @@ def test_ppo_data_parallel_two_ranks_match_single_process():
             assert g.value_loss == pytest.approx(want.value_loss, rel=1e-5, abs=1e-6)
     finally:
         P.set_precision(old)
+
+
+def test_pipeline_per_step_streaming_matches_prefetch():
+    """Per-step segment streaming stages exactly the
+    bytes a whole-segment prefetch does: identical update results."""
+    T, N = 6, 256
+    segd, actor, critic = _synthetic(T, N, 40, 44, 6, (64, 64), seed=21)
+    cfg = A.PpoConfig(epochs=2, minibatches=2)
+    arch_a, arch_c = TN.Arch(40, (64, 64), 6), TN.Arch(44, (64, 64), 1)
+
+    def run(stream):
+        p = A.AcParams(TN.ModelParams.from_numpy(arch_a, actor.flat()),
+                       TN.ModelParams.from_numpy(arch_c, critic.flat()))
+        pipe = A.PpoPipeline(p, A.AcOpt.for_params(p, cfg.lr), cfg, A.DeviceRng(5))
+        seg = A.RolloutSegment(**segd)
+        if stream:
+            w = pipe.stream_segment(T, N)
+            for t in range(T):
+                w.push(t, seg.obs[t], seg.critic_obs[t], seg.actions[t],
+                       seg.behavior_log_prob[t], seg.rewards[t], seg.terminated[t],
+                       seg.truncated[t], seg.values[t],
+                       None if seg.truncation_values is None else seg.truncation_values[t])
+            w.finish(seg.bootstrap_value)
+        else:
+            pipe.prefetch(seg)
+        st = pipe.update()
+        return st, p
+
+    s1, p1 = run(False)
+    s2, p2 = run(True)
+    assert s1.policy_loss == s2.policy_loss and s1.value_loss == s2.value_loss
+    np.testing.assert_array_equal(p1.actor.flat(), p2.actor.flat())
+    np.testing.assert_array_equal(p1.critic.flat(), p2.critic.flat())
