@@ -392,3 +392,55 @@ def test_pipeline_per_step_streaming_matches_prefetch():
     assert s1.policy_loss == s2.policy_loss and s1.value_loss == s2.value_loss
     np.testing.assert_array_equal(p1.actor.flat(), p2.actor.flat())
     np.testing.assert_array_equal(p1.critic.flat(), p2.critic.flat())
+
+
+def test_checkpoint_roundtrip_and_reference_format(tmp_path):
+    """save/load_checkpoint (R:tensornet/checkpoint.py:23-81): device params +
+    normalizer round-trip, and the npz keys/shapes the reference reads."""
+    arch = TN.Arch(7, (16, 8), 3)
+    p = TN.init_params(arch, 4)
+    p.version = 9
+    norm = TN.Normalizer(7, count=5.0, mean=np.arange(7.0), var=np.ones(7) * 2.0, frozen=True)
+    path = tmp_path / "ck.npz"
+    TN.save_checkpoint(path, p, norm)
+    with np.load(path) as d:
+        assert d["layer0_w"].shape == (16, 7) and d["layer2_b"].shape == (3,)
+        assert int(d["version"]) == 9 and d["log_std"].shape == (3,)
+    q, n2 = TN.load_checkpoint(path)
+    np.testing.assert_array_equal(q.flat(), p.flat())
+    assert q.version == 9 and q.arch == arch
+    np.testing.assert_array_equal(n2.mean, np.arange(7.0))
+    assert n2.count == 5.0 and n2.frozen
+
+
+def test_checkpoint_reads_reference_file():
+    """A checkpoint written by the reference's own save_checkpoint
+    (tests/golden/gen_checkpoint.py) loads into device params unchanged."""
+    from pathlib import Path
+
+    g = Path(__file__).resolve().parent / "golden"
+    q, n = TN.load_checkpoint(g / "ckpt_ref.npz")
+    e = np.load(g / "ckpt_ref_expect.npz")
+    np.testing.assert_array_equal(q.flat(), e["flat"])
+    assert q.version == 17 and q.arch.hidden_dims == (8, 4)
+    np.testing.assert_allclose(n.mean, e["mean"], rtol=0, atol=0)
+    np.testing.assert_allclose(n.var, e["var"], rtol=0, atol=0)
+    assert n.count == float(e["count"])
+
+
+def test_gpu_trace_spans_on_host_clock():
+    """Tracer.gpu_span: CUDA-event spans converted to the host clock, ordered,
+    with device durations."""
+    from paper_2605_30313_b200.trace import Tracer
+
+    tr = Tracer()
+    x = torch.randn(4096, 4096, device="cuda")
+    with tr.gpu_span("learner", "learner/update"):
+        for _ in range(4):
+            x = x @ x * 1e-3
+    with tr.gpu_span("learner", "learner/replay_sample"):
+        x.add_(1.0)
+    assert tr.flush_gpu() == 2
+    ev = tr.events()
+    assert [e.name for e in ev] == ["learner/update", "learner/replay_sample"]
+    assert ev[0].duration_ns > 0 and ev[1].ts_start >= ev[0].ts_start
