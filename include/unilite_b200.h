@@ -208,6 +208,24 @@ int ul_ring_insert(float* ring, int64_t cap, int64_t width, int64_t head, const 
  * shuffle of R:algos/ppo.py:162). */
 int ul_device_permutation(int64_t n, uint64_t key, int64_t* out, void* stream);
 
+/* ------------------------------------------- FlashSAC collector transforms */
+/* Device ReturnStdNormalizer.normalize + NStepPacker.push + replay insert
+ * (R:algos/estimators.py:153-207, R:replaypath/storage.py:17-46; SURVEY.md
+ * 8(f) item 3).  state = ul_nstep_state_bytes(...) zeroed bytes; inputs for
+ * one env step are device arrays (obs/next_obs [N,d], act [N,a], r [N] f32,
+ * term/trunc [N] u8); emitted codec rows land at ring[(head + i) % cap]
+ * (pitch ldr floats) in the reference's env-major order; *count_out (device
+ * or pinned) = rows written.  norm_gamma <= 0: no reward normalisation. */
+int64_t ul_nstep_state_bytes(int n_envs, int n, int obs_dim, int act_dim);
+int ul_nstep_push(void* state, int n_envs, int n, int obs_dim, int act_dim, double gamma,
+                  double norm_gamma, double g_max, double eps, const float* obs, const float* act,
+                  const float* r, const float* next_obs, const uint8_t* term,
+                  const uint8_t* trunc, float* ring, int64_t cap, int64_t ldr, int64_t head,
+                  int64_t* count_out, void* stream);
+/* normaliser (count, mean, m2, std) -> out[4] */
+int ul_nstep_norm_stats(void* state, int n_envs, int n, int obs_dim, int act_dim, double* out,
+                        void* stream);
+
 /* ------------------------------------------------------------ K3 normaliser */
 /* state = float64 [1 + 2D]: count, mean[D], var[D]
  * (R:tensornet/normalizer.py:14-25).  work = ul_norm_work_bytes(D) bytes of

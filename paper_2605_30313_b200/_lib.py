@@ -146,6 +146,10 @@ _PROTOS = {
     "ul_gemm_tc": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
                              vp, i64, C.c_int, C.c_int, vp]),
     "ul_tc_trace": (C.c_int, [vp]),
+    "ul_nstep_state_bytes": (i64, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "ul_nstep_push": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, f64, f64, f64, f64, vp,
+                                vp, vp, vp, vp, vp, vp, i64, i64, i64, vp, vp]),
+    "ul_nstep_norm_stats": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, vp]),
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                  C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
                                  vp]),
