@@ -19,6 +19,7 @@
 // GEMM's operand), fp32 otherwise (split-K dW partials, output layers).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 
@@ -165,6 +166,26 @@ __device__ __forceinline__ float elu_fast(float z) {
   return z > 0.f ? z : e;
 }
 
+// ELU of two values with one packed f16x2 MUFU.EX2 (half the SFU work of two
+// f32 exps); exp(z) - 1 for z <= 0 lies in (-1, 0], where f16's 11-bit
+// significand is finer than the bf16 the result is stored in.
+__device__ __forceinline__ void elu_pair_f16(float& z0, float& z1) {
+  const float t0 = fmaxf(z0, -16.f) * 1.4426950408889634f;  // log2(e); ex2(-23) ~ 1e-7
+  const float t1 = fmaxf(z1, -16.f) * 1.4426950408889634f;
+  uint32_t h;
+  asm("{\n"
+      ".reg .b32 t;\n"
+      "cvt.rn.f16x2.f32 t, %2, %1;\n"
+      "ex2.approx.f16x2 %0, t;\n"
+      "}\n"
+      : "=r"(h)
+      : "f"(t0), "f"(t1));
+  __half2 e2 = *reinterpret_cast<__half2*>(&h);
+  const float2 ef = __half22float2(e2);
+  z0 = z0 > 0.f ? z0 : ef.x - 1.f;
+  z1 = z1 > 0.f ? z1 : ef.y - 1.f;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -215,7 +236,10 @@ struct Smem {
   // B-resident: the ring streams A only; B's K tiles sit in smem for the
   // whole kernel (runtime-sized region after the ring)
   static constexpr int kStageBytes = kABytes + (BRES ? 0 : kBBytes);
-  static constexpr int kStagingBytes = kEpiWarps * 32 * 32 * OB;
+  // bf16 outputs double-buffer each warp's staging box (a chunk's TMA store
+  // reads one while the next chunk fills the other); fp32 boxes are single
+  static constexpr int kStg = OB == 2 ? 2 : 1;
+  static constexpr int kStagingBytes = kEpiWarps * kStg * 32 * 32 * OB;
   // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
   static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
   static constexpr int kFixed =
@@ -550,10 +574,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int n = lane; n < kCsumMaxN; n += 32)
         if ((n % BN) / kSlice == slice) csum_s[quarter * kCsumMaxN + n] = 0.f;
     }
-    uint8_t* stg = staging + ew * kBoxBytes;
     uint64_t* abar = aux_bar + ew;
     uint32_t aphase = 0;
     int local = 0;
+    int cj = 0;  // this warp's chunk counter (staging buffer = cj % kStg)
+    // diagnostics: epilogue warp 0, tiles 0-1, chunks 0-1 -> trace slots 100..
+#define UL_ETRACE(k) \
+  if (ew == 0 && lane == 0 && local < 2 && cj < 4) trace_at(p0_.trace, 100 + cj * 6 + (k))
     for (int t = cl; t < ngroups; t += ncl, ++local) {
       const Tile T = tile_of(t);
       const int m0 = T.m0, n0 = T.n0, z = T.z;
@@ -576,10 +603,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int crow = m0 + quarter * 32;  // row of this warp's 32-row box in C (split z)
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
-      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 32) {
-        // staging tile free again (previous TMA store has read it)
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 32, ++cj) {
+        uint8_t* stg = staging + (ew * S::kStg + cj % S::kStg) * kBoxBytes;
+        // this staging box free again (the TMA store issued from it has read it)
+        if (lane == 0) {
+          if (S::kStg == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
+        UL_ETRACE(0);
         if (EPI == kEpiEluGrad) {
           if (lane == 0) {
             mbar_expect_tx(abar, kBoxBytes);
@@ -590,6 +622,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (have) {
           tmem_ld16(taddr + (uint32_t)c0, *reinterpret_cast<float(*)[16]>(v));
           tmem_ld16(taddr + (uint32_t)(c0 + 16), *reinterpret_cast<float(*)[16]>(v + 16));
+          UL_ETRACE(1);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -606,9 +639,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
         }
         if (EPI == kEpiBiasElu) {
+          // (a packed f16x2 MUFU variant, elu_pair_f16, measured no faster)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = elu_fast(v[i]);
         }
+        UL_ETRACE(2);
         if constexpr (!kOutBf16) {
           // 32 rows x 128 B, 128 B swizzle: 16 B granule q of row r at q ^ (r & 7)
           float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
@@ -653,6 +688,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                       pack_bf16(v[8 * q + 4], v[8 * q + 5]),
                                       pack_bf16(v[8 * q + 6], v[8 * q + 7]));
         }
+        UL_ETRACE(3);
         if (p.tma_store) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -706,6 +742,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           __syncwarp();  // staging reads done before the next chunk reuses it
         }
+        UL_ETRACE(4);
         if (csum_on && T.pr == cs_pr) {
           // butterfly reduce-scatter over the warp's 32 rows: afterwards lane
           // l holds the sum of column c0 + l (rows >= M contribute zeros)
@@ -723,6 +760,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (n < kCsumMaxN) csum_s[quarter * kCsumMaxN + n] += v[0];
         }
       }
+#undef UL_ETRACE
       if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M) {
         TO* cp = reinterpret_cast<TO*>(p.C);
         cp[(int64_t)m * p.ldc + p.ones_col] = (TO)1.f;

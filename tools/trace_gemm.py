@@ -32,7 +32,8 @@ def trace():
     t0 = t[0]
     rel = lambda a: [round((x - t0) / 1e3, 2) if x else None for x in a]  # noqa: E731
     return dict(setup=rel([t[1]])[0], issue=rel(t[2:34]), mma=rel(t[34:66]),
-                acc=rel(t[66:82]), epi=rel(t[82:98]), exit=rel([t[98]])[0])
+                acc=rel(t[66:82]), epi=rel(t[82:98]), exit=rel([t[98]])[0],
+                chunks=[rel(t[100 + 6 * c:105 + 6 * c]) for c in range(4)])
 
 
 def run(name, fn):
@@ -51,6 +52,8 @@ def run(name, fn):
     print("  mma  ", strip(tr["mma"]))
     print("  acc  ", strip(tr["acc"]))
     print("  epi  ", strip(tr["epi"]))
+    for c, ch in enumerate(tr["chunks"]):
+        print(f"  chunk{c} [start, tmem, math, staged, stored]", ch)
 
 
 def main():
