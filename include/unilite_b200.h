@@ -125,6 +125,11 @@ int ul_polyak(float* target, const float* online, int64_t n, double tau, void* s
 typedef struct ul_net_desc {
   int32_t n_layers;
   int32_t dims[UL_MAX_LAYERS + 1];
+  /* 1: LayerNorm (gain g, shift beta; eps 1e-5) between every hidden layer's
+   * affine map and its ELU -- an extension for cfg3's critics, not in the
+   * reference.  Params per hidden layer become W, b, g, beta; hidden widths
+   * must be multiples of 4. */
+  int32_t layer_norm;
 } ul_net_desc;
 
 /* number of floats of the flat parameter vector (incl. log_std) */

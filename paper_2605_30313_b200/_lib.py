@@ -42,14 +42,15 @@ f64 = C.c_double
 
 
 class NetDesc(C.Structure):
-    _fields_ = [("n_layers", i32), ("dims", i32 * (UL_MAX_LAYERS + 1))]
+    _fields_ = [("n_layers", i32), ("dims", i32 * (UL_MAX_LAYERS + 1)), ("layer_norm", i32)]
 
     @classmethod
-    def of(cls, dims) -> "NetDesc":
+    def of(cls, dims, layer_norm: bool = False) -> "NetDesc":
         d = cls()
         d.n_layers = len(dims) - 1
         for i, x in enumerate(dims):
             d.dims[i] = int(x)
+        d.layer_norm = int(bool(layer_norm))
         return d
 
 

@@ -119,7 +119,20 @@ struct NetView {
   int64_t w_off[UL_MAX_LAYERS], b_off[UL_MAX_LAYERS], logstd_off, total;
   int64_t wp_off[UL_MAX_LAYERS], wp_total;  // staged (16 B-row) weight layout
   int64_t wb_off[UL_MAX_LAYERS];            // bf16 staged layout (ld round_up(in, 8))
+  int ln;                                   // LayerNorm on hidden layers
+  int64_t g_off[UL_MAX_LAYERS], beta_off[UL_MAX_LAYERS];
 };
+// LayerNorm rows (ln.cu): a [M, D] fp32 (GEMM output) -> h (dtype) = elu(LN(a) g + beta)
+int ln_forward(const float* a, int64_t lda, int64_t M, int D, const float* g, const float* beta,
+               float* stats, void* h, int64_t ldh, int ones_col, int dtype, cudaStream_t s);
+// dn -> da in place; partial sums of dg | dbeta | colsum(da) described by *job
+int ln_backward(void* dn, int64_t ldd, const float* a, int64_t lda, const float* stats,
+                const float* g, int64_t M, int D, float* part, int dtype, float* gg, float* gbeta,
+                float* gb, ReduceJob* job, cudaStream_t s);
+int ln_part_floats(int64_t M, int D);
+// pre-LayerNorm rows a_i [M, round_up(D,4)] fp32 and stats [M][2] of hidden layer i
+void ln_bufs(const NetView& v, const float* acts, int64_t M, int i, float** a, int64_t* lda,
+             float** stats);
 int make_view(const ul_net_desc* d, NetView* v);
 // hidden activation row stride (elements): round_up(d + 1, 4) fp32 /
 // round_up(d + 1, 8) bf16 -- 16-byte rows plus the ones column

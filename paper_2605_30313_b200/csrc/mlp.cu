@@ -229,6 +229,7 @@ int make_view(const ul_net_desc* d, NetView* v) {
   UL_CHECK_ARG(d->n_layers >= 1 && d->n_layers <= UL_MAX_LAYERS,
                "net: n_layers %d outside [1,%d]", d->n_layers, UL_MAX_LAYERS);
   v->n_layers = d->n_layers;
+  v->ln = d->layer_norm ? 1 : 0;
   int64_t off = 0, woff = 0;
   for (int i = 0; i <= d->n_layers; ++i) {
     UL_CHECK_ARG(d->dims[i] > 0, "all layer dims must be positive");
@@ -239,6 +240,14 @@ int make_view(const ul_net_desc* d, NetView* v) {
     off += (int64_t)v->dims[i + 1] * v->dims[i];
     v->b_off[i] = off;
     off += v->dims[i + 1];
+    v->g_off[i] = v->beta_off[i] = -1;
+    if (v->ln && i < d->n_layers - 1) {  // hidden layer: LayerNorm gain / shift
+      UL_CHECK_ARG(v->dims[i + 1] % 4 == 0, "layer_norm: hidden widths must be multiples of 4");
+      v->g_off[i] = off;
+      off += v->dims[i + 1];
+      v->beta_off[i] = off;
+      off += v->dims[i + 1];
+    }
     v->wp_off[i] = woff;
     woff += (int64_t)v->dims[i + 1] * rup(v->dims[i], 4);
   }
@@ -256,7 +265,19 @@ int make_view(const ul_net_desc* d, NetView* v) {
 int64_t act_floats(const NetView& v, int64_t M) {
   int64_t s = 0;
   for (int i = 1; i < v.n_layers; ++i) s += act_ld(v.dims[i]) * M;
+  if (v.ln)  // pre-LayerNorm rows + row stats per hidden layer
+    for (int i = 1; i < v.n_layers; ++i) s += (rup(v.dims[i], 4) + 2) * M;
   return s;
+}
+
+void ln_bufs(const NetView& v, const float* acts, int64_t M, int i, float** a, int64_t* lda,
+             float** stats) {
+  int64_t off = 0;
+  for (int j = 1; j < v.n_layers; ++j) off += act_ld(v.dims[j]) * M;
+  for (int j = 1; j <= i; ++j) off += (rup(v.dims[j], 4) + 2) * M;
+  *lda = rup(v.dims[i + 1], 4);
+  *a = const_cast<float*>(acts) + off;
+  *stats = *a + *lda * M;
 }
 
 static int64_t max_hidden_ld(const NetView& v) {
@@ -291,12 +312,23 @@ static int64_t dw_ws_floats(const NetView& v, int64_t M) {
   return rup(ws, 64);
 }
 
-int64_t bwd_work_floats(const NetView& v, int64_t M) {
+static int64_t sk_ws_floats(const NetView& v, int64_t M) {
   const int last = v.n_layers - 1;
   int64_t sk = skinny_part_floats(M, v.dims[last], v.dims[last + 1]);
   // (the region also holds the dX epilogue's per-CTA column-sum partials)
   sk = sk > (int64_t)kNumSMs * kCsumMaxN ? sk : (int64_t)kNumSMs * kCsumMaxN;
-  return 2 * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk;
+  return rup(sk, 64);
+}
+
+int64_t bwd_work_floats(const NetView& v, int64_t M) {
+  const int64_t sk = sk_ws_floats(v, M);
+  int64_t lnp = 0;  // LayerNorm partials (live until the layer's own reduction)
+  if (v.ln)
+    for (int i = 1; i < v.n_layers; ++i) {
+      const int64_t q = ln_part_floats(M, v.dims[i]);
+      lnp = q > lnp ? q : lnp;
+    }
+  return 2 * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk + lnp;
 }
 
 // hidden layer i's activation rows (byte offsets: bf16 rows are half as wide)
@@ -385,24 +417,27 @@ struct Lanes {
 // one launch for up to kMaxReduceJobs fixed-order partial reductions
 int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
   // shallow (split-K) and deep (per-block / per-CTA partial) jobs take the
-  // 8- and 32-warp variants
+  // 8- and 32-warp variants; at most kMaxReduceJobs per launch
   for (int deep = 0; deep < 2; ++deep) {
-    ReduceTable tab{};
-    int64_t bx = 1;
-    int n = 0;
-    for (int q = 0; q < nj; ++q) {
-      if ((jobs[q].nz > 64) != (deep == 1)) continue;
-      tab.r[n++] = jobs[q];
-      const int64_t b = ceil_div(jobs[q].len, 128);
-      bx = b > bx ? b : bx;
+    int q = 0;
+    while (q < nj) {
+      ReduceTable tab{};
+      int64_t bx = 1;
+      int cnt = 0;
+      for (; q < nj && cnt < kMaxReduceJobs; ++q) {
+        if ((jobs[q].nz > 64) != (deep == 1)) continue;
+        tab.r[cnt++] = jobs[q];
+        const int64_t b = ceil_div(jobs[q].len, 128);
+        bx = b > bx ? b : bx;
+      }
+      if (cnt == 0) continue;
+      if (deep)
+        UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel<32>,
+                          dim3((unsigned)bx, (unsigned)cnt), dim3(1024), 0, s, tab));
+      else
+        UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel<8>,
+                          dim3((unsigned)bx, (unsigned)cnt), dim3(256), 0, s, tab));
     }
-    if (n == 0) continue;
-    if (deep)
-      UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel<32>, dim3((unsigned)bx, (unsigned)n),
-                        dim3(1024), 0, s, tab));
-    else
-      UL_TRY(launch_pdl("reduce_dw_kernel", reduce_dw_kernel<8>, dim3((unsigned)bx, (unsigned)n),
-                        dim3(256), 0, s, tab));
   }
   return UL_OK;
 }
@@ -446,6 +481,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
     ldh[k] = nets[k].ldx;
   }
   const int nl = nets[0].v->n_layers;
+  bool ln_pending[2] = {false, false};
   for (int i = 0; i < nl; ++i) {
     const bool last = i == nl - 1;
     GemmDesc g[2] = {};
@@ -469,6 +505,16 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       G.splits = 1;
       G.C = dst; G.ldc = lddst;
       G.dtype = dt;
+      if (v.ln && !last) {  // a = W x + b (fp32) -> LayerNorm + ELU kernel below
+        float* la;
+        float* lst;
+        int64_t lla;
+        ln_bufs(v, N.acts, M, i, &la, &lla, &lst);
+        G.epi = kEpiBias;
+        G.C = la;
+        G.ldc = lla;
+        ln_pending[k] = true;
+      }
       // tf32 keeps a wide output layer on the SIMT kernel; bf16 runs it on
       // the tensor cores with an fp32 bias epilogue
       use[k] = tc && N.wp && (!last || dt == kBf16);
@@ -479,11 +525,24 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
         G.ldb = v.dims[i];
       }
       has[k] = true;
-      ones[k] = last ? -1 : v.dims[i + 1];
+      ones[k] = (last || ln_pending[k]) ? -1 : v.dims[i + 1];
       h[k] = dst;
       ldh[k] = lddst;
     }
     UL_TRY(run_gemms(g, has, use, ones, s));
+    for (int k = 0; k < n; ++k) {
+      if (!ln_pending[k]) continue;
+      ln_pending[k] = false;
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      float* la;
+      float* lst;
+      int64_t lla;
+      ln_bufs(v, N.acts, M, i, &la, &lla, &lst);
+      UL_TRY(ln_forward(la, lla, M, v.dims[i + 1], N.params + v.g_off[i],
+                        N.params + v.beta_off[i], lst, const_cast<float*>(h[k]), ldh[k],
+                        v.dims[i + 1], dt, s));
+    }
     if (skinny[0] || skinny[1]) {
       UL_TRY(L.open());
       for (int k = 0; k < n; ++k) {
@@ -518,8 +577,9 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     int ping;
     int db_done;  // layer whose db the layer above already produced (skinny column sums)
     float* sk_part;
+    float* ln_part;
   } st[2];
-  ReduceJob pend[4];  // deferred reductions (skinny heads, fused column sums) for the next reduce launch
+  ReduceJob pend[8];  // deferred reductions (skinny heads, column sums, LayerNorm) for the next reduce launch
   int npend = 0;
   const int nl = nets[0].v->n_layers;
   UL_TRY(L.open());
@@ -534,6 +594,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     st[k].dh_buf[1] = N.work + M * H;
     st[k].ws = N.work + 2 * M * H;
     st[k].sk_part = st[k].ws + dw_ws_floats(v, M);
+    st[k].ln_part = st[k].sk_part + sk_ws_floats(v, M);
     st[k].dh = N.dout;
     st[k].lddh = N.ld_dout;
     st[k].dh_f32 = true;
@@ -559,7 +620,9 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       S.ping ^= 1;
       const int64_t in_below = v.dims[i - 1];
       const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
-      const bool need_cs = N.want_dw && tc && N.wp && !ones_free_of(in_below, below_ones);
+      // (a LayerNorm layer's db is colsum of its da, which ln_backward makes)
+      const bool need_cs =
+          N.want_dw && tc && N.wp && !v.ln && !ones_free_of(in_below, below_ones);
       // its partial reduction waits for the next layer's reduce launch
       ReduceJob* dj = (N.want_dw || need_cs) ? &pend[npend] : nullptr;
       UL_TRY(skinny_bwd(inp, ldin, M, (int)in, (int)out, N.params + v.w_off[i], S.dh, S.lddh,
@@ -595,6 +658,28 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       S.lddh = ldcv;
       S.dh_f32 = false;
     }
+    // ---- LayerNorm of hidden layer i: dn (grad at the LN output, from the
+    // ELU-gradient epilogue above) -> da in place, + dg / dbeta / db partials
+    for (int k = 0; k < n; ++k) {
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      if (!v.ln || i >= nl - 1 || skinny_done[k]) continue;
+      St& S = st[k];
+      const bool has_ones = i == 0 ? (N.x_has_ones && N.ldx >= v.dims[i] + 1) : true;
+      const bool db_here = N.want_dw && tc && N.wp && !ones_free_of(v.dims[i], has_ones);
+      float* la;
+      float* lst;
+      int64_t lla;
+      ln_bufs(v, N.acts, M, i, &la, &lla, &lst);
+      ReduceJob job;
+      UL_TRY(ln_backward(const_cast<float*>(S.dh), S.lddh, la, lla, lst, N.params + v.g_off[i], M,
+                         v.dims[i + 1], S.ln_part, dt,
+                         N.want_dw ? N.grads + v.g_off[i] : nullptr,
+                         N.want_dw ? N.grads + v.beta_off[i] : nullptr,
+                         db_here ? N.grads + v.b_off[i] : nullptr, &job, L.of(k)));
+      if (N.want_dw) pend[npend++] = job;
+      if (db_here) S.db_done = i;
+    }
     UL_TRY(L.close());
     // ---- dW (+db via the ones column) for both networks: one grouped launch
     GemmDesc gw[2] = {};
@@ -626,7 +711,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       for (int k = 0; k < n; ++k)
         if (tc_w[k]) UL_TRY(gemm_tc(gw[k], -1, s));
     if (tc_w[0] || tc_w[1]) {
-      ReduceJob jobs[kMaxReduceJobs];
+      ReduceJob jobs[2 + 8];
       int nj = 0;
       for (int k = 0; k < n; ++k) {
         if (!tc_w[k]) continue;
@@ -737,7 +822,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       // epilogue produce per-CTA partials (reduced with the next reduction)
       const int64_t in_below = v.dims[i - 1];
       const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
-      if (N.want_dw && tc_x[k] && in <= kCsumMaxN && S.db_done != i - 1 &&
+      if (N.want_dw && tc_x[k] && in <= kCsumMaxN && S.db_done != i - 1 && !v.ln &&
           !ones_free_of(in_below, below_ones)) {
         G.csum_part = S.sk_part;
         G.csum_nz = &cs_nz[k];

@@ -33,14 +33,18 @@ class HostParams:
         self._buf = buf
         self.arch = arch
         self.version = version
-        layers, off = [], 0
-        for out_dim, in_dim in arch.layer_dims:
+        layers, lns, off = [], [], 0
+        for k, (out_dim, in_dim) in enumerate(arch.layer_dims):
             w = buf[off:off + out_dim * in_dim].reshape(out_dim, in_dim)
             off += out_dim * in_dim
             b = buf[off:off + out_dim]
             off += out_dim
             layers.append((w, b))
+            if getattr(arch, "layer_norm", False) and k < len(arch.hidden_dims):
+                lns.append((buf[off:off + out_dim], buf[off + out_dim:off + 2 * out_dim]))
+                off += 2 * out_dim
         self.layers = layers
+        self.layer_norms = lns
         self.log_std = buf[off:off + arch.output_dim]
 
     def flat(self) -> np.ndarray:

@@ -25,6 +25,9 @@ class Arch:
     hidden_dims: tuple = ()
     output_dim: int = 1
     activation: str = "elu"
+    # extension (not in the reference): LayerNorm (gain, shift) between each
+    # hidden layer's affine map and its ELU -- cfg3's FastSAC critics
+    layer_norm: bool = False
 
     def __post_init__(self) -> None:
         object.__setattr__(self, "hidden_dims", tuple(int(h) for h in self.hidden_dims))
@@ -46,21 +49,28 @@ class Arch:
         return [(d[i + 1], d[i]) for i in range(len(d) - 1)]
 
     def desc(self) -> _lib.NetDesc:
-        return _lib.NetDesc.of(self.dims)
+        return _lib.NetDesc.of(self.dims, self.layer_norm)
 
     @property
     def param_count(self) -> int:
-        return sum(o * i + o for o, i in self.layer_dims) + self.output_dim
+        ln = 2 * sum(self.hidden_dims) if self.layer_norm else 0
+        return sum(o * i + o for o, i in self.layer_dims) + ln + self.output_dim
 
 
-def _views(buf: torch.Tensor, arch: Arch):
-    layers, off = [], 0
-    for o, i in arch.layer_dims:
+def _views(buf: torch.Tensor, arch: Arch, with_ln: bool = False):
+    layers, lns, off = [], [], 0
+    nl = len(arch.layer_dims)
+    for k, (o, i) in enumerate(arch.layer_dims):
         w = buf[off:off + o * i].view(o, i)
         off += o * i
         b = buf[off:off + o]
         off += o
         layers.append((w, b))
+        if arch.layer_norm and k < nl - 1:
+            lns.append((buf[off:off + o], buf[off + o:off + 2 * o]))
+            off += 2 * o
+    if with_ln:
+        return layers, buf[off:off + arch.output_dim], lns
     return layers, buf[off:off + arch.output_dim]
 
 
@@ -80,6 +90,11 @@ class _FlatRecord:
     @property
     def log_std(self) -> torch.Tensor:
         return _views(self.buf, self.arch)[1]
+
+    @property
+    def layer_norms(self):
+        """(gain, shift) per hidden layer when arch.layer_norm (else [])."""
+        return _views(self.buf, self.arch, with_ln=True)[2]
 
     def flat(self) -> np.ndarray:
         """All parameters (incl. log_std) as one host float vector (D2H)."""
@@ -148,10 +163,14 @@ def init_params(arch: Arch, seed: int, init_noise_std: float = 1.0,
         raise ValueError("device parameters are float32")
     rng = np.random.default_rng(seed)
     parts = []
-    for out_dim, in_dim in arch.layer_dims:
+    nl = len(arch.layer_dims)
+    for k, (out_dim, in_dim) in enumerate(arch.layer_dims):
         bound = np.sqrt(1.0 / in_dim)
         parts.append(rng.uniform(-bound, bound, (out_dim, in_dim)).astype(np.float32).ravel())
         parts.append(np.zeros(out_dim, np.float32))
+        if arch.layer_norm and k < nl - 1:  # gain 1, shift 0
+            parts.append(np.ones(out_dim, np.float32))
+            parts.append(np.zeros(out_dim, np.float32))
     parts.append(np.full(arch.output_dim, np.log(init_noise_std), dtype=np.float32))
     return ModelParams.from_numpy(arch, np.concatenate(parts))
 

@@ -52,6 +52,12 @@ def test_struct_layouts_match_native():
     d = _lib.NetDesc.of((235, 512, 256, 128, 12))
     assert _lib.lib().ul_net_param_count(ctypes.byref(d)) == \
         235 * 512 + 512 + 512 * 256 + 256 + 256 * 128 + 128 + 128 * 12 + 12 + 12
+    from paper_2605_30313_b200.tensornet import Arch
+
+    ln = Arch(input_dim=235, hidden_dims=(512, 256, 128), output_dim=12, layer_norm=True)
+    dl = ln.desc()
+    assert _lib.lib().ul_net_param_count(ctypes.byref(dl)) == ln.param_count == \
+        ctypes.c_int64(_lib.lib().ul_net_param_count(ctypes.byref(d))).value + 2 * (512 + 256 + 128)
 
 
 def test_product_fails_loudly_without_gpu():
