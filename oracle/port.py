@@ -46,19 +46,29 @@ class Net:
     dims: tuple            # (in, h1, ..., out)
     layers: list           # [[W, b], ...]
     log_std: np.ndarray
+    # builder extension (not in the reference): [[g, beta], ...] per hidden
+    # layer when the net has LayerNorm; flat order W, b, g, beta per layer
+    ln: list = field(default_factory=list)
+
+    def pairs(self) -> list:
+        """Parameter pairs in flat order: [W0,b0], [g0,beta0]?, [W1,b1], ..."""
+        out = []
+        for i, pair in enumerate(self.layers):
+            out.append(pair)
+            if i < len(self.ln):
+                out.append(self.ln[i])
+        return out
+
+    def arrays(self) -> list:
+        return [a for pair in self.pairs() for a in pair] + [self.log_std]
 
     def flat(self) -> np.ndarray:
-        parts = []
-        for w, b in self.layers:
-            parts.append(w.ravel())
-            parts.append(b.ravel())
-        parts.append(self.log_std.ravel())
-        return np.concatenate(parts)
+        return np.concatenate([a.ravel() for a in self.arrays()])
 
     def load_flat(self, vec: np.ndarray) -> "Net":
         out = self.clone()
         pos = 0
-        for pair in out.layers:
+        for pair in out.pairs():
             for j in range(2):
                 n = pair[j].size
                 pair[j] = vec[pos:pos + n].reshape(pair[j].shape).astype(pair[j].dtype)
@@ -68,23 +78,33 @@ class Net:
 
     def clone(self) -> "Net":
         return Net(self.dims, [[w.copy(), b.copy()] for w, b in self.layers],
-                   self.log_std.copy())
+                   self.log_std.copy(), [[g.copy(), b.copy()] for g, b in self.ln])
 
     def zeros(self) -> "Net":
         return Net(self.dims, [[np.zeros_like(w), np.zeros_like(b)] for w, b in self.layers],
-                   np.zeros_like(self.log_std))
+                   np.zeros_like(self.log_std),
+                   [[np.zeros_like(g), np.zeros_like(b)] for g, b in self.ln])
 
 
-def net_init(dims, seed: int, noise_std: float = 1.0, dtype=np.float32) -> Net:
+class _Acts(list):
+    """Hidden activations; .ln holds the LayerNorm caches of an LN net."""
+
+    ln: list
+
+
+def net_init(dims, seed: int, noise_std: float = 1.0, dtype=np.float32,
+             layer_norm: bool = False) -> Net:
     """U(+-sqrt(1/fan_in)) weights drawn layer by layer from default_rng(seed), zero
-    biases, log_std = ln(noise_std) (R:tensornet/mlp.py:116-131)."""
+    biases, log_std = ln(noise_std) (R:tensornet/mlp.py:116-131).  layer_norm
+    (extension) adds gain 1 / shift 0 per hidden layer, drawing nothing."""
     gen = np.random.default_rng(seed)
     layers = []
     for fan_in, fan_out in zip(dims[:-1], dims[1:]):
         lim = np.sqrt(1.0 / fan_in)
         layers.append([gen.uniform(-lim, lim, (fan_out, fan_in)).astype(dtype),
                        np.zeros(fan_out, dtype=dtype)])
-    return Net(tuple(dims), layers, np.full(dims[-1], np.log(noise_std), dtype=dtype))
+    ln = [[np.ones(d, dtype), np.zeros(d, dtype)] for d in dims[1:-1]] if layer_norm else []
+    return Net(tuple(dims), layers, np.full(dims[-1], np.log(noise_std), dtype=dtype), ln)
 
 
 def elu(z):
@@ -103,12 +123,17 @@ def mlp_forward(net: Net, x):
     x = np.asarray(x)
     if x.ndim != 2 or x.shape[1] != net.dims[0]:
         raise ValueError("input width mismatch")
-    acts = []
+    acts = _Acts()
+    acts.ln = []
     h = x
     last = len(net.layers) - 1
     for i, (w, b) in enumerate(net.layers):
         z = h @ w.T + b
         if i < last:
+            if net.ln:  # extension: z -> LN(z) g + beta before the ELU
+                n, cache = ln_forward(z, net.ln[i][0], net.ln[i][1])
+                acts.ln.append(cache)
+                z = n.astype(z.dtype)
             h = elu(z)
             acts.append(h)
         else:
@@ -130,6 +155,11 @@ def mlp_backward(net: Net, x, acts, dout):
         dh = dh @ w
         if i > 0:
             dh = dh * elu_grad_from_act(acts[i - 1])
+            if net.ln:
+                dz, dg, db = ln_backward(dh, net.ln[i - 1][0], acts.ln[i - 1])
+                g.ln[i - 1][0] += dg.astype(g.ln[i - 1][0].dtype)
+                g.ln[i - 1][1] += db.astype(g.ln[i - 1][1].dtype)
+                dh = dz.astype(dh.dtype)
     return dh, g
 
 
@@ -239,8 +269,7 @@ class Opt:
 
 def grad_norm(g: Net) -> float:
     """sqrt(sum over arrays of float(sum(a*a))) (R:tensornet/mlp.py:104-107)."""
-    acc = sum(float(np.sum(a * a)) for w, b in g.layers for a in (w, b))
-    return float(np.sqrt(acc + float(np.sum(g.log_std ** 2))))
+    return float(np.sqrt(sum(float(np.sum(a * a)) for a in g.arrays())))
 
 
 def clip_norm(grads: list, max_norm: float) -> float:
@@ -250,7 +279,7 @@ def clip_norm(grads: list, max_norm: float) -> float:
     if max_norm > 0 and total > max_norm:
         f = max_norm / (total + 1e-12)
         for g in grads:
-            for pair in g.layers:
+            for pair in g.pairs():
                 pair[0] *= f
                 pair[1] *= f
             g.log_std *= f
@@ -274,9 +303,9 @@ def adam(net: Net, g: Net, opt: Opt, max_norm: float = 0.0) -> None:
         v += (1 - opt.b2) * gr * gr
         p -= (opt.lr * (m / bc1) / (np.sqrt(v / bc2) + opt.eps)).astype(p.dtype)
 
-    for i in range(len(net.layers)):
+    for p, gp, mp, vp in zip(net.pairs(), g.pairs(), opt.m.pairs(), opt.v.pairs()):
         for j in range(2):
-            one(net.layers[i][j], g.layers[i][j], opt.m.layers[i][j], opt.v.layers[i][j])
+            one(p[j], gp[j], mp[j], vp[j])
     one(net.log_std, g.log_std, opt.m.log_std, opt.v.log_std)
 
 
@@ -474,7 +503,7 @@ class SacSt:
 
 def polyak(target: Net, online: Net, tau: float) -> None:
     """target <- (1-tau) target + tau online, in place (R:algos/sac.py:100-108)."""
-    for tp, op in zip(target.layers, online.layers):
+    for tp, op in zip(target.pairs(), online.pairs()):
         for j in range(2):
             tp[j] *= 1.0 - tau
             tp[j] += tau * op[j]

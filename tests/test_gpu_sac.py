@@ -143,3 +143,46 @@ def test_sac_data_parallel_two_ranks_match_single_process(golden):
                 np.testing.assert_allclose(a.flat(), b.flat(), atol=2e-6)
             assert st.params.log_alpha == pytest.approx(ref.params.log_alpha, abs=1e-9)
         np.testing.assert_array_equal(ranks[0].params.q1.flat(), ranks[1].params.q1.flat())
+
+
+@pytest.mark.parametrize("prec,tol,patol", [("fp32", 3e-5, 2e-5), ("bf16", 2e-2, 3e-3)])
+def test_sac_layernorm_critics_match_oracle(prec, tol, patol):
+    """cfg3's FastSAC critics carry LayerNorm (extension; the oracle's LN is
+    FD-pinned): four updates with LN twin critics track the oracle's
+    LN-extended sac_update (losses, and every parameter set incl. g / beta)."""
+    from oracle import port as O
+
+    P.set_precision(prec)
+    od, ad, hid, n = 12, 4, (64, 32), 256
+    rng = np.random.default_rng(3)
+    a0 = O.net_init((od, *hid, ad), 0)
+    q0 = [O.net_init((od + ad, *hid, 1), s, layer_norm=True) for s in (1, 2)]
+    for q in q0:  # non-trivial gains / shifts
+        for g, b in q.ln:
+            g[:] = rng.uniform(0.5, 1.5, g.shape)
+            b[:] = rng.normal(0, 0.2, b.shape)
+    ocfg = O.SacCfg(policy_frequency=2)
+    ost = O.SacSt.create(a0.clone(), q0[0].clone(), q0[1].clone(), ocfg)
+    cfg = A.SacConfig(policy_frequency=2, batch_size=n)
+    qa = TN.Arch(od + ad, hid, 1, layer_norm=True)
+    st = A.SacState.create(TN.ModelParams.from_numpy(TN.Arch(od, hid, ad), a0.flat()),
+                           TN.ModelParams.from_numpy(qa, q0[0].flat()),
+                           TN.ModelParams.from_numpy(qa, q0[1].flat()), cfg)
+    r_ref, r_got = O.philox_stream(5, "learner"), O.philox_stream(5, "learner")
+    for s in range(4):
+        batch = dict(obs=rng.normal(size=(n, od)).astype(np.float32),
+                     action=np.tanh(rng.normal(size=(n, ad))).astype(np.float32),
+                     reward=rng.normal(size=n).astype(np.float32),
+                     next_obs=rng.normal(size=(n, od)).astype(np.float32),
+                     terminated=rng.random(n) < 0.05, n_used=np.ones(n, np.int64))
+        want = O.sac_update(batch, ost, ocfg, r_ref)
+        got = A.sac_update(batch, st, cfg, r_got).extra
+        for k in want:
+            assert got[k] == pytest.approx(want[k], rel=tol, abs=tol * 1e-1), (s, k)
+        p = st.params
+        for mine, ref in ((p.actor, ost.actor), (p.q1, ost.q1), (p.q2, ost.q2),
+                          (p.q1_targ, ost.q1t), (p.q2_targ, ost.q2t)):
+            # patol: bf16 activations may flip the sign of near-zero Adam
+            # steps (|step| <= lr = 3e-4 per update)
+            d = np.abs(mine.flat() - ref.flat()).max()
+            assert d < patol, (s, d)
