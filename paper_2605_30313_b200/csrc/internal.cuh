@@ -87,6 +87,8 @@ struct GemmDesc {
   int* csum_nz = nullptr;
 };
 constexpr int kCsumMaxN = 512;
+// widest input-gradient column slice the skinny dX path takes (SAC dQ/da)
+constexpr int kSkinnyDxMax = 32;
 int gemm_f32(const GemmDesc& d, cudaStream_t s);
 // number of K splits gemm_f32 actually launches for a requested split count
 int gemm_num_splits(int64_t K, int splits);

@@ -188,6 +188,15 @@ __global__ void __launch_bounds__(256) colsum_kernel(const T* __restrict__ x, in
 
 // fp32 rows -> bf16 rows (the upstream gradient of a wide output layer on the
 // bf16 path)
+// out[j][c] = W[c][col0 + j]: the input-gradient column slice, transposed
+__global__ void slice_t_kernel(const float* __restrict__ W, int ldw, int col0, int nc, int K,
+                               float* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nc * K) return;
+  const int c = (int)(e % K), j = (int)(e / K);
+  out[e] = W[(int64_t)c * ldw + col0 + j];
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, int64_t ldx, int64_t M,
                                    int64_t N, __nv_bfloat16* __restrict__ y, int64_t ldy) {
   const int64_t total = M * N;
@@ -328,7 +337,9 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
       const int64_t q = ln_part_floats(M, v.dims[i]);
       lnp = q > lnp ? q : lnp;
     }
-  return 2 * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk + lnp;
+  // + the transposed W column slice of the skinny input-gradient path
+  return 2 * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk + rup(lnp, 64) +
+         rup((int64_t)kSkinnyDxMax * v.dims[1], 64);
 }
 
 // hidden layer i's activation rows (byte offsets: bf16 rows are half as wide)
@@ -578,6 +589,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     int db_done;  // layer whose db the layer above already produced (skinny column sums)
     float* sk_part;
     float* ln_part;
+    float* dxw;
   } st[2];
   ReduceJob pend[8];  // deferred reductions (skinny heads, column sums, LayerNorm) for the next reduce launch
   int npend = 0;
@@ -587,14 +599,24 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     const MlpNet& N = nets[k];
     const NetView& v = *N.v;
     UL_CHECK_ARG(dt == kF32 || N.wp, "bf16 MLP needs staged weights");
-    UL_CHECK_ARG(dt == kF32 || N.dx == nullptr,
-                 "bf16 MLP backward: input gradients (dx) need the fp32 / tf32 back end");
+    UL_CHECK_ARG(dt == kF32 || N.dx == nullptr || N.dx_ncols <= kSkinnyDxMax,
+                 "bf16 MLP backward: input gradients (dx) wider than %d columns need the fp32 "
+                 "/ tf32 back end", kSkinnyDxMax);
     const int64_t H = max_hidden_ld(v);
     st[k].dh_buf[0] = N.work;
     st[k].dh_buf[1] = N.work + M * H;
     st[k].ws = N.work + 2 * M * H;
     st[k].sk_part = st[k].ws + dw_ws_floats(v, M);
     st[k].ln_part = st[k].sk_part + sk_ws_floats(v, M);
+    {
+      int64_t lnp = 0;
+      if (v.ln)
+        for (int i = 1; i < v.n_layers; ++i) {
+          const int64_t q = ln_part_floats(M, v.dims[i]);
+          lnp = q > lnp ? q : lnp;
+        }
+      st[k].dxw = st[k].ln_part + rup(lnp, 64);
+    }
     st[k].dh = N.dout;
     st[k].lddh = N.ld_dout;
     st[k].dh_f32 = true;
@@ -774,6 +796,21 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
         const MlpNet& N = nets[k];
         if (N.dx == nullptr) continue;
         const NetView& v = *N.v;
+        const int dxdt = st[k].dh_f32 ? kF32 : dt;
+        const int dxeb = dxdt == kBf16 ? 2 : 4;
+        if (N.dx_ncols <= kSkinnyDxMax && skinny_ok(N.dx_ncols, v.dims[1]) &&
+            al16(st[k].dh, st[k].lddh, dxeb)) {
+          // few input columns (SAC's dQ/da): dX = dh W[:, cols] as a skinny
+          // product over the once-transposed column slice, one read of dh
+          const int64_t tot = (int64_t)N.dx_ncols * v.dims[1];
+          slice_t_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, L.of(k)>>>(
+              N.params + v.w_off[0], v.dims[0], N.dx_col0, N.dx_ncols, v.dims[1], st[k].dxw);
+          UL_TRY(check_launch("slice_t_kernel"));
+          UL_TRY(skinny_fwd(st[k].dh, st[k].lddh, M, v.dims[1], N.dx_ncols, st[k].dxw, nullptr,
+                            N.dx, N.lddx, dxdt, L.of(k)));
+          continue;
+        }
+        UL_CHECK_ARG(dxdt == kF32, "bf16 MLP backward: dx GEMM needs fp32 rows");
         GemmDesc G{};
         G.M = M; G.N = N.dx_ncols; G.K = v.dims[1];
         G.A = st[k].dh; G.lda = st[k].lddh; G.B = N.params + v.w_off[0] + N.dx_col0;

@@ -524,12 +524,13 @@ int sac_critic_grads(SacPlan* p, cudaStream_t s) {
   const int be = p->d.gemm_backend;
   const int64_t B = p->B, D = p->D, A = p->A;
   const float* ls = b.actor + p->va.logstd_off;
-  if (be == 1) {
-    UL_TRY(stage_weights(p->va, b.actor, p->ws_a, s));
-    UL_TRY(stage_weights(p->vq, b.q1, p->ws_q1, s));
-    UL_TRY(stage_weights(p->vq, b.q2, p->ws_q2, s));
-    UL_TRY(stage_weights(p->vq, b.q1t, p->ws_q1t, s));
-    UL_TRY(stage_weights(p->vq, b.q2t, p->ws_q2t, s));
+  if (be != 0) {  // tensor-core back ends read 16-B-row staged (tf32 / bf16) weights
+    const int wd = backend_dtype(be);
+    UL_TRY(stage_weights_dt(p->va, b.actor, p->ws_a, wd, s));
+    UL_TRY(stage_weights_dt(p->vq, b.q1, p->ws_q1, wd, s));
+    UL_TRY(stage_weights_dt(p->vq, b.q2, p->ws_q2, wd, s));
+    UL_TRY(stage_weights_dt(p->vq, b.q1t, p->ws_q1t, wd, s));
+    UL_TRY(stage_weights_dt(p->vq, b.q2t, p->ws_q2t, wd, s));
   }
   // ---- K10 target
   UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, p->qn, p->ldq, B, p->acts_a, p->mean, A, s));
@@ -575,9 +576,9 @@ int sac_actor_grads(SacPlan* p, cudaStream_t s) {
   const int be = p->d.gemm_backend;
   const int64_t B = p->B, D = p->D, A = p->A;
   const float* ls = b.actor + p->va.logstd_off;
-  if (be == 1) {
-    UL_TRY(stage_weights(p->vq, b.q1, p->ws_q1, s));
-    UL_TRY(stage_weights(p->vq, b.q2, p->ws_q2, s));
+  if (be != 0) {  // the critics just took their Adam step
+    UL_TRY(stage_weights_dt(p->vq, b.q1, p->ws_q1, backend_dtype(be), s));
+    UL_TRY(stage_weights_dt(p->vq, b.q2, p->ws_q2, backend_dtype(be), s));
   }
   const float* eps2 = p->eps + B * A;
   UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, B, p->acts_a, p->mean, A, s));

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThr) skinny_fwd_kernel(const TH* __restrict__
   if (gr < M) {
 #pragma unroll
     for (int j = 0; j < NP; ++j)
-      if ((j & 3) == q && j < N) out[gr * ldo + j] = acc[j] + __ldg(b + j);
+      if ((j & 3) == q && j < N) out[gr * ldo + j] = acc[j] + (b ? __ldg(b + j) : 0.f);
   }
 }
 

@@ -70,7 +70,8 @@ def _rel(got, ref):
 @pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
 @pytest.mark.parametrize("dims,rows", [((235, (512, 256, 128), 12), 1000),
                                        ((48, (256, 256), 1), 4096),
-                                       ((20, (64,), 4), 37)])
+                                       ((20, (64,), 4), 37),
+                                       ((16, (1028, 100), 3), 300)])  # generic LN kernels
 def test_ln_mlp_matches_oracle(prec, dims, rows):
     inp, hid, outd = dims
     arch = TN.Arch(input_dim=inp, hidden_dims=hid, output_dim=outd, layer_norm=True)
