@@ -161,9 +161,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
 
 // ELU on the tensor-core path: exp via ex2.approx (abs. error ~1e-7 near 0,
 // far inside the tf32/bf16 GEMM error; the fp32 parity path keeps expm1f)
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 4 instructions: FMUL, MUFU.EX2, FSETP, predicated FADD (very negative z
+// flushes to exp = 0; large positive z selects z)
 __device__ __forceinline__ float elu_fast(float z) {
-  const float e = __expf(fmaxf(z, -60.f)) - 1.f;
-  return z > 0.f ? z : e;
+  const float e = ex2_ftz(z * 1.4426950408889634f);
+  return z > 0.f ? z : e - 1.f;
 }
 
 // ELU of two values with one packed f16x2 MUFU.EX2 (half the SFU work of two
@@ -236,10 +243,9 @@ struct Smem {
   // B-resident: the ring streams A only; B's K tiles sit in smem for the
   // whole kernel (runtime-sized region after the ring)
   static constexpr int kStageBytes = kABytes + (BRES ? 0 : kBBytes);
-  // bf16 outputs double-buffer each warp's staging box (a chunk's TMA store
-  // reads one while the next chunk fills the other); fp32 boxes are single
-  static constexpr int kStg = OB == 2 ? 2 : 1;
-  static constexpr int kStagingBytes = kEpiWarps * kStg * 32 * 32 * OB;
+  // each epilogue warp double-buffers a 32-row x 64-byte staging box (a
+  // box's TMA store reads one while the next box fills the other)
+  static constexpr int kStagingBytes = kEpiWarps * 2 * 32 * 64;
   // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
   static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
   static constexpr int kFixed =
@@ -330,11 +336,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   constexpr uint32_t kChunkBytes = (uint32_t)BK * 128;  // one MN-major TMA box
   constexpr int kStages = S::kStages;
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
-  constexpr uint32_t kBoxBytes = 32 * 32 * sizeof(TO);
+  constexpr uint32_t kBoxBytes = 32 * 64;  // one epilogue staging box
   static_assert(kStages >= 2, "shared memory too small for the pipeline");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1 KB-aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared state space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   const uint32_t bres_bytes = BRES ? (uint32_t)p0_.bres_kt * S::kBBytes : 0u;
   uint8_t* sbres = smem + kStages * S::kStageBytes;  // B-resident K tiles
   uint8_t* staging = sbres + bres_bytes;
@@ -551,16 +558,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     // 16 warps: TMEM lane quarter = warp % 4 (hardware rule), column slice =
-    // (warp - 2) / 4 of four BN/4-wide slices.  Per 32-column group each warp
-    // owns a 32 x 32 staging tile (fp32: 4 KB, 128 B swizzle; bf16: 2 KB,
-    // 64 B swizzle): the ELU-gradient operand arrives there by TMA, results
-    // leave by TMA store (full lines instead of thread-per-row scattered
-    // stores).
+    // (warp - 2) / 4 of four BN/4-wide slices.  Each warp owns two 32-row x
+    // 64-byte staging boxes (64 B swizzle; bf16: 32 columns, fp32: 16) used
+    // alternately: the ELU-gradient operand arrives in a box by TMA, results
+    // leave it by TMA store while the next box fills.  Values are computed
+    // 16 columns at a time (one tcgen05.ld x16) so the ELU math never holds
+    // more than 16 accumulators live (no register spills at 96 registers).
+    constexpr int kBoxC = 64 / (int)sizeof(TO);  // columns per staging box
     const int ew = warp - 2;
     const int quarter = warp & 3;
     const int slice = ew >> 2;
     const int row = quarter * 32 + lane;
     constexpr int kSlice = BN / 4;
+    constexpr int kBiasPer = kSlice / 32;  // bias values each lane stages per tile
     float* sbias = reinterpret_cast<float*>(tmem_slot + 4);
     // column sums of the ELU-gradient output (the bias gradient of the layer
     // below): csum_s[quarter][n]; each (quarter, n) has exactly one writer
@@ -577,8 +587,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t* abar = aux_bar + ew;
     uint32_t aphase = 0;
     int local = 0;
-    int cj = 0;  // this warp's chunk counter (staging buffer = cj % kStg)
-    // diagnostics: epilogue warp 0, tiles 0-1, chunks 0-1 -> trace slots 100..
+    int cj = 0;  // this warp's box counter (staging buffer = cj & 1)
+    // bias of the next tile, loaded one tile ahead so its global latency hides
+    // behind the current tile's epilogue
+    float bnext[kBiasPer];
+    auto load_bias = [&](int t) {
+      if (t >= ngroups) return;
+      const Tile T = tile_of(t);
+      const TcArgs& p = T.pr ? p1_ : p0_;
+#pragma unroll
+      for (int j = 0; j < kBiasPer; ++j) {
+        const int n = T.n0 + slice * kSlice + j * 32 + lane;
+        bnext[j] = n < p.N ? __ldg(p.bias + n) : 0.f;
+      }
+    };
+    if (EPI == kEpiBias || EPI == kEpiBiasElu) load_bias(cl);
+    // diagnostics: epilogue warp 0, tiles 0-1, boxes 0-3 -> trace slots 100..
 #define UL_ETRACE(k) \
   if (ew == 0 && lane == 0 && local < 2 && cj < 4) trace_at(p0_.trace, 100 + cj * 6 + (k))
     for (int t = cl; t < ngroups; t += ncl, ++local) {
@@ -590,11 +614,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int b = local & 1;
       const bool have = T.kt_n > 0;
       if (EPI == kEpiBias || EPI == kEpiBiasElu) {
-        for (int c = lane; c < kSlice; c += 32) {
-          const int n = n0 + slice * kSlice + c;
-          sbias[b * BN + slice * kSlice + c] = n < p.N ? __ldg(p.bias + n) : 0.f;
-        }
+#pragma unroll
+        for (int j = 0; j < kBiasPer; ++j) sbias[b * BN + slice * kSlice + j * 32 + lane] = bnext[j];
         __syncwarp();
+        load_bias(t + ncl);
       }
       if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
       if (ew == 0 && lane == 0 && local < 16) trace_at(p0_.trace, 66 + local);
@@ -603,13 +626,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int crow = m0 + quarter * 32;  // row of this warp's 32-row box in C (split z)
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
-      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += 32, ++cj) {
-        uint8_t* stg = staging + (ew * S::kStg + cj % S::kStg) * kBoxBytes;
-        // this staging box free again (the TMA store issued from it has read it)
-        if (lane == 0) {
-          if (S::kStg == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
+      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += kBoxC, ++cj) {
+        uint8_t* stg = staging + (ew * 2 + (cj & 1)) * kBoxBytes;
+        // this staging box free again (the TMA store issued from it two boxes
+        // ago has read it)
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         UL_ETRACE(0);
         if (EPI == kEpiEluGrad) {
@@ -618,75 +639,94 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tma_load_3d(stg, tX, abar, n0 + c0, m0 + quarter * 32, 0);
           }
         }
-        float v[32];
-        if (have) {
-          tmem_ld16(taddr + (uint32_t)c0, *reinterpret_cast<float(*)[16]>(v));
-          tmem_ld16(taddr + (uint32_t)(c0 + 16), *reinterpret_cast<float(*)[16]>(v + 16));
-          UL_ETRACE(1);
-        } else {
+        // 32 rows x 64 B, 64 B swizzle: 16 B granule q of row r at q ^ ((r >> 1) & 3)
+        uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
+        const int sw = (lane >> 1) & 3;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        }
-        if (EPI == kEpiBias || EPI == kEpiBiasElu) {
-          const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + c0);
+        for (int h = 0; h < kBoxC / 16; ++h) {
+          const int cc = c0 + 16 * h;  // first column of these 16
+          float v[16];
+          if (have) {
+            tmem_ld16(taddr + (uint32_t)cc, v);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float4 q = bv[i];
-            v[4 * i] += q.x;
-            v[4 * i + 1] += q.y;
-            v[4 * i + 2] += q.z;
-            v[4 * i + 3] += q.w;
+            for (int i = 0; i < 16; ++i) v[i] = 0.f;
           }
-        }
-        if (EPI == kEpiBiasElu) {
-          // (a packed f16x2 MUFU variant, elu_pair_f16, measured no faster)
+          if (h == 0) UL_ETRACE(1);
+          if (EPI == kEpiBias || EPI == kEpiBiasElu) {
+            const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + cc);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = elu_fast(v[i]);
-        }
-        UL_ETRACE(2);
-        if constexpr (!kOutBf16) {
-          // 32 rows x 128 B, 128 B swizzle: 16 B granule q of row r at q ^ (r & 7)
-          float4* srow = reinterpret_cast<float4*>(stg + lane * 128);
-          if (EPI == kEpiEluGrad) {
-            mbar_wait(abar, aphase);
-            aphase ^= 1;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 h4 = srow[q ^ (lane & 7)];
-              v[4 * q] *= elu_grad_from_act(h4.x);
-              v[4 * q + 1] *= elu_grad_from_act(h4.y);
-              v[4 * q + 2] *= elu_grad_from_act(h4.z);
-              v[4 * q + 3] *= elu_grad_from_act(h4.w);
+            for (int i = 0; i < 4; ++i) {
+              const float4 q = bv[i];
+              v[4 * i] += q.x;
+              v[4 * i + 1] += q.y;
+              v[4 * i + 2] += q.z;
+              v[4 * i + 3] += q.w;
             }
           }
+          if (EPI == kEpiBiasElu) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            srow[q ^ (lane & 7)] =
-                make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-          // 32 rows x 64 B, 64 B swizzle: 16 B granule q of row r at q ^ ((r >> 1) & 3)
-          uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
-          const int sw = (lane >> 1) & 3;
-          if (EPI == kEpiEluGrad) {
+            for (int i = 0; i < 16; ++i) v[i] = elu_fast(v[i]);
+          }
+          if (EPI == kEpiEluGrad && h == 0) {
             mbar_wait(abar, aphase);
             aphase ^= 1;
+          }
+          if (h == 0) UL_ETRACE(2);
+          if constexpr (!kOutBf16) {
+            // 4 granules of 4 floats
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint4 h = srow[q ^ sw];
-              const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                v[8 * q + 2 * e] *= elu_grad_from_act(bf_lo(hw[e]));
-                v[8 * q + 2 * e + 1] *= elu_grad_from_act(bf_hi(hw[e]));
+              float4* g = reinterpret_cast<float4*>(srow + (q ^ sw));
+              if (EPI == kEpiEluGrad) {
+                const float4 h4 = *g;
+                v[4 * q] = fmaf(v[4 * q], fminf(h4.x, 0.f), v[4 * q]);
+                v[4 * q + 1] = fmaf(v[4 * q + 1], fminf(h4.y, 0.f), v[4 * q + 1]);
+                v[4 * q + 2] = fmaf(v[4 * q + 2], fminf(h4.z, 0.f), v[4 * q + 2]);
+                v[4 * q + 3] = fmaf(v[4 * q + 3], fminf(h4.w, 0.f), v[4 * q + 3]);
               }
+              *g = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+          } else {
+            // granules 2h, 2h + 1 of 8 bf16
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int q = 2 * h + j;
+              if (EPI == kEpiEluGrad) {
+                const uint4 hq = srow[q ^ sw];
+                const uint32_t hw[4] = {hq.x, hq.y, hq.z, hq.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  // v * elu'(h) = v * (min(h, 0) + 1) = fma(v, min(h, 0), v)
+                  v[8 * j + 2 * e] = fmaf(v[8 * j + 2 * e], fminf(bf_lo(hw[e]), 0.f), v[8 * j + 2 * e]);
+                  v[8 * j + 2 * e + 1] =
+                      fmaf(v[8 * j + 2 * e + 1], fminf(bf_hi(hw[e]), 0.f), v[8 * j + 2 * e + 1]);
+                }
+              }
+              srow[q ^ sw] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]),
+                                        pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                        pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                                        pack_bf16(v[8 * j + 6], v[8 * j + 7]));
             }
           }
+          if (csum_on && T.pr == cs_pr) {
+            // butterfly reduce-scatter over the warp's 32 rows: afterwards
+            // lanes l and l ^ 16 hold the sum of column cc + (l & 15) (rows
+            // >= M contribute zeros)
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            srow[q ^ sw] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]),
-                                      pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                                      pack_bf16(v[8 * q + 4], v[8 * q + 5]),
-                                      pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+            for (int wd = 8; wd >= 1; wd >>= 1) {
+              const bool up = (lane & wd) != 0;
+#pragma unroll
+              for (int i = 0; i < wd; ++i) {
+                const float send = up ? v[i] : v[i + wd];
+                const float keep = up ? v[i + wd] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
+              }
+            }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+            const int n = n0 + cc + lane;
+            if (lane < 16 && n < kCsumMaxN) csum_s[quarter * kCsumMaxN + n] += v[0];
+          }
         }
         UL_ETRACE(3);
         if (p.tma_store) {
@@ -702,63 +742,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         } else {
-          // coalesced 16-byte stores straight from the staging tile: the warp
+          // coalesced 16-byte stores straight from the staging box: the warp
           // never waits on an async store engine shared with the operand loads
           __syncwarp();
           const int rows_ok = p.M - crow;  // rows of this warp's box inside M
+          constexpr int kPer = 16 / (int)sizeof(TO);  // elements per granule
           TO* cb = reinterpret_cast<TO*>(p.C) + ((int64_t)z * p.M + crow) * p.ldc + n0 + c0;
-          if constexpr (!kOutBf16) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = i * 4 + (lane >> 3), g = lane & 7;
-              if (r < rows_ok) {
-                const float4 val = reinterpret_cast<const float4*>(stg + r * 128)[g ^ (r & 7)];
-                float* dst = reinterpret_cast<float*>(cb) + (int64_t)r * p.ldc + 4 * g;
-                const int col = n0 + c0 + 4 * g;
-                if (col + 4 <= p.N) {
-                  *reinterpret_cast<float4*>(dst) = val;
-                } else {
-                  const float e4[4] = {val.x, val.y, val.z, val.w};
-                  for (int e = 0; e < 4 && col + e < p.N; ++e) dst[e] = e4[e];
-                }
-              }
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int r = i * 8 + (lane >> 2), g = lane & 3;
-              if (r < rows_ok) {
-                const uint4 val = reinterpret_cast<const uint4*>(stg + r * 64)[g ^ ((r >> 1) & 3)];
-                __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(cb) + (int64_t)r * p.ldc + 8 * g;
-                const int col = n0 + c0 + 8 * g;
-                if (col + 8 <= p.N) {
-                  *reinterpret_cast<uint4*>(dst) = val;
-                } else {
-                  const __nv_bfloat16* e8 = reinterpret_cast<const __nv_bfloat16*>(&val);
-                  for (int e = 0; e < 8 && col + e < p.N; ++e) dst[e] = e8[e];
-                }
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2), g = lane & 3;
+            if (r < rows_ok) {
+              const uint4 val = reinterpret_cast<const uint4*>(stg + r * 64)[g ^ ((r >> 1) & 3)];
+              TO* dst = cb + (int64_t)r * p.ldc + kPer * g;
+              const int col = n0 + c0 + kPer * g;
+              if (col + kPer <= p.N) {
+                *reinterpret_cast<uint4*>(dst) = val;
+              } else {
+                const TO* e8 = reinterpret_cast<const TO*>(&val);
+                for (int e = 0; e < kPer && col + e < p.N; ++e) dst[e] = e8[e];
               }
             }
           }
-          __syncwarp();  // staging reads done before the next chunk reuses it
+          __syncwarp();  // staging reads done before the box is reused
         }
         UL_ETRACE(4);
-        if (csum_on && T.pr == cs_pr) {
-          // butterfly reduce-scatter over the warp's 32 rows: afterwards lane
-          // l holds the sum of column c0 + l (rows >= M contribute zeros)
-#pragma unroll
-          for (int wd = 16; wd >= 1; wd >>= 1) {
-            const bool up = (lane & wd) != 0;
-#pragma unroll
-            for (int i = 0; i < wd; ++i) {
-              const float send = up ? v[i] : v[i + wd];
-              const float keep = up ? v[i + wd] : v[i];
-              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
-            }
-          }
-          const int n = n0 + c0 + lane;
-          if (n < kCsumMaxN) csum_s[quarter * kCsumMaxN + n] += v[0];
-        }
       }
 #undef UL_ETRACE
       if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M) {
@@ -900,16 +907,17 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   const GemmDesc& d = *q.d;
   const CUtensorMapSwizzle mn_sw =
       eb == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
-  const CUtensorMapSwizzle out_sw = ob == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapSwizzle out_sw = CU_TENSOR_MAP_SWIZZLE_64B;  // 64-byte box rows
+  const int boxc = 64 / ob;
   // A(m,k): K-major -> rows=M, inner=K ; MN-major -> rows=K, inner=M
   if (A_MN) UL_TRY(make_map(&m->a, d.A, eb, d.M, d.K, d.lda, O::kChunk, O::BK, mn_sw));
   else UL_TRY(make_map(&m->a, d.A, eb, d.K, d.M, d.lda, O::BK, BM, CU_TENSOR_MAP_SWIZZLE_128B));
   if (B_MN) UL_TRY(make_map(&m->b, d.B, eb, d.N, d.K, d.ldb, O::kChunk, O::BK, mn_sw));
   else  // one CTA's share of the B tile
     UL_TRY(make_map(&m->b, d.B, eb, d.K, d.N, d.ldb, O::BK, BN / CS, CU_TENSOR_MAP_SWIZZLE_128B));
-  // C (and split-K partials [splits][M][ldc]) stored by 32x32 TMA boxes
-  UL_TRY(make_map(&m->c, d.C, ob, d.N, d.M, d.ldc, 32, 32, out_sw, q.zs));
-  if (EPI == kEpiEluGrad) UL_TRY(make_map(&m->x, d.aux, ob, d.N, d.M, d.ldaux, 32, 32, out_sw, 1));
+  // C (and split-K partials [splits][M][ldc]) stored by 32-row x 64-byte TMA boxes
+  UL_TRY(make_map(&m->c, d.C, ob, d.N, d.M, d.ldc, boxc, 32, out_sw, q.zs));
+  if (EPI == kEpiEluGrad) UL_TRY(make_map(&m->x, d.aux, ob, d.N, d.M, d.ldaux, boxc, 32, out_sw, 1));
   else m->x = m->c;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
   *a = TcArgs{(int)d.M, (int)d.N, (int)d.K, q.kps, mt, nt, q.zs, d.C, d.ldc, d.bias,

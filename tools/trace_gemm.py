@@ -72,6 +72,12 @@ def main():
                                   w2.stride(0), P(h2), h2.stride(0), P(b), None, 0, 1, DT,
                                   _dev.stream()))
     dh = torch.randn(rows, _lda(512), device=dev).to(EL)
+    wt = (torch.randn(512, _lda(256), device=dev) * 0.05).to(EL)
+    dh1 = torch.randn(rows, _lda(256), device=dev).to(EL)
+    dx = torch.empty(rows, _lda(512), device=dev, dtype=EL)
+    run("dx1", lambda: _lib.call("ul_gemm_tc", 1, 3, rows, 512, 256, P(dh1), dh1.stride(0), P(wt),
+                                 wt.stride(0), P(dx), dx.stride(0), None, P(h), h.stride(0), 1,
+                                 DT, _dev.stream()))
     C_ = torch.empty(40, 512, 236, device=dev)
     run("dw0", lambda: _lib.call("ul_gemm_tc", 0, 0, 512, 236, rows, P(dh), dh.stride(0), P(x),
                                  x.stride(0), P(C_), 236, None, None, 0, 37, DT, _dev.stream()))
