@@ -310,10 +310,19 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
 // CTAs' TMA loads complete on the leader's full barrier; the leader's commits
 // are multicast to both CTAs' empty / accumulator barriers; both epilogues
 // drain their own TMEM lanes and release the accumulator on the leader.
-// Up to two independent problems (the actor's and the critic's layer) share
-// one launch: tile groups [0, ng0) belong to problem 0, the rest to problem 1.
+// Up to kMaxProb independent problems (the actor's and the critic's layer,
+// or every deferred dW GEMM of a backward pass) share one launch: tile groups
+// [end[i-1], end[i]) belong to problem i.
 struct TcMaps {
   CUtensorMap a, b, c, x;
+};
+constexpr int kMaxProb = 8;
+struct TcBatch {
+  TcMaps m[kMaxProb];
+  TcArgs a[kMaxProb];
+  int end[kMaxProb];  // prefix sums of the problems' tile-group counts
+  int np, ngroups;
+  int cs_pr;          // problem whose epilogue emits column sums, or -1
 };
 
 // BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
@@ -322,9 +331,9 @@ struct TcMaps {
 // the 48 KB/stage ring for the forward and dX GEMMs (K = 128..256).
 template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR, bool BRES>
 __global__ void __launch_bounds__(kPThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ TcMaps m0_, const __grid_constant__ TcMaps m1_,
-                   const __grid_constant__ TcArgs p0_, const __grid_constant__ TcArgs p1_,
-                   int ng0, int ngroups) {
+    tc_gemm_kernel(const __grid_constant__ TcBatch B) {
+  const TcArgs& p0_ = B.a[0];
+  const int ngroups = B.ngroups;
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
   using S = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
@@ -377,11 +386,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&m0_.a) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&m0_.b) : "memory");
-    if (ngroups > ng0) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&m1_.a) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(&m1_.b) : "memory");
+    for (int i = 0; i < B.np; ++i) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&B.m[i].a) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&B.m[i].b) : "memory");
     }
   }
   if (warp == 1) {
@@ -412,9 +419,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
   };
   auto tile_of = [&](int t) {
     Tile T;
-    T.pr = t < ng0 ? 0 : 1;
-    const TcArgs& P = T.pr ? p1_ : p0_;
-    const int tl = T.pr ? t - ng0 : t;
+    T.pr = 0;
+    while (T.pr < B.np - 1 && t >= B.end[T.pr]) ++T.pr;
+    const TcArgs& P = B.a[T.pr];
+    const int tl = T.pr ? t - B.end[T.pr - 1] : t;
     const int mg = (P.mt + CS - 1) / CS;
     if (BRES) {  // N fastest: the grid is a multiple of nt, so a CTA keeps one N tile
       T.z = 0;
@@ -445,19 +453,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if (B_MN) {
 #pragma unroll
             for (int c = 0; c < BN / O::kChunk; ++c)
-              tma_load_2d(sb + c * kChunkBytes, &m0_.b, bres_bar, T0.n0 + O::kChunk * c,
+              tma_load_2d(sb + c * kChunkBytes, &B.m[0].b, bres_bar, T0.n0 + O::kChunk * c,
                           kt * BK);
           } else {
-            tma_load_2d(sb, &m0_.b, bres_bar, kt * BK, T0.n0);
+            tma_load_2d(sb, &B.m[0].b, bres_bar, kt * BK, T0.n0);
           }
         }
       }
       for (int t = cl; t < ngroups; t += ncl) {
         const Tile T = tile_of(t);
         const int m0 = T.m0, n0 = T.n0, kt_n = T.kt_n;
-        const TcArgs& P = T.pr ? p1_ : p0_;
-        const CUtensorMap* tA = T.pr ? &m1_.a : &m0_.a;
-        const CUtensorMap* tB = T.pr ? &m1_.b : &m0_.b;
+        const TcArgs& P = B.a[T.pr];
+        const CUtensorMap* tA = &B.m[T.pr].a;
+        const CUtensorMap* tB = &B.m[T.pr].b;
         const int nb0 = n0 + (int)crank * BNL;  // first B row (N) of this CTA's share
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
@@ -577,9 +585,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // warp -- the one with this quarter and n's slice -- so no atomics and a
     // fixed summation order.  Each warp zeroes the entries it owns.
     float* csum_s = sbias + 2 * BN;
-    const TcArgs& pcs = p0_.csum ? p0_ : p1_;
-    const int cs_pr = p0_.csum ? 0 : 1;
-    const bool csum_on = EPI == kEpiEluGrad && pcs.csum != nullptr;
+    const int cs_pr = B.cs_pr;
+    const bool csum_on = EPI == kEpiEluGrad && cs_pr >= 0;
     if (csum_on) {
       for (int n = lane; n < kCsumMaxN; n += 32)
         if ((n % BN) / kSlice == slice) csum_s[quarter * kCsumMaxN + n] = 0.f;
@@ -594,7 +601,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     auto load_bias = [&](int t) {
       if (t >= ngroups) return;
       const Tile T = tile_of(t);
-      const TcArgs& p = T.pr ? p1_ : p0_;
+      const TcArgs& p = B.a[T.pr];
 #pragma unroll
       for (int j = 0; j < kBiasPer; ++j) {
         const int n = T.n0 + slice * kSlice + j * 32 + lane;
@@ -608,9 +615,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     for (int t = cl; t < ngroups; t += ncl, ++local) {
       const Tile T = tile_of(t);
       const int m0 = T.m0, n0 = T.n0, z = T.z;
-      const TcArgs& p = T.pr ? p1_ : p0_;
-      const CUtensorMap* tC = T.pr ? &m1_.c : &m0_.c;
-      const CUtensorMap* tX = T.pr ? &m1_.x : &m0_.x;
+      const TcArgs& p = B.a[T.pr];
+      const CUtensorMap* tC = &B.m[T.pr].c;
+      const CUtensorMap* tX = &B.m[T.pr].x;
       const int b = local & 1;
       const bool have = T.kt_n > 0;
       if (EPI == kEpiBias || EPI == kEpiBiasElu) {
@@ -795,9 +802,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (EPI == kEpiEluGrad && (p0_.csum || p1_.csum)) {
+  if (EPI == kEpiEluGrad && B.cs_pr >= 0) {
     // this CTA's column-sum partial row (quarters in fixed order)
-    const TcArgs& pcs = p0_.csum ? p0_ : p1_;
+    const TcArgs& pcs = B.a[B.cs_pr];
     const float* csum_s = reinterpret_cast<const float*>(tmem_slot + 4) + 2 * BN;
     for (int n = threadIdx.x; n < pcs.ldcs; n += blockDim.x) {
       float v = 0.f;
@@ -933,19 +940,24 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   using TO = OutT<TI, EPI>;
   using SM = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
   constexpr int CS = PAIR ? 2 : 1;
-  TcMaps m[2];
-  TcArgs a[2];
-  int ng[2] = {0, 0};
-  for (int i = 0; i < np; ++i)
-    UL_TRY((make_problem<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>(q[i], &m[i], &a[i], &ng[i])));
-  if (np == 1) {
-    m[1] = m[0];
-    a[1] = a[0];
+  UL_CHECK_ARG(np >= 1 && np <= kMaxProb, "gemm_tc: 1..%d problems per launch", kMaxProb);
+  TcBatch B{};  // ~5 KB kernel parameter block (per call: launches may come from several threads)
+  B.np = np;
+  B.cs_pr = -1;
+  int total = 0;
+  for (int i = 0; i < np; ++i) {
+    int ng = 0;
+    UL_TRY((make_problem<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>(q[i], &B.m[i], &B.a[i], &ng)));
+    total += ng;
+    B.end[i] = total;
+    if (B.a[i].csum && B.cs_pr < 0) B.cs_pr = i;
+    else B.a[i].csum = nullptr;  // one column-sum problem per launch
   }
+  B.ngroups = total;
   auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
-  cfg.dynamicSmemBytes = SM::kBytes + (BRES ? (size_t)a[0].bres_kt * SM::kBBytes : 0);
+  cfg.dynamicSmemBytes = SM::kBytes + (BRES ? (size_t)B.a[0].bres_kt * SM::kBBytes : 0);
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -973,13 +985,12 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     }
     max_clusters = n;
   }
-  const int total = ng[0] + ng[1];
   int grid = (total < max_clusters ? total : max_clusters) * CS;
-  if (BRES) grid = grid / a[0].nt * a[0].nt;  // every CTA keeps one N tile
+  if (BRES) grid = grid / B.a[0].nt * B.a[0].nt;  // every CTA keeps one N tile
   cfg.gridDim = dim3((unsigned)grid);
   for (int i = 0; i < np; ++i)
-    if (q[i].d->csum_nz) *q[i].d->csum_nz = grid;
-  UL_CUDA(cudaLaunchKernelEx(&cfg, kern, m[0], m[1], a[0], a[1], ng[0], total));
+    if (q[i].d->csum_nz) *q[i].d->csum_nz = i == B.cs_pr ? grid : 0;
+  UL_CUDA(cudaLaunchKernelEx(&cfg, kern, B));
   return check_launch("tc_gemm_kernel");
 }
 
@@ -988,7 +999,12 @@ inline int bn_of(const GemmDesc& d) { return d.N > 128 ? 256 : 128; }
 template <typename TI>
 int dispatch(const Prob* q, int np, cudaStream_t s) {
   const GemmDesc& d = *q[0].d;
-  const int bn = bn_of(d);
+  int bn = 128;  // one tile width for the whole batch
+  bool all_two_m = true;
+  for (int i = 0; i < np; ++i) {
+    bn = bn_of(*q[i].d) > bn ? bn_of(*q[i].d) : bn;
+    all_two_m = all_two_m && ceil_div(q[i].d->M, BM) >= 2;
+  }
   const bool amn = !d.a_kmajor, bmn = !d.b_kmajor;
   // CTA pairs (cta_group::2, M = 256 per UMMA) whenever there are two M
   // tiles; UL_TC_PAIR=0 disables them (experiments).
@@ -1000,7 +1016,7 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   // default: pairs for tf32 (4-byte operands: the halved B traffic pays),
   // single CTAs for bf16 (measured faster end to end on the cfg2 update)
   const bool want = pair_ok == -2 ? sizeof(TI) == 4 : pair_ok != 0;
-  const bool pair = want && ceil_div(d.M, BM) >= 2;
+  const bool pair = want && all_two_m;
   // B resident (A streamed alone) when one problem's whole N tile of B fits
   // the smem left over by the 3-stage A ring, and there is no split-K
   static int bres_ok = -1;
@@ -1080,6 +1096,37 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   const tc::Prob q = prob_of(d, ones_col);
   if (d.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(&q, 1, s);
   return tc::dispatch<float>(&q, 1, s);
+}
+
+// Independent GEMMs in as few persistent launches as their compatibility
+// allows: problems sharing dtype, operand layouts and epilogue (at most one
+// with column sums) run as one batch of up to tc::kMaxProb.  Used for the
+// deferred dW GEMMs of a backward pass (every layer of both networks).
+int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s) {
+  bool done[64] = {};
+  UL_CHECK_ARG(n >= 0 && n <= 64, "gemm_tc_batch: at most 64 problems");
+  for (int i = 0; i < n; ++i) done[i] = d[i].M == 0 || d[i].N == 0;
+  for (int i = 0; i < n; ++i) {
+    if (done[i]) continue;
+    tc::Prob q[tc::kMaxProb];
+    int nq = 0;
+    bool cs = false;
+    for (int j = i; j < n && nq < tc::kMaxProb; ++j) {
+      if (done[j]) continue;
+      const GemmDesc& a = d[i];
+      const GemmDesc& b = d[j];
+      const bool csj = b.csum_part != nullptr;
+      if (b.dtype != a.dtype || b.a_kmajor != a.a_kmajor || b.b_kmajor != a.b_kmajor ||
+          b.epi != a.epi || (cs && csj))
+        continue;
+      cs = cs || csj;
+      q[nq++] = prob_of(b, -1);
+      done[j] = true;
+    }
+    if (d[i].dtype == kBf16) UL_TRY(tc::dispatch<__nv_bfloat16>(q, nq, s));
+    else UL_TRY(tc::dispatch<float>(q, nq, s));
+  }
+  return UL_OK;
 }
 
 // Two independent GEMMs (e.g. the actor's and the critic's layer) in one

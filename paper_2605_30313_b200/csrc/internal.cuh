@@ -112,7 +112,24 @@ struct ReduceJob {
   int64_t n0, n1, n2;
   float *o0, *o1, *o2;
 };
-constexpr int kMaxReduceJobs = 4;
+constexpr int kMaxReduceJobs = 16;
+
+// dW GEMMs of a backward pass collected for one batched tensor-core launch
+// (gemm_tc_batch) + one reduction pass of their split partials and the
+// pass's other deferred partial sets (run_deferred_dw, mlp.cu)
+struct DeferredDw {
+  static constexpr int kMax = 16;
+  GemmDesc dw[kMax];
+  int max_splits[kMax];  // split count each layer's workspace region holds
+  int dw_job[kMax];      // jobs[] index of each dW's reduction
+  int ndw = 0;
+  ReduceJob jobs[3 * kMax];
+  int nj = 0;
+  void add(const GemmDesc& g, const ReduceJob& j);
+};
+int run_deferred_dw(DeferredDw& D, cudaStream_t s);
+// independent tensor-core GEMMs, batched into as few launches as compatible
+int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s);
 
 // ------------------------------------------------------------------ MLP
 struct NetView {
@@ -183,8 +200,11 @@ struct MlpNet {
 // 1's small kernels on `side` between fork/join events when side != null)
 int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
+// dd: collector for deferred dW GEMMs (bf16 path) shared between calls -- the
+// caller runs run_deferred_dw after joining; null: the pass runs its own.
 int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
-                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
+                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join,
+                   DeferredDw* dd = nullptr);
 // dx_cols: compute dX only for input columns [dx_col0, dx_col0 + dx_ncols) (SAC dQ/da);
 // want_dw = false skips dW/db (pure input-gradient pass).  x_has_ones: column
 // dims[0] of x holds 1.0 (lets the tensor-core dW of layer 0 produce db).

@@ -172,8 +172,14 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
     UL_TRY(mlp_forward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr));
     UL_TRY(mlp_forward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr));
   } else {
-    UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr));
-    UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr));
+    // bf16: both networks' dW GEMMs are collected and run as one batched
+    // launch (+ one reduction) after the two dX chains join
+    DeferredDw dd;
+    UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr, &dd));
+    UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr, &dd));
+    UL_CUDA(cudaEventRecord(p->ev_join, p->side));
+    UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
+    return run_deferred_dw(dd, s);
   }
   UL_CUDA(cudaEventRecord(p->ev_join, p->side));
   UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
@@ -317,7 +323,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   mark(p, 2, s);
   // K8 backwards of both networks into the contiguous all-reduce buffer
   UL_TRY(mlp_pass(p, nets, be, ml, s, false));
-  mark(p, 0, s);
+  mark(p, 5, s);
   return UL_OK;
 }
 
@@ -586,12 +592,16 @@ extern "C" int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic
   p->prof->on = false;
   UL_TRY(st);
   UL_CUDA(cudaStreamSynchronize(s));
-  for (int c = 0; c < 5; ++c) ms[c] = 0.0;
+  for (int c = 0; c < 6; ++c) ms[c] = 0.0;
   for (int i = 1; i < p->prof->n; ++i) {
     float t = 0.f;
     UL_CUDA(cudaEventElapsedTime(&t, p->prof->ev[i - 1], p->prof->ev[i]));
     const int c = p->prof->cat[i];
     if (c >= 0 && c < 4) ms[c] += t;
+    if (c == 5) {  // MLP backward: counted with the GEMMs and on its own
+      ms[0] += t;
+      ms[5] += t;
+    }
     ms[4] += t;
   }
   return UL_OK;

@@ -306,20 +306,34 @@ static int dw_splits(int64_t out, int64_t in, int64_t M, bool tc) {
   return (int)(sp > 64 ? 64 : sp);
 }
 
-// backward workspace: [2 hidden-gradient buffers][split-K dW + column-sum
-// partials][skinny head partials] -- the head's partials outlive the next
-// layer's dW GEMM (their reduction is folded into that layer's reduction)
+// backward workspace: [hidden-gradient buffers][split-K dW + column-sum
+// partials, one region per layer][skinny head partials][dX column-sum
+// partials, one region per layer][LayerNorm partials][dX column slice].
+// Layer-by-layer backward reuses region 0 and two gradient buffers (the
+// head's partials outlive the next layer's dW GEMM: their reduction is folded
+// into that layer's reduction); the deferred-dW backward keeps every layer's
+// dZ and partials alive until one batched dW launch + one reduction at the end.
+static int64_t dw_layer_floats(const NetView& v, int64_t M, int i) {
+  const int64_t out = v.dims[i + 1], in = v.dims[i];
+  const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
+                     ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
+  return rup((int64_t)sp * (out * rup(in + 1, 4) + out) + 256 * out, 64);
+}
+
 static int64_t dw_ws_floats(const NetView& v, int64_t M) {
   int64_t ws = 0;
-  for (int i = 0; i < v.n_layers; ++i) {
-    const int64_t out = v.dims[i + 1], in = v.dims[i];
-    const int sp = dw_splits(out, in, M, false) > dw_splits(out, in, M, true)
-                       ? dw_splits(out, in, M, false) : dw_splits(out, in, M, true);
-    const int64_t need = (int64_t)sp * (out * rup(in + 1, 4) + out) + 256 * out;
-    ws = need > ws ? need : ws;
-  }
-  return rup(ws, 64);
+  for (int i = 0; i < v.n_layers; ++i) ws += dw_layer_floats(v, M, i);
+  return ws;
 }
+
+static int64_t dw_layer_off(const NetView& v, int64_t M, int i) {
+  int64_t o = 0;
+  for (int j = 0; j < i; ++j) o += dw_layer_floats(v, M, j);
+  return o;
+}
+
+static int n_dh_bufs(const NetView& v) { return v.n_layers > 2 ? v.n_layers : 2; }
+constexpr int64_t kCsRegion = (int64_t)kNumSMs * kCsumMaxN;  // one dX GEMM's column-sum partials
 
 static int64_t sk_ws_floats(const NetView& v, int64_t M) {
   const int last = v.n_layers - 1;
@@ -338,8 +352,8 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
       lnp = q > lnp ? q : lnp;
     }
   // + the transposed W column slice of the skinny input-gradient path
-  return 2 * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk + rup(lnp, 64) +
-         rup((int64_t)kSkinnyDxMax * v.dims[1], 64);
+  return n_dh_bufs(v) * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk +
+         kCsRegion * v.n_layers + rup(lnp, 64) + rup((int64_t)kSkinnyDxMax * v.dims[1], 64);
 }
 
 // hidden layer i's activation rows (byte offsets: bf16 rows are half as wide)
@@ -569,18 +583,67 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
   return UL_OK;
 }
 
+// Deferred dW: collected descs + their reductions, launched as one batched
+// tensor-core launch and one reduction pass (run_deferred_dw).
+void DeferredDw::add(const GemmDesc& g, const ReduceJob& j) {
+  if (ndw >= kMax || nj >= 3 * kMax) return;  // (callers stay far below: 2 nets x UL_MAX_LAYERS)
+  dw[ndw] = g;
+  jobs[nj] = j;
+  dw_job[ndw++] = nj++;
+}
+
+int run_deferred_dw(DeferredDw& D, cudaStream_t s) {
+  if (D.ndw == 0 && D.nj == 0) return UL_OK;
+  if (D.ndw) {
+    // one split count for the batch: about one persistent wave of tile-splits
+    int64_t tiles = 0;
+    for (int i = 0; i < D.ndw; ++i)
+      tiles += ceil_div(D.dw[i].M, 128) * ceil_div(D.dw[i].N, D.dw[i].N > 128 ? 256 : 128);
+    int64_t sp = kNumSMs / (tiles > 0 ? tiles : 1);
+    const int64_t cap = ceil_div(D.dw[0].K, 512);
+    sp = sp < cap ? sp : cap;
+    sp = sp < 1 ? 1 : sp;
+    for (int i = 0; i < D.ndw; ++i) {
+      // never more splits than the layer's workspace region was sized for
+      const int want = (int)(sp < D.max_splits[i] ? sp : D.max_splits[i]);
+      D.dw[i].splits = tc_num_splits(D.dw[i].K, want, D.dw[i].dtype);
+      D.jobs[D.dw_job[i]].nz = D.dw[i].splits;
+    }
+    UL_TRY(gemm_tc_batch(D.dw, D.ndw, s));
+  }
+  UL_TRY(launch_reduce(D.jobs, D.nj, s));
+  D.ndw = D.nj = 0;
+  return UL_OK;
+}
+
 int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
-                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
+                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join, DeferredDw* dd) {
   if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
-    UL_TRY(mlp_backward_n(nets, 1, backend, M, s, nullptr, nullptr, nullptr));
-    return mlp_backward_n(nets + 1, 1, backend, M, s, nullptr, nullptr, nullptr);
+    UL_TRY(mlp_backward_n(nets, 1, backend, M, s, nullptr, nullptr, nullptr, dd));
+    return mlp_backward_n(nets + 1, 1, backend, M, s, nullptr, nullptr, nullptr, dd);
   }
   const Lanes L{s, n == 2 ? side : nullptr, fork, join};
   const int dt = backend_dtype(backend);
   const int eb = dt == kBf16 ? 2 : 4;
   const bool tc = backend >= 1;
+  // Deferred dW (bf16 tensor-core back end, no LayerNorm): the dX chain runs
+  // first and keeps every layer's dZ; all dW GEMMs of the pass (of both
+  // networks when the caller shares its collector) then run as one batched
+  // launch with few K splits, and every partial reduction as one pass.
+  static int defer_env = -1;
+  if (defer_env < 0) {
+    const char* e = getenv("UL_DEFER_DW");
+    defer_env = e ? atoi(e) != 0 : 1;
+  }
+  bool defer = defer_env && tc && dt == kBf16;
+  for (int k = 0; k < n; ++k)
+    defer = defer && nets[k].want_dw && nets[k].wp && !nets[k].v->ln;
+  DeferredDw local_dd;
+  DeferredDw* D = defer ? (dd ? dd : &local_dd) : nullptr;
   struct St {
-    float* dh_buf[2];
+    float* dh_base;  // n_bufs hidden-gradient buffers, dh_stride floats apart
+    int64_t dh_stride;
+    int nbuf;
     float* ws;
     const float* dh;  // fp32 until the first hidden layer, then dt
     int64_t lddh;
@@ -588,10 +651,16 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     int ping;
     int db_done;  // layer whose db the layer above already produced (skinny column sums)
     float* sk_part;
+    float* cs_part;
     float* ln_part;
     float* dxw;
+    float* next() {
+      float* b = dh_base + (int64_t)ping * dh_stride;
+      ping = (ping + 1) % nbuf;
+      return b;
+    }
   } st[2];
-  ReduceJob pend[8];  // deferred reductions (skinny heads, column sums, LayerNorm) for the next reduce launch
+  ReduceJob pend[16];  // deferred reductions (skinny heads, column sums, LayerNorm) for the next reduce launch
   int npend = 0;
   const int nl = nets[0].v->n_layers;
   UL_TRY(L.open());
@@ -603,11 +672,14 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
                  "bf16 MLP backward: input gradients (dx) wider than %d columns need the fp32 "
                  "/ tf32 back end", kSkinnyDxMax);
     const int64_t H = max_hidden_ld(v);
-    st[k].dh_buf[0] = N.work;
-    st[k].dh_buf[1] = N.work + M * H;
-    st[k].ws = N.work + 2 * M * H;
-    st[k].sk_part = st[k].ws + dw_ws_floats(v, M);
-    st[k].ln_part = st[k].sk_part + sk_ws_floats(v, M);
+    St& S = st[k];
+    S.dh_base = N.work;
+    S.dh_stride = M * H;
+    S.nbuf = defer ? n_dh_bufs(v) : 2;
+    S.ws = N.work + n_dh_bufs(v) * M * H;
+    S.sk_part = S.ws + dw_ws_floats(v, M);
+    S.cs_part = S.sk_part + sk_ws_floats(v, M);
+    S.ln_part = S.cs_part + kCsRegion * v.n_layers;
     {
       int64_t lnp = 0;
       if (v.ln)
@@ -615,13 +687,13 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
           const int64_t q = ln_part_floats(M, v.dims[i]);
           lnp = q > lnp ? q : lnp;
         }
-      st[k].dxw = st[k].ln_part + rup(lnp, 64);
+      S.dxw = S.ln_part + rup(lnp, 64);
     }
-    st[k].dh = N.dout;
-    st[k].lddh = N.ld_dout;
-    st[k].dh_f32 = true;
-    st[k].ping = 0;
-    st[k].db_done = -1;
+    S.dh = N.dout;
+    S.lddh = N.ld_dout;
+    S.dh_f32 = true;
+    S.ping = 0;
+    S.db_done = -1;
     if (N.want_dw && N.zero_logstd && N.grads)
       UL_CUDA(cudaMemsetAsync(N.grads + v.logstd_off, 0, sizeof(float) * v.dims[nl], L.of(k)));
   }
@@ -638,8 +710,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       if (!(i == nl - 1 && skinny_ok((int)out, (int)in) && i > 0 && al16(inp, ldin, eb)))
         continue;
       St& S = st[k];
-      float* nxt = S.dh_buf[S.ping];
-      S.ping ^= 1;
+      float* nxt = S.next();
       const int64_t in_below = v.dims[i - 1];
       const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
       // (a LayerNorm layer's db is colsum of its da, which ln_backward makes)
@@ -668,8 +739,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       St& S = st[k];
       if (skinny_done[k] || !(S.dh_f32 && dt == kBf16)) continue;
       const int64_t out = nets[k].v->dims[i + 1];
-      float* cv = S.dh_buf[S.ping];
-      S.ping ^= 1;
+      float* cv = S.next();
       const int64_t ldcv = act_ld((int)out, dt);
       int64_t blocks = ceil_div(M * out, 256);
       blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
@@ -704,6 +774,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     }
     UL_TRY(L.close());
     // ---- dW (+db via the ones column) for both networks: one grouped launch
+    // (deferred: collected for the batched launch at the end)
     GemmDesc gw[2] = {};
     bool has_w[2] = {false, false}, tc_w[2] = {false, false}, free_w[2] = {false, false};
     for (int k = 0; k < n; ++k) {
@@ -718,7 +789,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       G.M = out; G.K = M;
       G.A = st[k].dh; G.lda = st[k].lddh; G.B = inp; G.ldb = ldin;
       G.a_kmajor = false; G.b_kmajor = false; G.epi = kEpiStore;
-      G.C = st[k].ws;
+      G.C = defer ? st[k].ws + dw_layer_off(v, M, i) : st[k].ws;
       G.dtype = dt;
       free_w[k] = ones_free_of(in, has_ones);
       G.N = free_w[k] ? in + 1 : in;
@@ -728,31 +799,46 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       if (tc_w[k]) G.splits = tc_num_splits(M, G.splits, dt);
       has_w[k] = true;
     }
-    if (tc_w[0] && tc_w[1]) UL_TRY(gemm_tc_group(gw[0], gw[1], s));
-    else
-      for (int k = 0; k < n; ++k)
-        if (tc_w[k]) UL_TRY(gemm_tc(gw[k], -1, s));
-    if (tc_w[0] || tc_w[1]) {
-      ReduceJob jobs[2 + 8];
-      int nj = 0;
+    UL_CHECK_ARG(!defer || ((!has_w[0] || tc_w[0]) && (!has_w[1] || tc_w[1])),
+                 "deferred dW: GEMM not tensor-core eligible");
+    ReduceJob wj[2];
+    for (int k = 0; k < n; ++k) {
+      if (!tc_w[k]) continue;
+      const NetView& v = *nets[k].v;
+      const int64_t out = v.dims[i + 1], in = v.dims[i];
+      ReduceJob& J = wj[k];
+      J = ReduceJob{};
+      J.src = gw[k].C;
+      J.nz = gw[k].splits;
+      J.kind = 0;
+      J.len = out * gw[k].ldc;
+      J.ldp = gw[k].ldc;
+      J.in = in;
+      J.gw = nets[k].grads + v.w_off[i];
+      J.gb = free_w[k] ? nets[k].grads + v.b_off[i] : nullptr;
+    }
+    if (defer) {
       for (int k = 0; k < n; ++k) {
         if (!tc_w[k]) continue;
         const NetView& v = *nets[k].v;
-        const int64_t out = v.dims[i + 1], in = v.dims[i];
-        ReduceJob& J = jobs[nj++];
-        J = ReduceJob{};
-        J.src = st[k].ws;
-        J.nz = gw[k].splits;
-        J.kind = 0;
-        J.len = out * gw[k].ldc;
-        J.ldp = gw[k].ldc;
-        J.in = in;
-        J.gw = nets[k].grads + v.w_off[i];
-        J.gb = free_w[k] ? nets[k].grads + v.b_off[i] : nullptr;
+        D->max_splits[D->ndw] = gw[k].splits;
+        D->add(gw[k], wj[k]);
+        (void)v;
       }
-      for (int q = 0; q < npend; ++q) jobs[nj++] = pend[q];
-      npend = 0;
-      UL_TRY(launch_reduce(jobs, nj, s));
+    } else {
+      if (tc_w[0] && tc_w[1]) UL_TRY(gemm_tc_group(gw[0], gw[1], s));
+      else
+        for (int k = 0; k < n; ++k)
+          if (tc_w[k]) UL_TRY(gemm_tc(gw[k], -1, s));
+      if (tc_w[0] || tc_w[1]) {
+        ReduceJob jobs[2 + 16];
+        int nj = 0;
+        for (int k = 0; k < n; ++k)
+          if (tc_w[k]) jobs[nj++] = wj[k];
+        for (int q = 0; q < npend; ++q) jobs[nj++] = pend[q];
+        npend = 0;
+        UL_TRY(launch_reduce(jobs, nj, s));
+      }
     }
     UL_TRY(L.open());
     for (int k = 0; k < n; ++k) {
@@ -767,7 +853,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
           // 128-row chunks (8 warps x 4 rows in flight x 4), at most 256 of them
           const int64_t chunks = ceil_div(M, 128) < 256 ? ceil_div(M, 128) : 256;
           const int64_t rows_per = ceil_div(M, chunks);
-          float* part = S.ws + (int64_t)gw[k].splits * out * gw[k].ldc;
+          float* part = gw[k].C + (int64_t)gw[k].splits * out * gw[k].ldc;
           const dim3 grid((unsigned)ceil_div(out, 256), (unsigned)chunks);
           if (dt == kBf16)
             UL_TRY(launch_pdl("colsum_kernel", colsum_kernel<__nv_bfloat16>, grid, dim3(256), 0,
@@ -823,7 +909,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       break;
     }
     UL_TRY(L.close());
-    if (npend) {  // no dW reduction at this layer to ride on
+    if (npend && !defer) {  // no dW reduction at this layer to ride on
       UL_TRY(launch_reduce(pend, npend, s));
       npend = 0;
     }
@@ -839,8 +925,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       if (skinny_done[k]) continue;
       const int64_t out = v.dims[i + 1], in = v.dims[i];
       St& S = st[k];
-      float* nxt = S.dh_buf[S.ping];
-      S.ping ^= 1;
+      float* nxt = S.next();
       GemmDesc& G = gx[k];
       G.M = M; G.N = in; G.K = out;
       G.A = S.dh; G.lda = S.lddh;
@@ -861,7 +946,8 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       const bool below_ones = i - 1 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
       if (N.want_dw && tc_x[k] && in <= kCsumMaxN && S.db_done != i - 1 && !v.ln &&
           !ones_free_of(in_below, below_ones)) {
-        G.csum_part = S.sk_part;
+        // (deferred: every layer's partials live until the final reduction)
+        G.csum_part = defer ? S.cs_part + kCsRegion * i : S.sk_part;
         G.csum_nz = &cs_nz[k];
         cs_on[k] = true;
       }
@@ -877,7 +963,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       const int64_t in = v.dims[i];
       ReduceJob& J = pend[npend++];
       J = ReduceJob{};
-      J.src = st[k].sk_part;
+      J.src = gx[k].csum_part;
       J.nz = cs_nz[k];
       J.kind = 1;
       J.len = ceil_div(in, 4) * 4;
@@ -887,9 +973,15 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     }
     UL_TRY(L.open());
   }
+  if (defer) {
+    for (int q = 0; q < npend; ++q) D->jobs[D->nj++] = pend[q];
+    npend = 0;
+    if (D == &local_dd) UL_TRY(run_deferred_dw(local_dd, s));
+  }
   if (npend) UL_TRY(launch_reduce(pend, npend, s));
   return UL_OK;
 }
+
 
 int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
                 const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
