@@ -996,6 +996,15 @@ int launch(const Prob* q, int np, cudaStream_t s) {
 
 inline int bn_of(const GemmDesc& d) { return d.N > 128 ? 256 : 128; }
 
+}  // namespace tc
+// whether a dW batch (MN-major A and B, store epilogue) runs on CTA pairs
+bool tc_dw_pairs() {
+  const char* e = getenv("UL_TC_PAIR_DW");
+  const char* e2 = getenv("UL_TC_PAIR");
+  return (e ? atoi(e) != 0 : true) && !(e2 && atoi(e2) == 0);
+}
+namespace tc {
+
 template <typename TI>
 int dispatch(const Prob* q, int np, cudaStream_t s) {
   const GemmDesc& d = *q[0].d;
@@ -1016,7 +1025,17 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   // default: pairs for tf32 (4-byte operands: the halved B traffic pays),
   // single CTAs for bf16 (measured faster end to end on the cfg2 update)
   const bool want = pair_ok == -2 ? sizeof(TI) == 4 : pair_ok != 0;
-  const bool pair = want && all_two_m;
+  // dW batches (both operands MN-major, K = the minibatch rows): CTA pairs
+  // split B between the two SMs, cutting the per-SM operand stream of these
+  // L2-bound GEMMs by a third; a single-M-tile problem's second CTA computes
+  // on TMA zero fill (UL_TC_PAIR_DW=0 disables)
+  static int pair_dw = -1;
+  if (pair_dw < 0) {
+    const char* e = getenv("UL_TC_PAIR_DW");
+    pair_dw = e ? atoi(e) != 0 : 1;
+  }
+  const bool dw_batch = amn && bmn && d.epi == kEpiStore;
+  const bool pair = (want && all_two_m) || (dw_batch && pair_dw && pair_ok != 0);
   // B resident (A streamed alone) when one problem's whole N tile of B fits
   // the smem left over by the 3-stage A ring, and there is no split-K
   static int bres_ok = -1;

@@ -21,6 +21,7 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
 int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s);
 bool tc_eligible(const GemmDesc& d);
 int tc_num_splits(int64_t K, int splits, int dtype);
+bool tc_dw_pairs();
 bool skinny_ok(int N, int K);
 int64_t skinny_part_floats(int64_t M, int K, int N);
 int skinny_fwd(const void* h, int64_t ldh, int64_t M, int K, int N, const float* W,
@@ -596,9 +597,12 @@ int run_deferred_dw(DeferredDw& D, cudaStream_t s) {
   if (D.ndw == 0 && D.nj == 0) return UL_OK;
   if (D.ndw) {
     // one split count for the batch: about one persistent wave of tile-splits
+    // (CTA pairs: two CTAs per 256-row tile, a lone 128-row tile included)
+    const int64_t pm = tc_dw_pairs() ? 2 : 1;
     int64_t tiles = 0;
     for (int i = 0; i < D.ndw; ++i)
-      tiles += ceil_div(D.dw[i].M, 128) * ceil_div(D.dw[i].N, D.dw[i].N > 128 ? 256 : 128);
+      tiles += ceil_div(ceil_div(D.dw[i].M, 128), pm) * pm *
+               ceil_div(D.dw[i].N, D.dw[i].N > 128 ? 256 : 128);
     int64_t sp = kNumSMs / (tiles > 0 ? tiles : 1);
     const int64_t cap = ceil_div(D.dw[0].K, 512);
     sp = sp < cap ? sp : cap;

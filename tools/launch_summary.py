@@ -6,7 +6,7 @@ import sys
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = next(r for r in rows if "Kernel Name" in r)
 data = [dict(zip(hdr, r)) for r in rows[rows.index(hdr) + 1:] if len(r) == len(hdr)]
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
 agg = collections.defaultdict(lambda: [0, 0.0])
 for d in data:
     name = d["Kernel Name"].split("(")[0].replace("void ", "")[:64]
