@@ -218,7 +218,9 @@ int launch_ppo_head(const PpoHeadArgs& a, cudaStream_t s) {
 }
 
 int ppo_head_partial_doubles(int64_t n_local, int A) {
-  return (int)(ceil_div(n_local > 0 ? n_local : 1, kHeadThr) * (3 + A));
+  // (per-CTA partials of ppo_head_kernel or of the fused output stage's
+  // 64-row blocks, whichever is more)
+  return (int)(ceil_div(n_local > 0 ? n_local : 1, 64) * (3 + A));
 }
 
 int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ticket, double* out,

@@ -128,6 +128,7 @@ struct DeferredDw {
   void add(const GemmDesc& g, const ReduceJob& j);
 };
 int run_deferred_dw(DeferredDw& D, cudaStream_t s);
+bool deferred_dw_enabled();  // UL_DEFER_DW (default on)
 // independent tensor-core GEMMs, batched into as few launches as compatible
 int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s);
 
@@ -195,7 +196,20 @@ struct MlpNet {
   int dx_col0, dx_ncols;
   bool want_dw, zero_logstd;
   float* work;
+  // output layer handled outside (the fused PPO output stage): the forward
+  // stops at the last hidden layer; the backward starts from dout = dZ of the
+  // layer below, held in the work area's first gradient buffer
+  // (bwd_head_dz), with that layer's db already produced when head_db_below
+  bool head_external = false;
+  bool head_db_below = false;
 };
+// first hidden-gradient buffer of a backward work area (the external head's
+// dZ) and the head partial region (skinny_part_floats of the output layer)
+float* bwd_head_dz(const NetView& v, float* work, int64_t M);
+float* bwd_head_part(const NetView& v, float* work, int64_t M);
+// whether the layer below the output layer needs colsum(dZ) for its db (no
+// free ones column in its dW GEMM)
+bool head_needs_colsum(const MlpNet& N);
 // n = 1 or 2 networks in lockstep (grouped tensor-core launches on s; network
 // 1's small kernels on `side` between fork/join events when side != null)
 int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,

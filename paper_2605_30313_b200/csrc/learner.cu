@@ -156,7 +156,10 @@ void free_plan(PpoPlan* p) {
 // layers with one tensor-core launch per layer for both networks.  Otherwise
 // the critic runs on the side stream concurrently with the actor (its
 // kernels fill the gaps and tails of the actor's).
-int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool fwd) {
+// dd (backward, may be null): deferred-dW collector, possibly pre-seeded with
+// the fused output stage's partial reductions
+int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool fwd,
+             DeferredDw* dd = nullptr) {
   static int grouped = -1;
   if (grouped < 0) {
     const char* e = getenv("UL_GROUP");
@@ -174,12 +177,13 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
   } else {
     // bf16: both networks' dW GEMMs are collected and run as one batched
     // launch (+ one reduction) after the two dX chains join
-    DeferredDw dd;
-    UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr, &dd));
-    UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr, &dd));
+    DeferredDw own;
+    DeferredDw* D = dd ? dd : &own;
+    UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr, D));
+    UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr, D));
     UL_CUDA(cudaEventRecord(p->ev_join, p->side));
     UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-    return run_deferred_dw(dd, s);
+    return run_deferred_dw(*D, s);
   }
   UL_CUDA(cudaEventRecord(p->ev_join, p->side));
   UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
@@ -289,8 +293,87 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   nets[1].want_dw = true;
   nets[1].zero_logstd = true;  // critic log_std never receives a gradient
   nets[1].work = p->work_c;
+  // Fused output stage (bf16, deferred dW): both skinny output layers'
+  // forward + backward and the K9 head in one kernel (ppo_fused.cu)
+  static int fused_env = -1;
+  if (fused_env < 0) {
+    const char* e = getenv("UL_FUSED_HEAD");
+    fused_env = e ? atoi(e) != 0 : 1;
+  }
+  const int nla = p->va.n_layers, nlc = p->vc.n_layers;
+  const bool fused = fused_env && be == 2 && tc && nla >= 2 && nlc >= 2 && !p->va.ln &&
+                     !p->vc.ln && p->vc.dims[nlc] == 1 &&
+                     ppo_fused_ok(p->A, p->va.dims[nla - 1], p->vc.dims[nlc - 1]) &&
+                     deferred_dw_enabled();
+  if (fused) {
+    for (int k = 0; k < 2; ++k) {
+      const NetView& v = k ? p->vc : p->va;
+      nets[k].head_external = true;
+      nets[k].dout = bwd_head_dz(v, nets[k].work, ml);
+      nets[k].ld_dout = act_ld(v.dims[v.n_layers - 1], p->dt);
+      nets[k].head_db_below = head_needs_colsum(nets[k]);
+    }
+  }
   UL_TRY(mlp_pass(p, nets, be, ml, s, true));
   mark(p, 0, s);
+  if (fused) {
+    PpoFusedArgs f{};
+    PpoHeadArgs& h = f.h;
+    h.n_local = ml;
+    h.n_global = (double)p->mb;
+    h.A = p->A;
+    h.log_std = b.actor_params + p->va.logstd_off;
+    h.act = p->mb_act;
+    h.ld_act = p->ld_ma;
+    h.blogp = p->mb_scal;
+    h.adv = p->mb_scal + ml;
+    h.ret = p->mb_scal + 2 * ml;
+    h.oldv = p->mb_scal + 3 * ml;
+    h.adv_stats = p->d.raw_advantages ? nullptr : p->adv_stats;
+    h.clip = p->d.clip_param;
+    h.vcoef = p->d.value_loss_coef;
+    h.clipped_v = p->d.use_clipped_value_loss;
+    h.part = p->head_part;
+    h.ticket = p->tickets;
+    h.dlogstd_out = p->red + p->va.logstd_off;
+    h.loss_out = p->red + p->Pa + p->Pc;
+    h.ent_coef_add = p->d.rank == 0 ? -p->d.entropy_coef : 0.0;
+    const NetView& va = p->va;
+    const NetView& vc = p->vc;
+    f.Ka = va.dims[nla - 1];
+    f.Kc = vc.dims[nlc - 1];
+    f.ha = act_ptr(va, p->acts_a, ml, nla - 2, p->dt);
+    f.ldha = act_ld(f.Ka, p->dt);
+    f.hc = act_ptr(vc, p->acts_c, ml, nlc - 2, p->dt);
+    f.ldhc = act_ld(f.Kc, p->dt);
+    f.Wa = b.actor_params + va.w_off[nla - 1];
+    f.ba = b.actor_params + va.b_off[nla - 1];
+    f.Wc = b.critic_params + vc.w_off[nlc - 1];
+    f.bc = b.critic_params + vc.b_off[nlc - 1];
+    f.dha = const_cast<float*>(nets[0].dout);
+    f.lddha = nets[0].ld_dout;
+    f.dhc = const_cast<float*>(nets[1].dout);
+    f.lddhc = nets[1].ld_dout;
+    f.csa = nets[0].head_db_below;
+    f.csc = nets[1].head_db_below;
+    f.parta = bwd_head_part(va, nets[0].work, ml);
+    f.plena = ceil_div((int64_t)p->A * f.Ka + p->A + f.Ka, 4) * 4;
+    f.gwa = nets[0].grads + va.w_off[nla - 1];
+    f.gba = nets[0].grads + va.b_off[nla - 1];
+    f.gcsa = f.csa ? nets[0].grads + va.b_off[nla - 2] : nullptr;
+    f.partc = bwd_head_part(vc, nets[1].work, ml);
+    f.plenc = ceil_div((int64_t)f.Kc + 1 + f.Kc, 4) * 4;
+    f.gwc = nets[1].grads + vc.w_off[nlc - 1];
+    f.gbc = nets[1].grads + vc.b_off[nlc - 1];
+    f.gcsc = f.csc ? nets[1].grads + vc.b_off[nlc - 2] : nullptr;
+    DeferredDw dd;
+    UL_TRY(launch_ppo_fused(f, p->dt, &dd.jobs[0], &dd.jobs[1], s));
+    dd.nj = 2;
+    mark(p, 2, s);
+    UL_TRY(mlp_pass(p, nets, be, ml, s, false, &dd));
+    mark(p, 5, s);
+    return UL_OK;
+  }
   // K9 head
   PpoHeadArgs h{};
   h.n_local = ml;

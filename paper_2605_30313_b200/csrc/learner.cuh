@@ -35,6 +35,38 @@ struct PpoHeadArgs {
 };
 
 int launch_ppo_head(const PpoHeadArgs& a, cudaStream_t s);
+
+// Fused output stage (ppo_fused.cu): both skinny output layers' forward and
+// backward around the loss head; h.mean / h.v / h.dmean / h.dv are unused.
+struct PpoFusedArgs {
+  PpoHeadArgs h;
+  const void* ha;  // actor's last hidden activations [n_local, Ka] (dtype rows)
+  int64_t ldha;
+  int Ka;
+  const float* Wa;  // actor output layer W [A, Ka], b [A]
+  const float* ba;
+  const void* hc;  // critic's last hidden activations [n_local, Kc]
+  int64_t ldhc;
+  int Kc;
+  const float* Wc;  // critic output layer w [1, Kc], b [1]
+  const float* bc;
+  void* dha;  // out: dZ of the actor's layer below (dtype rows)
+  int64_t lddha;
+  void* dhc;
+  int64_t lddhc;
+  float* parta;  // per-block [dW_a | db_a | colsum(dh_a)] partials
+  int64_t plena;
+  int csa;  // emit colsum(dh_a) (bias gradient of the layer below)
+  float *gwa, *gba, *gcsa;  // reduction targets
+  float* partc;
+  int64_t plenc;
+  int csc;
+  float *gwc, *gbc, *gcsc;
+};
+bool ppo_fused_ok(int A, int Ka, int Kc);
+// ja / jc: the partial reductions, for the caller's next reduction launch
+int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob* jc,
+                     cudaStream_t s);
 int ppo_head_partial_doubles(int64_t n_local, int A);
 int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ticket, double* out,
                      cudaStream_t s);

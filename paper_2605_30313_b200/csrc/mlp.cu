@@ -357,6 +357,16 @@ int64_t bwd_work_floats(const NetView& v, int64_t M) {
          kCsRegion * v.n_layers + rup(lnp, 64) + rup((int64_t)kSkinnyDxMax * v.dims[1], 64);
 }
 
+float* bwd_head_dz(const NetView& v, float* work, int64_t M) {
+  (void)v;
+  (void)M;
+  return work;
+}
+
+float* bwd_head_part(const NetView& v, float* work, int64_t M) {
+  return work + n_dh_bufs(v) * M * max_hidden_ld(v) + dw_ws_floats(v, M);
+}
+
 // hidden layer i's activation rows (byte offsets: bf16 rows are half as wide)
 const float* act_ptr(const NetView& v, const float* acts, int64_t M, int i, int dtype) {
   const int64_t eb = dtype == kBf16 ? 2 : 4;
@@ -489,6 +499,15 @@ bool ones_free_of(int64_t n_in, bool ones) {
 
 }  // namespace
 
+bool head_needs_colsum(const MlpNet& N) {
+  const NetView& v = *N.v;
+  const int nl = v.n_layers;
+  if (nl < 2 || !N.want_dw || !N.wp || v.ln) return false;
+  const int64_t in_below = v.dims[nl - 2];
+  const bool below_ones = nl - 2 == 0 ? N.x_has_ones && N.ldx >= in_below + 1 : true;
+  return !ones_free_of(in_below, below_ones);
+}
+
 int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
@@ -516,6 +535,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
     for (int k = 0; k < n; ++k) {
       const MlpNet& N = nets[k];
       const NetView& v = *N.v;
+      if (last && N.head_external) continue;  // the fused output stage computes it
       float* dst = last ? N.out : const_cast<float*>(act_ptr(v, N.acts, M, i, dt));
       const int64_t lddst = last ? N.ld_out : act_ld(v.dims[i + 1], dt);
       if (last && skinny_ok(v.dims[i + 1], v.dims[i]) && al16(h[k], ldh[k], eb)) {
@@ -586,6 +606,15 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
 
 // Deferred dW: collected descs + their reductions, launched as one batched
 // tensor-core launch and one reduction pass (run_deferred_dw).
+bool deferred_dw_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_DEFER_DW");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
+}
+
 void DeferredDw::add(const GemmDesc& g, const ReduceJob& j) {
   if (ndw >= kMax || nj >= 3 * kMax) return;  // (callers stay far below: 2 nets x UL_MAX_LAYERS)
   dw[ndw] = g;
@@ -634,12 +663,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
   // first and keeps every layer's dZ; all dW GEMMs of the pass (of both
   // networks when the caller shares its collector) then run as one batched
   // launch with few K splits, and every partial reduction as one pass.
-  static int defer_env = -1;
-  if (defer_env < 0) {
-    const char* e = getenv("UL_DEFER_DW");
-    defer_env = e ? atoi(e) != 0 : 1;
-  }
-  bool defer = defer_env && tc && dt == kBf16;
+  bool defer = deferred_dw_enabled() && tc && dt == kBf16;
   for (int k = 0; k < n; ++k)
     defer = defer && nets[k].want_dw && nets[k].wp && !nets[k].v->ln;
   DeferredDw local_dd;
@@ -698,6 +722,13 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     S.dh_f32 = true;
     S.ping = 0;
     S.db_done = -1;
+    if (N.head_external) {
+      // dZ of the layer below the output layer, in gradient buffer 0
+      UL_CHECK_ARG(nl >= 2 && N.dout == N.work, "external head: dZ must sit in work buffer 0");
+      S.dh_f32 = dt == kF32;
+      S.ping = 1;
+      if (N.head_db_below) S.db_done = nl - 2;
+    }
     if (N.want_dw && N.zero_logstd && N.grads)
       UL_CUDA(cudaMemsetAsync(N.grads + v.logstd_off, 0, sizeof(float) * v.dims[nl], L.of(k)));
   }
@@ -711,6 +742,10 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       const int64_t out = v.dims[i + 1], in = v.dims[i];
       const float* inp = i == 0 ? N.x : act_ptr(v, N.acts, M, i - 1, dt);
       const int64_t ldin = i == 0 ? N.ldx : act_ld(v.dims[i], dt);
+      if (i == nl - 1 && N.head_external) {  // done by the fused output stage
+        skinny_done[k] = true;
+        continue;
+      }
       if (!(i == nl - 1 && skinny_ok((int)out, (int)in) && i > 0 && al16(inp, ldin, eb)))
         continue;
       St& S = st[k];
