@@ -50,6 +50,11 @@ class DeviceSegment:
         self.has_tv = False
         self.slot = "ppo"
         self._raw: dict = {}  # width -> contiguous H2D landing buffer
+        # the zero fills above run on the current stream, but a pipeline slot
+        # is loaded on its copy stream: let the fills land first (once per
+        # slot), or a fill still queued behind a running update could
+        # overwrite freshly copied rows
+        torch.cuda.current_stream().synchronize()
 
     # ------------------------------------------------------------- loading
     def _put_rows(self, dst: torch.Tensor, src, width: int) -> None:

@@ -152,22 +152,33 @@ void free_plan(PpoPlan* p) {
   if (p->ev_join) cudaEventDestroy(p->ev_join);
 }
 
-// Both networks' MLP pass.  Grouped (default off, UL_GROUP=1): lockstep
-// layers with one tensor-core launch per layer for both networks.  Otherwise
-// the critic runs on the side stream concurrently with the actor (its
-// kernels fill the gaps and tails of the actor's).
+// Both networks' MLP pass.  Grouped: lockstep layers with one tensor-core
+// launch per layer for both networks (default for the forward: twice the
+// tiles per launch, better wave quantisation).  Otherwise the critic runs on
+// the side stream concurrently with the actor (its kernels fill the gaps and
+// tails of the actor's); default for the backward, whose dW GEMMs of both
+// networks are deferred into one batched launch either way.
+// UL_GROUP=0/1 forces both; UL_GROUP_FWD / UL_GROUP_BWD each pass.
 // dd (backward, may be null): deferred-dW collector, possibly pre-seeded with
 // the fused output stage's partial reductions
 int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool fwd,
              DeferredDw* dd = nullptr) {
-  static int grouped = -1;
-  if (grouped < 0) {
-    const char* e = getenv("UL_GROUP");
-    grouped = e ? atoi(e) != 0 : 0;
+  static int g_fwd = -1, g_bwd = -1;
+  if (g_fwd < 0) {
+    auto env = [](const char* n, int def) {
+      const char* e = getenv(n);
+      return e ? (atoi(e) != 0 ? 1 : 0) : def;
+    };
+    const int both = env("UL_GROUP", -1);
+    g_fwd = both >= 0 ? both : env("UL_GROUP_FWD", 1);
+    g_bwd = both >= 0 ? both : env("UL_GROUP_BWD", 0);
   }
-  if (grouped) {
-    return fwd ? mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join)
-               : mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join);
+  if (fwd && g_fwd) return mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join);
+  DeferredDw own;
+  DeferredDw* D = dd ? dd : &own;
+  if (!fwd && g_bwd) {
+    UL_TRY(mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join, D));
+    return run_deferred_dw(*D, s);
   }
   UL_CUDA(cudaEventRecord(p->ev_fork, s));
   UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
@@ -177,17 +188,12 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
   } else {
     // bf16: both networks' dW GEMMs are collected and run as one batched
     // launch (+ one reduction) after the two dX chains join
-    DeferredDw own;
-    DeferredDw* D = dd ? dd : &own;
     UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, p->side, nullptr, nullptr, nullptr, D));
     UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr, D));
-    UL_CUDA(cudaEventRecord(p->ev_join, p->side));
-    UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-    return run_deferred_dw(*D, s);
   }
   UL_CUDA(cudaEventRecord(p->ev_join, p->side));
   UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-  return UL_OK;
+  return fwd ? UL_OK : run_deferred_dw(*D, s);
 }
 
 void fill_stage_out(const PpoPlan* p, StageOut* so) {
