@@ -326,7 +326,10 @@ def run_ours(args):
     counts = P.plan_stats(params, cfg, ds)
     prof = P.profile_update(params, opt, cfg, ds)
     hbm, bf16, bf16_sus, src = _peaks()
-    gemm_tflops = counts["gemm_flops_per_update"] / (prof["gemm"] / 1e3) / 1e12
+    # the MLP passes: tcgen05 GEMMs + reductions, plus the fused output stage
+    # (both output layers' forward/backward around the loss head)
+    mlp_ms = prof["gemm"] + prof["heads"]
+    gemm_tflops = counts["gemm_flops_per_update"] / (mlp_ms / 1e3) / 1e12
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
@@ -355,9 +358,11 @@ def run_ours(args):
                 "serial_gae_ppo_update_ms": serial_ms},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_sus,
                      "unit": "TFLOP/s", "frac": gemm_tflops / bf16_sus, "traffic": traffic,
-                     "kernel": "MLP phase of one update: tcgen05 GEMMs (tc_gemm_kernel) + "
-                               "skinny head kernels + split-K reductions; traffic = ncu DRAM "
-                               "bytes of the tc_gemm launches per update (profiles/)",
+                     "kernel": "MLP passes of one update: tcgen05 GEMMs (tc_gemm_kernel: grouped "
+                               "forward, ELU-gradient dX, one batched dW launch per step) + "
+                               "split-K reductions + the fused output stage (ppo_fused_kernel); "
+                               "traffic = ncu DRAM bytes of the tc_gemm launches per update "
+                               "(profiles/ncu_traffic.json)",
                      "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
                      "algorithmic_flops_per_update": counts["gemm_flops_per_update"],
                      "phase_ms_per_update": prof},
