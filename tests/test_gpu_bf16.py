@@ -167,3 +167,54 @@ def test_ppo_update_bf16_small_net(bf16_mode):
         d_gpu = got.flat() - init.flat()
         cos = float(d_gpu @ d_ref / (np.linalg.norm(d_gpu) * np.linalg.norm(d_ref)))
         assert cos >= 0.97, cos
+
+
+def _blocks(flat, dims):
+    """Split a ModelParams.flat() vector into its [W_i, b_i ..., log_std] blocks
+    (R:tensornet/mlp.py:53-57 order)."""
+    out, o = [], 0
+    for i in range(len(dims) - 1):
+        for n in (dims[i + 1] * dims[i], dims[i + 1]):
+            out.append(flat[o:o + n])
+            o += n
+    out.append(flat[o:o + dims[-1]])
+    return out
+
+
+@pytest.mark.parametrize("hidden", [(512, 256, 128), (256, 128, 128)])
+def test_ppo_single_step_grads_bf16_per_layer(bf16_mode, hidden):
+    """One minibatch's gradients on the bf16 path (fused output stage, batched
+    dW, ELU-gradient dX) against the f64 oracle, block by block: every W, b and
+    log_std of both networks within 3e-2 relative norm error, so an error in a
+    small block (the 12 x 128 output layer) cannot hide in a whole-net norm."""
+    from helpers import _synthetic
+
+    T, N = 8, 1024
+    od = 235 if hidden[0] == 512 else 48
+    seg, actor, critic = _synthetic(T, N, od, od, 12, hidden, seed=5)
+    adv, ret = O.gae(seg["rewards"], seg["values"], seg["terminated"], seg["truncated"],
+                     seg["bootstrap_value"], 0.99, 0.95, seg["truncation_values"])
+    advn = O.normalize_adv(adv.reshape(-1))
+    to64 = lambda n: O.Net(n.dims, [[w.astype(np.float64), b.astype(np.float64)] for w, b in n.layers],
+                           n.log_std.astype(np.float64))
+    f = lambda a: a.reshape(-1, *a.shape[2:])
+    args = (f(seg["obs"]).astype(np.float64), f(seg["critic_obs"]).astype(np.float64),
+            f(seg["actions"]).astype(np.float64), seg["behavior_log_prob"].reshape(-1), advn,
+            ret.reshape(-1), seg["values"].reshape(-1))
+    terms, ga, gc = O.ppo_loss_grads(to64(actor), to64(critic), *args, O.PpoCfg())
+    params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(od, hidden, 12), actor.flat()),
+                        TN.ModelParams.from_numpy(TN.Arch(od, hidden, 1), critic.flat()))
+    gterms, gga, ggc = A.ppo_loss_and_grads(params, f(seg["obs"]), f(seg["critic_obs"]),
+                                            f(seg["actions"]), seg["behavior_log_prob"].reshape(-1),
+                                            advn, ret.reshape(-1), seg["values"].reshape(-1),
+                                            A.PpoConfig())
+    for k in ("policy_loss", "value_loss", "kl"):
+        assert abs(gterms[k] - terms[k]) <= BF16_TOL * max(1.0, abs(terms[k])), k
+    for ref, got, dims in ((ga, gga, (od, *hidden, 12)), (gc, ggc, (od, *hidden, 1))):
+        for i, (r, g) in enumerate(zip(_blocks(np.asarray(ref.flat(), np.float64), dims),
+                                       _blocks(np.asarray(got.flat(), np.float64), dims))):
+            nr = np.linalg.norm(r)
+            if nr == 0.0:  # the critic's log_std
+                assert np.all(g == 0.0)
+                continue
+            assert np.linalg.norm(g - r) / nr < 3e-2, (dims, i, np.linalg.norm(g - r) / nr)
