@@ -451,6 +451,488 @@ __global__ void __launch_bounds__(kFThr, 3) ppo_fused_kernel(const __grid_consta
 }
 
 
+// ---------------------------------------------------------------------------
+// Tensor-core variant (bf16 rows, A <= 32, K <= 256): the three small products
+// of the output layers run on warp-level mma.sync m16n8k16 (bf16 in, fp32
+// accumulate): mean = h W^T (M = rows, N = action dims), dh = dmean W
+// (K = action dims; the forward accumulator fragments are re-packed in
+// registers as the A operand) and dW = dmean^T h over the tile's rows
+// (ldmatrix.trans feeds h as the column-major B operand).  The critic's
+// one-output layer stays on SIMT lanes.  128 rows per block, 8 warps; warp w
+// owns rows [16w, 16w + 16) for the row-local phases and output columns
+// {8 n : n = w (mod 8)} for dW, so no cross-warp dW reduction is needed.
+constexpr int kMRows = 128, kMThr = 256, kMWarps = 8;
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ uint32_t pk_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 up_bf16(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+}
+
+__host__ __device__ inline int rup16(int k) { return (k + 15) / 16 * 16; }
+
+// dynamic smem layout (bytes) of the tensor-core variant
+struct MmaSmem {
+  int ka, kc, pa, pc, pwa, pwt, pdm;
+  size_t o_hc, o_wa, o_wt, o_dm, o_wc, o_dv, o_cs, total;
+  __host__ __device__ MmaSmem(int Ka, int Kc, int NJT) {
+    ka = rup16(Ka);
+    kc = rup8(Kc);
+    pa = ka + 8;               // bf16 row pitch of the h_a tile (16 B aligned, conflict-free)
+    pc = kc + 8;
+    pwa = ka + 8;              // W_a  [NJT*8][pwa] bf16 (B operand of the forward)
+    pwt = NJT * 8 + 8;         // W_a^T [ka][pwt] bf16 (B operand of dh)
+    pdm = kMRows + 8;          // dmean^T [NJT*8][pdm] bf16 (A operand of dW)
+    size_t o = (size_t)kMRows * pa * 2;
+    o_hc = o;
+    o += (size_t)kMRows * pc * 2;
+    o_wa = o;
+    o += (size_t)NJT * 8 * pwa * 2;
+    o_wt = o;
+    o += (size_t)ka * pwt * 2;
+    o_dm = o;
+    o += (size_t)NJT * 8 * pdm * 2;
+    o = (o + 15) / 16 * 16;
+    o_wc = o;
+    o += (size_t)kc * 4;
+    o_dv = o;
+    o += (size_t)kMRows * 4 * 2;  // v (forward) and dv, fp32
+    o_cs = o;
+    o += (size_t)kMWarps * ka * 4 + (size_t)kMWarps * 32 * 4 + (size_t)2 * kMThr * 4;
+    total = o;
+  }
+};
+
+template <int NJT>  // n-tiles of 8 action dims: A <= 8 * NJT (NJT = 2 or 4)
+__global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_constant__ PpoFusedArgs f) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int MT = NJT / 2;  // 16-row m tiles of action dims (dW) = k16 steps of dh
+  const PpoHeadArgs& a = f.h;
+  const int Ka = f.Ka, Kc = f.Kc, A = a.A, nq = 3 + A;
+  const MmaSmem L(Ka, Kc, NJT);
+  const int ka = L.ka, kc = L.kc;
+  __nv_bfloat16* sha = reinterpret_cast<__nv_bfloat16*>(smem);
+  __nv_bfloat16* shc = reinterpret_cast<__nv_bfloat16*>(smem + L.o_hc);
+  __nv_bfloat16* swa = reinterpret_cast<__nv_bfloat16*>(smem + L.o_wa);
+  __nv_bfloat16* swt = reinterpret_cast<__nv_bfloat16*>(smem + L.o_wt);
+  __nv_bfloat16* sdm = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dm);
+  float* swc = reinterpret_cast<float*>(smem + L.o_wc);
+  float* sv = reinterpret_cast<float*>(smem + L.o_dv);  // [128] v, then [128] dv
+  float* sdv = sv + kMRows;
+  float* scs = reinterpret_cast<float*>(smem + L.o_cs);  // [8][ka] colsum(dh_a) per warp
+  float* sdb = scs + kMWarps * ka;                       // [8][32] db_a per warp
+  float* scrit = sdb + kMWarps * 32;                     // [256] dw_c, [256] colsum(dh_c) slots
+  __shared__ double s_ls[UL_MAX_ACT], s_isd[UL_MAX_ACT];
+  __shared__ double red[kMWarps][3 + UL_MAX_ACT];
+  __shared__ double s_lsum;
+  __shared__ float s_b[UL_MAX_ACT + 1];
+
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, g = lane >> 2, q = lane & 3;
+  const int64_t r0 = (int64_t)blockIdx.x * kMRows;
+  const int64_t M = a.n_local;
+  pdl_trigger();
+  pdl_wait();
+  // ---- stage h tiles (cp.async; granules past the row's data zero-filled)
+  {
+    const int ga = (Ka + 7) / 8, gt = ka / 8;  // granules with data / per staged row
+    for (int e = t; e < kMRows * gt; e += kMThr) {
+      const int rr = e / gt, u = e - rr * gt;
+      const int64_t gr = r0 + rr;
+      const bool ok = gr < M && u < ga;
+      cpa16(sha + rr * L.pa + u * 8,
+            reinterpret_cast<const __nv_bfloat16*>(f.ha) + (ok ? gr * f.ldha + u * 8 : 0), ok);
+    }
+    const int gc = (Kc + 7) / 8, gtc = kc / 8;
+    for (int e = t; e < kMRows * gtc; e += kMThr) {
+      const int rr = e / gtc, u = e - rr * gtc;
+      const int64_t gr = r0 + rr;
+      const bool ok = gr < M && u < gc;
+      cpa16(shc + rr * L.pc + u * 8,
+            reinterpret_cast<const __nv_bfloat16*>(f.hc) + (ok ? gr * f.ldhc + u * 8 : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // ---- weights: W_a -> bf16 [j][c] and [c][j], w_c fp32, biases, log_std
+  for (int e = t; e < NJT * 8 * ka; e += kMThr) {
+    const int j = e / ka, c = e - j * ka;
+    const float v = (j < A && c < Ka) ? __ldg(f.Wa + (int64_t)j * Ka + c) : 0.f;
+    const __nv_bfloat16 b = __float2bfloat16_rn(v);
+    swa[j * L.pwa + c] = b;
+    swt[c * L.pwt + j] = b;
+  }
+  for (int c = t; c < kc; c += kMThr) swc[c] = c < Kc ? __ldg(f.Wc + c) : 0.f;
+  for (int j = t; j < A; j += kMThr) {
+    const double ls = (double)a.log_std[j];
+    s_ls[j] = ls;
+    s_isd[j] = exp(-ls);
+    s_b[j] = f.ba[j];
+  }
+  if (t == 0) s_b[UL_MAX_ACT] = f.bc[0];
+  // this lane's rows (R0 = 16w + g, R1 = R0 + 8) and action dims
+  // j = 8 nt + 2q + {0, 1}: row scalars and actions, loads in flight now
+  const int R[2] = {16 * w + g, 16 * w + g + 8};
+  bool ok[2];
+  float act[2][NJT][2];
+  double blogp[2], advr[2], ret[2], oldv[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t gr = r0 + R[h];
+    ok[h] = gr < M;
+#pragma unroll
+    for (int nt = 0; nt < NJT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 8 * nt + 2 * q + e;
+        act[h][nt][e] = (ok[h] && j < A) ? a.act[gr * a.ld_act + j] : 0.f;
+      }
+    blogp[h] = ok[h] ? (double)a.blogp[gr] : 0.0;
+    advr[h] = ok[h] ? (double)a.adv[gr] : 0.0;
+    ret[h] = ok[h] ? (double)a.ret[gr] : 0.0;
+    oldv[h] = ok[h] ? (double)a.oldv[gr] : 0.0;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
+    for (int j = 0; j < A; ++j) s += s_ls[j];
+    s_lsum = s;
+  }
+  // ---- critic forward (SIMT): two threads per row, halves of the columns
+  {
+    const int row = t >> 1, half = t & 1;
+    const int c0 = half * (kc / 2), c1 = half ? kc : kc / 2;
+    float s = 0.f;
+    const __nv_bfloat16* hr = shc + row * L.pc;
+    for (int c = c0; c < c1; c += 2) {
+      const float2 hv = up_bf16(*reinterpret_cast<const uint32_t*>(hr + c));
+      s = fmaf(hv.x, swc[c], fmaf(hv.y, swc[c + 1], s));
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (!half) sv[row] = s + s_b[UL_MAX_ACT];
+  }
+  // ---- actor forward on the tensor cores: acc[nt] = h[16 rows] W^T (8 dims)
+  float acc[NJT][4];
+#pragma unroll
+  for (int nt = 0; nt < NJT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[nt][e] = 0.f;
+  for (int kk = 0; kk < ka; kk += 16) {
+    uint32_t af[4];
+    ldsm_x4(af, sha + (16 * w + (lane & 15)) * L.pa + kk + (lane >> 4) * 8);
+#pragma unroll
+    for (int nt = 0; nt < NJT; ++nt) {
+      const __nv_bfloat16* bp = swa + (8 * nt + g) * L.pwa + kk + 2 * q;
+      mma16816(acc[nt], af, *reinterpret_cast<const uint32_t*>(bp),
+               *reinterpret_cast<const uint32_t*>(bp + 8));
+    }
+  }
+  __syncthreads();  // s_lsum, sv
+  // ---- K9 loss head in float64 (rows R0, R1; the quad of lanes sharing g
+  // splits the action dims), as ppo_head_kernel
+  double z[2][NJT][2];
+  double pol = 0.0, val = 0.0, kl = 0.0, dls[NJT][2];
+#pragma unroll
+  for (int nt = 0; nt < NJT; ++nt) dls[nt][0] = dls[nt][1] = 0.0;
+  float dm[2][NJT][2];
+  float dvv[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double zp = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NJT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 8 * nt + 2 * q + e;
+        z[h][nt][e] = 0.0;
+        if (j < A) {
+          const double mean = (double)(acc[nt][2 * h + e] + s_b[j]);
+          z[h][nt][e] = ((double)act[h][nt][e] - mean) * s_isd[j];
+          zp += z[h][nt][e] * z[h][nt][e];
+        }
+      }
+    zp += __shfl_xor_sync(0xffffffffu, zp, 1);
+    zp += __shfl_xor_sync(0xffffffffu, zp, 2);
+    double dlogp = 0.0, dv = 0.0;
+    if (ok[h]) {
+      const double adv_mean = a.adv_stats ? a.adv_stats[0] : 0.0;
+      const double adv_den = a.adv_stats ? a.adv_stats[1] + 1e-8 : 1.0;
+      const double logp = -s_lsum - A * (0.5 * kLog2PiF) - 0.5 * zp;
+      const double adv = (advr[h] - adv_mean) / adv_den;
+      const double ratio = exp(logp - blogp[h]);
+      const double s1 = ratio * adv;
+      const double rc = fmin(fmax(ratio, 1.0 - a.clip), 1.0 + a.clip);
+      const double s2 = rc * adv;
+      if (q == 0) {
+        pol += fmin(s1, s2);
+        kl += blogp[h] - logp;
+      }
+      dlogp = (s1 <= s2) ? -adv * ratio / a.n_global : 0.0;
+      const double v = (double)sv[R[h]];
+      double vl;
+      if (a.clipped_v) {
+        const double vc = oldv[h] + fmin(fmax(v - oldv[h], -a.clip), a.clip);
+        const double lu = (v - ret[h]) * (v - ret[h]), lc = (vc - ret[h]) * (vc - ret[h]);
+        vl = fmax(lu, lc);
+        dv = lu >= lc ? 2.0 * (v - ret[h]) / a.n_global : 0.0;
+      } else {
+        vl = (v - ret[h]) * (v - ret[h]);
+        dv = 2.0 * (v - ret[h]) / a.n_global;
+      }
+      if (q == 0) val += vl;
+    }
+    dvv[h] = (float)(dv * a.vcoef);
+#pragma unroll
+    for (int nt = 0; nt < NJT; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = 8 * nt + 2 * q + e;
+        dm[h][nt][e] = 0.f;
+        if (j < A) {
+          dm[h][nt][e] = (float)(dlogp * z[h][nt][e] * s_isd[j]);
+          dls[nt][e] += dlogp * (z[h][nt][e] * z[h][nt][e] - 1.0);
+        }
+      }
+  }
+  if (q == 0) {
+    sdv[R[0]] = dvv[0];
+    sdv[R[1]] = dvv[1];
+  }
+  // dmean^T (bf16) for the dW product; db_a and dlog_std partials of the warp
+#pragma unroll
+  for (int nt = 0; nt < NJT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = 8 * nt + 2 * q + e;
+      sdm[j * L.pdm + R[0]] = __float2bfloat16_rn(dm[0][nt][e]);
+      sdm[j * L.pdm + R[1]] = __float2bfloat16_rn(dm[1][nt][e]);
+      float sb = dm[0][nt][e] + dm[1][nt][e];
+      double sl = dls[nt][e];
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1) {
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+        sl += __shfl_xor_sync(0xffffffffu, sl, o);
+      }
+      if (g == 0) {
+        sdb[w * 32 + j] = sb;
+        if (j < A) red[w][3 + j] = sl;
+      }
+    }
+  {
+    double v = warp_sum(pol);
+    if (lane == 0) red[w][0] = v;
+    v = warp_sum(val);
+    if (lane == 0) red[w][1] = v;
+    v = warp_sum(kl);
+    if (lane == 0) red[w][2] = v;
+  }
+  // ---- dh_a = (dmean W) * elu'(h_a) on the tensor cores; the forward
+  // accumulators, rounded to bf16, are the A operand (k = action dims)
+  {
+    uint32_t af[MT][4];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      af[m][0] = pk_bf16(dm[0][2 * m][0], dm[0][2 * m][1]);
+      af[m][1] = pk_bf16(dm[1][2 * m][0], dm[1][2 * m][1]);
+      af[m][2] = pk_bf16(dm[0][2 * m + 1][0], dm[0][2 * m + 1][1]);
+      af[m][3] = pk_bf16(dm[1][2 * m + 1][0], dm[1][2 * m + 1][1]);
+    }
+    __nv_bfloat16* da0 = reinterpret_cast<__nv_bfloat16*>(f.dha) + (r0 + R[0]) * f.lddha;
+    __nv_bfloat16* da1 = reinterpret_cast<__nv_bfloat16*>(f.dha) + (r0 + R[1]) * f.lddha;
+    for (int nc = 0; nc < ka / 8; ++nc) {
+      float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const __nv_bfloat16* bp = swt + (8 * nc + g) * L.pwt + 16 * m + 2 * q;
+        mma16816(d, af[m], *reinterpret_cast<const uint32_t*>(bp),
+                 *reinterpret_cast<const uint32_t*>(bp + 8));
+      }
+      const int c = 8 * nc + 2 * q;
+      const float2 h0 = up_bf16(*reinterpret_cast<const uint32_t*>(sha + R[0] * L.pa + c));
+      const float2 h1 = up_bf16(*reinterpret_cast<const uint32_t*>(sha + R[1] * L.pa + c));
+      d[0] = fmaf(d[0], fminf(h0.x, 0.f), d[0]);
+      d[1] = fmaf(d[1], fminf(h0.y, 0.f), d[1]);
+      d[2] = fmaf(d[2], fminf(h1.x, 0.f), d[2]);
+      d[3] = fmaf(d[3], fminf(h1.y, 0.f), d[3]);
+      if (c < Ka) {  // Ka even (bf16 rows): c + 1 < Ka too
+        if (ok[0]) *reinterpret_cast<uint32_t*>(da0 + c) = pk_bf16(d[0], d[1]);
+        if (ok[1]) *reinterpret_cast<uint32_t*>(da1 + c) = pk_bf16(d[2], d[3]);
+      }
+      if (f.csa) {
+        float s0 = d[0] + d[2], s1 = d[1] + d[3];  // invalid rows: dmean = 0 -> d = 0
+#pragma unroll
+        for (int o = 4; o <= 16; o <<= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        }
+        if (g == 0) {
+          scs[w * ka + c] = s0;
+          scs[w * ka + c + 1] = s1;
+        }
+      }
+    }
+  }
+  __syncthreads();  // sdm, sdv, scs, sdb complete
+  // ---- critic backward (SIMT): thread = (column, half of the rows)
+  {
+    const int c = t % kc, hr = t / kc, nh = kMThr / kc;  // kc <= 256: nh >= 1
+    float dw = 0.f, cs = 0.f;
+    if (hr < nh) {
+      const float wcc = swc[c];
+      __nv_bfloat16* dcol = reinterpret_cast<__nv_bfloat16*>(f.dhc) + c;
+      for (int row = hr; row < kMRows; row += nh) {
+        const float hv = __bfloat162float(shc[row * L.pc + c]);
+        const float dvr = sdv[row];
+        const float dh = dvr * wcc * (fminf(hv, 0.f) + 1.f);
+        if (c < Kc && r0 + row < M) dcol[(r0 + row) * f.lddhc] = __float2bfloat16_rn(dh);
+        dw = fmaf(dvr, hv, dw);
+        cs += dh;
+      }
+      scrit[hr * kc + c] = dw;  // = slot t
+      scrit[kMThr + hr * kc + c] = cs;
+    }
+  }
+  // ---- dW_a partial = dmean^T h over the block's rows (tensor cores): warp
+  // w owns output columns 8 nt, nt = w, w + 8, ...
+  float* pa = f.parta + (int64_t)blockIdx.x * f.plena;
+  for (int nt = w; nt < ka / 8; nt += kMWarps) {
+    float d[MT][4];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) d[m][e] = 0.f;
+    for (int kr = 0; kr < kMRows; kr += 16) {
+      // B (k = rows, n = columns) from the row-major h tile, transposed by
+      // ldmatrix: lanes 0-15 address rows kr..kr+15 of column group nt
+      uint32_t bf[4];
+      ldsm_x4_t(bf, sha + (kr + (lane & 15)) * L.pa + 8 * nt);  // (x4: both halves identical)
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        uint32_t af[4];
+        const __nv_bfloat16* ap = sdm + (16 * m + g) * L.pdm + kr + 2 * q;
+        af[0] = *reinterpret_cast<const uint32_t*>(ap);
+        af[1] = *reinterpret_cast<const uint32_t*>(ap + 8 * L.pdm);
+        af[2] = *reinterpret_cast<const uint32_t*>(ap + 8);
+        af[3] = *reinterpret_cast<const uint32_t*>(ap + 8 * L.pdm + 8);
+        mma16816(d[m], af, bf[0], bf[1]);
+      }
+    }
+    const int c = 8 * nt + 2 * q;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int j0 = 16 * m + g, j1 = j0 + 8;
+      if (c < Ka) {
+        if (j0 < A) {
+          pa[(int64_t)j0 * Ka + c] = d[m][0];
+          pa[(int64_t)j0 * Ka + c + 1] = d[m][1];
+        }
+        if (j1 < A) {
+          pa[(int64_t)j1 * Ka + c] = d[m][2];
+          pa[(int64_t)j1 * Ka + c + 1] = d[m][3];
+        }
+      }
+    }
+  }
+  __syncthreads();  // scrit complete
+  // ---- remaining partials in fixed order: db_a, colsum(dh_a), critic
+  float* pc = f.partc + (int64_t)blockIdx.x * f.plenc;
+  if (t < A) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMWarps; ++k) s += sdb[k * 32 + t];
+    pa[(int64_t)A * Ka + t] = s;
+  }
+  if (f.csa)
+    for (int c = t; c < Ka; c += kMThr) {
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < kMWarps; ++k) s += scs[k * ka + c];
+      pa[(int64_t)A * Ka + A + c] = s;
+    }
+  {
+    const int nh = kMThr / kc;
+    for (int c = t; c < Kc; c += kMThr) {
+      float dw = 0.f, cs = 0.f;
+      for (int k = 0; k < nh; ++k) {
+        dw += scrit[k * kc + c];
+        cs += scrit[kMThr + k * kc + c];
+      }
+      pc[c] = dw;
+      if (f.csc) pc[Kc + 1 + c] = cs;
+    }
+    if (t == 0) {
+      float s = 0.f;
+      for (int rr = 0; rr < kMRows; ++rr) s += sdv[rr];
+      pc[Kc] = s;
+    }
+  }
+  // ---- loss / dlog_std partials, last CTA folds them in fixed order
+  double* part = a.part + (int64_t)blockIdx.x * nq;
+  for (int qq = t; qq < nq; qq += kMThr) {
+    double s = 0.0;
+    for (int k = 0; k < kMWarps; ++k) s += red[k][qq];
+    part[qq] = s;
+  }
+  if (!last_block_ticket(a.ticket, gridDim.x)) return;
+  const unsigned nb = gridDim.x;
+  for (int q0 = 0; q0 < nq; q0 += kMThr / 8) {
+    const int qq = q0 + (t >> 3), l = t & 7;
+    double s = 0.0;
+    if (qq < nq) {
+      for (unsigned b0 = l; b0 < nb; b0 += 64) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const unsigned b = b0 + 8 * u;
+          v[u] = b < nb ? a.part[(int64_t)b * nq + qq] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (qq < nq && l == 0) {
+      if (qq < 3) a.loss_out[qq] = (float)s;
+      else a.dlogstd_out[qq - 3] = (float)(s + a.ent_coef_add);
+    }
+  }
+}
+
+template <int NJT>
+int launch_mma(const PpoFusedArgs& f, cudaStream_t s) {
+  const MmaSmem L(f.Ka, f.Kc, NJT);
+  static bool attr = false;
+  if (!attr) {
+    UL_CUDA(cudaFuncSetAttribute(ppo_fused_mma_kernel<NJT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const unsigned blocks = (unsigned)ceil_div(f.h.n_local > 0 ? f.h.n_local : 1, kMRows);
+  return launch_pdl("ppo_fused_mma_kernel", ppo_fused_mma_kernel<NJT>, dim3(blocks), dim3(kMThr),
+                    L.total, s, f);
+}
+
 inline int pad_np(int N) {
   const int sizes[] = {1, 2, 4, 8, 12, 16, 24, 32};
   for (int v : sizes)
@@ -496,8 +978,17 @@ bool ppo_fused_ok(int A, int Ka, int Kc) {
 int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob* jc,
                      cudaStream_t s) {
   UL_CHECK_ARG(ppo_fused_ok(f.h.A, f.Ka, f.Kc), "ppo fused head: unsupported shape");
-  UL_TRY(dtype == kBf16 ? launch_t<__nv_bfloat16>(f, s) : launch_t<float>(f, s));
-  const int64_t nblk = ceil_div(f.h.n_local > 0 ? f.h.n_local : 1, kFRows);
+  static int mma_env = -1;
+  if (mma_env < 0) {
+    const char* e = getenv("UL_FUSED_MMA");
+    mma_env = e ? atoi(e) != 0 : 1;
+  }
+  // tensor-core variant: bf16 rows, even K (bf16 pairs), smem within budget
+  const bool mma = mma_env && dtype == kBf16 && (f.Ka % 2) == 0 && (f.Kc % 2) == 0 &&
+                   MmaSmem(f.Ka, f.Kc, f.h.A <= 16 ? 2 : 4).total <= 200 * 1024;
+  if (mma) UL_TRY(f.h.A <= 16 ? launch_mma<2>(f, s) : launch_mma<4>(f, s));
+  else UL_TRY(dtype == kBf16 ? launch_t<__nv_bfloat16>(f, s) : launch_t<float>(f, s));
+  const int64_t nblk = ceil_div(f.h.n_local > 0 ? f.h.n_local : 1, mma ? kMRows : kFRows);
   // fixed-order reductions of the block partials, folded into the caller's
   // next reduction launch: [dW | db | colsum(dh)] per network
   *ja = ReduceJob{};

@@ -1,9 +1,7 @@
 O=gpurun_out
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-  --log-file $O/launches_traffic.csv python tools/profile_ppo.py bf16 > $O/pp.log 2>&1
-python tools/ncu_traffic.py $O/launches_traffic.csv $O/ncu_traffic.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 3 > $O/bench_under_ncu.log 2>&1
-python tools/launch_summary.py $O/launches_bench.csv > $O/launches_bench_summary.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 24 -c 8 -o $O/gemm_step -f python tools/profile_ppo.py bf16 > $O/ncu_full.log 2>&1
-tail -2 $O/ncu_full.log
+timeout 300 python -m pytest tests/test_gpu_bf16.py -q -x 2>&1 | tail -3
+timeout 600 python -m pytest tests -q -x -m gpu 2>&1 | tail -2
+for v in 1 0; do UL_FUSED_MMA=$v timeout 300 python bench.py --no-cpu-baseline --steps 10 > $O/b.log 2>&1; python -c "
+import json
+d=json.loads(open('$O/b.log').read().strip().splitlines()[-1])
+print('mma=$v', round(d['ms_per_step'],3), 'ms', {k: round(v,3) for k,v in d['roofline']['phase_ms_per_update'].items()}, 'e2e', round(d['e2e']['ms_per_step'],2))"; done
