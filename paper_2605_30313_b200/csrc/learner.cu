@@ -1,3 +1,4 @@
+#include <cuda_bf16.h>
 // Native PPO/APPO update plan: the epoch x minibatch loop of R:algos/ppo.py:136-199.
 //
 // A plan owns every per-step device buffer (minibatch staging, activation
@@ -354,6 +355,8 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
     f.ldhc = act_ld(f.Kc, p->dt);
     f.Wa = b.actor_params + va.w_off[nla - 1];
     f.ba = b.actor_params + va.b_off[nla - 1];
+    f.wba = reinterpret_cast<const __nv_bfloat16*>(p->wst_a) + va.wb_off[nla - 1];
+    f.ldwb = (f.Ka + 7) / 8 * 8;
     f.Wc = b.critic_params + vc.w_off[nlc - 1];
     f.bc = b.critic_params + vc.b_off[nlc - 1];
     f.dha = const_cast<float*>(nets[0].dout);

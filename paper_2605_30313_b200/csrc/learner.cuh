@@ -45,6 +45,8 @@ struct PpoFusedArgs {
   int Ka;
   const float* Wa;  // actor output layer W [A, Ka], b [A]
   const float* ba;
+  const void* wba;  // the same W as the Adam-refreshed bf16 staged rows (pitch ldwb)
+  int64_t ldwb;
   const void* hc;  // critic's last hidden activations [n_local, Kc]
   int64_t ldhc;
   int Kc;

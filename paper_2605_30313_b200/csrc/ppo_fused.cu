@@ -458,10 +458,12 @@ __global__ void __launch_bounds__(kFThr, 3) ppo_fused_kernel(const __grid_consta
 // (K = action dims; the forward accumulator fragments are re-packed in
 // registers as the A operand) and dW = dmean^T h over the tile's rows
 // (ldmatrix.trans feeds h as the column-major B operand).  The critic's
-// one-output layer stays on SIMT lanes.  128 rows per block, 8 warps; warp w
+// one-output layer stays on SIMT lanes.  64 rows per block, 4 warps; warp w
 // owns rows [16w, 16w + 16) for the row-local phases and output columns
-// {8 n : n = w (mod 8)} for dW, so no cross-warp dW reduction is needed.
-constexpr int kMRows = 128, kMThr = 256, kMWarps = 8;
+// {8 n : n = w (mod 4)} for dW, so no cross-warp dW reduction is needed.
+// W_a arrives as the Adam-refreshed bf16 staged copy (cp.async); its
+// transpose for the dh product comes from ldmatrix.trans.
+constexpr int kMRows = 64, kMThr = 128, kMWarps = 4;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
@@ -493,23 +495,20 @@ __host__ __device__ inline int rup16(int k) { return (k + 15) / 16 * 16; }
 
 // dynamic smem layout (bytes) of the tensor-core variant
 struct MmaSmem {
-  int ka, kc, pa, pc, pwa, pwt, pdm;
-  size_t o_hc, o_wa, o_wt, o_dm, o_wc, o_dv, o_cs, total;
+  int ka, kc, pa, pc, pwa, pdm;
+  size_t o_hc, o_wa, o_dm, o_wc, o_dv, o_cs, total;
   __host__ __device__ MmaSmem(int Ka, int Kc, int NJT) {
     ka = rup16(Ka);
     kc = rup8(Kc);
     pa = ka + 8;               // bf16 row pitch of the h_a tile (16 B aligned, conflict-free)
     pc = kc + 8;
-    pwa = ka + 8;              // W_a  [NJT*8][pwa] bf16 (B operand of the forward)
-    pwt = NJT * 8 + 8;         // W_a^T [ka][pwt] bf16 (B operand of dh)
+    pwa = ka + 8;              // W_a  [NJT*8][pwa] bf16 (B of the forward; .trans: B of dh)
     pdm = kMRows + 8;          // dmean^T [NJT*8][pdm] bf16 (A operand of dW)
     size_t o = (size_t)kMRows * pa * 2;
     o_hc = o;
     o += (size_t)kMRows * pc * 2;
     o_wa = o;
     o += (size_t)NJT * 8 * pwa * 2;
-    o_wt = o;
-    o += (size_t)ka * pwt * 2;
     o_dm = o;
     o += (size_t)NJT * 8 * pdm * 2;
     o = (o + 15) / 16 * 16;
@@ -518,13 +517,13 @@ struct MmaSmem {
     o_dv = o;
     o += (size_t)kMRows * 4 * 2;  // v (forward) and dv, fp32
     o_cs = o;
-    o += (size_t)kMWarps * ka * 4 + (size_t)kMWarps * 32 * 4 + (size_t)2 * kMThr * 4;
+    o += (size_t)kMWarps * ka * 4 + (size_t)kMWarps * 32 * 4 + (size_t)2 * kMWarps * kc * 4;
     total = o;
   }
 };
 
 template <int NJT>  // n-tiles of 8 action dims: A <= 8 * NJT (NJT = 2 or 4)
-__global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_constant__ PpoFusedArgs f) {
+__global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_constant__ PpoFusedArgs f) {
   extern __shared__ __align__(16) uint8_t smem[];
   constexpr int MT = NJT / 2;  // 16-row m tiles of action dims (dW) = k16 steps of dh
   const PpoHeadArgs& a = f.h;
@@ -534,14 +533,13 @@ __global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_co
   __nv_bfloat16* sha = reinterpret_cast<__nv_bfloat16*>(smem);
   __nv_bfloat16* shc = reinterpret_cast<__nv_bfloat16*>(smem + L.o_hc);
   __nv_bfloat16* swa = reinterpret_cast<__nv_bfloat16*>(smem + L.o_wa);
-  __nv_bfloat16* swt = reinterpret_cast<__nv_bfloat16*>(smem + L.o_wt);
   __nv_bfloat16* sdm = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dm);
   float* swc = reinterpret_cast<float*>(smem + L.o_wc);
   float* sv = reinterpret_cast<float*>(smem + L.o_dv);  // [128] v, then [128] dv
   float* sdv = sv + kMRows;
-  float* scs = reinterpret_cast<float*>(smem + L.o_cs);  // [8][ka] colsum(dh_a) per warp
-  float* sdb = scs + kMWarps * ka;                       // [8][32] db_a per warp
-  float* scrit = sdb + kMWarps * 32;                     // [256] dw_c, [256] colsum(dh_c) slots
+  float* scs = reinterpret_cast<float*>(smem + L.o_cs);  // [warps][ka] colsum(dh_a)
+  float* sdb = scs + kMWarps * ka;                       // [warps][32] db_a
+  float* scrit = sdb + kMWarps * 32;                     // [warps][kc] dw_c, then colsum(dh_c)
   __shared__ double s_ls[UL_MAX_ACT], s_isd[UL_MAX_ACT];
   __shared__ double red[kMWarps][3 + UL_MAX_ACT];
   __shared__ double s_lsum;
@@ -572,13 +570,17 @@ __global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_co
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  // ---- weights: W_a -> bf16 [j][c] and [c][j], w_c fp32, biases, log_std
-  for (int e = t; e < NJT * 8 * ka; e += kMThr) {
-    const int j = e / ka, c = e - j * ka;
-    const float v = (j < A && c < Ka) ? __ldg(f.Wa + (int64_t)j * Ka + c) : 0.f;
-    const __nv_bfloat16 b = __float2bfloat16_rn(v);
-    swa[j * L.pwa + c] = b;
-    swt[c * L.pwt + j] = b;
+  // ---- weights: the staged bf16 W_a rows (cp.async, zero past A / Ka), w_c
+  // fp32, biases, log_std
+  {
+    const int ga = (Ka + 7) / 8, gt = ka / 8;
+    for (int e = t; e < NJT * 8 * gt; e += kMThr) {
+      const int j = e / gt, u = e - j * gt;
+      const bool okw = j < A && u < ga;
+      cpa16(swa + j * L.pwa + u * 8,
+            reinterpret_cast<const __nv_bfloat16*>(f.wba) + (okw ? j * f.ldwb + u * 8 : 0), okw);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int c = t; c < kc; c += kMThr) swc[c] = c < Kc ? __ldg(f.Wc + c) : 0.f;
   for (int j = t; j < A; j += kMThr) {
@@ -762,9 +764,10 @@ __global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_co
       float d[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        const __nv_bfloat16* bp = swt + (8 * nc + g) * L.pwt + 16 * m + 2 * q;
-        mma16816(d, af[m], *reinterpret_cast<const uint32_t*>(bp),
-                 *reinterpret_cast<const uint32_t*>(bp + 8));
+        // B (k = action dims, n = columns) = W_a rows transposed by ldmatrix
+        uint32_t bf[4];
+        ldsm_x4_t(bf, swa + (16 * m + (lane & 15)) * L.pwa + 8 * nc);
+        mma16816(d, af[m], bf[0], bf[1]);
       }
       const int c = 8 * nc + 2 * q;
       const float2 h0 = up_bf16(*reinterpret_cast<const uint32_t*>(sha + R[0] * L.pa + c));
@@ -792,24 +795,61 @@ __global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_co
     }
   }
   __syncthreads();  // sdm, sdv, scs, sdb complete
-  // ---- critic backward (SIMT): thread = (column, half of the rows)
+  // ---- critic backward (SIMT): thread = (8-column group, rows rg, rg + R/.. ),
+  // 16-byte row loads / stores; dw_c and colsum(dh_c) reduced over the row
+  // groups (lane pairs, then warps in fixed order)
   {
-    const int c = t % kc, hr = t / kc, nh = kMThr / kc;  // kc <= 256: nh >= 1
-    float dw = 0.f, cs = 0.f;
-    if (hr < nh) {
-      const float wcc = swc[c];
-      __nv_bfloat16* dcol = reinterpret_cast<__nv_bfloat16*>(f.dhc) + c;
-      for (int row = hr; row < kMRows; row += nh) {
-        const float hv = __bfloat162float(shc[row * L.pc + c]);
-        const float dvr = sdv[row];
-        const float dh = dvr * wcc * (fminf(hv, 0.f) + 1.f);
-        if (c < Kc && r0 + row < M) dcol[(r0 + row) * f.lddhc] = __float2bfloat16_rn(dh);
-        dw = fmaf(dvr, hv, dw);
-        cs += dh;
-      }
-      scrit[hr * kc + c] = dw;  // = slot t
-      scrit[kMThr + hr * kc + c] = cs;
+    const int ncg = kc / 8;                  // column groups (<= 32)
+    const int nrg = kMThr / ncg;             // row groups
+    const int cg = t % ncg, rg = t / ncg;
+    float dw[8], cs[8], wcc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      dw[e] = cs[e] = 0.f;
+      wcc[e] = swc[8 * cg + e];
     }
+    if (rg < nrg) {
+      for (int row = rg; row < kMRows; row += nrg) {
+        const uint4 hv = *reinterpret_cast<const uint4*>(shc + row * L.pc + 8 * cg);
+        const float dvr = sdv[row];
+        const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+        uint32_t ow[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 hh = up_bf16(hw[e]);
+          const float d0 = dvr * wcc[2 * e] * (fminf(hh.x, 0.f) + 1.f);
+          const float d1 = dvr * wcc[2 * e + 1] * (fminf(hh.y, 0.f) + 1.f);
+          dw[2 * e] = fmaf(dvr, hh.x, dw[2 * e]);
+          dw[2 * e + 1] = fmaf(dvr, hh.y, dw[2 * e + 1]);
+          cs[2 * e] += d0;
+          cs[2 * e + 1] += d1;
+          ow[e] = pk_bf16(d0, d1);
+        }
+        const int c = 8 * cg;
+        if (r0 + row < M && c < Kc) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(f.dhc) + (r0 + row) * f.lddhc + c;
+          if (c + 8 <= Kc && ((f.lddhc & 7) == 0)) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+          } else {
+            const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(ow);
+            for (int e = 0; e < 8 && c + e < Kc; ++e) dst[e] = ob[e];
+          }
+        }
+      }
+    }
+    // row groups of one warp: lanes l, l + ncg, ... share cg
+    for (int o = ncg; o < 32; o <<= 1)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        dw[e] += __shfl_xor_sync(0xffffffffu, dw[e], o);
+        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], o);
+      }
+    if (lane < ncg)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        scrit[w * kc + 8 * lane + e] = dw[e];
+        scrit[kMWarps * kc + w * kc + 8 * lane + e] = cs[e];
+      }
   }
   // ---- dW_a partial = dmean^T h over the block's rows (tensor cores): warp
   // w owns output columns 8 nt, nt = w, w + 8, ...
@@ -869,12 +909,12 @@ __global__ void __launch_bounds__(kMThr, 2) ppo_fused_mma_kernel(const __grid_co
       pa[(int64_t)A * Ka + A + c] = s;
     }
   {
-    const int nh = kMThr / kc;
     for (int c = t; c < Kc; c += kMThr) {
       float dw = 0.f, cs = 0.f;
-      for (int k = 0; k < nh; ++k) {
+#pragma unroll
+      for (int k = 0; k < kMWarps; ++k) {
         dw += scrit[k * kc + c];
-        cs += scrit[kMThr + k * kc + c];
+        cs += scrit[kMWarps * kc + k * kc + c];
       }
       pc[c] = dw;
       if (f.csc) pc[Kc + 1 + c] = cs;
@@ -984,7 +1024,9 @@ int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob*
     mma_env = e ? atoi(e) != 0 : 1;
   }
   // tensor-core variant: bf16 rows, even K (bf16 pairs), smem within budget
+  const int ncg = rup8(f.Kc) / 8;  // critic column groups: a power of two <= 32
   const bool mma = mma_env && dtype == kBf16 && (f.Ka % 2) == 0 && (f.Kc % 2) == 0 &&
+                   (ncg & (ncg - 1)) == 0 && ncg <= 32 && f.wba != nullptr &&
                    MmaSmem(f.Ka, f.Kc, f.h.A <= 16 ? 2 : 4).total <= 200 * 1024;
   if (mma) UL_TRY(f.h.A <= 16 ? launch_mma<2>(f, s) : launch_mma<4>(f, s));
   else UL_TRY(dtype == kBf16 ? launch_t<__nv_bfloat16>(f, s) : launch_t<float>(f, s));
