@@ -626,6 +626,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
         __syncwarp();
         load_bias(t + ncl);
       }
+      // ELU-gradient operand: when the slice fits the two staging boxes, load
+      // both boxes now (after every earlier store has read its box), so the
+      // TMA latency overlaps the accumulator wait and is paid once per tile
+      constexpr int kNBox = kSlice / kBoxC;
+      constexpr bool kAuxAhead = EPI == kEpiEluGrad && kNBox <= 2;
+      if (kAuxAhead) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_expect_tx(abar, kNBox * kBoxBytes);
+#pragma unroll
+          for (int k = 0; k < kNBox; ++k)
+            tma_load_3d(staging + (ew * 2 + ((cj + k) & 1)) * kBoxBytes, tX, abar,
+                        n0 + slice * kSlice + k * kBoxC, m0 + quarter * 32, 0);
+        }
+        __syncwarp();
+      }
       if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
       if (ew == 0 && lane == 0 && local < 16) trace_at(p0_.trace, 66 + local);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -637,10 +653,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         uint8_t* stg = staging + (ew * 2 + (cj & 1)) * kBoxBytes;
         // this staging box free again (the TMA store issued from it two boxes
         // ago has read it)
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (!kAuxAhead && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         UL_ETRACE(0);
-        if (EPI == kEpiEluGrad) {
+        if (EPI == kEpiEluGrad && !kAuxAhead) {
           if (lane == 0) {
             mbar_expect_tx(abar, kBoxBytes);
             tma_load_3d(stg, tX, abar, n0 + c0, m0 + quarter * 32, 0);
@@ -675,8 +691,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = elu_fast(v[i]);
           }
-          if (EPI == kEpiEluGrad && h == 0) {
-            mbar_wait(abar, aphase);
+          if (EPI == kEpiEluGrad && h == 0 && (!kAuxAhead || c0 == slice * kSlice)) {
+            mbar_wait(abar, aphase);  // (aux ahead: both boxes on one phase)
             aphase ^= 1;
           }
           if (h == 0) UL_ETRACE(2);
@@ -716,26 +732,34 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                         pack_bf16(v[8 * j + 6], v[8 * j + 7]));
             }
           }
-          if (csum_on && T.pr == cs_pr) {
-            // butterfly reduce-scatter over the warp's 32 rows: afterwards
-            // lanes l and l ^ 16 hold the sum of column cc + (l & 15) (rows
-            // >= M contribute zeros)
-#pragma unroll
-            for (int wd = 8; wd >= 1; wd >>= 1) {
-              const bool up = (lane & wd) != 0;
-#pragma unroll
-              for (int i = 0; i < wd; ++i) {
-                const float send = up ? v[i] : v[i + wd];
-                const float keep = up ? v[i + wd] : v[i];
-                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, wd);
-              }
-            }
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
-            const int n = n0 + cc + lane;
-            if (lane < 16 && n < kCsumMaxN) csum_s[quarter * kCsumMaxN + n] += v[0];
-          }
         }
         UL_ETRACE(3);
+        if (csum_on && T.pr == cs_pr) {
+          // column sums of the box as stored (what the dW GEMM reads): lanes
+          // l and l + 16 sum rows [0, 16) / [16, 32) of column group l & 15
+          // straight from the swizzled staging box (rows >= M hold zeros)
+          __syncwarp();
+          const int cg = lane & 15, rh = (lane >> 4) * 16;
+          float s0 = 0.f, s1 = 0.f;
+#pragma unroll 4
+          for (int r = rh; r < rh + 16; ++r) {
+            const uint8_t* rp = stg + r * 64 + ((((cg * (kOutBf16 ? 4 : 4)) >> 4) ^ ((r >> 1) & 3)) << 4);
+            if constexpr (kOutBf16) {  // column pair 2cg, 2cg + 1
+              const uint32_t u = *reinterpret_cast<const uint32_t*>(rp + (cg & 3) * 4);
+              s0 += bf_lo(u);
+              s1 += bf_hi(u);
+            } else {  // column cg
+              s0 += *reinterpret_cast<const float*>(rp + (cg & 3) * 4);
+            }
+          }
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+          if (lane < 16) {
+            const int n = n0 + c0 + (kOutBf16 ? 2 * cg : cg);
+            if (n < kCsumMaxN) csum_s[quarter * kCsumMaxN + n] += s0;
+            if (kOutBf16 && n + 1 < kCsumMaxN) csum_s[quarter * kCsumMaxN + n + 1] += s1;
+          }
+        }
         if (p.tma_store) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -1035,7 +1059,18 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
     pair_dw = e ? atoi(e) != 0 : 1;
   }
   const bool dw_batch = amn && bmn && d.epi == kEpiStore;
-  const bool pair = (want && all_two_m) || (dw_batch && pair_dw && pair_ok != 0);
+  // UL_TC_PAIR_DX / UL_TC_PAIR_FWD: pairs for the ELU-gradient dX GEMMs /
+  // the bias(+ELU) forward GEMMs only (experiments)
+  static int pair_dx = -1, pair_fwd = -1;
+  if (pair_dx < 0) {
+    const char* e = getenv("UL_TC_PAIR_DX");
+    pair_dx = e ? atoi(e) != 0 : 0;
+    const char* f = getenv("UL_TC_PAIR_FWD");
+    pair_fwd = f ? atoi(f) != 0 : 0;
+  }
+  const bool pair = (want && all_two_m) || (dw_batch && pair_dw && pair_ok != 0) ||
+                    (all_two_m && pair_dx && d.epi == kEpiEluGrad) ||
+                    (all_two_m && pair_fwd && (d.epi == kEpiBiasElu || d.epi == kEpiBias));
   // B resident (A streamed alone) when one problem's whole N tile of B fits
   // the smem left over by the 3-stage A ring, and there is no split-K
   static int bres_ok = -1;
