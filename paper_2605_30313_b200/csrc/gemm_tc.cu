@@ -1009,7 +1009,17 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     }
     max_clusters = n;
   }
-  int grid = (total < max_clusters ? total : max_clusters) * CS;
+  // UL_TC_GRID_DX: cap the CTA count of the ELU-gradient (dX) launches, so
+  // the two networks' dX chains (two streams) share the GPU instead of
+  // queueing whole-GPU launches behind each other (experiment)
+  static int grid_dx = -1;
+  if (grid_dx < 0) {
+    const char* e = getenv("UL_TC_GRID_DX");
+    grid_dx = e ? atoi(e) : 0;
+  }
+  int cap = max_clusters;
+  if (EPI == kEpiEluGrad && grid_dx > 0 && grid_dx / CS < cap) cap = grid_dx / CS;
+  int grid = (total < cap ? total : cap) * CS;
   if (BRES) grid = grid / B.a[0].nt * B.a[0].nt;  // every CTA keeps one N tile
   cfg.gridDim = dim3((unsigned)grid);
   for (int i = 0; i < np; ++i)

@@ -278,18 +278,21 @@ def test_pipeline_matches_serial_updates(prec):
         P.set_precision(old)
 
 
-def test_ppo_data_parallel_two_ranks_match_single_process():
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_ppo_data_parallel_two_ranks_match_single_process(prec):
     """SURVEY.md 8(e) for PPO: two ranks (threads on one GPU; the all-reduce a
     barrier + sum) in replicated-segment mode each take half of every
     reference-permuted minibatch; after the per-step gradient all-reduce the
-    replicated clip + Adam reproduce the single-process update."""
+    replicated clip + Adam reproduce the single-process update (fp32: to
+    3e-6; bf16 -- fused output stage, batched dW -- to the bf16 bound), and the
+    ranks' parameters are bit-identical either way."""
     import threading
 
     from oracle.port import philox_stream
     from paper_2605_30313_b200 import _dist
 
     old = P.get_precision()
-    P.set_precision("fp32")
+    P.set_precision(prec)
     try:
         T, N = 8, 256
         segd, actor, critic = _synthetic(T, N, 48, 52, 12, (128, 64), seed=11)
@@ -350,13 +353,26 @@ def test_ppo_data_parallel_two_ranks_match_single_process():
         for t in th:
             t.join()
         assert not errors, errors
-        for p, _ in states:
-            np.testing.assert_allclose(p.actor.flat(), p_ref.actor.flat(), atol=3e-6)
-            np.testing.assert_allclose(p.critic.flat(), p_ref.critic.flat(), atol=3e-6)
         np.testing.assert_array_equal(states[0][0].actor.flat(), states[1][0].actor.flat())
-        for g in got:
-            assert g.policy_loss == pytest.approx(want.policy_loss, abs=1e-5)
-            assert g.value_loss == pytest.approx(want.value_loss, rel=1e-5, abs=1e-6)
+        np.testing.assert_array_equal(states[0][0].critic.flat(), states[1][0].critic.flat())
+        if prec == "fp32":
+            for p, _ in states:
+                np.testing.assert_allclose(p.actor.flat(), p_ref.actor.flat(), atol=3e-6)
+                np.testing.assert_allclose(p.critic.flat(), p_ref.critic.flat(), atol=3e-6)
+            for g in got:
+                assert g.policy_loss == pytest.approx(want.policy_loss, abs=1e-5)
+                assert g.value_loss == pytest.approx(want.value_loss, rel=1e-5, abs=1e-6)
+        else:
+            a0, c0 = actor.flat(), critic.flat()
+            for p, _ in states:
+                for got_p, ref_p, init in ((p.actor.flat(), p_ref.actor.flat(), a0),
+                                           (p.critic.flat(), p_ref.critic.flat(), c0)):
+                    d_ref, d_got = ref_p - init, got_p - init
+                    cos = float(d_got @ d_ref / (np.linalg.norm(d_got) * np.linalg.norm(d_ref)))
+                    assert cos >= 0.97, cos
+            for g in got:
+                assert g.policy_loss == pytest.approx(want.policy_loss, abs=1e-2)
+                assert g.value_loss == pytest.approx(want.value_loss, rel=1e-2, abs=1e-2)
     finally:
         P.set_precision(old)
 

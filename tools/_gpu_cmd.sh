@@ -1,10 +1,5 @@
 O=gpurun_out
-timeout 600 python -m pytest tests -q -x -m gpu 2>&1 | tail -2
-BENCH_DT=1 timeout 120 python tools/bench_gemm.py | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().splitlines()[-1])
-print(' '.join(f\"{k}={v['us']:.1f}\" for k,v in d.items() if isinstance(v,dict)), 'total', round(d['total_us'],1))"
-for i in 1 2; do timeout 300 python bench.py --no-cpu-baseline --steps 10 > $O/b.log 2>&1; python -c "
+for cfg in "UL_TC_GRID_DX=0" "UL_TC_GRID_DX=74" "UL_TC_GRID_DX=96" "UL_TC_GRID_DX=74 UL_GROUP_BWD=0"; do env $cfg timeout 300 python bench.py --no-cpu-baseline --steps 10 > $O/b.log 2>&1; python -c "
 import json
 d=json.loads(open('$O/b.log').read().strip().splitlines()[-1])
-print('bench', round(d['ms_per_step'],3), 'ms', {k: round(v,3) for k,v in d['roofline']['phase_ms_per_update'].items()}, 'e2e', round(d['e2e']['ms_per_step'],2))"; done
+print('$cfg', round(d['ms_per_step'],3), 'ms', {k: round(v,3) for k,v in d['roofline']['phase_ms_per_update'].items()}, 'e2e', round(d['e2e']['ms_per_step'],2))"; done
