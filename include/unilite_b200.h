@@ -324,7 +324,8 @@ int ul_ppo_plan_finish(void* plan, ul_ppo_result* out, void* stream);
 int ul_ppo_plan_counts(void* plan, int64_t* kernels_per_update, double* gemm_flops_per_update);
 /* One un-graphed update with CUDA events around every kernel class:
  * ms[0] MLP passes (GEMMs), ms[1] gather, ms[2] heads/finalize, ms[3] optimizer,
- * ms[4] all, ms[5] the MLP backward part of ms[0] (ms must hold 6 doubles).
+ * ms[4] all, ms[5] the MLP backward part of ms[0], of which ms[6] the dX chains and
+ * ms[7] the batched dW launch (the rest: the deferred reduction).  ms holds 8 doubles.
  * Synchronises the stream. */
 int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
                         int64_t t_critic, double* ms, void* stream);

@@ -454,11 +454,12 @@ def profile_update(params: AcParams, opt: AcOpt, cfg: PpoConfig, ds) -> dict:
     """One un-graphed update with CUDA events per kernel class (ms)."""
     world, rank = _world()
     plan = _plan_for(params, cfg, ds, world, rank)
-    ms = (C.c_double * 6)()
+    ms = (C.c_double * 8)()
     _lib.call("ul_ppo_plan_profile", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
               opt.critic.t, ms, _dev.stream())
     res = _lib.PpoResult()
     _lib.lib().ul_ppo_plan_finish(plan.h, C.byref(res), _dev.stream())
     opt.actor.t, opt.critic.t = int(res.t_actor), int(res.t_critic)
-    return dict(gemm=ms[0], mlp_forward=ms[0] - ms[5], mlp_backward=ms[5], gather=ms[1],
-                heads=ms[2], optimizer=ms[3], total=ms[4])
+    return dict(gemm=ms[0], mlp_forward=ms[0] - ms[5], mlp_backward=ms[5], bwd_dx=ms[6],
+                bwd_dw=ms[7], bwd_reduce=ms[5] - ms[6] - ms[7], gather=ms[1], heads=ms[2],
+                optimizer=ms[3], total=ms[4])

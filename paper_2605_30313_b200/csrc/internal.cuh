@@ -127,7 +127,9 @@ struct DeferredDw {
   int nj = 0;
   void add(const GemmDesc& g, const ReduceJob& j);
 };
-int run_deferred_dw(DeferredDw& D, cudaStream_t s);
+int run_deferred_dw(DeferredDw& D, cudaStream_t s);  // = the two below
+int run_deferred_dw_gemms(DeferredDw& D, cudaStream_t s);
+int run_deferred_dw_reduce(DeferredDw& D, cudaStream_t s);
 bool deferred_dw_enabled();  // UL_DEFER_DW (default on)
 // independent tensor-core GEMMs, batched into as few launches as compatible
 int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s);

@@ -179,7 +179,10 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
   DeferredDw* D = dd ? dd : &own;
   if (!fwd && g_bwd) {
     UL_TRY(mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join, D));
-    return run_deferred_dw(*D, s);
+    mark(p, 6, s);
+    UL_TRY(run_deferred_dw_gemms(*D, s));
+    mark(p, 7, s);
+    return run_deferred_dw_reduce(*D, s);
   }
   UL_CUDA(cudaEventRecord(p->ev_fork, s));
   UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
@@ -194,7 +197,11 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
   }
   UL_CUDA(cudaEventRecord(p->ev_join, p->side));
   UL_CUDA(cudaStreamWaitEvent(s, p->ev_join, 0));
-  return fwd ? UL_OK : run_deferred_dw(*D, s);
+  if (fwd) return UL_OK;
+  mark(p, 6, s);  // (profiling) dX chains of both networks
+  UL_TRY(run_deferred_dw_gemms(*D, s));
+  mark(p, 7, s);  // the batched dW launch
+  return run_deferred_dw_reduce(*D, s);
 }
 
 void fill_stage_out(const PpoPlan* p, StageOut* so) {
@@ -684,15 +691,16 @@ extern "C" int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic
   p->prof->on = false;
   UL_TRY(st);
   UL_CUDA(cudaStreamSynchronize(s));
-  for (int c = 0; c < 6; ++c) ms[c] = 0.0;
+  for (int c = 0; c < 8; ++c) ms[c] = 0.0;
   for (int i = 1; i < p->prof->n; ++i) {
     float t = 0.f;
     UL_CUDA(cudaEventElapsedTime(&t, p->prof->ev[i - 1], p->prof->ev[i]));
     const int c = p->prof->cat[i];
     if (c >= 0 && c < 4) ms[c] += t;
-    if (c == 5) {  // MLP backward: counted with the GEMMs and on its own
+    if (c >= 5 && c <= 7) {  // MLP backward: counted with the GEMMs, in total and by part
       ms[0] += t;
       ms[5] += t;
+      if (c >= 6) ms[c] += t;
     }
     ms[4] += t;
   }

@@ -114,6 +114,110 @@ __global__ void __launch_bounds__(W * 32) reduce_dw_kernel(ReduceTable tab) {
   }
 }
 
+// Every partial reduction of a pass in ONE launch.  Blocks [end[i-1], end[i])
+// belong to job i.  Shallow jobs (split-K dW, nz <= kShallowZ): one thread per
+// float4 column, all of its nz loads in flight, summed in z order.  Deep jobs
+// (per-block / per-CTA partial sets): 32 float4 columns per block, the 8 warps
+// take z = w, w + 8, ... and combine in fixed order.  Deterministic.
+constexpr int kShallowZ = 64;
+struct ReduceAll {
+  ReduceJob r[kMaxReduceJobs];
+  int end[kMaxReduceJobs];
+  int n;
+};
+
+__device__ __forceinline__ void reduce_store(const ReduceJob& q, int64_t j, float4 t) {
+  const float tv[4] = {t.x, t.y, t.z, t.w};
+  if (q.kind == 0) {
+    const int64_t r = j / q.ldp, c0 = j - r * q.ldp;  // 4 | ldp: one row per float4
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t c = c0 + e;
+      if (c < q.in) q.gw[r * q.in + c] = tv[e];
+      else if (c == q.in && q.gb) q.gb[r] = tv[e];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t c = j + e;
+      if (c < q.n0) {
+        if (q.o0) q.o0[c] = tv[e];
+      } else if (c < q.n0 + q.n1) {
+        if (q.o1) q.o1[c - q.n0] = tv[e];
+      } else if (c < q.n0 + q.n1 + q.n2) {
+        if (q.o2) q.o2[c - q.n0 - q.n1] = tv[e];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) reduce_all_kernel(const __grid_constant__ ReduceAll tab) {
+  __shared__ float4 sm[8][32];
+  int ji = 0;
+  while (ji < tab.n - 1 && (int)blockIdx.x >= tab.end[ji]) ++ji;
+  const ReduceJob& q = tab.r[ji];
+  const int blk = (int)blockIdx.x - (ji ? tab.end[ji - 1] : 0);
+  pdl_trigger();
+  pdl_wait();
+  const float* __restrict__ ws = q.src;
+  const int nz = q.nz;
+  if (nz <= kShallowZ) {
+    const int64_t j = ((int64_t)blk * 256 + threadIdx.x) * 4;
+    if (j >= q.len) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int z0 = 0; z0 < nz; z0 += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = z0 + u < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)(z0 + u) * q.len + j))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+    reduce_store(q, j, acc);
+    return;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j = ((int64_t)blk * 32 + lane) * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (j < q.len) {
+    for (int z0 = w; z0 < nz; z0 += 64) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int z = z0 + 8 * u;
+        v[u] = z < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * q.len + j))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x += v[u].x;
+        acc.y += v[u].y;
+        acc.z += v[u].z;
+        acc.w += v[u].w;
+      }
+    }
+  }
+  sm[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && j < q.len) {
+    float4 t = sm[0][lane];
+    for (int k = 1; k < 8; ++k) {
+      const float4 q4 = sm[k][lane];
+      t.x += q4.x;
+      t.y += q4.y;
+      t.z += q4.z;
+      t.w += q4.w;
+    }
+    reduce_store(q, j, t);
+  }
+}
+
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
@@ -452,6 +556,29 @@ struct Lanes {
 
 // one launch for up to kMaxReduceJobs fixed-order partial reductions
 int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
+  static int one = -1;
+  if (one < 0) {
+    const char* e = getenv("UL_REDUCE_ONE");
+    one = e ? atoi(e) != 0 : 1;
+  }
+  if (one) {
+    // every job in one launch (reduce_all_kernel), kMaxReduceJobs per launch
+    for (int q = 0; q < nj;) {
+      ReduceAll tab{};
+      int blocks = 0;
+      for (; q < nj && tab.n < kMaxReduceJobs; ++q) {
+        if (jobs[q].len <= 0 || jobs[q].nz <= 0) continue;
+        tab.r[tab.n] = jobs[q];
+        const int64_t cols = ceil_div(jobs[q].len, 4);
+        blocks += (int)ceil_div(cols, jobs[q].nz <= kShallowZ ? 256 : 32);
+        tab.end[tab.n++] = blocks;
+      }
+      if (tab.n == 0) continue;
+      UL_TRY(launch_pdl("reduce_all_kernel", reduce_all_kernel, dim3((unsigned)blocks), dim3(256),
+                        0, s, tab));
+    }
+    return UL_OK;
+  }
   // shallow (split-K) and deep (per-block / per-CTA partial) jobs take the
   // 8- and 32-warp variants; at most kMaxReduceJobs per launch
   for (int deep = 0; deep < 2; ++deep) {
@@ -623,7 +750,11 @@ void DeferredDw::add(const GemmDesc& g, const ReduceJob& j) {
 }
 
 int run_deferred_dw(DeferredDw& D, cudaStream_t s) {
-  if (D.ndw == 0 && D.nj == 0) return UL_OK;
+  UL_TRY(run_deferred_dw_gemms(D, s));
+  return run_deferred_dw_reduce(D, s);
+}
+
+int run_deferred_dw_gemms(DeferredDw& D, cudaStream_t s) {
   if (D.ndw) {
     // one split count for the batch: about one persistent wave of tile-splits
     // (CTA pairs: two CTAs per 256-row tile, a lone 128-row tile included)
@@ -644,7 +775,12 @@ int run_deferred_dw(DeferredDw& D, cudaStream_t s) {
     }
     UL_TRY(gemm_tc_batch(D.dw, D.ndw, s));
   }
-  UL_TRY(launch_reduce(D.jobs, D.nj, s));
+  D.ndw = 0;
+  return UL_OK;
+}
+
+int run_deferred_dw_reduce(DeferredDw& D, cudaStream_t s) {
+  if (D.nj) UL_TRY(launch_reduce(D.jobs, D.nj, s));
   D.ndw = D.nj = 0;
   return UL_OK;
 }
