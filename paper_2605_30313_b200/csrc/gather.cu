@@ -18,6 +18,8 @@ namespace ul {
 namespace {
 
 constexpr int kMaxDesc = 12;
+// row groups in flight per warp (8 measured slower: fewer resident warps)
+constexpr int kRowGroups = 4;
 
 struct GatherTable {
   const char* src[kMaxDesc];
@@ -68,7 +70,7 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
                                           int64_t modulo, int64_t lo, int64_t hi, int* err,
                                           int64_t ones, int blk, int nblk) {
   using T = typename Vec<U>::T;
-  constexpr int R = 4;
+  constexpr int R = kRowGroups;
   const int lane = threadIdx.x & 31;
   const int lpr = 1 << lpr_shift, rpw = 32 >> lpr_shift;
   const int sub = lane & (lpr - 1);
@@ -77,21 +79,39 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
   const int64_t step = nw * rpw;  // rows between a warp's consecutive row groups
   const int ones_u = ones >= 0 ? (int)(ones / U) : -1;
   const int ones_e = ones >= 0 ? (int)((ones % U) / 4) : 0;
+  // the next row group's indices are loaded one iteration ahead, so a row's
+  // address is ready when its loads issue (index and row round trips overlap)
+  int64_t nxt[R];
+  {
+    const int64_t b0 = gw * rpw + (lane >> lpr_shift);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int64_t r = b0 + k * step;
+      nxt[k] = r < n ? (idx ? __ldg(idx + r) : r) : 0;
+    }
+  }
   for (int64_t base = gw * rpw + (lane >> lpr_shift); base < n; base += step * R) {
     const char* sp[R];
     char* dp[R];
+    int64_t cur[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      cur[k] = nxt[k];
+      const int64_t r = base + step * R + k * step;
+      nxt[k] = r < n ? (idx ? __ldg(idx + r) : r) : 0;
+    }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const int64_t r = base + k * step;
       sp[k] = nullptr;
       dp[k] = dst + r * dstr;
       if (r >= n) continue;
-      int64_t s = idx ? __ldg(idx + r) : r;
+      int64_t s = cur[k];
       if (s < lo || s >= hi) {
         if (err && sub == 0) atomicOr(err, 1);
         continue;
       }
-      if (modulo > 0) s %= modulo;
+      if (modulo > 0) s = (modulo & (modulo - 1)) == 0 ? (s & (modulo - 1)) : s % modulo;
       sp[k] = src + s * sst;
     }
     // two units per lane per row in flight (rows up to 64 units = 1 KB of
@@ -167,6 +187,15 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t,
       copy_rows<4, false>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
                           modulo, lo, hi, err, t.ones[d], blk, nblk);
   }
+}
+
+int64_t gather_cap_blocks() {
+  static int64_t cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("UL_GATHER_BLOCKS_PER_SM");
+    cap = (int64_t)(e ? atoi(e) : 8) * kNumSMs;  // 8 measured best (minibatch 4.3 TB/s)
+  }
+  return cap;
 }
 
 int unit_for(uintptr_t a, uintptr_t b, int64_t s1, int64_t s2, int64_t rb) {
@@ -253,10 +282,11 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
     int sh = 0;
     while (sh < 5 && (1 << sh) < t.units[d]) ++sh;
     t.lpr_shift[d] = sh;
-    // warps needed for R = 4 row groups in flight each -> 8-warp blocks
-    const int64_t warps = ceil_div(n, (int64_t)(32 >> sh) * 4);
+    // warps needed for kRowGroups row groups in flight each -> 8-warp blocks
+    const int64_t warps = ceil_div(n, (int64_t)(32 >> sh) * kRowGroups);
     int64_t nb = ceil_div(warps, 8);
-    nb = nb > 4 * kNumSMs ? 4 * kNumSMs : nb;
+    const int64_t cap = gather_cap_blocks();
+    nb = nb > cap ? cap : nb;
     t.blk0[d] = nb_total;
     nb_total += (int)nb;
   }

@@ -19,7 +19,10 @@ import torch  # noqa: E402
 from paper_2605_30313_b200 import _dev, _lib  # noqa: E402
 
 
-def _time(fn, reps=10, warm=3):
+def _time(fn, reps=10, warm=3, back_to_back=10):
+    """Best of `reps` per-launch device times, each the mean of `back_to_back`
+    consecutive launches between two events (so a short kernel's time is not
+    the host launch latency the first event waits through)."""
     s = torch.cuda.current_stream()
     for _ in range(warm):
         fn()
@@ -27,10 +30,11 @@ def _time(fn, reps=10, warm=3):
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        fn()
+        for _ in range(back_to_back):
+            fn()
         e1.record(s)
         e1.synchronize()
-        best = min(best, e0.elapsed_time(e1) * 1e-3)
+        best = min(best, e0.elapsed_time(e1) * 1e-3 / back_to_back)
     return best
 
 
