@@ -200,3 +200,22 @@ def test_normalizer_matches_reference_goldens(golden):
         if len(x):
             np.testing.assert_allclose(norm.apply(x).cpu().numpy(), g[f"n_apply{s}"], rtol=0,
                                        atol=2e-6)
+
+
+@pytest.mark.parametrize("D", [96, 8, 200, 1100])
+def test_normalizer_vectorized_moments(D):
+    """K3 vectorised path (D % 4 == 0: float4 lanes, one 1024-thread CTA per SM,
+    multi-phase last-CTA merge): running statistics over batches of very
+    different sizes, offset far from zero (the shifted sums must not cancel),
+    equal the float64 statistics of all rows seen (R:tensornet/normalizer.py:27-45)."""
+    rng = np.random.default_rng(D)
+    norm = TN.Normalizer(D)
+    seen = []
+    for B in (5000, 1, 3, 70000, 257):
+        x = (100.0 + 3.0 * rng.normal(size=(B, D))).astype(np.float32)
+        norm.update(x)
+        seen.append(x.astype(np.float64))
+        allx = np.concatenate(seen)
+        assert norm.count == float(len(allx))
+        np.testing.assert_allclose(norm.mean, allx.mean(0), rtol=1e-11, atol=1e-9)
+        np.testing.assert_allclose(norm.var, allx.var(0), rtol=1e-7, atol=1e-9)
