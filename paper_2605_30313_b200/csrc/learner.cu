@@ -452,10 +452,10 @@ int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
   st.n[1] = p->Pc;
   // joint clip + loss finalisation, then Adam (which also refreshes the
   // staged tensor-core weights for the next step)
-  UL_TRY(launch_prepare(st, p->ctl_d, s, &lf));
   StageOut so{};
   const bool tc = p->d.gemm_backend >= 1;
   if (tc) fill_stage_out(p, &so);
+  UL_TRY(launch_prepare(st, p->ctl_d, s, &lf));
   UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s, tc ? &so : nullptr));
   mark(p, 3, s);
   return UL_OK;

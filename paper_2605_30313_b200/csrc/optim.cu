@@ -47,41 +47,10 @@ __device__ void finalize_loss(const LossFinalize& f, ul_opt_ctl* ctl) {
   }
 }
 
-__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl,
-                                                               LossFinalize lf, int has_lf) {
-  __shared__ double scratch[32];
-  const int nb = gridDim.x;
-  pdl_trigger();
-  pdl_wait();
-  for (int s = 0; s < st.nseg; ++s) {
-    const float* g = st.g[s];
-    const int64_t n = st.n[s];
-    double acc = 0.0;
-    int bad = 0;
-    const int64_t stride = (int64_t)nb * blockDim.x;
-    // 8 loads in flight per thread (issued before the dependent adds)
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 8 * stride) {
-      float x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t i = i0 + u * stride;
-        x[u] = i < n ? __ldg(g + i) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc += (double)x[u] * (double)x[u];
-        bad |= !isfinite(x[u]);
-      }
-    }
-    const double tot = block_sum(acc, scratch);
-    const int any_bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) {
-      ctl->part[blockIdx.x][s] = tot;
-      ctl->part_bad[blockIdx.x][s] = any_bad;
-    }
-  }
-  if (!last_block_ticket(&ctl->ticket, nb)) return;
-  // last CTA: fixed-order, block-parallel fold of the per-CTA partials
+// last CTA of the prepare pass: fixed-order, block-parallel fold of the
+// per-CTA partials, loss finalisation, divergence latch, clip factor, t += 1
+__device__ void prepare_tail(const SegTable& st, ul_opt_ctl* ctl, const LossFinalize& lf,
+                             int has_lf, int nb, double* scratch) {
   __shared__ double red[UL_MAX_SEG];
   __shared__ int red_bad[UL_MAX_SEG];
   for (int s = 0; s < st.nseg; ++s) {
@@ -127,6 +96,43 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_o
   ctl->steps += 1;
 }
 
+__global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl,
+                                                               LossFinalize lf, int has_lf) {
+  __shared__ double scratch[32];
+  const int nb = gridDim.x;
+  pdl_trigger();
+  pdl_wait();
+  for (int s = 0; s < st.nseg; ++s) {
+    const float* g = st.g[s];
+    const int64_t n = st.n[s];
+    double acc = 0.0;
+    int bad = 0;
+    const int64_t stride = (int64_t)nb * blockDim.x;
+    // 8 loads in flight per thread (issued before the dependent adds)
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 8 * stride) {
+      float x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = i0 + u * stride;
+        x[u] = i < n ? __ldg(g + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc += (double)x[u] * (double)x[u];
+        bad |= !isfinite(x[u]);
+      }
+    }
+    const double tot = block_sum(acc, scratch);
+    const int any_bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) {
+      ctl->part[blockIdx.x][s] = tot;
+      ctl->part_bad[blockIdx.x][s] = any_bad;
+    }
+  }
+  if (!last_block_ticket(&ctl->ticket, nb)) return;
+  prepare_tail(st, ctl, lf, has_lf, nb, scratch);
+}
+
 struct AdamScalars {
   float b1, one_m_b1, b2, one_m_b2, bc1, bc2, lr, eps;
 };
@@ -157,32 +163,47 @@ __device__ __forceinline__ void stage_param(const StageOut& so, int s, int64_t i
   }
 }
 
-__global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
-                             int do_adam, StageOut so, int has_so) {
-  pdl_trigger();
-  pdl_wait();
-  const int s = blockIdx.y;
-  if (s >= st.nseg) return;
-  const int upd = ctl->seg_update[s];
+// the controller values the apply pass reads (copied once per CTA)
+struct ApplyCtl {
+  int upd[UL_MAX_SEG];
+  double t[UL_MAX_SEG], lr[UL_MAX_SEG];
+  double factor, beta1, beta2, eps;
+};
+
+__device__ __forceinline__ void read_apply_ctl(const volatile ul_opt_ctl* c, int nseg, ApplyCtl* o) {
+  for (int s = 0; s < nseg; ++s) {
+    o->upd[s] = c->seg_update[s];
+    o->t[s] = (double)c->t[s];
+    o->lr[s] = c->lr[s];
+  }
+  o->factor = c->factor;
+  o->beta1 = c->beta1;
+  o->beta2 = c->beta2;
+  o->eps = c->eps;
+}
+
+// clip scale + Adam over segment s, elements t0, t0 + stride, ... (float4
+// lanes when aligned); refreshes the staged tensor-core weights
+__device__ void apply_seg(const SegTable& st, const ApplyCtl& c, int s, int write_grads,
+                          int do_adam, const StageOut& so, int has_so, int64_t t0, int64_t stride) {
+  const int upd = c.upd[s];
   // clip_global_norm scales even when a later Adam raises; Adam itself only on upd
-  const float f = (float)ctl->factor;
-  const bool scale = ctl->factor != 1.0;
+  const float f = (float)c.factor;
+  const bool scale = c.factor != 1.0;
   float* __restrict__ g = st.g[s];
   const int64_t n = st.n[s];
   AdamScalars k;
   if (do_adam) {
-    const double t = (double)ctl->t[s];
-    k.b1 = (float)ctl->beta1;
-    k.one_m_b1 = (float)(1.0 - ctl->beta1);
-    k.b2 = (float)ctl->beta2;
-    k.one_m_b2 = (float)(1.0 - ctl->beta2);
-    k.bc1 = (float)(1.0 - pow(ctl->beta1, t));
-    k.bc2 = (float)(1.0 - pow(ctl->beta2, t));
-    k.lr = (float)ctl->lr[s];
-    k.eps = (float)ctl->eps;
+    const double t = c.t[s];
+    k.b1 = (float)c.beta1;
+    k.one_m_b1 = (float)(1.0 - c.beta1);
+    k.b2 = (float)c.beta2;
+    k.one_m_b2 = (float)(1.0 - c.beta2);
+    k.bc1 = (float)(1.0 - pow(c.beta1, t));
+    k.bc2 = (float)(1.0 - pow(c.beta2, t));
+    k.lr = (float)c.lr[s];
+    k.eps = (float)c.eps;
   }
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (!do_adam || !upd) {  // clip-only (clip_global_norm) or a skipped segment
     if (write_grads && scale)
       for (int64_t i = t0; i < n; i += stride) g[i] = __fmul_rn(g[i], f);
@@ -224,6 +245,19 @@ __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, in
     pp[i] = p;
     if (has_so && so.dst[s]) stage_param(so, s, i, p);
   }
+}
+
+__global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
+                             int do_adam, StageOut so, int has_so) {
+  __shared__ ApplyCtl c;
+  pdl_trigger();
+  pdl_wait();
+  const int s = blockIdx.y;
+  if (s >= st.nseg) return;
+  if (threadIdx.x == 0) read_apply_ctl(ctl, st.nseg, &c);
+  __syncthreads();
+  apply_seg(st, c, s, write_grads, do_adam, so, has_so,
+            (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 
 __global__ void polyak_kernel(float* __restrict__ tgt, const float* __restrict__ src, int64_t n,
