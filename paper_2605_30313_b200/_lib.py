@@ -147,6 +147,7 @@ _PROTOS = {
     "ul_gemm_tc": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,
                              vp, i64, C.c_int, C.c_int, vp]),
     "ul_tc_trace": (C.c_int, [vp]),
+    "ul_tc_trace_reset": (C.c_int, []),
     "ul_nstep_state_bytes": (i64, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "ul_nstep_push": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, f64, f64, f64, f64, vp,
                                 vp, vp, vp, vp, vp, vp, i64, i64, i64, vp, vp]),

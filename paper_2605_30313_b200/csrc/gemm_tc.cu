@@ -81,6 +81,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   __trap();
 }
 
+// diagnostics (UL_TC_TRACE): wait cycles accumulated per role, summed over
+// CTAs into trace slots 128.. (see ul_tc_trace / tools/trace_gemm.py)
+constexpr int kTraceSlots = 160;
+__device__ __forceinline__ void mbar_wait_acc(uint64_t* bar, uint32_t parity,
+                                              unsigned long long* acc) {
+  if (acc == nullptr) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  *acc += (unsigned long long)(clock64() - t0);
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
   asm volatile(
@@ -363,6 +377,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 2);  // keeps sbias 16 B aligned
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long w_prod = 0, w_full = 0, w_acc = 0, w_epi = 0;  // (UL_TC_TRACE)
+  const long long t_start = clock64();
   pdl_trigger();
   if (threadIdx.x == 0) trace_at(p0_.trace, 0);
 
@@ -469,7 +485,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int nb0 = n0 + (int)crank * BNL;  // first B row (N) of this CTA's share
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
-          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          mbar_wait_acc(&empty[s], ((it / kStages) & 1) ^ 1, p0_.trace ? &w_prod : nullptr);
           uint8_t* sa = smem + s * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
           const int k0 = T.z * P.k_per_split + kt * BK;
@@ -528,12 +544,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int t = cl; t < ngroups; t += ncl, ++local) {
         const int kt_n = tile_of(t).kt_n;
         const int b = local & 1;
-        mbar_wait(&acc_empty[b], ((local >> 1) & 1) ^ 1);  // epilogues drained this buffer
+        mbar_wait_acc(&acc_empty[b], ((local >> 1) & 1) ^ 1,  // epilogues drained this buffer
+                      p0_.trace ? &w_acc : nullptr);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc = tmem + (uint32_t)(b * BN);
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
-          mbar_wait(&full[s], (it / kStages) & 1);
+          mbar_wait_acc(&full[s], (it / kStages) & 1, p0_.trace ? &w_full : nullptr);
           if (it < 32) trace_at(p0_.trace, 34 + it);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a_base = su32(smem + s * S::kStageBytes);
@@ -642,7 +659,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         __syncwarp();
       }
-      if (have) mbar_wait(&acc_full[b], (local >> 1) & 1);
+      if (have) mbar_wait_acc(&acc_full[b], (local >> 1) & 1, p0_.trace ? &w_epi : nullptr);
       if (ew == 0 && lane == 0 && local < 16) trace_at(p0_.trace, 66 + local);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + row;
@@ -842,6 +859,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // smem / TMEM or arrive on its barriers
   if (PAIR) cluster_sync_all();
   if (threadIdx.x == 0) trace_at(p0_.trace, 98);
+  if (p0_.trace) {  // role wait cycles summed over CTAs: 128 producer, 129 MMA full, 130 MMA
+                    // acc-empty, 131 epilogue warp 2 acc-full, 132 CTA cycles, 133 CTAs
+    if (warp == 0 && lane == 0) atomicAdd(p0_.trace + 128, w_prod);
+    if (warp == 1 && lane == 0) {
+      atomicAdd(p0_.trace + 129, w_full);
+      atomicAdd(p0_.trace + 130, w_acc);
+    }
+    if (warp == 2 && lane == 0) {
+      atomicAdd(p0_.trace + 131, w_epi);
+      atomicAdd(p0_.trace + 132, (unsigned long long)(clock64() - t_start));
+      atomicAdd(p0_.trace + 133, 1ull);
+    }
+  }
   if (warp == 1) {
     if (PAIR)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
@@ -908,8 +938,8 @@ inline unsigned long long* trace_buffer() {
   if (on < 0) {
     const char* e = getenv("UL_TC_TRACE");
     on = e && atoi(e) != 0;
-    if (on && cudaMalloc(&buf, 128 * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
-    if (buf) cudaMemset(buf, 0, 128 * sizeof(unsigned long long));
+    if (on && cudaMalloc(&buf, kTraceSlots * sizeof(unsigned long long)) != cudaSuccess) buf = nullptr;
+    if (buf) cudaMemset(buf, 0, kTraceSlots * sizeof(unsigned long long));
   }
   return buf;
 }
@@ -1219,11 +1249,19 @@ int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
 
 }  // namespace ul
 
-// Diagnostics: copy the last traced launch's CTA-0 timestamps (128 x u64, ns).
+// Diagnostics: copy the trace buffer (kTraceSlots x u64: CTA-0 timestamps in ns,
+// role wait-cycle sums at 128..133).
 extern "C" int ul_tc_trace(unsigned long long* host_out) {
   unsigned long long* b = ul::tc::trace_buffer();
   UL_CHECK_ARG(b != nullptr, "tc trace: set UL_TC_TRACE=1 before the first GEMM");
-  UL_CUDA(cudaMemcpy(host_out, b, 128 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  UL_CUDA(cudaMemcpy(host_out, b, ul::tc::kTraceSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return UL_OK;
+}
+
+extern "C" int ul_tc_trace_reset(void) {
+  unsigned long long* b = ul::tc::trace_buffer();
+  UL_CHECK_ARG(b != nullptr, "tc trace: set UL_TC_TRACE=1 before the first GEMM");
+  UL_CUDA(cudaMemset(b, 0, ul::tc::kTraceSlots * sizeof(unsigned long long)));
   return UL_OK;
 }
 

@@ -26,12 +26,18 @@ def _lda(c):
 
 
 def trace():
-    buf = (C.c_ulonglong * 128)()
+    buf = (C.c_ulonglong * 160)()
     _lib.call("ul_tc_trace", C.cast(buf, C.c_void_p))
-    t = np.array(buf[:], dtype=np.float64)
+    t = np.array(buf[:], dtype=np.float64)  # (160 slots)
     t0 = t[0]
     rel = lambda a: [round((x - t0) / 1e3, 2) if x else None for x in a]  # noqa: E731
-    return dict(setup=rel([t[1]])[0], issue=rel(t[2:34]), mma=rel(t[34:66]),
+    n = max(t[133], 1.0)
+    waits = dict(ctas=int(t[133]), cta_kcycles=round(t[132] / n / 1e3, 2),
+                 producer_wait=round(t[128] / t[132], 3) if t[132] else None,
+                 mma_wait_full=round(t[129] / t[132], 3) if t[132] else None,
+                 mma_wait_acc=round(t[130] / t[132], 3) if t[132] else None,
+                 epi_wait_acc=round(t[131] / t[132], 3) if t[132] else None)
+    return dict(waits=waits, setup=rel([t[1]])[0], issue=rel(t[2:34]), mma=rel(t[34:66]),
                 acc=rel(t[66:82]), epi=rel(t[82:98]), exit=rel([t[98]])[0],
                 chunks=[rel(t[100 + 6 * c:105 + 6 * c]) for c in range(4)])
 
@@ -40,6 +46,7 @@ def run(name, fn):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    _lib.call("ul_tc_trace_reset")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     fn()
@@ -48,6 +55,7 @@ def run(name, fn):
     tr = trace()
     strip = lambda a: [x for x in a if x is not None]  # noqa: E731
     print(f"{name}: event {e0.elapsed_time(e1) * 1e3:.1f} us | setup {tr['setup']} | exit {tr['exit']}")
+    print("  wait fractions of CTA cycles:", tr["waits"])
     print("  issue", strip(tr["issue"]))
     print("  mma  ", strip(tr["mma"]))
     print("  acc  ", strip(tr["acc"]))
