@@ -36,7 +36,8 @@ def trace():
                  producer_wait=round(t[128] / t[132], 3) if t[132] else None,
                  mma_wait_full=round(t[129] / t[132], 3) if t[132] else None,
                  mma_wait_acc=round(t[130] / t[132], 3) if t[132] else None,
-                 epi_wait_acc=round(t[131] / t[132], 3) if t[132] else None)
+                 epi_wait_acc=round(t[131] / t[132], 3) if t[132] else None,
+                 mma_issue=round(t[134] / t[132], 3) if t[132] else None)
     return dict(waits=waits, setup=rel([t[1]])[0], issue=rel(t[2:34]), mma=rel(t[34:66]),
                 acc=rel(t[66:82]), epi=rel(t[82:98]), exit=rel([t[98]])[0],
                 chunks=[rel(t[100 + 6 * c:105 + 6 * c]) for c in range(4)])
