@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 2);  // keeps sbias 16 B aligned
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned long long w_prod = 0, w_full = 0, w_acc = 0, w_epi = 0;  // (UL_TC_TRACE)
+  unsigned long long w_prod = 0, w_full = 0, w_acc = 0, w_epi = 0, w_issue = 0;  // (UL_TC_TRACE)
   const long long t_start = clock64();
   pdl_trigger();
   if (threadIdx.x == 0) trace_at(p0_.trace, 0);
@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t a_base = su32(smem + s * S::kStageBytes);
           const uint32_t b_base =
               BRES ? su32(sbres + kt * S::kBBytes) : a_base + S::kABytes;
+          const long long ti0 = p0_.trace ? clock64() : 0;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             // K-major: 8-row x 128 B swizzle atoms (SBO 1024), one UMMA K step
@@ -575,6 +576,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           // frees the stage (in both CTAs of a pair) once these MMAs read it
           if (PAIR) mma_commit_pair(&empty[s]);
           else mma_commit(&empty[s]);
+          if (p0_.trace) w_issue += (unsigned long long)(clock64() - ti0);
         }
         if (PAIR) mma_commit_pair(&acc_full[b]);  // accumulator b complete (both CTAs)
         else mma_commit(&acc_full[b]);
@@ -865,6 +867,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (warp == 1 && lane == 0) {
       atomicAdd(p0_.trace + 129, w_full);
       atomicAdd(p0_.trace + 130, w_acc);
+      atomicAdd(p0_.trace + 134, w_issue);  // MMA issue + commit time
     }
     if (warp == 2 && lane == 0) {
       atomicAdd(p0_.trace + 131, w_epi);
