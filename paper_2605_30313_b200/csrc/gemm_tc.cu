@@ -259,11 +259,14 @@ struct Smem {
   static constexpr int kStageBytes = kABytes + (BRES ? 0 : kBBytes);
   // each epilogue warp double-buffers a 32-row x 64-byte staging box (a
   // box's TMA store reads one while the next box fills the other)
-  static constexpr int kStagingBytes = kEpiWarps * 2 * 32 * 64;
+  // (bf16 bias/ELU outputs: one box per warp, single-buffered -- its TMA
+  // store has a whole tile to read it -- which buys the 4th stage)
+  static constexpr int kNStg = (OB == 2 && (EPI == kEpiBias || EPI == kEpiBiasElu)) ? 1 : 2;
+  static constexpr int kStagingBytes = kEpiWarps * kNStg * 32 * 64;
   // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
   static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
   static constexpr int kFixed =
-      1024 /*align*/ + 512 /*barriers*/ + 2 * BN * 4 /*bias*/ + kCsumBytes;
+      512 /*barriers*/ + 2 * BN * 4 /*bias*/ + kCsumBytes;  // (base is 1 KB aligned)
   static constexpr int kBudget = 232448;
   static constexpr int kStagesFit = (kBudget - kStagingBytes - kFixed) / kStageBytes;
   static constexpr int kStages = BRES ? 3 : (kStagesFit > 6 ? 6 : kStagesFit);
@@ -361,10 +364,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
   constexpr uint32_t kBoxBytes = 32 * 64;  // one epilogue staging box
   static_assert(kStages >= 2, "shared memory too small for the pipeline");
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB-aligned base by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared state space (LDS/STS, not generic LD/ST)
-  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* smem = smem_raw;  // 1 KB aligned (128 B-swizzled TMA tiles need it)
+  if (threadIdx.x == 0 && (su32(smem_raw) & 1023u)) __trap();
   const uint32_t bres_bytes = BRES ? (uint32_t)p0_.bres_kt * S::kBBytes : 0u;
   uint8_t* sbres = smem + kStages * S::kStageBytes;  // B-resident K tiles
   uint8_t* staging = sbres + bres_bytes;
@@ -649,14 +653,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // both boxes now (after every earlier store has read its box), so the
       // TMA latency overlaps the accumulator wait and is paid once per tile
       constexpr int kNBox = kSlice / kBoxC;
-      constexpr bool kAuxAhead = EPI == kEpiEluGrad && kNBox <= 2;
+      constexpr bool kAuxAhead = EPI == kEpiEluGrad && kNBox <= S::kNStg;
       if (kAuxAhead) {
         if (lane == 0) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           mbar_expect_tx(abar, kNBox * kBoxBytes);
 #pragma unroll
           for (int k = 0; k < kNBox; ++k)
-            tma_load_3d(staging + (ew * 2 + ((cj + k) & 1)) * kBoxBytes, tX, abar,
+            tma_load_3d(staging + (ew * S::kNStg + (cj + k) % S::kNStg) * kBoxBytes, tX, abar,
                         n0 + slice * kSlice + k * kBoxC, m0 + quarter * 32, 0);
         }
         __syncwarp();
@@ -669,10 +673,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
 #pragma unroll 1
       for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += kBoxC, ++cj) {
-        uint8_t* stg = staging + (ew * 2 + (cj & 1)) * kBoxBytes;
+        uint8_t* stg = staging + (ew * S::kNStg + cj % S::kNStg) * kBoxBytes;
         // this staging box free again (the TMA store issued from it two boxes
         // ago has read it)
-        if (!kAuxAhead && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (!kAuxAhead && lane == 0) {
+          if (S::kNStg == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
         UL_ETRACE(0);
         if (EPI == kEpiEluGrad && !kAuxAhead) {
