@@ -219,3 +219,66 @@ def test_normalizer_vectorized_moments(D):
         assert norm.count == float(len(allx))
         np.testing.assert_allclose(norm.mean, allx.mean(0), rtol=1e-11, atol=1e-9)
         np.testing.assert_allclose(norm.var, allx.var(0), rtol=1e-7, atol=1e-9)
+
+
+def test_gather_rows_cfg2_minibatch_bit_exact():
+    """K4 at the cfg2 shape (98,304-row segment, one 24,576-row minibatch of a
+    reference-style permutation): obs rows (944 B, with the ones column), action
+    rows (48 B) and a per-row scalar gathered in one launch, bit-exact
+    (gathered minibatch contents bit-exact)."""
+    rng = np.random.default_rng(7)
+    rows, mb = 98304, 24576
+    obs = rng.normal(size=(rows, 236)).astype(np.float32)
+    act = rng.normal(size=(rows, 12)).astype(np.float32)
+    sc = rng.normal(size=rows).astype(np.float32)
+    idx = rng.permutation(rows)[:mb].astype(np.int64)
+    so, sa, ss = (torch.tensor(a, device="cuda") for a in (obs, act, sc))
+    do = torch.zeros((mb, 236), device="cuda")
+    da = torch.zeros((mb, 12), device="cuda")
+    ds = torch.zeros(mb, device="cuda")
+    idd = torch.tensor(idx, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P = _dev.ptr
+    _lib.call("ul_gather_rows", 3, _lib.ptr_array([P(so), P(sa), P(ss)]),
+              _lib.ptr_array([P(do), P(da), P(ds)]), _lib.i64_array([944, 48, 4]),
+              _lib.i64_array([944, 48, 4]), _lib.i64_array([944, 48, 4]),
+              _lib.i64_array([4 * 235, -1, -1]), P(idd), mb, 0, 0, rows, P(err), _dev.stream())
+    want = obs[idx].copy()
+    want[:, 235] = 1.0
+    np.testing.assert_array_equal(do.cpu().numpy(), want)
+    np.testing.assert_array_equal(da.cpu().numpy(), act[idx])
+    np.testing.assert_array_equal(ds.cpu().numpy(), sc[idx])
+    assert int(err.item()) == 0
+
+
+@pytest.mark.parametrize("cap", [1 << 20, 1000003])
+def test_gather_rows_replay_ring_window(cap):
+    """K6 replay sampling (R:replaypath/storage.py:106-133): absolute indices
+    mapped to ring slots by idx % capacity (power-of-two capacities take the
+    mask path), rows outside the [lo, hi) window skipped with the IndexError
+    flag raised; in-window rows bit-exact."""
+    rng = np.random.default_rng(cap % 97)
+    width = 220  # RowCodec(96, 23) = 218 floats, 16-byte pitch
+    ring = torch.randn(cap, width, device="cuda")
+    lo, hi = 3 * cap + 11, 4 * cap + 5  # the live window after wrapping
+    n = 8192
+    idx = rng.integers(lo, hi, n).astype(np.int64)
+    out = torch.zeros(n, width, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    P = _dev.ptr
+    rb = width * 4
+    args = lambda ix: (1, _lib.ptr_array([P(ring)]), _lib.ptr_array([P(out)]), _lib.i64_array([rb]),  # noqa: E731
+                       _lib.i64_array([rb]), _lib.i64_array([rb]), None, P(ix), n, cap, lo, hi,
+                       P(err), _dev.stream())
+    _lib.call("ul_gather_rows", *args(torch.tensor(idx, device="cuda")))
+    assert int(err.item()) == 0
+    np.testing.assert_array_equal(out.cpu().numpy(), ring.cpu().numpy()[idx % cap])
+    bad = idx.copy()
+    bad[17] = hi  # one row just past the window
+    out.zero_()
+    _lib.call("ul_gather_rows", *args(torch.tensor(bad, device="cuda")))
+    assert int(err.item()) == 1
+    got = out.cpu().numpy()
+    assert not got[17].any()
+    keep = np.arange(n) != 17
+    np.testing.assert_array_equal(got[keep], ring.cpu().numpy()[idx[keep] % cap])
