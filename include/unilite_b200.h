@@ -212,6 +212,10 @@ int ul_ring_insert(float* ring, int64_t cap, int64_t width, int64_t head, const 
 /* Device permutation of [0, n) (performance mode only; NOT the numpy Philox
  * shuffle of R:algos/ppo.py:162). */
 int ul_device_permutation(int64_t n, uint64_t key, int64_t* out, void* stream);
+/* count (<= 16) permutations of [0, n) in one launch, one per host key:
+ * out + e * ld holds the permutation of key e (the per-epoch minibatch orders). */
+int ul_device_permutations(int64_t n, int count, const uint64_t* host_keys, int64_t* out,
+                           int64_t ld, void* stream);
 
 /* ------------------------------------------- FlashSAC collector transforms */
 /* Device ReturnStdNormalizer.normalize + NStepPacker.push + replay insert

@@ -157,6 +157,7 @@ _PROTOS = {
                                  vp]),
     "ul_ring_insert": (C.c_int, [vp, i64, i64, i64, vp, i64, vp]),
     "ul_device_permutation": (C.c_int, [i64, C.c_uint64, vp, vp]),
+    "ul_device_permutations": (C.c_int, [i64, C.c_int, C.POINTER(C.c_uint64), vp, i64, vp]),
     "ul_norm_work_bytes": (i64, [i64]),
     "ul_norm_update": (C.c_int, [vp, i64, i64, i64, vp, vp, C.c_int, vp]),
     "ul_norm_apply": (C.c_int, [vp, i64, i64, i64, vp, vp, i64, vp]),

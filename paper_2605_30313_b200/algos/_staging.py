@@ -50,6 +50,8 @@ class DeviceSegment:
         self.has_tv = False
         self.slot = "ppo"
         self._raw: dict = {}  # width -> contiguous H2D landing buffer
+        self._pin: dict = {}  # field -> page-locked conversion buffer (f64 / bool -> f32 / u8)
+        self._pin_busy = None  # event after the last load's copies
         # the zero fills above run on the current stream, but a pipeline slot
         # is loaded on its copy stream: let the fills land first (once per
         # slot), or a fill still queued behind a running update could
@@ -86,7 +88,18 @@ class DeviceSegment:
             return
         a = np.asarray(src)
         if a.dtype != dtype:
-            a = a.astype(dtype)
+            # convert into this slot's page-locked buffer for the field, so the
+            # copy stays asynchronous (a pageable temporary would make the
+            # driver synchronise the copy stream, i.e. block the host behind
+            # the segment's large copies)
+            buf = self._pin.get(dst.data_ptr())
+            if buf is None or buf.size != a.size:
+                buf = _dev.pinned_empty((a.size,), dtype)
+                self._pin[dst.data_ptr()] = buf
+            if self._pin_busy is not None:
+                self._pin_busy.synchronize()  # the previous load's copies have read it
+            np.copyto(buf, a.reshape(-1), casting="unsafe")
+            a = buf
         _dev.h2d(dst, a.reshape(-1))
 
     def load(self, seg, with_advantages: bool = True) -> None:
@@ -108,6 +121,10 @@ class DeviceSegment:
         if with_advantages:
             self._put_vec(self.adv, seg.advantages)
             self._put_vec(self.ret, seg.returns)
+        if self._pin:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self._pin_busy = ev
 
     # ------------------------------------------------- per-step streaming
     def _put_step_rows(self, dst: torch.Tensor, t: int, src, width: int) -> None:

@@ -102,9 +102,13 @@ class _Plan:
                     oldv=oldv, actor_params=params.actor.buf, critic_params=params.critic.buf,
                     actor_m=opt.actor.m.buf, actor_v=opt.actor.v.buf, critic_m=opt.critic.m.buf,
                     critic_v=opt.critic.v.buf, perm=ds.perm, reduce_buf=red)
-        for k, v in vals.items():
-            setattr(b, k, _dev.ptr(v) if v is not None else None)
+        ptrs = tuple(_dev.ptr(v) if v is not None else None for v in vals.values())
+        if ptrs == self._bind_key:  # same buffers: the bound plan (and its graph) stands
+            return
+        for k, v in zip(vals, ptrs):
+            setattr(b, k, v)
         _lib.call("ul_ppo_plan_bind", self.h, C.byref(b))
+        self._bind_key = ptrs
 
 
 _PLANS: dict = {}
@@ -145,9 +149,9 @@ def fill_permutations(ds, rng, epochs: int) -> None:
     n = ds.rows
     if rng is None or isinstance(rng, DeviceRng):
         rng = rng if rng is not None else DeviceRng(0)
-        for e in range(epochs):
-            _lib.call("ul_device_permutation", n, rng.next_key(), _dev.ptr(ds.perm[e]),
-                      _dev.stream())
+        keys = (C.c_uint64 * epochs)(*[rng.next_key() for _ in range(epochs)])
+        _lib.call("ul_device_permutations", n, epochs, keys, _dev.ptr(ds.perm), ds.perm.stride(0),
+                  _dev.stream())
         return
     key = (n, epochs, _dist.world_info()[1])
     host = _PINNED_PERM.get(key)

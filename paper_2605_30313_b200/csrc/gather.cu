@@ -238,6 +238,37 @@ __global__ void feistel_perm_kernel(int64_t n, int half_bits, uint64_t seed, int
   }
 }
 
+struct PermKeys {
+  uint64_t key[16];
+};
+
+// blockIdx.y = permutation e (its own key), out rows ld apart
+__global__ void feistel_perms_kernel(int64_t n, int half_bits, PermKeys keys, int64_t* out,
+                                     int64_t ld) {
+  pdl_trigger();
+  pdl_wait();
+  const uint32_t mask = (1u << half_bits) - 1u;
+  const uint64_t seed = keys.key[blockIdx.y];
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  int64_t* o = out + (int64_t)blockIdx.y * ld;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t x = (uint64_t)i;
+    do {
+      uint32_t L = (uint32_t)(x >> half_bits) & mask, R = (uint32_t)x & mask;
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        const uint32_t F = mix32(R + (uint32_t)r * 0x632BE5ABu, (r & 1) ? k1 : k0) & mask;
+        const uint32_t nl = R;
+        R = L ^ F;
+        L = nl;
+      }
+      x = ((uint64_t)L << half_bits) | R;
+    } while (x >= (uint64_t)n);
+    o[i] = (int64_t)x;
+  }
+}
+
 }  // namespace
 }  // namespace ul
 
@@ -333,6 +364,24 @@ extern "C" int ul_ring_insert(float* ring, int64_t cap, int64_t width, int64_t h
     UL_CUDA(cudaMemcpyAsync(ring, src + part1 * width, rb * (count - part1), cudaMemcpyDefault,
                             s));
   return UL_OK;
+}
+
+// Several device permutations in one launch (the update's per-epoch orders).
+extern "C" int ul_device_permutations(int64_t n, int count, const uint64_t* host_keys,
+                                      int64_t* out, int64_t ld, void* stream) {
+  UL_CHECK_ARG(n >= 0 && n < (int64_t(1) << 62) && count >= 0 && count <= 16 && ld >= n,
+               "permutations: bad n / count / ld");
+  if (n == 0 || count == 0) return UL_OK;
+  int bits = 1;
+  while ((int64_t(1) << (2 * bits)) < n) ++bits;
+  ul::PermKeys k{};
+  for (int e = 0; e < count; ++e) k.key[e] = host_keys[e];
+  int64_t blocks = ul::ceil_div(n, 256);
+  const int64_t cap = ul::ceil_div(8 * ul::kNumSMs, count);
+  blocks = blocks > cap ? cap : blocks;
+  return ul::launch_pdl("feistel_perms_kernel", ul::feistel_perms_kernel,
+                        dim3((unsigned)blocks, (unsigned)count), dim3(256), 0,
+                        ul::as_stream(stream), n, bits, k, out, ld);
 }
 
 // Device minibatch permutation of [0, n) from a 64-bit key (performance mode).
