@@ -212,10 +212,16 @@ def run_ours(args):
                  "bf16": "tcgen05 kind::f16 bf16 operands, fp32 accumulation (TMA + TMEM)"}[prec]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # UL_DIST_BACKEND=gloo: a functional check of the multi-rank path when
+        # the ranks must share one GPU (NCCL refuses duplicate devices)
+        backend = os.environ.get("UL_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         _dist.set_segment_mode("local")
     T, N, od, cd, ad, hid = CONFIGS[CFG]
     cfg = A.PpoConfig()
