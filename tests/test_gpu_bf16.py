@@ -181,8 +181,10 @@ def _blocks(flat, dims):
     return out
 
 
-@pytest.mark.parametrize("hidden", [(512, 256, 128), (256, 128, 128)])
-def test_ppo_single_step_grads_bf16_per_layer(bf16_mode, hidden):
+@pytest.mark.parametrize("hidden,act_dim,cobs", [((512, 256, 128), 12, None),
+                                                 ((256, 128, 128), 12, None),
+                                                 ((512, 256, 128), 29, 101)])
+def test_ppo_single_step_grads_bf16_per_layer(bf16_mode, hidden, act_dim, cobs):
     """One minibatch's gradients on the bf16 path (fused output stage, batched
     dW, ELU-gradient dX) against the f64 oracle, block by block: every W, b and
     log_std of both networks within 3e-2 relative norm error, so an error in a
@@ -191,7 +193,10 @@ def test_ppo_single_step_grads_bf16_per_layer(bf16_mode, hidden):
 
     T, N = 8, 1024
     od = 235 if hidden[0] == 512 else 48
-    seg, actor, critic = _synthetic(T, N, od, od, 12, hidden, seed=5)
+    if act_dim == 29:  # cfg5 (G1 humanoid) shapes: obs 98 / critic obs 101 / 29 actions
+        od = 98
+    cd = cobs or od
+    seg, actor, critic = _synthetic(T, N, od, cd, act_dim, hidden, seed=5)
     adv, ret = O.gae(seg["rewards"], seg["values"], seg["terminated"], seg["truncated"],
                      seg["bootstrap_value"], 0.99, 0.95, seg["truncation_values"])
     advn = O.normalize_adv(adv.reshape(-1))
@@ -202,15 +207,15 @@ def test_ppo_single_step_grads_bf16_per_layer(bf16_mode, hidden):
             f(seg["actions"]).astype(np.float64), seg["behavior_log_prob"].reshape(-1), advn,
             ret.reshape(-1), seg["values"].reshape(-1))
     terms, ga, gc = O.ppo_loss_grads(to64(actor), to64(critic), *args, O.PpoCfg())
-    params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(od, hidden, 12), actor.flat()),
-                        TN.ModelParams.from_numpy(TN.Arch(od, hidden, 1), critic.flat()))
+    params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(od, hidden, act_dim), actor.flat()),
+                        TN.ModelParams.from_numpy(TN.Arch(cd, hidden, 1), critic.flat()))
     gterms, gga, ggc = A.ppo_loss_and_grads(params, f(seg["obs"]), f(seg["critic_obs"]),
                                             f(seg["actions"]), seg["behavior_log_prob"].reshape(-1),
                                             advn, ret.reshape(-1), seg["values"].reshape(-1),
                                             A.PpoConfig())
     for k in ("policy_loss", "value_loss", "kl"):
         assert abs(gterms[k] - terms[k]) <= BF16_TOL * max(1.0, abs(terms[k])), k
-    for ref, got, dims in ((ga, gga, (od, *hidden, 12)), (gc, ggc, (od, *hidden, 1))):
+    for ref, got, dims in ((ga, gga, (od, *hidden, act_dim)), (gc, ggc, (cd, *hidden, 1))):
         for i, (r, g) in enumerate(zip(_blocks(np.asarray(ref.flat(), np.float64), dims),
                                        _blocks(np.asarray(got.flat(), np.float64), dims))):
             nr = np.linalg.norm(r)
