@@ -117,8 +117,8 @@ __global__ void __launch_bounds__(W * 32) reduce_dw_kernel(ReduceTable tab) {
 // Every partial reduction of a pass in ONE launch.  Blocks [end[i-1], end[i])
 // belong to job i.  Shallow jobs (split-K dW, nz <= kShallowZ): one thread per
 // float4 column, all of its nz loads in flight, summed in z order.  Deep jobs
-// (per-block / per-CTA partial sets): 32 float4 columns per block, the 8 warps
-// take z = w, w + 8, ... and combine in fixed order.  Deterministic.
+// (per-block / per-CTA partial sets): 8 float4 columns per block, 32 z-phases
+// combined in fixed order.  Deterministic.
 constexpr int kShallowZ = 64;
 struct ReduceAll {
   ReduceJob r[kMaxReduceJobs];
@@ -182,15 +182,18 @@ __global__ void __launch_bounds__(256) reduce_all_kernel(const __grid_constant__
     reduce_store(q, j, acc);
     return;
   }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t j = ((int64_t)blk * 32 + lane) * 4;
+  // deep sets: 8 float4 columns per CTA, 32 z-phases (the CTA's 256 threads)
+  // each summing z = phase, phase + 32, ... with 8 loads in flight, then a
+  // fixed-order combine of the phases
+  const int c8 = threadIdx.x & 7, ph = threadIdx.x >> 3;
+  const int64_t j = ((int64_t)blk * 8 + c8) * 4;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (j < q.len) {
-    for (int z0 = w; z0 < nz; z0 += 64) {
+    for (int z0 = ph; z0 < nz; z0 += 32 * 8) {
       float4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int z = z0 + 8 * u;
+        const int z = z0 + 32 * u;
         v[u] = z < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * q.len + j))
                       : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -203,12 +206,13 @@ __global__ void __launch_bounds__(256) reduce_all_kernel(const __grid_constant__
       }
     }
   }
-  sm[w][lane] = acc;
+  float4* sp = &sm[0][0];  // [32 phases][8 columns]
+  sp[ph * 8 + c8] = acc;
   __syncthreads();
-  if (w == 0 && j < q.len) {
-    float4 t = sm[0][lane];
-    for (int k = 1; k < 8; ++k) {
-      const float4 q4 = sm[k][lane];
+  if (ph == 0 && j < q.len) {
+    float4 t = sp[c8];
+    for (int k = 1; k < 32; ++k) {
+      const float4 q4 = sp[k * 8 + c8];
       t.x += q4.x;
       t.y += q4.y;
       t.z += q4.z;
@@ -570,7 +574,7 @@ int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
         if (jobs[q].len <= 0 || jobs[q].nz <= 0) continue;
         tab.r[tab.n] = jobs[q];
         const int64_t cols = ceil_div(jobs[q].len, 4);
-        blocks += (int)ceil_div(cols, jobs[q].nz <= kShallowZ ? 256 : 32);
+        blocks += (int)ceil_div(cols, jobs[q].nz <= kShallowZ ? 256 : 8);
         tab.end[tab.n++] = blocks;
       }
       if (tab.n == 0) continue;
