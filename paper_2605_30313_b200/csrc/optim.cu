@@ -102,31 +102,64 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_o
   const int nb = gridDim.x;
   pdl_trigger();
   pdl_wait();
-  for (int s = 0; s < st.nseg; ++s) {
-    const float* g = st.g[s];
-    const int64_t n = st.n[s];
-    double acc = 0.0;
+  const int64_t stride = (int64_t)nb * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (st.nseg == 2) {
+    // the PPO / SAC case: both segments' first 8 loads in flight together
+    double acc[2] = {0.0, 0.0};
     int bad = 0;
-    const int64_t stride = (int64_t)nb * blockDim.x;
-    // 8 loads in flight per thread (issued before the dependent adds)
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 8 * stride) {
-      float x[8];
+    for (int64_t i0 = t0; i0 < st.n[0] || i0 < st.n[1]; i0 += 8 * stride) {
+      float x[2][8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int64_t i = i0 + u * stride;
-        x[u] = i < n ? __ldg(g + i) : 0.f;
-      }
+      for (int s = 0; s < 2; ++s)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc += (double)x[u] * (double)x[u];
-        bad |= !isfinite(x[u]);
-      }
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + u * stride;
+          x[s][u] = i < st.n[s] ? __ldg(st.g[s] + i) : 0.f;
+        }
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc[s] += (double)x[s][u] * (double)x[s][u];
+          bad |= (!isfinite(x[s][u])) << s;
+        }
     }
-    const double tot = block_sum(acc, scratch);
-    const int any_bad = __syncthreads_or(bad);
+    const double t0s = block_sum(acc[0], scratch);
+    const double t1s = block_sum(acc[1], scratch + 16);
+    const int any0 = __syncthreads_or(bad & 1), any1 = __syncthreads_or(bad & 2);
     if (threadIdx.x == 0) {
-      ctl->part[blockIdx.x][s] = tot;
-      ctl->part_bad[blockIdx.x][s] = any_bad;
+      ctl->part[blockIdx.x][0] = t0s;
+      ctl->part[blockIdx.x][1] = t1s;
+      ctl->part_bad[blockIdx.x][0] = any0;
+      ctl->part_bad[blockIdx.x][1] = any1 ? 1 : 0;
+    }
+  } else {
+    for (int s = 0; s < st.nseg; ++s) {
+      const float* g = st.g[s];
+      const int64_t n = st.n[s];
+      double acc = 0.0;
+      int bad = 0;
+      // 8 loads in flight per thread (issued before the dependent adds)
+      for (int64_t i0 = t0; i0 < n; i0 += 8 * stride) {
+        float x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + u * stride;
+          x[u] = i < n ? __ldg(g + i) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc += (double)x[u] * (double)x[u];
+          bad |= !isfinite(x[u]);
+        }
+      }
+      const double tot = block_sum(acc, scratch);
+      const int any_bad = __syncthreads_or(bad);
+      if (threadIdx.x == 0) {
+        ctl->part[blockIdx.x][s] = tot;
+        ctl->part_bad[blockIdx.x][s] = any_bad;
+      }
     }
   }
   if (!last_block_ticket(&ctl->ticket, nb)) return;
@@ -154,8 +187,13 @@ __device__ __forceinline__ void stage_param(const StageOut& so, int s, int64_t i
     const int64_t o = i - so.w_off[s][l];
     const int cols = so.cols[s][l];
     if (o >= 0 && o < (int64_t)so.rows[s][l] * cols) {
-      const int r = (int)o / cols, c = (int)o - r * cols;
-      const int64_t d = so.dst_off[s][l] + (int64_t)r * so.ld[s][l] + c;
+      int64_t d;
+      if (so.ld[s][l] == cols) {  // unpadded staged rows (in % 8 == 0): same offset
+        d = so.dst_off[s][l] + o;
+      } else {
+        const int r = (int)o / cols, c = (int)o - r * cols;
+        d = so.dst_off[s][l] + (int64_t)r * so.ld[s][l] + c;
+      }
       if (so.dtype == kBf16) reinterpret_cast<__nv_bfloat16*>(so.dst[s])[d] = __float2bfloat16_rn(p);
       else reinterpret_cast<float*>(so.dst[s])[d] = p;
       return;
@@ -184,26 +222,67 @@ __device__ __forceinline__ void read_apply_ctl(const volatile ul_opt_ctl* c, int
 
 // clip scale + Adam over segment s, elements t0, t0 + stride, ... (float4
 // lanes when aligned); refreshes the staged tensor-core weights
+struct AdamVec {
+  float4 g, m, v, p;
+};
+
+__device__ __forceinline__ AdamVec load_adam4(const SegTable& st, int s, int64_t i) {
+  AdamVec a;
+  a.g = reinterpret_cast<const float4*>(st.g[s])[i];
+  a.m = reinterpret_cast<const float4*>(st.m[s])[i];
+  a.v = reinterpret_cast<const float4*>(st.v[s])[i];
+  a.p = reinterpret_cast<const float4*>(st.p[s])[i];
+  return a;
+}
+
+__device__ __forceinline__ void adam4(const SegTable& st, int s, int64_t i, AdamVec a,
+                                      const AdamScalars& k, float f, bool scale, int write_grads,
+                                      const StageOut& so, int has_so) {
+  float* ga = reinterpret_cast<float*>(&a.g);
+  float* ma = reinterpret_cast<float*>(&a.m);
+  float* va = reinterpret_cast<float*>(&a.v);
+  float* pa = reinterpret_cast<float*>(&a.p);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (scale) ga[e] = __fmul_rn(ga[e], f);
+    adam_elem(ga[e], ma[e], va[e], pa[e], k);
+  }
+  if (write_grads && scale) reinterpret_cast<float4*>(st.g[s])[i] = a.g;
+  reinterpret_cast<float4*>(st.m[s])[i] = a.m;
+  reinterpret_cast<float4*>(st.v[s])[i] = a.v;
+  reinterpret_cast<float4*>(st.p[s])[i] = a.p;
+  if (has_so && so.dst[s]) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) stage_param(so, s, 4 * i + e, pa[e]);
+  }
+}
+
+__device__ __forceinline__ AdamScalars adam_scalars(const ApplyCtl& c, int s) {
+  AdamScalars k;
+  const double t = c.t[s];
+  k.b1 = (float)c.beta1;
+  k.one_m_b1 = (float)(1.0 - c.beta1);
+  k.b2 = (float)c.beta2;
+  k.one_m_b2 = (float)(1.0 - c.beta2);
+  k.bc1 = (float)(1.0 - pow(c.beta1, t));
+  k.bc2 = (float)(1.0 - pow(c.beta2, t));
+  k.lr = (float)c.lr[s];
+  k.eps = (float)c.eps;
+  return k;
+}
+
+// vector elements [v0, n4) step stride, scalar tail from 4 n4 + t0
 __device__ void apply_seg(const SegTable& st, const ApplyCtl& c, int s, int write_grads,
-                          int do_adam, const StageOut& so, int has_so, int64_t t0, int64_t stride) {
+                          int do_adam, const StageOut& so, int has_so, int64_t t0, int64_t stride,
+                          int64_t v0 = -1) {
   const int upd = c.upd[s];
   // clip_global_norm scales even when a later Adam raises; Adam itself only on upd
   const float f = (float)c.factor;
   const bool scale = c.factor != 1.0;
   float* __restrict__ g = st.g[s];
   const int64_t n = st.n[s];
-  AdamScalars k;
-  if (do_adam) {
-    const double t = c.t[s];
-    k.b1 = (float)c.beta1;
-    k.one_m_b1 = (float)(1.0 - c.beta1);
-    k.b2 = (float)c.beta2;
-    k.one_m_b2 = (float)(1.0 - c.beta2);
-    k.bc1 = (float)(1.0 - pow(c.beta1, t));
-    k.bc2 = (float)(1.0 - pow(c.beta2, t));
-    k.lr = (float)c.lr[s];
-    k.eps = (float)c.eps;
-  }
+  AdamScalars k{};
+  if (do_adam) k = adam_scalars(c, s);
   if (!do_adam || !upd) {  // clip-only (clip_global_norm) or a skipped segment
     if (write_grads && scale)
       for (int64_t i = t0; i < n; i += stride) g[i] = __fmul_rn(g[i], f);
@@ -212,28 +291,8 @@ __device__ void apply_seg(const SegTable& st, const ApplyCtl& c, int s, int writ
   float *pm = st.m[s], *pv = st.v[s], *pp = st.p[s];
   const bool vec = (((uintptr_t)g | (uintptr_t)pm | (uintptr_t)pv | (uintptr_t)pp) & 15) == 0;
   const int64_t n4 = vec ? n / 4 : 0;
-  for (int64_t i = t0; i < n4; i += stride) {  // 16 B per array per thread
-    float4 g4 = reinterpret_cast<const float4*>(g)[i];
-    float4 m4 = reinterpret_cast<float4*>(pm)[i], v4 = reinterpret_cast<float4*>(pv)[i];
-    float4 p4 = reinterpret_cast<float4*>(pp)[i];
-    float* ga = reinterpret_cast<float*>(&g4);
-    float* ma = reinterpret_cast<float*>(&m4);
-    float* va = reinterpret_cast<float*>(&v4);
-    float* pa = reinterpret_cast<float*>(&p4);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (scale) ga[e] = __fmul_rn(ga[e], f);
-      adam_elem(ga[e], ma[e], va[e], pa[e], k);
-    }
-    if (write_grads && scale) reinterpret_cast<float4*>(g)[i] = g4;
-    reinterpret_cast<float4*>(pm)[i] = m4;
-    reinterpret_cast<float4*>(pv)[i] = v4;
-    reinterpret_cast<float4*>(pp)[i] = p4;
-    if (has_so && so.dst[s]) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) stage_param(so, s, 4 * i + e, pa[e]);
-    }
-  }
+  for (int64_t i = v0 >= 0 ? v0 : t0; i < n4; i += stride)  // 16 B per array per thread
+    adam4(st, s, i, load_adam4(st, s, i), k, f, scale, write_grads, so, has_so);
   for (int64_t i = 4 * n4 + t0; i < n; i += stride) {
     float gi = g[i];
     if (scale) gi = __fmul_rn(gi, f);
