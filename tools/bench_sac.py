@@ -1,4 +1,4 @@
-"""cfg3 FastSAC learner benchmark (BASELINE.json
+"""cfg3 FastSAC / cfg4 FlashSAC learner benchmark.  cfg3 (BASELINE.json
 configs[2]): 2^20-row replay ring resident in HBM as codec rows
 (RowCodec(96, 23), 872 B/row), batch 8192 drawn by host indices, twin critics
 119->1024->512->256->1 with LayerNorm, actor 96->512->256->128->23,
@@ -7,7 +7,10 @@ updates).  Timed: K sac_update calls (a multiple of 4) with the batch indices
 already on the device and device noise (``value``), and the same through host
 index vectors + the host noise stream (``e2e``: H2D of 64 KB indices + noise
 per update).  CPU baseline: the oracle's sac_update on the same shapes
-(--cpu-updates, default 2).  Prints one JSON object.
+(--cpu-updates, default 2).  ``--cfg cfg4``: the FlashSAC wide/large-batch
+shape of SURVEY.md 8(d) -- batch 32,768, critics 119->1024->1024->1024->1
+(no LayerNorm), actor 96->512->512->23, flashsac_defaults (tau 0.01,
+policy_frequency 2).  Prints one JSON object.
 """
 from __future__ import annotations
 
@@ -30,14 +33,15 @@ from paper_2605_30313_b200.algos.ppo import DeviceRng  # noqa: E402
 
 OD, AD, B, RING = 96, 23, 8192, 1 << 20
 CH, AH = (1024, 512, 256), (512, 256, 128)
+PF = 4  # policy_frequency
 
 
 def flops_per_update(do_actor: bool) -> float:
     """2 flop/MAC; target fwd (actor + 2 target critics), 2 critic trainings
     (fwd + dW + dH) and, on actor steps, actor fwd + bwd (3x) + 2 critic fwd +
     dH/dX (2x) -- SURVEY.md §8(d) cfg3 row (~14.2 MFLOP/row averaged)."""
-    cq = (OD + AD) * CH[0] + CH[0] * CH[1] + CH[1] * CH[2] + CH[2]
-    ca = OD * AH[0] + AH[0] * AH[1] + AH[1] * AH[2] + AH[2] * AD
+    cq = (OD + AD) * CH[0] + sum(CH[i] * CH[i + 1] for i in range(len(CH) - 1)) + CH[-1]
+    ca = OD * AH[0] + sum(AH[i] * AH[i + 1] for i in range(len(AH) - 1)) + AH[-1] * AD
     f = 2 * B * (ca + 2 * cq)          # target
     f += 2 * 2 * B * 3 * cq           # critics fwd + dX-free bwd (dW + dH)
     if do_actor:
@@ -45,10 +49,10 @@ def flops_per_update(do_actor: bool) -> float:
     return float(f)
 
 
-def build(ln: bool):
+def build(ln: bool, flash: bool = False):
     actor = TN.init_params(TN.Arch(OD, AH, AD), 0)
     qa = TN.Arch(OD + AD, CH, 1, layer_norm=ln)
-    cfg = A.SacConfig()
+    cfg = A.flashsac_defaults() if flash else A.SacConfig()
     return A.SacState.create(actor, TN.init_params(qa, 1), TN.init_params(qa, 2), cfg), cfg
 
 
@@ -59,10 +63,15 @@ def main():
     ap.add_argument("--precision", default="bf16")
     ap.add_argument("--no-ln", action="store_true")
     ap.add_argument("--cpu-updates", type=int, default=2)
+    ap.add_argument("--cfg", choices=("cfg3", "cfg4"), default="cfg3")
     a = ap.parse_args()
+    global B, CH, AH, PF
+    if a.cfg == "cfg4":
+        B, CH, AH, PF = 32768, (1024, 1024, 1024), (512, 512), 2
+        a.no_ln = True
     K = (a.steps + 3) // 4 * 4
     P.set_precision(a.precision)
-    st, cfg = build(not a.no_ln)
+    st, cfg = build(not a.no_ln, a.cfg == "cfg4")
     width = 2 * OD + AD + 3
     g = torch.Generator(device="cuda").manual_seed(0)
     ring = torch.randn(RING, width, device="cuda", generator=g)
@@ -105,11 +114,12 @@ def main():
         out = e2e_step(i)
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / K
-    fl = (3 * flops_per_update(False) + flops_per_update(True)) / 4
+    fl = ((PF - 1) * flops_per_update(False) + flops_per_update(True)) / PF
     res = {
-        "workload": "cfg3 FastSAC sac_update (ring 2^20 x RowCodec(96,23), batch 8192, critics "
-                    f"119-1024-512-256-1{' +LN' if not a.no_ln else ''}, actor 96-512-256-128-23,"
-                    " policy_frequency 4)",
+        "workload": f"{a.cfg} {'FlashSAC' if a.cfg == 'cfg4' else 'FastSAC'} sac_update (ring 2^20 x "
+                    f"RowCodec(96,23), batch {B}, critics 119-{'-'.join(map(str, CH))}-1"
+                    f"{' +LN' if not a.no_ln else ''}, actor 96-{'-'.join(map(str, AH))}-23,"
+                    f" policy_frequency {PF})",
         "precision": a.precision, "updates": K,
         "ms_per_update": ms, "updates_per_s": 1e3 / ms,
         "e2e_ms_per_update": e2e_ms, "e2e_updates_per_s": 1e3 / e2e_ms,
