@@ -46,6 +46,10 @@ struct PpoPlan {
   cudaStream_t cap_stream = nullptr;
   cudaStream_t side = nullptr;  // critic branch (fork/join inside each step)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+  // the next minibatch's gather runs on the side stream under this step's
+  // optimizer (and all-reduce) -- ev_gfork / ev_gjoin bracket it
+  cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;
+  bool gathered_ahead = false;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
   // optional per-phase CUDA-event profiling (ul_ppo_plan_profile)
@@ -132,6 +136,8 @@ int alloc_plan(PpoPlan* p) {
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
   UL_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_gfork, cudaEventDisableTiming));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_gjoin, cudaEventDisableTiming));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
   return UL_OK;
 }
@@ -150,6 +156,8 @@ void free_plan(PpoPlan* p) {
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   if (p->side) cudaStreamDestroy(p->side);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_gfork) cudaEventDestroy(p->ev_gfork);
+  if (p->ev_gjoin) cudaEventDestroy(p->ev_gjoin);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
 }
 
@@ -226,6 +234,7 @@ void fill_stage_out(const PpoPlan* p, StageOut* so) {
 // device part of begin: stats reset + advantage statistics + staged weights
 // (graph-capturable)
 int begin_device(PpoPlan* p, cudaStream_t s) {
+  p->gathered_ahead = false;
   if (p->d.gemm_backend >= 1) {
     UL_TRY(stage_weights_dt(p->va, p->b.actor_params, p->wst_a, p->dt, s));
     UL_TRY(stage_weights_dt(p->vc, p->b.critic_params, p->wst_c, p->dt, s));
@@ -246,13 +255,13 @@ int upload_ctl(PpoPlan* p, double lr_a, double lr_c, int64_t t_a, int64_t t_c, c
   return UL_OK;
 }
 
-int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
+// K4: minibatch (e, k)'s rows of the 7 per-row arrays in one gather launch
+int step_gather(PpoPlan* p, int e, int k, cudaStream_t s) {
   const ul_ppo_bindings& b = p->b;
   const int64_t ml = p->mb_local;
   const int64_t* idx = p->d.local_shards
                            ? b.perm + (int64_t)e * p->rows + (int64_t)k * ml
                            : b.perm + (int64_t)e * p->rows + (int64_t)k * p->mb + p->d.rank * ml;
-  const bool tc = p->d.gemm_backend >= 1;
   const bool bf = p->dt == kBf16;
   // K4: one gather launch for the 7 per-row arrays; the obs / critic-obs
   // pad column is set to 1.0 (the tensor-core dW's bias column)
@@ -268,7 +277,45 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   const bool ones_o = p->d.ld_obs > od, ones_c = p->d.ld_cobs > cd;
   const int64_t ones[7] = {ones_o ? 4 * od : -1, ones_c ? 4 * cd : -1, -1, -1, -1, -1, -1};
   const int cvt[7] = {bf ? 1 : 0, bf ? 1 : 0, 0, 0, 0, 0, 0};
-  UL_TRY(gather_rows(7, src, dst, sst, dstr, rb, ones, cvt, idx, ml, 0, 0, p->rows, nullptr, s));
+  return gather_rows(7, src, dst, sst, dstr, rb, ones, cvt, idx, ml, 0, 0, p->rows, nullptr, s);
+}
+
+// After step (e, k)'s backward the minibatch staging is free: gather the next
+// step's rows on the side stream, where it runs under this step's optimizer
+// kernels (and the all-reduce in data-parallel runs) instead of before the
+// next forward.  UL_GATHER_AHEAD=0 disables.
+int gather_ahead(PpoPlan* p, int e, int k, cudaStream_t s) {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("UL_GATHER_AHEAD");
+    on = v ? atoi(v) != 0 : 1;
+  }
+  int ne = e, nk = k + 1;
+  if (nk == p->d.minibatches) {
+    nk = 0;
+    ++ne;
+  }
+  if (!on || ne >= p->d.epochs) return UL_OK;
+  UL_CUDA(cudaEventRecord(p->ev_gfork, s));
+  UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_gfork, 0));
+  UL_TRY(step_gather(p, ne, nk, p->side));
+  UL_CUDA(cudaEventRecord(p->ev_gjoin, p->side));
+  p->gathered_ahead = true;
+  return UL_OK;
+}
+
+int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
+  const ul_ppo_bindings& b = p->b;
+  const int64_t ml = p->mb_local;
+  const bool tc = p->d.gemm_backend >= 1;
+  const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
+  const bool ones_o = p->d.ld_obs > od, ones_c = p->d.ld_cobs > cd;
+  if (p->gathered_ahead) {  // gathered on the side stream under the previous step
+    UL_CUDA(cudaStreamWaitEvent(s, p->ev_gjoin, 0));
+    p->gathered_ahead = false;
+  } else {
+    UL_TRY(step_gather(p, e, k, s));
+  }
   mark(p, 1, s);
   // K7 forwards of both networks in lockstep: one grouped tensor-core launch
   // per layer, the critic's small kernels on the side stream.  Weights
@@ -388,7 +435,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
     mark(p, 2, s);
     UL_TRY(mlp_pass(p, nets, be, ml, s, false, &dd));
     mark(p, 5, s);
-    return UL_OK;
+    return gather_ahead(p, e, k, s);
   }
   // K9 head
   PpoHeadArgs h{};
@@ -423,7 +470,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   // K8 backwards of both networks into the contiguous all-reduce buffer
   UL_TRY(mlp_pass(p, nets, be, ml, s, false));
   mark(p, 5, s);
-  return UL_OK;
+  return gather_ahead(p, e, k, s);
 }
 
 int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
