@@ -80,6 +80,14 @@ def main():
     run("fwd2", lambda: _lib.call("ul_gemm_tc", 3, 2, rows, 128, 257, P(x2), x2.stride(0), P(w2),
                                   w2.stride(0), P(h2), h2.stride(0), P(b), None, 0, 1, DT,
                                   _dev.stream()))
+    # dx2: dh1 [rows, 256] = dZ2 [rows, 128] W2 [128, 256] * elu'(h1) (BRES, K = 128)
+    dz2 = torch.randn(rows, _lda(128), device=dev).to(EL)
+    w2 = (torch.randn(128, _lda(256), device=dev) * 0.05).to(EL)
+    h1 = torch.randn(rows, _lda(256), device=dev).to(EL)
+    dx2 = torch.empty(rows, _lda(256), device=dev, dtype=EL)
+    run("dx2", lambda: _lib.call("ul_gemm_tc", 1, 3, rows, 256, 128, P(dz2), dz2.stride(0), P(w2),
+                                 w2.stride(0), P(dx2), dx2.stride(0), None, P(h1), h1.stride(0), 1,
+                                 DT, _dev.stream()))
     dh = torch.randn(rows, _lda(512), device=dev).to(EL)
     wt = (torch.randn(512, _lda(256), device=dev) * 0.05).to(EL)
     dh1 = torch.randn(rows, _lda(256), device=dev).to(EL)
