@@ -355,7 +355,8 @@ def run_ours(args):
                    "segment_bytes_per_gpu": ds.h2d_bytes(seg), "gemm_precision": prec_name},
         "update_ms": ms,
         "parity_mode": {"value": transitions / (par_ms / 1e3), "unit": UNIT, "update_ms": par_ms,
-                        "indices": "host numpy Philox permutation per epoch (reference stream)"},
+                        "indices": "host numpy Philox permutation per epoch (reference stream), "
+                                   "drawn while the previous epoch runs (one CUDA graph per epoch)"},
         "e2e": {"value": transitions / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_ms,

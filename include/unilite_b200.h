@@ -322,6 +322,11 @@ int ul_ppo_plan_reduce_buffer(void* plan, float** ptr, int64_t* n);
 /* begin + every step (graph-captured when use_graph) */
 int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
                     int64_t t_critic, int use_graph, void* stream);
+/* One epoch of ul_ppo_plan_run as its own CUDA graph (epoch 0 also uploads the
+ * controller and stages the weights): lets the caller upload epoch e + 1's
+ * host permutation while epoch e runs.  Epochs must run 0, 1, ... in order. */
+int ul_ppo_plan_run_epoch(void* plan, int epoch, double lr_actor, double lr_critic,
+                          int64_t t_actor, int64_t t_critic, void* stream);
 /* D2H of the statistics + stream sync; UL_ERR_DIVERGENCE if a step diverged */
 int ul_ppo_plan_finish(void* plan, ul_ppo_result* out, void* stream);
 /* kernels per update (graph kernel nodes) and algorithmic GEMM FLOPs per update */

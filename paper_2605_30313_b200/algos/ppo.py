@@ -204,14 +204,37 @@ def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib
 
 def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False):
     world, rank = _world()
-    fill_permutations(ds, rng, cfg.epochs)
     plan = _plan_for(params, cfg, ds, world, rank, raw_adv)
+    host_rng = rng is not None and not isinstance(rng, DeviceRng)
+    if world == 1 and host_rng:
+        # parity mode: one graph per epoch, so the host draws the reference
+        # stream's permutation for epoch e + 1 while epoch e runs
+        plan.bind(ds, adv, ret, oldv, params, opt, None)
+        _pipelined_host_epochs(plan, ds, rng, cfg.epochs, opt)
+        return plan
+    fill_permutations(ds, rng, cfg.epochs)
     red = None
     if world > 1:
         red = _dist.reduce_buffer(plan.red_len)
     plan.bind(ds, adv, ret, oldv, params, opt, red)
     launch_plan(plan, params, opt, world, red)
     return plan
+
+
+def _pipelined_host_epochs(plan, ds, rng, epochs: int, opt) -> None:
+    n = ds.rows
+    key = (n, epochs, _dist.world_info()[1])
+    host = _PINNED_PERM.get(key)
+    if host is None:
+        host = _dev.pinned_empty((epochs, n), np.int64)
+        _PINNED_PERM[key] = host
+    s = _dev.stream()
+    _lib.call("ul_stream_sync", s)  # the previous update's copies out of `host` are done
+    for e in range(epochs):
+        host[e] = rng.permutation(n)  # (numpy releases the GIL; the GPU runs epoch e - 1)
+        _dev.h2d(ds.perm[e], host[e])
+        _lib.call("ul_ppo_plan_run_epoch", plan.h, e, opt.actor.lr, opt.critic.lr, opt.actor.t,
+                  opt.critic.t, s)
 
 
 def _stats(res, opt) -> UpdateStats:

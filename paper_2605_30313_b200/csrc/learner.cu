@@ -52,6 +52,11 @@ struct PpoPlan {
   bool gathered_ahead = false;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
+  // per-epoch graphs (parity mode: the host draws epoch e + 1's permutation
+  // while epoch e runs); epoch 0's also stages the weights
+  static constexpr int kMaxEpochGraphs = 32;
+  cudaGraphExec_t egraph[kMaxEpochGraphs] = {};
+  bool epoch_mode = false;  // capturing / running one epoch per graph
   // optional per-phase CUDA-event profiling (ul_ppo_plan_profile)
   struct Prof {
     static constexpr int kMax = 4096;
@@ -148,6 +153,8 @@ void free_plan(PpoPlan* p) {
     delete p->prof;
   }
   if (p->graph) cudaGraphExecDestroy(p->graph);
+  for (int e = 0; e < PpoPlan::kMaxEpochGraphs; ++e)
+    if (p->egraph[e]) cudaGraphExecDestroy(p->egraph[e]);
   if (p->arena) cudaFree(p->arena);
   if (p->ctl_h) cudaFreeHost(p->ctl_h);
   if (p->st_h) cudaFreeHost(p->st_h);
@@ -295,7 +302,8 @@ int gather_ahead(PpoPlan* p, int e, int k, cudaStream_t s) {
     nk = 0;
     ++ne;
   }
-  if (!on || ne >= p->d.epochs) return UL_OK;
+  // (one graph per epoch: the next epoch's permutation is not uploaded yet)
+  if (!on || ne >= p->d.epochs || (p->epoch_mode && ne != e)) return UL_OK;
   UL_CUDA(cudaEventRecord(p->ev_gfork, s));
   UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_gfork, 0));
   UL_TRY(step_gather(p, ne, nk, p->side));
@@ -595,6 +603,12 @@ extern "C" int ul_ppo_plan_bind(void* plan, const ul_ppo_bindings* b) {
   PpoPlan* p = (PpoPlan*)plan;
   UL_CHECK_ARG(p && b, "ppo plan: null argument");
   const bool same = p->bound && memcmp(&p->b, b, sizeof(*b)) == 0;
+  if (!same)
+    for (int e = 0; e < PpoPlan::kMaxEpochGraphs; ++e)
+      if (p->egraph[e]) {
+        cudaGraphExecDestroy(p->egraph[e]);
+        p->egraph[e] = nullptr;
+      }
   if (!same && p->graph) {
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
@@ -669,6 +683,43 @@ extern "C" int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, in
     UL_CUDA(ce);
   }
   UL_CUDA(cudaGraphLaunch(p->graph, p->cap_stream));
+  UL_CUDA(cudaEventRecord(p->ev_out, p->cap_stream));
+  UL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
+  return UL_OK;
+}
+
+// One epoch of the update as its own CUDA graph (parity mode with host
+// permutations: the caller uploads epoch e's permutation, launches epoch e,
+// and draws epoch e + 1's while it runs).  Epoch 0 uploads the controller and
+// stages the weights first.
+extern "C" int ul_ppo_plan_run_epoch(void* plan, int epoch, double lr_actor, double lr_critic,
+                                     int64_t t_actor, int64_t t_critic, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "ppo plan: not bound");
+  UL_CHECK_ARG(epoch >= 0 && epoch < p->d.epochs && epoch < PpoPlan::kMaxEpochGraphs,
+               "ppo plan: epoch %d outside [0, %d)", epoch, p->d.epochs);
+  cudaStream_t s = ul::as_stream(stream);
+  if (epoch == 0) UL_TRY(ul::upload_ctl(p, lr_actor, lr_critic, t_actor, t_critic, s));
+  UL_CUDA(cudaEventRecord(p->ev_in, s));
+  UL_CUDA(cudaStreamWaitEvent(p->cap_stream, p->ev_in, 0));
+  if (!p->egraph[epoch]) {
+    cudaGraph_t g;
+    p->epoch_mode = true;
+    UL_CUDA(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int st = epoch == 0 ? ul::begin_device(p, p->cap_stream) : UL_OK;
+    for (int k = 0; k < p->d.minibatches && st == UL_OK; ++k) {
+      st = ul::step_grads(p, epoch, k, p->cap_stream);
+      if (st == UL_OK) st = ul::step_apply(p, epoch, k, p->cap_stream);
+    }
+    cudaError_t ce = cudaStreamEndCapture(p->cap_stream, &g);
+    p->epoch_mode = false;
+    if (st != UL_OK) return st;
+    UL_CUDA(ce);
+    ce = cudaGraphInstantiate(&p->egraph[epoch], g, 0);
+    cudaGraphDestroy(g);
+    UL_CUDA(ce);
+  }
+  UL_CUDA(cudaGraphLaunch(p->egraph[epoch], p->cap_stream));
   UL_CUDA(cudaEventRecord(p->ev_out, p->cap_stream));
   UL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
   return UL_OK;
