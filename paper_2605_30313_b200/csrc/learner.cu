@@ -437,9 +437,10 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
     f.gwc = nets[1].grads + vc.w_off[nlc - 1];
     f.gbc = nets[1].grads + vc.b_off[nlc - 1];
     f.gcsc = f.csc ? nets[1].grads + vc.b_off[nlc - 2] : nullptr;
+    f.lossp = reinterpret_cast<float*>(p->head_part);  // (doubles region, ample as floats)
+    f.lossld = ceil_div(3 + p->A, 4) * 4;
     DeferredDw dd;
-    UL_TRY(launch_ppo_fused(f, p->dt, &dd.jobs[0], &dd.jobs[1], s));
-    dd.nj = 2;
+    UL_TRY(launch_ppo_fused(f, p->dt, dd.jobs, &dd.nj, s));
     mark(p, 2, s);
     UL_TRY(mlp_pass(p, nets, be, ml, s, false, &dd));
     mark(p, 5, s);

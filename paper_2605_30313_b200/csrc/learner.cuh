@@ -64,10 +64,16 @@ struct PpoFusedArgs {
   int64_t plenc;
   int csc;
   float *gwc, *gbc, *gcsc;
+  // optional (tensor-core variant): per-block loss / dlog_std partials as
+  // floats [block][lossld] for the pass's reduction launch instead of the
+  // last-CTA fold (block 0 carries the entropy-coefficient term)
+  float* lossp;
+  int64_t lossld;
 };
 bool ppo_fused_ok(int A, int Ka, int Kc);
-// ja / jc: the partial reductions, for the caller's next reduction launch
-int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob* jc,
+// jobs: the partial reductions (2, or 3 with the loss partials), for the
+// caller's next reduction launch; *njobs receives their count
+int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* jobs, int* njobs,
                      cudaStream_t s);
 int ppo_head_partial_doubles(int64_t n_local, int A);
 int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ticket, double* out,

@@ -926,6 +926,18 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
     }
   }
   // ---- loss / dlog_std partials, last CTA folds them in fixed order
+  if (f.lossp) {  // reduced with the pass's other partials (no last-CTA fold)
+    float* lp = f.lossp + (int64_t)blockIdx.x * f.lossld;
+    for (int qq = t; qq < f.lossld; qq += kMThr) {
+      double v = 0.0;
+      if (qq < nq) {
+        for (int k = 0; k < kMWarps; ++k) v += red[k][qq];
+        if (blockIdx.x == 0 && qq >= 3) v += a.ent_coef_add;
+      }
+      lp[qq] = (float)v;
+    }
+    return;
+  }
   double* part = a.part + (int64_t)blockIdx.x * nq;
   for (int qq = t; qq < nq; qq += kMThr) {
     double s = 0.0;
@@ -1015,8 +1027,11 @@ bool ppo_fused_ok(int A, int Ka, int Kc) {
          fused_smem<float>(Ka, Kc, pad_np(A)) <= 200 * 1024;
 }
 
-int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob* jc,
+int launch_ppo_fused(const PpoFusedArgs& fin, int dtype, ReduceJob* jobs, int* njobs,
                      cudaStream_t s) {
+  PpoFusedArgs f = fin;
+  ReduceJob* ja = jobs;
+  ReduceJob* jc = jobs + 1;
   UL_CHECK_ARG(ppo_fused_ok(f.h.A, f.Ka, f.Kc), "ppo fused head: unsupported shape");
   static int mma_env = -1;
   if (mma_env < 0) {
@@ -1028,6 +1043,7 @@ int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob*
   const bool mma = mma_env && dtype == kBf16 && (f.Ka % 2) == 0 && (f.Kc % 2) == 0 &&
                    (ncg & (ncg - 1)) == 0 && ncg <= 32 && f.wba != nullptr &&
                    MmaSmem(f.Ka, f.Kc, f.h.A <= 16 ? 2 : 4).total <= 200 * 1024;
+  if (!mma) f.lossp = nullptr;  // (the SIMT variant folds its loss partials itself)
   if (mma) UL_TRY(f.h.A <= 16 ? launch_mma<2>(f, s) : launch_mma<4>(f, s));
   else UL_TRY(dtype == kBf16 ? launch_t<__nv_bfloat16>(f, s) : launch_t<float>(f, s));
   const int64_t nblk = ceil_div(f.h.n_local > 0 ? f.h.n_local : 1, mma ? kMRows : kFRows);
@@ -1055,6 +1071,20 @@ int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* ja, ReduceJob*
   jc->o1 = f.gbc;
   jc->n2 = f.csc ? f.Kc : 0;
   jc->o2 = f.gcsc;
+  *njobs = 2;
+  if (f.lossp) {  // [pol, val, kl] -> loss_out, dlog_std -> the gradient slot
+    ReduceJob* jl = jobs + 2;
+    *jl = ReduceJob{};
+    jl->src = f.lossp;
+    jl->nz = (int)nblk;
+    jl->kind = 1;
+    jl->len = f.lossld;
+    jl->n0 = 3;
+    jl->o0 = f.h.loss_out;
+    jl->n1 = f.h.A;
+    jl->o1 = f.h.dlogstd_out;
+    *njobs = 3;
+  }
   return UL_OK;
 }
 
