@@ -28,40 +28,36 @@ constexpr int kPrepThreads = 256;
 
 constexpr double kLog2PiO = 1.8378770664093453;
 
-// R:algos/ppo.py loss bookkeeping of one minibatch step (see heads.cu)
-__device__ void finalize_loss(const LossFinalize& f, ul_opt_ctl* ctl) {
-  const double pol = -(double)f.loss[0] / f.n;
-  const double val = (double)f.loss[1] / f.n;
-  const double kl = (double)f.loss[2] / f.n;
-  double ent = 0.0;
-  for (int j = 0; j < f.A; ++j) ent += (double)f.log_std[j] + 0.5 * (kLog2PiO + 1.0);
-  const double total = pol + f.vcoef * val - f.ecoef * ent;
-  if (!isfinite(total)) ctl->loss_bad = 1;
-  if (!ctl->diverged && isfinite(total)) {
-    f.st->policy_sum += pol;
-    f.st->value_sum += val;
-    f.st->entropy_sum += ent;
-    f.st->kl_last = kl;
-    if (f.last_in_epoch) f.st->kl_epoch_sum += kl;
-    f.st->steps += 1;
-  }
-}
-
-// last CTA of the prepare pass: fixed-order, block-parallel fold of the
-// per-CTA partials, loss finalisation, divergence latch, clip factor, t += 1
-__device__ void prepare_tail(const SegTable& st, ul_opt_ctl* ctl, const LossFinalize& lf,
-                             int has_lf, int nb, double* scratch) {
+// Runs in ONE CTA (blockDim 256).  Every global value it depends on is loaded
+// up front with the loads in flight together -- the controller / stats
+// records sit behind pointers the compiler must assume alias, so written as
+// a chain of read-modify-writes the tail was ~10 us of serial load latency.
+// (partials: sum g^2 of segment s from block b at part[b * ldp + s], its
+// non-finite flag at bad[b * ldp + s])
+__device__ __noinline__ void prepare_tail(int nseg, const double* part, const int* bad_part,
+                                          int ldp, ul_opt_ctl* ctl, const LossFinalize& lf,
+                                          int has_lf, int nb, double* scratch) {
   __shared__ double red[UL_MAX_SEG];
   __shared__ int red_bad[UL_MAX_SEG];
-  for (int s = 0; s < st.nseg; ++s) {
-    double a = 0.0;
-    int bad = 0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-      a += ctl->part[b][s];
-      bad |= ctl->part_bad[b][s];
-    }
-    const double tot = block_sum(a, scratch);
-    const int any_bad = __syncthreads_or(bad);
+  __shared__ double lstd[UL_MAX_ACT];
+  // all segments' partials in one sweep (fixed per-thread order, then the
+  // fixed-order block sum: deterministic)
+  double acc[UL_MAX_SEG] = {0.0, 0.0, 0.0, 0.0};
+  int bad[UL_MAX_SEG] = {0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+#pragma unroll
+    for (int s = 0; s < UL_MAX_SEG; ++s)
+      if (s < nseg) {
+        acc[s] += part[(int64_t)b * ldp + s];
+        bad[s] |= bad_part[(int64_t)b * ldp + s];
+      }
+  }
+  if (has_lf && (int)threadIdx.x < lf.A) lstd[threadIdx.x] = (double)lf.log_std[threadIdx.x];
+#pragma unroll
+  for (int s = 0; s < UL_MAX_SEG; ++s) {
+    if (s >= nseg) break;
+    const double tot = block_sum(acc[s], scratch);
+    const int any_bad = __syncthreads_or(bad[s]);
     if (threadIdx.x == 0) {
       red[s] = tot;
       red_bad[s] = any_bad;
@@ -69,31 +65,64 @@ __device__ void prepare_tail(const SegTable& st, ul_opt_ctl* ctl, const LossFina
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  if (has_lf) finalize_loss(lf, ctl);
+  // ---- loads (independent, issued together)
+  const int loss_bad = ctl->loss_bad, was_diverged = ctl->diverged, steps = ctl->steps;
+  const double max_norm = ctl->max_norm;
+  int64_t t[UL_MAX_SEG];
+#pragma unroll
+  for (int s = 0; s < UL_MAX_SEG; ++s) t[s] = s < nseg ? ctl->t[s] : 0;
+  float loss[3] = {0.f, 0.f, 0.f};
+  ul_ppo_stats st{};
+  if (has_lf) {
+    loss[0] = lf.loss[0];
+    loss[1] = lf.loss[1];
+    loss[2] = lf.loss[2];
+    st = *lf.st;
+  }
+  // ---- R:algos/ppo.py loss bookkeeping of the step (see heads.cu)
+  int earlier_bad = loss_bad;
+  if (has_lf) {
+    const double pol = -(double)loss[0] / lf.n;
+    const double val = (double)loss[1] / lf.n;
+    const double kl = (double)loss[2] / lf.n;
+    double ent = 0.0;
+    for (int j = 0; j < lf.A; ++j) ent += lstd[j] + 0.5 * (kLog2PiO + 1.0);
+    const double total = pol + lf.vcoef * val - lf.ecoef * ent;
+    if (!isfinite(total)) earlier_bad = 1;
+    if (!was_diverged && isfinite(total)) {
+      st.policy_sum += pol;
+      st.value_sum += val;
+      st.entropy_sum += ent;
+      st.kl_last = kl;
+      if (lf.last_in_epoch) st.kl_epoch_sum += kl;
+      st.steps += 1;
+      *lf.st = st;
+    }
+  }
+  // ---- joint norm, per-segment update decision (reference order: loss
+  // check, then segment 0 finiteness, then segment 1, ...), divergence latch
   double joint = 0.0;
-  int earlier_bad = ctl->loss_bad;
-  const int was_diverged = ctl->diverged;
-  for (int s = 0; s < st.nseg; ++s) {
+  for (int s = 0; s < nseg; ++s) {
     const double sum = red[s];
-    const int bad = red_bad[s];
+    const int sbad = red_bad[s];
     ctl->sumsq[s] = sum;
-    ctl->seg_bad[s] = bad;
+    ctl->seg_bad[s] = sbad;
     joint += sum;
-    earlier_bad |= bad;
+    earlier_bad |= sbad;
     const int upd = !was_diverged && !earlier_bad;
     ctl->seg_update[s] = upd;
-    if (upd) ctl->t[s] += 1;
+    if (upd) ctl->t[s] = t[s] + 1;
   }
   const double norm = sqrt(joint);
   ctl->norm = norm;
   // reference: factor applied only when max_norm > 0 and total > max_norm (NaN -> no clip)
-  ctl->factor = (ctl->max_norm > 0.0 && norm > ctl->max_norm) ? ctl->max_norm / (norm + 1e-12) : 1.0;
+  ctl->factor = (max_norm > 0.0 && norm > max_norm) ? max_norm / (norm + 1e-12) : 1.0;
   if (earlier_bad && !was_diverged) {
     ctl->diverged = 1;
-    ctl->fail_step = ctl->steps;
+    ctl->fail_step = steps;
   }
   ctl->loss_bad = 0;
-  ctl->steps += 1;
+  ctl->steps = steps + 1;
 }
 
 __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl,
@@ -163,7 +192,8 @@ __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_o
     }
   }
   if (!last_block_ticket(&ctl->ticket, nb)) return;
-  prepare_tail(st, ctl, lf, has_lf, nb, scratch);
+  prepare_tail(st.nseg, &ctl->part[0][0], &ctl->part_bad[0][0], UL_MAX_SEG, ctl, lf, has_lf, nb,
+               scratch);
 }
 
 struct AdamScalars {
