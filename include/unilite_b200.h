@@ -322,6 +322,14 @@ int ul_ppo_plan_reduce_buffer(void* plan, float** ptr, int64_t* n);
 /* begin + every step (graph-captured when use_graph) */
 int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
                     int64_t t_critic, int use_graph, void* stream);
+/* ul_ppo_plan_run (graph) enqueued behind `prev`'s update on the same stream
+ * before the host has read prev's statistics: the Adam step counters and the
+ * divergence latch continue from prev's device controller (prev may be plan). */
+int ul_ppo_plan_run_after(void* plan, const void* prev, double lr_actor, double lr_critic,
+                          void* stream);
+/* Enqueue the D2H of the update's result records behind it; the next
+ * ul_ppo_plan_finish then waits for those records only (not the stream). */
+int ul_ppo_plan_collect(void* plan, void* stream);
 /* One epoch of ul_ppo_plan_run as its own CUDA graph (epoch 0 also uploads the
  * controller and stages the weights): lets the caller upload epoch e + 1's
  * host permutation while epoch e runs.  Epochs must run 0, 1, ... in order. */

@@ -170,6 +170,8 @@ _PROTOS = {
     "ul_ppo_plan_step_apply": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "ul_ppo_plan_reduce_buffer": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),
     "ul_ppo_plan_run": (C.c_int, [vp, f64, f64, i64, i64, C.c_int, vp]),
+    "ul_ppo_plan_run_after": (C.c_int, [vp, vp, f64, f64, vp]),
+    "ul_ppo_plan_collect": (C.c_int, [vp, vp]),
     "ul_ppo_plan_run_epoch": (C.c_int, [vp, C.c_int, f64, f64, i64, i64, vp]),
     "ul_ppo_plan_finish": (C.c_int, [vp, C.POINTER(PpoResult), vp]),
     "ul_sac_plan_create": (C.c_int, [C.POINTER(SacPlanDesc), C.POINTER(vp)]),

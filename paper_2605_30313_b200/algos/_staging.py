@@ -49,7 +49,8 @@ class DeviceSegment:
         self.perm = torch.zeros((max(epochs, 1), rows), dtype=torch.int64, device=dev)
         self.has_tv = False
         self.slot = "ppo"
-        self._raw: dict = {}  # width -> contiguous H2D landing buffer
+        self._raw: dict = {}  # field -> contiguous H2D landing buffer
+        self._land: dict = {}  # f32 field -> f64 landing buffer (pinned f64 sources)
         self._pin: dict = {}  # field -> page-locked conversion buffer (f64 / bool -> f32 / u8)
         self._pin_busy = None  # event after the last load's copies
         # the zero fills above run on the current stream, but a pipeline slot
@@ -59,10 +60,34 @@ class DeviceSegment:
         torch.cuda.current_stream().synchronize()
 
     # ------------------------------------------------------------- loading
-    def _put_rows(self, dst: torch.Tensor, src, width: int) -> None:
+    def _raw_for(self, name: str, width: int, device) -> torch.Tensor:
+        """The field's own contiguous H2D landing buffer (one per field, so every
+        copy of a segment can be queued before any re-pitch kernel)."""
+        raw = self._raw.get(name)
+        if raw is None or raw.numel() != self.rows * width:
+            raw = torch.empty(self.rows * width, dtype=torch.float32, device=device)
+            self._raw[name] = raw
+        return raw
+
+    def _repitch(self, jobs) -> None:
+        """One K4 row-kernel launch re-pitching landed fields into their HBM rows."""
+        if not jobs:
+            return
+        n = len(jobs)
+        _lib.call("ul_gather_rows", n, _lib.ptr_array([_dev.ptr(r) for r, _, _ in jobs]),
+                  _lib.ptr_array([_dev.ptr(d) for _, d, _ in jobs]),
+                  _lib.i64_array([w * 4 for _, _, w in jobs]),
+                  _lib.i64_array([d.stride(0) * 4 for _, d, _ in jobs]),
+                  _lib.i64_array([w * 4 for _, _, w in jobs]), None, None, jobs[0][1].shape[0],
+                  0, 0, jobs[0][1].shape[0], None, _dev.stream())
+
+    def _put_rows(self, name: str, dst: torch.Tensor, src, width: int, jobs: list) -> None:
         """Host [rows, width] -> HBM [rows, ld]: one contiguous H2D at full PCIe
-        rate into a raw landing buffer, then the K4 row kernel re-pitches it in
-        HBM (a pitched 2-D H2D of 940 B rows crawls at a fraction of link speed)."""
+        rate into the field's landing buffer; the re-pitch (K4 row kernel, a
+        pitched 2-D H2D of 940 B rows crawls at a fraction of link speed) is
+        appended to `jobs` and launched after every copy of the segment: on
+        the copy stream a kernel queued between two copies waits for SMs the
+        running update holds, and would stall the copies behind it."""
         if _is_dev(src):
             src = src.reshape(self.rows, width)
             dst[:, :width].copy_(src)  # device -> device staging copy
@@ -71,22 +96,29 @@ class DeviceSegment:
         if a.dtype != np.float32:
             a = a.astype(np.float32)
         a = np.ascontiguousarray(a.reshape(self.rows, width))
-        raw = self._raw.get(width)
-        if raw is None:
-            raw = torch.empty(self.rows * width, dtype=torch.float32, device=dst.device)
-            self._raw[width] = raw
+        raw = self._raw_for(name, width, dst.device)
         _dev.h2d(raw, a)
-        rb = width * 4
-        _lib.call("ul_gather_rows", 1, _lib.ptr_array([_dev.ptr(raw)]),
-                  _lib.ptr_array([_dev.ptr(dst)]), _lib.i64_array([rb]),
-                  _lib.i64_array([dst.stride(0) * 4]), _lib.i64_array([rb]), None, None, self.rows,
-                  0, 0, self.rows, None, _dev.stream())
+        jobs.append((raw, dst, width))
 
-    def _put_vec(self, dst: torch.Tensor, src, dtype=np.float32) -> None:
+    def _put_vec(self, dst: torch.Tensor, src, dtype=np.float32, casts: list | None = None) -> None:
         if _is_dev(src):
             dst.copy_(src.reshape(-1).to(dst.dtype))
             return
         a = np.asarray(src)
+        if a.dtype == np.bool_ and dtype == np.uint8:
+            a = a.view(np.uint8)  # same bytes
+        if casts is not None and a.dtype == np.float64 and dtype == np.float32 \
+                and _dev.is_pinned(a):
+            # pinned f64 (the reference's [T, N] per-step scalars): copy the
+            # bytes as they are and narrow on the device after the segment's
+            # copies -- no host conversion, no wait on the previous load
+            land = self._land.get(dst.data_ptr())
+            if land is None or land.numel() != a.size:
+                land = torch.empty(a.size, dtype=torch.float64, device=dst.device)
+                self._land[dst.data_ptr()] = land
+            _dev.h2d(land, a.reshape(-1))
+            casts.append((land, dst))
+            return
         if a.dtype != dtype:
             # convert into this slot's page-locked buffer for the field, so the
             # copy stays asynchronous (a pageable temporary would make the
@@ -106,38 +138,40 @@ class DeviceSegment:
         """Stage every field the learner reads (async on the current stream;
         pinned host arrays copy without a host sync)."""
         od, cd, ad = self.dims
-        self._put_rows(self.obs, seg.obs, od)
-        self._put_rows(self.cobs, seg.critic_obs, cd)
-        self._put_rows(self.act, seg.actions, ad)
-        self._put_vec(self.blogp, seg.behavior_log_prob)
-        self._put_vec(self.rewards, seg.rewards)
-        self._put_vec(self.values, seg.values)
+        jobs: list = []
+        casts: list = []
+        self._put_rows("obs", self.obs, seg.obs, od, jobs)
+        self._put_rows("cobs", self.cobs, seg.critic_obs, cd, jobs)
+        self._put_rows("act", self.act, seg.actions, ad, jobs)
+        self._put_vec(self.blogp, seg.behavior_log_prob, casts=casts)
+        self._put_vec(self.rewards, seg.rewards, casts=casts)
+        self._put_vec(self.values, seg.values, casts=casts)
         self._put_vec(self.term, seg.terminated, np.uint8)
         self._put_vec(self.trunc, seg.truncated, np.uint8)
-        self._put_vec(self.boot, seg.bootstrap_value)
+        self._put_vec(self.boot, seg.bootstrap_value, casts=casts)
         self.has_tv = seg.truncation_values is not None
         if self.has_tv:
-            self._put_vec(self.tv, seg.truncation_values)
+            self._put_vec(self.tv, seg.truncation_values, casts=casts)
         if with_advantages:
-            self._put_vec(self.adv, seg.advantages)
-            self._put_vec(self.ret, seg.returns)
-        if self._pin:
+            self._put_vec(self.adv, seg.advantages, casts=casts)
+            self._put_vec(self.ret, seg.returns, casts=casts)
+        if self._pin:  # (recorded before the re-pitch: the copies alone read the buffers)
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
             self._pin_busy = ev
+        for land, dst in casts:  # f64 -> f32 narrowing of the landed scalars
+            dst.copy_(land)
+        self._repitch(jobs)
 
     # ------------------------------------------------- per-step streaming
-    def _put_step_rows(self, dst: torch.Tensor, t: int, src, width: int) -> None:
+    def _put_step_rows(self, name: str, dst: torch.Tensor, t: int, src, width: int) -> None:
         """Step t's [N, width] host rows -> HBM rows [t*N, (t+1)*N) (t-major)."""
         N = self.N
         a = np.asarray(src)
         if a.dtype != np.float32:
             a = a.astype(np.float32)
         a = np.ascontiguousarray(a.reshape(N, width))
-        raw = self._raw.get(width)
-        if raw is None:
-            raw = torch.empty(self.rows * width, dtype=torch.float32, device=dst.device)
-            self._raw[width] = raw
+        raw = self._raw_for(name, width, dst.device)
         part = raw[t * N * width:(t + 1) * N * width]
         _dev.h2d(part, a)
         rb = width * 4
@@ -159,9 +193,9 @@ class DeviceSegment:
         if not 0 <= t < self.T:
             raise IndexError(f"step {t} outside [0, {self.T})")
         od, cd, ad = self.dims
-        self._put_step_rows(self.obs, t, obs, od)
-        self._put_step_rows(self.cobs, t, critic_obs, cd)
-        self._put_step_rows(self.act, t, actions, ad)
+        self._put_step_rows("obs", self.obs, t, obs, od)
+        self._put_step_rows("cobs", self.cobs, t, critic_obs, cd)
+        self._put_step_rows("act", self.act, t, actions, ad)
         self._put_step_vec(self.blogp, t, behavior_log_prob)
         self._put_step_vec(self.rewards, t, rewards)
         self._put_step_vec(self.term, t, terminated, np.uint8)
@@ -172,11 +206,22 @@ class DeviceSegment:
             self._put_step_vec(self.tv, t, truncation_values)
 
     def h2d_bytes(self, seg, with_advantages: bool = True) -> int:
+        """Bytes one load() moves over PCIe (pinned f64 scalars cross as f64)."""
         od, cd, ad = self.dims
-        n = self.rows * 4 * (od + cd + ad + 3 + (2 if with_advantages else 0))
-        n += self.rows * 2 + self.N * 4
+
+        def sc(a):
+            if _is_dev(a):
+                return 4
+            a = np.asarray(a)
+            return 8 if a.dtype == np.float64 and _dev.is_pinned(a) else 4
+
+        n = self.rows * 4 * (od + cd + ad)
+        n += self.rows * (sc(seg.behavior_log_prob) + sc(seg.rewards) + sc(seg.values))
+        if with_advantages:
+            n += self.rows * (sc(seg.advantages) + sc(seg.returns))
+        n += self.rows * 2 + self.N * sc(seg.bootstrap_value)
         if seg.truncation_values is not None:
-            n += self.rows * 4
+            n += self.rows * sc(seg.truncation_values)
         return n
 
 

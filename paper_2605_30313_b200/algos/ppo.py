@@ -84,6 +84,7 @@ class _Plan:
         self.h = h
         self.desc = desc
         self._bind_key = None
+        self.pending = None  # unread PendingUpdate whose records this plan holds
         n = C.c_int64()
         p = C.c_void_p()
         _lib.call("ul_ppo_plan_reduce_buffer", self.h, C.byref(p), C.byref(n))
@@ -169,11 +170,61 @@ def _world():
     return _dist.world_info()
 
 
-def launch_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> None:
-    """Enqueue one update (single GPU: one CUDA-graph launch, no host wait)."""
+class PendingUpdate:
+    """An update enqueued behind earlier ones without a host round trip
+    (``PpoPipeline.update_async``).  ``result()`` waits for this update's
+    result records only -- later updates may already be queued behind it --
+    and returns its ``UpdateStats``; results are read in launch order."""
+
+    def __init__(self, plan: _Plan, opt: AcOpt):
+        self.plan, self.opt = plan, opt
+        self._stats = None
+        self._err = None
+
+    @property
+    def done(self) -> bool:
+        return self._stats is not None or self._err is not None
+
+    def _finish(self) -> None:
+        if self.done:
+            return
+        try:
+            self._stats = _stats(finish_plan(self.plan, self.opt), self.opt)
+        except Exception as e:  # (DivergenceError: raised by result())
+            self._err = e
+        if self.plan.pending is self:
+            self.plan.pending = None
+
+    def result(self) -> UpdateStats:
+        _drain_pending(upto=self)
+        if self._err is not None:
+            raise self._err
+        return self._stats
+
+
+_PENDING: list = []  # enqueued, unread chained updates in launch order
+
+
+def _drain_pending(upto=None) -> None:
+    """Read pending chained updates in launch order (through `upto`, else all),
+    so the host copy of the Adam step counters is current again."""
+    while _PENDING:
+        h = _PENDING.pop(0)
+        h._finish()
+        if h is upto:
+            break
+
+
+def launch_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red,
+                prev: _Plan | None = None) -> None:
+    """Enqueue one update (single GPU: one CUDA-graph launch, no host wait).
+    prev: the plan of the update this one is chained behind on the device
+    (its step counters / divergence latch continue from prev's controller)."""
     s = _dev.stream()
     cfgd = plan.desc
-    if world == 1:
+    if world == 1 and prev is not None:
+        _lib.call("ul_ppo_plan_run_after", plan.h, prev.h, opt.actor.lr, opt.critic.lr, s)
+    elif world == 1:
         _lib.call("ul_ppo_plan_run", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
                   opt.critic.t, 1, s)
     else:
@@ -202,10 +253,15 @@ def run_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red) -> _lib
     return finish_plan(plan, opt)
 
 
-def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False):
+def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False, prev=None):
     world, rank = _world()
     plan = _plan_for(params, cfg, ds, world, rank, raw_adv)
     host_rng = rng is not None and not isinstance(rng, DeviceRng)
+    if prev is None or world != 1 or host_rng:
+        _drain_pending()  # the launch reads the host step counters
+        prev = None
+    elif plan.pending is not None:
+        _drain_pending(upto=plan.pending)  # its result records are about to be reused
     if world == 1 and host_rng:
         # parity mode: one graph per epoch, so the host draws the reference
         # stream's permutation for epoch e + 1 while epoch e runs
@@ -217,7 +273,7 @@ def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False):
     if world > 1:
         red = _dist.reduce_buffer(plan.red_len)
     plan.bind(ds, adv, ret, oldv, params, opt, red)
-    launch_plan(plan, params, opt, world, red)
+    launch_plan(plan, params, opt, world, red, prev)
     return plan
 
 
@@ -379,6 +435,7 @@ class PpoPipeline:
         self.slots: list = [None, None]
         self.queue: list = []  # slots holding staged, not yet consumed segments
         self.next_slot = 0
+        self._prev = None  # plan of the last update (device-chained launches)
 
     def prefetch(self, segment) -> None:
         """Start the H2D of a segment into the idle slot (returns at once when
@@ -421,6 +478,14 @@ class PpoPipeline:
     def update(self, next_segment=None) -> UpdateStats:
         """Run the update on the oldest staged segment; stage `next_segment`
         meanwhile.  Returns that update's statistics (host)."""
+        return self.update_async(next_segment).result()
+
+    def update_async(self, next_segment=None) -> PendingUpdate:
+        """``update`` without waiting for it: the update is enqueued behind the
+        previous one (single GPU, device permutations: Adam step counters and
+        the divergence latch continue on the device), so the host prepares
+        and launches update i+1 while update i runs.  ``result()`` on the
+        returned handle reads the statistics; read them in launch order."""
         if not self.queue:
             raise RuntimeError("no staged segment: call prefetch() first")
         k = self.queue.pop(0)
@@ -432,12 +497,23 @@ class PpoPipeline:
         if world > 1 and next_segment is not None:
             self.prefetch(next_segment)  # host-driven DP steps: stage first
             next_segment = None
+        chain = world == 1 and (self.rng is None or isinstance(self.rng, DeviceRng))
         plan = _launch_epochs(ds, ds.adv, ds.ret, ds.values, self.params, self.opt, self.cfg,
-                              self.rng)
+                              self.rng, prev=self._prev if chain else None)
+        h = PendingUpdate(plan, self.opt)
+        if chain:
+            _lib.call("ul_ppo_plan_collect", plan.h, _dev.stream())
+            plan.pending = h
+            _PENDING.append(h)
+            self._prev = plan
+        else:
+            self._prev = None
         self.free[k].record(cur)
         if next_segment is not None:
             self.prefetch(next_segment)  # overlaps the update just enqueued
-        return _stats(finish_plan(plan, self.opt), self.opt)
+        if not chain:
+            h._finish()
+        return h
 
 
 class SegmentStream:

@@ -46,6 +46,9 @@ struct PpoPlan {
   cudaStream_t cap_stream = nullptr;
   cudaStream_t side = nullptr;  // critic branch (fork/join inside each step)
   cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_fork = nullptr, ev_join = nullptr;
+  // ul_ppo_plan_collect: result records D2H'd behind the update, ev_res marks them
+  cudaEvent_t ev_res = nullptr;
+  bool collected = false;
   // the next minibatch's gather runs on the side stream under this step's
   // optimizer (and all-reduce) -- ev_gfork / ev_gjoin bracket it
   cudaEvent_t ev_gfork = nullptr, ev_gjoin = nullptr;
@@ -138,6 +141,7 @@ int alloc_plan(PpoPlan* p) {
   UL_CUDA(cudaHostAlloc(&p->st_h, sizeof(ul_ppo_stats), cudaHostAllocPortable));
   UL_CUDA(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_res, cudaEventDisableTiming));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
   UL_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking));
   UL_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
@@ -160,6 +164,7 @@ void free_plan(PpoPlan* p) {
   if (p->st_h) cudaFreeHost(p->st_h);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_res) cudaEventDestroy(p->ev_res);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   if (p->side) cudaStreamDestroy(p->side);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
@@ -253,13 +258,58 @@ int begin_device(PpoPlan* p, cudaStream_t s) {
   return launch_adv_stats(p->b.adv, p->rows, p->adv_part, p->tickets + 1, p->adv_stats, s);
 }
 
-int upload_ctl(PpoPlan* p, double lr_a, double lr_c, int64_t t_a, int64_t t_c, cudaStream_t s) {
+// The controller header travels as a kernel parameter, not a memcpy: an H2D
+// copy on the compute stream would queue on the copy engine behind the next
+// segment's ~190 MB of staging copies and hold the update back until they
+// drain.  src (may be dst itself, or null): an update chained behind another
+// one without a host round trip keeps that controller's Adam step counters
+// and divergence latch (read on the device, in stream order).
+struct CtlHeader {
+  uint32_t w[offsetof(ul_opt_ctl, part) / sizeof(uint32_t)];
+};
+
+__global__ void ctl_load_kernel(ul_opt_ctl* dst, const __grid_constant__ CtlHeader h,
+                                const ul_opt_ctl* src) {
+  int64_t t0 = 0, t1 = 0;
+  int32_t div = 0, fail = 0;
+  if (src) {
+    t0 = src->t[0];
+    t1 = src->t[1];
+    div = src->diverged;
+    fail = src->fail_step;
+  }
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  for (int i = 0; i < (int)(sizeof(h.w) / sizeof(uint32_t)); ++i) d[i] = h.w[i];
+  if (src) {
+    dst->t[0] = t0;
+    dst->t[1] = t1;
+    dst->diverged = div;
+    dst->fail_step = fail;
+  }
+}
+
+int load_ctl(PpoPlan* p, double lr_a, double lr_c, int64_t t_a, int64_t t_c, const PpoPlan* prev,
+             cudaStream_t s) {
+  // (built in a host-local record: p->ctl_h may still be receiving an earlier
+  // update's collected results)
   const double lr[2] = {lr_a, lr_c};
-  UL_TRY(ul_opt_ctl_init(p->ctl_h, 2, lr, 0.9, 0.999, 1e-8, p->d.max_grad_norm));
-  p->ctl_h->t[0] = t_a;
-  p->ctl_h->t[1] = t_c;
-  UL_CUDA(cudaMemcpyAsync(p->ctl_d, p->ctl_h, ctl_header_bytes(), cudaMemcpyHostToDevice, s));
-  return UL_OK;
+  static thread_local ul_opt_ctl c;
+  UL_TRY(ul_opt_ctl_init(&c, 2, lr, 0.9, 0.999, 1e-8, p->d.max_grad_norm));
+  c.t[0] = t_a;
+  c.t[1] = t_c;
+  CtlHeader h;
+  memcpy(&h, &c, sizeof(h));
+  ctl_load_kernel<<<1, 1, 0, s>>>(p->ctl_d, h, prev ? prev->ctl_d : nullptr);
+  return check_launch("ctl_load_kernel");
+}
+
+int upload_ctl(PpoPlan* p, double lr_a, double lr_c, int64_t t_a, int64_t t_c, cudaStream_t s) {
+  return load_ctl(p, lr_a, lr_c, t_a, t_c, nullptr, s);
+}
+
+int upload_ctl_chained(PpoPlan* p, const PpoPlan* prev, double lr_a, double lr_c,
+                       cudaStream_t s) {
+  return load_ctl(p, lr_a, lr_c, 0, 0, prev, s);
 }
 
 // K4: minibatch (e, k)'s rows of the 7 per-row arrays in one gather launch
@@ -651,6 +701,12 @@ extern "C" int ul_ppo_plan_reduce_buffer(void* plan, float** ptr, int64_t* n) {
   return UL_OK;
 }
 
+namespace ul {
+namespace {
+int run_graph(PpoPlan* p, cudaStream_t s);
+}  // namespace
+}  // namespace ul
+
 extern "C" int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
                                int64_t t_critic, int use_graph, void* stream) {
   PpoPlan* p = (PpoPlan*)plan;
@@ -658,6 +714,40 @@ extern "C" int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, in
   cudaStream_t s = ul::as_stream(stream);
   UL_TRY(ul::upload_ctl(p, lr_actor, lr_critic, t_actor, t_critic, s));
   if (!use_graph) return ul::all_steps(p, s);
+  return ul::run_graph(p, s);
+}
+
+// ul_ppo_plan_run (graph) chained behind `prev`'s update on the same stream:
+// the Adam step counters and the divergence latch continue from prev's
+// controller on the device, so the host may enqueue this update before it
+// has read prev's statistics.
+extern "C" int ul_ppo_plan_run_after(void* plan, const void* prev, double lr_actor,
+                                     double lr_critic, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  const PpoPlan* q = (const PpoPlan*)prev;
+  UL_CHECK_ARG(p && p->bound && q && q->ctl_d, "ppo plan: not bound / null previous plan");
+  cudaStream_t s = ul::as_stream(stream);
+  UL_TRY(ul::upload_ctl_chained(p, q, lr_actor, lr_critic, s));
+  return ul::run_graph(p, s);
+}
+
+// enqueue the D2H of the update's result records behind it (ev_res); the
+// next ul_ppo_plan_finish waits on that event instead of the whole stream,
+// so later updates may already be queued behind this one
+extern "C" int ul_ppo_plan_collect(void* plan, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "ppo plan: not bound");
+  cudaStream_t s = ul::as_stream(stream);
+  UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl_d, ul::ctl_header_bytes(), cudaMemcpyDeviceToHost, s));
+  UL_CUDA(cudaMemcpyAsync(p->st_h, p->st_d, sizeof(ul_ppo_stats), cudaMemcpyDeviceToHost, s));
+  UL_CUDA(cudaEventRecord(p->ev_res, s));
+  p->collected = true;
+  return UL_OK;
+}
+
+namespace ul {
+namespace {
+int run_graph(PpoPlan* p, cudaStream_t s) {
   // run on the plan's capture stream, ordered after / before the caller's stream
   UL_CUDA(cudaEventRecord(p->ev_in, s));
   UL_CUDA(cudaStreamWaitEvent(p->cap_stream, p->ev_in, 0));
@@ -688,6 +778,8 @@ extern "C" int ul_ppo_plan_run(void* plan, double lr_actor, double lr_critic, in
   UL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
   return UL_OK;
 }
+}  // namespace
+}  // namespace ul
 
 // One epoch of the update as its own CUDA graph (parity mode with host
 // permutations: the caller uploads epoch e's permutation, launches epoch e,
@@ -730,9 +822,14 @@ extern "C" int ul_ppo_plan_finish(void* plan, ul_ppo_result* out, void* stream) 
   PpoPlan* p = (PpoPlan*)plan;
   UL_CHECK_ARG(p && out, "ppo plan: null argument");
   cudaStream_t s = ul::as_stream(stream);
-  UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl_d, ul::ctl_header_bytes(), cudaMemcpyDeviceToHost, s));
-  UL_CUDA(cudaMemcpyAsync(p->st_h, p->st_d, sizeof(ul_ppo_stats), cudaMemcpyDeviceToHost, s));
-  UL_CUDA(cudaStreamSynchronize(s));
+  if (p->collected) {  // (ul_ppo_plan_collect) only this update's records
+    p->collected = false;
+    UL_CUDA(cudaEventSynchronize(p->ev_res));
+  } else {
+    UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl_d, ul::ctl_header_bytes(), cudaMemcpyDeviceToHost, s));
+    UL_CUDA(cudaMemcpyAsync(p->st_h, p->st_d, sizeof(ul_ppo_stats), cudaMemcpyDeviceToHost, s));
+    UL_CUDA(cudaStreamSynchronize(s));
+  }
   const double nb = (double)p->d.epochs * p->d.minibatches;
   const ul_ppo_stats& st = *p->st_h;
   out->policy_loss = nb > 0 ? st.policy_sum / nb : 0.0;

@@ -278,6 +278,92 @@ def test_pipeline_matches_serial_updates(prec):
         P.set_precision(old)
 
 
+def _pipe_setup(nseg, T=8, N=512):
+    segs = []
+    for sd in range(3, 3 + nseg):
+        segd, actor, critic = _synthetic(T, N, 48, 52, 12, (128, 64), seed=sd)
+        segs.append(A.RolloutSegment(**segd))
+    cfg = A.PpoConfig(epochs=2, minibatches=2)
+    arch_a, arch_c = TN.Arch(48, (128, 64), 12), TN.Arch(52, (128, 64), 1)
+
+    def fresh():
+        p = A.AcParams(TN.ModelParams.from_numpy(arch_a, actor.flat()),
+                       TN.ModelParams.from_numpy(arch_c, critic.flat()))
+        return p, A.AcOpt.for_params(p, cfg.lr)
+
+    return segs, cfg, fresh
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_pipeline_async_chained_matches_serial(prec):
+    """update_async: update i+1 enqueued (Adam step counters continued on the
+    device) before update i's statistics are read == serial updates, bit for
+    bit, and the host step counters end where the serial run's do."""
+    old = P.get_precision()
+    P.set_precision(prec)
+    try:
+        segs, cfg, fresh = _pipe_setup(4)
+        p1, o1 = fresh()
+        rng1 = A.DeviceRng(7)
+        serial = []
+        for sg in segs:
+            sg.advantages, sg.returns = A.gae(sg.rewards, sg.values, sg.terminated, sg.truncated,
+                                              sg.bootstrap_value, cfg.gamma, cfg.lam,
+                                              truncation_values=sg.truncation_values)
+            serial.append(A.ppo_update(sg, p1, o1, cfg, rng1))
+        p2, o2 = fresh()
+        pipe = A.PpoPipeline(p2, o2, cfg, A.DeviceRng(7))
+        pipe.prefetch(segs[0])
+        hs, piped = [], []
+        for i in range(len(segs)):
+            hs.append(pipe.update_async(next_segment=segs[i + 1] if i + 1 < len(segs) else None))
+            if i >= 1:
+                piped.append(hs[i - 1].result())
+        piped.append(hs[-1].result())
+        for a, b in zip(serial, piped):
+            assert a.policy_loss == b.policy_loss and a.value_loss == b.value_loss
+            assert a.grad_norm == b.grad_norm and a.kl == b.kl
+        np.testing.assert_array_equal(p1.actor.flat(), p2.actor.flat())
+        np.testing.assert_array_equal(p1.critic.flat(), p2.critic.flat())
+        assert (o2.actor.t, o2.critic.t) == (o1.actor.t, o1.critic.t)
+        # a plain update() after the chain starts from the device-chained state
+        pipe.prefetch(segs[0])
+        b = pipe.update()
+        a = A.ppo_update(segs[0], p1, o1, cfg, rng1)
+        assert a.policy_loss == b.policy_loss
+        np.testing.assert_array_equal(p1.actor.flat(), p2.actor.flat())
+    finally:
+        P.set_precision(old)
+
+
+def test_pipeline_async_divergence_latch_carries():
+    """A diverging update inside a chain: its result raises DivergenceError,
+    and the update already queued behind it inherits the latch on the device
+    (no step applied), so the parameters stay where the last good update
+    left them -- as after the serial reference's DivergenceError."""
+    segs, cfg, fresh = _pipe_setup(3, T=6, N=256)
+    segs[1].rewards[0, 0] = np.nan
+    p1, o1 = fresh()
+    sg = segs[0]
+    sg.advantages, sg.returns = A.gae(sg.rewards, sg.values, sg.terminated, sg.truncated,
+                                      sg.bootstrap_value, cfg.gamma, cfg.lam,
+                                      truncation_values=sg.truncation_values)
+    A.ppo_update(sg, p1, o1, cfg, A.DeviceRng(9))
+    p2, o2 = fresh()
+    pipe = A.PpoPipeline(p2, o2, cfg, A.DeviceRng(9))
+    pipe.prefetch(segs[0])
+    h0 = pipe.update_async(next_segment=segs[1])
+    h1 = pipe.update_async(next_segment=segs[2])
+    h2 = pipe.update_async()
+    h0.result()
+    with pytest.raises(TN.DivergenceError):
+        h1.result()
+    with pytest.raises(TN.DivergenceError):
+        h2.result()
+    np.testing.assert_array_equal(p1.actor.flat(), p2.actor.flat())
+    np.testing.assert_array_equal(p1.critic.flat(), p2.critic.flat())
+
+
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
 def test_ppo_data_parallel_two_ranks_match_single_process(prec):
     """SURVEY.md 8(e) for PPO: two ranks (threads on one GPU; the all-reduce a
