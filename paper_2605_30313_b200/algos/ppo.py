@@ -196,7 +196,8 @@ class PendingUpdate:
             self.plan.pending = None
 
     def result(self) -> UpdateStats:
-        _drain_pending(upto=self)
+        if not self.done:
+            _drain_pending(upto=self)
         if self._err is not None:
             raise self._err
         return self._stats
@@ -208,6 +209,9 @@ _PENDING: list = []  # enqueued, unread chained updates in launch order
 def _drain_pending(upto=None) -> None:
     """Read pending chained updates in launch order (through `upto`, else all),
     so the host copy of the Adam step counters is current again."""
+    if upto is not None and upto not in _PENDING:
+        upto._finish()  # (not queued: nothing older to read first)
+        return
     while _PENDING:
         h = _PENDING.pop(0)
         h._finish()

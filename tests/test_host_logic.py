@@ -179,3 +179,51 @@ def test_data_parallel_gradient_allreduce_gloo():
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
     assert result[0] < 1e-12 and result[1] < 1e-12
+
+
+def test_pending_updates_drain_in_launch_order(monkeypatch):
+    """update_async bookkeeping (no GPU): results are read in launch order,
+    reading a later handle first drains the earlier ones, a failing update's
+    error surfaces from its own result(), and the host step counters end at
+    the newest update's."""
+    from paper_2605_30313_b200.algos import ppo as P
+    from paper_2605_30313_b200.errors import DivergenceError
+
+    class Plan:
+        def __init__(self, name):
+            self.name, self.pending = name, None
+
+    class Opt:
+        class S:
+            t = 0
+        actor, critic, lr = S(), S(), 1e-3
+
+    seen = []
+
+    def fake_finish(plan, opt):
+        seen.append(plan.name)
+        opt.actor.t = opt.critic.t = len(seen) * 10
+        if plan.name == "c":
+            raise DivergenceError("non-finite at step 3")
+        return plan.name
+
+    monkeypatch.setattr(P, "finish_plan", fake_finish)
+    monkeypatch.setattr(P, "_stats", lambda res, opt: res)
+    monkeypatch.setattr(P, "_PENDING", [])
+    opt = Opt()
+    hs = []
+    for n in "abcd":
+        pl = Plan(n)
+        h = P.PendingUpdate(pl, opt)
+        pl.pending = h
+        P._PENDING.append(h)
+        hs.append(h)
+    assert hs[1].result() == "b" and seen == ["a", "b"]  # a drained first
+    assert hs[0].result() == "a" and seen == ["a", "b"]  # cached, not re-read
+    with pytest.raises(DivergenceError):
+        hs[2].result()
+    with pytest.raises(DivergenceError):  # the error stays with its handle
+        hs[2].result()
+    P._drain_pending()
+    assert seen == ["a", "b", "c", "d"] and hs[3].result() == "d"
+    assert opt.actor.t == 40 and all(h.plan.pending is None for h in hs)
