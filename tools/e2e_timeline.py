@@ -1,4 +1,4 @@
-"""Device timeline of the async e2e loop: per update, the copy-stream H2D
+"""Device timeline of the async e2e loop (PpoPipeline.update_async, cfg2): per update, the copy-stream H2D
 duration and the compute-stream span, and the gap between updates."""
 import sys
 from pathlib import Path
