@@ -11,15 +11,25 @@ GAE + ppo_update.
   value  device-resident: the segment is already in HBM; K x (GAE kernel +
          the update plan replayed as one CUDA graph), CUDA events, max over
          ranks.  Minibatch indices: device permutation ("performance mode").
-  e2e    through the public drop-in API (algos.gae + algos.ppo_update) from
-         pinned HOST buffers: every step H2D of the segment, the update, and
-         the D2H of UpdateStats.
+  e2e    through the public pipeline API (algos.PpoPipeline.update_async:
+         double-buffered pinned-host -> HBM staging ring, GAE on the device,
+         statistics read one update behind) from pinned HOST buffers: every
+         step H2D of the whole segment (~192 MB), the update, and the D2H of
+         the update's result record.  The serial reference-signature flow
+         (algos.gae + algos.ppo_update per step) is reported beside it.
+  tf32_arm  the same update with tf32 tensor-core GEMMs (same-width check
+         next to the bf16 headline).
 Multi-GPU (torchrun): one process per GPU, NCCL all-reduce of the gradient
-buffer every minibatch step; every rank owns its own 4096-env segment (weak
-scaling), so value = (N x 98,304 transitions) / max-over-ranks step time.
+buffer every minibatch step.  --scaling weak (default): every rank owns its
+own 4096-env segment, value = (N x 98,304 transitions) / max-over-ranks step
+time.  --scaling strong: one 4096-env segment replicated on every rank, each
+rank takes 1/N of every minibatch (value = 98,304 / step time).
 
-``--impl reference`` times the reference's CPU learner (the numpy oracle port
-of R:algos/estimators.py + R:algos/ppo.py, kind "port") on the host cores.
+``--impl reference`` times the reference's own CPU learner: the UNMODIFIED
+reference package installed into baseline/_ref (pip --target), called through
+its public API (unilite.algos.gae + unilite.algos.ppo_update, reference Philox
+update stream) on every host core, whole learner iterations (not
+extrapolated); the numpy oracle port is used only if baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -51,6 +61,9 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--precision", choices=("fp32", "tf32", "bf16"), default="bf16")
+    ap.add_argument("--ref-budget", type=float, default=60.0,
+                    help="seconds of timed reference updates (--impl reference)")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak")
     return ap.parse_args()
 
 
@@ -119,73 +132,154 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- CPU reference arm
-def _cpu_threads():
-    try:
-        from threadpoolctl import threadpool_limits
-
-        n = os.cpu_count() or 1
-        return threadpool_limits(limits=n), n
-    except Exception:
-        return None, 1
+REF_DIR = ROOT / "baseline" / "_ref"  # unmodified reference package (pip --target install)
 
 
-def cpu_reference_sample(seed: int = 0, epochs_sampled: int = 1):
-    """Time the reference CPU learner on a bounded cfg2 sample: GAE + the first
-    `epochs_sampled` of 5 epochs (4 minibatch steps each), extrapolated to the
-    full update.  Returns (transitions/s, update_ms, seconds spent)."""
-    from oracle import port as O
-    from paper_2605_30313_b200.workload import CONFIGS, make_rollout
+def _cpu_threads(n=None):
+    """Limit BLAS/OpenMP pools to n threads (default: every host core)."""
+    from threadpoolctl import threadpool_limits
 
-    T, N, od, cd, ad, hid = CONFIGS[CFG]
-    w = make_rollout(CFG, seed)
-    actor = O.net_init((od, *hid, ad), 0)
-    critic = O.net_init((cd, *hid, 1), 1)
-    flat = lambda a: a.reshape(-1, a.shape[-1])
-    mean, _ = O.mlp_forward(actor, flat(w.obs))
-    blogp = O.gauss_logp(mean, actor.log_std, flat(w.actions)).reshape(T, N).astype(np.float64)
-    vals = O.value_forward(critic, flat(w.critic_obs))[0].reshape(T, N).astype(np.float64)
-    cfg = O.PpoCfg(epochs=epochs_sampled)
-    oa, oc = O.Opt.for_net(actor, cfg.lr), O.Opt.for_net(critic, cfg.lr)
-    t0 = time.perf_counter()
-    adv, ret = O.gae(w.rewards, vals, w.terminated, w.truncated, w.bootstrap_value, 0.99, 0.95,
-                     w.truncation_values)
-    t1 = time.perf_counter()
-    seg = dict(obs=w.obs, critic_obs=w.critic_obs, actions=w.actions, behavior_log_prob=blogp,
-               rewards=w.rewards, terminated=w.terminated, truncated=w.truncated, values=vals,
-               bootstrap_value=w.bootstrap_value, advantages=adv, returns=ret)
-    O.ppo_update(seg, actor, critic, oa, oc, cfg, O.philox_stream(1, "update"))
-    t2 = time.perf_counter()
-    update_s = (t1 - t0) + (t2 - t1) * (5.0 / epochs_sampled)
-    return T * N / update_s, update_s * 1e3, t2 - t0
+    n = n or os.cpu_count() or 1
+    return threadpool_limits(limits=n), n
+
+
+def _reference_pkg():
+    """The unmodified reference (``unilite``) from baseline/_ref, or None."""
+    if not (REF_DIR / "unilite").is_dir():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import unilite  # noqa: F401
+    import unilite.algos
+    import unilite.envcore.rng
+    import unilite.tensornet
+
+    return unilite
+
+
+class RefLearner:
+    """The reference's own CPU learner step on the cfg2 workload, through its
+    public API: ``gae`` + ``ppo_update`` (R:runtime/ppo_runner.py:95-102) with
+    the reference update stream ``stream(1, "update")``.  Falls back to the
+    numpy oracle port (kind "port") only when baseline/_ref is absent."""
+
+    def __init__(self, seed: int = 0):
+        from paper_2605_30313_b200.workload import CONFIGS, make_rollout
+
+        T, N, od, cd, ad, hid = CONFIGS[CFG]
+        self.T, self.N = T, N
+        w = make_rollout(CFG, seed)
+        U = _reference_pkg()
+        self.kind = "reference" if U is not None else "port"
+        flat = lambda a: a.reshape(-1, a.shape[-1])
+        if U is not None:
+            TN, AL = U.tensornet, U.algos
+            actor = TN.init_params(TN.Arch(od, hid, ad), 0)
+            critic = TN.init_params(TN.Arch(cd, hid, 1), 1)
+            mean, _ = TN.forward(actor, flat(w.obs))
+            blogp = TN.gaussian_log_prob(mean, actor.log_std, flat(w.actions))
+            vals, _ = TN.value_forward(critic, flat(w.critic_obs))
+            self.seg = AL.RolloutSegment(
+                obs=w.obs, critic_obs=w.critic_obs, actions=w.actions,
+                behavior_log_prob=np.asarray(blogp, np.float64).reshape(T, N),
+                rewards=w.rewards, terminated=w.terminated, truncated=w.truncated,
+                values=np.asarray(vals, np.float64).reshape(T, N),
+                bootstrap_value=w.bootstrap_value, truncation_values=w.truncation_values)
+            self.params = AL.AcParams(actor, critic)
+            self.cfg = AL.PpoConfig()
+            self.opt = AL.AcOpt.for_params(self.params, self.cfg.lr)
+            self.rng = U.envcore.rng.stream(1, "update")
+            self.U = U
+        else:
+            from oracle import port as O
+
+            actor = O.net_init((od, *hid, ad), 0)
+            critic = O.net_init((cd, *hid, 1), 1)
+            mean, _ = O.mlp_forward(actor, flat(w.obs))
+            blogp = O.gauss_logp(mean, actor.log_std, flat(w.actions)).reshape(T, N)
+            vals = O.value_forward(critic, flat(w.critic_obs))[0].reshape(T, N)
+            self.seg = dict(obs=w.obs, critic_obs=w.critic_obs, actions=w.actions,
+                            behavior_log_prob=blogp.astype(np.float64), rewards=w.rewards,
+                            terminated=w.terminated, truncated=w.truncated,
+                            values=vals.astype(np.float64), bootstrap_value=w.bootstrap_value,
+                            truncation_values=w.truncation_values)
+            self.actor, self.critic = actor, critic
+            self.cfg = O.PpoCfg()
+            self.oa, self.oc = O.Opt.for_net(actor, self.cfg.lr), O.Opt.for_net(critic, self.cfg.lr)
+            self.rng = O.philox_stream(1, "update")
+            self.O = O
+
+    def step(self, epochs: int | None = None) -> float:
+        """One learner iteration (GAE + the full update, or its first
+        `epochs` epochs); returns seconds."""
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            AL = self.U.algos
+            s = self.seg
+            s.advantages, s.returns = AL.gae(s.rewards, s.values, s.terminated, s.truncated,
+                                             s.bootstrap_value, self.cfg.gamma, self.cfg.lam,
+                                             truncation_values=s.truncation_values)
+            cfg = self.cfg if epochs is None else AL.PpoConfig(epochs=epochs)
+            AL.ppo_update(s, self.params, self.opt, cfg, self.rng)
+        else:
+            O, s = self.O, self.seg
+            adv, ret = O.gae(s["rewards"], s["values"], s["terminated"], s["truncated"],
+                             s["bootstrap_value"], 0.99, 0.95, s["truncation_values"])
+            cfg = self.cfg if epochs is None else O.PpoCfg(epochs=epochs)
+            O.ppo_update(dict(s, advantages=adv, returns=ret), self.actor, self.critic, self.oa,
+                         self.oc, cfg, self.rng)
+        return time.perf_counter() - t0
+
+
+def cpu_reference_run(steps: int, warmup: int, budget_s: float, seed: int = 0):
+    """Whole reference learner iterations on every host core: `warmup`
+    untimed, then up to `steps` timed, stopping once `budget_s` seconds of
+    timed work have run (at least one).  Also a 1-thread reading on a
+    bounded sample (GAE + 1 of 5 epochs, x5).  Returns a dict."""
+    ref = RefLearner(seed)
+    lim, cores = _cpu_threads()
+    for _ in range(warmup):
+        ref.step()
+    times = []
+    while len(times) < steps:
+        times.append(ref.step())
+        if sum(times) >= budget_s:
+            break
+    lim1, _ = _cpu_threads(1)
+    one = ref.step(epochs=1)
+    _cpu_threads()
+    update_s = float(np.median(times))
+    return {"kind": ref.kind, "cores": cores, "steps_run": len(times), "update_ms": update_s * 1e3,
+            "value": ref.T * ref.N / update_s, "seconds": float(sum(times)),
+            "threads_1": {"update_ms_est": one * 5e3, "value": ref.T * ref.N / (one * 5),
+                          "sample": "GAE + 1 of 5 epochs at 1 BLAS thread, x5"}}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    lim, cores = _cpu_threads()
-    for _ in range(max(args.warmup, 0)):
-        cpu_reference_sample()
-    vals, ms = [], []
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, m, _ = cpu_reference_sample()
-        vals.append(v)
-        ms.append(m)
+    r = cpu_reference_run(args.steps, min(args.warmup, 1), budget_s=args.ref_budget)
     wall = time.perf_counter() - t0
-    value = float(np.median(vals))
-    sample = ("cfg2 GAE + 1 of 5 PPO epochs (4 minibatch steps of 24,576 rows), "
-              "extrapolated x5 to the full update; numpy/OpenBLAS oracle port")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": float(np.median(ms)), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+    src = ("unmodified reference package (baseline/_ref/unilite): unilite.algos.gae + "
+           "unilite.algos.ppo_update" if r["kind"] == "reference"
+           else "numpy oracle port of R:algos/estimators.py + R:algos/ppo.py")
+    sample = (f"{r['steps_run']} whole cfg2 learner iterations (GAE + ppo_update, 5 epochs x 4 "
+              f"minibatches of 24,576 rows), median; {src}; {r['cores']} BLAS threads")
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": r["steps_run"], "steps_requested": args.steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": r["update_ms"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 networks / f64 estimators+loss (reference numpy)", "data": "synthetic",
             "config": {"workload": "PPO update, cfg2 locomotion shape (4096 envs x 24, obs 235, "
                                    "act 12, 512-256-128, 5x4 minibatches)",
-                       "global_batch": 98304, "parallelism": "host CPU"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "global_batch": 98304, "parallelism": "host CPU",
+                       "indices": "reference Philox stream(1, 'update')"},
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                             "kind": r["kind"], "sample": sample,
+                             "threads_1": r["threads_1"]},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
@@ -222,7 +316,9 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-        _dist.set_segment_mode("local")
+        _dist.set_segment_mode("local" if args.scaling == "weak" else "replicated")
+    strong = args.scaling == "strong" and world > 1
+    seed_rank = 0 if strong else rank  # strong scaling: one replicated segment / stream
     T, N, od, cd, ad, hid = CONFIGS[CFG]
     cfg = A.PpoConfig()
 
@@ -231,7 +327,7 @@ def run_ours(args):
     critic = TN.init_params(TN.Arch(cd, hid, 1), 1)
     params = A.AcParams(actor, critic)
     opt = A.AcOpt.for_params(params, cfg.lr)
-    w = make_rollout(CFG, seed=rank, alloc=_dev.pinned_empty)
+    w = make_rollout(CFG, seed=seed_rank, alloc=_dev.pinned_empty)
     # behaviour log-prob and values at init, computed by our own kernels
     mean, _ = TN.forward(actor, w.obs.reshape(-1, od))
     blogp = TN.gaussian_log_prob(mean, actor.log_std, w.actions.reshape(-1, ad))
@@ -247,7 +343,7 @@ def run_ours(args):
 
     ds = staging_for(T, N, od, cd, ad, cfg.epochs)
     ds.load(seg, with_advantages=False)
-    rng = A.DeviceRng(seed=1000 + rank)
+    rng = A.DeviceRng(seed=1000 + seed_rank)
 
     def barrier():
         if world > 1:
@@ -276,13 +372,13 @@ def run_ours(args):
         torch.cuda.synchronize()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-    transitions = world * T * N
+    transitions = (1 if strong else world) * T * N
     value = transitions / (ms / 1e3)
 
     # ---- parity mode: the reference's own host Philox permutations
     from paper_2605_30313_b200.algos.ppo import fill_permutations  # noqa: F401
 
-    prng = np.random.Generator(np.random.Philox(key=1234 + rank))
+    prng = np.random.Generator(np.random.Philox(key=1234 + seed_rank))
     P.ppo_update_resident(ds, params, opt, cfg, prng)
     torch.cuda.synchronize()
     barrier()
@@ -292,6 +388,28 @@ def run_ours(args):
         P.ppo_update_resident(ds, params, opt, cfg, prng)
     torch.cuda.synchronize()
     par_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_par)
+
+    # ---- same-width arm: the identical update with tf32 tensor-core GEMMs
+    # (fp32 storage / activations), device permutations, CUDA events
+    tf32 = None
+    if prec != "tf32":
+        PKG.set_precision("tf32")
+        for _ in range(2):
+            P.ppo_update_resident(ds, params, opt, cfg, rng)
+        torch.cuda.synchronize()
+        barrier()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_tf = max(3, min(args.steps, 10))
+        t0e.record()
+        for _ in range(n_tf):
+            P.ppo_update_resident(ds, params, opt, cfg, rng)
+        t1e.record()
+        torch.cuda.synchronize()
+        tf_ms = max_over_ranks(t0e.elapsed_time(t1e)) / n_tf
+        tf32 = {"value": transitions / (tf_ms / 1e3), "unit": UNIT, "update_ms": tf_ms,
+                "steps": n_tf, "gemm_precision": "tcgen05 kind::tf32 (fp32 storage, activations "
+                "and accumulation)"}
+        PKG.set_precision(prec)
 
     # ---- e2e through the public API from pinned host buffers: the
     # double-buffered staging pipeline (segment i+1's H2D overlaps update i;
@@ -348,8 +466,8 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get("tc_gemm_dram_bytes_per_update")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": {"fp32": "f32", "tf32": "tf32 (f32 storage/accum)",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": {"fp32": "f32", "tf32": "tf32 (f32 storage/accum)",
                   "bf16": "bf16 GEMM operands/activations, f32 accum/params/optimizer"}[prec],
         "data": "synthetic",
         "config": {"workload": "PPO update (GAE + 5 epochs x 4 minibatches), cfg2 locomotion "
@@ -360,6 +478,7 @@ def run_ours(args):
                    "mode)", "inputs_larger_than_l2": True,
                    "segment_bytes_per_gpu": ds.h2d_bytes(seg), "gemm_precision": prec_name},
         "update_ms": ms,
+        "tf32_arm": tf32,
         "parity_mode": {"value": transitions / (par_ms / 1e3), "unit": UNIT, "update_ms": par_ms,
                         "indices": "host numpy Philox permutation per epoch (reference stream), "
                                    "drawn while the previous epoch runs (one CUDA graph per epoch)"},
@@ -383,12 +502,13 @@ def run_ours(args):
         "gpu_launches": int((counts["kernels_per_update"] + 1) * args.steps),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        lim, cores = _cpu_threads()
-        v, m, spent = cpu_reference_sample()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                "update_ms": m,
-                                "sample": "cfg2 GAE + 1 of 5 PPO epochs on the numpy oracle port, "
-                                          "extrapolated x5", "seconds": spent}
+        r = cpu_reference_run(2, 1, budget_s=20.0)
+        line["cpu_baseline"] = {
+            "value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+            "update_ms": r["update_ms"], "seconds": r["seconds"], "threads_1": r["threads_1"],
+            "sample": f"{r['steps_run']} whole cfg2 learner iterations (GAE + ppo_update) of the "
+                      + ("unmodified reference (baseline/_ref/unilite)" if r["kind"] == "reference"
+                         else "numpy oracle port") + f" on {r['cores']} BLAS threads, after 1 warm-up"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -190,6 +190,13 @@ int ul_gemm_tc(int layout, int epi, int64_t M, int64_t N, int64_t K, const void*
                const void* B, int64_t ldb, void* C, int64_t ldc, const float* bias,
                const void* aux, int64_t ldaux, int splits, int dtype, void* stream);
 
+/* Diagnostics (no reference counterpart): with UL_TC_TRACE=1 in the
+ * environment every tcgen05 GEMM launch records CTA 0's event timestamps and
+ * per-role wait-cycle sums; ul_tc_trace copies the kTraceSlots (160) u64
+ * slots to host_out, ul_tc_trace_reset zeroes them (tools/trace_gemm.py). */
+int ul_tc_trace(unsigned long long* host_out);
+int ul_tc_trace_reset(void);
+
 /* ------------------------------------------------- K4 / K5 / K6 data path */
 /* Gather rows of up to 12 arrays sharing one index vector (PPO minibatch
  * copies of R:algos/ppo.py:161-176; replay sample copy of

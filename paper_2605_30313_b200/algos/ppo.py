@@ -115,6 +115,17 @@ class _Plan:
 _PLANS: dict = {}
 
 
+def release_slots(prefix: str) -> None:
+    """Drop the staging segments and update plans of every slot whose name
+    starts with `prefix` (a PpoPipeline's own slots)."""
+    from . import _staging
+
+    for k in [k for k in _PLANS if str(k[-1]).startswith(prefix)]:
+        del _PLANS[k]
+    for k in [k for k in _staging._CACHE if str(k[0]).startswith(prefix)]:
+        del _staging._CACHE[k]
+
+
 def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
               raw_adv: bool = False) -> _Plan:
     # one plan (and CUDA graph) per staging slot: the pipeline alternates two
@@ -180,6 +191,7 @@ class PendingUpdate:
         self.plan, self.opt = plan, opt
         self._stats = None
         self._err = None
+        self.t_after = None  # (actor t, critic t) the device reported
 
     @property
     def done(self) -> bool:
@@ -192,6 +204,7 @@ class PendingUpdate:
             self._stats = _stats(finish_plan(self.plan, self.opt), self.opt)
         except Exception as e:  # (DivergenceError: raised by result())
             self._err = e
+        self.t_after = (self.opt.actor.t, self.opt.critic.t)
         if self.plan.pending is self:
             self.plan.pending = None
 
@@ -431,8 +444,13 @@ class PpoPipeline:
             stats = pipe.update(next_segment=seg_next_or_None)
     """
 
+    _ids = iter(range(1 << 62))
+
     def __init__(self, params: AcParams, opt: AcOpt, cfg: PpoConfig, rng):
         self.params, self.opt, self.cfg, self.rng = params, opt, cfg, rng
+        # staging slots (and the plans / CUDA graphs bound to them) are owned
+        # by this pipeline alone: two pipelines never share buffers
+        self._tag = f"pipe{next(PpoPipeline._ids)}"
         self.copy = torch.cuda.Stream()
         self.ready = [torch.cuda.Event(), torch.cuda.Event()]
         self.free = [torch.cuda.Event(), torch.cuda.Event()]
@@ -440,7 +458,35 @@ class PpoPipeline:
         self.queue: list = []  # slots holding staged, not yet consumed segments
         self.next_slot = 0
         self._prev = None  # plan of the last update (device-chained launches)
+        self._last = None  # PendingUpdate of the last chained update
 
+    def close(self) -> None:
+        """Release this pipeline's staging slots and plans."""
+        _drain_pending()
+        release_slots(self._tag)
+        self.slots = [None, None]
+        self.queue.clear()
+        self._prev = self._last = None
+
+    def __del__(self):
+        try:
+            release_slots(self._tag)
+        except Exception:
+            pass
+
+    def _chain_ok(self) -> bool:
+        """Chain the next update behind the last one on the device only while
+        the device-held Adam step counters / divergence latch are the truth:
+        not after an update that raised, nor when the host changed the step
+        counters since that update was read."""
+        h = self._last
+        if self._prev is None or h is None:
+            return False
+        if not h.done:
+            return True  # still in flight: the host holds no newer state
+        if h._err is not None:
+            return False
+        return (self.opt.actor.t, self.opt.critic.t) == h.t_after
     def prefetch(self, segment) -> None:
         """Start the H2D of a segment into the idle slot (returns at once when
         the host arrays are pinned)."""
@@ -452,7 +498,7 @@ class PpoPipeline:
             raise ValueError(f"minibatches {self.cfg.minibatches} must divide batch size {T * N}")
         k = self.next_slot
         self.next_slot ^= 1
-        ds = staging_for(T, N, od, cd, ad, self.cfg.epochs, slot=f"pipe{k}")
+        ds = staging_for(T, N, od, cd, ad, self.cfg.epochs, slot=f"{self._tag}_{k}")
         self.slots[k] = ds
         with torch.cuda.stream(self.copy):
             self.copy.wait_event(self.free[k])  # the update that last read this slot
@@ -473,7 +519,7 @@ class PpoPipeline:
             raise ValueError(f"minibatches {self.cfg.minibatches} must divide batch size {T * N}")
         k = self.next_slot
         self.next_slot ^= 1
-        ds = staging_for(T, N, od, cd, ad, self.cfg.epochs, slot=f"pipe{k}")
+        ds = staging_for(T, N, od, cd, ad, self.cfg.epochs, slot=f"{self._tag}_{k}")
         self.slots[k] = ds
         ds.has_tv = False
         self.copy.wait_event(self.free[k])
@@ -502,16 +548,17 @@ class PpoPipeline:
             self.prefetch(next_segment)  # host-driven DP steps: stage first
             next_segment = None
         chain = world == 1 and (self.rng is None or isinstance(self.rng, DeviceRng))
+        prev = self._prev if chain and self._chain_ok() else None
         plan = _launch_epochs(ds, ds.adv, ds.ret, ds.values, self.params, self.opt, self.cfg,
-                              self.rng, prev=self._prev if chain else None)
+                              self.rng, prev=prev)
         h = PendingUpdate(plan, self.opt)
         if chain:
             _lib.call("ul_ppo_plan_collect", plan.h, _dev.stream())
             plan.pending = h
             _PENDING.append(h)
-            self._prev = plan
+            self._prev, self._last = plan, h
         else:
-            self._prev = None
+            self._prev = self._last = None
         self.free[k].record(cur)
         if next_segment is not None:
             self.prefetch(next_segment)  # overlaps the update just enqueued

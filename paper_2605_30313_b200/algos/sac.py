@@ -313,7 +313,10 @@ def sac_update(batch, state: SacState, cfg: SacConfig, rng) -> UpdateStats:
     out = _lib.SacCtl()
     st = _lib.lib().ul_sac_plan_finish(plan.h, C.byref(out), ts, s)
     state.actor_opt.t, state.q1_opt.t, state.q2_opt.t = int(ts[0]), int(ts[1]), int(ts[2])
-    state.update_count += 1
+    if not (st != 0 and out.diverged == 1):
+        # the reference counts the update only once the critic step is finite
+        # (R:algos/sac.py:158-163); an actor-side divergence comes after it
+        state.update_count += 1
     if do_actor:
         p.log_alpha = float(out.log_alpha)
         state.alpha_opt.m, state.alpha_opt.v = float(out.a_m), float(out.a_v)

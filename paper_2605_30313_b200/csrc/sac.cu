@@ -673,16 +673,22 @@ extern "C" int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, void
   cudaStream_t s = ul::as_stream(stream);
   UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl, sizeof(ul_sac_ctl), cudaMemcpyDeviceToHost, s));
   ul_opt_ctl* srcs[3] = {p->oc_a, p->oc_q1, p->oc_q2};
-  int bad = 0;
+  int bad[3] = {0, 0, 0};
   for (int k = 0; k < 3; ++k) {
     UL_CUDA(cudaMemcpyAsync(p->oc_h, srcs[k], ul::ctl_hdr(), cudaMemcpyDeviceToHost, s));
     UL_CUDA(cudaStreamSynchronize(s));
     ts[k] = p->oc_h->t[0];
-    bad |= p->oc_h->diverged;
+    bad[k] = p->oc_h->diverged;
   }
   *out = *p->ctl_h;
-  if (bad || out->diverged || !isfinite(out->critic_loss)) {
-    ul::set_error("non-finite SAC loss or gradients");
+  // out->diverged: 1 = critic side (the reference raises before counting the
+  // update), 2 = actor / alpha side (raised after the count)
+  const bool critic_bad = bad[1] || bad[2] || !isfinite(out->critic_loss);
+  const bool actor_bad = bad[0] || out->diverged;
+  out->diverged = critic_bad ? 1 : (actor_bad ? 2 : 0);
+  if (critic_bad || actor_bad) {
+    ul::set_error(critic_bad ? "non-finite SAC critic loss or gradients"
+                             : "non-finite SAC actor / alpha loss or gradients");
     return UL_ERR_DIVERGENCE;
   }
   return UL_OK;

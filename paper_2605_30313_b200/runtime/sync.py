@@ -81,10 +81,13 @@ class _PinnedPool:
 
 
 def _snapshot(params, pool: _PinnedPool, version: int, stream: int,
-              wait: bool = True) -> HostParams:
+              wait: bool = True, src=None) -> HostParams:
+    """D2H of params (or of `src`, a device copy of them) into a pooled
+    pinned buffer on `stream`; frozen numpy views."""
     n = params.buf.numel()
     buf = pool.take(n)
-    _lib.call("ul_memcpy_async", buf.ctypes.data, _dev.ptr(params.buf), n * 4, stream)
+    dsrc = params.buf if src is None else src
+    _lib.call("ul_memcpy_async", buf.ctypes.data, _dev.ptr(dsrc), n * 4, stream)
     if wait:
         _lib.call("ul_stream_sync", stream)
     view = buf[:]
@@ -96,6 +99,41 @@ def _snapshot(params, pool: _PinnedPool, version: int, stream: int,
         b.setflags(write=False)
     snap.log_std.setflags(write=False)
     return snap
+
+
+class _DeviceShadow:
+    """Two HBM copies per published network: publish() snapshots the live
+    parameters with a D2D copy ON THE LEARNER STREAM (so the next in-place
+    update cannot race the snapshot -- the reference's "never a mix"
+    guarantee, R:runtime/sync.py:40-54) and the slow PCIe D2H then reads the
+    shadow on the copy stream.  A shadow is reused only after the D2H out of
+    it has completed (the learner stream waits on that event)."""
+
+    def __init__(self):
+        self._bufs: dict = {}
+        self._k = 0
+
+    def stage(self, key, params, cur_stream):
+        import torch
+
+        slot = self._bufs.setdefault(key, [[None, None], [None, None]])
+        k = self._k
+        buf, ev = slot[k]
+        n = params.buf.numel()
+        if buf is None or buf.numel() != n:
+            buf = torch.empty(n, dtype=torch.float32, device=params.buf.device)
+        if ev is not None:
+            cur_stream.wait_event(ev)  # the D2H that last read this shadow
+        _lib.call("ul_memcpy_async", _dev.ptr(buf), _dev.ptr(params.buf), n * 4,
+                  cur_stream.cuda_stream)
+        slot[k] = [buf, None]
+        return buf
+
+    def mark(self, key, ev) -> None:
+        self._bufs[key][self._k][1] = ev
+
+    def flip(self) -> None:
+        self._k ^= 1
 
 
 class WeightSlot:
@@ -115,6 +153,7 @@ class WeightSlot:
         self._pending = None  # (version, snapshot, event)
         self._pool = _PinnedPool()
         self._copy = None
+        self._shadow = _DeviceShadow()
         self._blocking = blocking
         self.publish_timestamp = 0
 
@@ -144,22 +183,30 @@ class WeightSlot:
                     s = _dev.stream()
                     ev = None
                 else:
+                    cur = torch.cuda.current_stream()
                     cs = self._copy_stream()
-                    cs.wait_stream(torch.cuda.current_stream())
                     s = cs.cuda_stream
                     ev = torch.cuda.Event()
                 wait = self._blocking
-                if hasattr(params, "actor") and hasattr(params, "critic") \
-                        and not hasattr(params, "q1"):
-                    snap = HostAcParams(_snapshot(params.actor, self._pool, version, s, wait),
-                                        _snapshot(params.critic, self._pool, version, s, wait))
-                else:
-                    snap = _snapshot(params, self._pool, version, s, wait)
+                nets = (("actor", params.actor), ("critic", params.critic)) if (
+                    hasattr(params, "actor") and hasattr(params, "critic")
+                    and not hasattr(params, "q1")) else (("net", params),)
+                shadows = {}
+                if ev is not None:
+                    for key, p in nets:
+                        shadows[key] = self._shadow.stage(key, p, cur)
+                    cs.wait_stream(cur)  # after the D2D snapshot, not after later updates
+                snaps = [_snapshot(p, self._pool, version, s, wait, shadows.get(key))
+                         for key, p in nets]
+                snap = HostAcParams(*snaps) if len(snaps) == 2 else snaps[0]
                 if ev is None:
                     self._pair = (version, snap)
                     self._pending = None
                 else:
                     ev.record(self._copy)
+                    for key, _ in nets:
+                        self._shadow.mark(key, ev)
+                    self._shadow.flip()
                     self._pending = (version, snap, ev)
                 self.publish_timestamp = now_ns()
             args["version"] = version

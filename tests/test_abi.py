@@ -35,6 +35,18 @@ def test_library_exports_every_declared_symbol():
     assert lib.ul_version() == 1
 
 
+def test_header_declares_every_exported_symbol():
+    """The header is the complete ABI: nothing is exported undeclared."""
+    import subprocess
+
+    so = ROOT / "paper_2605_30313_b200" / "libunilite_b200.so"
+    out = subprocess.run(["nm", "-D", "--defined-only", str(so)], capture_output=True,
+                         text=True).stdout
+    exported = {l.split()[-1] for l in out.splitlines() if l.strip()}
+    undeclared = sorted(exported - set(declared_symbols()))
+    assert not undeclared, f"exported but not declared in the header: {undeclared}"
+
+
 def test_only_abi_symbols_exported():
     import subprocess
 
