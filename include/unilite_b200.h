@@ -360,7 +360,8 @@ int ul_ppo_plan_profile(void* plan, double lr_actor, double lr_critic, int64_t t
 typedef struct ul_sac_ctl {
   double log_alpha, a_m, a_v, a_t, alpha_lr;
   double critic_loss, actor_loss, alpha_loss, logp_sum;
-  int32_t diverged, pad0;
+  int32_t diverged;      /* 0 ok, 1 critic side, 2 actor / alpha side (first failure) */
+  int32_t fail_update;   /* index of the first diverged update of a run, -1 none  */
 } ul_sac_ctl;
 
 typedef struct ul_sac_plan_desc {
@@ -385,6 +386,47 @@ typedef struct ul_sac_bindings {
   float *critic_red, *actor_red;
 } ul_sac_bindings;
 
+/* ------------------------------------------- per-call SAC / Gaussian API */
+/* Kernels behind the reference's per-call functions (the fused update is the
+ * plan below).  Reductions write per-block partials into `work`
+ * (ul_api_work_doubles() doubles, zeroed once by the caller; its last slot
+ * is the replay-safe last-block ticket). */
+int64_t ul_api_work_doubles(void);
+/* gaussian_dist / squashed_log_prob (R:tensornet/distributions.py:29-70),
+ * float64.  mode 0: plain sample (x = eps), 1: plain evaluation (x = action),
+ * 2: squashed sample (x = eps), 3: squashed evaluation (x = action, clipped
+ * to +-(1 - 1e-6), u = atanh), 4: squashed log-prob of given (u = x, a = a_in).
+ * sample / u_out [n, A] (may be NULL), logp [n]. */
+int ul_gaussian_dist(const double* mean, int64_t ldm, const double* log_std, const double* x,
+                     int64_t ldx, const double* a_in, int64_t n, int A, int mode, double* sample,
+                     double* u_out, double* logp, void* stream);
+/* sample_squashed (R:tensornet/distributions.py:73-84) in float32 arithmetic:
+ * u = mean + exp(log_std) eps, a = tanh(u), logp [n] */
+int ul_sample_squashed(const float* mean, int64_t ldm, const float* log_std, const float* eps,
+                       int64_t lde, int64_t n, int A, float* a, float* u, float* logp,
+                       void* stream);
+/* critic_target's y = r + gamma^n_used (1 - term)(min(q1t, q2t) - alpha logp)
+ * (R:algos/sac.py:111-125), float64 */
+int ul_sac_soft_target(const double* r, const double* term, const double* nused,
+                       const float* q1t, const float* q2t, const float* logp, double log_alpha,
+                       double gamma, int64_t n, double* y, void* stream);
+/* critic_loss_and_grads head (R:algos/sac.py:128-136): *loss = mean((q-y)^2),
+ * dq = 2 (q - y) / n cast to float32 (device scalar / vector) */
+int ul_sac_mse_head(const float* q, const double* y, int64_t n, float* dq, double* loss,
+                    double* work, void* stream);
+/* actor_loss_and_grads pick (R:algos/sac.py:194-205): *loss = mean(alpha
+ * logp - min(q1, q2)), d1 = [q1 <= q2], d2 = 1 - d1 */
+int ul_sac_pick_head(const float* q1, const float* q2, const float* logp, int64_t n,
+                     double log_alpha, float* d1, float* d2, double* loss, double* work,
+                     void* stream);
+/* actor gradient head (R:algos/sac.py:207-217): dQ/da = dq1 + dq2 (rows of
+ * ldq, the action columns); dmean [n, A]; dlog_std [A] is ADDED to */
+int ul_sac_actor_head(const float* a, const float* eps, const float* dq1, const float* dq2,
+                      int64_t ldq, const float* log_std, int64_t n, int A, double log_alpha,
+                      float* dmean, float* dlog_std, double* work, void* stream);
+/* *out = sum_i (x[i] + shift), float64 (alpha_loss_and_grad's mean) */
+int ul_sum_f64(const float* x, int64_t n, double shift, double* out, double* work, void* stream);
+
 /* sac_update (R:algos/sac.py:139-178) as a native plan.  Batches come as
  * codec rows (R:replaypath/storage.py:17-46) gathered from a device replay
  * ring or a staged batch. */
@@ -394,13 +436,24 @@ int ul_sac_plan_bind(void* plan, const ul_sac_bindings* b);
 /* rows[(idx[i] % modulo)] (pitch in floats); idx NULL = rows 0..B-1 */
 int ul_sac_plan_load_rows(void* plan, const float* rows, int64_t pitch, const int64_t* idx,
                           int64_t modulo, int64_t lo, int64_t hi, int* err, void* stream);
-/* upload alpha state + per-network (lr, t): order actor, q1, q2 */
+/* upload alpha state + per-network (lr, t): order actor, q1, q2 (async, no
+ * host sync: pinned staging per record) */
 int ul_sac_plan_begin(void* plan, const ul_sac_ctl* host_ctl, const double* lrs,
                       const int64_t* ts, void* stream);
-/* noise: [2, B, A] float32 (eps for the target, eps for the actor step);
- * either fill it from the host (parity mode) or on the device */
+/* room for runs of up to n updates: noise [n][2][B][A] float32 (per update:
+ * eps of the target, eps of the actor step) and per-update statistics */
+int ul_sac_plan_reserve(void* plan, int n_updates);
+/* noise buffer (reserved updates x [2, B, A]); fill it from the host (parity
+ * mode: the reference draw order) or on the device */
 int ul_sac_plan_noise_ptr(void* plan, float** eps);
 int ul_sac_plan_device_noise(void* plan, uint64_t key, uint64_t counter, void* stream);
+/* n consecutive sac_update calls on the loaded batch (FlashSAC's
+ * updates_per_step loop, R:runtime/sac_runner.py:313-321) as ONE CUDA graph
+ * launch: update u takes the actor / alpha step when (update_count0 + u + 1)
+ * % policy_frequency == 0.  Everything stays on the device between updates;
+ * the first divergence latches every later step off (the reference raises). */
+int ul_sac_plan_run(void* plan, int n_updates, int64_t update_count0, int policy_frequency,
+                    void* stream);
 int ul_sac_plan_update(void* plan, int do_actor, void* stream);
 /* The same update split at its two data-parallel exchange points (SURVEY
  * 8(e)): critic_grads -> all-reduce(critic buffer) -> critic_apply ->
@@ -413,8 +466,11 @@ int ul_sac_plan_critic_apply(void* plan, void* stream);
 int ul_sac_plan_actor_grads(void* plan, void* stream);
 int ul_sac_plan_actor_apply(void* plan, void* stream);
 int ul_sac_plan_polyak(void* plan, void* stream);
-/* D2H of the control records (+ sync): ts = step counters (actor, q1, q2) */
-int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, void* stream);
+/* D2H of the control records (+ one sync): ts = step counters (actor, q1,
+ * q2); stats (may be NULL): n x [critic_loss, actor_loss, alpha_loss, alpha]
+ * of the last run (NaN where an update took no actor step) */
+int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, double* stats, int n,
+                       void* stream);
 
 #ifdef __cplusplus
 }

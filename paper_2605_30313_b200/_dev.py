@@ -131,3 +131,32 @@ def to_numpy(t) -> np.ndarray:
     if isinstance(t, torch.Tensor):
         return t.detach().cpu().numpy()
     return np.asarray(t)
+
+
+def to_device_f64(x) -> torch.Tensor:
+    """numpy / torch -> contiguous CUDA float64 (host-side dtype cast for the
+    transfer only; the arithmetic runs in the kernels)."""
+    dev = require_cuda()
+    if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 \
+            and x.is_contiguous():
+        return x
+    arr = x.detach().cpu().numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    out = torch.empty(arr.shape, dtype=torch.float64, device=dev)
+    if arr.size:
+        h2d(out, arr)
+    return out
+
+
+_API_WORK: dict = {}
+
+
+def api_work() -> torch.Tensor:
+    """Per-device workspace of the per-call reduction kernels (zeroed once:
+    its last slot is the self-resetting last-block ticket)."""
+    dev = require_cuda()
+    w = _API_WORK.get(dev.index)
+    if w is None:
+        w = torch.zeros(int(_lib.lib().ul_api_work_doubles()), dtype=torch.float64, device=dev)
+        _API_WORK[dev.index] = w
+    return w

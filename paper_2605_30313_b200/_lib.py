@@ -85,7 +85,7 @@ class PpoBindings(C.Structure):
 class SacCtl(C.Structure):
     _fields_ = [(n, f64) for n in ("log_alpha", "a_m", "a_v", "a_t", "alpha_lr", "critic_loss",
                                    "actor_loss", "alpha_loss", "logp_sum")] + \
-               [("diverged", i32), ("pad0", i32)]
+               [("diverged", i32), ("fail_update", i32)]
 
 
 class SacPlanDesc(C.Structure):
@@ -162,6 +162,16 @@ _PROTOS = {
     "ul_norm_update": (C.c_int, [vp, i64, i64, i64, vp, vp, C.c_int, vp]),
     "ul_norm_apply": (C.c_int, [vp, i64, i64, i64, vp, vp, i64, vp]),
     "ul_gaussian_logp": (C.c_int, [vp, i64, vp, vp, i64, i64, C.c_int, vp, vp]),
+    "ul_api_work_doubles": (i64, []),
+    "ul_gaussian_dist": (C.c_int, [vp, i64, vp, vp, i64, vp, i64, C.c_int, C.c_int, vp, vp, vp,
+                                   vp]),
+    "ul_sample_squashed": (C.c_int, [vp, i64, vp, vp, i64, i64, C.c_int, vp, vp, vp, vp]),
+    "ul_sac_soft_target": (C.c_int, [vp, vp, vp, vp, vp, vp, f64, f64, i64, vp, vp]),
+    "ul_sac_mse_head": (C.c_int, [vp, vp, i64, vp, vp, vp, vp]),
+    "ul_sac_pick_head": (C.c_int, [vp, vp, vp, i64, f64, vp, vp, vp, vp, vp]),
+    "ul_sac_actor_head": (C.c_int, [vp, vp, vp, vp, i64, vp, i64, C.c_int, f64, vp, vp, vp,
+                                    vp]),
+    "ul_sum_f64": (C.c_int, [vp, i64, f64, vp, vp, vp]),
     "ul_ppo_plan_create": (C.c_int, [C.POINTER(PpoPlanDesc), C.POINTER(vp)]),
     "ul_ppo_plan_destroy": (C.c_int, [vp]),
     "ul_ppo_plan_bind": (C.c_int, [vp, C.POINTER(PpoBindings)]),
@@ -180,6 +190,8 @@ _PROTOS = {
     "ul_sac_plan_load_rows": (C.c_int, [vp, vp, i64, vp, i64, i64, i64, vp, vp]),
     "ul_sac_plan_begin": (C.c_int, [vp, C.POINTER(SacCtl), C.POINTER(f64), C.POINTER(i64), vp]),
     "ul_sac_plan_noise_ptr": (C.c_int, [vp, C.POINTER(vp)]),
+    "ul_sac_plan_reserve": (C.c_int, [vp, C.c_int]),
+    "ul_sac_plan_run": (C.c_int, [vp, C.c_int, i64, C.c_int, vp]),
     "ul_sac_plan_device_noise": (C.c_int, [vp, C.c_uint64, C.c_uint64, vp]),
     "ul_sac_plan_update": (C.c_int, [vp, C.c_int, vp]),
     "ul_sac_plan_reduce_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64), C.POINTER(vp),
@@ -189,7 +201,7 @@ _PROTOS = {
     "ul_sac_plan_actor_grads": (C.c_int, [vp, vp]),
     "ul_sac_plan_actor_apply": (C.c_int, [vp, vp]),
     "ul_sac_plan_polyak": (C.c_int, [vp, vp]),
-    "ul_sac_plan_finish": (C.c_int, [vp, C.POINTER(SacCtl), C.POINTER(i64), vp]),
+    "ul_sac_plan_finish": (C.c_int, [vp, C.POINTER(SacCtl), C.POINTER(i64), vp, C.c_int, vp]),
     "ul_ppo_plan_counts": (C.c_int, [vp, C.POINTER(i64), C.POINTER(f64)]),
     "ul_ppo_plan_profile": (C.c_int, [vp, f64, f64, i64, i64, C.POINTER(f64), vp]),
 }

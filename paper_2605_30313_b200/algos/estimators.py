@@ -1,16 +1,14 @@
-"""GAE / V-trace on the device + the host collector-side packers
+"""GAE / V-trace and the FlashSAC collector transforms on the device
 (mirror of R:algos/estimators.py).
 
 ``gae`` and ``vtrace`` keep the reference signatures and return device
 float32 [T, N] tensors computed by ul_gae_f32 / ul_vtrace_f32 (float64
-arithmetic inside the kernel).  ``ReturnStdNormalizer`` and ``NStepPacker``
-run on the collector thread in the reference (R:runtime/sac_runner.py:220-247)
-and stay host code here.
+arithmetic inside the kernel).  ``ReturnStdNormalizer`` / ``NStepPacker`` /
+``nstep_and_reward_norm`` keep the reference API over the n-step kernels of
+csrc/nstep.cu.
 """
 
 from __future__ import annotations
-
-from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -77,72 +75,112 @@ def vtrace(behavior_log_prob, target_log_prob, rewards, values, terminated, boot
     return vs, pg
 
 
-# ------------------------------------------------------- host collector side
-@dataclass
+# ------------------------------------------- collector-side transforms
+# R:algos/estimators.py:125-224 run per env in Python on the reference's
+# collector thread.  Here the same objects drive the device kernels of
+# csrc/nstep.cu (replaypath.DeviceNStepReplay): the pending n-step windows,
+# the discounted-return statistics and the packing live in HBM; push()
+# returns the emitted transitions as the reference's tuples (one D2H of the
+# emitted rows) so a host collector can keep its code unchanged -- or use
+# DeviceNStepReplay directly and never bring the rows back.
 class ReturnStdNormalizer:
     """Running std of per-env discounted returns (R:algos/estimators.py:125-163).
-    Host-side: it runs on the collector thread before replay insertion."""
+    The statistics live on the device; they are bound into an NStepPacker by
+    ``nstep_and_reward_norm`` (fused normalise + pack), or driven alone by
+    ``normalize`` (a 1-step packer over the rewards)."""
 
-    gamma: float
-    g_max: float
-    n_envs: int
-    eps: float = 1e-8
-    returns: np.ndarray = None
-    count: float = 0.0
-    mean: float = 0.0
-    m2: float = 0.0
+    def __init__(self, gamma: float, g_max: float, n_envs: int, eps: float = 1e-8):
+        self.gamma, self.g_max, self.n_envs, self.eps = float(gamma), float(g_max), int(n_envs), eps
+        self._engine = None  # the DeviceNStepReplay holding the statistics
 
-    def __post_init__(self) -> None:
-        if self.returns is None:
-            self.returns = np.zeros(self.n_envs, dtype=np.float64)
+    def _stats(self):
+        if self._engine is None:
+            return (0.0, 0.0, 0.0, 1.0)
+        return self._engine.norm_stats()
+
+    @property
+    def count(self) -> float:
+        return self._stats()[0]
+
+    @property
+    def mean(self) -> float:
+        return self._stats()[1]
+
+    @property
+    def m2(self) -> float:
+        return self._stats()[2]
 
     @property
     def std(self) -> float:
-        return 1.0 if self.count < 2 else float(np.sqrt(self.m2 / self.count))
+        return self._stats()[3]
 
     def normalize(self, rewards, done):
-        rewards = np.asarray(rewards, dtype=np.float64)
-        self.returns = self.returns * self.gamma * (~np.asarray(done, bool)) + rewards
-        # sequential Welford over the envs, same order as the reference loop
-        for g in self.returns:
-            self.count += 1
-            d = g - self.mean
-            self.mean += d / self.count
-            self.m2 += d * (g - self.mean)
-        bound = (1.0 - self.gamma) * self.g_max
-        return np.clip(rewards / (self.std + self.eps), -bound, bound)
+        """Update the return statistics with this step and return the clipped
+        normalised rewards (R:algos/estimators.py:153-163)."""
+        from ..replaypath.device_insert import DeviceNStepReplay
+
+        if self._engine is None:
+            self._engine = DeviceNStepReplay(1, self.gamma, self.n_envs, 1, 1,
+                                             capacity=self.n_envs, norm_gamma=self.gamma,
+                                             g_max=self.g_max, eps=self.eps)
+        elif self._engine.n != 1:
+            raise RuntimeError("normaliser is bound to an NStepPacker; use nstep_and_reward_norm")
+        z = np.zeros((self.n_envs, 1), np.float32)
+        done = np.asarray(done, bool)
+        eng = self._engine
+        h0 = eng.head
+        eng.push(z, z, np.asarray(rewards, np.float64), z, done, np.zeros_like(done))
+        rows = eng.rows(h0, eng.head)
+        return rows[:, 2].astype(np.float64)  # RowCodec(1, 1): obs | act | reward | ...
 
 
 class NStepPacker:
-    """Per-env n-step packing (R:algos/estimators.py:166-207); host-side."""
+    """Per-env n-step packing (R:algos/estimators.py:166-207) on the device."""
 
     def __init__(self, n: int, gamma: float, n_envs: int):
         if n < 1:
             raise ValueError("n must be >= 1")
-        self.n, self.gamma = n, gamma
-        self._pending = [[] for _ in range(n_envs)]
+        self.n, self.gamma, self.n_envs = int(n), float(gamma), int(n_envs)
+        self._engine = None
+        self._norm = None
 
-    def push(self, obs, actions, rewards, next_obs, terminated, truncated):
-        out = []
-        done = np.asarray(terminated, bool) | np.asarray(truncated, bool)
-        for e, pend in enumerate(self._pending):
-            for item in pend:
-                item[2] += (self.gamma ** item[3]) * rewards[e]
-                item[3] += 1
-            pend.append([obs[e].copy(), actions[e].copy(), float(rewards[e]), 1])
-            if done[e]:
-                out.extend((it[0], it[1], it[2], next_obs[e].copy(), bool(terminated[e]), it[3])
-                           for it in pend)
-                pend.clear()
-            elif pend[0][3] == self.n:
-                it = pend.pop(0)
-                out.append((it[0], it[1], it[2], next_obs[e].copy(), False, self.n))
-        return out
+    def _bind(self, obs_dim: int, act_dim: int, norm=None):
+        from ..replaypath.device_insert import DeviceNStepReplay
+
+        if self._engine is None:
+            if norm is not None and norm._engine is not None:
+                raise RuntimeError("normaliser already driven on its own")
+            self._engine = DeviceNStepReplay(
+                self.n, self.gamma, self.n_envs, obs_dim, act_dim,
+                capacity=self.n_envs * (self.n + 1),
+                norm_gamma=norm.gamma if norm is not None else None,
+                g_max=norm.g_max if norm is not None else 10.0,
+                eps=norm.eps if norm is not None else 1e-8)
+            self._norm = norm
+            if norm is not None:
+                norm._engine = self._engine
+        elif norm is not self._norm:
+            raise RuntimeError("an NStepPacker is bound to one normaliser (or none)")
+        return self._engine
+
+    def push(self, obs, actions, rewards, next_obs, terminated, truncated, _norm=None):
+        """One env step; returns the emitted (obs, action, reward, next_obs,
+        terminated, n_used) tuples in the reference's env-major order."""
+        obs = np.asarray(_dev.to_numpy(obs), np.float32)
+        actions = np.asarray(_dev.to_numpy(actions), np.float32)
+        eng = self._bind(obs.shape[1], actions.shape[1], _norm)
+        h0 = eng.head
+        eng.push(obs, actions, np.asarray(_dev.to_numpy(rewards), np.float64), next_obs,
+                 terminated, truncated)
+        if eng.head == h0:
+            return []
+        rows = eng.rows(h0, eng.head)
+        d, a = eng.obs_dim, eng.act_dim
+        return [(r[:d].copy(), r[d:d + a].copy(), float(r[d + a]), r[d + a + 1:2 * d + a + 1].copy(),
+                 bool(r[2 * d + a + 1] > 0.5), int(r[2 * d + a + 2])) for r in rows]
 
 
 def nstep_and_reward_norm(packer, norm, obs, actions, rewards, next_obs, terminated, truncated):
-    """R:algos/estimators.py:210-224."""
-    if norm is not None:
-        done = np.asarray(terminated, bool) | np.asarray(truncated, bool)
-        rewards = norm.normalize(rewards, done)
-    return packer.push(obs, actions, rewards, next_obs, terminated, truncated)
+    """Reward normalisation (optional) + n-step packing of one step
+    (R:algos/estimators.py:210-224), fused on the device."""
+    return packer.push(obs, actions, rewards, next_obs, terminated, truncated, _norm=norm)

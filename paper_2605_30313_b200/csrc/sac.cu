@@ -17,6 +17,8 @@
 // The replay batch arrives as codec rows (obs | action | r | next_obs | term |
 // n_used, R:replaypath/storage.py:17-46) gathered straight from the device
 // replay ring (K6) into the critic / actor / target input matrices.
+#include <cuda_bf16.h>
+
 #include <new>
 
 #include "learner.cuh"
@@ -25,15 +27,16 @@ namespace ul {
 namespace {
 
 constexpr double kLog2Pi = 1.8378770664093453;
-constexpr float kSquashEps = 1e-6f;
 
 // ---------------------------------------------------------------- kernels
 // a = tanh(mean + std*eps) (f32 like the reference), logp = Gaussian(u) -
 // sum log1p(-a^2 + 1e-6); a is written into dst[:, col0:col0+A] (a critic
-// input matrix) and, optionally, a_out (for the actor gradient).
+// input matrix, fp32 or bf16 rows) and, optionally, a_out (for the actor
+// gradient).
+template <typename T>
 __global__ void squash_kernel(const float* __restrict__ mean, int64_t ldm,
                               const float* __restrict__ log_std, const float* __restrict__ eps,
-                              int64_t lde, int64_t n, int A, float* __restrict__ dst, int64_t ldd,
+                              int64_t lde, int64_t n, int A, T* __restrict__ dst, int64_t ldd,
                               int col0, float* __restrict__ a_out, float* __restrict__ logp) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -47,10 +50,62 @@ __global__ void squash_kernel(const float* __restrict__ mean, int64_t ldm,
       const double z = ((double)u - (double)m) / (double)sd;
       lp += -(double)ls - 0.5 * kLog2Pi - 0.5 * z * z;
       lp -= log1p(-(double)a * (double)a + 1e-6);
-      dst[i * ldd + col0 + j] = a;
+      dst[i * ldd + col0 + j] = (T)a;
       if (a_out) a_out[i * A + j] = a;
     }
     logp[i] = (float)lp;
+  }
+}
+
+// Codec rows (obs | act | r | next_obs | term | n_used, R:replaypath/
+// storage.py:17-46) -> the plan's network inputs in their GEMM dtype:
+// qin = [obs | act | 1], obs = [obs | 1], qa = [obs | (a_pi)], qn =
+// [next_obs | (a')] and the fp32 scalars.  One warp per row, lanes across
+// the row (one coalesced read of its bytes); idx (may be NULL) addresses the
+// ring by absolute index (% modulo), rows outside [lo, hi) are skipped and
+// flag *err.
+template <typename T>
+__global__ void __launch_bounds__(256) sac_load_kernel(
+    const float* __restrict__ rows, int64_t pitch, const int64_t* __restrict__ idx,
+    int64_t modulo, int64_t lo, int64_t hi, int* err, int64_t B, int D, int A,
+    T* __restrict__ qin, int64_t ldq, T* __restrict__ obs, int64_t ldo, T* __restrict__ qa,
+    T* __restrict__ qn, float* __restrict__ rew, float* __restrict__ term,
+    float* __restrict__ nused) {
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const T one = (T)1.0f;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < B; r += warps) {
+    int64_t slot = r;
+    if (idx) {
+      const int64_t a = idx[r];
+      if (a < lo || a >= hi) {
+        if (lane == 0 && err) *err = 1;
+        continue;
+      }
+      slot = modulo > 0 ? a % modulo : a;
+    }
+    const float* src = rows + slot * pitch;
+    T* qi = qin + r * ldq;
+    T* ob = obs + r * ldo;
+    T* qar = qa + r * ldq;
+    T* qnr = qn + r * ldq;
+    for (int j = lane; j < D; j += 32) {
+      const T o = (T)src[j];
+      qi[j] = o;
+      ob[j] = o;
+      qar[j] = o;
+      qnr[j] = (T)src[D + A + 1 + j];
+    }
+    for (int j = lane; j < A; j += 32) qi[D + j] = (T)src[D + j];
+    if (lane == 0) {
+      qi[D + A] = one;
+      ob[D] = one;
+      rew[r] = src[D + A];
+      term[r] = src[2 * D + A + 1];
+      nused[r] = src[2 * D + A + 2];
+    }
   }
 }
 
@@ -76,7 +131,7 @@ __global__ void __launch_bounds__(256) critic_head_kernel(const float* __restric
                                                           double inv_n, float* __restrict__ dq1,
                                                           float* __restrict__ dq2, double* part,
                                                           unsigned int* ticket, ul_sac_ctl* ctl,
-                                                          float* loss_slot) {
+                                                          float* loss_slot, double* rec) {
   __shared__ double scratch[32];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double l1 = 0.0, l2 = 0.0;
@@ -103,6 +158,10 @@ __global__ void __launch_bounds__(256) critic_head_kernel(const float* __restric
     ctl->critic_loss = s1 * inv_n + s2 * inv_n;
     // data-parallel: this rank's share, all-reduced with the critic gradients
     if (loss_slot) loss_slot[0] = (float)ctl->critic_loss;
+    if (rec) {  // per-update statistics of a run: critic loss, alpha before
+      rec[0] = ctl->critic_loss;
+      rec[3] = exp(ctl->log_alpha);
+    }
   }
 }
 
@@ -113,7 +172,7 @@ __global__ void __launch_bounds__(256) pick_head_kernel(const float* __restrict_
                                                         double n_global, float* __restrict__ d1,
                                                         float* __restrict__ d2, double* part,
                                                         unsigned int* ticket, ul_sac_ctl* ctl,
-                                                        float* slots) {
+                                                        float* slots, double* rec) {
   __shared__ double scratch[32];
   const double alpha = exp(ctl->log_alpha);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,6 +200,7 @@ __global__ void __launch_bounds__(256) pick_head_kernel(const float* __restrict_
     }
     ctl->actor_loss = s1 / n_global;
     ctl->logp_sum = s2;
+    if (rec) rec[1] = ctl->actor_loss;
     if (slots) {  // data-parallel shares, all-reduced with the actor gradients
       slots[0] = (float)ctl->actor_loss;
       slots[1] = (float)s2;
@@ -193,15 +253,18 @@ __global__ void __launch_bounds__(256) actor_head_kernel(
   }
 }
 
-// ScalarAdam on log_alpha (R:algos/sac.py:35-53, :224-229, :245-249)
-__global__ void alpha_step_kernel(ul_sac_ctl* ctl, double n, double target_entropy) {
+// ScalarAdam on log_alpha (R:algos/sac.py:35-53, :224-229, :245-249); skipped
+// once any step of the run diverged (the reference raised before it)
+__global__ void alpha_step_kernel(ul_sac_ctl* ctl, const ul_opt_ctl* oc_a, double n,
+                                  double target_entropy, double* rec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (oc_a->diverged || ctl->diverged) return;
   const double excess = ctl->logp_sum / n + target_entropy;
   const double la = ctl->log_alpha;
   ctl->alpha_loss = -la * excess;
   const double g = -excess;
   if (!isfinite(g)) {
-    ctl->diverged = 1;
+    ctl->diverged = 2;
     return;
   }
   ctl->a_t += 1.0;
@@ -211,6 +274,66 @@ __global__ void alpha_step_kernel(ul_sac_ctl* ctl, double n, double target_entro
   const double mh = ctl->a_m / (1.0 - pow(b1, ctl->a_t));
   const double vh = ctl->a_v / (1.0 - pow(b2, ctl->a_t));
   ctl->log_alpha = la - ctl->alpha_lr * mh / (sqrt(vh) + 1e-8);
+  if (rec) {
+    rec[2] = ctl->alpha_loss;
+    rec[3] = exp(ctl->log_alpha);
+  }
+}
+
+// Divergence latch between the phases of a run.  side 1 (after the critic
+// Adam steps): a latched critic controller or a non-finite critic loss;
+// side 2 (after the actor step): the actor controller or alpha.  The first
+// failure is recorded (ctl->diverged = side, fail_update = u) and every
+// controller is latched so no later step of the run mutates anything
+// (R:algos/sac.py:158-163 / :238-241 raise at that point).
+__global__ void sac_latch_kernel(ul_sac_ctl* ctl, ul_opt_ctl* oc_a, ul_opt_ctl* oc_q1,
+                                 ul_opt_ctl* oc_q2, int side, int u) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const bool crit = oc_q1->diverged || oc_q2->diverged || !isfinite(ctl->critic_loss);
+  const bool act = side == 2 && (oc_a->diverged || ctl->diverged == 2 ||
+                                 !isfinite(ctl->actor_loss));
+  if (ctl->diverged == 0 && (crit || act)) {
+    ctl->diverged = crit ? 1 : 2;
+    ctl->fail_update = u;
+  }
+  if (ctl->diverged) {
+    oc_a->diverged = 1;
+    oc_q1->diverged = 1;
+    oc_q2->diverged = 1;
+  }
+}
+
+// Polyak of both target critics in one launch (R:algos/sac.py:100-108,
+// :176-177): t *= (1 - tau); t += tau * o with two f32 roundings each (the
+// numpy order); skipped once the run diverged.
+__global__ void polyak2_kernel(float* __restrict__ t1, const float* __restrict__ o1,
+                               float* __restrict__ t2, const float* __restrict__ o2, int64_t n4,
+                               int64_t n, float keep, float tau,
+                               const ul_opt_ctl* __restrict__ guard) {
+  pdl_trigger();
+  pdl_wait();
+  if (guard && guard->diverged) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float4* a4 = reinterpret_cast<float4*>(t1);
+  float4* b4 = reinterpret_cast<float4*>(t2);
+  const float4* c4 = reinterpret_cast<const float4*>(o1);
+  const float4* d4 = reinterpret_cast<const float4*>(o2);
+  auto mix = [&](float4 t, float4 o) {
+    return make_float4(__fadd_rn(__fmul_rn(t.x, keep), __fmul_rn(tau, o.x)),
+                       __fadd_rn(__fmul_rn(t.y, keep), __fmul_rn(tau, o.y)),
+                       __fadd_rn(__fmul_rn(t.z, keep), __fmul_rn(tau, o.z)),
+                       __fadd_rn(__fmul_rn(t.w, keep), __fmul_rn(tau, o.w)));
+  };
+  for (int64_t i = i0; i < n4; i += stride) {
+    const float4 a = a4[i], b = b4[i], c = __ldg(c4 + i), d = __ldg(d4 + i);
+    a4[i] = mix(a, c);
+    b4[i] = mix(b, d);
+  }
+  for (int64_t i = 4 * n4 + i0; i < n; i += stride) {
+    t1[i] = __fadd_rn(__fmul_rn(t1[i], keep), __fmul_rn(tau, o1[i]));
+    t2[i] = __fadd_rn(__fmul_rn(t2[i], keep), __fmul_rn(tau, o2[i]));
+  }
 }
 
 // device standard normals (performance mode): Philox4x32-10 + Box-Muller
@@ -250,20 +373,37 @@ __global__ void normal_kernel(float* out, int64_t n, uint64_t key, uint64_t coun
   }
 }
 
+__global__ void fill_f64_kernel(double* dst, int n, double v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = v;
+}
+
+int fill_f64(double* dst, int n, double v, cudaStream_t s) {
+  fill_f64_kernel<<<(n + 127) / 128, 128, 0, s>>>(dst, n, v);
+  return check_launch("fill_f64_kernel");
+}
+
 int grid_for(int64_t n) {
   int64_t b = ceil_div(n > 0 ? n : 1, 256);
   return (int)(b > 8 * kNumSMs ? 8 * kNumSMs : b);
 }
 
 // ------------------------------------------------------------------- plan
+struct SacGraph {
+  int n = 0;
+  uint64_t mask = 0;  // bit u: update u takes the actor step
+  cudaGraphExec_t exec = nullptr;
+};
+
 struct SacPlan {
   ul_sac_plan_desc d{};
   NetView va{}, vq{};
   int D = 0, A = 0;
+  int dt = kF32;  // dtype of the network inputs / activations (bf16 back end: kBf16)
   int64_t B = 0, ldq = 0, ldo = 0, Pa = 0, Pq = 0;
   char* arena = nullptr;
-  float *qin = nullptr, *qn = nullptr, *qa = nullptr, *obs = nullptr, *rew = nullptr,
-        *term = nullptr, *nused = nullptr;
+  void *qin = nullptr, *qn = nullptr, *qa = nullptr, *obs = nullptr;
+  float *rew = nullptr, *term = nullptr, *nused = nullptr;
   float *acts_a = nullptr, *acts_q1 = nullptr, *acts_q2 = nullptr;
   float *mean = nullptr, *a_pi = nullptr, *logp = nullptr, *q1o = nullptr, *q2o = nullptr,
         *q1t = nullptr, *q2t = nullptr, *dq1 = nullptr, *dq2 = nullptr, *din1 = nullptr,
@@ -274,15 +414,24 @@ struct SacPlan {
   int world = 1;
   double n_global = 0.0;
   float *ws_a = nullptr, *ws_q1 = nullptr, *ws_q2 = nullptr, *ws_q1t = nullptr, *ws_q2t = nullptr;
-  float *eps = nullptr;  // [2, B, A] device noise
+  // per-update noise [n_cap][2][B][A] and statistics [n_cap][4]
+  int n_cap = 0;
+  float* eps = nullptr;
+  double* stats = nullptr;
+  int u = 0;  // update index of the phase being issued (noise / stats slot)
   double* part = nullptr;
   unsigned int* tickets = nullptr;
   ul_opt_ctl *oc_a = nullptr, *oc_q1 = nullptr, *oc_q2 = nullptr;
-  ul_opt_ctl* oc_h = nullptr;  // pinned staging
+  ul_opt_ctl* oc_h = nullptr;  // pinned staging, 3 records (actor, q1, q2)
   ul_sac_ctl* ctl = nullptr;
   ul_sac_ctl* ctl_h = nullptr;
   ul_sac_bindings b{};
   bool bound = false;
+  cudaStream_t cap = nullptr;  // capture / replay stream of the run graphs
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  static constexpr int kMaxGraphs = 16;
+  SacGraph graphs[kMaxGraphs];
+  int n_graphs = 0;
 };
 
 int alloc_sac(SacPlan* p) {
@@ -294,12 +443,14 @@ int alloc_sac(SacPlan* p) {
   };
   const int64_t B = p->B;
   const int64_t wa = bwd_work_floats(p->va, B), wq = bwd_work_floats(p->vq, B);
+  // input matrices sized for fp32 rows (bf16 rows are narrower)
+  const int64_t ldq32 = act_ld(p->D + p->A), ldo32 = act_ld(p->D);
   size_t o[40];
   int k = 0;
-  o[k++] = carve(4 * B * p->ldq);                 // 0 qin
-  o[k++] = carve(4 * B * p->ldq);                 // 1 qn
-  o[k++] = carve(4 * B * p->ldq);                 // 2 qa
-  o[k++] = carve(4 * B * p->ldo);                 // 3 obs
+  o[k++] = carve(4 * B * ldq32);                  // 0 qin
+  o[k++] = carve(4 * B * ldq32);                  // 1 qn
+  o[k++] = carve(4 * B * ldq32);                  // 2 qa
+  o[k++] = carve(4 * B * ldo32);                  // 3 obs
   o[k++] = carve(4 * B);                          // 4 rew
   o[k++] = carve(4 * B);                          // 5 term
   o[k++] = carve(4 * B);                          // 6 nused
@@ -328,7 +479,7 @@ int alloc_sac(SacPlan* p) {
   o[k++] = carve(4 * p->vq.wp_total);             // 29
   o[k++] = carve(4 * p->vq.wp_total);             // 30
   o[k++] = carve(4 * p->vq.wp_total);             // 31
-  o[k++] = carve(4 * 2 * B * p->A);               // 32 eps
+  o[k++] = carve(8);                              // 32 (noise: ul_sac_plan_reserve)
   o[k++] = carve(8 * (ceil_div(B, 256) * (UL_MAX_ACT + 2) + 64));  // 33 part
   o[k++] = carve(4 * 16);                         // 34 tickets
   o[k++] = carve(sizeof(ul_opt_ctl));             // 35
@@ -338,10 +489,14 @@ int alloc_sac(SacPlan* p) {
   UL_CUDA(cudaMalloc(&p->arena, off));
   UL_CUDA(cudaMemset(p->arena, 0, off));
   char* a = p->arena;
-  float** fp[] = {&p->qin, &p->qn, &p->qa, &p->obs, &p->rew, &p->term, &p->nused, &p->acts_a,
-                  &p->acts_q1, &p->acts_q2, &p->mean, &p->a_pi, &p->logp, &p->q1o, &p->q2o,
-                  &p->q1t, &p->q2t, &p->dq1, &p->dq2, &p->din1, &p->din2, &p->dmean};
-  for (int i = 0; i < 22; ++i) *fp[i] = (float*)(a + o[i]);
+  p->qin = a + o[0];
+  p->qn = a + o[1];
+  p->qa = a + o[2];
+  p->obs = a + o[3];
+  float** fp[] = {&p->rew, &p->term, &p->nused, &p->acts_a, &p->acts_q1, &p->acts_q2, &p->mean,
+                  &p->a_pi, &p->logp, &p->q1o, &p->q2o, &p->q1t, &p->q2t, &p->dq1, &p->dq2,
+                  &p->din1, &p->din2, &p->dmean};
+  for (int i = 0; i < 18; ++i) *fp[i] = (float*)(a + o[4 + i]);
   p->y = (double*)(a + o[22]);
   p->ga_own = (float*)(a + o[23]);
   p->gq_own = (float*)(a + o[24]);
@@ -354,28 +509,42 @@ int alloc_sac(SacPlan* p) {
   p->ws_q2 = (float*)(a + o[29]);
   p->ws_q1t = (float*)(a + o[30]);
   p->ws_q2t = (float*)(a + o[31]);
-  p->eps = (float*)(a + o[32]);
   p->part = (double*)(a + o[33]);
   p->tickets = (unsigned int*)(a + o[34]);
   p->oc_a = (ul_opt_ctl*)(a + o[35]);
   p->oc_q1 = (ul_opt_ctl*)(a + o[36]);
   p->oc_q2 = (ul_opt_ctl*)(a + o[37]);
   p->ctl = (ul_sac_ctl*)(a + o[38]);
-  UL_CUDA(cudaHostAlloc(&p->oc_h, sizeof(ul_opt_ctl), cudaHostAllocPortable));
+  UL_CUDA(cudaHostAlloc(&p->oc_h, 3 * sizeof(ul_opt_ctl), cudaHostAllocPortable));
   UL_CUDA(cudaHostAlloc(&p->ctl_h, sizeof(ul_sac_ctl), cudaHostAllocPortable));
+  UL_CUDA(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_in, cudaEventDisableTiming));
+  UL_CUDA(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
   return UL_OK;
 }
 
+void drop_graphs(SacPlan* p) {
+  for (int i = 0; i < p->n_graphs; ++i)
+    if (p->graphs[i].exec) cudaGraphExecDestroy(p->graphs[i].exec);
+  p->n_graphs = 0;
+}
+
 void free_sac(SacPlan* p) {
+  drop_graphs(p);
   if (p->arena) cudaFree(p->arena);
+  if (p->eps) cudaFree(p->eps);
+  if (p->stats) cudaFree(p->stats);
   if (p->oc_h) cudaFreeHost(p->oc_h);
   if (p->ctl_h) cudaFreeHost(p->ctl_h);
+  if (p->cap) cudaStreamDestroy(p->cap);
+  if (p->ev_in) cudaEventDestroy(p->ev_in);
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
 }
 
 size_t ctl_hdr() { return offsetof(ul_opt_ctl, part); }
 
-int adam_one(SacPlan* p, float* params, float* grads, float* m, float* v, int64_t n,
-             ul_opt_ctl* oc, cudaStream_t s) {
+int adam_one(float* params, float* grads, float* m, float* v, int64_t n, ul_opt_ctl* oc,
+             cudaStream_t s) {
   SegTable st{};
   st.nseg = 1;
   st.g[0] = grads;
@@ -385,6 +554,23 @@ int adam_one(SacPlan* p, float* params, float* grads, float* m, float* v, int64_
   st.n[0] = n;
   UL_TRY(launch_prepare(st, oc, s));
   return launch_apply(st, oc, 0, 1, s);
+}
+
+int launch_squash(SacPlan* p, const float* eps, void* dst, float* a_out, cudaStream_t s) {
+  const float* ls = p->b.actor + p->va.logstd_off;
+  const int64_t B = p->B;
+  if (p->dt == kBf16)
+    squash_kernel<__nv_bfloat16><<<grid_for(B), 256, 0, s>>>(
+        p->mean, p->A, ls, eps, p->A, B, p->A, (__nv_bfloat16*)dst, p->ldq, p->D, a_out, p->logp);
+  else
+    squash_kernel<float><<<grid_for(B), 256, 0, s>>>(p->mean, p->A, ls, eps, p->A, B, p->A,
+                                                     (float*)dst, p->ldq, p->D, a_out, p->logp);
+  return check_launch("squash_kernel");
+}
+
+double* rec_of(SacPlan* p) { return p->stats ? p->stats + 4 * (int64_t)p->u : nullptr; }
+const float* eps_of(SacPlan* p, int which) {
+  return p->eps + ((int64_t)p->u * 2 + which) * p->B * p->A;
 }
 
 }  // namespace
@@ -417,13 +603,17 @@ extern "C" int ul_sac_plan_create(const ul_sac_plan_desc* desc, void** plan) {
   if (p->vq.dims[0] != p->D + p->A || p->vq.dims[p->vq.n_layers] != 1)
     return fail("sac plan: critic must map obs+act -> 1");
   if (p->A > UL_MAX_ACT) return fail("sac plan: action dim above UL_MAX_ACT");
-  p->ldq = ul::act_ld(p->D + p->A);
-  p->ldo = ul::act_ld(p->D);
+  if (desc->gemm_backend < 0 || desc->gemm_backend > 2)
+    return fail("sac plan: gemm_backend must be 0 (fp32), 1 (tf32) or 2 (bf16)");
+  p->dt = ul::backend_dtype(desc->gemm_backend);
+  p->ldq = ul::act_ld(p->D + p->A, p->dt);
+  p->ldo = ul::act_ld(p->D, p->dt);
   p->world = desc->world_size > 1 ? desc->world_size : 1;
   p->n_global = (double)p->B * p->world;
   p->Pa = p->va.total;
   p->Pq = p->vq.total;
   st = ul::alloc_sac(p);
+  if (st == UL_OK) st = ul_sac_plan_reserve(p, 1);
   if (st != UL_OK) {
     ul::free_sac(p);
     delete p;
@@ -441,9 +631,28 @@ extern "C" int ul_sac_plan_destroy(void* plan) {
   return UL_OK;
 }
 
+extern "C" int ul_sac_plan_reserve(void* plan, int n_updates) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && n_updates >= 1 && n_updates <= 64, "sac plan: reserve 1..64 updates");
+  if (n_updates <= p->n_cap) return UL_OK;
+  UL_CUDA(cudaDeviceSynchronize());  // the old buffers may still be read
+  ul::drop_graphs(p);                // (graphs hold the old pointers)
+  if (p->eps) cudaFree(p->eps);
+  if (p->stats) cudaFree(p->stats);
+  p->eps = nullptr;
+  p->stats = nullptr;
+  UL_CUDA(cudaMalloc(&p->eps, sizeof(float) * 2 * (size_t)n_updates * p->B * p->A));
+  UL_CUDA(cudaMemset(p->eps, 0, sizeof(float) * 2 * (size_t)n_updates * p->B * p->A));
+  UL_CUDA(cudaMalloc(&p->stats, sizeof(double) * 4 * (size_t)n_updates));
+  p->n_cap = n_updates;
+  return UL_OK;
+}
+
 extern "C" int ul_sac_plan_bind(void* plan, const ul_sac_bindings* b) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p && b, "sac plan: null argument");
+  const bool same = p->bound && memcmp(&p->b, b, sizeof(*b)) == 0;
+  if (!same) ul::drop_graphs(p);  // graphs bake the parameter pointers
   p->b = *b;
   p->bound = true;
   float* gq = b->critic_red ? b->critic_red : p->gq_own;
@@ -454,54 +663,59 @@ extern "C" int ul_sac_plan_bind(void* plan, const ul_sac_bindings* b) {
 }
 
 // Load a batch of codec rows (obs | act | r | next_obs | term | n_used):
-// rows[idx[i] % modulo] for device ring rows (idx may be NULL for rows 0..B-1).
+// rows[idx[i] % modulo] for device ring rows (idx may be NULL for rows
+// 0..B-1), written in the back end's input dtype by one kernel.
 extern "C" int ul_sac_plan_load_rows(void* plan, const float* rows, int64_t pitch,
                                      const int64_t* idx, int64_t modulo, int64_t lo, int64_t hi,
                                      int* err, void* stream) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p, "sac plan: null");
-  const int64_t D = p->D, A = p->A;
-  const int64_t width = 2 * D + A + 3;
+  const int64_t width = 2 * (int64_t)p->D + p->A + 3;
   UL_CHECK_ARG(pitch >= width, "sac plan: row pitch below codec width");
-  const char* r = (const char*)rows;
-  const void* src[7] = {r, r, r, r + 4 * (D + A + 1), r + 4 * (D + A), r + 4 * (2 * D + A + 1),
-                        r + 4 * (2 * D + A + 2)};
-  void* dst[7] = {p->qin, p->obs, p->qa, p->qn, p->rew, p->term, p->nused};
-  const int64_t ps = 4 * pitch;
-  const int64_t sst[7] = {ps, ps, ps, ps, ps, ps, ps};
-  const int64_t dstr[7] = {4 * p->ldq, 4 * p->ldo, 4 * p->ldq, 4 * p->ldq, 4, 4, 4};
-  // critic input [obs | act] and actor input obs each carry one extra column
-  // overwritten with 1.0: the bias column of the tensor-core dW
-  const int64_t rb[7] = {4 * (D + A + 1), 4 * (D + 1), 4 * D, 4 * D, 4, 4, 4};
-  const int64_t ones[7] = {4 * (D + A), 4 * D, -1, -1, -1, -1, -1};
-  return ul_gather_rows(7, src, dst, sst, dstr, rb, ones, idx, p->B, modulo, lo, hi, err, stream);
+  cudaStream_t s = ul::as_stream(stream);
+  int64_t blocks = ul::ceil_div(p->B, 8);
+  blocks = blocks > 8 * ul::kNumSMs ? 8 * ul::kNumSMs : blocks;
+  if (p->dt == ul::kBf16) {
+    using T = __nv_bfloat16;
+    return ul::launch_pdl("sac_load_kernel", ul::sac_load_kernel<T>, dim3((unsigned)blocks),
+                          dim3(256), 0, s, rows, pitch, idx, modulo, lo, hi, err, p->B, p->D,
+                          p->A, (T*)p->qin, p->ldq, (T*)p->obs, p->ldo, (T*)p->qa, (T*)p->qn,
+                          p->rew, p->term, p->nused);
+  }
+  return ul::launch_pdl("sac_load_kernel", ul::sac_load_kernel<float>, dim3((unsigned)blocks),
+                        dim3(256), 0, s, rows, pitch, idx, modulo, lo, hi, err, p->B, p->D, p->A,
+                        (float*)p->qin, p->ldq, (float*)p->obs, p->ldo, (float*)p->qa,
+                        (float*)p->qn, p->rew, p->term, p->nused);
 }
 
-// Upload the optimizer / alpha control state (host values -> device).
+// Upload the optimizer / alpha control state (host values -> device):
+// asynchronous, one pinned staging record each (the previous finish synced).
 extern "C" int ul_sac_plan_begin(void* plan, const ul_sac_ctl* host_ctl, const double* lrs,
                                  const int64_t* ts, void* stream) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p && p->bound && host_ctl && lrs && ts, "sac plan: not bound");
   cudaStream_t s = ul::as_stream(stream);
   *p->ctl_h = *host_ctl;
+  p->ctl_h->diverged = 0;
+  p->ctl_h->fail_update = -1;
   UL_CUDA(cudaMemcpyAsync(p->ctl, p->ctl_h, sizeof(ul_sac_ctl), cudaMemcpyHostToDevice, s));
   ul_opt_ctl* dst[3] = {p->oc_a, p->oc_q1, p->oc_q2};
   for (int k = 0; k < 3; ++k) {
     const double lr = lrs[k];
-    UL_TRY(ul_opt_ctl_init(p->oc_h, 1, &lr, 0.9, 0.999, 1e-8, p->d.max_grad_norm));
-    p->oc_h->t[0] = ts[k];
-    UL_CUDA(cudaMemcpyAsync(dst[k], p->oc_h, ul::ctl_hdr(), cudaMemcpyHostToDevice, s));
-    UL_CUDA(cudaStreamSynchronize(s));  // pinned staging reused for the next record
+    UL_TRY(ul_opt_ctl_init(p->oc_h + k, 1, &lr, 0.9, 0.999, 1e-8, p->d.max_grad_norm));
+    p->oc_h[k].t[0] = ts[k];
+    UL_CUDA(cudaMemcpyAsync(dst[k], p->oc_h + k, ul::ctl_hdr(), cudaMemcpyHostToDevice, s));
   }
   return UL_OK;
 }
 
-// Fill the two noise blocks [2, B, A] on device (performance mode).
+// Fill the whole reserved noise buffer [n_cap][2][B][A] on the device
+// (performance mode).
 extern "C" int ul_sac_plan_device_noise(void* plan, uint64_t key, uint64_t counter,
                                         void* stream) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p, "sac plan: null");
-  const int64_t n = 2 * p->B * p->A;
+  const int64_t n = 2 * (int64_t)p->n_cap * p->B * p->A;
   ul::normal_kernel<<<ul::grid_for(ul::ceil_div(n, 4)), 256, 0, ul::as_stream(stream)>>>(
       p->eps, n, key, counter);
   return ul::check_launch("normal_kernel");
@@ -517,55 +731,61 @@ extern "C" int ul_sac_plan_noise_ptr(void* plan, float** eps) {
 namespace ul {
 namespace {
 
+int stage_critics(SacPlan* p, cudaStream_t s) {
+  const int wd = backend_dtype(p->d.gemm_backend);
+  UL_TRY(stage_weights_dt(p->vq, p->b.q1, p->ws_q1, wd, s));
+  return stage_weights_dt(p->vq, p->b.q2, p->ws_q2, wd, s);
+}
+
 // phase 1: staged weights, soft target, critic forwards + MSE head + critic
 // backwards into [g_q1 | g_q2 | loss share]
 int sac_critic_grads(SacPlan* p, cudaStream_t s) {
   const ul_sac_bindings& b = p->b;
   const int be = p->d.gemm_backend;
-  const int64_t B = p->B, D = p->D, A = p->A;
-  const float* ls = b.actor + p->va.logstd_off;
+  const int64_t B = p->B, A = p->A;
+  const float* qin = (const float*)p->qin;  // (rows of the back end's dtype)
+  const float* qn = (const float*)p->qn;
   if (be != 0) {  // tensor-core back ends read 16-B-row staged (tf32 / bf16) weights
     const int wd = backend_dtype(be);
     UL_TRY(stage_weights_dt(p->va, b.actor, p->ws_a, wd, s));
-    UL_TRY(stage_weights_dt(p->vq, b.q1, p->ws_q1, wd, s));
-    UL_TRY(stage_weights_dt(p->vq, b.q2, p->ws_q2, wd, s));
+    UL_TRY(stage_critics(p, s));
     UL_TRY(stage_weights_dt(p->vq, b.q1t, p->ws_q1t, wd, s));
     UL_TRY(stage_weights_dt(p->vq, b.q2t, p->ws_q2t, wd, s));
   }
-  // ---- K10 target
-  UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, p->qn, p->ldq, B, p->acts_a, p->mean, A, s));
-  squash_kernel<<<grid_for(B), 256, 0, s>>>(p->mean, A, ls, p->eps, A, B, (int)A, p->qn, p->ldq,
-                                           (int)D, nullptr, p->logp);
-  UL_TRY(check_launch("squash_kernel"));
-  UL_TRY(mlp_forward(p->vq, b.q1t, p->ws_q1t, be, p->qn, p->ldq, B, p->acts_q1, p->q1t, 1, s));
-  UL_TRY(mlp_forward(p->vq, b.q2t, p->ws_q2t, be, p->qn, p->ldq, B, p->acts_q2, p->q2t, 1, s));
+  // ---- K10 target (next_obs rows of qn, actions a' written by the squash)
+  UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, qn, p->ldq, B, p->acts_a, p->mean, A, s));
+  UL_TRY(launch_squash(p, eps_of(p, 0), p->qn, nullptr, s));
+  UL_TRY(mlp_forward(p->vq, b.q1t, p->ws_q1t, be, qn, p->ldq, B, p->acts_q1, p->q1t, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q2t, p->ws_q2t, be, qn, p->ldq, B, p->acts_q2, p->q2t, 1, s));
   sac_target_kernel<<<grid_for(B), 256, 0, s>>>(p->rew, p->term, p->nused, p->q1t, p->q2t,
                                                p->logp, p->ctl, p->d.gamma, B, p->y);
   UL_TRY(check_launch("sac_target_kernel"));
   // ---- K11 critics (ones column of qin at D+A feeds the tensor-core db)
-  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, B, p->acts_q1, p->q1o, 1, s));
-  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, qin, p->ldq, B, p->acts_q1, p->q1o, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, qin, p->ldq, B, p->acts_q2, p->q2o, 1, s));
   const unsigned nb = (unsigned)ceil_div(B, 256);
   critic_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->y, B, 1.0 / p->n_global, p->dq1,
                                         p->dq2, p->part, p->tickets, p->ctl,
-                                        p->world > 1 ? p->g_q1 + 2 * p->Pq : nullptr);
+                                        p->world > 1 ? p->g_q1 + 2 * p->Pq : nullptr, rec_of(p));
   UL_TRY(check_launch("critic_head_kernel"));
-  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qin, p->ldq, true, B, p->acts_q1, p->dq1, 1,
+  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, qin, p->ldq, true, B, p->acts_q1, p->dq1, 1,
                       p->g_q1, nullptr, 0, 0, 0, true, true, p->work, s));
-  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qin, p->ldq, true, B, p->acts_q2, p->dq2, 1,
+  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, qin, p->ldq, true, B, p->acts_q2, p->dq2, 1,
                       p->g_q2, nullptr, 0, 0, 0, true, true, p->work, s));
   return UL_OK;
 }
 
-// phase 2: (reduced loss back into ctl) Adam(q1), Adam(q2)
+// phase 2: (reduced loss back into ctl) Adam(q1), Adam(q2), latch
 int sac_critic_apply(SacPlan* p, cudaStream_t s) {
   const ul_sac_bindings& b = p->b;
   if (p->world > 1) {
     sac_reduced_scalars_kernel<<<1, 32, 0, s>>>(p->ctl, p->g_q1 + 2 * p->Pq, nullptr);
     UL_TRY(check_launch("sac_reduced_scalars_kernel"));
   }
-  UL_TRY(adam_one(p, b.q1, p->g_q1, b.q1_m, b.q1_v, p->Pq, p->oc_q1, s));
-  return adam_one(p, b.q2, p->g_q2, b.q2_m, b.q2_v, p->Pq, p->oc_q2, s);
+  UL_TRY(adam_one(b.q1, p->g_q1, b.q1_m, b.q1_v, p->Pq, p->oc_q1, s));
+  UL_TRY(adam_one(b.q2, p->g_q2, b.q2_m, b.q2_v, p->Pq, p->oc_q2, s));
+  sac_latch_kernel<<<1, 32, 0, s>>>(p->ctl, p->oc_a, p->oc_q1, p->oc_q2, 1, p->u);
+  return check_launch("sac_latch_kernel");
 }
 
 // phase 3 (actor steps): actor fwd -> squash(eps2) -> UPDATED critics fwd ->
@@ -576,69 +796,130 @@ int sac_actor_grads(SacPlan* p, cudaStream_t s) {
   const int be = p->d.gemm_backend;
   const int64_t B = p->B, D = p->D, A = p->A;
   const float* ls = b.actor + p->va.logstd_off;
-  if (be != 0) {  // the critics just took their Adam step
-    UL_TRY(stage_weights_dt(p->vq, b.q1, p->ws_q1, backend_dtype(be), s));
-    UL_TRY(stage_weights_dt(p->vq, b.q2, p->ws_q2, backend_dtype(be), s));
-  }
-  const float* eps2 = p->eps + B * A;
-  UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, B, p->acts_a, p->mean, A, s));
-  squash_kernel<<<grid_for(B), 256, 0, s>>>(p->mean, A, ls, eps2, A, B, (int)A, p->qa, p->ldq,
-                                           (int)D, p->a_pi, p->logp);
-  UL_TRY(check_launch("squash_kernel"));
-  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, B, p->acts_q1, p->q1o, 1, s));
-  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  const float* qa = (const float*)p->qa;
+  const float* obs = (const float*)p->obs;
+  if (be != 0) UL_TRY(stage_critics(p, s));  // the critics just took their Adam step
+  const float* eps2 = eps_of(p, 1);
+  UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, obs, p->ldo, B, p->acts_a, p->mean, A, s));
+  UL_TRY(launch_squash(p, eps2, p->qa, p->a_pi, s));
+  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, qa, p->ldq, B, p->acts_q1, p->q1o, 1, s));
+  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, qa, p->ldq, B, p->acts_q2, p->q2o, 1, s));
   const unsigned nb = (unsigned)ceil_div(B, 256);
   pick_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->logp, B, p->n_global, p->dq1, p->dq2,
                                       p->part, p->tickets + 1, p->ctl,
-                                      p->world > 1 ? p->g_a + p->Pa : nullptr);
+                                      p->world > 1 ? p->g_a + p->Pa : nullptr, rec_of(p));
   UL_TRY(check_launch("pick_head_kernel"));
-  // dQ/da through each critic's input gradient, action columns only
-  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, p->qa, p->ldq, false, B, p->acts_q1, p->dq1, 1,
+  // dQ/da through each critic's input gradient, action columns only (fp32 out)
+  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, qa, p->ldq, false, B, p->acts_q1, p->dq1, 1,
                       nullptr, p->din1, A, (int)D, (int)A, false, false, p->work, s));
-  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, p->qa, p->ldq, false, B, p->acts_q2, p->dq2, 1,
+  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, qa, p->ldq, false, B, p->acts_q2, p->dq2, 1,
                       nullptr, p->din2, A, (int)D, (int)A, false, false, p->work, s));
   actor_head_kernel<<<nb, 256, 0, s>>>(p->a_pi, eps2, A, p->din1, p->din2, A, ls, B, p->n_global,
                                        (int)A, p->ctl, p->dmean, p->part, p->tickets + 2,
                                        p->g_a + p->va.logstd_off);
   UL_TRY(check_launch("actor_head_kernel"));
-  return mlp_backward(p->va, b.actor, p->ws_a, be, p->obs, p->ldo, true, B, p->acts_a, p->dmean,
+  return mlp_backward(p->va, b.actor, p->ws_a, be, obs, p->ldo, true, B, p->acts_a, p->dmean,
                       A, p->g_a, nullptr, 0, 0, 0, true, false, p->work, s);
 }
 
-// phase 4: (reduced scalars back into ctl) Adam(actor), alpha ScalarAdam
+// phase 4: (reduced scalars back into ctl) Adam(actor), alpha ScalarAdam, latch
 int sac_actor_apply(SacPlan* p, cudaStream_t s) {
   const ul_sac_bindings& b = p->b;
   if (p->world > 1) {
     sac_reduced_scalars_kernel<<<1, 32, 0, s>>>(p->ctl, nullptr, p->g_a + p->Pa);
     UL_TRY(check_launch("sac_reduced_scalars_kernel"));
   }
-  UL_TRY(adam_one(p, b.actor, p->g_a, b.actor_m, b.actor_v, p->Pa, p->oc_a, s));
-  alpha_step_kernel<<<1, 32, 0, s>>>(p->ctl, p->n_global, p->d.target_entropy);
-  return check_launch("alpha_step_kernel");
+  UL_TRY(adam_one(b.actor, p->g_a, b.actor_m, b.actor_v, p->Pa, p->oc_a, s));
+  alpha_step_kernel<<<1, 32, 0, s>>>(p->ctl, p->oc_a, p->n_global, p->d.target_entropy,
+                                     rec_of(p));
+  UL_TRY(check_launch("alpha_step_kernel"));
+  sac_latch_kernel<<<1, 32, 0, s>>>(p->ctl, p->oc_a, p->oc_q1, p->oc_q2, 2, p->u);
+  return check_launch("sac_latch_kernel");
 }
 
-// phase 5: Polyak q1t <- q1, q2t <- q2 (R:algos/sac.py:176-177)
+// phase 5: Polyak q1t <- q1, q2t <- q2 (R:algos/sac.py:176-177), one launch,
+// skipped after a divergence
 int sac_polyak(SacPlan* p, cudaStream_t s) {
-  UL_TRY(ul_polyak(p->b.q1t, p->b.q1, p->Pq, p->d.tau, s));
-  return ul_polyak(p->b.q2t, p->b.q2, p->Pq, p->d.tau, s);
+  const int64_t n = p->Pq;
+  const bool vec = ((((uintptr_t)p->b.q1t | (uintptr_t)p->b.q1 | (uintptr_t)p->b.q2t |
+                      (uintptr_t)p->b.q2) & 15) == 0);
+  const int64_t n4 = vec ? n / 4 : 0;
+  int64_t blocks = ceil_div(n4 > 0 ? n4 : n, 256);
+  blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
+  return launch_pdl("polyak2_kernel", polyak2_kernel, dim3((unsigned)(blocks > 0 ? blocks : 1)),
+                    dim3(256), 0, s, p->b.q1t, (const float*)p->b.q1, p->b.q2t,
+                    (const float*)p->b.q2, n4, n, (float)(1.0 - p->d.tau), (float)p->d.tau,
+                    (const ul_opt_ctl*)p->oc_q1);
+}
+
+int one_update(SacPlan* p, int u, bool do_actor, cudaStream_t s) {
+  p->u = u;
+  UL_TRY(sac_critic_grads(p, s));
+  UL_TRY(sac_critic_apply(p, s));
+  if (do_actor) {
+    UL_TRY(sac_actor_grads(p, s));
+    UL_TRY(sac_actor_apply(p, s));
+  }
+  return sac_polyak(p, s);
 }
 
 }  // namespace
 }  // namespace ul
 
-// One sac_update (R:algos/sac.py:139-178).  do_actor: update_count %
-// policy_frequency == 0 after the increment.
+// One sac_update (R:algos/sac.py:139-178), issued kernel by kernel.  do_actor:
+// update_count % policy_frequency == 0 after the increment.
 extern "C" int ul_sac_plan_update(void* plan, int do_actor, void* stream) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p && p->bound, "sac plan: not bound");
   cudaStream_t s = ul::as_stream(stream);
-  UL_TRY(ul::sac_critic_grads(p, s));
-  UL_TRY(ul::sac_critic_apply(p, s));
-  if (do_actor) {
-    UL_TRY(ul::sac_actor_grads(p, s));
-    UL_TRY(ul::sac_actor_apply(p, s));
+  UL_TRY(ul::fill_f64(p->stats, 4, __builtin_nan(""), s));
+  return ul::one_update(p, 0, do_actor != 0, s);
+}
+
+// n updates as one CUDA graph (cached per (n, actor-step pattern)); the stats
+// rows start as NaN so updates without an actor step report none.
+extern "C" int ul_sac_plan_run(void* plan, int n_updates, int64_t update_count0,
+                               int policy_frequency, void* stream) {
+  SacPlan* p = (SacPlan*)plan;
+  UL_CHECK_ARG(p && p->bound, "sac plan: not bound");
+  UL_CHECK_ARG(n_updates >= 1 && n_updates <= p->n_cap,
+               "sac plan: %d updates exceed the reserved %d", n_updates, p->n_cap);
+  UL_CHECK_ARG(policy_frequency >= 1, "sac plan: policy_frequency must be >= 1");
+  cudaStream_t s = ul::as_stream(stream);
+  uint64_t mask = 0;
+  for (int u = 0; u < n_updates; ++u)
+    if ((update_count0 + u + 1) % policy_frequency == 0) mask |= uint64_t(1) << u;
+  ul::SacGraph* g = nullptr;
+  for (int i = 0; i < p->n_graphs; ++i)
+    if (p->graphs[i].n == n_updates && p->graphs[i].mask == mask) g = &p->graphs[i];
+  UL_CUDA(cudaEventRecord(p->ev_in, s));
+  UL_CUDA(cudaStreamWaitEvent(p->cap, p->ev_in, 0));
+  if (!g) {
+    if (p->n_graphs == SacPlan::kMaxGraphs) ul::drop_graphs(p);
+    cudaGraph_t gr;
+    UL_CUDA(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+    int st = UL_OK;
+    const double nanv = __builtin_nan("");
+    for (int u = 0; u < n_updates && st == UL_OK; ++u) {
+      // NaN-fill the update's stats row (a memset node would need a byte
+      // pattern): the heads overwrite what the update produces
+      st = ul::fill_f64(p->stats + 4 * u, 4, nanv, p->cap);
+      if (st == UL_OK) st = ul::one_update(p, u, (mask >> u) & 1, p->cap);
+    }
+    cudaError_t ce = cudaStreamEndCapture(p->cap, &gr);
+    if (st != UL_OK) return st;
+    UL_CUDA(ce);
+    g = &p->graphs[p->n_graphs++];
+    g->n = n_updates;
+    g->mask = mask;
+    ce = cudaGraphInstantiate(&g->exec, gr, 0);
+    cudaGraphDestroy(gr);
+    UL_CUDA(ce);
   }
-  return ul::sac_polyak(p, s);
+  UL_CUDA(cudaGraphLaunch(g->exec, p->cap));
+  UL_CUDA(cudaEventRecord(p->ev_out, p->cap));
+  UL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
+  return UL_OK;
 }
 
 extern "C" int ul_sac_plan_reduce_buffers(void* plan, float** critic, int64_t* n_critic,
@@ -656,6 +937,7 @@ extern "C" int ul_sac_plan_reduce_buffers(void* plan, float** critic, int64_t* n
   extern "C" int NAME(void* plan, void* stream) {               \
     SacPlan* p = (SacPlan*)plan;                                \
     UL_CHECK_ARG(p && p->bound, "sac plan: not bound");         \
+    p->u = 0;                                                   \
     return ul::FN(p, ul::as_stream(stream));                    \
   }
 UL_SAC_PHASE(ul_sac_plan_critic_grads, sac_critic_grads)
@@ -665,30 +947,27 @@ UL_SAC_PHASE(ul_sac_plan_actor_apply, sac_actor_apply)
 UL_SAC_PHASE(ul_sac_plan_polyak, sac_polyak)
 #undef UL_SAC_PHASE
 
-// Read back the control records; UL_ERR_DIVERGENCE if an Adam step or the
-// critic / actor loss saw non-finite values.
-extern "C" int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, void* stream) {
+// Read back the control records (and the run's per-update statistics) with
+// one sync; UL_ERR_DIVERGENCE if any step of the run diverged (out->diverged:
+// 1 critic side, 2 actor / alpha side; out->fail_update: which update).
+extern "C" int ul_sac_plan_finish(void* plan, ul_sac_ctl* out, int64_t* ts, double* stats,
+                                  int n, void* stream) {
   SacPlan* p = (SacPlan*)plan;
   UL_CHECK_ARG(p && out && ts, "sac plan: null");
+  UL_CHECK_ARG(!stats || (n >= 0 && n <= p->n_cap), "sac plan: stats rows exceed the reserve");
   cudaStream_t s = ul::as_stream(stream);
   UL_CUDA(cudaMemcpyAsync(p->ctl_h, p->ctl, sizeof(ul_sac_ctl), cudaMemcpyDeviceToHost, s));
   ul_opt_ctl* srcs[3] = {p->oc_a, p->oc_q1, p->oc_q2};
-  int bad[3] = {0, 0, 0};
-  for (int k = 0; k < 3; ++k) {
-    UL_CUDA(cudaMemcpyAsync(p->oc_h, srcs[k], ul::ctl_hdr(), cudaMemcpyDeviceToHost, s));
-    UL_CUDA(cudaStreamSynchronize(s));
-    ts[k] = p->oc_h->t[0];
-    bad[k] = p->oc_h->diverged;
-  }
+  for (int k = 0; k < 3; ++k)
+    UL_CUDA(cudaMemcpyAsync(p->oc_h + k, srcs[k], ul::ctl_hdr(), cudaMemcpyDeviceToHost, s));
+  if (stats && n > 0)
+    UL_CUDA(cudaMemcpyAsync(stats, p->stats, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
+  UL_CUDA(cudaStreamSynchronize(s));
+  for (int k = 0; k < 3; ++k) ts[k] = p->oc_h[k].t[0];
   *out = *p->ctl_h;
-  // out->diverged: 1 = critic side (the reference raises before counting the
-  // update), 2 = actor / alpha side (raised after the count)
-  const bool critic_bad = bad[1] || bad[2] || !isfinite(out->critic_loss);
-  const bool actor_bad = bad[0] || out->diverged;
-  out->diverged = critic_bad ? 1 : (actor_bad ? 2 : 0);
-  if (critic_bad || actor_bad) {
-    ul::set_error(critic_bad ? "non-finite SAC critic loss or gradients"
-                             : "non-finite SAC actor / alpha loss or gradients");
+  if (out->diverged) {
+    ul::set_error(out->diverged == 1 ? "non-finite SAC critic loss or gradients"
+                                     : "non-finite SAC actor / alpha loss or gradients");
     return UL_ERR_DIVERGENCE;
   }
   return UL_OK;

@@ -20,7 +20,8 @@ near-zero gradient components).  The exact-fp32 path must track the f32
 reference itself (<= 0.05 / >= 0.999; measured 0.009 / 0.99996).  APPO bf16
 at cfg5 shapes: <= 0.15 / >= 0.99 (measured 0.105 / 0.9945; the reference's
 own f32-vs-f64 actor gap there is 0.050 / 0.9987); APPO tf32 <= 0.10 / >= 0.995.
-Update statistics (losses, kl) within 1e-3 * max(1, |ref|) of the f32 oracle.
+Update statistics (losses, kl) within 1e-3 * max(1, |ref|) of the f32 oracle
+(APPO: 5e-3, its value targets come from the tensor-core recompute forward).
 """
 
 import numpy as np
@@ -139,15 +140,15 @@ def _rel_cos(d, r):
     return rel, cos
 
 
-def _check(ref, got, which, rel_max, cos_max):
+def _check(ref, got, which, rel_max, cos_max, loss_tol=1e-3):
     da, dc, st = got
     for name, d, r in (("actor", da, ref[which][0]), ("critic", dc, ref[which][1])):
         rel, cos = _rel_cos(d, r)
         assert rel <= rel_max and cos >= cos_max, (name, which, rel, cos)
     ost = ref["f32"][2]
     for k in ("policy_loss", "value_loss", "kl"):
-        assert abs(getattr(st, k) - ost[k]) <= 1e-3 * max(1.0, abs(ost[k])), (k, getattr(st, k),
-                                                                            ost[k])
+        assert abs(getattr(st, k) - ost[k]) <= loss_tol * max(1.0, abs(ost[k])), (
+            k, getattr(st, k), ost[k])
 
 
 @pytest.mark.parametrize("prec", ["tf32", "bf16"])
@@ -169,7 +170,9 @@ def test_appo_cfg5_quarter_update_matches_f64_oracle(cfg5q_oracle, prec, rel_max
     """appo_update at cfg5 shapes (1/4 of the envs): recompute over 98,304 rows,
     V-trace with ratios != 1, 5 x 4 minibatch steps."""
     got = _gpu_update(CFG5Q, cfg5q_oracle, prec, appo=True)
-    _check(cfg5q_oracle, got, "f64", rel_max, cos_min)
+    # (the mean value loss also carries the recomputed values_now of the
+    # tensor-core forward: measured 2e-3 from the f32 oracle for tf32 and bf16)
+    _check(cfg5q_oracle, got, "f64", rel_max, cos_min, loss_tol=5e-3)
 
 
 def test_performance_mode_matches_parity_mode_statistically():

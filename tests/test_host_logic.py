@@ -10,8 +10,6 @@ import pytest
 
 from oracle import port as O
 from paper_2605_30313_b200 import _dist
-from paper_2605_30313_b200.algos.estimators import (NStepPacker, ReturnStdNormalizer,
-                                                    nstep_and_reward_norm)
 from paper_2605_30313_b200.errors import PipelineStall, SlotStateError
 from paper_2605_30313_b200.replaypath.slots import PackSlotPair, SlotState, pack
 from paper_2605_30313_b200.replaypath.storage import ReplayStorage, RowCodec
@@ -102,27 +100,6 @@ def test_tracer_registry_and_overlap():
         tr.record("learner", "learner/update", 5, 12)
     with pytest.raises(ValueError):
         tr.record("learner", "not/registered", 20, 30)
-
-
-def test_collector_packers_match_reference_known_answers():
-    # R:tests/test_estimators.py:246-262 boundary truncation
-    g = 0.9
-    p = NStepPacker(n=3, gamma=g, n_envs=1)
-    z = np.zeros((1, 1))
-    assert p.push(z, z, np.array([1.0]), z, np.array([False]), np.array([False])) == []
-    rows = p.push(z + 1, z, np.array([2.0]), z + 9, np.array([True]), np.array([False]))
-    assert len(rows) == 2 and rows[0][2] == pytest.approx(1.0 + g * 2.0) and rows[0][5] == 2
-    # clip bound (1 - gamma) g_max (:303-312)
-    norm = ReturnStdNormalizer(gamma=0.97, g_max=5.0, n_envs=2)
-    rng = np.random.default_rng(5)
-    for _ in range(50):
-        out = norm.normalize(rng.normal(scale=3.0, size=2), np.zeros(2, bool))
-        assert np.all(np.abs(out) <= (1 - 0.97) * 5.0 + 1e-12)
-    packer = NStepPacker(n=1, gamma=0.97, n_envs=1)
-    rows = nstep_and_reward_norm(packer, ReturnStdNormalizer(0.97, 5.0, 1), np.zeros((1, 2)),
-                                 np.zeros((1, 1)), np.array([100.0]), np.ones((1, 2)),
-                                 np.array([False]), np.array([False]))
-    assert len(rows) == 1 and abs(rows[0][2]) <= (1 - 0.97) * 5.0 + 1e-12
 
 
 def test_shard_rows():

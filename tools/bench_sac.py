@@ -69,9 +69,12 @@ def main():
     if a.cfg == "cfg4":
         B, CH, AH, PF = 32768, (1024, 1024, 1024), (512, 512), 2
         a.no_ln = True
-    K = (a.steps + 3) // 4 * 4
     P.set_precision(a.precision)
     st, cfg = build(not a.no_ln, a.cfg == "cfg4")
+    # one learner tick = updates_per_step sac_updates on one batch, one graph
+    # launch (R:runtime/sac_runner.py:313-321); cfg4: UTD 8
+    utd = 8 if a.cfg == "cfg4" else cfg.updates_per_step
+    K = max(1, (a.steps + utd - 1) // utd)
     width = 2 * OD + AD + 3
     g = torch.Generator(device="cuda").manual_seed(0)
     ring = torch.randn(RING, width, device="cuda", generator=g)
@@ -82,18 +85,18 @@ def main():
     idx_dev = [torch.from_numpy(hrng.integers(0, RING, B)).cuda() for _ in range(K)]
     drng = DeviceRng(0)
     s = torch.cuda.current_stream()
-    for i in range(a.warmup):
-        A.sac_update(A.DeviceRows(ring, width, idx_dev[i % K], B), st, cfg, drng)
+    for i in range(max(2, a.warmup // utd)):
+        A.sac_updates(A.DeviceRows(ring, width, idx_dev[i % K], B), st, cfg, drng, utd)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.nvtx.range_push("timed")
     e0.record(s)
     for i in range(K):
-        A.sac_update(A.DeviceRows(ring, width, idx_dev[i], B), st, cfg, drng)
+        A.sac_updates(A.DeviceRows(ring, width, idx_dev[i], B), st, cfg, drng, utd)
     e1.record(s)
     torch.cuda.nvtx.range_pop()
     e1.synchronize()
-    ms = e0.elapsed_time(e1) / K
+    ms = e0.elapsed_time(e1) / (K * utd)
     # e2e: host index vector (pinned) + host noise stream each update
     pin = [_dev.pinned_empty((B,), np.int64) for _ in range(2)]
     idx_buf = torch.empty(B, dtype=torch.int64, device="cuda")
@@ -104,7 +107,7 @@ def main():
         h = pin[i & 1]
         h[:] = host_rng.integers(0, RING, B)
         idx_buf.copy_(torch.from_numpy(h), non_blocking=True)
-        return A.sac_update(A.DeviceRows(ring, width, idx_buf, B), st, cfg, nrng)
+        return A.sac_updates(A.DeviceRows(ring, width, idx_buf, B), st, cfg, nrng, utd)[-1]
 
     for i in range(4):
         e2e_step(i)
@@ -113,14 +116,15 @@ def main():
     for i in range(K):
         out = e2e_step(i)
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / K
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / (K * utd)
     fl = ((PF - 1) * flops_per_update(False) + flops_per_update(True)) / PF
     res = {
         "workload": f"{a.cfg} {'FlashSAC' if a.cfg == 'cfg4' else 'FastSAC'} sac_update (ring 2^20 x "
                     f"RowCodec(96,23), batch {B}, critics 119-{'-'.join(map(str, CH))}-1"
                     f"{' +LN' if not a.no_ln else ''}, actor 96-{'-'.join(map(str, AH))}-23,"
                     f" policy_frequency {PF})",
-        "precision": a.precision, "updates": K,
+        "precision": a.precision, "updates": K * utd, "updates_per_tick": utd,
+        "graph": "one CUDA graph launch per tick (sac_updates)",
         "ms_per_update": ms, "updates_per_s": 1e3 / ms,
         "e2e_ms_per_update": e2e_ms, "e2e_updates_per_s": 1e3 / e2e_ms,
         "tflops_achieved": fl / (ms * 1e-3) / 1e12,
