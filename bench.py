@@ -464,6 +464,46 @@ def run_ours(args):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get("tc_gemm_dram_bytes_per_update")
+    # Which floor binds the MLP phase: tensor pipe (algorithmic FLOPs at the
+    # bf16 peak) or HBM (the DRAM bytes ncu measured for these launches at the
+    # measured copy bandwidth)?  The layer-by-layer schedule materialises every
+    # activation, so its HBM floor sits above the tensor floor.
+    flops = counts["gemm_flops_per_update"]
+    tensor_floor_ms = flops / (bf16_sus * 1e12) * 1e3
+    hbm_floor_ms = traffic / (hbm * 1e9) * 1e3 if traffic else 0.0
+    tensor_view = {"achieved": gemm_tflops, "peak": bf16_sus, "unit": "TFLOP/s",
+                   "frac": gemm_tflops / bf16_sus, "floor_ms": tensor_floor_ms,
+                   "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)"}
+    kernel_desc = ("MLP passes of one update: tcgen05 GEMMs (tc_gemm_kernel: grouped forward, "
+                   "ELU-gradient dX, one batched dW launch per step) + split-K reductions + the "
+                   "fused output stage (ppo_fused_mma_kernel); traffic = ncu DRAM bytes of the "
+                   "tc_gemm launches per update (profiles/ncu_traffic.json)")
+    if traffic and hbm_floor_ms > tensor_floor_ms:
+        gbs = traffic / (mlp_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": gbs / hbm, "traffic": traffic, "floor_ms": hbm_floor_ms,
+                    "tensor": tensor_view, "kernel": kernel_desc,
+                    "peak_source": f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)",
+                    "algorithmic_flops_per_update": flops, "phase_ms_per_update": prof}
+    else:
+        roofline = dict(tensor_view, bound="tensor", traffic=traffic, kernel=kernel_desc,
+                        algorithmic_flops_per_update=flops, phase_ms_per_update=prof,
+                        hbm_floor_ms=hbm_floor_ms)
+    # memory-bound kernels at sizes above L2 (tools/bench_kernels.py): GAE /
+    # V-trace scans, minibatch / replay gathers, Welford, Polyak, Adam
+    hbm_kernels = None
+    if rank == 0:
+        import importlib.util
+
+        spec = importlib.util.spec_from_file_location("bench_kernels",
+                                                      ROOT / "tools" / "bench_kernels.py")
+        bk = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(bk)
+        hbm_kernels = {k: {"gbs": v["gbs"], "frac": v["frac"]} for k, v in bk.run(hbm).items()}
+        hbm_kernels["peak_gbs"] = hbm
+        hbm_kernels["note"] = ("algorithmic bytes / CUDA-event time, back-to-back launches, "
+                               "inputs larger than L2; frac of the measured copy bandwidth")
+        torch.cuda.empty_cache()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -488,16 +528,8 @@ def run_ours(args):
                 "api": "algos.PpoPipeline.update_async (double-buffered pinned H2D ring, GAE on device, stats read one update behind), "
                        "pinned host segment",
                 "serial_gae_ppo_update_ms": serial_ms},
-        "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_sus,
-                     "unit": "TFLOP/s", "frac": gemm_tflops / bf16_sus, "traffic": traffic,
-                     "kernel": "MLP passes of one update: tcgen05 GEMMs (tc_gemm_kernel: grouped "
-                               "forward, ELU-gradient dX, one batched dW launch per step) + "
-                               "split-K reductions + the fused output stage (ppo_fused_kernel); "
-                               "traffic = ncu DRAM bytes of the tc_gemm launches per update "
-                               "(profiles/ncu_traffic.json)",
-                     "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
-                     "algorithmic_flops_per_update": counts["gemm_flops_per_update"],
-                     "phase_ms_per_update": prof},
+        "roofline": roofline,
+        "hbm_kernels": hbm_kernels,
         "clocks": smi.summary(),
         "gpu_launches": int((counts["kernels_per_update"] + 1) * args.steps),
     }

@@ -4,9 +4,10 @@
 from ..errors import PipelineStall
 from .learners import (AppoLearner, PpoLearner, SacLearner, build_ac_params, run_appo,
                        run_ppo_sync)
+from .sac_pipeline import SacPipeline, stream
 from .sync import (ErrorBox, HostAcParams, HostParams, RolloutRing, WeightSlot, fetch_weights,
                    publish_weights)
 
 __all__ = ["AppoLearner", "ErrorBox", "HostAcParams", "HostParams", "PipelineStall",
-           "PpoLearner", "RolloutRing", "SacLearner", "WeightSlot", "build_ac_params",
-           "fetch_weights", "publish_weights", "run_appo", "run_ppo_sync"]
+           "PpoLearner", "RolloutRing", "SacLearner", "SacPipeline", "WeightSlot", "build_ac_params",
+           "fetch_weights", "publish_weights", "run_appo", "run_ppo_sync", "stream"]

@@ -23,7 +23,7 @@ import threading
 import numpy as np
 
 from ..algos import (AcOpt, AcParams, adaptive_lr_step, appo_update, gae, ppo_update,
-                     sac_update)
+                     sac_updates)
 from ..tensornet import Arch, init_params
 from ..trace import Tracer, now_ns
 from .sync import ErrorBox, RolloutRing, WeightSlot
@@ -95,12 +95,14 @@ class SacLearner:
         self.consumed_samples = 0
 
     def tick(self, batch) -> dict:
+        """updates_per_step sac_updates on one batch as one CUDA-graph launch."""
         merged = {}
-        for _ in range(self.cfg.updates_per_step):
-            with self.tracer.span("learner", "learner/update"):
-                stats = sac_update(batch, self.state, self.cfg, self.rng)
-            self.consumed_samples += self.cfg.batch_size
-            merged.update(stats.extra)
+        with self.tracer.span("learner", "learner/update", updates=self.cfg.updates_per_step):
+            stats = sac_updates(batch, self.state, self.cfg, self.rng,
+                                self.cfg.updates_per_step)
+        self.consumed_samples += self.cfg.batch_size * self.cfg.updates_per_step
+        for s in stats:
+            merged.update(s.extra)
         self.slot.publish(self.state.params.actor)
         return merged
 

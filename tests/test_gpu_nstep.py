@@ -100,7 +100,8 @@ def test_return_std_normalizer_alone():
         bound = (1.0 - gamma) * g_max
         np.testing.assert_allclose(got, np.clip(r / (std + 1e-8), -bound, bound), rtol=1e-6,
                                    atol=1e-7)
-    assert nrm.count == count and nrm.std == pytest.approx(std, rel=1e-9)
+    # (the device merges each step's return statistics with Chan's formula)
+    assert nrm.count == count and nrm.std == pytest.approx(std, rel=1e-7)
 
 
 def test_collector_packers_match_reference_known_answers():
@@ -116,12 +117,12 @@ def test_collector_packers_match_reference_known_answers():
     rng = np.random.default_rng(5)
     for _ in range(50):
         out = norm.normalize(rng.normal(scale=3.0, size=2), np.zeros(2, bool))
-        assert np.all(np.abs(out) <= (1 - 0.97) * 5.0 + 1e-12)
+        assert np.all(np.abs(out) <= (1 - 0.97) * 5.0 + 1e-7)  # (f32 codec rows)
     packer = A.NStepPacker(n=1, gamma=0.97, n_envs=1)
     rows = A.nstep_and_reward_norm(packer, A.ReturnStdNormalizer(0.97, 5.0, 1), np.zeros((1, 2)),
                                  np.zeros((1, 1)), np.array([100.0]), np.ones((1, 2)),
                                  np.array([False]), np.array([False]))
-    assert len(rows) == 1 and abs(rows[0][2]) <= (1 - 0.97) * 5.0 + 1e-12
+    assert len(rows) == 1 and abs(rows[0][2]) <= (1 - 0.97) * 5.0 + 1e-7
 
 
 def test_device_nstep_rows_feed_sac_update():

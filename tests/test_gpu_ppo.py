@@ -546,3 +546,20 @@ def test_gpu_trace_spans_on_host_clock():
     ev = tr.events()
     assert [e.name for e in ev] == ["learner/update", "learner/replay_sample"]
     assert ev[0].duration_ns > 0 and ev[1].ts_start >= ev[0].ts_start
+
+
+def test_weight_slot_snapshot_never_mixes_versions():
+    """R:runtime/sync.py:40-54 'never a mix': an in-place parameter write queued
+    right behind a non-blocking publish must not leak into the snapshot (the
+    publish snapshots on the learner stream before the slow D2H)."""
+    from paper_2605_30313_b200 import runtime as RT
+
+    p = TN.init_params(TN.Arch(256, (1024, 1024), 64), 0)  # ~1.4M params
+    before = p.flat().copy()
+    slot = RT.WeightSlot()
+    for k in range(3):
+        slot.publish(p)
+        p.buf.add_(1.0)  # the next "update", in place, on the learner stream
+        v, snap = slot.fetch()
+        assert v == k + 1
+        np.testing.assert_array_equal(snap.flat(), before + k)

@@ -204,3 +204,24 @@ def test_pending_updates_drain_in_launch_order(monkeypatch):
     P._drain_pending()
     assert seen == ["a", "b", "c", "d"] and hs[3].result() == "d"
     assert opt.actor.t == 40 and all(h.plan.pending is None for h in hs)
+
+
+def test_product_adaptive_lr_step_known_answers():
+    """The product's adaptive_lr_step (host scalar logic on the learner thread)
+    against the reference test-suite's known answers (R:tests/test_ppo.py:
+    218-238; R:algos/ppo.py:232-250) and the oracle on a sweep."""
+    from oracle import port as O
+    from paper_2605_30313_b200.algos import PpoConfig, adaptive_lr_step
+
+    cfg = PpoConfig()
+    assert adaptive_lr_step(1e-3, 0.02, cfg, update_index=5) == pytest.approx(1e-3 / 1.2)
+    assert adaptive_lr_step(1e-3, 0.005, cfg, update_index=10) == pytest.approx(1.1e-3)
+    assert adaptive_lr_step(1e-3, 0.0095, cfg, 5) == 1e-3
+    assert adaptive_lr_step(1e-3, 0.02, cfg, update_index=3) == 1e-3
+    assert adaptive_lr_step(9.5e-3, 0.001, cfg, 5) == 1e-2
+    assert adaptive_lr_step(1.1e-6, 1.0, cfg, 5) == 1e-6
+    assert adaptive_lr_step(1e-3, 0.5, PpoConfig(schedule="fixed"), 5) == 1e-3
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        lr, kl, it = 10 ** rng.uniform(-6.5, -1.5), 10 ** rng.uniform(-4, 0), int(rng.integers(0, 20))
+        assert adaptive_lr_step(lr, kl, cfg, it) == O.adaptive_lr(lr, kl, it)
