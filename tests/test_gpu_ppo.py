@@ -555,11 +555,12 @@ def test_weight_slot_snapshot_never_mixes_versions():
     from paper_2605_30313_b200 import runtime as RT
 
     p = TN.init_params(TN.Arch(256, (1024, 1024), 64), 0)  # ~1.4M params
-    before = p.flat().copy()
+    want = p.flat().astype(np.float32)
     slot = RT.WeightSlot()
     for k in range(3):
         slot.publish(p)
         p.buf.add_(1.0)  # the next "update", in place, on the learner stream
         v, snap = slot.fetch()
         assert v == k + 1
-        np.testing.assert_array_equal(snap.flat(), before + k)
+        np.testing.assert_array_equal(snap.flat(), want)
+        want = want + np.float32(1.0)
