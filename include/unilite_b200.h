@@ -321,6 +321,12 @@ int ul_ppo_plan_bind(void* plan, const ul_ppo_bindings* b);
 /* upload lr / step counters, reset stats, advantage statistics */
 int ul_ppo_plan_begin(void* plan, double lr_actor, double lr_critic, int64_t t_actor,
                       int64_t t_critic, void* stream);
+/* Data-parallel "local" shards: this rank's raw advantage sums [sum A,
+ * sum A^2, n] after begin (3 doubles into dst), and the (mean, std) of the
+ * loss head from the all-reduced sums (normalize_advantages over the union
+ * of the ranks' rows, R:algos/ppo.py:132-133). */
+int ul_ppo_plan_adv_sums(void* plan, double* dst, void* stream);
+int ul_ppo_plan_adv_finalize(void* plan, const double* sums, void* stream);
 int ul_ppo_plan_step_grads(void* plan, int epoch, int k, void* stream);
 int ul_ppo_plan_step_apply(void* plan, int epoch, int k, void* stream);
 /* contiguous [actor grads | critic grads | 3 loss partials] buffer that a

@@ -44,6 +44,32 @@ def segment_mode() -> str:
     return _MODE["segment"]
 
 
+# Test hook: run the data-parallel step path (step_grads -> all-reduce ->
+# step_apply, NCCL in the graph) even in a 1-rank process group.
+_FORCE = {"dp": False}
+
+
+def force_dp(on: bool) -> None:
+    _FORCE["dp"] = bool(on)
+
+
+def dp_forced() -> bool:
+    return _FORCE["dp"]
+
+
+def dp_graph_enabled() -> bool:
+    """Capture the data-parallel update (20 x step_grads / NCCL all-reduce /
+    step_apply) in one CUDA graph (UL_DP_GRAPH=0 disables)."""
+    import os
+
+    import torch.distributed as dist
+
+    if os.environ.get("UL_DP_GRAPH", "1") == "0" or getattr(_LOCAL, "emu", None) is not None:
+        return False
+    # only NCCL collectives can be captured in a CUDA graph (gloo runs on the host)
+    return dist.is_available() and dist.is_initialized() and dist.get_backend() == "nccl"
+
+
 def world_info() -> tuple[int, int]:
     import torch.distributed as dist
 
@@ -83,5 +109,20 @@ def all_reduce_sum(t: torch.Tensor) -> None:
     if emu is not None:
         emu[2](t)
         return
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized() and (dist.get_world_size() > 1
+                                                           or _FORCE["dp"]):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+
+_BUFS64: dict = {}
+
+
+def sums_buffer(n: int = 3) -> torch.Tensor:
+    """A small float64 device buffer for all-reduced statistics."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    key = (n, str(dev), world_info()[1])
+    t = _BUFS64.get(key)
+    if t is None:
+        t = torch.zeros(n, dtype=torch.float64, device=dev)
+        _BUFS64[key] = t
+    return t

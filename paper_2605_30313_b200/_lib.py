@@ -176,6 +176,8 @@ _PROTOS = {
     "ul_ppo_plan_destroy": (C.c_int, [vp]),
     "ul_ppo_plan_bind": (C.c_int, [vp, C.POINTER(PpoBindings)]),
     "ul_ppo_plan_begin": (C.c_int, [vp, f64, f64, i64, i64, vp]),
+    "ul_ppo_plan_adv_sums": (C.c_int, [vp, vp, vp]),
+    "ul_ppo_plan_adv_finalize": (C.c_int, [vp, vp, vp]),
     "ul_ppo_plan_step_grads": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "ul_ppo_plan_step_apply": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "ul_ppo_plan_reduce_buffer": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),

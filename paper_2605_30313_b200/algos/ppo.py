@@ -131,7 +131,7 @@ def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
     # one plan (and CUDA graph) per staging slot: the pipeline alternates two
     key = (params.actor.arch, params.critic.arch, ds.rows, ds.ld, cfg.epochs, cfg.minibatches,
            cfg.clip_param, cfg.entropy_coef, cfg.value_loss_coef, cfg.use_clipped_value_loss,
-           cfg.max_grad_norm, world, rank, raw_adv, _dist.segment_mode(),
+           cfg.max_grad_norm, world, rank, raw_adv, _dist.segment_mode(), _dist.dp_forced(),
            _lib.gemm_backend(), torch.cuda.current_device(), getattr(ds, "slot", "ppo"))
     plan = _PLANS.get(key)
     if plan is None:
@@ -146,7 +146,7 @@ def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
         d.use_clipped_value_loss = int(cfg.use_clipped_value_loss)
         d.max_grad_norm = cfg.max_grad_norm
         d.world_size, d.rank, d.raw_advantages = world, rank, int(raw_adv)
-        d.local_shards = int(_dist.segment_mode() == "local" and world > 1)
+        d.local_shards = int(_dist.segment_mode() == "local" and _dp_path(world))
         d.gemm_backend = _lib.gemm_backend()
         plan = _Plan(d)
         _PLANS[key] = plan
@@ -236,22 +236,59 @@ def launch_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red,
                 prev: _Plan | None = None) -> None:
     """Enqueue one update (single GPU: one CUDA-graph launch, no host wait).
     prev: the plan of the update this one is chained behind on the device
-    (its step counters / divergence latch continue from prev's controller)."""
+    (its step counters / divergence latch continue from prev's controller).
+    Data-parallel (world > 1): the controller upload + advantage statistics
+    (all-reduced across "local" shards), then the 20 x (step_grads -> NCCL
+    all-reduce of the gradient buffer -> step_apply) sequence -- captured once
+    per bound plan as ONE CUDA graph with the NCCL all-reduces inside it."""
     s = _dev.stream()
     cfgd = plan.desc
-    if world == 1 and prev is not None:
+    if not _dp_path(world) and prev is not None:
         _lib.call("ul_ppo_plan_run_after", plan.h, prev.h, opt.actor.lr, opt.critic.lr, s)
-    elif world == 1:
+        return
+    if not _dp_path(world):
         _lib.call("ul_ppo_plan_run", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
                   opt.critic.t, 1, s)
-    else:
-        _lib.call("ul_ppo_plan_begin", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
-                  opt.critic.t, s)
+        return
+    _lib.call("ul_ppo_plan_begin", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
+              opt.critic.t, s)
+    if cfgd.local_shards and not cfgd.raw_advantages:
+        sums = _dist.sums_buffer(3)
+        _lib.call("ul_ppo_plan_adv_sums", plan.h, _dev.ptr(sums), s)
+        _dist.all_reduce_sum(sums)
+        _lib.call("ul_ppo_plan_adv_finalize", plan.h, _dev.ptr(sums), s)
+
+    def steps():
+        st = _dev.stream()
         for e in range(cfgd.epochs):
             for k in range(cfgd.minibatches):
-                _lib.call("ul_ppo_plan_step_grads", plan.h, e, k, s)
+                _lib.call("ul_ppo_plan_step_grads", plan.h, e, k, st)
                 _dist.all_reduce_sum(red)
-                _lib.call("ul_ppo_plan_step_apply", plan.h, e, k, s)
+                _lib.call("ul_ppo_plan_step_apply", plan.h, e, k, st)
+
+    if not _dist.dp_graph_enabled():
+        steps()
+        return
+    key = (plan._bind_key, _dev.ptr(red))
+    if getattr(plan, "dp_graph_key", None) != key:
+        # capture once per binding (the first update runs eagerly so NCCL's
+        # communicator and the plan's lazily built state exist before capture)
+        if getattr(plan, "dp_warm", None) != key:
+            plan.dp_warm = key
+            steps()
+            return
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=cs):
+            steps()
+        plan.dp_graph, plan.dp_graph_key = g, key
+    plan.dp_graph.replay()
+
+
+def _dp_path(world: int) -> bool:
+    return world > 1 or _dist.dp_forced()
 
 
 def finish_plan(plan: _Plan, opt: AcOpt) -> _lib.PpoResult:
@@ -274,12 +311,12 @@ def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False, pre
     world, rank = _world()
     plan = _plan_for(params, cfg, ds, world, rank, raw_adv)
     host_rng = rng is not None and not isinstance(rng, DeviceRng)
-    if prev is None or world != 1 or host_rng:
+    if prev is None or _dp_path(world) or host_rng:
         _drain_pending()  # the launch reads the host step counters
         prev = None
     elif plan.pending is not None:
         _drain_pending(upto=plan.pending)  # its result records are about to be reused
-    if world == 1 and host_rng:
+    if not _dp_path(world) and host_rng:
         # parity mode: one graph per epoch, so the host draws the reference
         # stream's permutation for epoch e + 1 while epoch e runs
         plan.bind(ds, adv, ret, oldv, params, opt, None)
@@ -287,7 +324,7 @@ def _launch_epochs(ds, adv, ret, oldv, params, opt, cfg, rng, raw_adv=False, pre
         return plan
     fill_permutations(ds, rng, cfg.epochs)
     red = None
-    if world > 1:
+    if _dp_path(world):
         red = _dist.reduce_buffer(plan.red_len)
     plan.bind(ds, adv, ret, oldv, params, opt, red)
     launch_plan(plan, params, opt, world, red, prev)
@@ -544,10 +581,10 @@ class PpoPipeline:
         cur.wait_event(self.ready[k])
         gae_into(ds, self.cfg.gamma, self.cfg.lam)
         world, _ = _world()
-        if world > 1 and next_segment is not None:
+        if _dp_path(world) and next_segment is not None:
             self.prefetch(next_segment)  # host-driven DP steps: stage first
             next_segment = None
-        chain = world == 1 and (self.rng is None or isinstance(self.rng, DeviceRng))
+        chain = not _dp_path(world) and (self.rng is None or isinstance(self.rng, DeviceRng))
         prev = self._prev if chain and self._chain_ok() else None
         plan = _launch_epochs(ds, ds.adv, ds.ret, ds.values, self.params, self.opt, self.cfg,
                               self.rng, prev=prev)

@@ -168,7 +168,23 @@ __global__ void __launch_bounds__(256) adv_stats_kernel(const float* __restrict_
     out[1] = sqrt(var);
     // NaN advantages -> NaN stats -> non-finite loss -> DivergenceError (reference test)
     if (!isfinite(t1) || !isfinite(t2)) out[0] = out[1] = NAN;
+    // raw sums for a cross-rank combination (ul_ppo_plan_adv_sums)
+    const double nn = (double)n;
+    out[2] = t1 + nn * c;
+    out[3] = t2 + 2.0 * c * t1 + nn * c * c;
+    out[4] = nn;
   }
+}
+
+// (mean, population std) from all-reduced [sum A, sum A^2, n]
+__global__ void adv_finalize_kernel(const double* __restrict__ sums, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double n = sums[2], m = sums[0] / n;
+  double var = sums[1] / n - m * m;
+  var = var < 0.0 ? 0.0 : var;
+  out[0] = m;
+  out[1] = sqrt(var);
+  if (!isfinite(sums[0]) || !isfinite(sums[1])) out[0] = out[1] = NAN;
 }
 
 // per-step loss finalisation after the (optional) all-reduce of the partials
@@ -229,6 +245,11 @@ int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ti
   blocks = blocks < 1 ? 1 : (blocks > kAdvStatBlocks ? kAdvStatBlocks : blocks);
   adv_stats_kernel<<<blocks, 256, 0, s>>>(adv, n, part, ticket, out);
   return check_launch("adv_stats_kernel");
+}
+
+int launch_adv_finalize(const double* sums, double* out, cudaStream_t s) {
+  adv_finalize_kernel<<<1, 32, 0, s>>>(sums, out);
+  return check_launch("adv_finalize_kernel");
 }
 
 int launch_ppo_loss_finalize(const float* loss, const float* log_std, int A, double n,

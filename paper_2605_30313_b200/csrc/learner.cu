@@ -105,7 +105,7 @@ int alloc_plan(PpoPlan* p) {
   const size_t o_workc = carve(sizeof(float) * wc);
   const size_t o_red = carve(sizeof(float) * (p->Pa + p->Pc + 4));
   const size_t o_hp = carve(sizeof(double) * ppo_head_partial_doubles(ml, p->A));
-  const size_t o_as = carve(sizeof(double) * 4);
+  const size_t o_as = carve(sizeof(double) * 8);  // mean, std, S1, S2, n
   const size_t o_ap = carve(sizeof(double) * 2 * kAdvStatBlocks);
   const size_t o_tk = carve(sizeof(unsigned int) * 8);
   const size_t o_ctl = carve(sizeof(ul_opt_ctl));
@@ -677,6 +677,26 @@ extern "C" int ul_ppo_plan_begin(void* plan, double lr_actor, double lr_critic, 
   cudaStream_t s = ul::as_stream(stream);
   UL_TRY(ul::upload_ctl(p, lr_actor, lr_critic, t_actor, t_critic, s));
   return ul::begin_device(p, s);
+}
+
+// Global advantage statistics across data-parallel ranks that own different
+// rows ("local" shards, weak scaling): the begin step leaves this rank's raw
+// sums [sum A, sum A^2, n] behind; the caller all-reduces them and finalize
+// turns the global sums into the (mean, population std) the loss head reads
+// -- normalize_advantages over the union of the ranks' segments
+// (R:algos/ppo.py:132-133, :156).
+extern "C" int ul_ppo_plan_adv_sums(void* plan, double* dst, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && dst, "ppo plan: null argument");
+  UL_CUDA(cudaMemcpyAsync(dst, p->adv_stats + 2, 3 * sizeof(double), cudaMemcpyDeviceToDevice,
+                          ul::as_stream(stream)));
+  return UL_OK;
+}
+
+extern "C" int ul_ppo_plan_adv_finalize(void* plan, const double* sums, void* stream) {
+  PpoPlan* p = (PpoPlan*)plan;
+  UL_CHECK_ARG(p && sums, "ppo plan: null argument");
+  return ul::launch_adv_finalize(sums, p->adv_stats, ul::as_stream(stream));
 }
 
 extern "C" int ul_ppo_plan_step_grads(void* plan, int epoch, int k, void* stream) {

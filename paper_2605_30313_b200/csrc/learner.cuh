@@ -78,6 +78,7 @@ int launch_ppo_fused(const PpoFusedArgs& f, int dtype, ReduceJob* jobs, int* njo
 int ppo_head_partial_doubles(int64_t n_local, int A);
 int launch_adv_stats(const float* adv, int64_t n, double* part, unsigned int* ticket, double* out,
                      cudaStream_t s);
+int launch_adv_finalize(const double* sums, double* out, cudaStream_t s);
 int launch_ppo_loss_finalize(const float* loss, const float* log_std, int A, double n,
                              double vcoef, double ecoef, int last_in_epoch, ul_opt_ctl* ctl,
                              ul_ppo_stats* st, cudaStream_t s);
