@@ -245,7 +245,8 @@ constexpr int kPThreads = (2 + kEpiWarps) * 32;
 
 // bf16 operands -> bf16 hidden activations / gradients; everything else fp32
 template <typename TI, int EPI>
-using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu || EPI == kEpiEluGrad),
+using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu || EPI == kEpiEluGrad ||
+                                                            EPI == kEpiBiasLn),
                                        __nv_bfloat16, float>::type;
 
 // [stage ring][16 epilogue staging boxes][barriers][bias x 2]; as many stages
@@ -261,7 +262,8 @@ struct Smem {
   // box's TMA store reads one while the next box fills the other)
   // (bf16 bias/ELU outputs: one box per warp, single-buffered -- its TMA
   // store has a whole tile to read it -- which buys the 4th stage)
-  static constexpr int kNStg = (OB == 2 && (EPI == kEpiBias || EPI == kEpiBiasElu)) ? 1 : 2;
+  static constexpr int kNStg =
+      (OB == 2 && (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn)) ? 1 : 2;
   static constexpr int kStagingBytes = kEpiWarps * kNStg * 32 * 64;
   // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
   static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
@@ -631,7 +633,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         bnext[j] = n < p.N ? __ldg(p.bias + n) : 0.f;
       }
     };
-    if (EPI == kEpiBias || EPI == kEpiBiasElu) load_bias(cl);
+    if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn) load_bias(cl);
     // diagnostics: epilogue warp 0, tiles 0-1, boxes 0-3 -> trace slots 100..
 #define UL_ETRACE(k) \
   if (ew == 0 && lane == 0 && local < 2 && cj < 4) trace_at(p0_.trace, 100 + cj * 6 + (k))
@@ -643,7 +645,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const CUtensorMap* tX = &B.m[T.pr].x;
       const int b = local & 1;
       const bool have = T.kt_n > 0;
-      if (EPI == kEpiBias || EPI == kEpiBiasElu) {
+      if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn) {
 #pragma unroll
         for (int j = 0; j < kBiasPer; ++j) sbias[b * BN + slice * kSlice + j * 32 + lane] = bnext[j];
         __syncwarp();
@@ -702,7 +704,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
           }
           if (h == 0) UL_ETRACE(1);
-          if (EPI == kEpiBias || EPI == kEpiBiasElu) {
+          if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn) {
             const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + cc);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -1120,7 +1122,8 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   }
   const bool pair = (want && all_two_m) || (dw_batch && pair_dw && pair_ok != 0) ||
                     (all_two_m && pair_dx && d.epi == kEpiEluGrad) ||
-                    (all_two_m && pair_fwd && (d.epi == kEpiBiasElu || d.epi == kEpiBias));
+                    (all_two_m && pair_fwd && (d.epi == kEpiBiasElu || d.epi == kEpiBias ||
+                                               d.epi == kEpiBiasLn));
   // B resident (A streamed alone) when one problem's whole N tile of B fits
   // the smem left over by the 3-stage A ring, and there is no split-K
   static int bres_ok = -1;
@@ -1146,6 +1149,7 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
     UL_TC_BN(AMN, BMN, EPI, 128)                  \
   }
   UL_TC_CASE(false, false, kEpiBias)
+  UL_TC_CASE(false, false, kEpiBiasLn)
   UL_TC_CASE(false, false, kEpiBiasElu)
   UL_TC_CASE(false, false, kEpiStore)
   UL_TC_CASE(false, true, kEpiEluGrad)
@@ -1163,7 +1167,8 @@ int tc_bk(int dtype) { return dtype == kBf16 ? tc::Op<__nv_bfloat16>::BK : tc::O
 
 bool tc_eligible(const GemmDesc& d) {
   const int eb = d.dtype == kBf16 ? 2 : 4;
-  const int ob = (d.dtype == kBf16 && (d.epi == kEpiBiasElu || d.epi == kEpiEluGrad)) ? 2 : 4;
+  const int ob = (d.dtype == kBf16 && (d.epi == kEpiBiasElu || d.epi == kEpiEluGrad ||
+                                       d.epi == kEpiBiasLn)) ? 2 : 4;
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   // bf16 runs every hidden GEMM on the tensor cores (TMA zero-fills partial
   // tiles); tf32 keeps tiny shapes on the SIMT kernel

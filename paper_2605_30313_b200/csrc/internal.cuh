@@ -47,6 +47,7 @@ enum Epilogue : int {
   kEpiBias = 1,      // C = acc + bias[n]
   kEpiBiasElu = 2,   // C = elu(acc + bias[n])
   kEpiEluGrad = 3,   // C = acc * (min(aux[m,n],0)+1)
+  kEpiBiasLn = 4,    // C = acc + bias[n] as bf16 rows (a LayerNorm layer's pre-LN activation)
 };
 
 // operand storage of a GEMM / activation buffer
@@ -145,12 +146,14 @@ struct NetView {
   int64_t g_off[UL_MAX_LAYERS], beta_off[UL_MAX_LAYERS];
 };
 // LayerNorm rows (ln.cu): a [M, D] fp32 (GEMM output) -> h (dtype) = elu(LN(a) g + beta)
-int ln_forward(const float* a, int64_t lda, int64_t M, int D, const float* g, const float* beta,
-               float* stats, void* h, int64_t ldh, int ones_col, int dtype, cudaStream_t s);
+// a: pre-LN rows, fp32 or (a_bf16) bf16 (the bf16 GEMM's kEpiBiasLn output)
+int ln_forward(const void* a, int64_t lda, int64_t M, int D, const float* g, const float* beta,
+               float* stats, void* h, int64_t ldh, int ones_col, int dtype, cudaStream_t s,
+               bool a_bf16 = false);
 // dn -> da in place; partial sums of dg | dbeta | colsum(da) described by *job
-int ln_backward(void* dn, int64_t ldd, const float* a, int64_t lda, const float* stats,
+int ln_backward(void* dn, int64_t ldd, const void* a, int64_t lda, const float* stats,
                 const float* g, int64_t M, int D, float* part, int dtype, float* gg, float* gbeta,
-                float* gb, ReduceJob* job, cudaStream_t s);
+                float* gb, ReduceJob* job, cudaStream_t s, bool a_bf16 = false);
 int ln_part_floats(int64_t M, int D);
 // pre-LayerNorm rows a_i [M, round_up(D,4)] fp32 and stats [M][2] of hidden layer i
 void ln_bufs(const NetView& v, const float* acts, int64_t M, int i, float** a, int64_t* lda,
@@ -168,6 +171,9 @@ int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t
 // gradients are bf16 (rows of act_ld(d, kBf16)), params / grads / outputs fp32
 inline int backend_dtype(int backend) { return backend == 2 ? kBf16 : kF32; }
 int stage_weights_dt(const NetView& v, const float* params, void* wp, int dtype, cudaStream_t s);
+// n networks' staged rows in one launch
+int stage_weights_multi(int n, const NetView* const* v, const float* const* params,
+                        void* const* wp, int dtype, cudaStream_t s);
 
 // ------------------------------------------------------------------ gather
 // ul_gather_rows with an optional per-desc fp32 -> bf16 conversion (cvt)

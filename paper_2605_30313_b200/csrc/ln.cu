@@ -49,8 +49,8 @@ __device__ __forceinline__ void st1<__nv_bfloat16>(__nv_bfloat16* p, float v) {
   *p = __float2bfloat16_rn(v);
 }
 
-template <typename TO>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ a, int64_t lda,
+template <typename TA, typename TO>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const TA* __restrict__ a, int64_t lda,
                                                      int64_t M, int D, const float* __restrict__ g,
                                                      const float* __restrict__ beta,
                                                      float* __restrict__ stats, TO* __restrict__ h,
@@ -60,19 +60,19 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ a
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < M; r += nw) {
-    const float* ar = a + r * lda;
+    const TA* ar = a + r * lda;
     float s = 0.f;
-    for (int c = lane; c < D; c += 32) s += ar[c];
+    for (int c = lane; c < D; c += 32) s += ld1<TA>(ar + c);
     const float mean = warp_sum(s) / D;
     float q = 0.f;
     for (int c = lane; c < D; c += 32) {
-      const float d = ar[c] - mean;
+      const float d = ld1<TA>(ar + c) - mean;
       q += d * d;
     }
     const float rstd = rsqrtf(warp_sum(q) / D + kLnEps);
     TO* hr = h + r * ldh;
     for (int c = lane; c < D; c += 32) {
-      const float n = (ar[c] - mean) * rstd * g[c] + beta[c];
+      const float n = (ld1<TA>(ar + c) - mean) * rstd * g[c] + beta[c];
       st1<TO>(hr + c, elu_f(n));
     }
     if (lane == 0) {
@@ -84,9 +84,9 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ a
 }
 
 // part: [gridDim.x][3][D] = dg | dbeta | colsum(da)
-template <typename TD>
+template <typename TA, typename TD>
 __global__ void __launch_bounds__(kLnWarps * 32) ln_bwd_kernel(
-    TD* __restrict__ dn, int64_t ldd, const float* __restrict__ a, int64_t lda,
+    TD* __restrict__ dn, int64_t ldd, const TA* __restrict__ a, int64_t lda,
     const float* __restrict__ stats, const float* __restrict__ g, int64_t M, int D,
     float* __restrict__ part) {
   extern __shared__ float acc[];  // [kLnWarps][3][D]
@@ -99,18 +99,18 @@ __global__ void __launch_bounds__(kLnWarps * 32) ln_bwd_kernel(
   const int64_t nw = (int64_t)gridDim.x * kLnWarps;
   for (int64_t r = (int64_t)blockIdx.x * kLnWarps + w; r < M; r += nw) {
     TD* dr = dn + r * ldd;
-    const float* ar = a + r * lda;
+    const TA* ar = a + r * lda;
     const float mean = stats[2 * r], rstd = stats[2 * r + 1];
     float s1 = 0.f, s2 = 0.f;
     for (int c = lane; c < D; c += 32) {
-      const float xh = (ar[c] - mean) * rstd;
+      const float xh = (ld1<TA>(ar + c) - mean) * rstd;
       const float dx = ld1<TD>(dr + c) * g[c];
       s1 += dx;
       s2 += dx * xh;
     }
     const float m1 = warp_sum(s1) / D, m2 = warp_sum(s2) / D;
     for (int c = lane; c < D; c += 32) {
-      const float xh = (ar[c] - mean) * rstd;
+      const float xh = (ld1<TA>(ar + c) - mean) * rstd;
       const float dnv = ld1<TD>(dr + c);
       const float da = rstd * (dnv * g[c] - m1 - xh * m2);
       st1<TD>(dr + c, da);
@@ -161,9 +161,9 @@ struct V4<__nv_bfloat16> {
 
 constexpr int kRegWarps = 8;
 
-template <int NV, typename TO>
+template <int NV, typename TA, typename TO>
 __global__ void __launch_bounds__(kRegWarps * 32) ln_fwd_reg(
-    const float* __restrict__ a, int64_t lda, int64_t M, int D, const float* __restrict__ g,
+    const TA* __restrict__ a, int64_t lda, int64_t M, int D, const float* __restrict__ g,
     const float* __restrict__ beta, float* __restrict__ stats, TO* __restrict__ h, int64_t ldh,
     int ones_col) {
   pdl_trigger();
@@ -179,13 +179,13 @@ __global__ void __launch_bounds__(kRegWarps * 32) ln_fwd_reg(
   }
   const float inv_d = 1.f / D;
   for (int64_t r = (int64_t)blockIdx.x * kRegWarps + (threadIdx.x >> 5); r < M; r += nw) {
-    const float* ar = a + r * lda;
+    const TA* ar = a + r * lda;
     float4 x[NV];
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = 4 * lane + 128 * j;
-      x[j] = c < D ? V4<float>::ld(ar + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[j] = c < D ? V4<TA>::ld(ar + c) : make_float4(0.f, 0.f, 0.f, 0.f);
       s += (x[j].x + x[j].y) + (x[j].z + x[j].w);
     }
     const float mean = warp_sum(s) * inv_d;
@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(kRegWarps * 32) ln_fwd_reg(
 }
 
 // part: [gridDim.x][3][D] = dg | dbeta | colsum(da); smem [3][D]
-template <int NV, typename TD>
+template <int NV, typename TA, typename TD>
 __global__ void __launch_bounds__(kRegWarps * 32, 1) ln_bwd_reg(
-    TD* __restrict__ dn, int64_t ldd, const float* __restrict__ a, int64_t lda,
+    TD* __restrict__ dn, int64_t ldd, const TA* __restrict__ a, int64_t lda,
     const float* __restrict__ stats, const float* __restrict__ g, int64_t M, int D,
     float* __restrict__ part) {
   extern __shared__ float4 red4[];
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) ln_bwd_reg(
   const int64_t nw = (int64_t)gridDim.x * kRegWarps;
   for (int64_t r = (int64_t)blockIdx.x * kRegWarps + w; r < M; r += nw) {
     TD* dr = dn + r * ldd;
-    const float* ar = a + r * lda;
+    const TA* ar = a + r * lda;
     const float2 st = reinterpret_cast<const float2*>(stats)[r];
     float4 xh[NV], dv[NV];
     float s1 = 0.f, s2 = 0.f;
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) ln_bwd_reg(
     for (int j = 0; j < NV; ++j) {
       const int c = 4 * lane + 128 * j;
       if (c < D) {
-        const float4 x = V4<float>::ld(ar + c);
+        const float4 x = V4<TA>::ld(ar + c);
         dv[j] = V4<TD>::ld(dr + c);
         xh[j] = make_float4((x.x - st.x) * st.y, (x.y - st.x) * st.y, (x.z - st.x) * st.y,
                             (x.w - st.x) * st.y);
@@ -318,6 +318,168 @@ __global__ void __launch_bounds__(kRegWarps * 32, 1) ln_bwd_reg(
   for (int c = threadIdx.x; c < 3 * D4; c += blockDim.x) pz[c] = red4[c];
 }
 
+// ---- two-kernel backward (any D % 4 == 0): rows first, then columns.
+// K1 (warp per row, streaming, no row-sized register arrays): the two row
+// means of the LN backward, m1 = mean(dn g), m2 = mean(dn g xh) -> rs[M].
+// K2 (column-parallel: a thread owns 4 adjacent columns, a block a chunk of
+// rows): da = rstd (dn g - m1 - xh m2) written over dn, and the column sums
+// dg = sum dn xh, dbeta = sum dn, colsum(da) accumulated in registers over
+// the chunk -> block partials [chunk][3][D] (the ReduceJob layout).  Two
+// coalesced reads of a and dn, one write of da, full occupancy: the row-
+// register kernel held 3 x D column accumulators per warp and ran one
+// 8-warp block per SM.
+template <typename TA, typename TD>
+__global__ void __launch_bounds__(256) ln_bwd_rows(const TD* __restrict__ dn, int64_t ldd,
+                                                   const TA* __restrict__ a, int64_t lda,
+                                                   const float* __restrict__ stats,
+                                                   const float* __restrict__ g, int64_t M, int D,
+                                                   float2* __restrict__ rs) {
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const float inv_d = 1.f / D;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < M; r += nw) {
+    const TD* dr = dn + r * ldd;
+    const TA* ar = a + r * lda;
+    const float2 st = reinterpret_cast<const float2*>(stats)[r];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = 4 * lane; c < D; c += 128) {
+      const float4 x = V4<TA>::ld(ar + c), d = V4<TD>::ld(dr + c), gv = V4<float>::ld(g + c);
+      const float e0 = d.x * gv.x, e1 = d.y * gv.y, e2 = d.z * gv.z, e3 = d.w * gv.w;
+      s1 += (e0 + e1) + (e2 + e3);
+      s2 += (e0 * (x.x - st.x) + e1 * (x.y - st.x)) + (e2 * (x.z - st.x) + e3 * (x.w - st.x));
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) rs[r] = make_float2(s1 * inv_d, s2 * st.y * inv_d);
+  }
+}
+
+template <typename TA, typename TD>
+__global__ void __launch_bounds__(256) ln_bwd_cols(TD* __restrict__ dn, int64_t ldd,
+                                                   const TA* __restrict__ a, int64_t lda,
+                                                   const float* __restrict__ stats,
+                                                   const float2* __restrict__ rs,
+                                                   const float* __restrict__ g, int64_t M, int D,
+                                                   int64_t rows_per, float* __restrict__ part) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int U = 4;  // rows in flight per thread (all loads issued before the math)
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
+  float* pz = part + (int64_t)blockIdx.x * 3 * D;
+  for (int c = 4 * threadIdx.x; c < D; c += 4 * blockDim.x) {
+    const float4 gv = V4<float>::ld(g + c);
+    float4 ag = make_float4(0.f, 0.f, 0.f, 0.f), ab = ag, aa = ag;
+    for (int64_t rb = r0; rb < r1; rb += U) {
+      float4 x[U], d[U];
+      float2 st[U], m[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = rb + u < r1 ? rb + u : r1 - 1;
+        st[u] = reinterpret_cast<const float2*>(stats)[r];
+        m[u] = rs[r];
+        x[u] = V4<TA>::ld(a + r * lda + c);
+        d[u] = V4<TD>::ld(dn + r * ldd + c);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (rb + u >= r1) break;
+        const float4 xh = make_float4((x[u].x - st[u].x) * st[u].y, (x[u].y - st[u].x) * st[u].y,
+                                      (x[u].z - st[u].x) * st[u].y, (x[u].w - st[u].x) * st[u].y);
+        const float4 dv = d[u];
+        const float4 da = make_float4(st[u].y * (dv.x * gv.x - m[u].x - xh.x * m[u].y),
+                                      st[u].y * (dv.y * gv.y - m[u].x - xh.y * m[u].y),
+                                      st[u].y * (dv.z * gv.z - m[u].x - xh.z * m[u].y),
+                                      st[u].y * (dv.w * gv.w - m[u].x - xh.w * m[u].y));
+        V4<TD>::st(dn + (rb + u) * ldd + c, da);
+        ag.x += dv.x * xh.x; ag.y += dv.y * xh.y; ag.z += dv.z * xh.z; ag.w += dv.w * xh.w;
+        ab.x += dv.x; ab.y += dv.y; ab.z += dv.z; ab.w += dv.w;
+        aa.x += da.x; aa.y += da.y; aa.z += da.z; aa.w += da.w;
+      }
+    }
+    V4<float>::st(pz + c, ag);
+    V4<float>::st(pz + D + c, ab);
+    V4<float>::st(pz + 2 * D + c, aa);
+  }
+}
+
+// ---- two-kernel forward: K1 row statistics (warp per row, streaming, the
+// centred variance from a second sweep that hits L1), K2 column-parallel
+// normalise + gain / shift + ELU (a thread owns 4 columns, 4 rows in flight).
+template <typename TA>
+__global__ void __launch_bounds__(256) ln_fwd_rows(const TA* __restrict__ a, int64_t lda,
+                                                   int64_t M, int D, float* __restrict__ stats) {
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const float inv_d = 1.f / D;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < M; r += nw) {
+    const TA* ar = a + r * lda;
+    float s = 0.f;
+    for (int c = 4 * lane; c < D; c += 128) {
+      const float4 x = V4<TA>::ld(ar + c);
+      s += (x.x + x.y) + (x.z + x.w);
+    }
+    const float mean = warp_sum(s) * inv_d;
+    float q = 0.f;
+    for (int c = 4 * lane; c < D; c += 128) {
+      const float4 x = V4<TA>::ld(ar + c);
+      const float d0 = x.x - mean, d1 = x.y - mean, d2 = x.z - mean, d3 = x.w - mean;
+      q += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    }
+    const float rstd = rsqrtf(warp_sum(q) * inv_d + kLnEps);
+    if (lane == 0) reinterpret_cast<float2*>(stats)[r] = make_float2(mean, rstd);
+  }
+}
+
+template <typename TA, typename TO>
+__global__ void __launch_bounds__(256) ln_fwd_cols(const TA* __restrict__ a, int64_t lda,
+                                                   int64_t M, int D, const float* __restrict__ g,
+                                                   const float* __restrict__ beta,
+                                                   const float* __restrict__ stats,
+                                                   TO* __restrict__ h, int64_t ldh, int ones_col,
+                                                   int64_t rows_per) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int U = 4;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
+  for (int c = 4 * threadIdx.x; c < D; c += 4 * blockDim.x) {
+    const float4 gv = V4<float>::ld(g + c), bv = V4<float>::ld(beta + c);
+    for (int64_t rb = r0; rb < r1; rb += U) {
+      float4 x[U];
+      float2 st[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = rb + u < r1 ? rb + u : r1 - 1;
+        st[u] = reinterpret_cast<const float2*>(stats)[r];
+        x[u] = V4<TA>::ld(a + r * lda + c);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (rb + u >= r1) break;
+        float4 o;
+        o.x = elu_f((x[u].x - st[u].x) * st[u].y * gv.x + bv.x);
+        o.y = elu_f((x[u].y - st[u].x) * st[u].y * gv.y + bv.y);
+        o.z = elu_f((x[u].z - st[u].x) * st[u].y * gv.z + bv.z);
+        o.w = elu_f((x[u].w - st[u].x) * st[u].y * gv.w + bv.w);
+        V4<TO>::st(h + (rb + u) * ldh + c, o);
+      }
+    }
+  }
+  if (ones_col >= 0 && threadIdx.x == 0)
+    for (int64_t r = r0; r < r1; ++r) st1<TO>(h + r * ldh + ones_col, 1.f);
+}
+
+// row chunks of the column-parallel backward (<= its partial capacity)
+int ln_col_chunks(int64_t M) {
+  const int64_t b = ceil_div(M, 16);
+  return (int)(b > 4 * kNumSMs ? 4 * kNumSMs : (b < 1 ? 1 : b));
+}
+
 int ln_blocks(int64_t M) {
   int64_t b = ceil_div(M, kLnWarps * 8);
   return (int)(b > 2 * kNumSMs ? 2 * kNumSMs : (b < 1 ? 1 : b));
@@ -325,7 +487,12 @@ int ln_blocks(int64_t M) {
 
 }  // namespace
 
-int ln_part_floats(int64_t M, int D) { return ln_blocks(M) * 3 * ceil_div(D, 4) * 4; }
+// block partials [ln_blocks][3][D] + the two-kernel backward's per-row
+// (m1, m2) scratch [M] (8-byte aligned: the partial block is a multiple of 4 floats)
+int ln_part_floats(int64_t M, int D) {
+  const int64_t nb = ln_blocks(M) > ln_col_chunks(M) ? ln_blocks(M) : ln_col_chunks(M);
+  return (int)(nb * 3 * ceil_div(D, 4) * 4 + 2 * M);
+}
 
 namespace {
 bool al(const void* p, int bytes) { return ((uintptr_t)p & (bytes - 1)) == 0; }
@@ -334,111 +501,208 @@ int reg_nv(int D) {
   return D <= 128 ? 1 : D <= 256 ? 2 : D <= 512 ? 4 : 8;
 }
 
-template <typename TO>
-int fwd_reg(int nv, unsigned blocks, const float* a, int64_t lda, int64_t M, int D, const float* g,
+template <typename TA, typename TO>
+int fwd_reg(int nv, unsigned blocks, const TA* a, int64_t lda, int64_t M, int D, const float* g,
             const float* beta, float* stats, TO* h, int64_t ldh, int ones_col, cudaStream_t s) {
   const dim3 gr(blocks), bl(kRegWarps * 32);
   switch (nv) {
     case 1:
-      return launch_pdl("ln_fwd_reg", ln_fwd_reg<1, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
+      return launch_pdl("ln_fwd_reg", ln_fwd_reg<1, TA, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
                         stats, h, ldh, ones_col);
     case 2:
-      return launch_pdl("ln_fwd_reg", ln_fwd_reg<2, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
+      return launch_pdl("ln_fwd_reg", ln_fwd_reg<2, TA, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
                         stats, h, ldh, ones_col);
     case 4:
-      return launch_pdl("ln_fwd_reg", ln_fwd_reg<4, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
+      return launch_pdl("ln_fwd_reg", ln_fwd_reg<4, TA, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
                         stats, h, ldh, ones_col);
     default:
-      return launch_pdl("ln_fwd_reg", ln_fwd_reg<8, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
+      return launch_pdl("ln_fwd_reg", ln_fwd_reg<8, TA, TO>, gr, bl, 0, s, a, lda, M, D, g, beta,
                         stats, h, ldh, ones_col);
   }
 }
 
-template <typename TD>
-int bwd_reg(int nv, unsigned blocks, TD* dn, int64_t ldd, const float* a, int64_t lda,
+template <typename TA, typename TD>
+int bwd_reg(int nv, unsigned blocks, TD* dn, int64_t ldd, const TA* a, int64_t lda,
             const float* stats, const float* g, int64_t M, int D, float* part, cudaStream_t s) {
   const dim3 gr(blocks), bl(kRegWarps * 32);
   const size_t sm = (size_t)3 * D * sizeof(float);
   switch (nv) {
     case 1:
-      return launch_pdl("ln_bwd_reg", ln_bwd_reg<1, TD>, gr, bl, sm, s, dn, ldd, a, lda, stats, g,
-                        M, D, part);
+      return launch_pdl("ln_bwd_reg", ln_bwd_reg<1, TA, TD>, gr, bl, sm, s, dn, ldd, a, lda,
+                        stats, g, M, D, part);
     case 2:
-      return launch_pdl("ln_bwd_reg", ln_bwd_reg<2, TD>, gr, bl, sm, s, dn, ldd, a, lda, stats, g,
-                        M, D, part);
+      return launch_pdl("ln_bwd_reg", ln_bwd_reg<2, TA, TD>, gr, bl, sm, s, dn, ldd, a, lda,
+                        stats, g, M, D, part);
     case 4:
-      return launch_pdl("ln_bwd_reg", ln_bwd_reg<4, TD>, gr, bl, sm, s, dn, ldd, a, lda, stats, g,
-                        M, D, part);
+      return launch_pdl("ln_bwd_reg", ln_bwd_reg<4, TA, TD>, gr, bl, sm, s, dn, ldd, a, lda,
+                        stats, g, M, D, part);
     default:
-      return launch_pdl("ln_bwd_reg", ln_bwd_reg<8, TD>, gr, bl, sm, s, dn, ldd, a, lda, stats, g,
-                        M, D, part);
+      return launch_pdl("ln_bwd_reg", ln_bwd_reg<8, TA, TD>, gr, bl, sm, s, dn, ldd, a, lda,
+                        stats, g, M, D, part);
   }
 }
 }  // namespace
 
-int ln_forward(const float* a, int64_t lda, int64_t M, int D, const float* g, const float* beta,
-               float* stats, void* h, int64_t ldh, int ones_col, int dtype, cudaStream_t s) {
+// forward: the row-register kernel measured faster in the SAC update than the
+// two-kernel version (cfg3 0.89 vs 0.95 ms / update); UL_LN_FWD_TWO_PASS=1
+// selects the latter
+static bool ln_fwd_two_pass() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_LN_FWD_TWO_PASS");
+    on = e ? atoi(e) != 0 : 0;
+  }
+  return on == 1;
+}
+
+static bool ln_two_pass() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_LN_TWO_PASS");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
+}
+
+// a: the pre-LN rows, fp32 or (a_bf16) bf16; h in dtype
+int ln_forward(const void* a, int64_t lda, int64_t M, int D, const float* g, const float* beta,
+               float* stats, void* h, int64_t ldh, int ones_col, int dtype, cudaStream_t s,
+               bool a_bf16) {
   if (M == 0) return UL_OK;
+  using BF = __nv_bfloat16;
   const int nv = reg_nv(D);
   const int hb = dtype == kBf16 ? 8 : 16;
-  if (nv && lda % 4 == 0 && ldh % 4 == 0 && al(a, 16) && al(g, 16) && al(beta, 16) &&
-      al(stats, 8) && al(h, hb)) {
+  if (ln_fwd_two_pass() && D % 4 == 0 && lda % 4 == 0 && ldh % 4 == 0 &&
+      al(a, a_bf16 ? 8 : 16) && al(g, 16) && al(beta, 16) && al(stats, 8) && al(h, hb)) {
+    int64_t b1 = ceil_div(M, 8);
+    b1 = b1 > 8 * kNumSMs ? 8 * kNumSMs : b1;
+    const int64_t rows_per = 16;
+    const int64_t nb = ceil_div(M, rows_per);
+    int64_t thr = ceil_div((int64_t)D / 4, 32) * 32;
+    thr = thr > 256 ? 256 : thr;
+    const dim3 g1((unsigned)b1), g2((unsigned)nb), bl1(256), bl2((unsigned)thr);
+#define UL_LNF(TA_, TO_)                                                                     \
+  do {                                                                                       \
+    UL_TRY(launch_pdl("ln_fwd_rows", ln_fwd_rows<TA_>, g1, bl1, 0, s, (const TA_*)a, lda, M, \
+                      D, stats));                                                           \
+    return launch_pdl("ln_fwd_cols", ln_fwd_cols<TA_, TO_>, g2, bl2, 0, s, (const TA_*)a,  \
+                      lda, M, D, g, beta, (const float*)stats, (TO_*)h, ldh, ones_col,       \
+                      rows_per);                                                            \
+  } while (0)
+    if (a_bf16 && dtype == kBf16) UL_LNF(BF, BF);
+    if (a_bf16) UL_LNF(BF, float);
+    if (dtype == kBf16) UL_LNF(float, BF);
+    UL_LNF(float, float);
+#undef UL_LNF
+  }
+  if (nv && lda % 4 == 0 && ldh % 4 == 0 && al(a, a_bf16 ? 8 : 16) && al(g, 16) &&
+      al(beta, 16) && al(stats, 8) && al(h, hb)) {
     int64_t blocks = ceil_div(M, kRegWarps);
     blocks = blocks > 4 * kNumSMs ? 4 * kNumSMs : blocks;
+    const unsigned nb = (unsigned)blocks;
+    if (a_bf16 && dtype == kBf16)
+      return fwd_reg(nv, nb, (const BF*)a, lda, M, D, g, beta, stats, (BF*)h, ldh, ones_col, s);
+    if (a_bf16)
+      return fwd_reg(nv, nb, (const BF*)a, lda, M, D, g, beta, stats, (float*)h, ldh, ones_col, s);
     if (dtype == kBf16)
-      return fwd_reg(nv, (unsigned)blocks, a, lda, M, D, g, beta, stats,
-                     reinterpret_cast<__nv_bfloat16*>(h), ldh, ones_col, s);
-    return fwd_reg(nv, (unsigned)blocks, a, lda, M, D, g, beta, stats, reinterpret_cast<float*>(h),
-                   ldh, ones_col, s);
+      return fwd_reg(nv, nb, (const float*)a, lda, M, D, g, beta, stats, (BF*)h, ldh, ones_col,
+                     s);
+    return fwd_reg(nv, nb, (const float*)a, lda, M, D, g, beta, stats, (float*)h, ldh, ones_col,
+                   s);
   }
   int64_t blocks = ceil_div(M, 8);
   blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : blocks;
+  const dim3 gr((unsigned)blocks), bl(256);
+  if (a_bf16 && dtype == kBf16)
+    return launch_pdl("ln_fwd_kernel", ln_fwd_kernel<BF, BF>, gr, bl, 0, s, (const BF*)a, lda, M,
+                      D, g, beta, stats, (BF*)h, ldh, ones_col);
+  if (a_bf16)
+    return launch_pdl("ln_fwd_kernel", ln_fwd_kernel<BF, float>, gr, bl, 0, s, (const BF*)a, lda,
+                      M, D, g, beta, stats, (float*)h, ldh, ones_col);
   if (dtype == kBf16)
-    return launch_pdl("ln_fwd_kernel", ln_fwd_kernel<__nv_bfloat16>, dim3((unsigned)blocks),
-                      dim3(256), 0, s, a, lda, M, D, g, beta, stats,
-                      reinterpret_cast<__nv_bfloat16*>(h), ldh, ones_col);
-  return launch_pdl("ln_fwd_kernel", ln_fwd_kernel<float>, dim3((unsigned)blocks), dim3(256), 0,
-                    s, a, lda, M, D, g, beta, stats, reinterpret_cast<float*>(h), ldh, ones_col);
+    return launch_pdl("ln_fwd_kernel", ln_fwd_kernel<float, BF>, gr, bl, 0, s, (const float*)a,
+                      lda, M, D, g, beta, stats, (BF*)h, ldh, ones_col);
+  return launch_pdl("ln_fwd_kernel", ln_fwd_kernel<float, float>, gr, bl, 0, s, (const float*)a,
+                    lda, M, D, g, beta, stats, (float*)h, ldh, ones_col);
 }
 
 // dn (dtype rows, ld ldd) -> da in place; partials for the ReduceJob in
 // *job (segments dg | dbeta | colsum(da), each D long, padded to 4).
-int ln_backward(void* dn, int64_t ldd, const float* a, int64_t lda, const float* stats,
+int ln_backward(void* dn, int64_t ldd, const void* a, int64_t lda, const float* stats,
                 const float* g, int64_t M, int D, float* part, int dtype, float* gg, float* gbeta,
-                float* gb, ReduceJob* job, cudaStream_t s) {
+                float* gb, ReduceJob* job, cudaStream_t s, bool a_bf16) {
   if (M == 0) return UL_OK;
+  using BF = __nv_bfloat16;
   int nb = ln_blocks(M);
   const int Dp = (int)(ceil_div(D, 4) * 4);
   const size_t sm = (size_t)kLnWarps * 3 * D * sizeof(float);
-  static bool attr[2] = {false, false};
+  static bool attr[4] = {false, false, false, false};
   const int nv = reg_nv(D);
   const int db = dtype == kBf16 ? 8 : 16;
-  if (nv && lda % 4 == 0 && ldd % 4 == 0 && al(a, 16) && al(g, 16) && al(stats, 8) &&
-      al(dn, db) && al(part, 16)) {
+  const bool bd = dtype == kBf16;
+  const int64_t nbmax = ln_blocks(M) > ln_col_chunks(M) ? ln_blocks(M) : ln_col_chunks(M);
+  float2* rs = reinterpret_cast<float2*>(part + nbmax * 3 * Dp);
+  if (D % 4 == 0 && lda % 4 == 0 && ldd % 4 == 0 && al(a, a_bf16 ? 8 : 16) &&
+      al(g, 16) && al(stats, 8) && al(dn, db) && al(part, 16) && ln_two_pass()) {
+    int64_t b1 = ceil_div(M, 8);
+    b1 = b1 > 8 * kNumSMs ? 8 * kNumSMs : b1;
+    int64_t rows_per = ceil_div(M, (int64_t)ln_col_chunks(M));
+    rows_per = rows_per < 16 ? 16 : rows_per;
+    nb = (int)ceil_div(M, rows_per);
+    int64_t thr = ceil_div((int64_t)D / 4, 32) * 32;
+    thr = thr > 256 ? 256 : thr;
+    const dim3 g1((unsigned)b1), g2((unsigned)nb), bl1(256), bl2((unsigned)thr);
+#define UL_LN2(TA_, TD_)                                                                       \
+  do {                                                                                         \
+    UL_TRY(launch_pdl("ln_bwd_rows", ln_bwd_rows<TA_, TD_>, g1, bl1, 0, s, (const TD_*)dn, ldd, \
+                      (const TA_*)a, lda, stats, g, M, D, rs));                                \
+    UL_TRY(launch_pdl("ln_bwd_cols", ln_bwd_cols<TA_, TD_>, g2, bl2, 0, s, (TD_*)dn, ldd,       \
+                      (const TA_*)a, lda, stats, (const float2*)rs, g, M, D, rows_per, part)); \
+  } while (0)
+    if (a_bf16 && bd) UL_LN2(BF, BF);
+    else if (a_bf16) UL_LN2(BF, float);
+    else if (bd) UL_LN2(float, BF);
+    else UL_LN2(float, float);
+#undef UL_LN2
+  } else if (nv && lda % 4 == 0 && ldd % 4 == 0 && al(a, a_bf16 ? 8 : 16) && al(g, 16) &&
+      al(stats, 8) && al(dn, db) && al(part, 16)) {
     int64_t b = ceil_div(M, kRegWarps * 4);
     nb = (int)(b > kNumSMs ? kNumSMs : b);
-    if (dtype == kBf16)
-      UL_TRY(bwd_reg(nv, nb, reinterpret_cast<__nv_bfloat16*>(dn), ldd, a, lda, stats, g, M, D,
-                     part, s));
+    if (a_bf16 && bd)
+      UL_TRY(bwd_reg(nv, nb, (BF*)dn, ldd, (const BF*)a, lda, stats, g, M, D, part, s));
+    else if (a_bf16)
+      UL_TRY(bwd_reg(nv, nb, (float*)dn, ldd, (const BF*)a, lda, stats, g, M, D, part, s));
+    else if (bd)
+      UL_TRY(bwd_reg(nv, nb, (BF*)dn, ldd, (const float*)a, lda, stats, g, M, D, part, s));
     else
-      UL_TRY(bwd_reg(nv, nb, reinterpret_cast<float*>(dn), ldd, a, lda, stats, g, M, D, part, s));
-  } else if (dtype == kBf16) {
-    if (!attr[1]) {
-      UL_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<__nv_bfloat16>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr[1] = true;
-    }
-    UL_TRY(launch_pdl("ln_bwd_kernel", ln_bwd_kernel<__nv_bfloat16>, dim3(nb), dim3(kLnWarps * 32),
-                      sm, s, reinterpret_cast<__nv_bfloat16*>(dn), ldd, a, lda, stats, g, M, D,
-                      part));
+      UL_TRY(bwd_reg(nv, nb, (float*)dn, ldd, (const float*)a, lda, stats, g, M, D, part, s));
   } else {
-    if (!attr[0]) {
-      UL_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<float>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr[0] = true;
+    const int ai = (a_bf16 ? 2 : 0) + (bd ? 1 : 0);
+    auto attr_once = [&](const void* fn) -> int {
+      if (!attr[ai]) {
+        UL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr[ai] = true;
+      }
+      return UL_OK;
+    };
+    const dim3 gr(nb), bl(kLnWarps * 32);
+    if (a_bf16 && bd) {
+      UL_TRY(attr_once((const void*)ln_bwd_kernel<BF, BF>));
+      UL_TRY(launch_pdl("ln_bwd_kernel", ln_bwd_kernel<BF, BF>, gr, bl, sm, s, (BF*)dn, ldd,
+                        (const BF*)a, lda, stats, g, M, D, part));
+    } else if (a_bf16) {
+      UL_TRY(attr_once((const void*)ln_bwd_kernel<BF, float>));
+      UL_TRY(launch_pdl("ln_bwd_kernel", ln_bwd_kernel<BF, float>, gr, bl, sm, s, (float*)dn, ldd,
+                        (const BF*)a, lda, stats, g, M, D, part));
+    } else if (bd) {
+      UL_TRY(attr_once((const void*)ln_bwd_kernel<float, BF>));
+      UL_TRY(launch_pdl("ln_bwd_kernel", ln_bwd_kernel<float, BF>, gr, bl, sm, s, (BF*)dn, ldd,
+                        (const float*)a, lda, stats, g, M, D, part));
+    } else {
+      UL_TRY(attr_once((const void*)ln_bwd_kernel<float, float>));
+      UL_TRY(launch_pdl("ln_bwd_kernel", ln_bwd_kernel<float, float>, gr, bl, sm, s, (float*)dn,
+                        ldd, (const float*)a, lda, stats, g, M, D, part));
     }
-    UL_TRY(launch_pdl("ln_bwd_kernel", ln_bwd_kernel<float>, dim3(nb), dim3(kLnWarps * 32), sm, s,
-                      reinterpret_cast<float*>(dn), ldd, a, lda, stats, g, M, D, part));
   }
   // block partials are [3][D] rows; expose them as one segment job of
   // length 3*D (the reduction kernel wants len % 4 == 0: D % 4 == 0 here)

@@ -388,6 +388,16 @@ int64_t act_floats(const NetView& v, int64_t M) {
   return s;
 }
 
+// pre-LN rows in bf16 on the bf16 back end (UL_LN_A_BF16=0: fp32 rows)
+bool ln_a_bf16(int dtype) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_LN_A_BF16");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return dtype == kBf16 && on == 1;
+}
+
 void ln_bufs(const NetView& v, const float* acts, int64_t M, int i, float** a, int64_t* lda,
              float** stats) {
   int64_t off = 0;
@@ -452,14 +462,18 @@ static int64_t sk_ws_floats(const NetView& v, int64_t M) {
   return rup(sk, 64);
 }
 
+// LayerNorm block partials: one region per LN layer (with the deferred dW
+// pass every layer's partials live until the single reduction at the end)
+static int64_t ln_layer_off(const NetView& v, int64_t M, int i) {
+  int64_t o = 0;
+  if (v.ln)
+    for (int j = 0; j < i && j < v.n_layers - 1; ++j) o += rup(ln_part_floats(M, v.dims[j + 1]), 64);
+  return o;
+}
+
 int64_t bwd_work_floats(const NetView& v, int64_t M) {
   const int64_t sk = sk_ws_floats(v, M);
-  int64_t lnp = 0;  // LayerNorm partials (live until the layer's own reduction)
-  if (v.ln)
-    for (int i = 1; i < v.n_layers; ++i) {
-      const int64_t q = ln_part_floats(M, v.dims[i]);
-      lnp = q > lnp ? q : lnp;
-    }
+  const int64_t lnp = ln_layer_off(v, M, v.n_layers - 1);
   // + the transposed W column slice of the skinny input-gradient path
   return n_dh_bufs(v) * M * max_hidden_ld(v) + dw_ws_floats(v, M) + sk +
          kCsRegion * v.n_layers + rup(lnp, 64) + rup((int64_t)kSkinnyDxMax * v.dims[1], 64);
@@ -504,6 +518,63 @@ int stage_weights_dt(const NetView& v, const float* params, void* wp, int dtype,
                       reinterpret_cast<__nv_bfloat16*>(wp));
   return launch_pdl("stage_weights_kernel", stage_weights_kernel<float>, dim3((unsigned)blocks),
                     dim3(256), 0, s, params, t, reinterpret_cast<float*>(wp));
+}
+
+// Several networks' staged operand rows in ONE launch (the SAC plan restages
+// actor, q1, q2 and both targets every update): warp per staged row, lanes
+// across the row (coalesced), zero padding to the 16-byte pitch.
+constexpr int kMultiStage = 5 * UL_MAX_LAYERS;
+struct MultiStage {
+  const float* src[kMultiStage];
+  void* dst[kMultiStage];
+  int cols[kMultiStage], ld[kMultiStage];
+  int64_t row0[kMultiStage + 1];  // prefix sums of rows
+  int n;
+};
+
+template <typename T>
+__global__ void stage_multi_kernel(const __grid_constant__ MultiStage t) {
+  pdl_trigger();
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < t.row0[t.n];
+       r += nw) {
+    int e = 0;
+    while (e + 1 < t.n && r >= t.row0[e + 1]) ++e;
+    const int64_t rr = r - t.row0[e];
+    const float* s = t.src[e] + rr * t.cols[e];
+    T* d = reinterpret_cast<T*>(t.dst[e]) + rr * t.ld[e];
+    for (int c = lane; c < t.ld[e]; c += 32) d[c] = (T)(c < t.cols[e] ? s[c] : 0.f);
+  }
+}
+
+int stage_weights_multi(int n, const NetView* const* v, const float* const* params,
+                        void* const* wp, int dtype, cudaStream_t s) {
+  MultiStage t{};
+  const int a = dtype == kBf16 ? 8 : 4;
+  const int eb = dtype == kBf16 ? 2 : 4;
+  int e = 0;
+  t.row0[0] = 0;
+  for (int k = 0; k < n; ++k)
+    for (int i = 0; i < v[k]->n_layers; ++i) {
+      UL_CHECK_ARG(e < kMultiStage, "stage_weights_multi: too many layers");
+      t.src[e] = params[k] + v[k]->w_off[i];
+      t.dst[e] = reinterpret_cast<char*>(wp[k]) +
+                 (dtype == kBf16 ? v[k]->wb_off[i] : v[k]->wp_off[i]) * eb;
+      t.cols[e] = v[k]->dims[i];
+      t.ld[e] = (int)rup(v[k]->dims[i], a);
+      t.row0[e + 1] = t.row0[e] + v[k]->dims[i + 1];
+      ++e;
+    }
+  t.n = e;
+  int64_t blocks = ceil_div(t.row0[e], 8);
+  blocks = blocks > 8 * kNumSMs ? 8 * kNumSMs : (blocks < 1 ? 1 : blocks);
+  if (dtype == kBf16)
+    return launch_pdl("stage_multi_kernel", stage_multi_kernel<__nv_bfloat16>,
+                      dim3((unsigned)blocks), dim3(256), 0, s, t);
+  return launch_pdl("stage_multi_kernel", stage_multi_kernel<float>, dim3((unsigned)blocks),
+                    dim3(256), 0, s, t);
 }
 
 int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t s) {
@@ -682,14 +753,17 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       G.splits = 1;
       G.C = dst; G.ldc = lddst;
       G.dtype = dt;
-      if (v.ln && !last) {  // a = W x + b (fp32) -> LayerNorm + ELU kernel below
+      if (v.ln && !last) {  // a = W x + b -> LayerNorm + ELU kernel below
         float* la;
         float* lst;
         int64_t lla;
         ln_bufs(v, N.acts, M, i, &la, &lla, &lst);
-        G.epi = kEpiBias;
+        // bf16 back end: the epilogue writes the pre-LN rows as bf16 (half
+        // the bytes the LN kernels stream in the forward and the backward)
+        const bool abf = ln_a_bf16(dt);
+        G.epi = abf ? kEpiBiasLn : kEpiBias;
         G.C = la;
-        G.ldc = lla;
+        G.ldc = abf ? rup(v.dims[i + 1], 8) : lla;
         ln_pending[k] = true;
       }
       // tf32 keeps a wide output layer on the SIMT kernel; bf16 runs it on
@@ -716,9 +790,10 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       float* lst;
       int64_t lla;
       ln_bufs(v, N.acts, M, i, &la, &lla, &lst);
-      UL_TRY(ln_forward(la, lla, M, v.dims[i + 1], N.params + v.g_off[i],
-                        N.params + v.beta_off[i], lst, const_cast<float*>(h[k]), ldh[k],
-                        v.dims[i + 1], dt, s));
+      const bool abf = ln_a_bf16(dt);
+      UL_TRY(ln_forward(la, abf ? rup(v.dims[i + 1], 8) : lla, M, v.dims[i + 1],
+                        N.params + v.g_off[i], N.params + v.beta_off[i], lst,
+                        const_cast<float*>(h[k]), ldh[k], v.dims[i + 1], dt, s, abf));
     }
     if (skinny[0] || skinny[1]) {
       UL_TRY(L.open());
@@ -789,6 +864,16 @@ int run_deferred_dw_reduce(DeferredDw& D, cudaStream_t s) {
   return UL_OK;
 }
 
+// LayerNorm networks join the deferred dW pass (UL_LN_DEFER=0: per-layer dW)
+static bool ln_defer_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_LN_DEFER");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
+}
+
 int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
                    cudaStream_t side, cudaEvent_t fork, cudaEvent_t join, DeferredDw* dd) {
   if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
@@ -799,13 +884,13 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
   const int dt = backend_dtype(backend);
   const int eb = dt == kBf16 ? 2 : 4;
   const bool tc = backend >= 1;
-  // Deferred dW (bf16 tensor-core back end, no LayerNorm): the dX chain runs
+  // Deferred dW (bf16 tensor-core back end, LayerNorm included): the dX chain runs
   // first and keeps every layer's dZ; all dW GEMMs of the pass (of both
   // networks when the caller shares its collector) then run as one batched
   // launch with few K splits, and every partial reduction as one pass.
   bool defer = deferred_dw_enabled() && tc && dt == kBf16;
   for (int k = 0; k < n; ++k)
-    defer = defer && nets[k].want_dw && nets[k].wp && !nets[k].v->ln;
+    defer = defer && nets[k].want_dw && nets[k].wp && (!nets[k].v->ln || ln_defer_enabled());
   DeferredDw local_dd;
   DeferredDw* D = defer ? (dd ? dd : &local_dd) : nullptr;
   struct St {
@@ -848,15 +933,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
     S.sk_part = S.ws + dw_ws_floats(v, M);
     S.cs_part = S.sk_part + sk_ws_floats(v, M);
     S.ln_part = S.cs_part + kCsRegion * v.n_layers;
-    {
-      int64_t lnp = 0;
-      if (v.ln)
-        for (int i = 1; i < v.n_layers; ++i) {
-          const int64_t q = ln_part_floats(M, v.dims[i]);
-          lnp = q > lnp ? q : lnp;
-        }
-      S.dxw = S.ln_part + rup(lnp, 64);
-    }
+    S.dxw = S.ln_part + rup(ln_layer_off(v, M, v.n_layers - 1), 64);
     S.dh = N.dout;
     S.lddh = N.ld_dout;
     S.dh_f32 = true;
@@ -943,11 +1020,13 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       int64_t lla;
       ln_bufs(v, N.acts, M, i, &la, &lla, &lst);
       ReduceJob job;
-      UL_TRY(ln_backward(const_cast<float*>(S.dh), S.lddh, la, lla, lst, N.params + v.g_off[i], M,
-                         v.dims[i + 1], S.ln_part, dt,
+      const bool abf = ln_a_bf16(dt);
+      UL_TRY(ln_backward(const_cast<float*>(S.dh), S.lddh, la,
+                         abf ? rup(v.dims[i + 1], 8) : lla, lst, N.params + v.g_off[i], M,
+                         v.dims[i + 1], S.ln_part + ln_layer_off(v, M, i), dt,
                          N.want_dw ? N.grads + v.g_off[i] : nullptr,
                          N.want_dw ? N.grads + v.beta_off[i] : nullptr,
-                         db_here ? N.grads + v.b_off[i] : nullptr, &job, L.of(k)));
+                         db_here ? N.grads + v.b_off[i] : nullptr, &job, L.of(k), abf));
       if (N.want_dw) pend[npend++] = job;
       if (db_here) S.db_done = i;
     }

@@ -732,9 +732,10 @@ namespace ul {
 namespace {
 
 int stage_critics(SacPlan* p, cudaStream_t s) {
-  const int wd = backend_dtype(p->d.gemm_backend);
-  UL_TRY(stage_weights_dt(p->vq, p->b.q1, p->ws_q1, wd, s));
-  return stage_weights_dt(p->vq, p->b.q2, p->ws_q2, wd, s);
+  const NetView* v[2] = {&p->vq, &p->vq};
+  const float* src[2] = {p->b.q1, p->b.q2};
+  void* dst[2] = {p->ws_q1, p->ws_q2};
+  return stage_weights_multi(2, v, src, dst, backend_dtype(p->d.gemm_backend), s);
 }
 
 // phase 1: staged weights, soft target, critic forwards + MSE head + critic
@@ -745,12 +746,12 @@ int sac_critic_grads(SacPlan* p, cudaStream_t s) {
   const int64_t B = p->B, A = p->A;
   const float* qin = (const float*)p->qin;  // (rows of the back end's dtype)
   const float* qn = (const float*)p->qn;
-  if (be != 0) {  // tensor-core back ends read 16-B-row staged (tf32 / bf16) weights
-    const int wd = backend_dtype(be);
-    UL_TRY(stage_weights_dt(p->va, b.actor, p->ws_a, wd, s));
-    UL_TRY(stage_critics(p, s));
-    UL_TRY(stage_weights_dt(p->vq, b.q1t, p->ws_q1t, wd, s));
-    UL_TRY(stage_weights_dt(p->vq, b.q2t, p->ws_q2t, wd, s));
+  if (be != 0) {  // tensor-core back ends read 16-B-row staged (tf32 / bf16) weights:
+    // all five networks in one launch
+    const NetView* v[5] = {&p->va, &p->vq, &p->vq, &p->vq, &p->vq};
+    const float* src[5] = {b.actor, b.q1, b.q2, b.q1t, b.q2t};
+    void* dst[5] = {p->ws_a, p->ws_q1, p->ws_q2, p->ws_q1t, p->ws_q2t};
+    UL_TRY(stage_weights_multi(5, v, src, dst, backend_dtype(be), s));
   }
   // ---- K10 target (next_obs rows of qn, actions a' written by the squash)
   UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, qn, p->ldq, B, p->acts_a, p->mean, A, s));
