@@ -216,6 +216,11 @@ int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
 int ul_ring_insert(float* ring, int64_t cap, int64_t width, int64_t head, const float* rows,
                    int64_t n, void* stream);
 
+/* float64 -> float32 narrowing of k <= 8 device arrays in one launch (the
+ * rollout segment's float64 per-step scalars, landed by a raw H2D) */
+int ul_narrow_f64(int k, const double* const* src, float* const* dst, const int64_t* n,
+                  void* stream);
+
 /* Device permutation of [0, n) (performance mode only; NOT the numpy Philox
  * shuffle of R:algos/ppo.py:162). */
 int ul_device_permutation(int64_t n, uint64_t key, int64_t* out, void* stream);

@@ -155,6 +155,7 @@ _PROTOS = {
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                  C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
                                  vp]),
+    "ul_narrow_f64": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), vp]),
     "ul_ring_insert": (C.c_int, [vp, i64, i64, i64, vp, i64, vp]),
     "ul_device_permutation": (C.c_int, [i64, C.c_uint64, vp, vp]),
     "ul_device_permutations": (C.c_int, [i64, C.c_int, C.POINTER(C.c_uint64), vp, i64, vp]),

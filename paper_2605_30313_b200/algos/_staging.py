@@ -159,8 +159,10 @@ class DeviceSegment:
             ev = torch.cuda.Event()
             ev.record(torch.cuda.current_stream())
             self._pin_busy = ev
-        for land, dst in casts:  # f64 -> f32 narrowing of the landed scalars
-            dst.copy_(land)
+        if casts:  # f64 -> f32 narrowing of the landed scalars, one launch
+            _lib.call("ul_narrow_f64", len(casts), _lib.ptr_array([_dev.ptr(l) for l, _ in casts]),
+                      _lib.ptr_array([_dev.ptr(d) for _, d in casts]),
+                      _lib.i64_array([l.numel() for l, _ in casts]), _dev.stream())
         self._repitch(jobs)
 
     # ------------------------------------------------- per-step streaming

@@ -395,3 +395,45 @@ extern "C" int ul_device_permutation(int64_t n, uint64_t key, int64_t* out, void
   ul::feistel_perm_kernel<<<(unsigned)blocks, 256, 0, ul::as_stream(stream)>>>(n, bits, key, out);
   return ul::check_launch("feistel_perm_kernel");
 }
+
+// f64 -> f32 narrowing of up to 8 device arrays in one launch (the pinned
+// float64 per-step scalars of a rollout segment, landed as-is by the H2D:
+// no host conversion, R:algos/segment.py field dtypes)
+namespace ul {
+namespace {
+struct NarrowTable {
+  const double* src[8];
+  float* dst[8];
+  int64_t n[8];
+  int k;
+};
+__global__ void narrow_kernel(const __grid_constant__ NarrowTable t) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int a = 0; a < t.k; ++a)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t.n[a]; i += stride)
+      t.dst[a][i] = (float)t.src[a][i];
+}
+}  // namespace
+}  // namespace ul
+
+extern "C" int ul_narrow_f64(int k, const double* const* src, float* const* dst,
+                             const int64_t* n, void* stream) {
+  UL_CHECK_ARG(k >= 0 && k <= 8, "narrow: 0..8 arrays");
+  if (k == 0) return UL_OK;
+  ul::NarrowTable t{};
+  t.k = k;
+  int64_t mx = 1;
+  for (int a = 0; a < k; ++a) {
+    t.src[a] = src[a];
+    t.dst[a] = dst[a];
+    t.n[a] = n[a];
+    mx = n[a] > mx ? n[a] : mx;
+  }
+  int64_t blocks = ul::ceil_div(mx, 256);
+  blocks = blocks > 4 * ul::kNumSMs ? 4 * ul::kNumSMs : blocks;
+  return ul::launch_pdl("narrow_kernel", ul::narrow_kernel, dim3((unsigned)blocks), dim3(256), 0,
+                        ul::as_stream(stream), t);
+}
+
