@@ -365,43 +365,65 @@ __global__ void __launch_bounds__(256) ln_bwd_cols(TD* __restrict__ dn, int64_t 
                                                    int64_t rows_per, float* __restrict__ part) {
   pdl_trigger();
   pdl_wait();
-  constexpr int U = 4;  // rows in flight per thread (all loads issued before the math)
+  // a thread owns 8 adjacent columns (two 4-wide vectors: 16 B of bf16 per
+  // array and row) and keeps U rows of loads in flight -- enough bytes in
+  // flight per SM to stream at HBM rate
+  constexpr int U = 8;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
   float* pz = part + (int64_t)blockIdx.x * 3 * D;
-  for (int c = 4 * threadIdx.x; c < D; c += 4 * blockDim.x) {
-    const float4 gv = V4<float>::ld(g + c);
-    float4 ag = make_float4(0.f, 0.f, 0.f, 0.f), ab = ag, aa = ag;
+  for (int c0 = 8 * threadIdx.x; c0 < D; c0 += 8 * blockDim.x) {
+    const int nh = c0 + 4 < D ? 2 : 1;  // (D % 4 == 0: the second half may not exist)
+    float4 gv[2], ag[2], ab[2], aa[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      gv[hh] = hh < nh ? V4<float>::ld(g + c0 + 4 * hh) : make_float4(0.f, 0.f, 0.f, 0.f);
+      ag[hh] = ab[hh] = aa[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     for (int64_t rb = r0; rb < r1; rb += U) {
-      float4 x[U], d[U];
+      float4 x[U][2], d[U][2];
       float2 st[U], m[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t r = rb + u < r1 ? rb + u : r1 - 1;
         st[u] = reinterpret_cast<const float2*>(stats)[r];
         m[u] = rs[r];
-        x[u] = V4<TA>::ld(a + r * lda + c);
-        d[u] = V4<TD>::ld(dn + r * ldd + c);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c = c0 + 4 * (hh < nh ? hh : 0);
+          x[u][hh] = V4<TA>::ld(a + r * lda + c);
+          d[u][hh] = V4<TD>::ld(dn + r * ldd + c);
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (rb + u >= r1) break;
-        const float4 xh = make_float4((x[u].x - st[u].x) * st[u].y, (x[u].y - st[u].x) * st[u].y,
-                                      (x[u].z - st[u].x) * st[u].y, (x[u].w - st[u].x) * st[u].y);
-        const float4 dv = d[u];
-        const float4 da = make_float4(st[u].y * (dv.x * gv.x - m[u].x - xh.x * m[u].y),
-                                      st[u].y * (dv.y * gv.y - m[u].x - xh.y * m[u].y),
-                                      st[u].y * (dv.z * gv.z - m[u].x - xh.z * m[u].y),
-                                      st[u].y * (dv.w * gv.w - m[u].x - xh.w * m[u].y));
-        V4<TD>::st(dn + (rb + u) * ldd + c, da);
-        ag.x += dv.x * xh.x; ag.y += dv.y * xh.y; ag.z += dv.z * xh.z; ag.w += dv.w * xh.w;
-        ab.x += dv.x; ab.y += dv.y; ab.z += dv.z; ab.w += dv.w;
-        aa.x += da.x; aa.y += da.y; aa.z += da.z; aa.w += da.w;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh >= nh) break;
+          const float4 xv = x[u][hh], dv = d[u][hh], gg = gv[hh];
+          const float mu = st[u].x, rstd = st[u].y;
+          const float4 xh = make_float4((xv.x - mu) * rstd, (xv.y - mu) * rstd,
+                                        (xv.z - mu) * rstd, (xv.w - mu) * rstd);
+          const float4 da = make_float4(rstd * (dv.x * gg.x - m[u].x - xh.x * m[u].y),
+                                        rstd * (dv.y * gg.y - m[u].x - xh.y * m[u].y),
+                                        rstd * (dv.z * gg.z - m[u].x - xh.z * m[u].y),
+                                        rstd * (dv.w * gg.w - m[u].x - xh.w * m[u].y));
+          V4<TD>::st(dn + (rb + u) * ldd + c0 + 4 * hh, da);
+          ag[hh].x += dv.x * xh.x; ag[hh].y += dv.y * xh.y;
+          ag[hh].z += dv.z * xh.z; ag[hh].w += dv.w * xh.w;
+          ab[hh].x += dv.x; ab[hh].y += dv.y; ab[hh].z += dv.z; ab[hh].w += dv.w;
+          aa[hh].x += da.x; aa[hh].y += da.y; aa[hh].z += da.z; aa[hh].w += da.w;
+        }
       }
     }
-    V4<float>::st(pz + c, ag);
-    V4<float>::st(pz + D + c, ab);
-    V4<float>::st(pz + 2 * D + c, aa);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      if (hh >= nh) break;
+      V4<float>::st(pz + c0 + 4 * hh, ag[hh]);
+      V4<float>::st(pz + D + c0 + 4 * hh, ab[hh]);
+      V4<float>::st(pz + 2 * D + c0 + 4 * hh, aa[hh]);
+    }
   }
 }
 
@@ -444,29 +466,42 @@ __global__ void __launch_bounds__(256) ln_fwd_cols(const TA* __restrict__ a, int
                                                    int64_t rows_per) {
   pdl_trigger();
   pdl_wait();
-  constexpr int U = 4;
+  constexpr int U = 8;  // rows in flight; 8 columns (two 4-wide vectors) per thread
   const int64_t r0 = (int64_t)blockIdx.x * rows_per;
   const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
-  for (int c = 4 * threadIdx.x; c < D; c += 4 * blockDim.x) {
-    const float4 gv = V4<float>::ld(g + c), bv = V4<float>::ld(beta + c);
+  for (int c0 = 8 * threadIdx.x; c0 < D; c0 += 8 * blockDim.x) {
+    const int nh = c0 + 4 < D ? 2 : 1;
+    float4 gv[2], bv[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int c = c0 + 4 * (hh < nh ? hh : 0);
+      gv[hh] = V4<float>::ld(g + c);
+      bv[hh] = V4<float>::ld(beta + c);
+    }
     for (int64_t rb = r0; rb < r1; rb += U) {
-      float4 x[U];
+      float4 x[U][2];
       float2 st[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t r = rb + u < r1 ? rb + u : r1 - 1;
         st[u] = reinterpret_cast<const float2*>(stats)[r];
-        x[u] = V4<TA>::ld(a + r * lda + c);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) x[u][hh] = V4<TA>::ld(a + r * lda + c0 + 4 * (hh < nh ? hh : 0));
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (rb + u >= r1) break;
-        float4 o;
-        o.x = elu_f((x[u].x - st[u].x) * st[u].y * gv.x + bv.x);
-        o.y = elu_f((x[u].y - st[u].x) * st[u].y * gv.y + bv.y);
-        o.z = elu_f((x[u].z - st[u].x) * st[u].y * gv.z + bv.z);
-        o.w = elu_f((x[u].w - st[u].x) * st[u].y * gv.w + bv.w);
-        V4<TO>::st(h + (rb + u) * ldh + c, o);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh >= nh) break;
+          const float mu = st[u].x, rstd = st[u].y;
+          float4 o;
+          o.x = elu_f((x[u][hh].x - mu) * rstd * gv[hh].x + bv[hh].x);
+          o.y = elu_f((x[u][hh].y - mu) * rstd * gv[hh].y + bv[hh].y);
+          o.z = elu_f((x[u][hh].z - mu) * rstd * gv[hh].z + bv[hh].z);
+          o.w = elu_f((x[u][hh].w - mu) * rstd * gv[hh].w + bv[hh].w);
+          V4<TO>::st(h + (rb + u) * ldh + c0 + 4 * hh, o);
+        }
       }
     }
   }
@@ -578,7 +613,7 @@ int ln_forward(const void* a, int64_t lda, int64_t M, int D, const float* g, con
     b1 = b1 > 8 * kNumSMs ? 8 * kNumSMs : b1;
     const int64_t rows_per = 16;
     const int64_t nb = ceil_div(M, rows_per);
-    int64_t thr = ceil_div((int64_t)D / 4, 32) * 32;
+    int64_t thr = ceil_div(ceil_div((int64_t)D, 8), 32) * 32;
     thr = thr > 256 ? 256 : thr;
     const dim3 g1((unsigned)b1), g2((unsigned)nb), bl1(256), bl2((unsigned)thr);
 #define UL_LNF(TA_, TO_)                                                                     \
@@ -649,7 +684,7 @@ int ln_backward(void* dn, int64_t ldd, const void* a, int64_t lda, const float* 
     int64_t rows_per = ceil_div(M, (int64_t)ln_col_chunks(M));
     rows_per = rows_per < 16 ? 16 : rows_per;
     nb = (int)ceil_div(M, rows_per);
-    int64_t thr = ceil_div((int64_t)D / 4, 32) * 32;
+    int64_t thr = ceil_div(ceil_div((int64_t)D, 8), 32) * 32;
     thr = thr > 256 ? 256 : thr;
     const dim3 g1((unsigned)b1), g2((unsigned)nb), bl1(256), bl2((unsigned)thr);
 #define UL_LN2(TA_, TD_)                                                                       \

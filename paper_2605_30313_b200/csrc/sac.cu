@@ -34,14 +34,17 @@ constexpr double kLog2Pi = 1.8378770664093453;
 // input matrix, fp32 or bf16 rows) and, optionally, a_out (for the actor
 // gradient).
 template <typename T>
-__global__ void squash_kernel(const float* __restrict__ mean, int64_t ldm,
-                              const float* __restrict__ log_std, const float* __restrict__ eps,
-                              int64_t lde, int64_t n, int A, T* __restrict__ dst, int64_t ldd,
-                              int col0, float* __restrict__ a_out, float* __restrict__ logp) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+__global__ void __launch_bounds__(256) squash_kernel(
+    const float* __restrict__ mean, int64_t ldm, const float* __restrict__ log_std,
+    const float* __restrict__ eps, int64_t lde, int64_t n, int A, T* __restrict__ dst, int64_t ldd,
+    int col0, float* __restrict__ a_out, float* __restrict__ logp) {
+  // warp per row, lane per action dimension (A <= UL_MAX_ACT = 64: two
+  // passes of 32 lanes); the f64 log-prob terms meet in a warp sum
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
     double lp = 0.0;
-    for (int j = 0; j < A; ++j) {
+    for (int j = lane; j < A; j += 32) {
       const float ls = log_std[j];
       const float sd = expf(ls);
       const float m = mean[i * ldm + j];
@@ -53,7 +56,8 @@ __global__ void squash_kernel(const float* __restrict__ mean, int64_t ldm,
       dst[i * ldd + col0 + j] = (T)a;
       if (a_out) a_out[i * A + j] = a;
     }
-    logp[i] = (float)lp;
+    lp = warp_sum(lp);
+    if (lane == 0) logp[i] = (float)lp;
   }
 }
 
@@ -559,12 +563,15 @@ int adam_one(float* params, float* grads, float* m, float* v, int64_t n, ul_opt_
 int launch_squash(SacPlan* p, const float* eps, void* dst, float* a_out, cudaStream_t s) {
   const float* ls = p->b.actor + p->va.logstd_off;
   const int64_t B = p->B;
+  int64_t blocks = ceil_div(B, 8);  // 8 rows (warps) per block
+  blocks = blocks > 16 * kNumSMs ? 16 * kNumSMs : blocks;
   if (p->dt == kBf16)
-    squash_kernel<__nv_bfloat16><<<grid_for(B), 256, 0, s>>>(
+    squash_kernel<__nv_bfloat16><<<(unsigned)blocks, 256, 0, s>>>(
         p->mean, p->A, ls, eps, p->A, B, p->A, (__nv_bfloat16*)dst, p->ldq, p->D, a_out, p->logp);
   else
-    squash_kernel<float><<<grid_for(B), 256, 0, s>>>(p->mean, p->A, ls, eps, p->A, B, p->A,
-                                                     (float*)dst, p->ldq, p->D, a_out, p->logp);
+    squash_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(p->mean, p->A, ls, eps, p->A, B, p->A,
+                                                          (float*)dst, p->ldq, p->D, a_out,
+                                                          p->logp);
   return check_launch("squash_kernel");
 }
 
