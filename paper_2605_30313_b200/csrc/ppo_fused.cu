@@ -496,7 +496,7 @@ __host__ __device__ inline int rup16(int k) { return (k + 15) / 16 * 16; }
 // dynamic smem layout (bytes) of the tensor-core variant
 struct MmaSmem {
   int ka, kc, pa, pc, pwa, pdm;
-  size_t o_hc, o_wa, o_dm, o_wc, o_dv, o_cs, total;
+  size_t o_hc, o_wa, o_dm, o_wc, o_dv, o_cs, o_dh, total;
   __host__ __device__ MmaSmem(int Ka, int Kc, int NJT) {
     ka = rup16(Ka);
     kc = rup8(Kc);
@@ -518,6 +518,9 @@ struct MmaSmem {
     o += (size_t)kMRows * 4 * 2;  // v (forward) and dv, fp32
     o_cs = o;
     o += (size_t)kMWarps * ka * 4 + (size_t)kMWarps * 32 * 4 + (size_t)2 * kMWarps * kc * 4;
+    o = (o + 15) / 16 * 16;
+    o_dh = o;                  // dh_a tile [kMRows][pa] bf16 (coalesced store + column sums)
+    o += (size_t)kMRows * pa * 2;
     total = o;
   }
 };
@@ -758,8 +761,10 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
       af[m][2] = pk_bf16(dm[0][2 * m + 1][0], dm[0][2 * m + 1][1]);
       af[m][3] = pk_bf16(dm[1][2 * m + 1][0], dm[1][2 * m + 1][1]);
     }
-    __nv_bfloat16* da0 = reinterpret_cast<__nv_bfloat16*>(f.dha) + (r0 + R[0]) * f.lddha;
-    __nv_bfloat16* da1 = reinterpret_cast<__nv_bfloat16*>(f.dha) + (r0 + R[1]) * f.lddha;
+    // results go to a shared-memory tile first; the whole CTA then writes it
+    // with coalesced 16-byte stores and takes the column sums (no per-tile
+    // shuffles or 4-byte global stores in this loop)
+    __nv_bfloat16* sdh = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dh);
     for (int nc = 0; nc < ka / 8; ++nc) {
       float d[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -776,23 +781,39 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
       d[1] = fmaf(d[1], fminf(h0.y, 0.f), d[1]);
       d[2] = fmaf(d[2], fminf(h1.x, 0.f), d[2]);
       d[3] = fmaf(d[3], fminf(h1.y, 0.f), d[3]);
-      if (c < Ka) {  // Ka even (bf16 rows): c + 1 < Ka too
-        if (ok[0]) *reinterpret_cast<uint32_t*>(da0 + c) = pk_bf16(d[0], d[1]);
-        if (ok[1]) *reinterpret_cast<uint32_t*>(da1 + c) = pk_bf16(d[2], d[3]);
-      }
-      if (f.csa) {
-        float s0 = d[0] + d[2], s1 = d[1] + d[3];  // invalid rows: dmean = 0 -> d = 0
-#pragma unroll
-        for (int o = 4; o <= 16; o <<= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-        }
-        if (g == 0) {
-          scs[w * ka + c] = s0;
-          scs[w * ka + c + 1] = s1;
-        }
+      // (invalid rows: dmean = 0 -> d = 0; columns >= Ka: zero W rows -> 0)
+      *reinterpret_cast<uint32_t*>(sdh + R[0] * L.pa + c) = pk_bf16(d[0], d[1]);
+      *reinterpret_cast<uint32_t*>(sdh + R[1] * L.pa + c) = pk_bf16(d[2], d[3]);
+    }
+  }
+  __syncthreads();  // sdh complete
+  {
+    __nv_bfloat16* sdh = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dh);
+    const int gk = ka / 8;  // 16-byte granules per row
+    const bool vec = (Ka % 8) == 0 && (f.lddha % 8) == 0;
+    for (int e = t; e < kMRows * gk; e += kMThr) {
+      const int rr = e / gk, u = e - rr * gk;
+      const int64_t gr = r0 + rr;
+      const int c = 8 * u;
+      if (gr >= M || c >= Ka) continue;
+      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(f.dha) + gr * f.lddha + c;
+      if (vec) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(sdh + rr * L.pa + c);
+      } else {
+        for (int k2 = 0; k2 < 8 && c + k2 < Ka; ++k2) dst[k2] = sdh[rr * L.pa + c + k2];
       }
     }
+    // colsum(dh_a) per column over the tile's rows, as the values were
+    // stored (bf16): one thread per column, fixed row order (the per-warp
+    // slots of scs keep the downstream fixed-order fold: warp 0 holds all)
+    if (f.csa)
+      for (int c = t; c < ka; c += kMThr) {
+        float s = 0.f;
+#pragma unroll 8
+        for (int rr = 0; rr < kMRows; ++rr) s += __bfloat162float(sdh[rr * L.pa + c]);
+        scs[c] = s;
+        for (int k = 1; k < kMWarps; ++k) scs[k * ka + c] = 0.f;
+      }
   }
   __syncthreads();  // sdm, sdv, scs, sdb complete
   // ---- critic backward (SIMT): thread = (8-column group, rows rg, rg + R/.. ),
