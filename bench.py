@@ -389,6 +389,14 @@ def run_ours(args):
     torch.cuda.synchronize()
     par_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_par)
 
+    # host cost of the reference's index stream alone (SURVEY.md 7 hard part
+    # 10): cfg.epochs Philox permutations of the update's rows
+    t0 = time.perf_counter()
+    hr = np.random.Generator(np.random.Philox(key=7))
+    for _ in range(cfg.epochs):
+        hr.permutation(T * N)
+    host_perm_ms = (time.perf_counter() - t0) * 1e3
+
     # ---- same-width arm: the identical update with tf32 tensor-core GEMMs
     # (fp32 storage / activations), device permutations, CUDA events
     tf32 = None
@@ -521,7 +529,8 @@ def run_ours(args):
         "tf32_arm": tf32,
         "parity_mode": {"value": transitions / (par_ms / 1e3), "unit": UNIT, "update_ms": par_ms,
                         "indices": "host numpy Philox permutation per epoch (reference stream), "
-                                   "drawn while the previous epoch runs (one CUDA graph per epoch)"},
+                                   "drawn while the previous epoch runs (one CUDA graph per epoch)",
+                        "host_index_gen_ms_per_update": host_perm_ms},
         "e2e": {"value": transitions / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": e2e_ms,
