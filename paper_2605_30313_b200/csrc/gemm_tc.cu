@@ -1070,7 +1070,21 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   return check_launch("tc_gemm_kernel");
 }
 
-inline int bn_of(const GemmDesc& d) { return d.N > 128 ? 256 : 128; }
+// N tile: 256 for N > 128; UL_TC_BN_FWD / UL_TC_BN_DX = 128 cap the forward
+// (bias epilogues) / ELU-gradient tiles (wave-quantisation experiments)
+inline int bn_of(const GemmDesc& d) {
+  static int cap_fwd = -1, cap_dx = -1;
+  if (cap_fwd < 0) {
+    const char* e = getenv("UL_TC_BN_FWD");
+    cap_fwd = e ? atoi(e) : 256;
+    const char* f = getenv("UL_TC_BN_DX");
+    cap_dx = f ? atoi(f) : 256;
+  }
+  const int cap = d.epi == kEpiEluGrad ? cap_dx
+                  : (d.epi == kEpiBias || d.epi == kEpiBiasElu || d.epi == kEpiBiasLn) ? cap_fwd
+                                                                                         : 256;
+  return d.N > 128 && cap >= 256 ? 256 : 128;
+}
 
 }  // namespace tc
 // whether a dW batch (MN-major A and B, store epilogue) runs on CTA pairs
