@@ -152,6 +152,9 @@ int ul_stage_weights(const ul_net_desc* net, const float* params, float* wstage,
                         * x, hidden activations and hidden gradients stored bf16
                         * (rows of round_up(d + 1, 8)); params, grads, outputs
                         * and the upstream gradient stay fp32 (1e-2 tolerance) */
+#define UL_GEMM_TF32X3 3 /* tcgen05 kind::tf32 over 3xTF32-split fp32 operands
+                          * (hi*hi + hi*lo + lo*hi as one GEMM over a tripled K):
+                          * the fp32-parity path on the tensor cores */
 /* activation row pitch (elements) of a hidden layer of width d for a back end */
 int64_t ul_mlp_act_ld(int d, int backend);
 /* stage W for a back end (UL_GEMM_BF16 writes bf16 rows of round_up(in, 8)) */
@@ -288,7 +291,7 @@ typedef struct ul_ppo_plan_desc {
                                        its own segment rows (weak scaling) and a
                                        global minibatch is the union of the
                                        ranks' local minibatches              */
-  int32_t gemm_backend;             /* UL_GEMM_FP32 / _TF32 / _BF16           */
+  int32_t gemm_backend;             /* UL_GEMM_FP32 / _TF32 / _BF16 / _TF32X3 */
 } ul_ppo_plan_desc;
 
 typedef struct ul_ppo_bindings {

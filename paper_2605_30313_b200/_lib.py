@@ -21,6 +21,7 @@ UL_MAX_ACT = 64
 UL_GEMM_FP32 = 0
 UL_GEMM_TF32 = 1
 UL_GEMM_BF16 = 2
+UL_GEMM_TF32X3 = 3
 
 # Process-wide GEMM back end of the MLP passes ("fp32": SIMT exact-fp32 parity
 # path; "tf32": tcgen05 tensor cores).  See paper_2605_30313_b200.set_precision.
@@ -33,6 +34,8 @@ def gemm_backend(input_grads: bool = False) -> int:
     g = _PRECISION["gemm"]
     if g == "bf16":
         return UL_GEMM_TF32 if input_grads else UL_GEMM_BF16
+    if g == "tf32x3":
+        return UL_GEMM_TF32X3
     return UL_GEMM_TF32 if g == "tf32" else UL_GEMM_FP32
 
 vp = C.c_void_p

@@ -1214,8 +1214,108 @@ static tc::Prob prob_of(const GemmDesc& d, int ones_col) {
 
 // Same contract as gemm_f32 (split partials [zs][M][ldc] at C when splits >
 // 1); `ones_col` >= 0 additionally writes 1.0 into that column.
+// ---------------------------------------------------------------- 3xTF32
+// a = hi + lo with hi = rna_tf32(a) (exactly representable in tf32) and lo =
+// a - hi (exact in fp32); a*b ~= hi_a hi_b + hi_a lo_b + lo_a hi_b, the
+// dropped lo*lo term and lo's own tf32 rounding are ~2^-22 relative -- fp32
+// parity.  The three products are ONE tf32 GEMM over a tripled K:
+// A' = [A_hi | A_hi | A_lo], B' = [B_hi | B_lo | B_hi] along K (columns of a
+// K-major operand, rows of an MN-major one; each block zero-padded to Kp), so
+// every epilogue, split-K and layout of the tf32 kernel is reused unchanged.
+namespace {
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return __uint_as_float(u);
+}
+
+__global__ void split3_kernel(const float* __restrict__ src, int64_t lds, int64_t R, int64_t C,
+                              int kcols, int64_t Kp, int lo_mask, float* __restrict__ dst,
+                              int64_t ldd) {
+  const int64_t total = kcols ? R * 3 * Kp : 3 * Kp * C;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+    int64_t r, c, di;
+    int b;
+    float v;
+    if (kcols) {  // dst [R][3 Kp]
+      r = i / (3 * Kp);
+      const int64_t j = i - r * 3 * Kp;
+      b = (int)(j / Kp);
+      c = j - b * Kp;
+      v = c < C ? src[r * lds + c] : 0.f;
+      di = r * ldd + j;
+    } else {  // dst [3 Kp][C]
+      const int64_t rr = i / C;
+      c = i - rr * C;
+      b = (int)(rr / Kp);
+      r = rr - b * Kp;
+      v = r < R ? src[r * lds + c] : 0.f;
+      di = rr * ldd + c;
+    }
+    const float hi = tf32_rna(v);
+    dst[di] = ((lo_mask >> b) & 1) ? v - hi : hi;
+  }
+}
+
+float* g_x3 = nullptr;
+size_t g_x3_cap = 0;
+}  // namespace
+
+// Grows by allocating a larger buffer; a replaced buffer is never freed,
+// because CUDA graphs captured earlier keep its address baked in.
+int x3_reserve(size_t floats) {
+  if (floats <= g_x3_cap) return UL_OK;
+  float* nb = nullptr;
+  UL_CUDA(cudaMalloc(&nb, floats * sizeof(float)));
+  g_x3 = nb;
+  g_x3_cap = floats;
+  return UL_OK;
+}
+
+int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
+
+static int gemm_tc_x3(const GemmDesc& d, int ones_col, cudaStream_t s) {
+  const int64_t Kp = ceil_div(d.K, 4) * 4;
+  // stored shapes (rows R x cols C) of the operands
+  const int64_t Ra = d.a_kmajor ? d.M : d.K, Ca = d.a_kmajor ? d.K : d.M;
+  const int64_t Rb = d.b_kmajor ? d.N : d.K, Cb = d.b_kmajor ? d.K : d.N;
+  const int64_t lda2 = d.a_kmajor ? 3 * Kp : d.lda, ldb2 = d.b_kmajor ? 3 * Kp : d.ldb;
+  const int64_t na = d.a_kmajor ? d.M * 3 * Kp : 3 * Kp * d.lda;
+  const int64_t nb = d.b_kmajor ? d.N * 3 * Kp : 3 * Kp * d.ldb;
+  const size_t need = (size_t)(ceil_div(na, 64) * 64 + nb);
+  if (need > g_x3_cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    UL_CHECK_ARG(cs == cudaStreamCaptureStatusNone,
+                 "3xTF32: split scratch (%zu floats) not reserved before graph capture", need);
+    UL_TRY(x3_reserve(need));
+  }
+  float* a2 = g_x3;
+  float* b2 = g_x3 + ceil_div(na, 64) * 64;
+  auto blocks = [](int64_t n) {
+    int64_t b = ceil_div(n, 256);
+    return (unsigned)(b > 8 * kNumSMs ? 8 * kNumSMs : (b < 1 ? 1 : b));
+  };
+  split3_kernel<<<blocks(d.a_kmajor ? Ra * 3 * Kp : 3 * Kp * Ca), 256, 0, s>>>(
+      d.A, d.lda, Ra, Ca, d.a_kmajor ? 1 : 0, Kp, 0b100, a2, lda2);
+  UL_TRY(check_launch("split3_kernel"));
+  split3_kernel<<<blocks(d.b_kmajor ? Rb * 3 * Kp : 3 * Kp * Cb), 256, 0, s>>>(
+      d.B, d.ldb, Rb, Cb, d.b_kmajor ? 1 : 0, Kp, 0b010, b2, ldb2);
+  UL_TRY(check_launch("split3_kernel"));
+  GemmDesc e = d;
+  e.x3 = false;
+  e.A = a2;
+  e.lda = lda2;
+  e.B = b2;
+  e.ldb = ldb2;
+  e.K = 3 * Kp;
+  return gemm_tc(e, ones_col, s);
+}
+
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
   if (d.M == 0 || d.N == 0) return UL_OK;
+  if (d.x3) return gemm_tc_x3(d, ones_col, s);
   const tc::Prob q = prob_of(d, ones_col);
   if (d.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(&q, 1, s);
   return tc::dispatch<float>(&q, 1, s);
@@ -1228,6 +1328,11 @@ int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s) {
 int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s) {
   bool done[64] = {};
   UL_CHECK_ARG(n >= 0 && n <= 64, "gemm_tc_batch: at most 64 problems");
+  for (int i = 0; i < n; ++i)
+    if (d[i].x3) {  // one at a time through the split scratch
+      for (int j = 0; j < n; ++j) UL_TRY(gemm_tc(d[j], -1, s));
+      return UL_OK;
+    }
   for (int i = 0; i < n; ++i) done[i] = d[i].M == 0 || d[i].N == 0;
   for (int i = 0; i < n; ++i) {
     if (done[i]) continue;
@@ -1257,7 +1362,7 @@ int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s) {
 // CTA pairing; otherwise two launches.  Each desc's ones_col applies.
 int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
   const bool e0 = d0.M == 0 || d0.N == 0, e1 = d1.M == 0 || d1.N == 0;
-  if (e0 || e1) {
+  if (e0 || e1 || d0.x3 || d1.x3) {  // (3xTF32: one split scratch, one GEMM at a time)
     if (!e0) UL_TRY(gemm_tc(d0, -1, s));
     if (!e1) UL_TRY(gemm_tc(d1, -1, s));
     return UL_OK;

@@ -86,6 +86,9 @@ struct GemmDesc {
   // below, reduced later with a ReduceJob)
   float* csum_part = nullptr;
   int* csum_nz = nullptr;
+  // fp32 operands through the tf32 tensor cores as 3xTF32 (hi/lo split,
+  // hi*hi + hi*lo + lo*hi): the exact-fp32 parity back end on tcgen05
+  bool x3 = false;
 };
 constexpr int kCsumMaxN = 512;
 // widest input-gradient column slice the skinny dX path takes (SAC dQ/da)
@@ -170,6 +173,12 @@ int stage_weights(const NetView& v, const float* params, float* wp, cudaStream_t
 // 2: tcgen05 bf16 -- x, the hidden activations and the backward's hidden
 // gradients are bf16 (rows of act_ld(d, kBf16)), params / grads / outputs fp32
 inline int backend_dtype(int backend) { return backend == 2 ? kBf16 : kF32; }
+// backend 3: tcgen05 kind::tf32 on 3xTF32-split fp32 operands (exact-fp32 parity)
+constexpr int kBackendTf32x3 = 3;
+// scratch of the 3xTF32 split operands: grown on demand outside graph
+// capture; plans reserve their bound at creation
+int x3_reserve(size_t floats);
+size_t x3_bound(const NetView& v, int64_t M);
 int stage_weights_dt(const NetView& v, const float* params, void* wp, int dtype, cudaStream_t s);
 // n networks' staged rows in one launch
 int stage_weights_multi(int n, const NetView* const* v, const float* const* params,

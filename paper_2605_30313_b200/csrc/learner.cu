@@ -621,9 +621,17 @@ extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
   }
   if (desc->ld_obs < p->va.dims[0] || desc->ld_cobs < p->vc.dims[0] || desc->ld_act < p->A)
     return fail("ppo plan: leading dimension below feature width");
-  if (desc->gemm_backend < 0 || desc->gemm_backend > 2)
-    return fail("ppo plan: gemm_backend must be UL_GEMM_FP32, _TF32 or _BF16");
+  if (desc->gemm_backend < 0 || desc->gemm_backend > 3)
+    return fail("ppo plan: gemm_backend must be UL_GEMM_FP32, _TF32, _BF16 or _TF32X3");
   p->dt = ul::backend_dtype(desc->gemm_backend);
+  if (desc->gemm_backend == ul::kBackendTf32x3) {  // split scratch before any graph capture
+    const size_t a = ul::x3_bound(p->va, p->mb_local), c = ul::x3_bound(p->vc, p->mb_local);
+    st = ul::x3_reserve(a > c ? a : c);
+    if (st != UL_OK) {
+      delete p;
+      return st;
+    }
+  }
   if (p->dt == ul::kBf16 && ((desc->ld_obs * 4) % 16 || (desc->ld_cobs * 4) % 16))
     return fail("ppo plan: the bf16 back end needs 16-byte obs / critic-obs rows");
   // bf16 staging rows: round_up(ld, 8) elements (16-byte TMA rows)

@@ -471,6 +471,26 @@ static int64_t ln_layer_off(const NetView& v, int64_t M, int i) {
   return o;
 }
 
+// largest 3xTF32 split scratch one GEMM of a pass over M rows needs: the
+// forward (A [M, 3Kp], B [N, 3Kp]), the input gradient (A [M, 3 out_p],
+// B [3 out_p, ld_in]) and the weight gradient (A [3 Mp, ld_out],
+// B [3 Mp, ld_in + ones]) of every layer
+size_t x3_bound(const NetView& v, int64_t M) {
+  size_t mx = 0;
+  const int64_t Mp = rup(M, 4);
+  for (int i = 0; i < v.n_layers; ++i) {
+    const int64_t in = v.dims[i], out = v.dims[i + 1];
+    const int64_t ip = rup(in + 1, 4), op = rup(out + 1, 4);
+    const size_t fwd = (size_t)(rup(M * 3 * ip, 64) + out * 3 * ip);
+    const size_t dx = (size_t)(rup(M * 3 * op, 64) + 3 * op * ip);
+    const size_t dw = (size_t)(rup(3 * Mp * op, 64) + 3 * Mp * ip);
+    const size_t m = fwd > dx ? fwd : dx;
+    mx = m > mx ? m : mx;
+    mx = dw > mx ? dw : mx;
+  }
+  return mx;
+}
+
 int64_t bwd_work_floats(const NetView& v, int64_t M) {
   const int64_t sk = sk_ws_floats(v, M);
   const int64_t lnp = ln_layer_off(v, M, v.n_layers - 1);
@@ -753,6 +773,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       G.splits = 1;
       G.C = dst; G.ldc = lddst;
       G.dtype = dt;
+      G.x3 = backend == kBackendTf32x3;
       if (v.ln && !last) {  // a = W x + b -> LayerNorm + ELU kernel below
         float* la;
         float* lst;
@@ -1049,6 +1070,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       G.a_kmajor = false; G.b_kmajor = false; G.epi = kEpiStore;
       G.C = defer ? st[k].ws + dw_layer_off(v, M, i) : st[k].ws;
       G.dtype = dt;
+      G.x3 = backend == kBackendTf32x3;
       free_w[k] = ones_free_of(in, has_ones);
       G.N = free_w[k] ? in + 1 : in;
       G.splits = dw_splits(out, in, M, true);
@@ -1191,6 +1213,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       G.aux = act_ptr(v, N.acts, M, i - 1, dt); G.ldaux = act_ld((int)in, dt);
       G.a_kmajor = true; G.b_kmajor = false; G.epi = kEpiEluGrad; G.splits = 1;
       G.dtype = dt;
+      G.x3 = backend == kBackendTf32x3;
       tc_x[k] = tc && N.wp && (out >= 32 || dt == kBf16);
       if (tc_x[k]) {
         G.B = staged_w(v, N.wp, i, dt, &G.ldb);
@@ -1318,7 +1341,8 @@ extern "C" int ul_mlp_forward(const ul_net_desc* net, const float* params, const
   UL_TRY(ul::make_view(net, &v));
   UL_CHECK_ARG(M >= 0, "forward: negative batch");
   UL_CHECK_ARG(ldx >= v.dims[0], "forward: ldx %lld < input_dim %d", (long long)ldx, v.dims[0]);
-  UL_CHECK_ARG(backend >= 0 && backend <= 2, "forward: backend must be 0 (fp32), 1 (tf32) or 2 (bf16)");
+  UL_CHECK_ARG(backend >= 0 && backend <= 3,
+               "forward: backend must be 0 (fp32), 1 (tf32), 2 (bf16) or 3 (3xTF32)");
   return ul::mlp_forward(v, params, wstage, backend, x, ldx, M, acts, out, ld_out,
                          ul::as_stream(stream));
 }
@@ -1330,7 +1354,8 @@ extern "C" int ul_mlp_backward(const ul_net_desc* net, const float* params, cons
   ul::NetView v;
   UL_TRY(ul::make_view(net, &v));
   UL_CHECK_ARG(M >= 0, "backward: negative batch");
-  UL_CHECK_ARG(backend >= 0 && backend <= 2, "backward: backend must be 0 (fp32), 1 (tf32) or 2 (bf16)");
+  UL_CHECK_ARG(backend >= 0 && backend <= 3,
+               "backward: backend must be 0 (fp32), 1 (tf32), 2 (bf16) or 3 (3xTF32)");
   return ul::mlp_backward(v, params, wstage, backend, x, ldx, x_has_ones != 0, M, acts, dout,
                           ld_dout, grads, dx, lddx, 0, v.dims[0], true, true, work,
                           ul::as_stream(stream));

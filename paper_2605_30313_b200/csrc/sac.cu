@@ -610,8 +610,15 @@ extern "C" int ul_sac_plan_create(const ul_sac_plan_desc* desc, void** plan) {
   if (p->vq.dims[0] != p->D + p->A || p->vq.dims[p->vq.n_layers] != 1)
     return fail("sac plan: critic must map obs+act -> 1");
   if (p->A > UL_MAX_ACT) return fail("sac plan: action dim above UL_MAX_ACT");
-  if (desc->gemm_backend < 0 || desc->gemm_backend > 2)
-    return fail("sac plan: gemm_backend must be 0 (fp32), 1 (tf32) or 2 (bf16)");
+  if (desc->gemm_backend < 0 || desc->gemm_backend > 3)
+    return fail("sac plan: gemm_backend must be 0 (fp32), 1 (tf32), 2 (bf16) or 3 (3xTF32)");
+  if (desc->gemm_backend == ul::kBackendTf32x3) {
+    const size_t a = ul::x3_bound(p->va, p->B), q = ul::x3_bound(p->vq, p->B);
+    if (ul::x3_reserve(a > q ? a : q) != UL_OK) {
+      delete p;
+      return UL_ERR_CUDA;
+    }
+  }
   p->dt = ul::backend_dtype(desc->gemm_backend);
   p->ldq = ul::act_ld(p->D + p->A, p->dt);
   p->ldo = ul::act_ld(p->D, p->dt);

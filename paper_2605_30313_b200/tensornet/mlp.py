@@ -216,7 +216,7 @@ def _staged(params: ModelParams):
     """(backend, staged weights) for one MLP pass: the tensor-core path reads
     W through 16-byte-aligned padded rows restaged from the live parameters."""
     be = _lib.gemm_backend(input_grads=True)
-    if be != _lib.UL_GEMM_TF32:
+    if be not in (_lib.UL_GEMM_TF32, _lib.UL_GEMM_TF32X3):
         return be, None
     desc = params.arch.desc()
     ws = torch.empty(max(_lib.lib().ul_mlp_wstage_floats(desc), 1), dtype=torch.float32,
