@@ -1229,32 +1229,69 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(u);
 }
 
-__global__ void split3_kernel(const float* __restrict__ src, int64_t lds, int64_t R, int64_t C,
-                              int kcols, int64_t Kp, int lo_mask, float* __restrict__ dst,
-                              int64_t ldd) {
-  const int64_t total = kcols ? R * 3 * Kp : 3 * Kp * C;
+// K' = zs x [hi | hi-or-lo | ...] blocks: split-K chunk z of the original
+// operand (K range [z Kp, (z+1) Kp)) becomes K' range [3 z Kp, 3 (z+1) Kp)
+// holding its three parts, so a split-K GEMM keeps the same zs partials.
+// Memory-bound: 4 K' elements (one float4) per thread, the block / chunk
+// decomposition computed once per float4 (Kp % 32 == 0) in 32-bit math.
+__device__ __forceinline__ float split_part(float v, int b, int lo_mask) {
+  const float hi = tf32_rna(v);
+  return ((lo_mask >> b) & 1) ? v - hi : hi;
+}
+
+// K-major operand [R][K] -> [R][K3]
+__global__ void split3_cols_kernel(const float* __restrict__ src, int64_t lds, int R, int K,
+                                   int Kp, int K3, int lo_mask, float* __restrict__ dst,
+                                   int64_t ldd) {
+  const int q4 = K3 / 4;  // float4 per row (K3 % 4 == 0)
+  const int64_t total = (int64_t)R * q4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-    int64_t r, c, di;
-    int b;
-    float v;
-    if (kcols) {  // dst [R][3 Kp]
-      r = i / (3 * Kp);
-      const int64_t j = i - r * 3 * Kp;
-      b = (int)(j / Kp);
-      c = j - b * Kp;
-      v = c < C ? src[r * lds + c] : 0.f;
-      di = r * ldd + j;
-    } else {  // dst [3 Kp][C]
-      const int64_t rr = i / C;
-      c = i - rr * C;
-      b = (int)(rr / Kp);
-      r = rr - b * Kp;
-      v = r < R ? src[r * lds + c] : 0.f;
-      di = rr * ldd + c;
+    const int r = (int)(i / q4), j = 4 * (int)(i - (int64_t)r * q4);
+    const int z = j / (3 * Kp), rem = j - z * 3 * Kp, b = rem / Kp;
+    const int k0 = z * Kp + rem - b * Kp;
+    const float* s = src + (int64_t)r * lds;
+    float4 o;
+    o.x = split_part(k0 < K ? s[k0] : 0.f, b, lo_mask);
+    o.y = split_part(k0 + 1 < K ? s[k0 + 1] : 0.f, b, lo_mask);
+    o.z = split_part(k0 + 2 < K ? s[k0 + 2] : 0.f, b, lo_mask);
+    o.w = split_part(k0 + 3 < K ? s[k0 + 3] : 0.f, b, lo_mask);
+    *reinterpret_cast<float4*>(dst + (int64_t)r * ldd + j) = o;
+  }
+}
+
+// MN-major operand [K][C] -> [K3][C]: dst row j <- source row k (or zeros)
+__global__ void split3_rows_kernel(const float* __restrict__ src, int64_t lds, int K, int C,
+                                   int Kp, int K3, int lo_mask, float* __restrict__ dst,
+                                   int64_t ldd) {
+  const int c4 = (C + 3) / 4;
+  for (int j = blockIdx.y; j < K3; j += gridDim.y) {
+    const int z = j / (3 * Kp), rem = j - z * 3 * Kp, b = rem / Kp;
+    const int k = z * Kp + rem - b * Kp;
+    const float* s = src + (int64_t)k * lds;
+    float* d = dst + (int64_t)j * ldd;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < c4; q += gridDim.x * blockDim.x) {
+      const int c = 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k < K) {
+        if (c + 3 < C && ((lds & 3) == 0)) v = *reinterpret_cast<const float4*>(s + c);
+        else {
+          v.x = s[c];
+          v.y = c + 1 < C ? s[c + 1] : 0.f;
+          v.z = c + 2 < C ? s[c + 2] : 0.f;
+          v.w = c + 3 < C ? s[c + 3] : 0.f;
+        }
+      }
+      float4 o = make_float4(split_part(v.x, b, lo_mask), split_part(v.y, b, lo_mask),
+                             split_part(v.z, b, lo_mask), split_part(v.w, b, lo_mask));
+      if (c + 3 < C || ((ldd & 3) == 0 && c + 3 < ldd)) {
+        *reinterpret_cast<float4*>(d + c) = o;
+      } else {
+        d[c] = o.x;
+        if (c + 1 < C) d[c + 1] = o.y;
+        if (c + 2 < C) d[c + 2] = o.z;
+      }
     }
-    const float hi = tf32_rna(v);
-    dst[di] = ((lo_mask >> b) & 1) ? v - hi : hi;
   }
 }
 
@@ -1276,13 +1313,16 @@ int x3_reserve(size_t floats) {
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
 
 static int gemm_tc_x3(const GemmDesc& d, int ones_col, cudaStream_t s) {
-  const int64_t Kp = ceil_div(d.K, 4) * 4;
+  const int64_t splits = d.splits < 1 ? 1 : d.splits;
+  const int64_t Kp = ceil_div(ceil_div(d.K, splits), 32) * 32;  // per split, tf32 BK multiple
+  const int64_t zs = ceil_div(d.K > 0 ? d.K : 1, Kp);
+  const int64_t K3 = 3 * Kp * zs;
   // stored shapes (rows R x cols C) of the operands
   const int64_t Ra = d.a_kmajor ? d.M : d.K, Ca = d.a_kmajor ? d.K : d.M;
   const int64_t Rb = d.b_kmajor ? d.N : d.K, Cb = d.b_kmajor ? d.K : d.N;
-  const int64_t lda2 = d.a_kmajor ? 3 * Kp : d.lda, ldb2 = d.b_kmajor ? 3 * Kp : d.ldb;
-  const int64_t na = d.a_kmajor ? d.M * 3 * Kp : 3 * Kp * d.lda;
-  const int64_t nb = d.b_kmajor ? d.N * 3 * Kp : 3 * Kp * d.ldb;
+  const int64_t lda2 = d.a_kmajor ? K3 : d.lda, ldb2 = d.b_kmajor ? K3 : d.ldb;
+  const int64_t na = d.a_kmajor ? d.M * K3 : K3 * d.lda;
+  const int64_t nb = d.b_kmajor ? d.N * K3 : K3 * d.ldb;
   const size_t need = (size_t)(ceil_div(na, 64) * 64 + nb);
   if (need > g_x3_cap) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -1293,23 +1333,34 @@ static int gemm_tc_x3(const GemmDesc& d, int ones_col, cudaStream_t s) {
   }
   float* a2 = g_x3;
   float* b2 = g_x3 + ceil_div(na, 64) * 64;
-  auto blocks = [](int64_t n) {
-    int64_t b = ceil_div(n, 256);
-    return (unsigned)(b > 8 * kNumSMs ? 8 * kNumSMs : (b < 1 ? 1 : b));
+  auto split = [&](const float* srcp, int64_t lds, bool kmajor, int64_t R, int64_t C, int mask,
+                   float* dst, int64_t ldd) -> int {
+    if (kmajor) {  // [R][K] -> [R][K3]
+      int64_t b = ceil_div(R * (K3 / 4), 256);
+      b = b > 16 * kNumSMs ? 16 * kNumSMs : (b < 1 ? 1 : b);
+      split3_cols_kernel<<<(unsigned)b, 256, 0, s>>>(srcp, lds, (int)R, (int)d.K, (int)Kp,
+                                                     (int)K3, mask, dst, ldd);
+      return check_launch("split3_cols_kernel");
+    }
+    // [K][C] -> [K3][C]
+    const int64_t c4 = ceil_div(C, 4);
+    const unsigned gx = (unsigned)ceil_div(c4, 128);
+    int64_t gy = (16 * kNumSMs) / (int64_t)gx;
+    gy = gy > K3 ? K3 : (gy < 1 ? 1 : gy);
+    split3_rows_kernel<<<dim3(gx, (unsigned)gy), 128, 0, s>>>(srcp, lds, (int)d.K, (int)C,
+                                                              (int)Kp, (int)K3, mask, dst, ldd);
+    return check_launch("split3_rows_kernel");
   };
-  split3_kernel<<<blocks(d.a_kmajor ? Ra * 3 * Kp : 3 * Kp * Ca), 256, 0, s>>>(
-      d.A, d.lda, Ra, Ca, d.a_kmajor ? 1 : 0, Kp, 0b100, a2, lda2);
-  UL_TRY(check_launch("split3_kernel"));
-  split3_kernel<<<blocks(d.b_kmajor ? Rb * 3 * Kp : 3 * Kp * Cb), 256, 0, s>>>(
-      d.B, d.ldb, Rb, Cb, d.b_kmajor ? 1 : 0, Kp, 0b010, b2, ldb2);
-  UL_TRY(check_launch("split3_kernel"));
+  UL_TRY(split(d.A, d.lda, d.a_kmajor, Ra, Ca, 0b100, a2, lda2));
+  UL_TRY(split(d.B, d.ldb, d.b_kmajor, Rb, Cb, 0b010, b2, ldb2));
   GemmDesc e = d;
   e.x3 = false;
   e.A = a2;
   e.lda = lda2;
   e.B = b2;
   e.ldb = ldb2;
-  e.K = 3 * Kp;
+  e.K = K3;
+  e.splits = (int)zs;
   return gemm_tc(e, ones_col, s);
 }
 

@@ -194,10 +194,14 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
     g_fwd = both >= 0 ? both : env("UL_GROUP_FWD", 1);
     g_bwd = both >= 0 ? both : env("UL_GROUP_BWD", 0);
   }
-  if (fwd && g_fwd) return mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join);
+  // 3xTF32: the split-operand scratch is shared, so every GEMM of the pass
+  // stays on one stream (the grouped drivers; small kernels still fork)
+  const bool x3 = be == kBackendTf32x3;
+  if (fwd && (g_fwd || x3))
+    return mlp_forward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join);
   DeferredDw own;
   DeferredDw* D = dd ? dd : &own;
-  if (!fwd && g_bwd) {
+  if (!fwd && (g_bwd || x3)) {
     UL_TRY(mlp_backward_n(nets, 2, be, ml, s, p->side, p->ev_fork, p->ev_join, D));
     mark(p, 6, s);
     UL_TRY(run_deferred_dw_gemms(*D, s));

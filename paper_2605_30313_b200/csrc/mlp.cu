@@ -477,13 +477,15 @@ static int64_t ln_layer_off(const NetView& v, int64_t M, int i) {
 // B [3 Mp, ld_in + ones]) of every layer
 size_t x3_bound(const NetView& v, int64_t M) {
   size_t mx = 0;
-  const int64_t Mp = rup(M, 4);
+  // (each split-K chunk is padded to a multiple of 32: at most 64 chunks)
+  const int64_t Mk = rup(M, 32) + 32 * 64;
   for (int i = 0; i < v.n_layers; ++i) {
     const int64_t in = v.dims[i], out = v.dims[i + 1];
-    const int64_t ip = rup(in + 1, 4), op = rup(out + 1, 4);
+    const int64_t ip = rup(in + 1, 32), op = rup(out + 1, 32);
+    const int64_t ldi = rup(in + 1, 4), ldo = rup(out + 1, 4);
     const size_t fwd = (size_t)(rup(M * 3 * ip, 64) + out * 3 * ip);
-    const size_t dx = (size_t)(rup(M * 3 * op, 64) + 3 * op * ip);
-    const size_t dw = (size_t)(rup(3 * Mp * op, 64) + 3 * Mp * ip);
+    const size_t dx = (size_t)(rup(M * 3 * op, 64) + 3 * op * ldi);
+    const size_t dw = (size_t)(rup(3 * Mk * ldo, 64) + 3 * Mk * ldi);
     const size_t m = fwd > dx ? fwd : dx;
     mx = m > mx ? m : mx;
     mx = dw > mx ? dw : mx;
