@@ -112,7 +112,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.01)  # (the timed region is ~0.1 s: sample every 10 ms)
 
     def __enter__(self):
         if self.nv is not None:

@@ -157,7 +157,7 @@ int ln_forward(const void* a, int64_t lda, int64_t M, int D, const float* g, con
 int ln_backward(void* dn, int64_t ldd, const void* a, int64_t lda, const float* stats,
                 const float* g, int64_t M, int D, float* part, int dtype, float* gg, float* gbeta,
                 float* gb, ReduceJob* job, cudaStream_t s, bool a_bf16 = false);
-int ln_part_floats(int64_t M, int D);
+int64_t ln_part_floats(int64_t M, int D);
 // pre-LayerNorm rows a_i [M, round_up(D,4)] fp32 and stats [M][2] of hidden layer i
 void ln_bufs(const NetView& v, const float* acts, int64_t M, int i, float** a, int64_t* lda,
              float** stats);

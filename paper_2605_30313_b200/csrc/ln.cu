@@ -520,9 +520,9 @@ int ln_blocks(int64_t M) {
 
 // block partials [ln_blocks][3][D] + the two-kernel backward's per-row
 // (m1, m2) scratch [M] (8-byte aligned: the partial block is a multiple of 4 floats)
-int ln_part_floats(int64_t M, int D) {
+int64_t ln_part_floats(int64_t M, int D) {
   const int64_t nb = ln_blocks(M) > ln_col_chunks(M) ? ln_blocks(M) : ln_col_chunks(M);
-  return (int)(nb * 3 * ceil_div(D, 4) * 4 + 2 * M);
+  return nb * 3 * ceil_div(D, 4) * 4 + 2 * M;
 }
 
 namespace {
