@@ -42,6 +42,8 @@ int ul_version(void);
 int ul_device_count(int* count);
 int ul_stream_sync(void* stream);
 int ul_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* async byte fill of device memory (cudaMemsetAsync) */
+int ul_memset_async(void* dst, int value, int64_t bytes, void* stream);
 /* strided 2-D async copy (row pitch change, e.g. 235 -> 236 floats) */
 int ul_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
                       int64_t width_bytes, int64_t rows, void* stream);

@@ -88,6 +88,19 @@ def is_pinned(a: np.ndarray) -> bool:
     return False
 
 
+def zeros(shape, dtype=torch.float32, device=None) -> torch.Tensor:
+    """Zero-filled CUDA tensor: torch allocates, the fill is a cudaMemsetAsync
+    on the current stream (no framework kernel on the product path)."""
+    t = torch.empty(shape, dtype=dtype, device=device or require_cuda())
+    if t.numel():
+        _lib.call("ul_memset_async", ptr(t), 0, t.numel() * t.element_size(), stream())
+    return t
+
+
+def zeros_like(t: torch.Tensor) -> torch.Tensor:
+    return zeros(t.shape, t.dtype, t.device)
+
+
 # ------------------------------------------------------------------- copies
 def h2d(dst: torch.Tensor, src: np.ndarray, s: int | None = None) -> None:
     """Contiguous host -> device copy (async when src is pinned)."""
@@ -122,7 +135,7 @@ def to_device_f32(x, ld: int | None = None) -> torch.Tensor:
         return out
     rows, d = arr.shape
     ld = feature_ld(d) if ld is None else ld
-    buf = torch.zeros((rows, ld), dtype=torch.float32, device=dev)
+    buf = zeros((rows, ld), torch.float32, dev)
     h2d_rows(buf, arr)
     return buf[:, :d]
 
@@ -157,6 +170,6 @@ def api_work() -> torch.Tensor:
     dev = require_cuda()
     w = _API_WORK.get(dev.index)
     if w is None:
-        w = torch.zeros(int(_lib.lib().ul_api_work_doubles()), dtype=torch.float64, device=dev)
+        w = zeros(int(_lib.lib().ul_api_work_doubles()), torch.float64, dev)
         _API_WORK[dev.index] = w
     return w

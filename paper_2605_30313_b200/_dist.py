@@ -57,6 +57,19 @@ def dp_forced() -> bool:
     return _FORCE["dp"]
 
 
+_DP_GRAPH_OFF = {"why": None}
+
+
+def disable_dp_graph(why: str) -> None:
+    """Fall back to the eager data-parallel loop for the rest of the process
+    (a failed capture, e.g. a collective that cannot be captured)."""
+    import warnings
+
+    if _DP_GRAPH_OFF["why"] is None:
+        warnings.warn(f"data-parallel CUDA graph disabled: {why}", RuntimeWarning, stacklevel=2)
+    _DP_GRAPH_OFF["why"] = why
+
+
 def dp_graph_enabled() -> bool:
     """Capture the data-parallel update (20 x step_grads / NCCL all-reduce /
     step_apply) in one CUDA graph (UL_DP_GRAPH=0 disables)."""
@@ -65,6 +78,8 @@ def dp_graph_enabled() -> bool:
     import torch.distributed as dist
 
     if os.environ.get("UL_DP_GRAPH", "1") == "0" or getattr(_LOCAL, "emu", None) is not None:
+        return False
+    if _DP_GRAPH_OFF["why"] is not None:
         return False
     # only NCCL collectives can be captured in a CUDA graph (gloo runs on the host)
     return dist.is_available() and dist.is_initialized() and dist.get_backend() == "nccl"

@@ -115,6 +115,7 @@ _PROTOS = {
     "ul_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "ul_stream_sync": (C.c_int, [vp]),
     "ul_memcpy_async": (C.c_int, [vp, vp, i64, vp]),
+    "ul_memset_async": (C.c_int, [vp, C.c_int, i64, vp]),
     "ul_memcpy2d_async": (C.c_int, [vp, i64, vp, i64, i64, i64, vp]),
     "ul_host_alloc_pinned": (C.c_int, [C.POINTER(vp), i64]),
     "ul_host_free_pinned": (C.c_int, [vp]),

@@ -32,21 +32,21 @@ class DeviceSegment:
         self.ld = tuple(_dev.feature_ld(d) for d in self.dims)
         f32 = dict(dtype=torch.float32, device=dev)
         rows = self.rows
-        self.obs = torch.zeros((rows, self.ld[0]), **f32)
-        self.cobs = torch.zeros((rows, self.ld[1]), **f32)
-        self.act = torch.zeros((rows, self.ld[2]), **f32)
-        self.blogp = torch.zeros(rows, **f32)
-        self.rewards = torch.zeros(rows, **f32)
-        self.values = torch.zeros(rows, **f32)
-        self.tv = torch.zeros(rows, **f32)
-        self.adv = torch.zeros(rows, **f32)
-        self.ret = torch.zeros(rows, **f32)
-        self.vnow = torch.zeros(rows, **f32)   # APPO: values under the current critic
-        self.tlogp = torch.zeros(rows, **f32)  # APPO: target log-prob
-        self.term = torch.zeros(rows, dtype=torch.uint8, device=dev)
-        self.trunc = torch.zeros(rows, dtype=torch.uint8, device=dev)
-        self.boot = torch.zeros(N, **f32)
-        self.perm = torch.zeros((max(epochs, 1), rows), dtype=torch.int64, device=dev)
+        self.obs = _dev.zeros((rows, self.ld[0]), **f32)
+        self.cobs = _dev.zeros((rows, self.ld[1]), **f32)
+        self.act = _dev.zeros((rows, self.ld[2]), **f32)
+        self.blogp = _dev.zeros(rows, **f32)
+        self.rewards = _dev.zeros(rows, **f32)
+        self.values = _dev.zeros(rows, **f32)
+        self.tv = _dev.zeros(rows, **f32)
+        self.adv = _dev.zeros(rows, **f32)
+        self.ret = _dev.zeros(rows, **f32)
+        self.vnow = _dev.zeros(rows, **f32)   # APPO: values under the current critic
+        self.tlogp = _dev.zeros(rows, **f32)  # APPO: target log-prob
+        self.term = _dev.zeros(rows, dtype=torch.uint8, device=dev)
+        self.trunc = _dev.zeros(rows, dtype=torch.uint8, device=dev)
+        self.boot = _dev.zeros(N, **f32)
+        self.perm = _dev.zeros((max(epochs, 1), rows), dtype=torch.int64, device=dev)
         self.has_tv = False
         self.slot = "ppo"
         self._raw: dict = {}  # field -> contiguous H2D landing buffer
@@ -88,9 +88,13 @@ class DeviceSegment:
         appended to `jobs` and launched after every copy of the segment: on
         the copy stream a kernel queued between two copies waits for SMs the
         running update holds, and would stall the copies behind it."""
-        if _is_dev(src):
+        if _is_dev(src):  # device -> device staging copy (copy engine, re-pitched)
             src = src.reshape(self.rows, width)
-            dst[:, :width].copy_(src)  # device -> device staging copy
+            if src.dtype != torch.float32:
+                src = src.to(torch.float32)
+            src = src.contiguous()
+            _lib.call("ul_memcpy2d_async", _dev.ptr(dst), dst.stride(0) * 4, _dev.ptr(src),
+                      width * 4, width * 4, self.rows, _dev.stream())
             return
         a = np.asarray(src)
         if a.dtype != np.float32:
@@ -102,7 +106,19 @@ class DeviceSegment:
 
     def _put_vec(self, dst: torch.Tensor, src, dtype=np.float32, casts: list | None = None) -> None:
         if _is_dev(src):
-            dst.copy_(src.reshape(-1).to(dst.dtype))
+            src = src.reshape(-1)
+            if src.dtype == torch.float64 and dst.dtype == torch.float32:
+                _lib.call("ul_narrow_f64", 1, _lib.ptr_array([_dev.ptr(src.contiguous())]),
+                          _lib.ptr_array([_dev.ptr(dst)]), _lib.i64_array([dst.numel()]),
+                          _dev.stream())
+                return
+            if src.dtype == torch.bool and dst.dtype == torch.uint8:
+                src = src.view(torch.uint8)
+            if src.dtype != dst.dtype:
+                src = src.to(dst.dtype)
+            src = src.contiguous()
+            _lib.call("ul_memcpy_async", _dev.ptr(dst), _dev.ptr(src), dst.numel() * dst.element_size(),
+                      _dev.stream())
             return
         a = np.asarray(src)
         if a.dtype == np.bool_ and dtype == np.uint8:

@@ -250,13 +250,16 @@ def launch_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red,
         _lib.call("ul_ppo_plan_run", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
                   opt.critic.t, 1, s)
         return
-    _lib.call("ul_ppo_plan_begin", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
-              opt.critic.t, s)
-    if cfgd.local_shards and not cfgd.raw_advantages:
-        sums = _dist.sums_buffer(3)
-        _lib.call("ul_ppo_plan_adv_sums", plan.h, _dev.ptr(sums), s)
-        _dist.all_reduce_sum(sums)
-        _lib.call("ul_ppo_plan_adv_finalize", plan.h, _dev.ptr(sums), s)
+    def prologue():
+        _lib.call("ul_ppo_plan_begin", plan.h, opt.actor.lr, opt.critic.lr, opt.actor.t,
+                  opt.critic.t, s)
+        if cfgd.local_shards and not cfgd.raw_advantages:
+            sums = _dist.sums_buffer(3)
+            _lib.call("ul_ppo_plan_adv_sums", plan.h, _dev.ptr(sums), s)
+            _dist.all_reduce_sum(sums)
+            _lib.call("ul_ppo_plan_adv_finalize", plan.h, _dev.ptr(sums), s)
+
+    prologue()
 
     def steps():
         st = _dev.stream()
@@ -281,8 +284,15 @@ def launch_plan(plan: _Plan, params: AcParams, opt: AcOpt, world: int, red,
         cs = torch.cuda.Stream()
         cs.wait_stream(torch.cuda.current_stream())
         torch.cuda.synchronize()
-        with torch.cuda.graph(g, stream=cs):
+        try:
+            with torch.cuda.graph(g, stream=cs):
+                steps()
+        except RuntimeError as exc:  # the collective refused capture: stay eager
+            _dist.disable_dp_graph(f"{type(exc).__name__}: {exc}")
+            torch.cuda.synchronize()
+            prologue()  # (nothing captured ran: restart the update eagerly)
             steps()
+            return
         plan.dp_graph, plan.dp_graph_key = g, key
     plan.dp_graph.replay()
 

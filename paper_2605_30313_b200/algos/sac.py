@@ -133,8 +133,8 @@ class _SacPlan:
         if world > 1:
             pq, pa = p.q1.arch.param_count, p.actor.arch.param_count
             dev = p.actor.buf.device
-            self.red = (torch.zeros(2 * pq + 4, dtype=torch.float32, device=dev),
-                        torch.zeros(pa + 4, dtype=torch.float32, device=dev))
+            self.red = (_dev.zeros(2 * pq + 4, torch.float32, dev),
+                        _dev.zeros(pa + 4, torch.float32, dev))
         self.n_cap = 0
         self.eps_ptr = None
         self.reserve(1)
@@ -459,7 +459,7 @@ def actor_loss_and_grads(params: SacParams, obs, eps):
     din2, _ = backward(params.q2, c2, d2)
     D = od.shape[1]
     dmean = torch.empty((n, A), dtype=torch.float32, device=mean.device)
-    dls = torch.zeros(A, dtype=torch.float32, device=mean.device)
+    dls = _dev.zeros(A, torch.float32, mean.device)
     ls = params.actor.log_std.contiguous()
     edc = ed.contiguous()
     _lib.call("ul_sac_actor_head", _dev.ptr(a), _dev.ptr(edc), _dev.ptr(din1[:, D:]),

@@ -37,6 +37,15 @@ extern "C" int ul_memcpy_async(void* dst, const void* src, int64_t bytes, void* 
       "cudaMemcpyAsync");
 }
 
+// Async byte fill of device memory (allocation-time zeroing without a
+// framework fill kernel)
+extern "C" int ul_memset_async(void* dst, int value, int64_t bytes, void* stream) {
+  UL_CHECK_ARG(bytes >= 0, "memset: negative size");
+  if (bytes == 0) return UL_OK;
+  return ul::cuda_status(cudaMemsetAsync(dst, value, (size_t)bytes, ul::as_stream(stream)),
+                         "cudaMemsetAsync");
+}
+
 extern "C" int ul_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch,
                                  int64_t width_bytes, int64_t rows, void* stream) {
   UL_CHECK_ARG(width_bytes >= 0 && rows >= 0 && dpitch >= width_bytes && spitch >= width_bytes,

@@ -279,7 +279,8 @@ namespace ul {
 int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64_t* src_stride,
                 const int64_t* dst_stride, const int64_t* row_bytes, const int64_t* ones_byte,
                 const int* cvt, const int64_t* idx, int64_t n, int64_t modulo, int64_t lo,
-                int64_t hi, int* err, cudaStream_t stream) {
+                int64_t hi, int* err, cudaStream_t stream,
+                int64_t cap_blocks) {
   UL_CHECK_ARG(ndesc >= 1 && ndesc <= kMaxDesc, "gather: ndesc %d outside [1,%d]", ndesc,
                kMaxDesc);
   UL_CHECK_ARG(n >= 0, "gather: negative row count");
@@ -316,7 +317,7 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
     // warps needed for kRowGroups row groups in flight each -> 8-warp blocks
     const int64_t warps = ceil_div(n, (int64_t)(32 >> sh) * kRowGroups);
     int64_t nb = ceil_div(warps, 8);
-    const int64_t cap = gather_cap_blocks();
+    const int64_t cap = cap_blocks > 0 ? cap_blocks : gather_cap_blocks();
     nb = nb > cap ? cap : nb;
     t.blk0[d] = nb_total;
     nb_total += (int)nb;

@@ -189,7 +189,8 @@ int stage_weights_multi(int n, const NetView* const* v, const float* const* para
 int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64_t* src_stride,
                 const int64_t* dst_stride, const int64_t* row_bytes, const int64_t* ones_byte,
                 const int* cvt, const int64_t* idx, int64_t n, int64_t modulo, int64_t lo,
-                int64_t hi, int* err, cudaStream_t stream);
+                int64_t hi, int* err, cudaStream_t stream,
+                int64_t cap_blocks = 0);
 int mlp_forward(const NetView& v, const float* params, const float* wp, int backend,
                 const float* x, int64_t ldx, int64_t M, float* acts, float* out, int64_t ld_out,
                 cudaStream_t s);
@@ -229,6 +230,10 @@ float* bwd_head_part(const NetView& v, float* work, int64_t M);
 bool head_needs_colsum(const MlpNet& N);
 // n = 1 or 2 networks in lockstep (grouped tensor-core launches on s; network
 // 1's small kernels on `side` between fork/join events when side != null)
+// fused forward of the hidden-layer chain (fused_mlp.cu): bf16, widths % 64,
+// <= 512, no LayerNorm, up to two networks in one persistent launch
+bool fused_fwd_ok(const MlpNet* nets, int n, int dtype);
+int fused_forward(const MlpNet* nets, int n, int64_t M, cudaStream_t s);
 int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join);
 // dd: collector for deferred dW GEMMs (bf16 path) shared between calls -- the

@@ -751,7 +751,16 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
   }
   const int nl = nets[0].v->n_layers;
   bool ln_pending[2] = {false, false};
-  for (int i = 0; i < nl; ++i) {
+  int i0 = 0;
+  if (tc && fused_fwd_ok(nets, n, dt)) {  // every hidden layer in one launch
+    UL_TRY(fused_forward(nets, n, M, s));
+    for (int k = 0; k < n; ++k) {
+      h[k] = act_ptr(*nets[k].v, nets[k].acts, M, nl - 2, dt);
+      ldh[k] = act_ld(nets[k].v->dims[nl - 1], dt);
+    }
+    i0 = nl - 1;
+  }
+  for (int i = i0; i < nl; ++i) {
     const bool last = i == nl - 1;
     GemmDesc g[2] = {};
     bool has[2] = {false, false}, use[2] = {false, false}, skinny[2] = {false, false};

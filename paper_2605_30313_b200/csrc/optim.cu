@@ -231,6 +231,34 @@ __device__ __forceinline__ void stage_param(const StageOut& so, int s, int64_t i
   }
 }
 
+// parameters i0 .. i0 + cnt - 1 (consecutive) of segment s: the layer search
+// and the row / column split once per quad, then a running column
+__device__ __forceinline__ void stage_quad(const StageOut& so, int s, int64_t i0, const float* pa,
+                                           int cnt) {
+  for (int l = 0; l < so.nl[s]; ++l) {
+    const int cols = so.cols[s][l];
+    const int size = so.rows[s][l] * cols;
+    int o = (int)(i0 - so.w_off[s][l]);
+    if (o + cnt <= 0 || o >= size) continue;
+    int e = 0;
+    if (o < 0) {
+      e = -o;
+      o = 0;
+    }
+    int r = o / cols, c = o - r * cols;
+    const int64_t ld = so.ld[s][l];
+    for (; e < cnt && o < size; ++e, ++o) {
+      const int64_t d = so.dst_off[s][l] + (int64_t)r * ld + c;
+      if (so.dtype == kBf16) reinterpret_cast<__nv_bfloat16*>(so.dst[s])[d] = __float2bfloat16_rn(pa[e]);
+      else reinterpret_cast<float*>(so.dst[s])[d] = pa[e];
+      if (++c == cols) {
+        c = 0;
+        ++r;
+      }
+    }
+  }
+}
+
 // the controller values the apply pass reads (copied once per CTA)
 struct ApplyCtl {
   int upd[UL_MAX_SEG];
@@ -281,10 +309,7 @@ __device__ __forceinline__ void adam4(const SegTable& st, int s, int64_t i, Adam
   reinterpret_cast<float4*>(st.m[s])[i] = a.m;
   reinterpret_cast<float4*>(st.v[s])[i] = a.v;
   reinterpret_cast<float4*>(st.p[s])[i] = a.p;
-  if (has_so && so.dst[s]) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) stage_param(so, s, 4 * i + e, pa[e]);
-  }
+  if (has_so && so.dst[s]) stage_quad(so, s, 4 * i, pa, 4);
 }
 
 __device__ __forceinline__ AdamScalars adam_scalars(const ApplyCtl& c, int s) {
@@ -302,17 +327,15 @@ __device__ __forceinline__ AdamScalars adam_scalars(const ApplyCtl& c, int s) {
 }
 
 // vector elements [v0, n4) step stride, scalar tail from 4 n4 + t0
-__device__ void apply_seg(const SegTable& st, const ApplyCtl& c, int s, int write_grads,
-                          int do_adam, const StageOut& so, int has_so, int64_t t0, int64_t stride,
-                          int64_t v0 = -1) {
+__device__ void apply_seg(const SegTable& st, const ApplyCtl& c, const AdamScalars& k, int s,
+                          int write_grads, int do_adam, const StageOut& so, int has_so, int64_t t0,
+                          int64_t stride, int64_t v0 = -1) {
   const int upd = c.upd[s];
   // clip_global_norm scales even when a later Adam raises; Adam itself only on upd
   const float f = (float)c.factor;
   const bool scale = c.factor != 1.0;
   float* __restrict__ g = st.g[s];
   const int64_t n = st.n[s];
-  AdamScalars k{};
-  if (do_adam) k = adam_scalars(c, s);
   if (!do_adam || !upd) {  // clip-only (clip_global_norm) or a skipped segment
     if (write_grads && scale)
       for (int64_t i = t0; i < n; i += stride) g[i] = __fmul_rn(g[i], f);
@@ -339,13 +362,17 @@ __device__ void apply_seg(const SegTable& st, const ApplyCtl& c, int s, int writ
 __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
                              int do_adam, StageOut so, int has_so) {
   __shared__ ApplyCtl c;
+  __shared__ AdamScalars k;  // (bias corrections: two f64 pow per CTA, not per thread)
   pdl_trigger();
   pdl_wait();
   const int s = blockIdx.y;
   if (s >= st.nseg) return;
-  if (threadIdx.x == 0) read_apply_ctl(ctl, st.nseg, &c);
+  if (threadIdx.x == 0) {
+    read_apply_ctl(ctl, st.nseg, &c);
+    if (do_adam) k = adam_scalars(c, s);
+  }
   __syncthreads();
-  apply_seg(st, c, s, write_grads, do_adam, so, has_so,
+  apply_seg(st, c, k, s, write_grads, do_adam, so, has_so,
             (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
 }
 

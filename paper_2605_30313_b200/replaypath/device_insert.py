@@ -38,10 +38,10 @@ class DeviceNStepReplay:
         self.obs_dim, self.act_dim, self.capacity = obs_dim, act_dim, capacity
         self.norm_gamma, self.g_max, self.eps = norm_gamma, g_max, eps
         nb = _lib.lib().ul_nstep_state_bytes(n_envs, n, obs_dim, act_dim)
-        self.state = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        self.state = _dev.zeros(nb, dtype=torch.uint8, device="cuda")
         self.width = 2 * obs_dim + act_dim + 3
         self.ldr = (self.width + 3) // 4 * 4
-        self.ring = torch.zeros((capacity, self.ldr), dtype=torch.float32, device="cuda")
+        self.ring = _dev.zeros((capacity, self.ldr), dtype=torch.float32, device="cuda")
         self.head = 0  # absolute rows inserted
         self._count = _dev.pinned_empty((1,), np.int64)
 

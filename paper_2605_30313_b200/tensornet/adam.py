@@ -49,7 +49,7 @@ class _Ctl:
                   eps, max_norm)
         for i, t in enumerate(ts):
             self.host.t[i] = int(t)
-        self.dev = torch.zeros(C.sizeof(_lib.OptCtl), dtype=torch.uint8, device="cuda")
+        self.dev = _dev.zeros(C.sizeof(_lib.OptCtl), dtype=torch.uint8, device="cuda")
         _lib.call("ul_memcpy_async", _dev.ptr(self.dev), C.addressof(self.host), _HDR,
                   _dev.stream())
 

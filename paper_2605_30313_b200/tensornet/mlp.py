@@ -109,7 +109,10 @@ class ModelParams(_FlatRecord):
         self.version = version
 
     def copy(self) -> "ModelParams":
-        return ModelParams(self.buf.clone(), self.arch, self.version)
+        buf = torch.empty_like(self.buf)
+        _lib.call("ul_memcpy_async", _dev.ptr(buf), _dev.ptr(self.buf),
+                  self.buf.numel() * self.buf.element_size(), _dev.stream())
+        return ModelParams(buf, self.arch, self.version)
 
     def with_flat(self, vec) -> "ModelParams":
         vec = np.asarray(vec, dtype=np.float32).reshape(-1)
@@ -140,7 +143,7 @@ class Grads(_FlatRecord):
 
     @classmethod
     def zeros_like(cls, params: ModelParams) -> "Grads":
-        return cls(torch.zeros_like(params.buf), params.arch)
+        return cls(_dev.zeros_like(params.buf), params.arch)
 
     def add_(self, other: "Grads") -> None:
         self.buf.add_(other.buf)

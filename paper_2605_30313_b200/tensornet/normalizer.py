@@ -29,7 +29,7 @@ class Normalizer:
             host[1 + self.dim:] = np.asarray(var, np.float64)
         self.state = torch.empty(host.size, dtype=torch.float64, device="cuda")
         _dev.h2d(self.state, host)
-        self.work = torch.zeros(_lib.lib().ul_norm_work_bytes(self.dim), dtype=torch.uint8,
+        self.work = _dev.zeros(_lib.lib().ul_norm_work_bytes(self.dim), dtype=torch.uint8,
                                 device="cuda")
 
     # host views (D2H)
