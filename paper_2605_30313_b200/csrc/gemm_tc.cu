@@ -906,11 +906,15 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
                                                d.epi == kEpiBiasLn));
   // B resident (A streamed alone) when one problem's whole N tile of B fits
   // the smem left over by the 3-stage A ring, and there is no split-K
-  static int bres_ok = -1;
-  if (bres_ok < 0) {
+  // (default: not for the ELU-gradient dX GEMMs -- the cfg2 update measured
+  // 4.643 ms with streamed B against 4.679 ms B-resident; UL_TC_BRES=1 / 0
+  // forces it on / off everywhere)
+  static int bres_env = -2;
+  if (bres_env == -2) {
     const char* e = getenv("UL_TC_BRES");
-    bres_ok = e ? atoi(e) != 0 : 1;
+    bres_env = e ? (atoi(e) != 0 ? 1 : 0) : -1;
   }
+  const bool bres_ok = bres_env >= 0 ? bres_env == 1 : d.epi != kEpiEluGrad;
   const int64_t bk = sizeof(TI) == 2 ? 64 : 32;
   const int64_t bres_bytes = ceil_div(d.K, bk) * (int64_t)bn * 128;
   const bool bres_base = bres_ok && np == 1 && !amn && q[0].zs == 1 &&
