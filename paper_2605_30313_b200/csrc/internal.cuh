@@ -118,6 +118,25 @@ struct ReduceJob {
 };
 constexpr int kMaxReduceJobs = 16;
 
+// Optional fold of the K13 prepare pass into the reduction that produces the
+// final gradients (single-process PPO step): every value the reduction
+// stores inside [base, base + n0) (segment 0) or [base + n0, base + n0 + n1)
+// (segment 1) also enters a per-block (sum g^2, non-finite) partial; the
+// last block runs the prepare tail (opt_tail.cuh).  Valid only when the
+// reduction writes EVERY element of both segments that can be nonzero (the
+// bf16 fused-head PPO step: all dW / db / dlog_std values come out of it).
+struct SqFold {
+  int on;
+  const float* base;
+  int64_t n0, n1;
+  double* part;      // [blocks][2]
+  int* bad;          // [blocks][2]
+  int cap;           // blocks the partial arrays hold
+  unsigned int* ticket;
+  ul_opt_ctl* ctl;
+  LossFinalize lf;
+};
+
 // dW GEMMs of a backward pass collected for one batched tensor-core launch
 // (gemm_tc_batch) + one reduction pass of their split partials and the
 // pass's other deferred partial sets (run_deferred_dw, mlp.cu)
@@ -129,6 +148,8 @@ struct DeferredDw {
   int ndw = 0;
   ReduceJob jobs[3 * kMax];
   int nj = 0;
+  const SqFold* fold = nullptr;  // fold the prepare pass into the reduction
+  bool folded = false;           // (out) the reduction ran the prepare tail
   void add(const GemmDesc& g, const ReduceJob& j);
 };
 int run_deferred_dw(DeferredDw& D, cudaStream_t s);  // = the two below

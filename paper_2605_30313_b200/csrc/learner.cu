@@ -35,7 +35,14 @@ struct PpoPlan {
         *red_own = nullptr;
   float *wst_a = nullptr, *wst_c = nullptr;  // staged (16 B-row) weights, tensor-core path
   double *head_part = nullptr, *adv_stats = nullptr, *adv_part = nullptr;
-  unsigned int* tickets = nullptr;  // [0] head, [1] adv stats
+  unsigned int* tickets = nullptr;  // [0] head, [1] adv stats, [2] folded prepare
+  // K13 prepare folded into the step's gradient reduction (single process,
+  // fused-head bf16 step; UL_FOLD_PREP=0 disables): block partials
+  static constexpr int kFoldCap = 8192;
+  double* fold_part = nullptr;
+  int* fold_bad = nullptr;
+  bool fold_on = false;
+  bool prep_folded = false;  // the last step_grads ran the prepare tail
   ul_opt_ctl* ctl_d = nullptr;
   ul_ppo_stats* st_d = nullptr;
   // pinned mirrors
@@ -110,6 +117,8 @@ int alloc_plan(PpoPlan* p) {
   const size_t o_tk = carve(sizeof(unsigned int) * 8);
   const size_t o_ctl = carve(sizeof(ul_opt_ctl));
   const size_t o_st = carve(sizeof(ul_ppo_stats));
+  const size_t o_fp = carve(sizeof(double) * 2 * PpoPlan::kFoldCap);
+  const size_t o_fb = carve(sizeof(int) * 2 * PpoPlan::kFoldCap);
   const size_t o_wa = carve(sizeof(float) * p->va.wp_total);
   const size_t o_wc = carve(sizeof(float) * p->vc.wp_total);
   UL_CUDA(cudaMalloc(&p->arena, off));
@@ -135,6 +144,8 @@ int alloc_plan(PpoPlan* p) {
   p->tickets = (unsigned int*)(a + o_tk);
   p->ctl_d = (ul_opt_ctl*)(a + o_ctl);
   p->st_d = (ul_ppo_stats*)(a + o_st);
+  p->fold_part = (double*)(a + o_fp);
+  p->fold_bad = (int*)(a + o_fb);
   p->wst_a = (float*)(a + o_wa);
   p->wst_c = (float*)(a + o_wc);
   UL_CUDA(cudaHostAlloc(&p->ctl_h, sizeof(ul_opt_ctl), cudaHostAllocPortable));
@@ -182,8 +193,10 @@ void free_plan(PpoPlan* p) {
 // UL_GROUP=0/1 forces both; UL_GROUP_FWD / UL_GROUP_BWD each pass.
 // dd (backward, may be null): deferred-dW collector, possibly pre-seeded with
 // the fused output stage's partial reductions
+int gather_ahead(PpoPlan* p, int e, int k, cudaStream_t s);
+
 int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool fwd,
-             DeferredDw* dd = nullptr) {
+             DeferredDw* dd = nullptr, int ahead_e = -1, int ahead_k = -1) {
   static int g_fwd = -1, g_bwd = -1;
   if (g_fwd < 0) {
     auto env = [](const char* n, int def) {
@@ -206,6 +219,9 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
     mark(p, 6, s);
     UL_TRY(run_deferred_dw_gemms(*D, s));
     mark(p, 7, s);
+    // the minibatch staging is free once the dW GEMMs have read it: the next
+    // step's gather runs beside the reduction and the optimizer
+    if (ahead_e >= 0) UL_TRY(gather_ahead(p, ahead_e, ahead_k, s));
     return run_deferred_dw_reduce(*D, s);
   }
   UL_CUDA(cudaEventRecord(p->ev_fork, s));
@@ -225,6 +241,7 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
   mark(p, 6, s);  // (profiling) dX chains of both networks
   UL_TRY(run_deferred_dw_gemms(*D, s));
   mark(p, 7, s);  // the batched dW launch
+  if (ahead_e >= 0) UL_TRY(gather_ahead(p, ahead_e, ahead_k, s));
   return run_deferred_dw_reduce(*D, s);
 }
 
@@ -375,7 +392,22 @@ int gather_ahead(PpoPlan* p, int e, int k, cudaStream_t s) {
   return UL_OK;
 }
 
+// the loss bookkeeping of step (., k) for the prepare tail
+LossFinalize loss_finalize_of(const PpoPlan* p, int k) {
+  LossFinalize lf{};
+  lf.loss = p->red + p->Pa + p->Pc;
+  lf.log_std = p->b.actor_params + p->va.logstd_off;
+  lf.A = p->A;
+  lf.n = (double)p->mb;
+  lf.vcoef = p->d.value_loss_coef;
+  lf.ecoef = p->d.entropy_coef;
+  lf.last_in_epoch = k == p->d.minibatches - 1;
+  lf.st = p->st_d;
+  return lf;
+}
+
 int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
+  p->prep_folded = false;
   const ul_ppo_bindings& b = p->b;
   const int64_t ml = p->mb_local;
   const bool tc = p->d.gemm_backend >= 1;
@@ -505,9 +537,28 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
     DeferredDw dd;
     UL_TRY(launch_ppo_fused(f, p->dt, dd.jobs, &dd.nj, s));
     mark(p, 2, s);
-    UL_TRY(mlp_pass(p, nets, be, ml, s, false, &dd));
+    // single process: the reduction that writes the final gradients also
+    // takes their joint norm / finiteness and runs the prepare tail (every
+    // element of both segments is written by it on this path; the critic's
+    // log_std slot stays zero)
+    SqFold fold{};
+    if (p->fold_on && p->d.world_size <= 1) {
+      fold.on = 1;
+      fold.base = p->red;
+      fold.n0 = p->Pa;
+      fold.n1 = p->Pc;
+      fold.part = p->fold_part;
+      fold.bad = p->fold_bad;
+      fold.cap = PpoPlan::kFoldCap;
+      fold.ticket = p->tickets + 2;
+      fold.ctl = p->ctl_d;
+      fold.lf = loss_finalize_of(p, k);
+      dd.fold = &fold;
+    }
+    UL_TRY(mlp_pass(p, nets, be, ml, s, false, &dd, e, k));
+    p->prep_folded = dd.folded;
     mark(p, 5, s);
-    return gather_ahead(p, e, k, s);
+    return UL_OK;
   }
   // K9 head
   PpoHeadArgs h{};
@@ -548,15 +599,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
 int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
   (void)e;
   const ul_ppo_bindings& b = p->b;
-  LossFinalize lf{};
-  lf.loss = p->red + p->Pa + p->Pc;
-  lf.log_std = b.actor_params + p->va.logstd_off;
-  lf.A = p->A;
-  lf.n = (double)p->mb;
-  lf.vcoef = p->d.value_loss_coef;
-  lf.ecoef = p->d.entropy_coef;
-  lf.last_in_epoch = k == p->d.minibatches - 1;
-  lf.st = p->st_d;
+  const LossFinalize lf = loss_finalize_of(p, k);
   SegTable st{};
   st.nseg = 2;
   st.g[0] = p->red;
@@ -574,7 +617,9 @@ int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
   StageOut so{};
   const bool tc = p->d.gemm_backend >= 1;
   if (tc) fill_stage_out(p, &so);
-  UL_TRY(launch_prepare(st, p->ctl_d, s, &lf));
+  // (folded: the step's gradient reduction already ran the prepare tail)
+  if (!p->prep_folded) UL_TRY(launch_prepare(st, p->ctl_d, s, &lf));
+  p->prep_folded = false;
   UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s, tc ? &so : nullptr));
   mark(p, 3, s);
   return UL_OK;
@@ -600,6 +645,10 @@ extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
   PpoPlan* p = new (std::nothrow) PpoPlan();
   UL_CHECK_ARG(p != nullptr, "ppo plan: out of host memory");
   p->d = *desc;
+  {
+    const char* e = getenv("UL_FOLD_PREP");  // read per plan (tests compare both)
+    p->fold_on = e ? atoi(e) != 0 : true;
+  }
   int st = ul::make_view(&desc->actor, &p->va);
   if (st == UL_OK) st = ul::make_view(&desc->critic, &p->vc);
   if (st != UL_OK) {

@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include "internal.cuh"
+#include "opt_tail.cuh"
 
 namespace ul {
 
@@ -114,111 +115,161 @@ __global__ void __launch_bounds__(W * 32) reduce_dw_kernel(ReduceTable tab) {
   }
 }
 
-// Every partial reduction of a pass in ONE launch.  Blocks [end[i-1], end[i])
-// belong to job i.  Shallow jobs (split-K dW, nz <= kShallowZ): one thread per
-// float4 column, all of its nz loads in flight, summed in z order.  Deep jobs
-// (per-block / per-CTA partial sets): 8 float4 columns per block, 32 z-phases
-// combined in fixed order.  Deterministic.
 constexpr int kShallowZ = 64;
 struct ReduceAll {
   ReduceJob r[kMaxReduceJobs];
   int end[kMaxReduceJobs];
   int n;
+  SqFold fold;
 };
 
-__device__ __forceinline__ void reduce_store(const ReduceJob& q, int64_t j, float4 t) {
+// (fold) value v stored at address a: sum of squares / finiteness per segment
+struct FoldAcc {
+  double s0 = 0.0, s1 = 0.0;
+  int bad = 0;
+  __device__ __forceinline__ void add(const SqFold& f, const float* a, float v) {
+    const int64_t o = (int64_t)((uintptr_t)a - (uintptr_t)f.base) / (int64_t)sizeof(float);
+    if (o >= 0 && o < f.n0) {
+      s0 += (double)v * (double)v;
+      bad |= isfinite(v) ? 0 : 1;
+    } else if (o >= f.n0 && o < f.n0 + f.n1) {
+      s1 += (double)v * (double)v;
+      bad |= isfinite(v) ? 0 : 2;
+    }
+  }
+};
+
+template <bool FOLD>
+__device__ __forceinline__ void reduce_store(const ReduceJob& q, int64_t j, float4 t, const SqFold& f,
+                                             FoldAcc& fa) {
   const float tv[4] = {t.x, t.y, t.z, t.w};
   if (q.kind == 0) {
     const int64_t r = j / q.ldp, c0 = j - r * q.ldp;  // 4 | ldp: one row per float4
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int64_t c = c0 + e;
-      if (c < q.in) q.gw[r * q.in + c] = tv[e];
-      else if (c == q.in && q.gb) q.gb[r] = tv[e];
+      float* dst = nullptr;
+      if (c < q.in) dst = q.gw + r * q.in + c;
+      else if (c == q.in && q.gb) dst = q.gb + r;
+      if (dst) {
+        *dst = tv[e];
+        if (FOLD) fa.add(f, dst, tv[e]);
+      }
     }
   } else {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int64_t c = j + e;
+      float* dst = nullptr;
       if (c < q.n0) {
-        if (q.o0) q.o0[c] = tv[e];
+        if (q.o0) dst = q.o0 + c;
       } else if (c < q.n0 + q.n1) {
-        if (q.o1) q.o1[c - q.n0] = tv[e];
+        if (q.o1) dst = q.o1 + (c - q.n0);
       } else if (c < q.n0 + q.n1 + q.n2) {
-        if (q.o2) q.o2[c - q.n0 - q.n1] = tv[e];
+        if (q.o2) dst = q.o2 + (c - q.n0 - q.n1);
+      }
+      if (dst) {
+        *dst = tv[e];
+        if (FOLD) fa.add(f, dst, tv[e]);
       }
     }
   }
 }
 
+// Every partial reduction of a pass in ONE launch.  Blocks [end[i-1], end[i])
+// belong to job i.  Shallow jobs (split-K dW, nz <= kShallowZ): one thread per
+// float4 column, all of its nz loads in flight, summed in z order.  Deep jobs
+// (per-block / per-CTA partial sets): 8 float4 columns per block, 32 z-phases
+// combined in fixed order.  Deterministic.  FOLD: the K13 prepare pass rides
+// along (SqFold) -- per-block sum g^2 / non-finite partials of the stored
+// gradients, the last block runs the prepare tail, so the Adam apply kernel
+// follows this launch directly.
+template <bool FOLD>
 __global__ void __launch_bounds__(256) reduce_all_kernel(const __grid_constant__ ReduceAll tab) {
   __shared__ float4 sm[8][32];
   int ji = 0;
   while (ji < tab.n - 1 && (int)blockIdx.x >= tab.end[ji]) ++ji;
   const ReduceJob& q = tab.r[ji];
   const int blk = (int)blockIdx.x - (ji ? tab.end[ji - 1] : 0);
+  FoldAcc fa;
   pdl_trigger();
   pdl_wait();
   const float* __restrict__ ws = q.src;
   const int nz = q.nz;
   if (nz <= kShallowZ) {
     const int64_t j = ((int64_t)blk * 256 + threadIdx.x) * 4;
-    if (j >= q.len) return;
+    if (j < q.len) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int z0 = 0; z0 < nz; z0 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = z0 + u < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)(z0 + u) * q.len + j))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+          acc.z += v[u].z;
+          acc.w += v[u].w;
+        }
+      }
+      reduce_store<FOLD>(q, j, acc, tab.fold, fa);
+    }
+  } else {
+    // deep sets: 8 float4 columns per CTA, 32 z-phases (the CTA's 256 threads)
+    // each summing z = phase, phase + 32, ... with 8 loads in flight, then a
+    // fixed-order combine of the phases
+    const int c8 = threadIdx.x & 7, ph = threadIdx.x >> 3;
+    const int64_t j = ((int64_t)blk * 8 + c8) * 4;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int z0 = 0; z0 < nz; z0 += 8) {
-      float4 v[8];
+    if (j < q.len) {
+      for (int z0 = ph; z0 < nz; z0 += 32 * 8) {
+        float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = z0 + u < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)(z0 + u) * q.len + j))
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 8; ++u) {
+          const int z = z0 + 32 * u;
+          v[u] = z < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * q.len + j))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc.x += v[u].x;
-        acc.y += v[u].y;
-        acc.z += v[u].z;
-        acc.w += v[u].w;
+        for (int u = 0; u < 8; ++u) {
+          acc.x += v[u].x;
+          acc.y += v[u].y;
+          acc.z += v[u].z;
+          acc.w += v[u].w;
+        }
       }
     }
-    reduce_store(q, j, acc);
-    return;
-  }
-  // deep sets: 8 float4 columns per CTA, 32 z-phases (the CTA's 256 threads)
-  // each summing z = phase, phase + 32, ... with 8 loads in flight, then a
-  // fixed-order combine of the phases
-  const int c8 = threadIdx.x & 7, ph = threadIdx.x >> 3;
-  const int64_t j = ((int64_t)blk * 8 + c8) * 4;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (j < q.len) {
-    for (int z0 = ph; z0 < nz; z0 += 32 * 8) {
-      float4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int z = z0 + 32 * u;
-        v[u] = z < nz ? __ldg(reinterpret_cast<const float4*>(ws + (int64_t)z * q.len + j))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4* sp = &sm[0][0];  // [32 phases][8 columns]
+    sp[ph * 8 + c8] = acc;
+    __syncthreads();
+    if (ph == 0 && j < q.len) {
+      float4 t = sp[c8];
+      for (int k = 1; k < 32; ++k) {
+        const float4 q4 = sp[k * 8 + c8];
+        t.x += q4.x;
+        t.y += q4.y;
+        t.z += q4.z;
+        t.w += q4.w;
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc.x += v[u].x;
-        acc.y += v[u].y;
-        acc.z += v[u].z;
-        acc.w += v[u].w;
-      }
+      reduce_store<FOLD>(q, j, t, tab.fold, fa);
     }
   }
-  float4* sp = &sm[0][0];  // [32 phases][8 columns]
-  sp[ph * 8 + c8] = acc;
-  __syncthreads();
-  if (ph == 0 && j < q.len) {
-    float4 t = sp[c8];
-    for (int k = 1; k < 32; ++k) {
-      const float4 q4 = sp[k * 8 + c8];
-      t.x += q4.x;
-      t.y += q4.y;
-      t.z += q4.z;
-      t.w += q4.w;
+  if constexpr (FOLD) {
+    __shared__ double scratch[32];
+    const SqFold& F = tab.fold;
+    const double t0 = block_sum(fa.s0, scratch);
+    const double t1 = block_sum(fa.s1, scratch + 16);
+    const int any0 = __syncthreads_or(fa.bad & 1), any1 = __syncthreads_or(fa.bad & 2);
+    if (threadIdx.x == 0) {
+      F.part[2 * blockIdx.x] = t0;
+      F.part[2 * blockIdx.x + 1] = t1;
+      F.bad[2 * blockIdx.x] = any0 ? 1 : 0;
+      F.bad[2 * blockIdx.x + 1] = any1 ? 1 : 0;
     }
-    reduce_store(q, j, t);
+    if (!last_block_ticket(F.ticket, gridDim.x)) return;
+    prepare_tail(2, F.part, F.bad, 2, F.ctl, F.lf, 1, (int)gridDim.x, scratch);
   }
 }
 
@@ -652,14 +703,21 @@ struct Lanes {
 };
 
 // one launch for up to kMaxReduceJobs fixed-order partial reductions
-int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
+// fold (may be null): run the K13 prepare pass inside the reduction when
+// every job fits one launch and the block partials fit the fold's arrays;
+// *folded (may be null) tells the caller whether it did
+int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s, const SqFold* fold = nullptr,
+                  bool* folded = nullptr) {
   static int one = -1;
   if (one < 0) {
     const char* e = getenv("UL_REDUCE_ONE");
     one = e ? atoi(e) != 0 : 1;
   }
+  if (folded) *folded = false;
   if (one) {
     // every job in one launch (reduce_all_kernel), kMaxReduceJobs per launch
+    int live = 0;
+    for (int q = 0; q < nj; ++q) live += (jobs[q].len > 0 && jobs[q].nz > 0) ? 1 : 0;
     for (int q = 0; q < nj;) {
       ReduceAll tab{};
       int blocks = 0;
@@ -671,8 +729,15 @@ int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s) {
         tab.end[tab.n++] = blocks;
       }
       if (tab.n == 0) continue;
-      UL_TRY(launch_pdl("reduce_all_kernel", reduce_all_kernel, dim3((unsigned)blocks), dim3(256),
-                        0, s, tab));
+      if (fold && fold->on && live <= kMaxReduceJobs && blocks <= fold->cap) {
+        tab.fold = *fold;
+        UL_TRY(launch_pdl("reduce_all_kernel", reduce_all_kernel<true>, dim3((unsigned)blocks),
+                          dim3(256), 0, s, tab));
+        if (folded) *folded = true;
+      } else {
+        UL_TRY(launch_pdl("reduce_all_kernel", reduce_all_kernel<false>, dim3((unsigned)blocks),
+                          dim3(256), 0, s, tab));
+      }
     }
     return UL_OK;
   }
@@ -891,7 +956,8 @@ int run_deferred_dw_gemms(DeferredDw& D, cudaStream_t s) {
 }
 
 int run_deferred_dw_reduce(DeferredDw& D, cudaStream_t s) {
-  if (D.nj) UL_TRY(launch_reduce(D.jobs, D.nj, s));
+  D.folded = false;
+  if (D.nj) UL_TRY(launch_reduce(D.jobs, D.nj, s, D.fold, &D.folded));
   D.ndw = D.nj = 0;
   return UL_OK;
 }

@@ -20,110 +20,12 @@
 #include <cuda_bf16.h>
 
 #include "internal.cuh"
+#include "opt_tail.cuh"
 
 namespace ul {
 namespace {
 
 constexpr int kPrepThreads = 256;
-
-constexpr double kLog2PiO = 1.8378770664093453;
-
-// Runs in ONE CTA (blockDim 256).  Every global value it depends on is loaded
-// up front with the loads in flight together -- the controller / stats
-// records sit behind pointers the compiler must assume alias, so written as
-// a chain of read-modify-writes the tail was ~10 us of serial load latency.
-// (partials: sum g^2 of segment s from block b at part[b * ldp + s], its
-// non-finite flag at bad[b * ldp + s])
-__device__ __noinline__ void prepare_tail(int nseg, const double* part, const int* bad_part,
-                                          int ldp, ul_opt_ctl* ctl, const LossFinalize& lf,
-                                          int has_lf, int nb, double* scratch) {
-  __shared__ double red[UL_MAX_SEG];
-  __shared__ int red_bad[UL_MAX_SEG];
-  __shared__ double lstd[UL_MAX_ACT];
-  // all segments' partials in one sweep (fixed per-thread order, then the
-  // fixed-order block sum: deterministic)
-  double acc[UL_MAX_SEG] = {0.0, 0.0, 0.0, 0.0};
-  int bad[UL_MAX_SEG] = {0, 0, 0, 0};
-  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-#pragma unroll
-    for (int s = 0; s < UL_MAX_SEG; ++s)
-      if (s < nseg) {
-        acc[s] += part[(int64_t)b * ldp + s];
-        bad[s] |= bad_part[(int64_t)b * ldp + s];
-      }
-  }
-  if (has_lf && (int)threadIdx.x < lf.A) lstd[threadIdx.x] = (double)lf.log_std[threadIdx.x];
-#pragma unroll
-  for (int s = 0; s < UL_MAX_SEG; ++s) {
-    if (s >= nseg) break;
-    const double tot = block_sum(acc[s], scratch);
-    const int any_bad = __syncthreads_or(bad[s]);
-    if (threadIdx.x == 0) {
-      red[s] = tot;
-      red_bad[s] = any_bad;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  // ---- loads (independent, issued together)
-  const int loss_bad = ctl->loss_bad, was_diverged = ctl->diverged, steps = ctl->steps;
-  const double max_norm = ctl->max_norm;
-  int64_t t[UL_MAX_SEG];
-#pragma unroll
-  for (int s = 0; s < UL_MAX_SEG; ++s) t[s] = s < nseg ? ctl->t[s] : 0;
-  float loss[3] = {0.f, 0.f, 0.f};
-  ul_ppo_stats st{};
-  if (has_lf) {
-    loss[0] = lf.loss[0];
-    loss[1] = lf.loss[1];
-    loss[2] = lf.loss[2];
-    st = *lf.st;
-  }
-  // ---- R:algos/ppo.py loss bookkeeping of the step (see heads.cu)
-  int earlier_bad = loss_bad;
-  if (has_lf) {
-    const double pol = -(double)loss[0] / lf.n;
-    const double val = (double)loss[1] / lf.n;
-    const double kl = (double)loss[2] / lf.n;
-    double ent = 0.0;
-    for (int j = 0; j < lf.A; ++j) ent += lstd[j] + 0.5 * (kLog2PiO + 1.0);
-    const double total = pol + lf.vcoef * val - lf.ecoef * ent;
-    if (!isfinite(total)) earlier_bad = 1;
-    if (!was_diverged && isfinite(total)) {
-      st.policy_sum += pol;
-      st.value_sum += val;
-      st.entropy_sum += ent;
-      st.kl_last = kl;
-      if (lf.last_in_epoch) st.kl_epoch_sum += kl;
-      st.steps += 1;
-      *lf.st = st;
-    }
-  }
-  // ---- joint norm, per-segment update decision (reference order: loss
-  // check, then segment 0 finiteness, then segment 1, ...), divergence latch
-  double joint = 0.0;
-  for (int s = 0; s < nseg; ++s) {
-    const double sum = red[s];
-    const int sbad = red_bad[s];
-    ctl->sumsq[s] = sum;
-    ctl->seg_bad[s] = sbad;
-    joint += sum;
-    earlier_bad |= sbad;
-    const int upd = !was_diverged && !earlier_bad;
-    ctl->seg_update[s] = upd;
-    if (upd) ctl->t[s] = t[s] + 1;
-  }
-  const double norm = sqrt(joint);
-  ctl->norm = norm;
-  // reference: factor applied only when max_norm > 0 and total > max_norm (NaN -> no clip)
-  ctl->factor = (max_norm > 0.0 && norm > max_norm) ? max_norm / (norm + 1e-12) : 1.0;
-  if (earlier_bad && !was_diverged) {
-    ctl->diverged = 1;
-    ctl->fail_step = steps;
-  }
-  ctl->loss_bad = 0;
-  ctl->steps = steps + 1;
-}
 
 __global__ void __launch_bounds__(kPrepThreads) prepare_kernel(SegTable st, ul_opt_ctl* ctl,
                                                                LossFinalize lf, int has_lf) {
@@ -364,16 +266,40 @@ __global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, in
   __shared__ ApplyCtl c;
   __shared__ AdamScalars k;  // (bias corrections: two f64 pow per CTA, not per thread)
   pdl_trigger();
-  pdl_wait();
   const int s = blockIdx.y;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // The thread's first float4 of m, v, p is loaded BEFORE the dependency
+  // wait: only an earlier Adam apply writes them, and that one completed
+  // before this step's forward GEMMs ran (the kernels this launch may overlap
+  // -- the gradient reduction / prepare -- never touch them).  g and the
+  // controller come after the wait.
+  bool pre = false;
+  AdamVec a0{};
+  if (s < st.nseg && do_adam) {
+    const bool vec =
+        (((uintptr_t)st.g[s] | (uintptr_t)st.m[s] | (uintptr_t)st.v[s] | (uintptr_t)st.p[s]) & 15) == 0;
+    if (vec && t0 < st.n[s] / 4) {
+      pre = true;
+      a0.m = reinterpret_cast<const float4*>(st.m[s])[t0];
+      a0.v = reinterpret_cast<const float4*>(st.v[s])[t0];
+      a0.p = reinterpret_cast<const float4*>(st.p[s])[t0];
+    }
+  }
+  pdl_wait();
   if (s >= st.nseg) return;
   if (threadIdx.x == 0) {
     read_apply_ctl(ctl, st.nseg, &c);
     if (do_adam) k = adam_scalars(c, s);
   }
+  if (pre) a0.g = reinterpret_cast<const float4*>(st.g[s])[t0];
   __syncthreads();
-  apply_seg(st, c, k, s, write_grads, do_adam, so, has_so,
-            (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+  if (pre && c.upd[s]) {
+    adam4(st, s, t0, a0, k, (float)c.factor, c.factor != 1.0, write_grads, so, has_so);
+    apply_seg(st, c, k, s, write_grads, do_adam, so, has_so, t0, stride, t0 + stride);
+  } else {
+    apply_seg(st, c, k, s, write_grads, do_adam, so, has_so, t0, stride);
+  }
 }
 
 __global__ void polyak_kernel(float* __restrict__ tgt, const float* __restrict__ src, int64_t n,
