@@ -452,17 +452,22 @@ __global__ void __launch_bounds__(kFThr, 3) ppo_fused_kernel(const __grid_consta
 
 
 // ---------------------------------------------------------------------------
-// Tensor-core variant (bf16 rows, A <= 32, K <= 256): the three small products
-// of the output layers run on warp-level mma.sync m16n8k16 (bf16 in, fp32
-// accumulate): mean = h W^T (M = rows, N = action dims), dh = dmean W
-// (K = action dims; the forward accumulator fragments are re-packed in
-// registers as the A operand) and dW = dmean^T h over the tile's rows
-// (ldmatrix.trans feeds h as the column-major B operand).  The critic's
-// one-output layer stays on SIMT lanes.  64 rows per block, 4 warps; warp w
-// owns rows [16w, 16w + 16) for the row-local phases and output columns
-// {8 n : n = w (mod 4)} for dW, so no cross-warp dW reduction is needed.
-// W_a arrives as the Adam-refreshed bf16 staged copy (cp.async); its
-// transpose for the dh product comes from ldmatrix.trans.
+// Tensor-core variant (bf16 rows, A <= 32, K <= 256).  Two CTA roles per
+// 64-row tile (grid.y = 2): every quantity of one network's output stage is
+// row-local or a column sum over the tile, so the networks never exchange data.
+//  actor (y = 0): the three small products on warp-level mma.sync m16n8k16
+//    (bf16 in, fp32 accumulate) -- mean = h W^T, dh = dmean W (the dmean
+//    fragments re-packed in registers as the A operand) and dW = dmean^T h
+//    over the tile's rows (ldmatrix.trans feeds h as the column-major B
+//    operand) -- around the Gaussian log-prob / clipped surrogate in float64;
+//  critic (y = 1): v = h w + b, the clipped value loss, dh = dv w * elu'(h),
+//    dw and colsum(dh) on SIMT lanes.
+// 4 warps; actor warp w owns rows [16w, 16w + 16) for the row-local phases and
+// output columns {8 n : n = w (mod 4)} for dW (no cross-warp dW reduction).
+// W_a arrives as the Adam-refreshed bf16 staged copy (cp.async).  Split roles
+// halve each CTA's serial chain and shared memory, so the whole grid (2 x 384
+// CTAs at cfg2) is resident at once; tile staging loops carry no per-element
+// integer division.
 constexpr int kMRows = 64, kMThr = 128, kMWarps = 4;
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
@@ -492,113 +497,105 @@ __device__ __forceinline__ float2 up_bf16(uint32_t u) {
 }
 
 __host__ __device__ inline int rup16(int k) { return (k + 15) / 16 * 16; }
+__host__ __device__ inline size_t al16(size_t o) { return (o + 15) / 16 * 16; }
 
-// dynamic smem layout (bytes) of the tensor-core variant
-struct MmaSmem {
-  int ka, kc, pa, pc, pwa, pdm;
-  size_t o_hc, o_wa, o_dm, o_wc, o_dv, o_cs, o_dh, total;
-  __host__ __device__ MmaSmem(int Ka, int Kc, int NJT) {
+// dynamic smem layouts (bytes) of the two roles
+struct ActorSmem {
+  int ka, pa, pwa, pdm;
+  size_t o_wa, o_dm, o_cs, o_dh, total;
+  __host__ __device__ ActorSmem(int Ka, int NJT) {
     ka = rup16(Ka);
-    kc = rup8(Kc);
-    pa = ka + 8;               // bf16 row pitch of the h_a tile (16 B aligned, conflict-free)
-    pc = kc + 8;
-    pwa = ka + 8;              // W_a  [NJT*8][pwa] bf16 (B of the forward; .trans: B of dh)
-    pdm = kMRows + 8;          // dmean^T [NJT*8][pdm] bf16 (A operand of dW)
+    pa = ka + 8;        // bf16 row pitch of the h_a tile (16 B aligned, conflict-free)
+    pwa = ka + 8;       // W_a  [NJT*8][pwa] bf16 (B of the forward; .trans: B of dh)
+    pdm = kMRows + 8;   // dmean^T [NJT*8][pdm] bf16 (A operand of dW)
     size_t o = (size_t)kMRows * pa * 2;
-    o_hc = o;
-    o += (size_t)kMRows * pc * 2;
     o_wa = o;
     o += (size_t)NJT * 8 * pwa * 2;
     o_dm = o;
     o += (size_t)NJT * 8 * pdm * 2;
-    o = (o + 15) / 16 * 16;
-    o_wc = o;
-    o += (size_t)kc * 4;
-    o_dv = o;
-    o += (size_t)kMRows * 4 * 2;  // v (forward) and dv, fp32
-    o_cs = o;
-    o += (size_t)kMWarps * ka * 4 + (size_t)kMWarps * 32 * 4 + (size_t)2 * kMWarps * kc * 4;
-    o = (o + 15) / 16 * 16;
-    o_dh = o;                  // dh_a tile [kMRows][pa] bf16 (coalesced store + column sums)
+    o = al16(o);
+    o_cs = o;           // colsum(dh_a) [ka], then db_a [warps][32]
+    o += (size_t)ka * 4 + (size_t)kMWarps * 32 * 4;
+    o = al16(o);
+    o_dh = o;           // dh_a tile [kMRows][pa] bf16 (coalesced store + column sums)
     o += (size_t)kMRows * pa * 2;
     total = o;
   }
 };
+struct CriticSmem {
+  int kc, pc;
+  size_t o_wc, o_v, o_cr, total;
+  __host__ __device__ CriticSmem(int Kc) {
+    kc = rup8(Kc);
+    pc = kc + 8;
+    size_t o = al16((size_t)kMRows * pc * 2);
+    o_wc = o;
+    o += (size_t)kc * 4;
+    o_v = o;            // v (forward) and dv, fp32
+    o += (size_t)kMRows * 4 * 2;
+    o_cr = o;           // [warps][kc] dw_c, then [warps][kc] colsum(dh_c)
+    o += (size_t)2 * kMWarps * kc * 4;
+    total = o;
+  }
+};
+
+// cp.async of rows [0, R) of a bf16 row block (row rr = global row r0 + rr,
+// valid while < nvalid; granules of 8 past k, and invalid rows, zero-filled)
+// into rows of pitch P.  Thread t owns granule u = t % gt of rows t / gt,
+// t / gt + kMThr / gt, ...  (gt = kpad / 8 <= 32).
+__device__ __forceinline__ void stage_bf16_rows(const void* g, int64_t ld, int64_t r0,
+                                                int64_t nvalid, int R, int k, int kpad,
+                                                __nv_bfloat16* s, int P) {
+  const int gdat = (k + 7) / 8, gt = kpad / 8;
+  const int rstep = kMThr / gt;
+  const int t = threadIdx.x;
+  if (t >= rstep * gt) return;
+  const int u = t % gt;
+  const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(g);
+  for (int rr = t / gt; rr < R; rr += rstep) {
+    const int64_t gr = r0 + rr;
+    const bool ok = gr < nvalid && u < gdat;
+    cpa16(s + rr * P + u * 8, gb + (ok ? gr * ld + u * 8 : 0), ok);
+  }
+}
 
 template <int NJT>  // n-tiles of 8 action dims: A <= 8 * NJT (NJT = 2 or 4)
-__global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_constant__ PpoFusedArgs f) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__device__ __forceinline__ void fused_actor(const PpoFusedArgs& f, uint8_t* smem) {
   constexpr int MT = NJT / 2;  // 16-row m tiles of action dims (dW) = k16 steps of dh
   const PpoHeadArgs& a = f.h;
-  const int Ka = f.Ka, Kc = f.Kc, A = a.A, nq = 3 + A;
-  const MmaSmem L(Ka, Kc, NJT);
-  const int ka = L.ka, kc = L.kc;
+  const int Ka = f.Ka, A = a.A, nq = 3 + A;
+  const ActorSmem L(Ka, NJT);
+  const int ka = L.ka;
   __nv_bfloat16* sha = reinterpret_cast<__nv_bfloat16*>(smem);
-  __nv_bfloat16* shc = reinterpret_cast<__nv_bfloat16*>(smem + L.o_hc);
   __nv_bfloat16* swa = reinterpret_cast<__nv_bfloat16*>(smem + L.o_wa);
   __nv_bfloat16* sdm = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dm);
-  float* swc = reinterpret_cast<float*>(smem + L.o_wc);
-  float* sv = reinterpret_cast<float*>(smem + L.o_dv);  // [128] v, then [128] dv
-  float* sdv = sv + kMRows;
-  float* scs = reinterpret_cast<float*>(smem + L.o_cs);  // [warps][ka] colsum(dh_a)
-  float* sdb = scs + kMWarps * ka;                       // [warps][32] db_a
-  float* scrit = sdb + kMWarps * 32;                     // [warps][kc] dw_c, then colsum(dh_c)
+  float* scs = reinterpret_cast<float*>(smem + L.o_cs);  // [ka] colsum(dh_a)
+  float* sdb = scs + ka;                                 // [warps][32] db_a
+  __nv_bfloat16* sdh = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dh);
   __shared__ double s_ls[UL_MAX_ACT], s_isd[UL_MAX_ACT];
   __shared__ double red[kMWarps][3 + UL_MAX_ACT];
   __shared__ double s_lsum;
-  __shared__ float s_b[UL_MAX_ACT + 1];
+  __shared__ float s_b[UL_MAX_ACT];
 
   const int t = threadIdx.x, lane = t & 31, w = t >> 5, g = lane >> 2, q = lane & 3;
   const int64_t r0 = (int64_t)blockIdx.x * kMRows;
   const int64_t M = a.n_local;
-  pdl_trigger();
-  pdl_wait();
-  // ---- stage h tiles (cp.async; granules past the row's data zero-filled)
-  {
-    const int ga = (Ka + 7) / 8, gt = ka / 8;  // granules with data / per staged row
-    for (int e = t; e < kMRows * gt; e += kMThr) {
-      const int rr = e / gt, u = e - rr * gt;
-      const int64_t gr = r0 + rr;
-      const bool ok = gr < M && u < ga;
-      cpa16(sha + rr * L.pa + u * 8,
-            reinterpret_cast<const __nv_bfloat16*>(f.ha) + (ok ? gr * f.ldha + u * 8 : 0), ok);
-    }
-    const int gc = (Kc + 7) / 8, gtc = kc / 8;
-    for (int e = t; e < kMRows * gtc; e += kMThr) {
-      const int rr = e / gtc, u = e - rr * gtc;
-      const int64_t gr = r0 + rr;
-      const bool ok = gr < M && u < gc;
-      cpa16(shc + rr * L.pc + u * 8,
-            reinterpret_cast<const __nv_bfloat16*>(f.hc) + (ok ? gr * f.ldhc + u * 8 : 0), ok);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  // ---- weights: the staged bf16 W_a rows (cp.async, zero past A / Ka), w_c
-  // fp32, biases, log_std
-  {
-    const int ga = (Ka + 7) / 8, gt = ka / 8;
-    for (int e = t; e < NJT * 8 * gt; e += kMThr) {
-      const int j = e / gt, u = e - j * gt;
-      const bool okw = j < A && u < ga;
-      cpa16(swa + j * L.pwa + u * 8,
-            reinterpret_cast<const __nv_bfloat16*>(f.wba) + (okw ? j * f.ldwb + u * 8 : 0), okw);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  for (int c = t; c < kc; c += kMThr) swc[c] = c < Kc ? __ldg(f.Wc + c) : 0.f;
+  // ---- h_a tile and the staged bf16 W_a rows (cp.async, zero past A / Ka)
+  stage_bf16_rows(f.ha, f.ldha, r0, M, kMRows, Ka, ka, sha, L.pa);
+  stage_bf16_rows(f.wba, f.ldwb, 0, A, NJT * 8, Ka, ka, swa, L.pwa);
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int j = t; j < A; j += kMThr) {
     const double ls = (double)a.log_std[j];
     s_ls[j] = ls;
     s_isd[j] = exp(-ls);
     s_b[j] = f.ba[j];
   }
-  if (t == 0) s_b[UL_MAX_ACT] = f.bc[0];
   // this lane's rows (R0 = 16w + g, R1 = R0 + 8) and action dims
   // j = 8 nt + 2q + {0, 1}: row scalars and actions, loads in flight now
   const int R[2] = {16 * w + g, 16 * w + g + 8};
   bool ok[2];
   float act[2][NJT][2];
-  double blogp[2], advr[2], ret[2], oldv[2];
+  double blogp[2], advr[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t gr = r0 + R[h];
@@ -612,9 +609,9 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
       }
     blogp[h] = ok[h] ? (double)a.blogp[gr] : 0.0;
     advr[h] = ok[h] ? (double)a.adv[gr] : 0.0;
-    ret[h] = ok[h] ? (double)a.ret[gr] : 0.0;
-    oldv[h] = ok[h] ? (double)a.oldv[gr] : 0.0;
   }
+  const double adv_mean = a.adv_stats ? a.adv_stats[0] : 0.0;
+  const double adv_den = a.adv_stats ? a.adv_stats[1] + 1e-8 : 1.0;
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   if (t == 0) {
@@ -622,20 +619,7 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
     for (int j = 0; j < A; ++j) s += s_ls[j];
     s_lsum = s;
   }
-  // ---- critic forward (SIMT): two threads per row, halves of the columns
-  {
-    const int row = t >> 1, half = t & 1;
-    const int c0 = half * (kc / 2), c1 = half ? kc : kc / 2;
-    float s = 0.f;
-    const __nv_bfloat16* hr = shc + row * L.pc;
-    for (int c = c0; c < c1; c += 2) {
-      const float2 hv = up_bf16(*reinterpret_cast<const uint32_t*>(hr + c));
-      s = fmaf(hv.x, swc[c], fmaf(hv.y, swc[c + 1], s));
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (!half) sv[row] = s + s_b[UL_MAX_ACT];
-  }
-  // ---- actor forward on the tensor cores: acc[nt] = h[16 rows] W^T (8 dims)
+  // ---- forward on the tensor cores: acc[nt] = h[16 rows] W^T (8 dims)
   float acc[NJT][4];
 #pragma unroll
   for (int nt = 0; nt < NJT; ++nt)
@@ -651,36 +635,33 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
                *reinterpret_cast<const uint32_t*>(bp + 8));
     }
   }
-  __syncthreads();  // s_lsum, sv
-  // ---- K9 loss head in float64 (rows R0, R1; the quad of lanes sharing g
+  __syncthreads();  // s_lsum
+  // ---- K9 policy head in float64 (rows R0, R1; the quad of lanes sharing g
   // splits the action dims), as ppo_head_kernel
-  double z[2][NJT][2];
-  double pol = 0.0, val = 0.0, kl = 0.0, dls[NJT][2];
+  double pol = 0.0, kl = 0.0, dls[NJT][2];
 #pragma unroll
   for (int nt = 0; nt < NJT; ++nt) dls[nt][0] = dls[nt][1] = 0.0;
   float dm[2][NJT][2];
-  float dvv[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
+    double z[NJT][2];
     double zp = 0.0;
 #pragma unroll
     for (int nt = 0; nt < NJT; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int j = 8 * nt + 2 * q + e;
-        z[h][nt][e] = 0.0;
+        z[nt][e] = 0.0;
         if (j < A) {
           const double mean = (double)(acc[nt][2 * h + e] + s_b[j]);
-          z[h][nt][e] = ((double)act[h][nt][e] - mean) * s_isd[j];
-          zp += z[h][nt][e] * z[h][nt][e];
+          z[nt][e] = ((double)act[h][nt][e] - mean) * s_isd[j];
+          zp += z[nt][e] * z[nt][e];
         }
       }
     zp += __shfl_xor_sync(0xffffffffu, zp, 1);
     zp += __shfl_xor_sync(0xffffffffu, zp, 2);
-    double dlogp = 0.0, dv = 0.0;
+    double dlogp = 0.0;
     if (ok[h]) {
-      const double adv_mean = a.adv_stats ? a.adv_stats[0] : 0.0;
-      const double adv_den = a.adv_stats ? a.adv_stats[1] + 1e-8 : 1.0;
       const double logp = -s_lsum - A * (0.5 * kLog2PiF) - 0.5 * zp;
       const double adv = (advr[h] - adv_mean) / adv_den;
       const double ratio = exp(logp - blogp[h]);
@@ -692,20 +673,7 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
         kl += blogp[h] - logp;
       }
       dlogp = (s1 <= s2) ? -adv * ratio / a.n_global : 0.0;
-      const double v = (double)sv[R[h]];
-      double vl;
-      if (a.clipped_v) {
-        const double vc = oldv[h] + fmin(fmax(v - oldv[h], -a.clip), a.clip);
-        const double lu = (v - ret[h]) * (v - ret[h]), lc = (vc - ret[h]) * (vc - ret[h]);
-        vl = fmax(lu, lc);
-        dv = lu >= lc ? 2.0 * (v - ret[h]) / a.n_global : 0.0;
-      } else {
-        vl = (v - ret[h]) * (v - ret[h]);
-        dv = 2.0 * (v - ret[h]) / a.n_global;
-      }
-      if (q == 0) val += vl;
     }
-    dvv[h] = (float)(dv * a.vcoef);
 #pragma unroll
     for (int nt = 0; nt < NJT; ++nt)
 #pragma unroll
@@ -713,14 +681,10 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
         const int j = 8 * nt + 2 * q + e;
         dm[h][nt][e] = 0.f;
         if (j < A) {
-          dm[h][nt][e] = (float)(dlogp * z[h][nt][e] * s_isd[j]);
-          dls[nt][e] += dlogp * (z[h][nt][e] * z[h][nt][e] - 1.0);
+          dm[h][nt][e] = (float)(dlogp * z[nt][e] * s_isd[j]);
+          dls[nt][e] += dlogp * (z[nt][e] * z[nt][e] - 1.0);
         }
       }
-  }
-  if (q == 0) {
-    sdv[R[0]] = dvv[0];
-    sdv[R[1]] = dvv[1];
   }
   // dmean^T (bf16) for the dW product; db_a and dlog_std partials of the warp
 #pragma unroll
@@ -745,13 +709,12 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
   {
     double v = warp_sum(pol);
     if (lane == 0) red[w][0] = v;
-    v = warp_sum(val);
-    if (lane == 0) red[w][1] = v;
     v = warp_sum(kl);
     if (lane == 0) red[w][2] = v;
   }
-  // ---- dh_a = (dmean W) * elu'(h_a) on the tensor cores; the forward
-  // accumulators, rounded to bf16, are the A operand (k = action dims)
+  // ---- dh_a = (dmean W) * elu'(h_a) on the tensor cores; the dmean
+  // fragments, rounded to bf16, are the A operand (k = action dims); results
+  // to a shared-memory tile, then coalesced 16-byte stores + column sums
   {
     uint32_t af[MT][4];
 #pragma unroll
@@ -761,10 +724,6 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
       af[m][2] = pk_bf16(dm[0][2 * m + 1][0], dm[0][2 * m + 1][1]);
       af[m][3] = pk_bf16(dm[1][2 * m + 1][0], dm[1][2 * m + 1][1]);
     }
-    // results go to a shared-memory tile first; the whole CTA then writes it
-    // with coalesced 16-byte stores and takes the column sums (no per-tile
-    // shuffles or 4-byte global stores in this loop)
-    __nv_bfloat16* sdh = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dh);
     for (int nc = 0; nc < ka / 8; ++nc) {
       float d[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -786,94 +745,41 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
       *reinterpret_cast<uint32_t*>(sdh + R[1] * L.pa + c) = pk_bf16(d[2], d[3]);
     }
   }
-  __syncthreads();  // sdh complete
+  __syncthreads();  // sdh, sdm, sdb complete
   {
-    __nv_bfloat16* sdh = reinterpret_cast<__nv_bfloat16*>(smem + L.o_dh);
-    const int gk = ka / 8;  // 16-byte granules per row
+    const int gk = ka / 8;  // 16-byte granules per row (<= 32)
+    const int rstep = kMThr / gk;
     const bool vec = (Ka % 8) == 0 && (f.lddha % 8) == 0;
-    for (int e = t; e < kMRows * gk; e += kMThr) {
-      const int rr = e / gk, u = e - rr * gk;
-      const int64_t gr = r0 + rr;
-      const int c = 8 * u;
-      if (gr >= M || c >= Ka) continue;
-      __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(f.dha) + gr * f.lddha + c;
-      if (vec) {
-        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(sdh + rr * L.pa + c);
-      } else {
-        for (int k2 = 0; k2 < 8 && c + k2 < Ka; ++k2) dst[k2] = sdh[rr * L.pa + c + k2];
+    if (t < rstep * gk) {
+      const int u = t % gk, c = 8 * u;
+      for (int rr = t / gk; rr < kMRows; rr += rstep) {
+        const int64_t gr = r0 + rr;
+        if (gr >= M || c >= Ka) continue;
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(f.dha) + gr * f.lddha + c;
+        if (vec) {
+          *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(sdh + rr * L.pa + c);
+        } else {
+          for (int k2 = 0; k2 < 8 && c + k2 < Ka; ++k2) dst[k2] = sdh[rr * L.pa + c + k2];
+        }
       }
     }
-    // colsum(dh_a) per column over the tile's rows, as the values were
-    // stored (bf16): one thread per column, fixed row order (the per-warp
-    // slots of scs keep the downstream fixed-order fold: warp 0 holds all)
+    // colsum(dh_a) per column over the tile's rows, as the values were stored
+    // (bf16): two columns per thread pass, fixed row order
     if (f.csa)
-      for (int c = t; c < ka; c += kMThr) {
-        float s = 0.f;
+      for (int c2 = 2 * t; c2 < ka; c2 += 2 * kMThr) {
+        float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
-        for (int rr = 0; rr < kMRows; ++rr) s += __bfloat162float(sdh[rr * L.pa + c]);
-        scs[c] = s;
-        for (int k = 1; k < kMWarps; ++k) scs[k * ka + c] = 0.f;
-      }
-  }
-  __syncthreads();  // sdm, sdv, scs, sdb complete
-  // ---- critic backward (SIMT): thread = (8-column group, rows rg, rg + R/.. ),
-  // 16-byte row loads / stores; dw_c and colsum(dh_c) reduced over the row
-  // groups (lane pairs, then warps in fixed order)
-  {
-    const int ncg = kc / 8;                  // column groups (<= 32)
-    const int nrg = kMThr / ncg;             // row groups
-    const int cg = t % ncg, rg = t / ncg;
-    float dw[8], cs[8], wcc[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      dw[e] = cs[e] = 0.f;
-      wcc[e] = swc[8 * cg + e];
-    }
-    if (rg < nrg) {
-      for (int row = rg; row < kMRows; row += nrg) {
-        const uint4 hv = *reinterpret_cast<const uint4*>(shc + row * L.pc + 8 * cg);
-        const float dvr = sdv[row];
-        const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
-        uint32_t ow[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 hh = up_bf16(hw[e]);
-          const float d0 = dvr * wcc[2 * e] * (fminf(hh.x, 0.f) + 1.f);
-          const float d1 = dvr * wcc[2 * e + 1] * (fminf(hh.y, 0.f) + 1.f);
-          dw[2 * e] = fmaf(dvr, hh.x, dw[2 * e]);
-          dw[2 * e + 1] = fmaf(dvr, hh.y, dw[2 * e + 1]);
-          cs[2 * e] += d0;
-          cs[2 * e + 1] += d1;
-          ow[e] = pk_bf16(d0, d1);
+        for (int rr = 0; rr < kMRows; ++rr) {
+          const float2 v = up_bf16(*reinterpret_cast<const uint32_t*>(sdh + rr * L.pa + c2));
+          s0 += v.x;
+          s1 += v.y;
         }
-        const int c = 8 * cg;
-        if (r0 + row < M && c < Kc) {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(f.dhc) + (r0 + row) * f.lddhc + c;
-          if (c + 8 <= Kc && ((f.lddhc & 7) == 0)) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-          } else {
-            const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(ow);
-            for (int e = 0; e < 8 && c + e < Kc; ++e) dst[e] = ob[e];
-          }
-        }
-      }
-    }
-    // row groups of one warp: lanes l, l + ncg, ... share cg
-    for (int o = ncg; o < 32; o <<= 1)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        dw[e] += __shfl_xor_sync(0xffffffffu, dw[e], o);
-        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], o);
-      }
-    if (lane < ncg)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        scrit[w * kc + 8 * lane + e] = dw[e];
-        scrit[kMWarps * kc + w * kc + 8 * lane + e] = cs[e];
+        scs[c2] = s0;
+        scs[c2 + 1] = s1;
       }
   }
   // ---- dW_a partial = dmean^T h over the block's rows (tensor cores): warp
-  // w owns output columns 8 nt, nt = w, w + 8, ...
+  // w owns output columns 8 nt, nt = w, w + 4, ...
   float* pa = f.parta + (int64_t)blockIdx.x * f.plena;
   for (int nt = w; nt < ka / 8; nt += kMWarps) {
     float d[MT][4];
@@ -882,8 +788,6 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
 #pragma unroll
       for (int e = 0; e < 4; ++e) d[m][e] = 0.f;
     for (int kr = 0; kr < kMRows; kr += 16) {
-      // B (k = rows, n = columns) from the row-major h tile, transposed by
-      // ldmatrix: lanes 0-15 address rows kr..kr+15 of column group nt
       uint32_t bf[4];
       ldsm_x4_t(bf, sha + (kr + (lane & 15)) * L.pa + 8 * nt);  // (x4: both halves identical)
 #pragma unroll
@@ -913,9 +817,8 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
       }
     }
   }
-  __syncthreads();  // scrit complete
-  // ---- remaining partials in fixed order: db_a, colsum(dh_a), critic
-  float* pc = f.partc + (int64_t)blockIdx.x * f.plenc;
+  __syncthreads();  // scs complete
+  // ---- remaining partials in fixed order: db_a, colsum(dh_a)
   if (t < A) {
     float s = 0.f;
 #pragma unroll
@@ -923,78 +826,174 @@ __global__ void __launch_bounds__(kMThr, 4) ppo_fused_mma_kernel(const __grid_co
     pa[(int64_t)A * Ka + t] = s;
   }
   if (f.csa)
-    for (int c = t; c < Ka; c += kMThr) {
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < kMWarps; ++k) s += scs[k * ka + c];
-      pa[(int64_t)A * Ka + A + c] = s;
-    }
-  {
-    for (int c = t; c < Kc; c += kMThr) {
-      float dw = 0.f, cs = 0.f;
-#pragma unroll
-      for (int k = 0; k < kMWarps; ++k) {
-        dw += scrit[k * kc + c];
-        cs += scrit[kMWarps * kc + k * kc + c];
-      }
-      pc[c] = dw;
-      if (f.csc) pc[Kc + 1 + c] = cs;
-    }
-    if (t == 0) {
-      float s = 0.f;
-      for (int rr = 0; rr < kMRows; ++rr) s += sdv[rr];
-      pc[Kc] = s;
-    }
-  }
-  // ---- loss / dlog_std partials, last CTA folds them in fixed order
-  if (f.lossp) {  // reduced with the pass's other partials (no last-CTA fold)
-    float* lp = f.lossp + (int64_t)blockIdx.x * f.lossld;
-    for (int qq = t; qq < f.lossld; qq += kMThr) {
-      double v = 0.0;
-      if (qq < nq) {
-        for (int k = 0; k < kMWarps; ++k) v += red[k][qq];
-        if (blockIdx.x == 0 && qq >= 3) v += a.ent_coef_add;
-      }
-      lp[qq] = (float)v;
-    }
-    return;
-  }
-  double* part = a.part + (int64_t)blockIdx.x * nq;
-  for (int qq = t; qq < nq; qq += kMThr) {
-    double s = 0.0;
-    for (int k = 0; k < kMWarps; ++k) s += red[k][qq];
-    part[qq] = s;
-  }
-  if (!last_block_ticket(a.ticket, gridDim.x)) return;
-  const unsigned nb = gridDim.x;
-  for (int q0 = 0; q0 < nq; q0 += kMThr / 8) {
-    const int qq = q0 + (t >> 3), l = t & 7;
-    double s = 0.0;
+    for (int c = t; c < Ka; c += kMThr) pa[(int64_t)A * Ka + A + c] = scs[c];
+  // ---- policy-loss / kl / dlog_std partials (slot 1, the value loss, is the
+  // critic role's); reduced with the pass's other partials
+  float* lp = f.lossp + (int64_t)blockIdx.x * f.lossld;
+  for (int qq = t; qq < f.lossld; qq += kMThr) {
+    if (qq == 1) continue;
+    double v = 0.0;
     if (qq < nq) {
-      for (unsigned b0 = l; b0 < nb; b0 += 64) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const unsigned b = b0 + 8 * u;
-          v[u] = b < nb ? a.part[(int64_t)b * nq + qq] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += v[u];
-      }
+      for (int k = 0; k < kMWarps; ++k) v += red[k][qq];
+      if (blockIdx.x == 0 && qq >= 3) v += a.ent_coef_add;
+    }
+    lp[qq] = (float)v;
+  }
+}
+
+__device__ __forceinline__ void fused_critic(const PpoFusedArgs& f, uint8_t* smem) {
+  const PpoHeadArgs& a = f.h;
+  const int Kc = f.Kc;
+  const CriticSmem L(Kc);
+  const int kc = L.kc;
+  __nv_bfloat16* shc = reinterpret_cast<__nv_bfloat16*>(smem);
+  float* swc = reinterpret_cast<float*>(smem + L.o_wc);
+  float* sdv = reinterpret_cast<float*>(smem + L.o_v) + kMRows;
+  float* scrit = reinterpret_cast<float*>(smem + L.o_cr);  // [warps][kc] dw_c, then colsum(dh_c)
+  __shared__ double red[kMWarps];
+  __shared__ float s_bc;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * kMRows;
+  const int64_t M = a.n_local;
+  stage_bf16_rows(f.hc, f.ldhc, r0, M, kMRows, Kc, kc, shc, L.pc);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int c = t; c < kc; c += kMThr) swc[c] = c < Kc ? __ldg(f.Wc + c) : 0.f;
+  if (t == 0) s_bc = f.bc[0];
+  // two threads per row, halves of the columns; the even lane owns the row's loss
+  const int row = t >> 1, half = t & 1;
+  const int64_t gr = r0 + row;
+  const bool ok = gr < M;
+  const double ret = ok && !half ? (double)a.ret[gr] : 0.0;
+  const double oldv = ok && !half ? (double)a.oldv[gr] : 0.0;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  // ---- critic forward, clipped value loss (R:algos/ppo.py:104-113)
+  double vl = 0.0;
+  {
+    const int c0 = half * (kc / 2), c1 = half ? kc : kc / 2;
+    float s = 0.f;
+    const __nv_bfloat16* hr = shc + row * L.pc;
+    for (int c = c0; c < c1; c += 2) {
+      const float2 hv = up_bf16(*reinterpret_cast<const uint32_t*>(hr + c));
+      s = fmaf(hv.x, swc[c], fmaf(hv.y, swc[c + 1], s));
     }
     s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    if (qq < nq && l == 0) {
-      if (qq < 3) a.loss_out[qq] = (float)s;
-      else a.dlogstd_out[qq - 3] = (float)(s + a.ent_coef_add);
+    if (!half) {
+      double dv = 0.0;
+      if (ok) {
+        const double v = (double)(s + s_bc);
+        if (a.clipped_v) {
+          const double vc = oldv + fmin(fmax(v - oldv, -a.clip), a.clip);
+          const double lu = (v - ret) * (v - ret), lc = (vc - ret) * (vc - ret);
+          vl = fmax(lu, lc);
+          dv = lu >= lc ? 2.0 * (v - ret) / a.n_global : 0.0;
+        } else {
+          vl = (v - ret) * (v - ret);
+          dv = 2.0 * (v - ret) / a.n_global;
+        }
+      }
+      sdv[row] = (float)(dv * a.vcoef);
     }
+  }
+  {
+    const double v = warp_sum(vl);
+    if (lane == 0) red[w] = v;
+  }
+  __syncthreads();  // sdv, red
+  // ---- critic backward (SIMT): thread = (8-column group, rows rg, rg + R/..),
+  // 16-byte row loads / stores; dw_c and colsum(dh_c) reduced over the row
+  // groups (lane pairs, then warps in fixed order)
+  {
+    const int ncg = kc / 8;       // column groups (<= 32)
+    const int nrg = kMThr / ncg;  // row groups
+    const int cg = t % ncg, rg = t / ncg;
+    float dw[8], cs[8], wcc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      dw[e] = cs[e] = 0.f;
+      wcc[e] = swc[8 * cg + e];
+    }
+    if (rg < nrg) {
+      for (int rr = rg; rr < kMRows; rr += nrg) {
+        const uint4 hv = *reinterpret_cast<const uint4*>(shc + rr * L.pc + 8 * cg);
+        const float dvr = sdv[rr];
+        const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+        uint32_t ow[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 hh = up_bf16(hw[e]);
+          const float d0 = dvr * wcc[2 * e] * (fminf(hh.x, 0.f) + 1.f);
+          const float d1 = dvr * wcc[2 * e + 1] * (fminf(hh.y, 0.f) + 1.f);
+          dw[2 * e] = fmaf(dvr, hh.x, dw[2 * e]);
+          dw[2 * e + 1] = fmaf(dvr, hh.y, dw[2 * e + 1]);
+          cs[2 * e] += d0;
+          cs[2 * e + 1] += d1;
+          ow[e] = pk_bf16(d0, d1);
+        }
+        const int c = 8 * cg;
+        if (r0 + rr < M && c < Kc) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(f.dhc) + (r0 + rr) * f.lddhc + c;
+          if (c + 8 <= Kc && ((f.lddhc & 7) == 0)) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+          } else {
+            const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(ow);
+            for (int e = 0; e < 8 && c + e < Kc; ++e) dst[e] = ob[e];
+          }
+        }
+      }
+    }
+    // row groups of one warp: lanes l, l + ncg, ... share cg
+    for (int o = ncg; o < 32; o <<= 1)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        dw[e] += __shfl_xor_sync(0xffffffffu, dw[e], o);
+        cs[e] += __shfl_xor_sync(0xffffffffu, cs[e], o);
+      }
+    if (lane < ncg)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        scrit[w * kc + 8 * lane + e] = dw[e];
+        scrit[kMWarps * kc + w * kc + 8 * lane + e] = cs[e];
+      }
+  }
+  __syncthreads();  // scrit complete
+  float* pc = f.partc + (int64_t)blockIdx.x * f.plenc;
+  for (int c = t; c < Kc; c += kMThr) {
+    float dw = 0.f, cs = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMWarps; ++k) {
+      dw += scrit[k * kc + c];
+      cs += scrit[kMWarps * kc + k * kc + c];
+    }
+    pc[c] = dw;
+    if (f.csc) pc[Kc + 1 + c] = cs;
+  }
+  if (t == 0) {
+    float s = 0.f;
+    for (int rr = 0; rr < kMRows; ++rr) s += sdv[rr];
+    pc[Kc] = s;
+    double v = 0.0;
+    for (int k = 0; k < kMWarps; ++k) v += red[k];
+    f.lossp[(int64_t)blockIdx.x * f.lossld + 1] = (float)v;
   }
 }
 
 template <int NJT>
+__global__ void __launch_bounds__(kMThr, 5) ppo_fused_mma_kernel(const __grid_constant__ PpoFusedArgs f) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  pdl_trigger();
+  pdl_wait();
+  if (blockIdx.y == 0) fused_actor<NJT>(f, smem);
+  else fused_critic(f, smem);
+}
+
+inline size_t mma_smem(int Ka, int Kc, int NJT) {
+  const size_t x = ActorSmem(Ka, NJT).total, y = CriticSmem(Kc).total;
+  return x > y ? x : y;
+}
+
+template <int NJT>
 int launch_mma(const PpoFusedArgs& f, cudaStream_t s) {
-  const MmaSmem L(f.Ka, f.Kc, NJT);
   static bool attr = false;
   if (!attr) {
     UL_CUDA(cudaFuncSetAttribute(ppo_fused_mma_kernel<NJT>,
@@ -1002,8 +1001,8 @@ int launch_mma(const PpoFusedArgs& f, cudaStream_t s) {
     attr = true;
   }
   const unsigned blocks = (unsigned)ceil_div(f.h.n_local > 0 ? f.h.n_local : 1, kMRows);
-  return launch_pdl("ppo_fused_mma_kernel", ppo_fused_mma_kernel<NJT>, dim3(blocks), dim3(kMThr),
-                    L.total, s, f);
+  return launch_pdl("ppo_fused_mma_kernel", ppo_fused_mma_kernel<NJT>, dim3(blocks, 2), dim3(kMThr),
+                    mma_smem(f.Ka, f.Kc, NJT), s, f);
 }
 
 inline int pad_np(int N) {
@@ -1063,8 +1062,9 @@ int launch_ppo_fused(const PpoFusedArgs& fin, int dtype, ReduceJob* jobs, int* n
   const int ncg = rup8(f.Kc) / 8;  // critic column groups: a power of two <= 32
   const bool mma = mma_env && dtype == kBf16 && (f.Ka % 2) == 0 && (f.Kc % 2) == 0 &&
                    (ncg & (ncg - 1)) == 0 && ncg <= 32 && f.wba != nullptr &&
-                   MmaSmem(f.Ka, f.Kc, f.h.A <= 16 ? 2 : 4).total <= 200 * 1024;
+                   mma_smem(f.Ka, f.Kc, f.h.A <= 16 ? 2 : 4) <= 200 * 1024;
   if (!mma) f.lossp = nullptr;  // (the SIMT variant folds its loss partials itself)
+  UL_CHECK_ARG(!mma || f.lossp != nullptr, "ppo fused head: tensor-core variant needs lossp");
   if (mma) UL_TRY(f.h.A <= 16 ? launch_mma<2>(f, s) : launch_mma<4>(f, s));
   else UL_TRY(dtype == kBf16 ? launch_t<__nv_bfloat16>(f, s) : launch_t<float>(f, s));
   const int64_t nblk = ceil_div(f.h.n_local > 0 ? f.h.n_local : 1, mma ? kMRows : kFRows);
