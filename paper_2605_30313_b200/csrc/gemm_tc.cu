@@ -43,6 +43,13 @@ struct TcArgs {
   int ldcs;
   int bres_kt;                // B-resident launches: K tiles of B held in smem
   int tma_store;              // 1 (default): TMA bulk stores; 0: coalesced st.global (UL_TC_TMASTORE=0)
+  // kEpiLnFull: LayerNorm gain / shift, per-row (mean, rstd) out, h ones column
+  const float* ln_g;
+  const float* ln_beta;
+  float* ln_stats;
+  void* ln_h;
+  int ln_h_ones;
+  int64_t ldh;
 };
 
 // trace slots: [0] entry, [1] setup done, [2..33] producer k-tile issue,
@@ -57,12 +64,13 @@ __device__ __forceinline__ void trace_at(unsigned long long* tr, int slot) {
 }
 
 constexpr int kEpiWarps = 16;  // four warps per TMEM lane quarter, each a BN/4 column slice
+constexpr int kLnMaxRanks = kLnFullMaxN / 256;  // N-tile CTAs of one fused-LayerNorm cluster
 constexpr int kPThreads = (2 + kEpiWarps) * 32;
 
 // bf16 operands -> bf16 hidden activations / gradients; everything else fp32
 template <typename TI, int EPI>
 using OutT = typename std::conditional<sizeof(TI) == 2 && (EPI == kEpiBiasElu || EPI == kEpiEluGrad ||
-                                                            EPI == kEpiBiasLn),
+                                                            EPI == kEpiBiasLn || EPI == kEpiLnFull),
                                        __nv_bfloat16, float>::type;
 
 // [stage ring][16 epilogue staging boxes][barriers][bias x 2]; as many stages
@@ -83,8 +91,12 @@ struct Smem {
   static constexpr int kStagingBytes = kEpiWarps * kNStg * 32 * 64;
   // ELU-gradient epilogue: per-quarter column sums of the output (4 x 512 floats)
   static constexpr int kCsumBytes = EPI == kEpiEluGrad ? 4 * kCsumMaxN * 4 : 0;
-  static constexpr int kFixed =
-      512 /*barriers*/ + 2 * BN * 4 /*bias*/ + kCsumBytes;  // (base is 1 KB aligned)
+  // fused LayerNorm: per-row (mean, M2) of the 4 column slices [4][128] and the
+  // cluster's per-CTA partials, double-buffered [2][kLnMaxRanks][128] (float2)
+  // and the gain / shift of the tile's columns, double-buffered [2][2][BN]
+  static constexpr int kLnBytes = EPI == kEpiLnFull ? (4 + 2 * kLnMaxRanks) * 128 * 8 + 4 * BN * 4 : 0;
+  static constexpr int kFixed = 512 /*barriers*/ + 2 * BN * 4 /*bias*/ + kCsumBytes +
+                                kLnBytes;  // (base is 1 KB aligned)
   static constexpr int kBudget = 232448;
   static constexpr int kStagesFit = (kBudget - kStagingBytes - kFixed) / kStageBytes;
   static constexpr int kStages = BRES ? 3 : (kStagesFit > 6 ? 6 : kStagesFit);
@@ -158,6 +170,7 @@ struct TcBatch {
   int end[kMaxProb];  // prefix sums of the problems' tile-group counts
   int np, ngroups;
   int cs_pr;          // problem whose epilogue emits column sums, or -1
+  int lnc;            // kEpiLnFull: CTAs per cluster = N tiles of every problem
 };
 
 // BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
@@ -174,6 +187,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   using S = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
   static_assert(!(BRES && PAIR), "B-resident launches are single-CTA");
   constexpr bool kOutBf16 = sizeof(TO) == 2;
+  constexpr bool LN = EPI == kEpiLnFull;
+  static_assert(!(LN && (PAIR || BRES)), "fused LayerNorm launches are single-CTA MMA clusters");
   constexpr int CS = PAIR ? 2 : 1;
   constexpr int BNL = BN / CS;  // B rows (N) this CTA loads
   constexpr int BK = O::BK;
@@ -196,7 +211,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* acc_empty = acc_full + 2;    // [2]
   uint64_t* aux_bar = acc_empty + 2;     // [kEpiWarps]
   uint64_t* bres_bar = aux_bar + kEpiWarps;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_bar + 2);  // keeps sbias 16 B aligned
+  uint64_t* ln_bar = bres_bar + 2;  // [2] fused LayerNorm: the cluster's row partials landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ln_bar + 2);  // keeps sbias 16 B aligned
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long w_prod = 0, w_full = 0, w_acc = 0, w_epi = 0, w_issue = 0;  // (UL_TC_TRACE)
@@ -205,9 +221,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (threadIdx.x == 0) trace_at(p0_.trace, 0);
 
   uint32_t crank = 0;
-  if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
-  const bool leader = crank == 0;
-  const int cl = blockIdx.x / CS, ncl = gridDim.x / CS;
+  if (PAIR || LN) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const bool leader = !PAIR || crank == 0;
+  // (fused LayerNorm: a cluster of B.lnc CTAs walks the same M tiles, CTA
+  // rank r computing N tile r of each)
+  const int CSL = LN ? B.lnc : CS;
+  const int cl = blockIdx.x / CSL, ncl = gridDim.x / CSL;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -220,6 +239,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
     for (int w = 0; w < kEpiWarps; ++w) mbar_init(&aux_bar[w], 1);
     mbar_init(bres_bar, 1);
+    if (LN) {
+      mbar_init(&ln_bar[0], 1);
+      mbar_init(&ln_bar[1], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -244,7 +267,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (PAIR) cluster_sync_all();  // peer barriers initialised before any cross-CTA signal
+  if (PAIR || LN) cluster_sync_all();  // peer barriers initialised before any cross-CTA signal
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
   pdl_wait();  // setup above overlapped the previous kernel's tail
@@ -262,7 +285,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const TcArgs& P = B.a[T.pr];
     const int tl = T.pr ? t - B.end[T.pr - 1] : t;
     const int mg = (P.mt + CS - 1) / CS;
-    if (BRES) {  // N fastest: the grid is a multiple of nt, so a CTA keeps one N tile
+    if (LN) {  // one M tile per group; the cluster rank picks the N tile
+      T.z = 0;
+      T.n0 = (int)crank * BN;
+      T.m0 = tl * BM;
+    } else if (BRES) {  // N fastest: the grid is a multiple of nt, so a CTA keeps one N tile
       T.z = 0;
       T.n0 = (tl % P.nt) * BN;
       T.m0 = (tl / P.nt) * BM;
@@ -438,7 +465,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
     int cj = 0;  // this warp's box counter (staging buffer = cj & 1)
     // bias of the next tile, loaded one tile ahead so its global latency hides
     // behind the current tile's epilogue
-    float bnext[kBiasPer];
+    float bnext[kBiasPer], gnext[LN ? kBiasPer : 1], enext[LN ? kBiasPer : 1];
+    // fused LayerNorm smem: gain / shift [2][BN] each, slice partials
+    // [4][128] and the cluster's per-CTA partials [2][kLnMaxRanks][128]
+    float* ln_sg = csum_s + S::kCsumBytes / 4;
+    float* ln_se = ln_sg + 2 * BN;
+    float2* ln_sl = reinterpret_cast<float2*>(ln_se + 2 * BN);
+    float2* ln_buf = ln_sl + 4 * 128;
     auto load_bias = [&](int t) {
       if (t >= ngroups) return;
       const Tile T = tile_of(t);
@@ -447,9 +480,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int j = 0; j < kBiasPer; ++j) {
         const int n = T.n0 + slice * kSlice + j * 32 + lane;
         bnext[j] = n < p.N ? __ldg(p.bias + n) : 0.f;
+        if constexpr (LN) {
+          gnext[j] = n < p.N ? __ldg(p.ln_g + n) : 0.f;
+          enext[j] = n < p.N ? __ldg(p.ln_beta + n) : 0.f;
+        }
       }
     };
-    if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn) load_bias(cl);
+    if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn || LN) load_bias(cl);
     // diagnostics: epilogue warp 0, tiles 0-1, boxes 0-3 -> trace slots 100..
 #define UL_ETRACE(k) \
   if (ew == 0 && lane == 0 && local < 2 && cj < 4) trace_at(p0_.trace, 100 + cj * 6 + (k))
@@ -461,9 +498,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const CUtensorMap* tX = &B.m[T.pr].x;
       const int b = local & 1;
       const bool have = T.kt_n > 0;
-      if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn) {
+      if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn || LN) {
 #pragma unroll
-        for (int j = 0; j < kBiasPer; ++j) sbias[b * BN + slice * kSlice + j * 32 + lane] = bnext[j];
+        for (int j = 0; j < kBiasPer; ++j) {
+          sbias[b * BN + slice * kSlice + j * 32 + lane] = bnext[j];
+          if constexpr (LN) {
+            ln_sg[b * BN + slice * kSlice + j * 32 + lane] = gnext[j];
+            ln_se[b * BN + slice * kSlice + j * 32 + lane] = enext[j];
+          }
+        }
         __syncwarp();
         load_bias(t + ncl);
       }
@@ -489,6 +532,184 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int m = m0 + row;
       const int crow = m0 + quarter * 32;  // row of this warp's 32-row box in C (split z)
       const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN);
+      if constexpr (LN) {
+        // ---- fused LayerNorm (kEpiLnFull).  Pass 1: a = acc + bias, rounded
+        // to the stored bf16 (what the backward reads), -> C; this warp's
+        // running (mean, M2) of its valid columns, 16-column chunks merged
+        // with Chan's formula.
+        float mu = 0.f, m2 = 0.f;
+        float cnt = 0.f;
+#pragma unroll 1
+        for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += kBoxC, ++cj) {
+          uint8_t* stg = staging + (ew * S::kNStg + cj % S::kNStg) * kBoxBytes;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
+          const int sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int h = 0; h < kBoxC / 16; ++h) {
+            const int cc = c0 + 16 * h;
+            float v[16];
+            if (have) {
+              tmem_ld16(taddr + (uint32_t)cc, v);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + cc);
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 q4 = bv[i];
+              pk[2 * i] = pack_bf16(v[4 * i] + q4.x, v[4 * i + 1] + q4.y);
+              pk[2 * i + 1] = pack_bf16(v[4 * i + 2] + q4.z, v[4 * i + 3] + q4.w);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              v[2 * e] = bf_lo(pk[e]);
+              v[2 * e + 1] = bf_hi(pk[e]);
+            }
+            const int nv = min(16, max(0, p.N - (n0 + cc)));
+            if (nv > 0) {
+              float sm = 0.f, qd = 0.f, mc;
+              const float fn = (float)nv;
+              if (nv == 16) {  // (every chunk but a ragged row end)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) sm += v[i];
+                mc = sm * (1.f / 16.f);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) qd = fmaf(v[i] - mc, v[i] - mc, qd);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) sm += i < nv ? v[i] : 0.f;
+                mc = sm / fn;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const float d = v[i] - mc;
+                  qd += i < nv ? d * d : 0.f;
+                }
+              }
+              const float tot = cnt + fn, delta = mc - mu;
+              mu += delta * (fn / tot);
+              m2 += qd + delta * delta * (cnt * fn / tot);
+              cnt = tot;
+            }
+            srow[(2 * h) ^ sw] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            srow[(2 * h + 1) ^ sw] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tC),
+                "r"(su32(stg)), "r"(n0 + c0), "r"(crow), "r"(0)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+        // ---- row statistics: the 4 slices of this CTA (shared memory), then
+        // the cluster's N tiles (each CTA's partial stored into every rank's
+        // buffer by st.async, completing on that rank's ln_bar[b])
+        ln_sl[slice * 128 + row] = make_float2(mu, m2);
+        asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        const int lnc = B.lnc;
+        if (ew == 0 && lane == 0) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&ln_bar[b])),
+                       "r"((uint32_t)(lnc * 128 * 8))
+                       : "memory");
+        }
+        if (slice == 0) {
+          float cm = 0.f, cq = 0.f, cn = 0.f;
+#pragma unroll
+          for (int sl = 0; sl < 4; ++sl) {
+            const float fn = (float)min(kSlice, max(0, p.N - (n0 + sl * kSlice)));
+            if (fn > 0.f) {
+              const float2 pv = ln_sl[sl * 128 + row];
+              const float tot = cn + fn, delta = pv.x - cm;
+              cm += delta * (fn / tot);
+              cq += pv.y + delta * delta * (cn * fn / tot);
+              cn = tot;
+            }
+          }
+          const uint32_t src = su32(&ln_buf[(b * kLnMaxRanks + (int)crank) * 128 + row]);
+          const uint32_t bar = su32(&ln_bar[b]);
+          for (int r = 0; r < lnc; ++r) {
+            uint32_t ra, rb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(src), "r"(r));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(r));
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(ra),
+                "f"(cm), "f"(cq), "r"(rb)
+                : "memory");
+          }
+        }
+        mbar_wait(&ln_bar[b], (local >> 1) & 1);
+        float mean = 0.f, m2t = 0.f, ntot = 0.f;
+        for (int r = 0; r < lnc; ++r) {  // fixed rank order: deterministic
+          const float fn = (float)min(BN, max(0, p.N - r * BN));
+          if (fn > 0.f) {
+            const float2 pv = ln_buf[(b * kLnMaxRanks + r) * 128 + row];
+            const float tot = ntot + fn, delta = pv.x - mean;
+            mean += delta * (fn / tot);
+            m2t += pv.y + delta * delta * (ntot * fn / tot);
+            ntot = tot;
+          }
+        }
+        const float rstd = rsqrtf(m2t / (float)p.N + 1e-5f);
+        if (crank == 0 && slice == 0 && m < p.M) {
+          reinterpret_cast<float2*>(p.ln_stats)[m] = make_float2(mean, rstd);
+          if (p.ln_h_ones >= 0)
+            reinterpret_cast<__nv_bfloat16*>(p.ln_h)[(int64_t)m * p.ldh + p.ln_h_ones] =
+                __float2bfloat16_rn(1.f);
+        }
+        // ---- pass 2: h = elu((a - mean) rstd g + beta) from the same rounded a -> h
+#pragma unroll 1
+        for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += kBoxC, ++cj) {
+          uint8_t* stg = staging + (ew * S::kNStg + cj % S::kNStg) * kBoxBytes;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          uint4* srow = reinterpret_cast<uint4*>(stg + lane * 64);
+          const int sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int h = 0; h < kBoxC / 16; ++h) {
+            const int cc = c0 + 16 * h;
+            float v[16];
+            if (have) {
+              tmem_ld16(taddr + (uint32_t)cc, v);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            }
+            const float4* bv = reinterpret_cast<const float4*>(sbias + b * BN + cc);
+            const float4* gv = reinterpret_cast<const float4*>(ln_sg + b * BN + cc);
+            const float4* ev = reinterpret_cast<const float4*>(ln_se + b * BN + cc);
+            uint32_t pk[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 q4 = bv[i], g4 = gv[i], e4 = ev[i];
+              const uint32_t a01 = pack_bf16(v[4 * i] + q4.x, v[4 * i + 1] + q4.y);
+              const uint32_t a23 = pack_bf16(v[4 * i + 2] + q4.z, v[4 * i + 3] + q4.w);
+              // (x - mean) rstd g + beta = x (rstd g) + (beta - mean rstd g)
+              const float r0 = rstd * g4.x, r1 = rstd * g4.y, r2 = rstd * g4.z, r3 = rstd * g4.w;
+              pk[2 * i] = pack_bf16(elu_fast(fmaf(bf_lo(a01), r0, fmaf(-mean, r0, e4.x))),
+                                    elu_fast(fmaf(bf_hi(a01), r1, fmaf(-mean, r1, e4.y))));
+              pk[2 * i + 1] = pack_bf16(elu_fast(fmaf(bf_lo(a23), r2, fmaf(-mean, r2, e4.z))),
+                                        elu_fast(fmaf(bf_hi(a23), r3, fmaf(-mean, r3, e4.w))));
+            }
+            srow[(2 * h) ^ sw] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            srow[(2 * h + 1) ^ sw] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && n0 + c0 < p.N && m0 + quarter * 32 < p.M) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tX),
+                "r"(su32(stg)), "r"(n0 + c0), "r"(crow), "r"(0)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += kBoxC, ++cj) {
         uint8_t* stg = staging + (ew * S::kNStg + cj % S::kNStg) * kBoxBytes;
@@ -642,6 +863,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         UL_ETRACE(4);
       }
+      }  // (not LN)
 #undef UL_ETRACE
       if (p.ones_col >= 0 && n0 == 0 && slice == 0 && m < p.M) {
         TO* cp = reinterpret_cast<TO*>(p.C);
@@ -684,7 +906,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   // no CTA may leave (or free TMEM) while its pair can still write into its
   // smem / TMEM or arrive on its barriers
-  if (PAIR) cluster_sync_all();
+  if (PAIR || LN) cluster_sync_all();
   if (threadIdx.x == 0) trace_at(p0_.trace, 98);
   if (p0_.trace) {  // role wait cycles summed over CTAs: 128 producer, 129 MMA full, 130 MMA
                     // acc-empty, 131 epilogue warp 2 acc-full, 132 CTA cycles, 133 CTAs
@@ -757,6 +979,7 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   // C (and split-K partials [splits][M][ldc]) stored by 32-row x 64-byte TMA boxes
   UL_TRY(make_map(&m->c, d.C, ob, d.N, d.M, d.ldc, boxc, 32, out_sw, q.zs));
   if (EPI == kEpiEluGrad) UL_TRY(make_map(&m->x, d.aux, ob, d.N, d.M, d.ldaux, boxc, 32, out_sw, 1));
+  else if (EPI == kEpiLnFull) UL_TRY(make_map(&m->x, d.ln_h, ob, d.N, d.M, d.ldh, boxc, 32, out_sw, 1));
   else m->x = m->c;
   const int mt = (int)ceil_div(d.M, BM), nt = (int)ceil_div(d.N, BN);
   *a = TcArgs{(int)d.M, (int)d.N, (int)d.K, q.kps, mt, nt, q.zs, d.C, d.ldc, d.bias,
@@ -764,6 +987,18 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
               EPI == kEpiEluGrad && d.N <= kCsumMaxN ? d.csum_part : nullptr,
               (int)ceil_div(d.N, 4) * 4, BRES ? (int)ceil_div(d.K, O::BK) : 0, tma_store_on()};
   *ngroups = (int)ceil_div(mt, CS) * nt * q.zs;
+  if (EPI == kEpiLnFull) {  // a cluster of nt CTAs per M tile
+    UL_CHECK_ARG(nt <= kLnMaxRanks && q.zs == 1 && d.ln_h && d.ln_g && d.ln_beta && d.ln_stats,
+                 "gemm_tc: fused LayerNorm needs N <= %d, no split-K, h / g / beta / stats",
+                 kLnMaxRanks * BN);
+    a->ln_g = d.ln_g;
+    a->ln_beta = d.ln_beta;
+    a->ln_stats = d.ln_stats;
+    a->ln_h = d.ln_h;
+    a->ln_h_ones = d.ln_h_ones;
+    a->ldh = d.ldh;
+    *ngroups = mt;
+  }
   return UL_OK;
 }
 
@@ -786,6 +1021,11 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     else B.a[i].csum = nullptr;  // one column-sum problem per launch
   }
   B.ngroups = total;
+  // fused LayerNorm: every problem's N tiles form one cluster
+  const int CSX = EPI == kEpiLnFull ? B.a[0].nt : CS;
+  B.lnc = CSX;
+  for (int i = 1; i < np; ++i)
+    UL_CHECK_ARG(EPI != kEpiLnFull || B.a[i].nt == CSX, "gemm_tc: fused LayerNorm batch widths differ");
   auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
@@ -793,7 +1033,7 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.x = CSX;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -803,13 +1043,14 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   // persistent: as many clusters as can be co-resident (one CTA per SM; GPC
   // sizes may leave SMs idle for CS > 1, so ask the occupancy API rather than
   // queue a second wave behind the first)
-  static int max_clusters = 0;
+  static int max_cl[kLnMaxRanks + 1] = {};  // per cluster size
+  int& max_clusters = max_cl[CSX <= kLnMaxRanks ? CSX : 0];
   if (max_clusters == 0) {
     UL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  BRES ? SM::kBudget : SM::kBytes));
-    int n = kNumSMs / CS;
-    if (CS > 1) {
-      cfg.gridDim = dim3((unsigned)(n * CS));
+    int n = kNumSMs / CSX;
+    if (CSX > 1) {
+      cfg.gridDim = dim3((unsigned)(n * CSX));
       int qn = 0;
       if (cudaOccupancyMaxActiveClusters(&qn, kern, &cfg) == cudaSuccess && qn > 0 && qn < n)
         n = qn;
@@ -827,7 +1068,7 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   }
   int cap = max_clusters;
   if (EPI == kEpiEluGrad && grid_dx > 0 && grid_dx / CS < cap) cap = grid_dx / CS;
-  int grid = (total < cap ? total : cap) * CS;
+  int grid = (total < cap ? total : cap) * CSX;
   if (BRES) grid = grid / B.a[0].nt * B.a[0].nt;  // every CTA keeps one N tile
   cfg.gridDim = dim3((unsigned)grid);
   for (int i = 0; i < np; ++i)
@@ -847,7 +1088,8 @@ inline int bn_of(const GemmDesc& d) {
     cap_dx = f ? atoi(f) : 256;
   }
   const int cap = d.epi == kEpiEluGrad ? cap_dx
-                  : (d.epi == kEpiBias || d.epi == kEpiBiasElu || d.epi == kEpiBiasLn) ? cap_fwd
+                  : (d.epi == kEpiBias || d.epi == kEpiBiasElu || d.epi == kEpiBiasLn ||
+                     d.epi == kEpiLnFull) ? cap_fwd
                                                                                          : 256;
   return d.N > 128 && cap >= 256 ? 256 : 128;
 }
@@ -919,6 +1161,17 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   const int64_t bres_bytes = ceil_div(d.K, bk) * (int64_t)bn * 128;
   const bool bres_base = bres_ok && np == 1 && !amn && q[0].zs == 1 &&
                          ceil_div(d.N, bn) <= kNumSMs && (sizeof(TI) == 2 || !pair);
+  // fused LayerNorm (bf16 only): single-CTA MMA, clusters along N
+  if (d.epi == kEpiLnFull) {
+    if constexpr (sizeof(TI) == 2) {
+      if (!amn && !bmn) {
+        if (bn == 256) return launch<TI, false, false, kEpiLnFull, 256, false>(q, np, s);
+        return launch<TI, false, false, kEpiLnFull, 128, false>(q, np, s);
+      }
+    }
+    set_error("gemm_tc: fused LayerNorm needs bf16 K-major operands");
+    return UL_ERR_VALUE;
+  }
 #define UL_TC_BN(AMN, BMN, EPI, BN)                                                          \
   if (!AMN && bres_base &&                                                                  \
       bres_bytes <= Smem<BN, false, (int)sizeof(OutT<TI, EPI>), EPI, true>::kBresMax)       \
@@ -952,7 +1205,7 @@ int tc_bk(int dtype) { return dtype == kBf16 ? tc::Op<__nv_bfloat16>::BK : tc::O
 bool tc_eligible(const GemmDesc& d) {
   const int eb = d.dtype == kBf16 ? 2 : 4;
   const int ob = (d.dtype == kBf16 && (d.epi == kEpiBiasElu || d.epi == kEpiEluGrad ||
-                                       d.epi == kEpiBiasLn)) ? 2 : 4;
+                                       d.epi == kEpiBiasLn || d.epi == kEpiLnFull)) ? 2 : 4;
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   // bf16 runs every hidden GEMM on the tensor cores (TMA zero-fills partial
   // tiles); tf32 keeps tiny shapes on the SIMT kernel
@@ -1192,7 +1445,9 @@ int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
                     d0.b_kmajor == d1.b_kmajor && d0.epi == d1.epi &&
                     tc::bn_of(d0) == tc::bn_of(d1) &&
                     (ceil_div(d0.M, tc::BM) >= 2) == (ceil_div(d1.M, tc::BM) >= 2) &&
-                    !(d0.csum_part && d1.csum_part);
+                    !(d0.csum_part && d1.csum_part) &&
+                    (d0.epi != kEpiLnFull ||
+                     ceil_div(d0.N, tc::bn_of(d0)) == ceil_div(d1.N, tc::bn_of(d1)));
   if (!same) {
     UL_TRY(gemm_tc(d0, -1, s));
     return gemm_tc(d1, -1, s);

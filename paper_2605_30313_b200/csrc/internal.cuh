@@ -48,6 +48,8 @@ enum Epilogue : int {
   kEpiBiasElu = 2,   // C = elu(acc + bias[n])
   kEpiEluGrad = 3,   // C = acc * (min(aux[m,n],0)+1)
   kEpiBiasLn = 4,    // C = acc + bias[n] as bf16 rows (a LayerNorm layer's pre-LN activation)
+  kEpiLnFull = 5,    // kEpiBiasLn + the whole LayerNorm in the epilogue: row statistics
+                     // across a cluster of N-tile CTAs (DSMEM), h = elu(LN(a) g + beta)
 };
 
 // operand storage of a GEMM / activation buffer
@@ -89,8 +91,18 @@ struct GemmDesc {
   // fp32 operands through the tf32 tensor cores as 3xTF32 (hi/lo split,
   // hi*hi + hi*lo + lo*hi): the exact-fp32 parity back end on tcgen05
   bool x3 = false;
+  // kEpiLnFull only: C receives the pre-LN rows a (bf16), ln_h the layer's
+  // output h = elu((a - mean) rstd g + beta) (bf16, ld ldh, 1.0 in column
+  // ln_h_ones when >= 0), ln_stats the per-row (mean, rstd) float2
+  void* ln_h = nullptr;
+  int64_t ldh = 0;
+  const float* ln_g = nullptr;
+  const float* ln_beta = nullptr;
+  float* ln_stats = nullptr;
+  int ln_h_ones = -1;
 };
 constexpr int kCsumMaxN = 512;
+constexpr int kLnFullMaxN = 1024;  // widest LayerNorm row the fused epilogue takes (4 N tiles)
 // widest input-gradient column slice the skinny dX path takes (SAC dQ/da)
 constexpr int kSkinnyDxMax = 32;
 int gemm_f32(const GemmDesc& d, cudaStream_t s);

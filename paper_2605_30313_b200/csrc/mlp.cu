@@ -440,6 +440,14 @@ int64_t act_floats(const NetView& v, int64_t M) {
 }
 
 // pre-LN rows in bf16 on the bf16 back end (UL_LN_A_BF16=0: fp32 rows)
+// the whole LayerNorm forward in the tcgen05 epilogue (kEpiLnFull); read on
+// every call (a plan captures its choice), UL_LN_FUSED=0 keeps the separate
+// row / column kernels
+bool ln_fused_enabled() {
+  const char* e = getenv("UL_LN_FUSED");
+  return e ? atoi(e) != 0 : true;
+}
+
 bool ln_a_bf16(int dtype) {
   static int on = -1;
   if (on < 0) {
@@ -829,6 +837,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
     const bool last = i == nl - 1;
     GemmDesc g[2] = {};
     bool has[2] = {false, false}, use[2] = {false, false}, skinny[2] = {false, false};
+    bool ln_full[2] = {false, false};
     int ones[2] = {-1, -1};
     for (int k = 0; k < n; ++k) {
       const MlpNet& N = nets[k];
@@ -862,6 +871,31 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
         G.C = la;
         G.ldc = abf ? rup(v.dims[i + 1], 8) : lla;
         ln_pending[k] = true;
+        if (abf && tc && N.wp && ln_fused_enabled() && v.dims[i + 1] <= kLnFullMaxN) {
+          // the whole LayerNorm in the GEMM epilogue (row statistics across
+          // a cluster of N-tile CTAs): a, h and the row stats in one launch
+          GemmDesc T = G;
+          T.B = staged_w(v, N.wp, i, dt, &T.ldb);
+          T.epi = kEpiLnFull;
+          T.ln_h = dst;
+          T.ldh = lddst;
+          T.ln_g = N.params + v.g_off[i];
+          T.ln_beta = N.params + v.beta_off[i];
+          T.ln_stats = lst;
+          T.ln_h_ones = (int)v.dims[i + 1];
+          if (tc_eligible(T) && ((uintptr_t)lst & 7) == 0 && ((uintptr_t)dst & 15) == 0 &&
+              (lddst * 2) % 16 == 0) {
+            G.epi = kEpiLnFull;
+            G.ln_h = T.ln_h;
+            G.ldh = T.ldh;
+            G.ln_g = T.ln_g;
+            G.ln_beta = T.ln_beta;
+            G.ln_stats = T.ln_stats;
+            G.ln_h_ones = T.ln_h_ones;
+            ln_pending[k] = false;
+            ln_full[k] = true;
+          }
+        }
       }
       // tf32 keeps a wide output layer on the SIMT kernel; bf16 runs it on
       // the tensor cores with an fp32 bias epilogue
@@ -873,7 +907,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
         G.ldb = v.dims[i];
       }
       has[k] = true;
-      ones[k] = (last || ln_pending[k]) ? -1 : v.dims[i + 1];
+      ones[k] = (last || ln_pending[k] || ln_full[k]) ? -1 : v.dims[i + 1];
       h[k] = dst;
       ldh[k] = lddst;
     }

@@ -71,7 +71,8 @@ def _rel(got, ref):
 @pytest.mark.parametrize("dims,rows", [((235, (512, 256, 128), 12), 1000),
                                        ((48, (256, 256), 1), 4096),
                                        ((20, (64,), 4), 37),
-                                       ((16, (1028, 100), 3), 300)])  # generic LN kernels
+                                       ((16, (1028, 100), 3), 300),  # generic LN kernels
+                                       ((119, (1024, 512, 256), 1), 2048)])  # cfg3 critic
 def test_ln_mlp_matches_oracle(prec, dims, rows):
     inp, hid, outd = dims
     arch = TN.Arch(input_dim=inp, hidden_dims=hid, output_dim=outd, layer_norm=True)
@@ -115,3 +116,41 @@ def test_ln_param_layout_and_init():
     p = TN.init_params(arch, seed=0)
     (g0, b0), (g1, b1) = p.layer_norms
     assert torch.all(g0 == 1) and torch.all(b0 == 0) and g1.shape[0] == 8
+
+
+@pytest.mark.parametrize("dims,rows", [((119, (1024, 512, 256), 1), 8192),
+                                       ((48, (256, 256), 1), 1000),
+                                       ((40, (640, 96), 2), 777)])
+def test_ln_fused_epilogue_matches_separate_kernels(dims, rows, monkeypatch):
+    """bf16: the whole LayerNorm forward inside the tcgen05 epilogue
+    (kEpiLnFull: row statistics merged across a cluster of N-tile CTAs through
+    distributed shared memory, h = elu(LN(a) g + beta) written by the GEMM)
+    against the GEMM + separate row / column LN kernels (UL_LN_FUSED=0).
+    Both normalise the same bf16 pre-LN rows; the statistics differ only in
+    fp32 summation order, so outputs agree to a bf16 ulp, and the backward
+    (which reads the stored rows and statistics) to the same level."""
+    inp, hid, outd = dims
+    arch = TN.Arch(input_dim=inp, hidden_dims=hid, output_dim=outd, layer_norm=True)
+    params = TN.init_params(arch, seed=5)
+    rng = np.random.default_rng(3)
+    with torch.no_grad():
+        for g, be in params.layer_norms:
+            g.copy_(torch.from_numpy(rng.uniform(0.5, 1.5, g.shape[0]).astype(np.float32)))
+            be.copy_(torch.from_numpy(rng.normal(0, 0.2, be.shape[0]).astype(np.float32)))
+    x = rng.normal(size=(rows, inp)).astype(np.float32)
+    dout = rng.normal(size=(rows, outd)).astype(np.float32) / rows
+    old = P.get_precision()
+    P.set_precision("bf16")
+    res = {}
+    try:
+        for fused in ("0", "1"):
+            monkeypatch.setenv("UL_LN_FUSED", fused)
+            out, cache = TN.forward(params, x)
+            dx, grads = TN.backward(params, cache, dout)
+            torch.cuda.synchronize()
+            res[fused] = (out.cpu().numpy(), dx.cpu().numpy(), grads.buf.cpu().numpy())
+    finally:
+        P.set_precision(old)
+    for a, b in zip(res["0"], res["1"]):
+        assert np.all(np.isfinite(b))
+        assert _rel(b, a) < 2e-2, _rel(b, a)
