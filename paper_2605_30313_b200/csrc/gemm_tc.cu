@@ -171,6 +171,7 @@ struct TcBatch {
   int np, ngroups;
   int cs_pr;          // problem whose epilogue emits column sums, or -1
   int lnc;            // kEpiLnFull: CTAs per cluster = N tiles of every problem
+  int bres_c;         // B-resident: (problem, N tile) combos; CTA i keeps combo i % bres_c
 };
 
 // BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
@@ -227,6 +228,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // rank r computing N tile r of each)
   const int CSL = LN ? B.lnc : CS;
   const int cl = blockIdx.x / CSL, ncl = gridDim.x / CSL;
+  // this CTA's tile sequence t = t_begin, t_begin + t_step, ... < t_end.
+  // B-resident: CTA i keeps (problem, N tile) combo c = i % bres_c (its B
+  // tile loaded once) and walks that problem's M tiles i / bres_c, + G, ...
+  int t_begin = cl, t_step = ncl, t_end = ngroups, bres_pr = 0, bres_n = 0;
+  if (BRES) {
+    const int C = B.bres_c, c = (int)blockIdx.x % C;
+    int acc = 0;
+    while (bres_pr < B.np - 1 && c >= acc + B.a[bres_pr].nt) acc += B.a[bres_pr++].nt;
+    bres_n = c - acc;
+    t_begin = (int)blockIdx.x / C;
+    t_step = (int)gridDim.x / C;
+    t_end = B.a[bres_pr].mt;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -280,6 +294,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
   };
   auto tile_of = [&](int t) {
     Tile T;
+    if (BRES) {  // t = M tile of this CTA's (problem, N tile) combo
+      const TcArgs& P = B.a[bres_pr];
+      T.pr = bres_pr;
+      T.z = 0;
+      T.n0 = bres_n * BN;
+      T.m0 = t * BM;
+      T.kt_n = P.K > 0 ? (P.K + BK - 1) / BK : 0;
+      return T;
+    }
     T.pr = 0;
     while (T.pr < B.np - 1 && t >= B.end[T.pr]) ++T.pr;
     const TcArgs& P = B.a[T.pr];
@@ -289,10 +312,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
       T.z = 0;
       T.n0 = (int)crank * BN;
       T.m0 = tl * BM;
-    } else if (BRES) {  // N fastest: the grid is a multiple of nt, so a CTA keeps one N tile
-      T.z = 0;
-      T.n0 = (tl % P.nt) * BN;
-      T.m0 = (tl / P.nt) * BM;
     } else {
       T.z = tl / (mg * P.nt);
       const int r = tl - T.z * mg * P.nt;
@@ -309,23 +328,23 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int it = 0;
-      if (BRES && cl < ngroups) {
+      if (BRES && t_begin < t_end) {
         // this CTA's N tile of B, all K tiles, once
-        const Tile T0 = tile_of(cl);
+        const Tile T0 = tile_of(t_begin);
         mbar_expect_tx(bres_bar, bres_bytes);
         for (int kt = 0; kt < T0.kt_n; ++kt) {
           uint8_t* sb = sbres + kt * S::kBBytes;
           if (B_MN) {
 #pragma unroll
             for (int c = 0; c < BN / O::kChunk; ++c)
-              tma_load_2d(sb + c * kChunkBytes, &B.m[0].b, bres_bar, T0.n0 + O::kChunk * c,
+              tma_load_2d(sb + c * kChunkBytes, &B.m[T0.pr].b, bres_bar, T0.n0 + O::kChunk * c,
                           kt * BK);
           } else {
-            tma_load_2d(sb, &B.m[0].b, bres_bar, kt * BK, T0.n0);
+            tma_load_2d(sb, &B.m[T0.pr].b, bres_bar, kt * BK, T0.n0);
           }
         }
       }
-      for (int t = cl; t < ngroups; t += ncl) {
+      for (int t = t_begin; t < t_end; t += t_step) {
         const Tile T = tile_of(t);
         const int m0 = T.m0, n0 = T.n0, kt_n = T.kt_n;
         const TcArgs& P = B.a[T.pr];
@@ -389,8 +408,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((CS * BM) >> 4) << 24);
     if (lane == 0 && leader) {
       int it = 0, local = 0;
-      if (BRES && cl < ngroups) mbar_wait(bres_bar, 0);
-      for (int t = cl; t < ngroups; t += ncl, ++local) {
+      if (BRES && t_begin < t_end) mbar_wait(bres_bar, 0);
+      for (int t = t_begin; t < t_end; t += t_step, ++local) {
         const int kt_n = tile_of(t).kt_n;
         const int b = local & 1;
         mbar_wait_acc(&acc_empty[b], ((local >> 1) & 1) ^ 1,  // epilogues drained this buffer
@@ -473,7 +492,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     float2* ln_sl = reinterpret_cast<float2*>(ln_se + 2 * BN);
     float2* ln_buf = ln_sl + 4 * 128;
     auto load_bias = [&](int t) {
-      if (t >= ngroups) return;
+      if (t >= t_end) return;
       const Tile T = tile_of(t);
       const TcArgs& p = B.a[T.pr];
 #pragma unroll
@@ -486,11 +505,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
       }
     };
-    if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn || LN) load_bias(cl);
+    if (EPI == kEpiBias || EPI == kEpiBiasElu || EPI == kEpiBiasLn || LN) load_bias(t_begin);
     // diagnostics: epilogue warp 0, tiles 0-1, boxes 0-3 -> trace slots 100..
 #define UL_ETRACE(k) \
   if (ew == 0 && lane == 0 && local < 2 && cj < 4) trace_at(p0_.trace, 100 + cj * 6 + (k))
-    for (int t = cl; t < ngroups; t += ncl, ++local) {
+    for (int t = t_begin; t < t_end; t += t_step, ++local) {
       const Tile T = tile_of(t);
       const int m0 = T.m0, n0 = T.n0, z = T.z;
       const TcArgs& p = B.a[T.pr];
@@ -508,7 +527,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
         }
         __syncwarp();
-        load_bias(t + ncl);
+        load_bias(t + t_step);
       }
       // ELU-gradient operand: when the slice fits the two staging boxes, load
       // both boxes now (after every earlier store has read its box), so the
@@ -1027,9 +1046,18 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   for (int i = 1; i < np; ++i)
     UL_CHECK_ARG(EPI != kEpiLnFull || B.a[i].nt == CSX, "gemm_tc: fused LayerNorm batch widths differ");
   auto kern = tc_gemm_kernel<TI, A_MN, B_MN, EPI, BN, PAIR, BRES>;
+  // B-resident: one (problem, N tile) combo per CTA residue class; the B
+  // region holds the deepest problem's K tiles
+  int bres_kt = 0;
+  B.bres_c = 0;
+  for (int i = 0; i < np; ++i) {
+    B.bres_c += B.a[i].nt;
+    bres_kt = B.a[i].bres_kt > bres_kt ? B.a[i].bres_kt : bres_kt;
+  }
+  UL_CHECK_ARG(!BRES || B.bres_c <= kNumSMs, "gemm_tc: B-resident launch with too many N tiles");
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
-  cfg.dynamicSmemBytes = SM::kBytes + (BRES ? (size_t)B.a[0].bres_kt * SM::kBBytes : 0);
+  cfg.dynamicSmemBytes = SM::kBytes + (BRES ? (size_t)bres_kt * SM::kBBytes : 0);
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1069,7 +1097,10 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   int cap = max_clusters;
   if (EPI == kEpiEluGrad && grid_dx > 0 && grid_dx / CS < cap) cap = grid_dx / CS;
   int grid = (total < cap ? total : cap) * CSX;
-  if (BRES) grid = grid / B.a[0].nt * B.a[0].nt;  // every CTA keeps one N tile
+  if (BRES) {  // every CTA keeps one (problem, N tile) combo
+    grid = (cap < total ? cap : total) / B.bres_c * B.bres_c;
+    if (grid < B.bres_c) grid = B.bres_c;
+  }
   cfg.gridDim = dim3((unsigned)grid);
   for (int i = 0; i < np; ++i)
     if (q[i].d->csum_nz) *q[i].d->csum_nz = i == B.cs_pr ? grid : 0;
@@ -1158,9 +1189,35 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   }
   const bool bres_ok = bres_env >= 0 ? bres_env == 1 : d.epi != kEpiEluGrad;
   const int64_t bk = sizeof(TI) == 2 ? 64 : 32;
-  const int64_t bres_bytes = ceil_div(d.K, bk) * (int64_t)bn * 128;
-  const bool bres_base = bres_ok && np == 1 && !amn && q[0].zs == 1 &&
-                         ceil_div(d.N, bn) <= kNumSMs && (sizeof(TI) == 2 || !pair);
+  // (several problems: every CTA keeps one problem's N tile; UL_TC_BRES_MULTI=0
+  // restricts B residency to single-problem launches)
+  static int bres_multi = -1;
+  if (bres_multi < 0) {
+    const char* e = getenv("UL_TC_BRES_MULTI");
+    bres_multi = e ? atoi(e) != 0 : 1;
+  }
+  bool one_split = true;
+  for (int i = 0; i < np; ++i) one_split = one_split && q[i].zs == 1;
+  const bool bres_base = bres_ok && (np == 1 || bres_multi) && !amn && one_split &&
+                         (sizeof(TI) == 2 || !pair);
+  // B bytes per CTA / (problem, N tile) combos at tile width b
+  auto bres_fits = [&](int b, int64_t max_bytes) {
+    int64_t bytes = 0, combos = 0;
+    for (int i = 0; i < np; ++i) {
+      const int64_t x = ceil_div(q[i].d->K, bk) * (int64_t)b * 128;
+      bytes = x > bytes ? x : bytes;
+      combos += ceil_div(q[i].d->N, b);
+    }
+    return bres_base && bytes <= max_bytes && combos <= kNumSMs;
+  };
+  // UL_TC_BRES128=1: a 256-wide B tile too deep for shared memory becomes
+  // B-resident 128-wide tiles (measured: cfg2 update 4.41 -> 4.60 ms, cfg4
+  // 2.78 -> 2.84 ms, cfg3 0.724 -> 0.713 ms -- off by default)
+  static int bres128 = -1;
+  if (bres128 < 0) {
+    const char* e = getenv("UL_TC_BRES128");
+    bres128 = e ? atoi(e) != 0 : 0;
+  }
   // fused LayerNorm (bf16 only): single-CTA MMA, clusters along N
   if (d.epi == kEpiLnFull) {
     if constexpr (sizeof(TI) == 2) {
@@ -1172,10 +1229,12 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
     set_error("gemm_tc: fused LayerNorm needs bf16 K-major operands");
     return UL_ERR_VALUE;
   }
+#define UL_TC_BRES_MAX(EPI, BN) Smem<BN, false, (int)sizeof(OutT<TI, EPI>), EPI, true>::kBresMax
 #define UL_TC_BN(AMN, BMN, EPI, BN)                                                          \
-  if (!AMN && bres_base &&                                                                  \
-      bres_bytes <= Smem<BN, false, (int)sizeof(OutT<TI, EPI>), EPI, true>::kBresMax)       \
+  if (!AMN && bres_fits(BN, UL_TC_BRES_MAX(EPI, BN)))                                       \
     return launch<TI, AMN, BMN, EPI, BN, false, true>(q, np, s);                            \
+  if (BN == 256 && !AMN && bres128 && bres_fits(128, UL_TC_BRES_MAX(EPI, 128)))             \
+    return launch<TI, AMN, BMN, EPI, 128, false, true>(q, np, s);                           \
   if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(q, np, s);                           \
   return launch<TI, AMN, BMN, EPI, BN, false>(q, np, s);
 #define UL_TC_CASE(AMN, BMN, EPI)                 \
@@ -1194,6 +1253,7 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
   UL_TC_CASE(true, true, kEpiStore)
 #undef UL_TC_CASE
 #undef UL_TC_BN
+#undef UL_TC_BRES_MAX
   set_error("gemm_tc: unsupported layout/epilogue combination");
   return UL_ERR_VALUE;
 }

@@ -128,7 +128,7 @@ struct ReduceJob {
   int64_t n0, n1, n2;
   float *o0, *o1, *o2;
 };
-constexpr int kMaxReduceJobs = 16;
+constexpr int kMaxReduceJobs = 32;
 
 // Optional fold of the K13 prepare pass into the reduction that produces the
 // final gradients (single-process PPO step): every value the reduction

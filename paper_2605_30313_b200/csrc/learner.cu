@@ -557,6 +557,8 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
     }
     UL_TRY(mlp_pass(p, nets, be, ml, s, false, &dd, e, k));
     p->prep_folded = dd.folded;
+    if (fold.on && !dd.folded && getenv("UL_FOLD_DEBUG"))
+      fprintf(stderr, "[ul] step (%d, %d): prepare not folded\n", e, k);
     mark(p, 5, s);
     return UL_OK;
   }

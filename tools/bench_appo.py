@@ -82,6 +82,9 @@ def main():
            "transitions_per_s": rows / (ms * 1e-3), "policy_loss_last": st.policy_loss}
     # CPU: the oracle appo_update on cpu_envs envs, 1 epoch, extrapolated
     n = a.cpu_envs
+    if n <= 0:
+        print(json.dumps(res))
+        return
     sub = {k: v[:, :n] for k, v in dict(obs=w.obs, critic_obs=w.critic_obs, actions=w.actions,
                                         behavior_log_prob=blogp.astype(np.float64),
                                         rewards=w.rewards, terminated=w.terminated,
