@@ -99,7 +99,10 @@ struct Smem {
                                 kLnBytes;  // (base is 1 KB aligned)
   static constexpr int kBudget = 232448;
   static constexpr int kStagesFit = (kBudget - kStagingBytes - kFixed) / kStageBytes;
+  // (B-resident: the ring depth is chosen per launch from what the resident
+  // B tiles leave, up to kBresMaxStages; kStages = 3 sizes kBresMax)
   static constexpr int kStages = BRES ? 3 : (kStagesFit > 6 ? 6 : kStagesFit);
+  static constexpr int kBresMaxStages = 8;
   static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + kFixed;  // + B region
   static constexpr int kBresMax = kBudget - kBytes;
 };
@@ -172,6 +175,7 @@ struct TcBatch {
   int cs_pr;          // problem whose epilogue emits column sums, or -1
   int lnc;            // kEpiLnFull: CTAs per cluster = N tiles of every problem
   int bres_c;         // B-resident: (problem, N tile) combos; CTA i keeps combo i % bres_c
+  int bres_nst;       // B-resident: A ring depth of this launch
 };
 
 // BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
@@ -194,10 +198,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   constexpr int BNL = BN / CS;  // B rows (N) this CTA loads
   constexpr int BK = O::BK;
   constexpr uint32_t kChunkBytes = (uint32_t)BK * 128;  // one MN-major TMA box
-  constexpr int kStages = S::kStages;
+  // ring depth: compile-time, or per launch for B-resident launches (A-only
+  // stages are small; more of them keep more operand bytes in flight)
+  const int kStages = BRES ? B.bres_nst : S::kStages;
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
   constexpr uint32_t kBoxBytes = 32 * 64;  // one epilogue staging box
-  static_assert(kStages >= 2, "shared memory too small for the pipeline");
+  static_assert(S::kStages >= 2, "shared memory too small for the pipeline");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KB-aligned base by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared state space (LDS/STS, not generic LD/ST)
@@ -1055,9 +1061,26 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     bres_kt = B.a[i].bres_kt > bres_kt ? B.a[i].bres_kt : bres_kt;
   }
   UL_CHECK_ARG(!BRES || B.bres_c <= kNumSMs, "gemm_tc: B-resident launch with too many N tiles");
+  B.bres_nst = SM::kStages;
+  size_t bytes = SM::kBytes;
+  if (BRES) {  // as many A stages as the resident B leaves room for (UL_TC_BRES_STAGES caps)
+    static int cap_env = -1;
+    if (cap_env < 0) {
+      const char* e = getenv("UL_TC_BRES_STAGES");
+      cap_env = e ? atoi(e) : SM::kBresMaxStages;
+    }
+    const size_t bres = (size_t)bres_kt * SM::kBBytes;
+    const size_t other = SM::kBytes - (size_t)SM::kStages * SM::kStageBytes;
+    int nst = (int)((SM::kBudget - other - bres) / SM::kStageBytes);
+    nst = nst > cap_env ? cap_env : nst;
+    nst = nst > SM::kBresMaxStages ? SM::kBresMaxStages : nst;
+    UL_CHECK_ARG(nst >= 2, "gemm_tc: B-resident launch leaves no room for the A ring");
+    B.bres_nst = nst;
+    bytes = other + (size_t)nst * SM::kStageBytes + bres;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kPThreads);
-  cfg.dynamicSmemBytes = SM::kBytes + (BRES ? (size_t)bres_kt * SM::kBBytes : 0);
+  cfg.dynamicSmemBytes = bytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -87,6 +87,18 @@ inline void mark(PpoPlan* p, int cat, cudaStream_t s) {
   pr->n++;
 }
 
+// Diagnostics only (tools/step_ablate.py): UL_ABLATE bit mask drops pieces of
+// every step from the plan to time the rest -- 1 gather, 2 Adam apply, 4 the
+// fused output stage, 8 the forward.  Results are meaningless when set.
+int ablate_mask() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("UL_ABLATE");
+    m = e ? atoi(e) : 0;
+  }
+  return m;
+}
+
 size_t ctl_header_bytes() { return offsetof(ul_opt_ctl, part); }
 
 int alloc_plan(PpoPlan* p) {
@@ -383,7 +395,7 @@ int gather_ahead(PpoPlan* p, int e, int k, cudaStream_t s) {
     ++ne;
   }
   // (one graph per epoch: the next epoch's permutation is not uploaded yet)
-  if (!on || ne >= p->d.epochs || (p->epoch_mode && ne != e)) return UL_OK;
+  if (!on || (ablate_mask() & 1) || ne >= p->d.epochs || (p->epoch_mode && ne != e)) return UL_OK;
   UL_CUDA(cudaEventRecord(p->ev_gfork, s));
   UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_gfork, 0));
   UL_TRY(step_gather(p, ne, nk, p->side, true));
@@ -416,7 +428,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   if (p->gathered_ahead) {  // gathered on the side stream under the previous step
     UL_CUDA(cudaStreamWaitEvent(s, p->ev_gjoin, 0));
     p->gathered_ahead = false;
-  } else {
+  } else if (!(ablate_mask() & 1)) {
     UL_TRY(step_gather(p, e, k, s));
   }
   mark(p, 1, s);
@@ -478,7 +490,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
       nets[k].head_db_below = head_needs_colsum(nets[k]);
     }
   }
-  UL_TRY(mlp_pass(p, nets, be, ml, s, true));
+  if (!(ablate_mask() & 8)) UL_TRY(mlp_pass(p, nets, be, ml, s, true));
   mark(p, 0, s);
   if (fused) {
     PpoFusedArgs f{};
@@ -535,7 +547,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
     f.lossp = reinterpret_cast<float*>(p->head_part);  // (doubles region, ample as floats)
     f.lossld = ceil_div(3 + p->A, 4) * 4;
     DeferredDw dd;
-    UL_TRY(launch_ppo_fused(f, p->dt, dd.jobs, &dd.nj, s));
+    if (!(ablate_mask() & 4)) UL_TRY(launch_ppo_fused(f, p->dt, dd.jobs, &dd.nj, s));
     mark(p, 2, s);
     // single process: the reduction that writes the final gradients also
     // takes their joint norm / finiteness and runs the prepare tail (every
@@ -622,7 +634,7 @@ int step_apply(PpoPlan* p, int e, int k, cudaStream_t s) {
   // (folded: the step's gradient reduction already ran the prepare tail)
   if (!p->prep_folded) UL_TRY(launch_prepare(st, p->ctl_d, s, &lf));
   p->prep_folded = false;
-  UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s, tc ? &so : nullptr));
+  if (!(ablate_mask() & 2)) UL_TRY(launch_apply(st, p->ctl_d, 0, 1, s, tc ? &so : nullptr));
   mark(p, 3, s);
   return UL_OK;
 }
