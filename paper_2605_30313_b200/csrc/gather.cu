@@ -133,7 +133,11 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
         for (int e = 0; e < 2; ++e) {
           const int u = e ? u1 : u0;
           if (u >= upr) continue;
-          if (CVT) {
+          if constexpr (CVT && U == 4) {  // one fp32 -> one bf16 (4-byte-aligned source rows)
+            float f = __uint_as_float(v[k][e]);
+            if (u == ones_u) f = 1.f;
+            reinterpret_cast<__nv_bfloat16*>(dp[k])[u] = __float2bfloat16_rn(f);
+          } else if (CVT) {
             float4 f4 = *reinterpret_cast<float4*>(&v[k][e]);
             float f[4] = {f4.x, f4.y, f4.z, f4.w};
             if (u == ones_u) {  // (selects, no dynamically indexed local array)
@@ -158,6 +162,9 @@ __device__ __forceinline__ void copy_rows(const char* __restrict__ src, char* __
   }
 }
 
+// CVT4: some desc converts 4-byte-aligned rows one float per lane (a separate
+// instantiation, so the common launch keeps its register budget)
+template <bool CVT4>
 __global__ void __launch_bounds__(256) gather_kernel(GatherTable t,
                                                      const int64_t* __restrict__ idx, int64_t n,
                                                      int64_t modulo, int64_t lo, int64_t hi,
@@ -170,8 +177,12 @@ __global__ void __launch_bounds__(256) gather_kernel(GatherTable t,
   const int blk = (int)blockIdx.x - t.blk0[d], nblk = t.blk0[d + 1] - t.blk0[d];
   const int upr = (int)t.units[d], sh = t.lpr_shift[d];
   if (t.cvt[d]) {
-    copy_rows<16, true>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
-                        modulo, lo, hi, err, t.ones[d], blk, nblk);
+    if (!CVT4 || t.unit[d] == 16)
+      copy_rows<16, true>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
+                          modulo, lo, hi, err, t.ones[d], blk, nblk);
+    else
+      copy_rows<4, true>(t.src[d], t.dst[d], t.src_stride[d], t.dst_stride[d], upr, sh, idx, n,
+                         modulo, lo, hi, err, t.ones[d], blk, nblk);
     return;
   }
   switch (t.unit[d]) {
@@ -292,10 +303,17 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
     const int c = cvt ? cvt[d] : 0;
     int u;
     if (c) {
-      UL_CHECK_ARG(((uintptr_t)src[d] & 15) == 0 && ((uintptr_t)dst[d] & 7) == 0 &&
-                       src_stride[d] % 16 == 0 && dst_stride[d] % 8 == 0 && row_bytes[d] % 16 == 0,
-                   "gather: bf16 conversion needs 16-byte source rows (desc %d)", d);
-      u = 16;
+      // 16-byte fp32 units -> 8-byte bf16 units when the rows allow it, else
+      // one float -> one bf16 (4-byte-aligned rows, e.g. unpadded 940 B obs rows)
+      if (((uintptr_t)src[d] & 15) == 0 && ((uintptr_t)dst[d] & 7) == 0 &&
+          src_stride[d] % 16 == 0 && dst_stride[d] % 8 == 0 && row_bytes[d] % 16 == 0) {
+        u = 16;
+      } else {
+        UL_CHECK_ARG(((uintptr_t)src[d] & 3) == 0 && ((uintptr_t)dst[d] & 1) == 0 &&
+                         src_stride[d] % 4 == 0 && dst_stride[d] % 2 == 0 && row_bytes[d] % 4 == 0,
+                     "gather: bf16 conversion needs 4-byte source rows (desc %d)", d);
+        u = 4;
+      }
     } else {
       u = unit_for((uintptr_t)src[d], (uintptr_t)dst[d], src_stride[d], dst_stride[d],
                    row_bytes[d]);
@@ -323,7 +341,12 @@ int gather_rows(int ndesc, const void* const* src, void* const* dst, const int64
     nb_total += (int)nb;
   }
   t.blk0[ndesc] = nb_total;
-  return launch_pdl("gather_kernel", gather_kernel, dim3((unsigned)nb_total), dim3(256), 0,
+  bool cvt4 = false;
+  for (int d = 0; d < ndesc; ++d) cvt4 = cvt4 || (t.cvt[d] && t.unit[d] == 4);
+  if (cvt4)
+    return launch_pdl("gather_kernel", gather_kernel<true>, dim3((unsigned)nb_total), dim3(256), 0,
+                      stream, t, idx, n, modulo, lo, hi, err);
+  return launch_pdl("gather_kernel", gather_kernel<false>, dim3((unsigned)nb_total), dim3(256), 0,
                     stream, t, idx, n, modulo, lo, hi, err);
 }
 }  // namespace ul

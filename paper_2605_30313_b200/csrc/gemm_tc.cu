@@ -176,6 +176,7 @@ struct TcBatch {
   int lnc;            // kEpiLnFull: CTAs per cluster = N tiles of every problem
   int bres_c;         // B-resident: (problem, N tile) combos; CTA i keeps combo i % bres_c
   int bres_nst;       // B-resident: A ring depth of this launch
+  int bres_kt_max;    // B-resident: K tiles of the deepest problem (the smem layout)
 };
 
 // BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
@@ -209,7 +210,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // compiler keeps the shared state space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw;  // 1 KB aligned (128 B-swizzled TMA tiles need it)
   if (threadIdx.x == 0 && (su32(smem_raw) & 1023u)) __trap();
-  const uint32_t bres_bytes = BRES ? (uint32_t)p0_.bres_kt * S::kBBytes : 0u;
+  // (region sized for the deepest problem; a CTA fills its own problem's K tiles)
+  const uint32_t bres_bytes = BRES ? (uint32_t)B.bres_kt_max * S::kBBytes : 0u;
   uint8_t* sbres = smem + kStages * S::kStageBytes;  // B-resident K tiles
   uint8_t* staging = sbres + bres_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(staging + S::kStagingBytes);
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (BRES && t_begin < t_end) {
         // this CTA's N tile of B, all K tiles, once
         const Tile T0 = tile_of(t_begin);
-        mbar_expect_tx(bres_bar, bres_bytes);
+        mbar_expect_tx(bres_bar, (uint32_t)T0.kt_n * S::kBBytes);
         for (int kt = 0; kt < T0.kt_n; ++kt) {
           uint8_t* sb = sbres + kt * S::kBBytes;
           if (B_MN) {
@@ -1060,6 +1062,7 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     B.bres_c += B.a[i].nt;
     bres_kt = B.a[i].bres_kt > bres_kt ? B.a[i].bres_kt : bres_kt;
   }
+  B.bres_kt_max = bres_kt;
   UL_CHECK_ARG(!BRES || B.bres_c <= kNumSMs, "gemm_tc: B-resident launch with too many N tiles");
   B.bres_nst = SM::kStages;
   size_t bytes = SM::kBytes;

@@ -130,6 +130,19 @@ struct ReduceJob {
 };
 constexpr int kMaxReduceJobs = 32;
 
+// Diagnostics only (tools/step_ablate.py): UL_ABLATE bit mask drops pieces of
+// every PPO step to time the rest -- 1 gather, 2 Adam apply, 4 the fused
+// output stage, 8 the forward, 16 the dX GEMMs, 32 the batched dW GEMMs,
+// 64 the gradient reduction.  Results are meaningless when set.
+inline int ablate_mask() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("UL_ABLATE");
+    m = e ? atoi(e) : 0;
+  }
+  return m;
+}
+
 // Optional fold of the K13 prepare pass into the reduction that produces the
 // final gradients (single-process PPO step): every value the reduction
 // stores inside [base, base + n0) (segment 0) or [base + n0, base + n0 + n1)

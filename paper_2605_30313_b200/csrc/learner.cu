@@ -87,18 +87,6 @@ inline void mark(PpoPlan* p, int cat, cudaStream_t s) {
   pr->n++;
 }
 
-// Diagnostics only (tools/step_ablate.py): UL_ABLATE bit mask drops pieces of
-// every step from the plan to time the rest -- 1 gather, 2 Adam apply, 4 the
-// fused output stage, 8 the forward.  Results are meaningless when set.
-int ablate_mask() {
-  static int m = -1;
-  if (m < 0) {
-    const char* e = getenv("UL_ABLATE");
-    m = e ? atoi(e) : 0;
-  }
-  return m;
-}
-
 size_t ctl_header_bytes() { return offsetof(ul_opt_ctl, part); }
 
 int alloc_plan(PpoPlan* p) {
@@ -354,7 +342,10 @@ int step_gather(PpoPlan* p, int e, int k, cudaStream_t s, bool ahead = false) {
                            : b.perm + (int64_t)e * p->rows + (int64_t)k * p->mb + p->d.rank * ml;
   const bool bf = p->dt == kBf16;
   // K4: one gather launch for the 7 per-row arrays; the obs / critic-obs
-  // pad column is set to 1.0 (the tensor-core dW's bias column)
+  // pad column is set to 1.0 (the tensor-core dW's bias column).  Segment
+  // rows may be unpadded (ld == width, the H2D landing layout): the ones
+  // unit is then read one float past the row (the segment buffers carry a
+  // 16-byte tail) and replaced.
   const void* src[7] = {b.obs, b.cobs, b.act, b.blogp, b.adv, b.ret, b.oldv};
   void* dst[7] = {p->mb_obs, p->mb_cobs, p->mb_act, p->mb_scal, p->mb_scal + ml,
                   p->mb_scal + 2 * ml, p->mb_scal + 3 * ml};
@@ -362,9 +353,15 @@ int step_gather(PpoPlan* p, int e, int k, cudaStream_t s, bool ahead = false) {
   const int64_t xb = bf ? 2 : 4;
   const int64_t sst[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->d.ld_act, 4, 4, 4, 4};
   const int64_t dstr[7] = {xb * p->ld_mo, xb * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
-  const int64_t rb[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->ld_ma, 4, 4, 4, 4};
   const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
-  const bool ones_o = p->d.ld_obs > od, ones_c = p->d.ld_cobs > cd;
+  const bool ones_o = p->ld_mo > od, ones_c = p->ld_mc > cd;
+  // (a padded segment row is read whole -- 16-byte units when it allows;
+  // an unpadded one plus the ones unit)
+  auto row_b = [](bool ones, int64_t d, int64_t ld, int64_t ldm) {
+    return 4 * (!ones ? d : ld > d ? (ld < ldm ? ld : ldm) : d + 1);
+  };
+  const int64_t rb[7] = {row_b(ones_o, od, p->d.ld_obs, p->ld_mo),
+                         row_b(ones_c, cd, p->d.ld_cobs, p->ld_mc), 4 * p->ld_ma, 4, 4, 4, 4};
   const int64_t ones[7] = {ones_o ? 4 * od : -1, ones_c ? 4 * cd : -1, -1, -1, -1, -1, -1};
   const int cvt[7] = {bf ? 1 : 0, bf ? 1 : 0, 0, 0, 0, 0, 0};
   // the gather-ahead on the side stream takes at most 2 CTAs per SM, so it
@@ -424,7 +421,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   const int64_t ml = p->mb_local;
   const bool tc = p->d.gemm_backend >= 1;
   const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
-  const bool ones_o = p->d.ld_obs > od, ones_c = p->d.ld_cobs > cd;
+  const bool ones_o = p->ld_mo > od, ones_c = p->ld_mc > cd;
   if (p->gathered_ahead) {  // gathered on the side stream under the previous step
     UL_CUDA(cudaStreamWaitEvent(s, p->ev_gjoin, 0));
     p->gathered_ahead = false;
@@ -708,11 +705,15 @@ extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
       return st;
     }
   }
-  if (p->dt == ul::kBf16 && ((desc->ld_obs * 4) % 16 || (desc->ld_cobs * 4) % 16))
-    return fail("ppo plan: the bf16 back end needs 16-byte obs / critic-obs rows");
-  // bf16 staging rows: round_up(ld, 8) elements (16-byte TMA rows)
-  p->ld_mo = p->dt == ul::kBf16 ? (desc->ld_obs + 7) / 8 * 8 : desc->ld_obs;
-  p->ld_mc = p->dt == ul::kBf16 ? (desc->ld_cobs + 7) / 8 * 8 : desc->ld_cobs;
+  // minibatch staging rows: the feature width + the ones column, padded to
+  // 16-byte TMA rows (bf16: round_up(d + 1, 8) elements, fp32: round_up(d + 1, 4)),
+  // whatever the segment's own row pitch
+  {
+    const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
+    const int64_t q = p->dt == ul::kBf16 ? 8 : 4;
+    p->ld_mo = (od + 1 + q - 1) / q * q;
+    p->ld_mc = (cd + 1 + q - 1) / q * q;
+  }
   p->ld_ma = desc->ld_act;
   p->Pa = p->va.total;
   p->Pc = p->vc.total;

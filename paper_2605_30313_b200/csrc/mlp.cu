@@ -983,7 +983,7 @@ int run_deferred_dw_gemms(DeferredDw& D, cudaStream_t s) {
       D.dw[i].splits = tc_num_splits(D.dw[i].K, want, D.dw[i].dtype);
       D.jobs[D.dw_job[i]].nz = D.dw[i].splits;
     }
-    UL_TRY(gemm_tc_batch(D.dw, D.ndw, s));
+    if (!(ablate_mask() & 32)) UL_TRY(gemm_tc_batch(D.dw, D.ndw, s));
   }
   D.ndw = 0;
   return UL_OK;
@@ -991,7 +991,7 @@ int run_deferred_dw_gemms(DeferredDw& D, cudaStream_t s) {
 
 int run_deferred_dw_reduce(DeferredDw& D, cudaStream_t s) {
   D.folded = false;
-  if (D.nj) UL_TRY(launch_reduce(D.jobs, D.nj, s, D.fold, &D.folded));
+  if (D.nj && !(ablate_mask() & 64)) UL_TRY(launch_reduce(D.jobs, D.nj, s, D.fold, &D.folded));
   D.ndw = D.nj = 0;
   return UL_OK;
 }
@@ -1347,7 +1347,7 @@ int mlp_backward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream
       S.dh = nxt;
       S.lddh = act_ld((int)in, dt);
     }
-    UL_TRY(run_gemms(gx, has_x, tc_x, no_ones, s));
+    if (!(ablate_mask() & 16)) UL_TRY(run_gemms(gx, has_x, tc_x, no_ones, s));
     for (int k = 0; k < n; ++k) {
       if (!cs_on[k]) continue;
       if (cs_nz[k] == 0) continue;  // GEMM fell back to SIMT: colsum kernel later

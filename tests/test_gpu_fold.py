@@ -118,3 +118,36 @@ def test_folded_prepare_small_update_matches_separate():
     assert abs(s1.grad_norm - s0.grad_norm) <= 1e-9 * max(1.0, s0.grad_norm)
     for x, y in ((p0.actor.flat(), p1.actor.flat()), (p0.critic.flat(), p1.critic.flat())):
         assert np.abs(x.astype(np.float64) - y).max() <= 1e-6
+
+
+def test_unpadded_segment_rows_gather_identically():
+    """A segment staged in the host row layout (raw_rows: 940-byte obs rows,
+    no re-pitch; the minibatch gather converts one float per lane and reads
+    the ones unit one float past each row) gives the SAME bf16 update as the
+    padded 16-byte-row layout, bit for bit."""
+    from paper_2605_30313_b200.algos import _staging as STG
+
+    T, N, od, cd, ad, hid = 6, 512, 235, 101, 12, (256, 128, 128)
+    segd, actor, critic = _synthetic(T, N, od, cd, ad, hid, seed=8)
+    P.set_precision("bf16")
+    cfg = A.PpoConfig(epochs=2, minibatches=2)
+    out = []
+    for raw in (False, True):
+        PPO._PLANS.clear()
+        STG._CACHE.clear()
+        ds = STG.DeviceSegment(T, N, od, cd, ad, cfg.epochs, raw_rows=raw)
+        STG._CACHE[("ppo", T, N, od, cd, ad, cfg.epochs, torch.cuda.current_device())] = ds
+        params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(od, hid, ad), actor.flat()),
+                            TN.ModelParams.from_numpy(TN.Arch(cd, hid, 1), critic.flat()))
+        opt = A.AcOpt.for_params(params, 1e-3)
+        seg = A.RolloutSegment(**segd)
+        seg.advantages, seg.returns = A.gae(seg.rewards, seg.values, seg.terminated,
+                                            seg.truncated, seg.bootstrap_value, 0.99, 0.95,
+                                            truncation_values=seg.truncation_values)
+        st = A.ppo_update(seg, params, opt, cfg, O.philox_stream(2, "update"))
+        assert ds.obs.stride(0) == (od if raw else 236)
+        out.append((params.actor.flat(), params.critic.flat(), st.policy_loss))
+    STG._CACHE.clear()
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
