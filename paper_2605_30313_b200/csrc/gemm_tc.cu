@@ -1177,9 +1177,13 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
     const char* e = getenv("UL_TC_PAIR");
     pair_ok = e ? atoi(e) : -2;
   }
-  // default: pairs for tf32 (4-byte operands: the halved B traffic pays),
-  // single CTAs for bf16 (measured faster end to end on the cfg2 update)
-  const bool want = pair_ok == -2 ? sizeof(TI) == 4 : pair_ok != 0;
+  // default: pairs for tf32 (4-byte operands: the halved B traffic pays) and
+  // for deep-K bf16 GEMMs (K >= 1024: the FlashSAC 1024-wide critics, 2.81 ->
+  // 2.68 ms per cfg4 update); single CTAs for the shallow bf16 GEMMs (the cfg2
+  // update, K <= 512, measured faster without)
+  bool deep = true;
+  for (int i = 0; i < np; ++i) deep = deep && q[i].d->K >= 1024;
+  const bool want = pair_ok == -2 ? (sizeof(TI) == 4 || deep) : pair_ok != 0;
   // dW batches (both operands MN-major, K = the minibatch rows): CTA pairs
   // split B between the two SMs, cutting the per-SM operand stream of these
   // L2-bound GEMMs by a third; a single-M-tile problem's second CTA computes
