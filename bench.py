@@ -408,15 +408,19 @@ def run_ours(args):
         if arm == prec:
             continue
         PKG.set_precision(arm)
+        # (the bf16 headline stages bf16 observation rows; an fp32-storage
+        # back end gets its own fp32 staging of the same segment)
+        ds_arm = staging_for(T, N, od, cd, ad, cfg.epochs)
+        ds_arm.load(seg, with_advantages=False)
         for _ in range(2):
-            P.ppo_update_resident(ds, params, opt, cfg, rng)
+            P.ppo_update_resident(ds_arm, params, opt, cfg, rng)
         torch.cuda.synchronize()
         barrier()
         t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n_arm = max(3, min(args.steps, 10)) if arm == "tf32" else 3
         t0e.record()
         for _ in range(n_arm):
-            P.ppo_update_resident(ds, params, opt, cfg, rng)
+            P.ppo_update_resident(ds_arm, params, opt, cfg, rng)
         t1e.record()
         torch.cuda.synchronize()
         a_ms = max_over_ranks(t0e.elapsed_time(t1e)) / n_arm

@@ -214,6 +214,13 @@ int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
                    const int64_t* src_stride, const int64_t* dst_stride, const int64_t* row_bytes,
                    const int64_t* ones_byte, const int64_t* idx, int64_t n, int64_t modulo,
                    int64_t lo, int64_t hi, int* err, void* stream);
+/* ul_gather_rows + a per-desc conversion flag: cvt[d] = 1 turns fp32 source
+ * rows into bf16 destination rows (row_bytes / ones_byte count SOURCE bytes;
+ * the bf16 staging of a PPO segment's observation rows). */
+int ul_gather_rows_cvt(int ndesc, const void* const* src, void* const* dst,
+                       const int64_t* src_stride, const int64_t* dst_stride,
+                       const int64_t* row_bytes, const int64_t* ones_byte, const int* cvt,
+                       const int64_t* idx, int64_t n, void* stream);
 
 /* Replay ring insert (R:replaypath/storage.py:76-104): n rows of `width`
  * floats at absolute index `head`; rows may be pinned-host or device memory.
@@ -294,6 +301,9 @@ typedef struct ul_ppo_plan_desc {
                                        global minibatch is the union of the
                                        ranks' local minibatches              */
   int32_t gemm_backend;             /* UL_GEMM_FP32 / _TF32 / _BF16 / _TF32X3 */
+  int32_t obs_bf16;                 /* 1: obs / cobs bindings hold bf16 rows (ld_obs /
+                                       ld_cobs in elements, the ones column already
+                                       set); UL_GEMM_BF16 only                */
 } ul_ppo_plan_desc;
 
 typedef struct ul_ppo_bindings {

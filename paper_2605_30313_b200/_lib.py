@@ -76,6 +76,7 @@ class PpoPlanDesc(C.Structure):
         ("clip_param", f64), ("entropy_coef", f64), ("value_loss_coef", f64),
         ("use_clipped_value_loss", i32), ("max_grad_norm", f64), ("world_size", i32),
         ("rank", i32), ("raw_advantages", i32), ("local_shards", i32), ("gemm_backend", i32),
+        ("obs_bf16", i32),
     ]
 
 
@@ -159,6 +160,8 @@ _PROTOS = {
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                  C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
                                  vp]),
+    "ul_gather_rows_cvt": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
+                                     C.POINTER(i64), C.POINTER(i64), vp, vp, vp, i64, vp]),
     "ul_narrow_f64": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), vp]),
     "ul_ring_insert": (C.c_int, [vp, i64, i64, i64, vp, i64, vp]),
     "ul_device_permutation": (C.c_int, [i64, C.c_uint64, vp, vp]),

@@ -15,6 +15,8 @@ stays valid across updates: each update overwrites the same HBM.
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 import torch
 
@@ -27,7 +29,7 @@ def _is_dev(x) -> bool:
 
 class DeviceSegment:
     def __init__(self, T: int, N: int, obs_dim: int, cobs_dim: int, act_dim: int, epochs: int,
-                 raw_rows: bool = False):
+                 raw_rows: bool = False, bf16_rows: bool = False):
         dev = _dev.require_cuda()
         self.T, self.N, self.rows = T, N, T * N
         self.dims = (obs_dim, cobs_dim, act_dim)
@@ -37,18 +39,30 @@ class DeviceSegment:
         # Off by default: the gather then converts one float per lane (4-byte
         # aligned 940 B rows) and costs more per update (cfg2: 4.52 vs 4.34
         # ms) than the re-pitch pass it saves (e2e 4.74 vs 4.68 ms).
-        self.raw_rows = raw_rows
-        self.ld = tuple(self.dims) if raw_rows else tuple(_dev.feature_ld(d) for d in self.dims)
+        # bf16_rows (bf16 back end): obs / cobs are staged ONCE per segment as
+        # the bf16 rows the networks read -- round_up(d + 1, 8) wide, ones
+        # column set -- by the re-pitch pass that follows the H2D, so every
+        # minibatch gather copies half the bytes (16-byte units, no conversion)
+        self.raw_rows = raw_rows and not bf16_rows
+        self.bf16_rows = bf16_rows
+        if bf16_rows:
+            ld8 = lambda d: (d + 1 + 7) // 8 * 8  # noqa: E731
+            self.ld = (ld8(obs_dim), ld8(cobs_dim), _dev.feature_ld(act_dim))
+        elif raw_rows:
+            self.ld = tuple(self.dims)
+        else:
+            self.ld = tuple(_dev.feature_ld(d) for d in self.dims)
         f32 = dict(dtype=torch.float32, device=dev)
         rows = self.rows
 
-        def rows_buf(ld):
-            if not raw_rows:
-                return _dev.zeros((rows, ld), **f32)
+        def rows_buf(ld, dtype=torch.float32):
+            if not self.raw_rows:
+                return _dev.zeros((rows, ld), dtype=dtype, device=dev)
             return _dev.zeros(rows * ld + 4, **f32)[:rows * ld].view(rows, ld)
 
-        self.obs = rows_buf(self.ld[0])
-        self.cobs = rows_buf(self.ld[1])
+        row_dt = torch.bfloat16 if bf16_rows else torch.float32
+        self.obs = rows_buf(self.ld[0], row_dt)
+        self.cobs = rows_buf(self.ld[1], row_dt)
         self.act = rows_buf(self.ld[2])
         self.blogp = _dev.zeros(rows, **f32)
         self.rewards = _dev.zeros(rows, **f32)
@@ -80,21 +94,34 @@ class DeviceSegment:
         copy of a segment can be queued before any re-pitch kernel)."""
         raw = self._raw.get(name)
         if raw is None or raw.numel() != self.rows * width:
-            raw = torch.empty(self.rows * width, dtype=torch.float32, device=device)
+            # (+16 B: a bf16 re-pitch reads one float past the last row)
+            raw = torch.empty(self.rows * width + 4, dtype=torch.float32,
+                              device=device)[:self.rows * width]
             self._raw[name] = raw
         return raw
 
     def _repitch(self, jobs) -> None:
-        """One K4 row-kernel launch re-pitching landed fields into their HBM rows."""
+        """One K4 row-kernel launch re-pitching landed fields into their HBM rows
+        (bf16 destinations: converted on the way, ones column set)."""
         if not jobs:
             return
         n = len(jobs)
-        _lib.call("ul_gather_rows", n, _lib.ptr_array([_dev.ptr(r) for r, _, _ in jobs]),
-                  _lib.ptr_array([_dev.ptr(d) for _, d, _ in jobs]),
-                  _lib.i64_array([w * 4 for _, _, w in jobs]),
-                  _lib.i64_array([d.stride(0) * 4 for _, d, _ in jobs]),
-                  _lib.i64_array([w * 4 for _, _, w in jobs]), None, None, jobs[0][1].shape[0],
-                  0, 0, jobs[0][1].shape[0], None, _dev.stream())
+        nrows = jobs[0][1].shape[0]
+        src = _lib.ptr_array([_dev.ptr(r) for r, _, _ in jobs])
+        dst = _lib.ptr_array([_dev.ptr(d) for _, d, _ in jobs])
+        sst = _lib.i64_array([w * 4 for _, _, w in jobs])
+        dst_stride = _lib.i64_array([d.stride(0) * d.element_size() for _, d, _ in jobs])
+        if not any(d.dtype == torch.bfloat16 for _, d, _ in jobs):
+            _lib.call("ul_gather_rows", n, src, dst, sst, dst_stride, sst, None, None, nrows,
+                      0, 0, nrows, None, _dev.stream())
+            return
+        # bf16 rows: read the width + one float (replaced by the ones column;
+        # the landing buffers carry a 16-byte tail)
+        cvt = [1 if d.dtype == torch.bfloat16 else 0 for _, d, _ in jobs]
+        rb = _lib.i64_array([(w + c) * 4 for (_, _, w), c in zip(jobs, cvt)])
+        ones = _lib.i64_array([w * 4 if c else -1 for (_, _, w), c in zip(jobs, cvt)])
+        _lib.call("ul_gather_rows_cvt", n, src, dst, sst, dst_stride, rb, ones,
+                  (C.c_int * n)(*cvt), None, nrows, _dev.stream())
 
     def _put_rows(self, name: str, dst: torch.Tensor, src, width: int, jobs: list) -> None:
         """Host [rows, width] -> HBM [rows, ld]: one contiguous H2D at full PCIe
@@ -103,6 +130,13 @@ class DeviceSegment:
         appended to `jobs` and launched after every copy of the segment: on
         the copy stream a kernel queued between two copies waits for SMs the
         running update holds, and would stall the copies behind it."""
+        if _is_dev(src) and dst.dtype == torch.bfloat16:  # device rows -> bf16 rows
+            src = src.reshape(self.rows, width).to(torch.float32).contiguous()
+            raw = self._raw_for(name, width, dst.device)
+            _lib.call("ul_memcpy_async", _dev.ptr(raw), _dev.ptr(src), src.numel() * 4,
+                      _dev.stream())
+            jobs.append((raw, dst, width))
+            return
         if _is_dev(src):  # device -> device staging copy (copy engine, re-pitched)
             src = src.reshape(self.rows, width)
             if src.dtype != torch.float32:
@@ -214,6 +248,12 @@ class DeviceSegment:
         part = raw[t * N * width:(t + 1) * N * width]
         _dev.h2d(part, a)
         rb = width * 4
+        if dst.dtype == torch.bfloat16:  # converted, ones column set
+            _lib.call("ul_gather_rows_cvt", 1, _lib.ptr_array([_dev.ptr(part)]),
+                      _lib.ptr_array([_dev.ptr(dst[t * N:(t + 1) * N])]), _lib.i64_array([rb]),
+                      _lib.i64_array([dst.stride(0) * 2]), _lib.i64_array([rb + 4]),
+                      _lib.i64_array([rb]), (C.c_int * 1)(1), None, N, _dev.stream())
+            return
         _lib.call("ul_gather_rows", 1, _lib.ptr_array([_dev.ptr(part)]),
                   _lib.ptr_array([_dev.ptr(dst[t * N:(t + 1) * N])]), _lib.i64_array([rb]),
                   _lib.i64_array([dst.stride(0) * 4]), _lib.i64_array([rb]), None, None, N,
@@ -267,11 +307,21 @@ class DeviceSegment:
 _CACHE: dict = {}
 
 
+def bf16_rows_default(slot: str) -> bool:
+    """PPO staging on the bf16 back end keeps observation rows in bf16 (APPO's
+    recompute forward reads fp32 segment rows; UL_BF16_ROWS=0 disables)."""
+    import os
+
+    return (slot != "appo" and _lib.gemm_backend() == 2
+            and os.environ.get("UL_BF16_ROWS", "1") != "0")
+
+
 def staging_for(T, N, obs_dim, cobs_dim, act_dim, epochs, slot: str = "ppo") -> DeviceSegment:
-    key = (slot, T, N, obs_dim, cobs_dim, act_dim, max(epochs, 1), torch.cuda.current_device())
+    bf = bf16_rows_default(slot)
+    key = (slot, T, N, obs_dim, cobs_dim, act_dim, max(epochs, 1), torch.cuda.current_device(), bf)
     ds = _CACHE.get(key)
     if ds is None:
-        ds = DeviceSegment(T, N, obs_dim, cobs_dim, act_dim, epochs)
+        ds = DeviceSegment(T, N, obs_dim, cobs_dim, act_dim, epochs, bf16_rows=bf)
         ds.slot = slot
         _CACHE[key] = ds
     return ds

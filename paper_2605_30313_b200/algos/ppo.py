@@ -132,7 +132,8 @@ def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
     key = (params.actor.arch, params.critic.arch, ds.rows, ds.ld, cfg.epochs, cfg.minibatches,
            cfg.clip_param, cfg.entropy_coef, cfg.value_loss_coef, cfg.use_clipped_value_loss,
            cfg.max_grad_norm, world, rank, raw_adv, _dist.segment_mode(), _dist.dp_forced(),
-           _lib.gemm_backend(), torch.cuda.current_device(), getattr(ds, "slot", "ppo"))
+           _lib.gemm_backend(), torch.cuda.current_device(), getattr(ds, "slot", "ppo"),
+           getattr(ds, "bf16_rows", False))
     plan = _PLANS.get(key)
     if plan is None:
         d = _lib.PpoPlanDesc()
@@ -148,6 +149,7 @@ def _plan_for(params: AcParams, cfg: PpoConfig, ds, world: int, rank: int,
         d.world_size, d.rank, d.raw_advantages = world, rank, int(raw_adv)
         d.local_shards = int(_dist.segment_mode() == "local" and _dp_path(world))
         d.gemm_backend = _lib.gemm_backend()
+        d.obs_bf16 = int(getattr(ds, "bf16_rows", False))
         plan = _Plan(d)
         _PLANS[key] = plan
     return plan

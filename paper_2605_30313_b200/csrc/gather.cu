@@ -364,6 +364,15 @@ extern "C" int ul_gather_rows(int ndesc, const void* const* src, void* const* ds
                          idx, n, modulo, lo, hi, err, ul::as_stream(stream));
 }
 
+// ul_gather_rows with per-desc fp32 -> bf16 conversion (no index window)
+extern "C" int ul_gather_rows_cvt(int ndesc, const void* const* src, void* const* dst,
+                                  const int64_t* src_stride, const int64_t* dst_stride,
+                                  const int64_t* row_bytes, const int64_t* ones_byte,
+                                  const int* cvt, const int64_t* idx, int64_t n, void* stream) {
+  return ul::gather_rows(ndesc, src, dst, src_stride, dst_stride, row_bytes, ones_byte, cvt, idx,
+                         n, 0, 0, INT64_MAX, nullptr, ul::as_stream(stream));
+}
+
 // Replay ring insert (R:replaypath/storage.py:76-104): write n rows of `width`
 // floats at absolute index head.. into ring[cap, width]; rows may live in
 // pinned host memory (H2D) or device memory (D2D).  n >= cap keeps only the

@@ -351,7 +351,10 @@ int step_gather(PpoPlan* p, int e, int k, cudaStream_t s, bool ahead = false) {
                   p->mb_scal + 2 * ml, p->mb_scal + 3 * ml};
   // (bf16 path: the two network inputs are converted to bf16 rows on the way)
   const int64_t xb = bf ? 2 : 4;
-  const int64_t sst[7] = {4 * p->d.ld_obs, 4 * p->d.ld_cobs, 4 * p->d.ld_act, 4, 4, 4, 4};
+  // (bf16 segment rows: already converted, padded and carrying the ones
+  // column -- copied as whole 16-byte units, half the bytes of fp32 rows)
+  const int64_t sb = p->d.obs_bf16 ? 2 : 4;
+  const int64_t sst[7] = {sb * p->d.ld_obs, sb * p->d.ld_cobs, 4 * p->d.ld_act, 4, 4, 4, 4};
   const int64_t dstr[7] = {xb * p->ld_mo, xb * p->ld_mc, 4 * p->ld_ma, 4, 4, 4, 4};
   const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
   const bool ones_o = p->ld_mo > od, ones_c = p->ld_mc > cd;
@@ -360,10 +363,13 @@ int step_gather(PpoPlan* p, int e, int k, cudaStream_t s, bool ahead = false) {
   auto row_b = [](bool ones, int64_t d, int64_t ld, int64_t ldm) {
     return 4 * (!ones ? d : ld > d ? (ld < ldm ? ld : ldm) : d + 1);
   };
-  const int64_t rb[7] = {row_b(ones_o, od, p->d.ld_obs, p->ld_mo),
-                         row_b(ones_c, cd, p->d.ld_cobs, p->ld_mc), 4 * p->ld_ma, 4, 4, 4, 4};
-  const int64_t ones[7] = {ones_o ? 4 * od : -1, ones_c ? 4 * cd : -1, -1, -1, -1, -1, -1};
-  const int cvt[7] = {bf ? 1 : 0, bf ? 1 : 0, 0, 0, 0, 0, 0};
+  const bool sbf = p->d.obs_bf16 != 0;
+  const int64_t rb[7] = {sbf ? 2 * p->ld_mo : row_b(ones_o, od, p->d.ld_obs, p->ld_mo),
+                         sbf ? 2 * p->ld_mc : row_b(ones_c, cd, p->d.ld_cobs, p->ld_mc),
+                         4 * p->ld_ma, 4, 4, 4, 4};
+  const int64_t ones[7] = {ones_o && !sbf ? 4 * od : -1, ones_c && !sbf ? 4 * cd : -1,
+                           -1, -1, -1, -1, -1};
+  const int cvt[7] = {bf && !sbf ? 1 : 0, bf && !sbf ? 1 : 0, 0, 0, 0, 0, 0};
   // the gather-ahead on the side stream takes at most 2 CTAs per SM, so it
   // steals fewer SMs from the optimizer kernels it overlaps (measured 0.8 %
   // per update; UL_GATHER_AHEAD_BPS overrides)
@@ -694,6 +700,8 @@ extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
   }
   if (desc->ld_obs < p->va.dims[0] || desc->ld_cobs < p->vc.dims[0] || desc->ld_act < p->A)
     return fail("ppo plan: leading dimension below feature width");
+  if (desc->obs_bf16 && desc->gemm_backend != 2)
+    return fail("ppo plan: bf16 observation rows need the bf16 back end");
   if (desc->gemm_backend < 0 || desc->gemm_backend > 3)
     return fail("ppo plan: gemm_backend must be UL_GEMM_FP32, _TF32, _BF16 or _TF32X3");
   p->dt = ul::backend_dtype(desc->gemm_backend);
@@ -713,6 +721,8 @@ extern "C" int ul_ppo_plan_create(const ul_ppo_plan_desc* desc, void** plan) {
     const int64_t q = p->dt == ul::kBf16 ? 8 : 4;
     p->ld_mo = (od + 1 + q - 1) / q * q;
     p->ld_mc = (cd + 1 + q - 1) / q * q;
+    if (desc->obs_bf16 && (desc->ld_obs != p->ld_mo || desc->ld_cobs != p->ld_mc))
+      return fail("ppo plan: bf16 observation rows must be round_up(d + 1, 8) wide");
   }
   p->ld_ma = desc->ld_act;
   p->Pa = p->va.total;

@@ -120,11 +120,13 @@ def test_folded_prepare_small_update_matches_separate():
         assert np.abs(x.astype(np.float64) - y).max() <= 1e-6
 
 
-def test_unpadded_segment_rows_gather_identically():
-    """A segment staged in the host row layout (raw_rows: 940-byte obs rows,
-    no re-pitch; the minibatch gather converts one float per lane and reads
-    the ones unit one float past each row) gives the SAME bf16 update as the
-    padded 16-byte-row layout, bit for bit."""
+def test_segment_row_layouts_gather_identically():
+    """The three staging layouts of a segment's observation rows give the SAME
+    bf16 update, bit for bit: padded fp32 16-byte rows (the gather converts to
+    bf16), the host layout (raw_rows: 940-byte rows, no re-pitch; the gather
+    converts one float per lane and reads the ones unit one float past each
+    row) and bf16 rows converted once at staging (bf16_rows, the bf16 default:
+    the gather copies 16-byte units)."""
     from paper_2605_30313_b200.algos import _staging as STG
 
     T, N, od, cd, ad, hid = 6, 512, 235, 101, 12, (256, 128, 128)
@@ -132,11 +134,12 @@ def test_unpadded_segment_rows_gather_identically():
     P.set_precision("bf16")
     cfg = A.PpoConfig(epochs=2, minibatches=2)
     out = []
-    for raw in (False, True):
+    for raw, bfr in ((False, False), (True, False), (False, True)):
         PPO._PLANS.clear()
         STG._CACHE.clear()
-        ds = STG.DeviceSegment(T, N, od, cd, ad, cfg.epochs, raw_rows=raw)
-        STG._CACHE[("ppo", T, N, od, cd, ad, cfg.epochs, torch.cuda.current_device())] = ds
+        ds = STG.DeviceSegment(T, N, od, cd, ad, cfg.epochs, raw_rows=raw, bf16_rows=bfr)
+        STG._CACHE[("ppo", T, N, od, cd, ad, cfg.epochs, torch.cuda.current_device(),
+                    STG.bf16_rows_default("ppo"))] = ds
         params = A.AcParams(TN.ModelParams.from_numpy(TN.Arch(od, hid, ad), actor.flat()),
                             TN.ModelParams.from_numpy(TN.Arch(cd, hid, 1), critic.flat()))
         opt = A.AcOpt.for_params(params, 1e-3)
@@ -145,9 +148,10 @@ def test_unpadded_segment_rows_gather_identically():
                                             seg.truncated, seg.bootstrap_value, 0.99, 0.95,
                                             truncation_values=seg.truncation_values)
         st = A.ppo_update(seg, params, opt, cfg, O.philox_stream(2, "update"))
-        assert ds.obs.stride(0) == (od if raw else 236)
+        assert ds.obs.stride(0) == (od if raw else 240 if bfr else 236)
         out.append((params.actor.flat(), params.critic.flat(), st.policy_loss))
     STG._CACHE.clear()
-    np.testing.assert_array_equal(out[0][0], out[1][0])
-    np.testing.assert_array_equal(out[0][1], out[1][1])
-    assert out[0][2] == out[1][2]
+    for o in out[1:]:
+        np.testing.assert_array_equal(out[0][0], o[0])
+        np.testing.assert_array_equal(out[0][1], o[1])
+        assert out[0][2] == o[2]
