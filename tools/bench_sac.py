@@ -103,20 +103,26 @@ def main():
     host_rng = np.random.default_rng(2)
     nrng = np.random.default_rng(3)
 
-    def e2e_step(i):
+    def e2e_step(i, noise):
         h = pin[i & 1]
         h[:] = host_rng.integers(0, RING, B)
         idx_buf.copy_(torch.from_numpy(h), non_blocking=True)
-        return A.sac_updates(A.DeviceRows(ring, width, idx_buf, B), st, cfg, nrng, utd)[-1]
+        return A.sac_updates(A.DeviceRows(ring, width, idx_buf, B), st, cfg, noise, utd)[-1]
 
-    for i in range(4):
-        e2e_step(i)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for i in range(K):
-        out = e2e_step(i)
-    torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / (K * utd)
+    def e2e(noise):
+        for i in range(4):
+            e2e_step(i, noise)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(K):
+            e2e_step(i, noise)
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3 / (K * utd)
+
+    # performance mode (device Philox noise) and parity mode (the reference's
+    # host standard_normal stream: B x A normals twice per update on the host)
+    e2e_ms = e2e(drng)
+    e2e_parity_ms = e2e(nrng)
     fl = ((PF - 1) * flops_per_update(False) + flops_per_update(True)) / PF
     res = {
         "workload": f"{a.cfg} {'FlashSAC' if a.cfg == 'cfg4' else 'FastSAC'} sac_update (ring 2^20 x "
@@ -127,6 +133,8 @@ def main():
         "graph": "one CUDA graph launch per tick (sac_updates)",
         "ms_per_update": ms, "updates_per_s": 1e3 / ms,
         "e2e_ms_per_update": e2e_ms, "e2e_updates_per_s": 1e3 / e2e_ms,
+        "e2e": "host batch indices each tick (pinned H2D), device noise, one graph per tick",
+        "e2e_parity_mode_ms_per_update": e2e_parity_ms,
         "tflops_achieved": fl / (ms * 1e-3) / 1e12,
         "critic_loss_last": out.extra["critic_loss"],
     }
