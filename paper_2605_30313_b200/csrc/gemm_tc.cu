@@ -191,7 +191,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
   using O = Op<TI>;
   using TO = OutT<TI, EPI>;
   using S = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
-  static_assert(!(BRES && PAIR), "B-resident launches are single-CTA");
   constexpr bool kOutBf16 = sizeof(TO) == 2;
   constexpr bool LN = EPI == kEpiLnFull;
   static_assert(!(LN && (PAIR || BRES)), "fused LayerNorm launches are single-CTA MMA clusters");
@@ -240,14 +239,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // B-resident: CTA i keeps (problem, N tile) combo c = i % bres_c (its B
   // tile loaded once) and walks that problem's M tiles i / bres_c, + G, ...
   int t_begin = cl, t_step = ncl, t_end = ngroups, bres_pr = 0, bres_n = 0;
+  // (CTA pairs: per cluster; each CTA of the pair keeps its half of the B tile)
   if (BRES) {
-    const int C = B.bres_c, c = (int)blockIdx.x % C;
+    const int C = B.bres_c, c = cl % C;
     int acc = 0;
     while (bres_pr < B.np - 1 && c >= acc + B.a[bres_pr].nt) acc += B.a[bres_pr++].nt;
     bres_n = c - acc;
-    t_begin = (int)blockIdx.x / C;
-    t_step = (int)gridDim.x / C;
-    t_end = B.a[bres_pr].mt;
+    t_begin = cl / C;
+    t_step = ncl / C;
+    t_end = (B.a[bres_pr].mt + CS - 1) / CS;
   }
 
   if (threadIdx.x == 0) {
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       T.pr = bres_pr;
       T.z = 0;
       T.n0 = bres_n * BN;
-      T.m0 = t * BM;
+      T.m0 = (t * CS + (int)crank) * BM;
       T.kt_n = P.K > 0 ? (P.K + BK - 1) / BK : 0;
       return T;
     }
@@ -337,18 +337,27 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (lane == 0) {
       int it = 0;
       if (BRES && t_begin < t_end) {
-        // this CTA's N tile of B, all K tiles, once
+        // this CTA's N tile of B (a pair: its half, completing on the
+        // leader's barrier), all K tiles, once
         const Tile T0 = tile_of(t_begin);
-        mbar_expect_tx(bres_bar, (uint32_t)T0.kt_n * S::kBBytes);
+        const int nb = T0.n0 + (int)crank * BNL;
+        const uint32_t bbar = su32(bres_bar) & 0xFEFFFFFFu;
+        if (leader) mbar_expect_tx(bres_bar, (uint32_t)(CS * T0.kt_n) * S::kBBytes);
         for (int kt = 0; kt < T0.kt_n; ++kt) {
           uint8_t* sb = sbres + kt * S::kBBytes;
           if (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / O::kChunk; ++c)
-              tma_load_2d(sb + c * kChunkBytes, &B.m[T0.pr].b, bres_bar, T0.n0 + O::kChunk * c,
-                          kt * BK);
+            for (int c = 0; c < BNL / O::kChunk; ++c) {
+              if (PAIR)
+                tma_load_2d_pair(sb + c * kChunkBytes, &B.m[T0.pr].b, bbar, nb + O::kChunk * c,
+                                 kt * BK);
+              else
+                tma_load_2d(sb + c * kChunkBytes, &B.m[T0.pr].b, bres_bar, nb + O::kChunk * c,
+                            kt * BK);
+            }
           } else {
-            tma_load_2d(sb, &B.m[T0.pr].b, bres_bar, kt * BK, T0.n0);
+            if (PAIR) tma_load_2d_pair(sb, &B.m[T0.pr].b, bbar, kt * BK, nb);
+            else tma_load_2d(sb, &B.m[T0.pr].b, bres_bar, kt * BK, nb);
           }
         }
       }
@@ -377,7 +386,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             } else {
               tma_load_2d_pair(sa, tA, fb, k0, m0);
             }
-            if (B_MN) {
+            if (BRES) {
+              // (B resident: the stage holds A only)
+            } else if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BNL / O::kChunk; ++c)
                 tma_load_2d_pair(sb + c * kChunkBytes, tB, fb, nb0 + O::kChunk * c, k0);
@@ -1063,7 +1074,8 @@ int launch(const Prob* q, int np, cudaStream_t s) {
     bres_kt = B.a[i].bres_kt > bres_kt ? B.a[i].bres_kt : bres_kt;
   }
   B.bres_kt_max = bres_kt;
-  UL_CHECK_ARG(!BRES || B.bres_c <= kNumSMs, "gemm_tc: B-resident launch with too many N tiles");
+  UL_CHECK_ARG(!BRES || B.bres_c * CS <= kNumSMs,
+               "gemm_tc: B-resident launch with too many N tiles");
   B.bres_nst = SM::kStages;
   size_t bytes = SM::kBytes;
   if (BRES) {  // as many A stages as the resident B leaves room for (UL_TC_BRES_STAGES caps)
@@ -1123,9 +1135,10 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   int cap = max_clusters;
   if (EPI == kEpiEluGrad && grid_dx > 0 && grid_dx / CS < cap) cap = grid_dx / CS;
   int grid = (total < cap ? total : cap) * CSX;
-  if (BRES) {  // every CTA keeps one (problem, N tile) combo
-    grid = (cap < total ? cap : total) / B.bres_c * B.bres_c;
-    if (grid < B.bres_c) grid = B.bres_c;
+  if (BRES) {  // every CTA (pair) keeps one (problem, N tile) combo
+    int ncl_b = (cap < total ? cap : total) / B.bres_c * B.bres_c;
+    if (ncl_b < B.bres_c) ncl_b = B.bres_c;
+    grid = ncl_b * CSX;
   }
   cfg.gridDim = dim3((unsigned)grid);
   for (int i = 0; i < np; ++i)
@@ -1240,6 +1253,31 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
     }
     return bres_base && bytes <= max_bytes && combos <= kNumSMs;
   };
+  // A 256-wide B tile too deep for one CTA's shared memory: a CTA PAIR keeps
+  // it resident, half in each SM (cta_group::2 MMAs read both halves), and
+  // streams only A (opt-in UL_TC_PAIR_BRES=1; UL_TC_PAIR_BRES_DX=1 extends it
+  // to the ELU-gradient dX GEMMs.  Measured on the cfg2 update: 4.33 / 4.48 ms
+  // against 4.30 without -- the pair's cross-SM MMA costs more than the
+  // halved B stream saves at K <= 512)
+  static int pair_bres = -1, pair_bres_dx = -1;
+  if (pair_bres < 0) {
+    const char* e = getenv("UL_TC_PAIR_BRES");
+    pair_bres = e ? atoi(e) != 0 : 0;
+    const char* f = getenv("UL_TC_PAIR_BRES_DX");
+    pair_bres_dx = f ? atoi(f) != 0 : 0;
+  }
+  auto bres_fits_pair = [&](int b, int64_t max_bytes) {
+    if (!pair_bres || sizeof(TI) != 2 || !all_two_m || amn || !one_split) return false;
+    if (!(np == 1 || bres_multi)) return false;
+    if (d.epi == kEpiEluGrad ? !pair_bres_dx : !(bres_env != 0)) return false;
+    int64_t bytes = 0, combos = 0;
+    for (int i = 0; i < np; ++i) {
+      const int64_t x = ceil_div(q[i].d->K, bk) * (int64_t)(b / 2) * 128;
+      bytes = x > bytes ? x : bytes;
+      combos += ceil_div(q[i].d->N, b);
+    }
+    return bytes <= max_bytes && 2 * combos <= kNumSMs;
+  };
   // UL_TC_BRES128=1: a 256-wide B tile too deep for shared memory becomes
   // B-resident 128-wide tiles (measured: cfg2 update 4.41 -> 4.60 ms, cfg4
   // 2.78 -> 2.84 ms, cfg3 0.724 -> 0.713 ms -- off by default)
@@ -1260,9 +1298,12 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
     return UL_ERR_VALUE;
   }
 #define UL_TC_BRES_MAX(EPI, BN) Smem<BN, false, (int)sizeof(OutT<TI, EPI>), EPI, true>::kBresMax
+#define UL_TC_BRES_MAX_P(EPI, BN) Smem<BN, true, (int)sizeof(OutT<TI, EPI>), EPI, true>::kBresMax
 #define UL_TC_BN(AMN, BMN, EPI, BN)                                                          \
   if (!AMN && bres_fits(BN, UL_TC_BRES_MAX(EPI, BN)))                                       \
     return launch<TI, AMN, BMN, EPI, BN, false, true>(q, np, s);                            \
+  if (!AMN && bres_fits_pair(BN, UL_TC_BRES_MAX_P(EPI, BN)))                                \
+    return launch<TI, AMN, BMN, EPI, BN, true, true>(q, np, s);                             \
   if (BN == 256 && !AMN && bres128 && bres_fits(128, UL_TC_BRES_MAX(EPI, 128)))             \
     return launch<TI, AMN, BMN, EPI, 128, false, true>(q, np, s);                           \
   if (pair) return launch<TI, AMN, BMN, EPI, BN, true>(q, np, s);                           \
@@ -1284,6 +1325,7 @@ int dispatch(const Prob* q, int np, cudaStream_t s) {
 #undef UL_TC_CASE
 #undef UL_TC_BN
 #undef UL_TC_BRES_MAX
+#undef UL_TC_BRES_MAX_P
   set_error("gemm_tc: unsupported layout/epilogue combination");
   return UL_ERR_VALUE;
 }
