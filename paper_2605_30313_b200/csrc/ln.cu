@@ -505,6 +505,143 @@ __global__ void __launch_bounds__(256) ln_fwd_cols(const TA* __restrict__ a, int
     for (int64_t r = r0; r < r1; ++r) st1<TO>(h + r * ldh + ones_col, 1.f);
 }
 
+// ---- one-pass backward (the default when the rows fit shared memory): a
+// persistent CTA walks blocks of kFbR rows; each block's dn and a rows land in
+// shared memory by cp.async (double-buffered: block i + 1 loads while block i
+// computes), warp w takes row w's means m1 = mean(dn g), m2 = mean(dn g x^)
+// from shared memory, then a column-parallel pass over the same staged rows
+// writes da over dn and accumulates dg = sum dn x^, dbeta = sum dn,
+// colsum(da) in registers across all of the CTA's blocks -> one [3][D]
+// partial per CTA (the ReduceJob layout).  dn and a cross HBM once.
+constexpr int kFbR = 8;   // rows per block (one warp each in the row pass)
+constexpr int kFbJ = 2;   // column quads per thread: D <= 256 * 4 * kFbJ
+
+__device__ __forceinline__ void ln_cpa16(void* sdst, const void* gsrc, bool valid) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+template <typename TA, typename TD>
+__global__ void __launch_bounds__(256) ln_bwd_fused(TD* __restrict__ dn, int64_t ldd,
+                                                    const TA* __restrict__ a, int64_t lda,
+                                                    const float* __restrict__ stats,
+                                                    const float* __restrict__ g, int64_t M, int D,
+                                                    float* __restrict__ part) {
+  extern __shared__ __align__(16) uint8_t lsm[];
+  __shared__ float2 s_m[kFbR], s_st[kFbR];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int ua = D * (int)sizeof(TA) / 16, ud = D * (int)sizeof(TD) / 16;  // 16-B units per row
+  TA* sa[2];
+  TD* sd[2];
+  {
+    const size_t blk = (size_t)kFbR * 16 * (ua + ud);
+    for (int k = 0; k < 2; ++k) {
+      sa[k] = reinterpret_cast<TA*>(lsm + k * blk);
+      sd[k] = reinterpret_cast<TD*>(lsm + k * blk + (size_t)kFbR * 16 * ua);
+    }
+  }
+  pdl_trigger();
+  pdl_wait();
+  const int64_t nblk = (M + kFbR - 1) / kFbR;
+  auto load = [&](int64_t rb, int k) {
+    const int64_t r0 = rb * kFbR;
+    for (int e = tid; e < kFbR * ua; e += blockDim.x) {
+      const int rr = e / ua, u = e - rr * ua;
+      const int64_t gr = r0 + rr;
+      const bool ok = gr < M;
+      ln_cpa16(reinterpret_cast<uint8_t*>(sa[k]) + (size_t)e * 16,
+               reinterpret_cast<const uint8_t*>(a + (ok ? gr : 0) * lda) + (size_t)u * 16, ok);
+    }
+    for (int e = tid; e < kFbR * ud; e += blockDim.x) {
+      const int rr = e / ud, u = e - rr * ud;
+      const int64_t gr = r0 + rr;
+      const bool ok = gr < M;
+      ln_cpa16(reinterpret_cast<uint8_t*>(sd[k]) + (size_t)e * 16,
+               reinterpret_cast<const uint8_t*>(dn + (ok ? gr : 0) * ldd) + (size_t)u * 16, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const float inv_d = 1.f / D;
+  float4 ag[kFbJ], ab[kFbJ], aa[kFbJ], gv[kFbJ];
+#pragma unroll
+  for (int j = 0; j < kFbJ; ++j) {
+    const int c0 = 4 * tid + 1024 * j;
+    ag[j] = ab[j] = aa[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gv[j] = c0 < D ? V4<float>::ld(g + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  int k = 0;
+  if ((int64_t)blockIdx.x < nblk) load(blockIdx.x, 0);
+  for (int64_t rb = blockIdx.x; rb < nblk; rb += gridDim.x, k ^= 1) {
+    if (rb + gridDim.x < nblk) {
+      load(rb + gridDim.x, k ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    // row means (warp w: row w of the block)
+    {
+      const int64_t gr = rb * kFbR + w;
+      if (gr < M) {
+        const float2 st = reinterpret_cast<const float2*>(stats)[gr];
+        const TA* ar = sa[k] + (size_t)w * D;
+        const TD* dr = sd[k] + (size_t)w * D;
+        float s1 = 0.f, s2 = 0.f;
+        for (int c = 4 * lane; c < D; c += 128) {
+          const float4 x = V4<TA>::ld(ar + c), d = V4<TD>::ld(dr + c), gg = V4<float>::ld(g + c);
+          const float e0 = d.x * gg.x, e1 = d.y * gg.y, e2 = d.z * gg.z, e3 = d.w * gg.w;
+          s1 += (e0 + e1) + (e2 + e3);
+          s2 += (e0 * (x.x - st.x) + e1 * (x.y - st.x)) + (e2 * (x.z - st.x) + e3 * (x.w - st.x));
+        }
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+          s_m[w] = make_float2(s1 * inv_d, s2 * st.y * inv_d);
+          s_st[w] = st;
+        }
+      }
+    }
+    __syncthreads();
+    // column pass over the staged rows: da over dn, column partials in registers
+#pragma unroll
+    for (int j = 0; j < kFbJ; ++j) {
+      const int c0 = 4 * tid + 1024 * j;
+      if (c0 >= D) continue;
+      for (int r = 0; r < kFbR; ++r) {
+        const int64_t gr = rb * kFbR + r;
+        if (gr >= M) break;
+        const float4 xv = V4<TA>::ld(sa[k] + (size_t)r * D + c0);
+        const float4 dv = V4<TD>::ld(sd[k] + (size_t)r * D + c0);
+        const float mu = s_st[r].x, rstd = s_st[r].y;
+        const float2 m = s_m[r];
+        const float4 gg = gv[j];
+        const float4 xh = make_float4((xv.x - mu) * rstd, (xv.y - mu) * rstd,
+                                      (xv.z - mu) * rstd, (xv.w - mu) * rstd);
+        const float4 da = make_float4(rstd * (dv.x * gg.x - m.x - xh.x * m.y),
+                                      rstd * (dv.y * gg.y - m.x - xh.y * m.y),
+                                      rstd * (dv.z * gg.z - m.x - xh.z * m.y),
+                                      rstd * (dv.w * gg.w - m.x - xh.w * m.y));
+        V4<TD>::st(dn + gr * ldd + c0, da);
+        ag[j].x += dv.x * xh.x; ag[j].y += dv.y * xh.y; ag[j].z += dv.z * xh.z; ag[j].w += dv.w * xh.w;
+        ab[j].x += dv.x; ab[j].y += dv.y; ab[j].z += dv.z; ab[j].w += dv.w;
+        aa[j].x += da.x; aa[j].y += da.y; aa[j].z += da.z; aa[j].w += da.w;
+      }
+    }
+    __syncthreads();  // buffer k is re-filled two blocks later
+  }
+  float* pz = part + (int64_t)blockIdx.x * 3 * D;
+#pragma unroll
+  for (int j = 0; j < kFbJ; ++j) {
+    const int c0 = 4 * tid + 1024 * j;
+    if (c0 >= D) continue;
+    V4<float>::st(pz + c0, ag[j]);
+    V4<float>::st(pz + D + c0, ab[j]);
+    V4<float>::st(pz + 2 * D + c0, aa[j]);
+  }
+}
+
 // row chunks of the column-parallel backward (<= its partial capacity)
 int ln_col_chunks(int64_t M) {
   const int64_t b = ceil_div(M, 16);
@@ -673,7 +810,41 @@ int ln_backward(void* dn, int64_t ldd, const void* a, int64_t lda, const float* 
   const bool bd = dtype == kBf16;
   const int64_t nbmax = ln_blocks(M) > ln_col_chunks(M) ? ln_blocks(M) : ln_col_chunks(M);
   float2* rs = reinterpret_cast<float2*>(part + nbmax * 3 * Dp);
-  if (D % 4 == 0 && lda % 4 == 0 && ldd % 4 == 0 && al(a, a_bf16 ? 8 : 16) &&
+  // one-pass kernel: 16-byte staged rows, D <= 2048, both row blocks in
+  // shared memory (UL_LN_BWD_FUSED=0 keeps the row + column kernel pair)
+  static int fused_env = -1;
+  if (fused_env < 0) {
+    const char* e = getenv("UL_LN_BWD_FUSED");
+    fused_env = e ? atoi(e) != 0 : 1;
+  }
+  const int eA = a_bf16 ? 2 : 4, eD = bd ? 2 : 4;
+  const size_t fsm = (size_t)2 * kFbR * D * (eA + eD);
+  if (fused_env && D % 4 == 0 && D <= 1024 * kFbJ && (D * eA) % 16 == 0 && (D * eD) % 16 == 0 &&
+      (lda * eA) % 16 == 0 && (ldd * eD) % 16 == 0 && al(a, 16) && al(dn, 16) && al(g, 16) &&
+      al(stats, 8) && al(part, 16) && fsm <= 200 * 1024) {
+    const int64_t nblk = ceil_div(M, (int64_t)kFbR);
+    const int per_sm = fsm <= 72 * 1024 ? 3 : (fsm <= 110 * 1024 ? 2 : 1);
+    int64_t grid = (int64_t)per_sm * kNumSMs;
+    grid = grid < nblk ? grid : nblk;
+    grid = grid < nbmax ? grid : nbmax;  // (the partial buffer's chunk capacity)
+    nb = (int)grid;
+    static bool fattr[4] = {false, false, false, false};
+#define UL_LNF1(TA_, TD_, I_)                                                                     \
+  do {                                                                                            \
+    if (!fattr[I_]) {                                                                             \
+      UL_CUDA(cudaFuncSetAttribute(ln_bwd_fused<TA_, TD_>,                                        \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));     \
+      fattr[I_] = true;                                                                           \
+    }                                                                                             \
+    UL_TRY(launch_pdl("ln_bwd_fused", ln_bwd_fused<TA_, TD_>, dim3((unsigned)nb), dim3(256), fsm, \
+                      s, (TD_*)dn, ldd, (const TA_*)a, lda, stats, g, M, D, part));               \
+  } while (0)
+    if (a_bf16 && bd) UL_LNF1(BF, BF, 0);
+    else if (a_bf16) UL_LNF1(BF, float, 1);
+    else if (bd) UL_LNF1(float, BF, 2);
+    else UL_LNF1(float, float, 3);
+#undef UL_LNF1
+  } else if (D % 4 == 0 && lda % 4 == 0 && ldd % 4 == 0 && al(a, a_bf16 ? 8 : 16) &&
       al(g, 16) && al(stats, 8) && al(dn, db) && al(part, 16) && ln_two_pass()) {
     int64_t b1 = ceil_div(M, 8);
     b1 = b1 > 8 * kNumSMs ? 8 * kNumSMs : b1;
