@@ -217,6 +217,11 @@ int ul_gather_rows(int ndesc, const void* const* src, void* const* dst,
 /* ul_gather_rows + a per-desc conversion flag: cvt[d] = 1 turns fp32 source
  * rows into bf16 destination rows (row_bytes / ones_byte count SOURCE bytes;
  * the bf16 staging of a PPO segment's observation rows). */
+/* fp32 rows [rows, lds] (4-byte aligned, e.g. unpadded H2D landing rows) ->
+ * bf16 rows [rows, ldd] (ldd % 8 == 0): columns >= width zero, column
+ * ones_col (>= 0) set to 1.0 -- the once-per-segment bf16 observation staging. */
+int ul_rows_to_bf16(const float* src, int64_t lds, int width, void* dst, int64_t ldd,
+                    int64_t rows, int ones_col, void* stream);
 int ul_gather_rows_cvt(int ndesc, const void* const* src, void* const* dst,
                        const int64_t* src_stride, const int64_t* dst_stride,
                        const int64_t* row_bytes, const int64_t* ones_byte, const int* cvt,

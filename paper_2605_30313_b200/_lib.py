@@ -160,6 +160,7 @@ _PROTOS = {
     "ul_gather_rows": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                  C.POINTER(i64), C.POINTER(i64), vp, vp, i64, i64, i64, i64, vp,
                                  vp]),
+    "ul_rows_to_bf16": (C.c_int, [vp, i64, C.c_int, vp, i64, i64, C.c_int, vp]),
     "ul_gather_rows_cvt": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64),
                                      C.POINTER(i64), C.POINTER(i64), vp, vp, vp, i64, vp]),
     "ul_narrow_f64": (C.c_int, [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(i64), vp]),

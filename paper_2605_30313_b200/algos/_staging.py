@@ -15,8 +15,6 @@ stays valid across updates: each update overwrites the same HBM.
 
 from __future__ import annotations
 
-import ctypes as C
-
 import numpy as np
 import torch
 
@@ -105,23 +103,22 @@ class DeviceSegment:
         (bf16 destinations: converted on the way, ones column set)."""
         if not jobs:
             return
-        n = len(jobs)
         nrows = jobs[0][1].shape[0]
-        src = _lib.ptr_array([_dev.ptr(r) for r, _, _ in jobs])
-        dst = _lib.ptr_array([_dev.ptr(d) for _, d, _ in jobs])
-        sst = _lib.i64_array([w * 4 for _, _, w in jobs])
-        dst_stride = _lib.i64_array([d.stride(0) * d.element_size() for _, d, _ in jobs])
-        if not any(d.dtype == torch.bfloat16 for _, d, _ in jobs):
-            _lib.call("ul_gather_rows", n, src, dst, sst, dst_stride, sst, None, None, nrows,
-                      0, 0, nrows, None, _dev.stream())
+        # bf16 rows: one conversion pass per field (8 output columns per
+        # thread, ones column set)
+        for r, d, w in jobs:
+            if d.dtype == torch.bfloat16:
+                _lib.call("ul_rows_to_bf16", _dev.ptr(r), w, w, _dev.ptr(d), d.stride(0), nrows,
+                          w, _dev.stream())
+        jobs = [(r, d, w) for r, d, w in jobs if d.dtype != torch.bfloat16]
+        if not jobs:
             return
-        # bf16 rows: read the width + one float (replaced by the ones column;
-        # the landing buffers carry a 16-byte tail)
-        cvt = [1 if d.dtype == torch.bfloat16 else 0 for _, d, _ in jobs]
-        rb = _lib.i64_array([(w + c) * 4 for (_, _, w), c in zip(jobs, cvt)])
-        ones = _lib.i64_array([w * 4 if c else -1 for (_, _, w), c in zip(jobs, cvt)])
-        _lib.call("ul_gather_rows_cvt", n, src, dst, sst, dst_stride, rb, ones,
-                  (C.c_int * n)(*cvt), None, nrows, _dev.stream())
+        _lib.call("ul_gather_rows", len(jobs), _lib.ptr_array([_dev.ptr(r) for r, _, _ in jobs]),
+                  _lib.ptr_array([_dev.ptr(d) for _, d, _ in jobs]),
+                  _lib.i64_array([w * 4 for _, _, w in jobs]),
+                  _lib.i64_array([d.stride(0) * 4 for _, d, _ in jobs]),
+                  _lib.i64_array([w * 4 for _, _, w in jobs]), None, None, nrows,
+                  0, 0, nrows, None, _dev.stream())
 
     def _put_rows(self, name: str, dst: torch.Tensor, src, width: int, jobs: list) -> None:
         """Host [rows, width] -> HBM [rows, ld]: one contiguous H2D at full PCIe
@@ -249,10 +246,8 @@ class DeviceSegment:
         _dev.h2d(part, a)
         rb = width * 4
         if dst.dtype == torch.bfloat16:  # converted, ones column set
-            _lib.call("ul_gather_rows_cvt", 1, _lib.ptr_array([_dev.ptr(part)]),
-                      _lib.ptr_array([_dev.ptr(dst[t * N:(t + 1) * N])]), _lib.i64_array([rb]),
-                      _lib.i64_array([dst.stride(0) * 2]), _lib.i64_array([rb + 4]),
-                      _lib.i64_array([rb]), (C.c_int * 1)(1), None, N, _dev.stream())
+            _lib.call("ul_rows_to_bf16", _dev.ptr(part), width, width,
+                      _dev.ptr(dst[t * N:(t + 1) * N]), dst.stride(0), N, width, _dev.stream())
             return
         _lib.call("ul_gather_rows", 1, _lib.ptr_array([_dev.ptr(part)]),
                   _lib.ptr_array([_dev.ptr(dst[t * N:(t + 1) * N])]), _lib.i64_array([rb]),

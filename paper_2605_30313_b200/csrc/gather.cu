@@ -364,6 +364,60 @@ extern "C" int ul_gather_rows(int ndesc, const void* const* src, void* const* ds
                          idx, n, modulo, lo, hi, err, ul::as_stream(stream));
 }
 
+namespace ul {
+namespace {
+// fp32 rows [rows, lds] (any 4-byte alignment, e.g. the 940-byte H2D landing
+// rows) -> bf16 rows [rows, ldd]: thread = 8 output columns (one 16-byte
+// store), 8 coalesced 4-byte loads; columns >= width are 0 except `ones`
+// (1.0).  One pass over a whole segment field per H2D.
+__global__ void __launch_bounds__(256) rows_to_bf16_kernel(const float* __restrict__ src,
+                                                           int64_t lds, int width,
+                                                           __nv_bfloat16* __restrict__ dst,
+                                                           int64_t ldd, int64_t rows, int ones) {
+  pdl_trigger();
+  pdl_wait();
+  const int q8 = (int)(ldd / 8);
+  const int64_t total = rows * q8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / q8;
+    const int c0 = (int)(i - r * q8) * 8;
+    const float* sr = src + r * lds;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = c0 + e;
+      v[e] = c < width ? __ldg(sr + c) : (c == ones ? 1.f : 0.f);
+    }
+    uint4 o;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]), p1 = __floats2bfloat162_rn(v[2], v[3]);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]), p3 = __floats2bfloat162_rn(v[6], v[7]);
+    o.x = *reinterpret_cast<uint32_t*>(&p0);
+    o.y = *reinterpret_cast<uint32_t*>(&p1);
+    o.z = *reinterpret_cast<uint32_t*>(&p2);
+    o.w = *reinterpret_cast<uint32_t*>(&p3);
+    *reinterpret_cast<uint4*>(dst + r * ldd + c0) = o;
+  }
+}
+}  // namespace
+}  // namespace ul
+
+// fp32 rows -> bf16 rows of ldd elements (ldd % 8 == 0, dst 16-byte aligned),
+// columns past `width` zero except `ones_col` (1.0; -1 none)
+extern "C" int ul_rows_to_bf16(const float* src, int64_t lds, int width, void* dst, int64_t ldd,
+                               int64_t rows, int ones_col, void* stream) {
+  UL_CHECK_ARG(rows >= 0 && width >= 0 && lds >= width && ldd >= width && ldd % 8 == 0 &&
+                   ((uintptr_t)dst & 15) == 0 && ((uintptr_t)src & 3) == 0,
+               "rows_to_bf16: bad shape / alignment");
+  if (rows == 0) return UL_OK;
+  const int64_t total = rows * (ldd / 8);
+  int64_t blocks = ul::ceil_div(total, (int64_t)256);
+  blocks = blocks > 16 * ul::kNumSMs ? 16 * ul::kNumSMs : blocks;
+  return ul::launch_pdl("rows_to_bf16_kernel", ul::rows_to_bf16_kernel, dim3((unsigned)blocks),
+                        dim3(256), 0, ul::as_stream(stream), src, lds, width,
+                        reinterpret_cast<__nv_bfloat16*>(dst), ldd, rows, ones_col);
+}
+
 // ul_gather_rows with per-desc fp32 -> bf16 conversion (no index window)
 extern "C" int ul_gather_rows_cvt(int ndesc, const void* const* src, void* const* dst,
                                   const int64_t* src_stride, const int64_t* dst_stride,
