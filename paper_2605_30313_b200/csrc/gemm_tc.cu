@@ -177,7 +177,12 @@ struct TcBatch {
   int bres_c;         // B-resident: (problem, N tile) combos; CTA i keeps combo i % bres_c
   int bres_nst;       // B-resident: A ring depth of this launch
   int bres_kt_max;    // B-resident: K tiles of the deepest problem (the smem layout)
+  // chained layers (bias+ELU forward of stacked layers, one launch): problem
+  // net * chain_L + l is layer l of net `net`; a CTA runs whole row chains
+  // (every layer of one M tile), two chains interleaved layer by layer
+  int chain_L, chain_nets, chain_mt, chain_S;  // chain_S: tiles per chain
 };
+constexpr int kMaxChainL = 4;
 
 // BRES (B resident; single problem, no pair, no split-K, K <= a few tiles):
 // each CTA owns one N tile (CTA index mod nt) and walks M tiles; B's K tiles
@@ -220,7 +225,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* aux_bar = acc_empty + 2;     // [kEpiWarps]
   uint64_t* bres_bar = aux_bar + kEpiWarps;
   uint64_t* ln_bar = bres_bar + 2;  // [2] fused LayerNorm: the cluster's row partials landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ln_bar + 2);  // keeps sbias 16 B aligned
+  uint64_t* ready = ln_bar + 2;     // [2 slots][kMaxChainL] chained layers: layer l - 1 stored
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ready + 2 * kMaxChainL);  // (16 B aligned)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long w_prod = 0, w_full = 0, w_acc = 0, w_epi = 0, w_issue = 0;  // (UL_TC_TRACE)
@@ -249,6 +255,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
     t_step = ncl / C;
     t_end = (B.a[bres_pr].mt + CS - 1) / CS;
   }
+  // chained layers: this CTA's chains are cl, cl + ncl, ... (Q of them); its
+  // tile sequence t = 0.. walks them in pairs, layer by layer: the pair's
+  // layer-l tiles of chain A, then of chain B, then layer l + 1 ...
+  constexpr bool kChainable = EPI == kEpiBiasElu && !PAIR && !BRES && !LN;
+  const bool CH = kChainable && B.chain_L > 0;
+  int chainQ = 0;
+  if (CH) {
+    const int nch = B.chain_nets * B.chain_mt;
+    chainQ = cl < nch ? (nch - 1 - cl) / ncl + 1 : 0;
+    t_begin = 0;
+    t_step = 1;
+    t_end = (chainQ / 2) * 2 * B.chain_S + (chainQ % 2) * B.chain_S;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -265,6 +284,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_init(&ln_bar[0], 1);
       mbar_init(&ln_bar[1], 1);
     }
+    if (CH)  // layer l of a chain waits for every epilogue warp of layer l - 1's tiles
+      for (int sl = 0; sl < 2; ++sl)
+        for (int l = 1; l < B.chain_L; ++l)
+          mbar_init(&ready[sl * kMaxChainL + l], kEpiWarps * B.a[l - 1].nt);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -299,9 +322,40 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // group*CS + rank
   struct Tile {
     int pr, m0, n0, z, kt_n;
+    int slot, layer, pair;  // chained layers only
   };
   auto tile_of = [&](int t) {
     Tile T;
+    T.slot = T.layer = T.pair = 0;
+    if (CH) {
+      const int S = B.chain_S;
+      const int pp = t / (2 * S);
+      int r = t - pp * 2 * S;
+      const bool single = 2 * pp + 1 >= chainQ;  // a last pair with one chain
+      int l = 0, slot = 0, n = 0;
+      for (; l < B.chain_L; ++l) {
+        const int ntl = B.a[l].nt;
+        const int w = single ? ntl : 2 * ntl;
+        if (r < w) {
+          slot = r / ntl;
+          n = r - slot * ntl;
+          break;
+        }
+        r -= w;
+      }
+      const int c = cl + (2 * pp + slot) * ncl;
+      const int net = c / B.chain_mt, m = c - net * B.chain_mt;
+      T.pr = net * B.chain_L + l;
+      T.z = 0;
+      T.n0 = n * BN;
+      T.m0 = m * BM;
+      const int K = B.a[T.pr].K;
+      T.kt_n = K > 0 ? (K + BK - 1) / BK : 0;
+      T.slot = slot;
+      T.layer = l;
+      T.pair = pp;
+      return T;
+    }
     if (BRES) {  // t = M tile of this CTA's (problem, N tile) combo
       const TcArgs& P = B.a[bres_pr];
       T.pr = bres_pr;
@@ -368,6 +422,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const CUtensorMap* tA = &B.m[T.pr].a;
         const CUtensorMap* tB = &B.m[T.pr].b;
         const int nb0 = n0 + (int)crank * BNL;  // first B row (N) of this CTA's share
+        // chained layers: this tile's A rows are the previous layer's output
+        // rows of the same chain, stored by this CTA's epilogue
+        if (CH && T.layer > 0) mbar_wait(&ready[T.slot * kMaxChainL + T.layer], T.pair & 1);
         for (int kt = 0; kt < kt_n; ++kt, ++it) {
           const int s = it % kStages;
           mbar_wait_acc(&empty[s], ((it / kStages) & 1) ^ 1, p0_.trace ? &w_prod : nullptr);
@@ -429,7 +486,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
       int it = 0, local = 0;
       if (BRES && t_begin < t_end) mbar_wait(bres_bar, 0);
       for (int t = t_begin; t < t_end; t += t_step, ++local) {
-        const int kt_n = tile_of(t).kt_n;
+        const Tile TT = tile_of(t);
+        const int kt_n = TT.kt_n;
+        // (chained layers: a layer narrower than BN issues N = its width)
+        uint32_t idesc_t = idesc;
+        if (CH) {
+          const int w = min(BN, (B.a[TT.pr].N - TT.n0 + 15) / 16 * 16);
+          idesc_t = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(w >> 3) << 17);
+        }
         const int b = local & 1;
         mbar_wait_acc(&acc_empty[b], ((local >> 1) & 1) ^ 1,  // epilogues drained this buffer
                       p0_.trace ? &w_acc : nullptr);
@@ -457,8 +521,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                                  O::kMnSbo, O::kMnLayout)
                                      : smem_desc(b_base + kk * 32, 16, 1024, 2);
             const uint32_t accum = (kt > 0 || kk > 0) ? 1u : 0u;
-            if (PAIR) mma_pair<TI>(acc, da, db, idesc, accum);
-            else mma<TI>(acc, da, db, idesc, accum);
+            if (PAIR) mma_pair<TI>(acc, da, db, idesc_t, accum);
+            else mma<TI>(acc, da, db, idesc_t, accum);
           }
           // frees the stage (in both CTAs of a pair) once these MMAs read it
           if (PAIR) mma_commit_pair(&empty[s]);
@@ -748,8 +812,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
         }
       } else {
+      // (chained layers: a tile narrower than BN -- the 128-wide last hidden
+      // layer -- leaves the slices past its width untouched)
+      const int c_end = CH && n0 + (slice + 1) * kSlice > p.N
+                            ? max(slice * kSlice, (p.N - n0 + kBoxC - 1) / kBoxC * kBoxC)
+                            : (slice + 1) * kSlice;
 #pragma unroll 1
-      for (int c0 = slice * kSlice; c0 < (slice + 1) * kSlice; c0 += kBoxC, ++cj) {
+      for (int c0 = slice * kSlice; c0 < c_end; c0 += kBoxC, ++cj) {
         uint8_t* stg = staging + (ew * S::kNStg + cj % S::kNStg) * kBoxBytes;
         // this staging box free again (the TMA store issued from it two boxes
         // ago has read it)
@@ -922,6 +991,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
                        : "memory");
         }
       }
+      // chained layers: once this warp's stores of the tile have landed in
+      // global memory (and its ones-column writes are ordered before the async
+      // proxy), the next layer of the chain may TMA-load these rows
+      if (CH && T.layer + 1 < B.chain_L) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                           su32(&ready[T.slot * kMaxChainL + T.layer + 1]))
+                       : "memory");
+      }
     }
     // the staging smem must outlive the stores' reads; their global writes
     // complete with the grid (kernel boundary / the dependent launch's
@@ -1040,8 +1121,13 @@ int make_problem(const Prob& q, TcMaps* m, TcArgs* a, int* ngroups) {
   return UL_OK;
 }
 
+// chained layers (chain_L > 0): q[net * chain_L + l] is layer l of net `net`
+struct ChainSpec {
+  int nets, L;
+};
+
 template <typename TI, bool A_MN, bool B_MN, int EPI, int BN, bool PAIR, bool BRES = false>
-int launch(const Prob* q, int np, cudaStream_t s) {
+int launch(const Prob* q, int np, cudaStream_t s, const ChainSpec* chain = nullptr) {
   using TO = OutT<TI, EPI>;
   using SM = Smem<BN, PAIR, (int)sizeof(TO), EPI, BRES>;
   constexpr int CS = PAIR ? 2 : 1;
@@ -1135,6 +1221,21 @@ int launch(const Prob* q, int np, cudaStream_t s) {
   int cap = max_clusters;
   if (EPI == kEpiEluGrad && grid_dx > 0 && grid_dx / CS < cap) cap = grid_dx / CS;
   int grid = (total < cap ? total : cap) * CSX;
+  if (chain) {  // whole row chains: one CTA per chain up to the co-resident CTAs
+    UL_CHECK_ARG(EPI == kEpiBiasElu && !PAIR && !BRES && chain->L >= 1 && chain->L <= kMaxChainL &&
+                     chain->nets >= 1 && chain->nets * chain->L == np,
+                 "gemm_tc: bad chained-layer launch");
+    B.chain_L = chain->L;
+    B.chain_nets = chain->nets;
+    B.chain_mt = B.a[0].mt;
+    B.chain_S = 0;
+    for (int l = 0; l < chain->L; ++l) B.chain_S += B.a[l].nt;
+    for (int i = 0; i < np; ++i)
+      UL_CHECK_ARG(B.a[i].mt == B.chain_mt && B.a[i].nt == B.a[i % chain->L].nt && B.a[i].zt == 1,
+                   "gemm_tc: chained layers need equal M / widths per layer across nets");
+    const int nch = chain->nets * B.chain_mt;
+    grid = nch < cap ? nch : cap;
+  }
   if (BRES) {  // every CTA (pair) keeps one (problem, N tile) combo
     int ncl_b = (cap < total ? cap : total) / B.bres_c * B.bres_c;
     if (ncl_b < B.bres_c) ncl_b = B.bres_c;
@@ -1566,6 +1667,25 @@ int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s) {
 // Two independent GEMMs (e.g. the actor's and the critic's layer) in one
 // persistent launch when they share dtype, layouts, epilogue, tile width and
 // CTA pairing; otherwise two launches.  Each desc's ones_col applies.
+// Stacked bias+ELU layers of up to 2 networks as ONE launch (chained layers):
+// d[net * L + l] = layer l of net `net` (bf16, K-major operands, 256-wide N
+// tiles, layer l's A = layer l - 1's C).  A CTA runs whole row chains -- every
+// layer of one 128-row M tile, the next layer's tiles waiting only for this
+// CTA's own stores of the layer below -- so the per-launch fill / drain and
+// the grid-wide dependency wait between layers disappear.
+int gemm_tc_chain(const GemmDesc* d, int nets, int L, cudaStream_t s) {
+  UL_CHECK_ARG(nets >= 1 && nets <= 2 && L >= 1 && L <= tc::kMaxChainL, "chain: shape");
+  tc::Prob q[tc::kMaxProb];
+  for (int i = 0; i < nets * L; ++i) {
+    UL_CHECK_ARG(d[i].dtype == kBf16 && d[i].a_kmajor && d[i].b_kmajor && d[i].epi == kEpiBiasElu &&
+                     (d[i].splits <= 1) && !d[i].x3,
+                 "chain: layers must be bf16 bias+ELU GEMMs with K-major operands");
+    q[i] = prob_of(d[i], -1);
+  }
+  const tc::ChainSpec cs{nets, L};
+  return tc::launch<__nv_bfloat16, false, false, kEpiBiasElu, 256, false>(q, nets * L, s, &cs);
+}
+
 int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
   const bool e0 = d0.M == 0 || d0.N == 0, e1 = d1.M == 0 || d1.N == 0;
   if (e0 || e1 || d0.x3 || d1.x3) {  // (3xTF32: one split scratch, one GEMM at a time)

@@ -183,6 +183,8 @@ int run_deferred_dw_reduce(DeferredDw& D, cudaStream_t s);
 bool deferred_dw_enabled();  // UL_DEFER_DW (default on)
 // independent tensor-core GEMMs, batched into as few launches as compatible
 int gemm_tc_batch(const GemmDesc* d, int n, cudaStream_t s);
+// stacked bias+ELU layers of up to 2 networks in one launch (gemm_tc.cu)
+int gemm_tc_chain(const GemmDesc* d, int nets, int L, cudaStream_t s);
 
 // ------------------------------------------------------------------ MLP
 struct NetView {

@@ -805,6 +805,37 @@ bool head_needs_colsum(const MlpNet& N) {
   return !ones_free_of(in_below, below_ones);
 }
 
+// Chained hidden layers (gemm_tc_chain; opt-in UL_CHAIN_FWD=1): bf16, no
+// LayerNorm, 1-2 networks of equal hidden widths, shallow K.  Bit-identical
+// to one launch per layer; measured 4.40 vs 4.31 ms per cfg2 update (the
+// three launches serialised under ncu: 66.0 vs 65.9 us) -- the in-kernel
+// handoff between a chain's layers (stores landed -> next layer's loads)
+// costs what the launch boundaries did, and the chain gives up the
+// B-resident first / last layers
+constexpr int kMaxChainLayers = 4;
+static bool chain_fwd_ok(const MlpNet* nets, int n, int dt, int64_t M) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_CHAIN_FWD");
+    on = e ? atoi(e) != 0 : 0;
+  }
+  if (!on || dt != kBf16 || n < 1 || n > 2 || M <= 0 || M >= (int64_t(1) << 31)) return false;
+  const NetView& v0 = *nets[0].v;
+  const int L = v0.n_layers - 1;
+  if (L < 2 || L > kMaxChainLayers) return false;
+  for (int k = 0; k < n; ++k) {
+    const NetView& v = *nets[k].v;
+    if (v.ln || !nets[k].wp || v.n_layers != v0.n_layers) return false;
+    if (((uintptr_t)nets[k].x & 15) || (nets[k].ldx * 2) % 16) return false;
+    for (int i = 1; i <= L; ++i)
+      if (v.dims[i] != v0.dims[i]) return false;  // (equal widths per layer)
+    // (deep-K layers -- the FlashSAC 1024-wide critics -- run better as CTA-pair launches)
+    for (int i = 0; i < L; ++i)
+      if (v.dims[i] > 512) return false;
+  }
+  return true;
+}
+
 int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
   if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
@@ -832,6 +863,32 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       ldh[k] = act_ld(nets[k].v->dims[nl - 1], dt);
     }
     i0 = nl - 1;
+  } else if (tc && chain_fwd_ok(nets, n, dt, M)) {
+    // every hidden layer of both networks as one chained tcgen05 launch (row
+    // chains per CTA, gemm_tc_chain); the output layers follow as usual
+    const int L = nl - 1;
+    GemmDesc g[2 * kMaxChainLayers] = {};
+    for (int k = 0; k < n; ++k) {
+      const MlpNet& N = nets[k];
+      const NetView& v = *N.v;
+      for (int i = 0; i < L; ++i) {
+        GemmDesc& G = g[k * L + i];
+        G.M = M; G.N = v.dims[i + 1]; G.K = v.dims[i];
+        G.A = i == 0 ? N.x : act_ptr(v, N.acts, M, i - 1, dt);
+        G.lda = i == 0 ? N.ldx : act_ld(v.dims[i], dt);
+        G.B = staged_w(v, N.wp, i, dt, &G.ldb);
+        G.bias = N.params + v.b_off[i];
+        G.C = const_cast<float*>(act_ptr(v, N.acts, M, i, dt));
+        G.ldc = act_ld(v.dims[i + 1], dt);
+        G.a_kmajor = true; G.b_kmajor = true;
+        G.epi = kEpiBiasElu; G.splits = 1; G.dtype = dt;
+        G.ones_col = (int)v.dims[i + 1];
+      }
+      h[k] = act_ptr(v, N.acts, M, L - 1, dt);
+      ldh[k] = act_ld(v.dims[L], dt);
+    }
+    UL_TRY(gemm_tc_chain(g, n, L, s));
+    i0 = L;
   }
   for (int i = i0; i < nl; ++i) {
     const bool last = i == nl - 1;

@@ -69,3 +69,22 @@ def test_fused_forward_bf16_ppo_update_bit_exact(case, tmp_path):
     b = _run(case, False, str(tmp_path))
     for k in ("actor", "critic", "stats"):
         assert np.array_equal(a[k], b[k]), (k, float(np.max(np.abs(a[k] - b[k]))))
+
+
+def _run_env(case, env_extra, tmp, tag):
+    out = os.path.join(tmp, f"{tag}.npz")
+    env = dict(os.environ, PYTHONPATH=ROOT, **env_extra)
+    subprocess.run([sys.executable, "-c", _CHILD, json.dumps([case, out])], env=env,
+                   cwd=ROOT, check=True, timeout=300)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("case", CASES[:4])
+def test_chained_forward_bf16_ppo_update_bit_exact(case, tmp_path):
+    """Opt-in chained hidden layers (UL_CHAIN_FWD=1, csrc/gemm_tc.cu chain
+    mode: one launch, whole row chains per CTA, each layer's tiles waiting for
+    the CTA's own stores of the layer below) against one launch per layer."""
+    a = _run_env(case, {"UL_CHAIN_FWD": "1", "UL_FUSED_FWD": "0"}, str(tmp_path), "c")
+    b = _run_env(case, {"UL_CHAIN_FWD": "0", "UL_FUSED_FWD": "0"}, str(tmp_path), "l")
+    for k in ("actor", "critic", "stats"):
+        assert np.array_equal(a[k], b[k]), (k, float(np.max(np.abs(a[k] - b[k]))))
