@@ -261,7 +261,7 @@ __device__ void apply_seg(const SegTable& st, const ApplyCtl& c, const AdamScala
   }
 }
 
-__global__ void apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
+__global__ void __launch_bounds__(256, 4) apply_kernel(SegTable st, const ul_opt_ctl* __restrict__ ctl, int write_grads,
                              int do_adam, StageOut so, int has_so) {
   __shared__ ApplyCtl c;
   __shared__ AdamScalars k;  // (bias corrections: two f64 pow per CTA, not per thread)
