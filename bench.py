@@ -493,9 +493,25 @@ def run_ours(args):
     flops = counts["gemm_flops_per_update"]
     tensor_floor_ms = flops / (bf16_sus * 1e12) * 1e3
     hbm_floor_ms = traffic / (hbm * 1e9) * 1e3 if traffic else 0.0
+    # per-phase tensor view: the hidden-layer GEMM FLOPs of each phase of the
+    # tcgen05 schedule over its measured time (the output layers run in the
+    # fused output stage, "heads")
+    rows_upd = cfg.epochs * (T * N // world if strong else T * N)
+    fwd_mac = dx_mac = 0
+    for dims in ((od, *hid), (cd, *hid)):
+        for i in range(len(dims) - 1):
+            fwd_mac += dims[i] * dims[i + 1]
+            if i > 0:
+                dx_mac += dims[i] * dims[i + 1]
+    phase_fl = {"mlp_forward": 2.0 * fwd_mac * rows_upd, "bwd_dx": 2.0 * dx_mac * rows_upd,
+                "bwd_dw": 2.0 * fwd_mac * rows_upd}
+    phase_tflops = {k: (phase_fl[k] / (prof[k] / 1e3) / 1e12 if prof.get(k) else None)
+                    for k in phase_fl}
     tensor_view = {"achieved": gemm_tflops, "peak": bf16_sus, "unit": "TFLOP/s",
                    "frac": gemm_tflops / bf16_sus, "floor_ms": tensor_floor_ms,
-                   "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)"}
+                   "peak_source": f"{src} bf16 sustained (MEASURED_PEAKS.json)",
+                   "phase_tflops": phase_tflops,
+                   "phase_frac": {k: (v / bf16_sus if v else None) for k, v in phase_tflops.items()}}
     kernel_desc = ("MLP passes of one update: tcgen05 GEMMs (tc_gemm_kernel: grouped forward, "
                    "ELU-gradient dX, one batched dW launch per step) + split-K reductions + the "
                    "fused output stage (ppo_fused_mma_kernel); traffic = ncu DRAM bytes of the "
