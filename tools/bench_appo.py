@@ -74,11 +74,21 @@ def main():
     e1.record(s)
     e1.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
+    # the recompute forward (target log-prob + V(s) of the whole segment) and
+    # V-trace alone, for the phase split
+    e0.record(s)
+    for _ in range(a.steps):
+        AP.recompute_targets(ds, params)
+        AP.vtrace_into(ds, cfg)
+    e1.record(s)
+    e1.synchronize()
+    rec_ms = e0.elapsed_time(e1) / a.steps
     rows = T * N
     res = {"workload": "cfg5 APPO appo_update (V-trace), 24 x 16384 envs, obs 98 / cobs 101 / "
                        "act 29, actor+critic 512-256-128, 5 epochs x 4 minibatches, segment "
                        "resident in HBM, device minibatch permutations",
            "precision": a.precision, "steps": a.steps, "ms_per_update": ms,
+           "recompute_vtrace_ms": rec_ms,
            "transitions_per_s": rows / (ms * 1e-3), "policy_loss_last": st.policy_loss}
     # CPU: the oracle appo_update on cpu_envs envs, 1 epoch, extrapolated
     n = a.cpu_envs
