@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-3 session evidence: full GPU suite, bench line, ncu launch list of the
+# Round-2 second-session (r02b) evidence: full GPU suite, bench line, ncu launch list of the
 # bench command, DRAM traffic per kernel class of one cfg2 update, SAC cfg3 /
 # cfg4 and APPO cfg5 lines.  Outputs in gpurun_out/.
 O=gpurun_out
