@@ -414,6 +414,7 @@ struct SacPlan {
         *din2 = nullptr, *dmean = nullptr;
   double* y = nullptr;
   float *g_a = nullptr, *g_q1 = nullptr, *g_q2 = nullptr, *work = nullptr;
+  float* work2 = nullptr;  // q2's backward workspace (the twin critics run grouped)
   float *gq_own = nullptr, *ga_own = nullptr;  // plan-owned reduce buffers
   int world = 1;
   double n_global = 0.0;
@@ -476,7 +477,7 @@ int alloc_sac(SacPlan* p) {
   o[k++] = carve(8 * B);                          // 22 y
   o[k++] = carve(4 * (p->Pa + 8));                // 23 g_a | actor slots
   o[k++] = carve(4 * (2 * p->Pq + 8));            // 24 g_q1 | g_q2 | critic slot
-  o[k++] = carve(4 * 8);                          // 25 (unused)
+  o[k++] = carve(4 * wq);                         // 25 work2 (q2's backward)
   o[k++] = carve(4 * (wa > wq ? wa : wq));        // 26 work
   o[k++] = carve(4 * p->va.wp_total);             // 27
   o[k++] = carve(4 * p->vq.wp_total);             // 28
@@ -508,6 +509,7 @@ int alloc_sac(SacPlan* p) {
   p->g_q1 = p->gq_own;
   p->g_q2 = p->gq_own + p->Pq;
   p->work = (float*)(a + o[26]);
+  p->work2 = (float*)(a + o[25]);
   p->ws_a = (float*)(a + o[27]);
   p->ws_q1 = (float*)(a + o[28]);
   p->ws_q2 = (float*)(a + o[29]);
@@ -546,6 +548,76 @@ void free_sac(SacPlan* p) {
 }
 
 size_t ctl_hdr() { return offsetof(ul_opt_ctl, part); }
+
+// The twin critics as ONE grouped pass (one tcgen05 launch per layer for
+// both networks, one batched dW launch): x rows shared, per-network params,
+// staged weights, activation caches, outputs (UL_SAC_GROUP=0: one network at
+// a time)
+bool sac_group() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_SAC_GROUP");
+    on = e ? atoi(e) != 0 : 1;
+  }
+  return on == 1;
+}
+
+int critics_forward(const SacPlan* p, int be, const float* x, const float* w1, const float* ws1,
+                    float* out1, const float* w2, const float* ws2, float* out2, cudaStream_t s) {
+  if (!sac_group()) {
+    UL_TRY(mlp_forward(p->vq, w1, ws1, be, x, p->ldq, p->B, p->acts_q1, out1, 1, s));
+    return mlp_forward(p->vq, w2, ws2, be, x, p->ldq, p->B, p->acts_q2, out2, 1, s);
+  }
+  MlpNet n[2] = {};
+  for (int k = 0; k < 2; ++k) {
+    n[k].v = &p->vq;
+    n[k].params = k ? w2 : w1;
+    n[k].wp = be >= 1 ? (k ? ws2 : ws1) : nullptr;
+    n[k].x = x;
+    n[k].ldx = p->ldq;
+    n[k].acts = k ? p->acts_q2 : p->acts_q1;
+    n[k].out = k ? out2 : out1;
+    n[k].ld_out = 1;
+  }
+  return mlp_forward_n(n, 2, be, p->B, s, nullptr, nullptr, nullptr);
+}
+
+// backward of both online critics from dq1 / dq2: parameter gradients
+// (grads1/2, want_dw) or the input gradient over columns [dx_col0, + dx_ncols)
+int critics_backward(const SacPlan* p, int be, const float* x, bool x_has_ones, bool want_dw,
+                     float* grads1, float* grads2, float* din1, float* din2, int dx_col0,
+                     int dx_ncols, bool zero_logstd, cudaStream_t s) {
+  const ul_sac_bindings& b = p->b;
+  if (!sac_group()) {
+    UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, x, p->ldq, x_has_ones, p->B, p->acts_q1,
+                        p->dq1, 1, grads1, din1, din1 ? p->A : 0, dx_col0, dx_ncols, want_dw,
+                        zero_logstd, p->work, s));
+    return mlp_backward(p->vq, b.q2, p->ws_q2, be, x, p->ldq, x_has_ones, p->B, p->acts_q2,
+                        p->dq2, 1, grads2, din2, din2 ? p->A : 0, dx_col0, dx_ncols, want_dw,
+                        zero_logstd, p->work, s);
+  }
+  MlpNet n[2] = {};
+  for (int k = 0; k < 2; ++k) {
+    n[k].v = &p->vq;
+    n[k].params = k ? b.q2 : b.q1;
+    n[k].wp = be >= 1 ? (k ? p->ws_q2 : p->ws_q1) : nullptr;
+    n[k].x = x;
+    n[k].ldx = p->ldq;
+    n[k].x_has_ones = x_has_ones;
+    n[k].acts = k ? p->acts_q2 : p->acts_q1;
+    n[k].dout = k ? p->dq2 : p->dq1;
+    n[k].ld_dout = 1;
+    n[k].grads = k ? grads2 : grads1;
+    n[k].dx = k ? din2 : din1;
+    n[k].lddx = (k ? din2 : din1) ? p->A : 0;
+    n[k].dx_col0 = dx_col0;
+    n[k].dx_ncols = dx_ncols;
+    n[k].want_dw = want_dw;
+    n[k].zero_logstd = zero_logstd;
+    n[k].work = k ? p->work2 : p->work;
+  }
+  return mlp_backward_n(n, 2, be, p->B, s, nullptr, nullptr, nullptr, nullptr);
+}
 
 int adam_one(float* params, float* grads, float* m, float* v, int64_t n, ul_opt_ctl* oc,
              cudaStream_t s) {
@@ -770,24 +842,19 @@ int sac_critic_grads(SacPlan* p, cudaStream_t s) {
   // ---- K10 target (next_obs rows of qn, actions a' written by the squash)
   UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, qn, p->ldq, B, p->acts_a, p->mean, A, s));
   UL_TRY(launch_squash(p, eps_of(p, 0), p->qn, nullptr, s));
-  UL_TRY(mlp_forward(p->vq, b.q1t, p->ws_q1t, be, qn, p->ldq, B, p->acts_q1, p->q1t, 1, s));
-  UL_TRY(mlp_forward(p->vq, b.q2t, p->ws_q2t, be, qn, p->ldq, B, p->acts_q2, p->q2t, 1, s));
+  UL_TRY(critics_forward(p, be, qn, b.q1t, p->ws_q1t, p->q1t, b.q2t, p->ws_q2t, p->q2t, s));
   sac_target_kernel<<<grid_for(B), 256, 0, s>>>(p->rew, p->term, p->nused, p->q1t, p->q2t,
                                                p->logp, p->ctl, p->d.gamma, B, p->y);
   UL_TRY(check_launch("sac_target_kernel"));
   // ---- K11 critics (ones column of qin at D+A feeds the tensor-core db)
-  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, qin, p->ldq, B, p->acts_q1, p->q1o, 1, s));
-  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, qin, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  UL_TRY(critics_forward(p, be, qin, b.q1, p->ws_q1, p->q1o, b.q2, p->ws_q2, p->q2o, s));
   const unsigned nb = (unsigned)ceil_div(B, 256);
   critic_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->y, B, 1.0 / p->n_global, p->dq1,
                                         p->dq2, p->part, p->tickets, p->ctl,
                                         p->world > 1 ? p->g_q1 + 2 * p->Pq : nullptr, rec_of(p));
   UL_TRY(check_launch("critic_head_kernel"));
-  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, qin, p->ldq, true, B, p->acts_q1, p->dq1, 1,
-                      p->g_q1, nullptr, 0, 0, 0, true, true, p->work, s));
-  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, qin, p->ldq, true, B, p->acts_q2, p->dq2, 1,
-                      p->g_q2, nullptr, 0, 0, 0, true, true, p->work, s));
-  return UL_OK;
+  return critics_backward(p, be, qin, true, true, p->g_q1, p->g_q2, nullptr, nullptr, 0, 0, true,
+                          s);
 }
 
 // phase 2: (reduced loss back into ctl) Adam(q1), Adam(q2), latch
@@ -817,18 +884,15 @@ int sac_actor_grads(SacPlan* p, cudaStream_t s) {
   const float* eps2 = eps_of(p, 1);
   UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, obs, p->ldo, B, p->acts_a, p->mean, A, s));
   UL_TRY(launch_squash(p, eps2, p->qa, p->a_pi, s));
-  UL_TRY(mlp_forward(p->vq, b.q1, p->ws_q1, be, qa, p->ldq, B, p->acts_q1, p->q1o, 1, s));
-  UL_TRY(mlp_forward(p->vq, b.q2, p->ws_q2, be, qa, p->ldq, B, p->acts_q2, p->q2o, 1, s));
+  UL_TRY(critics_forward(p, be, qa, b.q1, p->ws_q1, p->q1o, b.q2, p->ws_q2, p->q2o, s));
   const unsigned nb = (unsigned)ceil_div(B, 256);
   pick_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->logp, B, p->n_global, p->dq1, p->dq2,
                                       p->part, p->tickets + 1, p->ctl,
                                       p->world > 1 ? p->g_a + p->Pa : nullptr, rec_of(p));
   UL_TRY(check_launch("pick_head_kernel"));
   // dQ/da through each critic's input gradient, action columns only (fp32 out)
-  UL_TRY(mlp_backward(p->vq, b.q1, p->ws_q1, be, qa, p->ldq, false, B, p->acts_q1, p->dq1, 1,
-                      nullptr, p->din1, A, (int)D, (int)A, false, false, p->work, s));
-  UL_TRY(mlp_backward(p->vq, b.q2, p->ws_q2, be, qa, p->ldq, false, B, p->acts_q2, p->dq2, 1,
-                      nullptr, p->din2, A, (int)D, (int)A, false, false, p->work, s));
+  UL_TRY(critics_backward(p, be, qa, false, false, nullptr, nullptr, p->din1, p->din2, (int)D,
+                          (int)A, false, s));
   actor_head_kernel<<<nb, 256, 0, s>>>(p->a_pi, eps2, A, p->din1, p->din2, A, ls, B, p->n_global,
                                        (int)A, p->ctl, p->dmean, p->part, p->tickets + 2,
                                        p->g_a + p->va.logstd_off);
