@@ -1686,27 +1686,41 @@ int gemm_tc_chain(const GemmDesc* d, int nets, int L, cudaStream_t s) {
   return tc::launch<__nv_bfloat16, false, false, kEpiBiasElu, 256, false>(q, nets * L, s, &cs);
 }
 
-int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
-  const bool e0 = d0.M == 0 || d0.N == 0, e1 = d1.M == 0 || d1.N == 0;
-  if (e0 || e1 || d0.x3 || d1.x3) {  // (3xTF32: one split scratch, one GEMM at a time)
-    if (!e0) UL_TRY(gemm_tc(d0, -1, s));
-    if (!e1) UL_TRY(gemm_tc(d1, -1, s));
+static bool group_compatible(const GemmDesc& d0, const GemmDesc& d1) {
+  return d0.dtype == d1.dtype && d0.a_kmajor == d1.a_kmajor && d0.b_kmajor == d1.b_kmajor &&
+         d0.epi == d1.epi && tc::bn_of(d0) == tc::bn_of(d1) &&
+         (ceil_div(d0.M, tc::BM) >= 2) == (ceil_div(d1.M, tc::BM) >= 2) &&
+         !(d0.csum_part && d1.csum_part) &&
+         (d0.epi != kEpiLnFull || ceil_div(d0.N, tc::bn_of(d0)) == ceil_div(d1.N, tc::bn_of(d1)));
+}
+
+// n (<= kMaxProb) independent GEMMs -- the same layer of several networks --
+// in one persistent launch when all share dtype, layouts, epilogue, tile
+// width and CTA pairing (and at most one carries a column-sum output);
+// otherwise one launch each.  Each desc's ones_col applies.
+int gemm_tc_group_n(const GemmDesc* d, int n, cudaStream_t s) {
+  UL_CHECK_ARG(n >= 1 && n <= tc::kMaxProb, "gemm_tc_group_n: 1..8 problems");
+  bool split = n == 1;
+  int ncs = 0;
+  for (int k = 0; k < n; ++k) {
+    split = split || d[k].M == 0 || d[k].N == 0 || d[k].x3 ||  // (3xTF32: one split scratch)
+            !group_compatible(d[0], d[k]);
+    ncs += d[k].csum_part != nullptr;
+  }
+  if (split || ncs > 1) {
+    for (int k = 0; k < n; ++k)
+      if (d[k].M != 0 && d[k].N != 0) UL_TRY(gemm_tc(d[k], -1, s));
     return UL_OK;
   }
-  const bool same = d0.dtype == d1.dtype && d0.a_kmajor == d1.a_kmajor &&
-                    d0.b_kmajor == d1.b_kmajor && d0.epi == d1.epi &&
-                    tc::bn_of(d0) == tc::bn_of(d1) &&
-                    (ceil_div(d0.M, tc::BM) >= 2) == (ceil_div(d1.M, tc::BM) >= 2) &&
-                    !(d0.csum_part && d1.csum_part) &&
-                    (d0.epi != kEpiLnFull ||
-                     ceil_div(d0.N, tc::bn_of(d0)) == ceil_div(d1.N, tc::bn_of(d1)));
-  if (!same) {
-    UL_TRY(gemm_tc(d0, -1, s));
-    return gemm_tc(d1, -1, s);
-  }
-  const tc::Prob q[2] = {prob_of(d0, -1), prob_of(d1, -1)};
-  if (d0.dtype == kBf16) return tc::dispatch<__nv_bfloat16>(q, 2, s);
-  return tc::dispatch<float>(q, 2, s);
+  tc::Prob q[tc::kMaxProb];
+  for (int k = 0; k < n; ++k) q[k] = prob_of(d[k], -1);
+  if (d[0].dtype == kBf16) return tc::dispatch<__nv_bfloat16>(q, n, s);
+  return tc::dispatch<float>(q, n, s);
+}
+
+int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s) {
+  const GemmDesc d[2] = {d0, d1};
+  return gemm_tc_group_n(d, 2, s);
 }
 
 }  // namespace ul

@@ -244,6 +244,7 @@ int mlp_forward(const NetView& v, const float* params, const float* wp, int back
                 cudaStream_t s);
 // One network's operands for a (possibly paired) MLP pass: forward uses
 // x/acts/out, backward additionally dout..work.
+constexpr int kMaxNets = 4;  // networks advanced in lockstep by mlp_forward_n
 struct MlpNet {
   const NetView* v;
   const float* params;

@@ -20,6 +20,7 @@ namespace ul {
 
 int gemm_tc(const GemmDesc& d, int ones_col, cudaStream_t s);
 int gemm_tc_group(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t s);
+int gemm_tc_group_n(const GemmDesc* d, int n, cudaStream_t s);
 bool tc_eligible(const GemmDesc& d);
 int tc_num_splits(int64_t K, int splits, int dtype);
 bool tc_dw_pairs();
@@ -775,15 +776,27 @@ int launch_reduce(const ReduceJob* jobs, int nj, cudaStream_t s, const SqFold* f
   return UL_OK;
 }
 
-// run 1 or 2 independent GEMMs; tensor-core pairs share a launch
-int run_gemms(GemmDesc* g, const bool* has, const bool* use_tc, const int* ones, cudaStream_t s) {
-  bool tc_ok[2];
-  for (int k = 0; k < 2; ++k) {
+// run 1 to kMaxNets independent GEMMs (n: how many slots); when every
+// present one runs on the tensor cores they share one grouped launch
+int run_gemms(GemmDesc* g, const bool* has, const bool* use_tc, const int* ones, cudaStream_t s,
+              int n = 2) {
+  bool tc_ok[kMaxNets];
+  int n_has = 0, n_tc = 0;
+  for (int k = 0; k < n; ++k) {
     g[k].ones_col = ones[k];
     tc_ok[k] = has[k] && use_tc[k] && tc_eligible(g[k]);
+    n_has += has[k];
+    n_tc += tc_ok[k];
   }
-  if (tc_ok[0] && tc_ok[1]) return gemm_tc_group(g[0], g[1], s);
-  for (int k = 0; k < 2; ++k)
+  if (n == 2 && tc_ok[0] && tc_ok[1]) return gemm_tc_group(g[0], g[1], s);
+  if (n > 2 && n_tc == n_has && n_tc > 1) {
+    GemmDesc q[kMaxNets];
+    int m = 0;
+    for (int k = 0; k < n; ++k)
+      if (has[k]) q[m++] = g[k];
+    return gemm_tc_group_n(q, m, s);
+  }
+  for (int k = 0; k < n; ++k)
     if (has[k]) UL_TRY(run_gemm(g[k], use_tc[k], ones[k], s));
   return UL_OK;
 }
@@ -838,23 +851,26 @@ static bool chain_fwd_ok(const MlpNet* nets, int n, int dt, int64_t M) {
 
 int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_t s,
                   cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
-  if (n == 2 && nets[0].v->n_layers != nets[1].v->n_layers) {
-    UL_TRY(mlp_forward_n(nets, 1, backend, M, s, nullptr, nullptr, nullptr));
-    return mlp_forward_n(nets + 1, 1, backend, M, s, nullptr, nullptr, nullptr);
-  }
+  UL_CHECK_ARG(n >= 1 && n <= kMaxNets, "mlp_forward_n: 1..kMaxNets networks");
+  for (int k = 1; k < n; ++k)
+    if (nets[k].v->n_layers != nets[0].v->n_layers) {  // (lockstep needs equal depths)
+      for (int j = 0; j < n; ++j)
+        UL_TRY(mlp_forward_n(nets + j, 1, backend, M, s, nullptr, nullptr, nullptr));
+      return UL_OK;
+    }
   const Lanes L{s, n == 2 ? side : nullptr, fork, join};
   const int dt = backend_dtype(backend);
   const int eb = dt == kBf16 ? 2 : 4;
   const bool tc = backend >= 1;
-  const float* h[2];
-  int64_t ldh[2];
+  const float* h[kMaxNets];
+  int64_t ldh[kMaxNets];
   for (int k = 0; k < n; ++k) {
     UL_CHECK_ARG(dt == kF32 || nets[k].wp, "bf16 MLP needs staged weights");
     h[k] = nets[k].x;
     ldh[k] = nets[k].ldx;
   }
   const int nl = nets[0].v->n_layers;
-  bool ln_pending[2] = {false, false};
+  bool ln_pending[kMaxNets] = {};
   int i0 = 0;
   if (tc && fused_fwd_ok(nets, n, dt)) {  // every hidden layer in one launch
     UL_TRY(fused_forward(nets, n, M, s));
@@ -892,10 +908,11 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
   }
   for (int i = i0; i < nl; ++i) {
     const bool last = i == nl - 1;
-    GemmDesc g[2] = {};
-    bool has[2] = {false, false}, use[2] = {false, false}, skinny[2] = {false, false};
-    bool ln_full[2] = {false, false};
-    int ones[2] = {-1, -1};
+    GemmDesc g[kMaxNets] = {};
+    bool has[kMaxNets] = {}, use[kMaxNets] = {}, skinny[kMaxNets] = {};
+    bool ln_full[kMaxNets] = {};
+    int ones[kMaxNets] = {-1, -1, -1, -1};
+    bool any_skinny = false;
     for (int k = 0; k < n; ++k) {
       const MlpNet& N = nets[k];
       const NetView& v = *N.v;
@@ -903,7 +920,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       float* dst = last ? N.out : const_cast<float*>(act_ptr(v, N.acts, M, i, dt));
       const int64_t lddst = last ? N.ld_out : act_ld(v.dims[i + 1], dt);
       if (last && skinny_ok(v.dims[i + 1], v.dims[i]) && al16(h[k], ldh[k], eb)) {
-        skinny[k] = true;  // 12-/1-wide head, launched below
+        skinny[k] = any_skinny = true;  // 12-/1-wide head, launched below
         continue;
       }
       GemmDesc& G = g[k];
@@ -968,7 +985,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
       h[k] = dst;
       ldh[k] = lddst;
     }
-    UL_TRY(run_gemms(g, has, use, ones, s));
+    UL_TRY(run_gemms(g, has, use, ones, s, n > 2 ? n : 2));
     for (int k = 0; k < n; ++k) {
       if (!ln_pending[k]) continue;
       ln_pending[k] = false;
@@ -983,7 +1000,7 @@ int mlp_forward_n(const MlpNet* nets, int n, int backend, int64_t M, cudaStream_
                         N.params + v.g_off[i], N.params + v.beta_off[i], lst,
                         const_cast<float*>(h[k]), ldh[k], v.dims[i + 1], dt, s, abf));
     }
-    if (skinny[0] || skinny[1]) {
+    if (any_skinny) {
       UL_TRY(L.open());
       for (int k = 0; k < n; ++k) {
         if (!skinny[k]) continue;

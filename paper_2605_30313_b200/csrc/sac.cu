@@ -409,6 +409,7 @@ struct SacPlan {
   void *qin = nullptr, *qn = nullptr, *qa = nullptr, *obs = nullptr;
   float *rew = nullptr, *term = nullptr, *nused = nullptr;
   float *acts_a = nullptr, *acts_q1 = nullptr, *acts_q2 = nullptr;
+  float *acts_q1t = nullptr, *acts_q2t = nullptr;  // (the 4-network grouped forward)
   float *mean = nullptr, *a_pi = nullptr, *logp = nullptr, *q1o = nullptr, *q2o = nullptr,
         *q1t = nullptr, *q2t = nullptr, *dq1 = nullptr, *dq2 = nullptr, *din1 = nullptr,
         *din2 = nullptr, *dmean = nullptr;
@@ -439,6 +440,20 @@ struct SacPlan {
   int n_graphs = 0;
 };
 
+// The twin critics as ONE grouped pass (one tcgen05 launch per layer for
+// both networks, one batched dW launch): x rows shared, per-network params,
+// staged weights, activation caches, outputs.  UL_SAC_GROUP=0: one network
+// at a time; 2 (default 1): the target critics' and the online critics'
+// forwards as one 4-network pass (own activation caches for the targets)
+int sac_group() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("UL_SAC_GROUP");
+    on = e ? atoi(e) : 1;
+  }
+  return on;
+}
+
 int alloc_sac(SacPlan* p) {
   size_t off = 0;
   auto carve = [&](size_t bytes) {
@@ -450,7 +465,7 @@ int alloc_sac(SacPlan* p) {
   const int64_t wa = bwd_work_floats(p->va, B), wq = bwd_work_floats(p->vq, B);
   // input matrices sized for fp32 rows (bf16 rows are narrower)
   const int64_t ldq32 = act_ld(p->D + p->A), ldo32 = act_ld(p->D);
-  size_t o[40];
+  size_t o[42];
   int k = 0;
   o[k++] = carve(4 * B * ldq32);                  // 0 qin
   o[k++] = carve(4 * B * ldq32);                  // 1 qn
@@ -491,6 +506,9 @@ int alloc_sac(SacPlan* p) {
   o[k++] = carve(sizeof(ul_opt_ctl));             // 36
   o[k++] = carve(sizeof(ul_opt_ctl));             // 37
   o[k++] = carve(sizeof(ul_sac_ctl));             // 38
+  const bool four = sac_group() >= 2;
+  o[k++] = carve(four ? 4 * act_floats(p->vq, B) : 0);  // 39 acts_q1t
+  o[k++] = carve(four ? 4 * act_floats(p->vq, B) : 0);  // 40 acts_q2t
   UL_CUDA(cudaMalloc(&p->arena, off));
   UL_CUDA(cudaMemset(p->arena, 0, off));
   char* a = p->arena;
@@ -521,6 +539,8 @@ int alloc_sac(SacPlan* p) {
   p->oc_q1 = (ul_opt_ctl*)(a + o[36]);
   p->oc_q2 = (ul_opt_ctl*)(a + o[37]);
   p->ctl = (ul_sac_ctl*)(a + o[38]);
+  p->acts_q1t = four ? (float*)(a + o[39]) : nullptr;
+  p->acts_q2t = four ? (float*)(a + o[40]) : nullptr;
   UL_CUDA(cudaHostAlloc(&p->oc_h, 3 * sizeof(ul_opt_ctl), cudaHostAllocPortable));
   UL_CUDA(cudaHostAlloc(&p->ctl_h, sizeof(ul_sac_ctl), cudaHostAllocPortable));
   UL_CUDA(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
@@ -549,18 +569,6 @@ void free_sac(SacPlan* p) {
 
 size_t ctl_hdr() { return offsetof(ul_opt_ctl, part); }
 
-// The twin critics as ONE grouped pass (one tcgen05 launch per layer for
-// both networks, one batched dW launch): x rows shared, per-network params,
-// staged weights, activation caches, outputs (UL_SAC_GROUP=0: one network at
-// a time)
-bool sac_group() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("UL_SAC_GROUP");
-    on = e ? atoi(e) != 0 : 1;
-  }
-  return on == 1;
-}
 
 int critics_forward(const SacPlan* p, int be, const float* x, const float* w1, const float* ws1,
                     float* out1, const float* w2, const float* ws2, float* out2, cudaStream_t s) {
@@ -580,6 +588,29 @@ int critics_forward(const SacPlan* p, int be, const float* x, const float* w1, c
     n[k].ld_out = 1;
   }
   return mlp_forward_n(n, 2, be, p->B, s, nullptr, nullptr, nullptr);
+}
+
+// target critics on the next rows (xt) and online critics on the current
+// rows (x) as one 4-network lockstep pass (UL_SAC_GROUP=2)
+int critics_forward4(const SacPlan* p, int be, const float* xt, const float* x,
+                     cudaStream_t s) {
+  const ul_sac_bindings& b = p->b;
+  const float* w[4] = {b.q1t, b.q2t, b.q1, b.q2};
+  const float* ws[4] = {p->ws_q1t, p->ws_q2t, p->ws_q1, p->ws_q2};
+  float* acts[4] = {p->acts_q1t, p->acts_q2t, p->acts_q1, p->acts_q2};
+  float* out[4] = {p->q1t, p->q2t, p->q1o, p->q2o};
+  MlpNet n[4] = {};
+  for (int k = 0; k < 4; ++k) {
+    n[k].v = &p->vq;
+    n[k].params = w[k];
+    n[k].wp = be >= 1 ? ws[k] : nullptr;
+    n[k].x = k < 2 ? xt : x;
+    n[k].ldx = p->ldq;
+    n[k].acts = acts[k];
+    n[k].out = out[k];
+    n[k].ld_out = 1;
+  }
+  return mlp_forward_n(n, 4, be, p->B, s, nullptr, nullptr, nullptr);
 }
 
 // backward of both online critics from dq1 / dq2: parameter gradients
@@ -842,12 +873,17 @@ int sac_critic_grads(SacPlan* p, cudaStream_t s) {
   // ---- K10 target (next_obs rows of qn, actions a' written by the squash)
   UL_TRY(mlp_forward(p->va, b.actor, p->ws_a, be, qn, p->ldq, B, p->acts_a, p->mean, A, s));
   UL_TRY(launch_squash(p, eps_of(p, 0), p->qn, nullptr, s));
-  UL_TRY(critics_forward(p, be, qn, b.q1t, p->ws_q1t, p->q1t, b.q2t, p->ws_q2t, p->q2t, s));
+  const bool four = p->acts_q1t != nullptr;
+  if (four)
+    UL_TRY(critics_forward4(p, be, qn, qin, s));
+  else
+    UL_TRY(critics_forward(p, be, qn, b.q1t, p->ws_q1t, p->q1t, b.q2t, p->ws_q2t, p->q2t, s));
   sac_target_kernel<<<grid_for(B), 256, 0, s>>>(p->rew, p->term, p->nused, p->q1t, p->q2t,
                                                p->logp, p->ctl, p->d.gamma, B, p->y);
   UL_TRY(check_launch("sac_target_kernel"));
   // ---- K11 critics (ones column of qin at D+A feeds the tensor-core db)
-  UL_TRY(critics_forward(p, be, qin, b.q1, p->ws_q1, p->q1o, b.q2, p->ws_q2, p->q2o, s));
+  if (!four)
+    UL_TRY(critics_forward(p, be, qin, b.q1, p->ws_q1, p->q1o, b.q2, p->ws_q2, p->q2o, s));
   const unsigned nb = (unsigned)ceil_div(B, 256);
   critic_head_kernel<<<nb, 256, 0, s>>>(p->q1o, p->q2o, p->y, B, 1.0 / p->n_global, p->dq1,
                                         p->dq2, p->part, p->tickets, p->ctl,
