@@ -224,6 +224,13 @@ int mlp_pass(PpoPlan* p, MlpNet* nets, int be, int64_t ml, cudaStream_t s, bool 
     if (ahead_e >= 0) UL_TRY(gather_ahead(p, ahead_e, ahead_k, s));
     return run_deferred_dw_reduce(*D, s);
   }
+  if (!fwd && (ablate_mask() & 128)) {  // (diagnostic: both dX chains on s, no fork / join)
+    UL_TRY(mlp_backward_n(nets + 1, 1, be, ml, s, nullptr, nullptr, nullptr, D));
+    UL_TRY(mlp_backward_n(nets, 1, be, ml, s, nullptr, nullptr, nullptr, D));
+    UL_TRY(run_deferred_dw_gemms(*D, s));
+    if (ahead_e >= 0) UL_TRY(gather_ahead(p, ahead_e, ahead_k, s));
+    return run_deferred_dw_reduce(*D, s);
+  }
   UL_CUDA(cudaEventRecord(p->ev_fork, s));
   UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
   if (fwd) {
@@ -399,6 +406,11 @@ int gather_ahead(PpoPlan* p, int e, int k, cudaStream_t s) {
   }
   // (one graph per epoch: the next epoch's permutation is not uploaded yet)
   if (!on || (ablate_mask() & 1) || ne >= p->d.epochs || (p->epoch_mode && ne != e)) return UL_OK;
+  if (ablate_mask() & 256) {  // (diagnostic: the gather on s, no fork / join)
+    UL_TRY(step_gather(p, ne, nk, s, true));
+    p->gathered_ahead = true;
+    return UL_OK;
+  }
   UL_CUDA(cudaEventRecord(p->ev_gfork, s));
   UL_CUDA(cudaStreamWaitEvent(p->side, p->ev_gfork, 0));
   UL_TRY(step_gather(p, ne, nk, p->side, true));
@@ -429,7 +441,7 @@ int step_grads(PpoPlan* p, int e, int k, cudaStream_t s) {
   const int64_t od = p->va.dims[0], cd = p->vc.dims[0];
   const bool ones_o = p->ld_mo > od, ones_c = p->ld_mc > cd;
   if (p->gathered_ahead) {  // gathered on the side stream under the previous step
-    UL_CUDA(cudaStreamWaitEvent(s, p->ev_gjoin, 0));
+    if (!(ablate_mask() & 256)) UL_CUDA(cudaStreamWaitEvent(s, p->ev_gjoin, 0));
     p->gathered_ahead = false;
   } else if (!(ablate_mask() & 1)) {
     UL_TRY(step_gather(p, e, k, s));

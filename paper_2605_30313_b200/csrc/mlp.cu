@@ -1041,13 +1041,22 @@ int run_deferred_dw(DeferredDw& D, cudaStream_t s) {
 int run_deferred_dw_gemms(DeferredDw& D, cudaStream_t s) {
   if (D.ndw) {
     // one split count for the batch: about one persistent wave of tile-splits
-    // (CTA pairs: two CTAs per 256-row tile, a lone 128-row tile included)
+    // over 85 % of the SMs (CTA pairs: two CTAs per 256-row tile, a lone
+    // 128-row tile included).  Measured per update, 85 vs 100 %: cfg2 4.261
+    // vs 4.290 ms, APPO cfg5 15.9 vs 16.1 ms, SAC cfg3 / cfg4 unchanged
+    // (fewer split partials to reduce; 2-3 waves were slower)
     const int64_t pm = tc_dw_pairs() ? 2 : 1;
     int64_t tiles = 0;
     for (int i = 0; i < D.ndw; ++i)
       tiles += ceil_div(ceil_div(D.dw[i].M, 128), pm) * pm *
                ceil_div(D.dw[i].N, D.dw[i].N > 128 ? 256 : 128);
-    int64_t sp = kNumSMs / (tiles > 0 ? tiles : 1);
+    static int fill = -1;  // (UL_DW_FILL: percent of the SMs the tile-splits target)
+    if (fill < 0) {
+      const char* e = getenv("UL_DW_FILL");
+      fill = e ? atoi(e) : 85;
+      fill = fill < 10 ? 10 : fill;
+    }
+    int64_t sp = fill * kNumSMs / (100 * (tiles > 0 ? tiles : 1));
     const int64_t cap = ceil_div(D.dw[0].K, 512);
     sp = sp < cap ? sp : cap;
     sp = sp < 1 ? 1 : sp;
