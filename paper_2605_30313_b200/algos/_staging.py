@@ -303,12 +303,14 @@ _CACHE: dict = {}
 
 
 def bf16_rows_default(slot: str) -> bool:
-    """PPO staging on the bf16 back end keeps observation rows in bf16 (APPO's
-    recompute forward reads fp32 segment rows; UL_BF16_ROWS=0 disables)."""
+    """Staging on the bf16 back end keeps observation rows in bf16 (PPO, and
+    APPO whose recompute forward then runs bf16 too; UL_BF16_ROWS=0 disables,
+    UL_APPO_BF16_RECOMPUTE=0 keeps APPO on fp32 rows and a tf32 recompute)."""
     import os
 
-    return (slot != "appo" and _lib.gemm_backend() == 2
-            and os.environ.get("UL_BF16_ROWS", "1") != "0")
+    if slot == "appo" and os.environ.get("UL_APPO_BF16_RECOMPUTE", "1") == "0":
+        return False
+    return _lib.gemm_backend() == 2 and os.environ.get("UL_BF16_ROWS", "1") != "0"
 
 
 def staging_for(T, N, obs_dim, cobs_dim, act_dim, epochs, slot: str = "ppo") -> DeviceSegment:

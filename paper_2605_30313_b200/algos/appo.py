@@ -17,7 +17,7 @@ from .configs import AppoConfig
 from .ppo import AcOpt, AcParams, _check_dims, _epochs_on_device
 from .segment import UpdateStats
 
-_CHUNK = 65536
+_CHUNK = 1 << 19  # rows per recompute launch set (cfg5: 393,216 rows in one)
 _SCRATCH: dict = {}
 
 
@@ -27,6 +27,14 @@ def _scratch(key, n, dev):
         t = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
         _SCRATCH[key] = t
     return t
+
+
+def _staged_bf16(params, key):
+    desc = params.arch.desc()
+    ws = _scratch(key, _lib.lib().ul_mlp_wstage_floats(desc), params.buf.device)
+    _lib.call("ul_stage_weights_ex", desc, _dev.ptr(params.buf), _dev.ptr(ws), _lib.UL_GEMM_BF16,
+              _dev.stream())
+    return _lib.UL_GEMM_BF16, ws
 
 
 def recompute_targets(ds, params: AcParams) -> None:
@@ -41,8 +49,14 @@ def recompute_targets(ds, params: AcParams) -> None:
     mean = _scratch("mean", chunk * ad, dev)
     s = _dev.stream()
     ls = params.actor.buf[params.actor.buf.numel() - ad:]
-    be_a, ws_a = _staged(params.actor)
-    be_c, ws_c = _staged(params.critic)
+    if getattr(ds, "bf16_rows", False):
+        # bf16 segment rows: the recompute forward runs on the bf16 back end
+        # (no input gradients here), weights staged as bf16 rows
+        be_a, ws_a = _staged_bf16(params.actor, "wsb_a")
+        be_c, ws_c = _staged_bf16(params.critic, "wsb_c")
+    else:
+        be_a, ws_a = _staged(params.actor)
+        be_c, ws_c = _staged(params.critic)
     for r0 in range(0, rows, chunk):
         m = min(chunk, rows - r0)
         _lib.call("ul_mlp_forward", a_arch.desc(), _dev.ptr(params.actor.buf), _dev.ptr(ws_a),
