@@ -169,6 +169,16 @@ int ul_mlp_forward(const ul_net_desc* net, const float* params, const float* wst
                    const float* x, int64_t ldx, int64_t M, float* acts, float* out,
                    int64_t ld_out, void* stream);
 
+/* Two independent networks over the same M rows (APPO's target recompute:
+ * the actor on obs rows, the critic on critic_obs rows) in lockstep, one
+ * grouped tensor-core launch per layer; per network identical to
+ * ul_mlp_forward.  Replaces the pair of forwards at R:algos/appo.py:35-39. */
+int ul_mlp_forward2(const ul_net_desc* net_a, const float* params_a, const float* wstage_a,
+                    const float* x_a, int64_t ldx_a, float* acts_a, float* out_a, int64_t ld_out_a,
+                    const ul_net_desc* net_b, const float* params_b, const float* wstage_b,
+                    const float* x_b, int64_t ldx_b, float* acts_b, float* out_b, int64_t ld_out_b,
+                    int backend, int64_t M, void* stream);
+
 /* Backward from the upstream gradient dout[M, out] (ld_dout): writes the flat
  * gradient vector `grads` (log_std slot zeroed) and, if dx != NULL, the input
  * gradient dx[M, in] (lddx).  x_has_ones: column `in` of x holds 1.0 (lets

@@ -145,6 +145,9 @@ _PROTOS = {
     "ul_mlp_act_ld": (i64, [C.c_int, C.c_int]),
     "ul_mlp_forward": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp, i64, i64, vp, vp, i64,
                                  vp]),
+    "ul_mlp_forward2": (C.c_int, [C.POINTER(NetDesc), vp, vp, vp, i64, vp, vp, i64,
+                                  C.POINTER(NetDesc), vp, vp, vp, i64, vp, vp, i64, C.c_int, i64,
+                                  vp]),
     "ul_mlp_backward": (C.c_int, [C.POINTER(NetDesc), vp, vp, C.c_int, vp, i64, C.c_int, i64, vp,
                                   vp, i64, vp, vp, i64, vp, vp]),
     "ul_gemm_f32": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp,

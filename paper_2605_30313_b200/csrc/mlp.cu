@@ -1541,6 +1541,44 @@ extern "C" int ul_mlp_forward(const ul_net_desc* net, const float* params, const
                          ul::as_stream(stream));
 }
 
+// Two independent networks over the same M rows in lockstep (APPO's target
+// recompute: actor on obs, critic on critic_obs): one grouped tensor-core
+// launch per layer; each network's result is the same as ul_mlp_forward's.
+extern "C" int ul_mlp_forward2(const ul_net_desc* net_a, const float* params_a, const float* wstage_a,
+                               const float* x_a, int64_t ldx_a, float* acts_a, float* out_a,
+                               int64_t ld_out_a, const ul_net_desc* net_b, const float* params_b,
+                               const float* wstage_b, const float* x_b, int64_t ldx_b,
+                               float* acts_b, float* out_b, int64_t ld_out_b, int backend,
+                               int64_t M, void* stream) {
+  ul::NetView va, vb;
+  UL_TRY(ul::make_view(net_a, &va));
+  UL_TRY(ul::make_view(net_b, &vb));
+  UL_CHECK_ARG(M >= 0, "forward2: negative batch");
+  UL_CHECK_ARG(ldx_a >= va.dims[0] && ldx_b >= vb.dims[0], "forward2: ldx below input_dim");
+  UL_CHECK_ARG(backend >= 0 && backend <= 3,
+               "forward2: backend must be 0 (fp32), 1 (tf32), 2 (bf16) or 3 (3xTF32)");
+  ul::MlpNet n[2] = {};
+  const ul::NetView* v[2] = {&va, &vb};
+  const float* pr[2] = {params_a, params_b};
+  const float* ws[2] = {wstage_a, wstage_b};
+  const float* x[2] = {x_a, x_b};
+  const int64_t ldx[2] = {ldx_a, ldx_b};
+  float* acts[2] = {acts_a, acts_b};
+  float* out[2] = {out_a, out_b};
+  const int64_t ldo[2] = {ld_out_a, ld_out_b};
+  for (int k = 0; k < 2; ++k) {
+    n[k].v = v[k];
+    n[k].params = pr[k];
+    n[k].wp = backend >= 1 ? ws[k] : nullptr;
+    n[k].x = x[k];
+    n[k].ldx = ldx[k];
+    n[k].acts = acts[k];
+    n[k].out = out[k];
+    n[k].ld_out = ldo[k];
+  }
+  return ul::mlp_forward_n(n, 2, backend, M, ul::as_stream(stream), nullptr, nullptr, nullptr);
+}
+
 extern "C" int ul_mlp_backward(const ul_net_desc* net, const float* params, const float* wstage,
                                int backend, const float* x, int64_t ldx, int x_has_ones, int64_t M,
                                const float* acts, const float* dout, int64_t ld_dout,
